@@ -1,0 +1,155 @@
+/*
+ * kkb200.h -- C ABI of libkkb200.so, the B200 (sm_100a) Kramers-Kronig
+ * receiver hot path.  Plain pointers, sizes and a cudaStream_t passed as
+ * void*; no C++ or torch types cross this boundary; no exceptions.
+ *
+ * The reference (`kkmodem`, /root/reference/pkg/src/kkmodem) is pure Python
+ * and has no FFI of its own: its plugin surface is the Python API of
+ * kkmodem.rxdsp consumed by kkmodem/harness/runner.py:16-24.  Each entry
+ * point below replaces one reference function (cited as rxdsp.py:line etc.);
+ * paper_2108_07001_b200/rxdsp.py re-exposes the reference's Python surface
+ * on top of these calls (ctypes), and INTEGRATION.md shows the binding a
+ * kkmodem maintainer would add.
+ *
+ * Conventions
+ *   - every entry point returns an int status: KK_OK, or KK_ERR_PARAM
+ *     (-> ParameterError, sigcore.py:37), KK_ERR_SYNC (-> SyncError,
+ *     rxdsp.py:63), KK_ERR_CUDA / KK_ERR_INTERNAL (-> RuntimeError);
+ *     kk_last_error() returns the thread-local message of the last failure.
+ *   - all array pointers are DEVICE pointers unless named *_host; complex
+ *     arrays are interleaved float32 (re, im) = complex64.
+ *   - the library owns only immutable per-device twiddle tables (built once,
+ *     std::call_once); all streaming state lives in caller buffers.
+ *   - entry points are reentrant across pipelines and devices; calls on one
+ *     pipeline must be serialised by the caller (one stream).
+ */
+#ifndef KKB200_H
+#define KKB200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define KK_ABI_VERSION 1
+
+#define KK_OK 0
+#define KK_ERR_PARAM 1
+#define KK_ERR_SYNC 2
+#define KK_ERR_CUDA 3
+#define KK_ERR_INTERNAL 4
+
+#define KK_DTYPE_I16 0 /* ADC codes; value = code * in_scale (odd half-LSB codes) */
+#define KK_DTYPE_F32 1
+#define KK_DTYPE_F64 2
+
+const char *kk_last_error(void);
+int kk_version(void);
+int kk_device_sync(void);
+
+/*
+ * K1 kk_fused -- replaces rxdsp.py:184-244 `kk_reconstruct` (+ the downshift
+ * rxdsp.py:247-257 / :690-696 and the carrier segment sums rxdsp.py:685-687).
+ * Processes n_hops hops of 512 ADC samples in pairs (hop 2p, 2p+1 of this
+ * call).  State in/out = the reference state dict: u_tail[512] (float),
+ * a_hist[256] (float), dead_hist[256] (uint8).  Output out[n_hops*512] is
+ * the field, rotated by exp(-2 pi i (rot_p*g mod rot_q)/rot_q) at global
+ * index g = n0_global + i when rot_q > 0, conjugated when mirror != 0.
+ * hop_sum[n_hops]: per-hop sum of the (unrotated) field; hop_dead[n_hops];
+ * clamped: += clamped-sample count.  clamp_rel: rxdsp.py:188 (1e-12).
+ */
+int kk_reconstruct_pairs(int in_dtype, const void *in, float in_scale, float clamp_rel, int64_t n_hops,
+                         const float *st_u, const float *st_a, const uint8_t *st_dead,
+                         float *new_u, float *new_a, uint8_t *new_dead, void *out,
+                         void *hop_sum, uint8_t *hop_dead, unsigned long long *clamped,
+                         int64_t n0_global, int rot_p, int rot_q, const void *rot_tab,
+                         int mirror, void *stream);
+
+/*
+ * Carrier means -- replaces the per-segment np.mean of rxdsp.py:685-687.
+ * mean[s] = sum(hop_sum[s*hps .. (s+1)*hps)) / len, len = seg_len, or
+ * last_len for the final (flush-partial) segment when last_len > 0.
+ */
+int kk_carrier_means(const void *hop_sum, int64_t n_segs, int hops_per_seg, int64_t n_hops_avail,
+                     int64_t last_len, int seg_len, void *mean, void *stream);
+
+/*
+ * K2 static_fused -- replaces rxdsp.py:698-720 `_run_static`
+ * (== :414-453 `static_equalize_and_resample`) fused with the carrier
+ * subtraction rxdsp.py:687.  Block hb (global static hop, 16384 samples)
+ * reads s[16384(hb-1) .. 16384(hb+1)) where s = z - conj(mean*rot)
+ * (mirror) and writes 8192 2-sps outputs.  h_even/h_odd: the response
+ * _static_response (rxdsp.py:401-411) at even / odd kept indices.
+ */
+int kk_static_blocks(const void *z, int64_t z_index0, int64_t hb0, int64_t n_blocks, int64_t valid_end,
+                     const void *seg_mean, int64_t seg_index0, int seg_len, int carrier, int rot_p,
+                     int rot_q, const void *rot_tab, int mirror, const void *h_even, const void *h_odd,
+                     void *out, void *stream);
+
+/*
+ * K3 sync -- replaces rxdsp.py:574-601 `symbol_sync` and the eq_scale RMS of
+ * rxdsp.py:734-737.  result_host[4] = {parity, k, peak-to-rms ratio,
+ * rms(head[skip:])}; offset = 2k + parity.  Blocking (one stream sync).
+ */
+size_t kk_symbol_sync_scratch_bytes(int64_t n_head, int n_ref);
+int kk_symbol_sync(const void *head, int64_t n_head, const void *ref, int n_ref, int64_t skip,
+                   double *result_host, void *scratch, size_t scratch_bytes, void *stream);
+
+/*
+ * K4 sequential chain -- replaces rxdsp.py:460-499 `_ddlms_core` exactly
+ * (complex form, fp32): used by the functional ddlms_wl API (rxdsp.py:510),
+ * non-widely-linear mode and exact fallbacks.  wg[2*n_taps] complex = w, g;
+ * fz[2] = {frozen, div_count}; both updated in place.  Constellation tables
+ * are host arrays: pts_host[2*order] (re, im), grid_host[grid_m^2] maps
+ * (i_re*m + i_im) -> point index for square QAM (grid_m = 0: brute force).
+ */
+int kk_ddlms_sequential(const void *x, int64_t n_out, float scale, int n_taps, const void *train,
+                        int64_t n_train, void *wg, int *fz, int order, const float *pts_host,
+                        const uint8_t *grid_host, int grid_m, float norm, float max_radius,
+                        float guard_factor, int guard_run, float mu, int widely_linear,
+                        uint8_t *labels, void *soft, void *dec, void *stream);
+
+/*
+ * K4 exact block-parallel WL DDLMS (4 taps) -- same results as the
+ * sequential recurrence rxdsp.py:465-498 (speculative affine prefix scan to
+ * the certified fixpoint).  T_init_host / T_final_host: float[16], the WL
+ * taps in real 2x8 form.  stats_host[6] = {iterations, blocks re-run,
+ * fallback (0 none, 1 guard exceeded -> caller re-runs sequentially,
+ * 2 not converged -> chained), guard exceedances, changed decisions in the
+ * last iteration, blocks}.
+ */
+size_t kk_ddlms_workspace_bytes(int64_t nsym, int block);
+int kk_ddlms_solve(const void *x, int64_t nsym, float scale, const void *train, int64_t n_train,
+                   const float *T_init_host, int order, const float *pts_host, const uint8_t *grid_host,
+                   int grid_m, float norm, float max_radius, float guard_factor, int guard_run,
+                   float mu, int block, int max_iter, float soft_tol, uint8_t *labels, void *soft,
+                   float *T_final_host, void *workspace, size_t ws_bytes, int64_t *stats_host,
+                   void *stream);
+
+/*
+ * BER -- replaces demap (rxdsp.py:548-567) + the XOR count of
+ * runner.py:360-362: total += popcount(label[lab[i]] ^ label[ref[i]]);
+ * win[i / win_syms] += the same (win may be NULL when win_syms <= 0).
+ * Symbols with (i + ex_phase) mod ex_period >= ex_period - ex_len are
+ * skipped when ex_period > 0 (tile seams of a tiled capture);
+ * n_counted (may be NULL) += symbols counted.
+ */
+int kk_bit_errors(const uint8_t *labels, const uint8_t *ref_idx, int64_t n, const uint8_t *point_label,
+                  int64_t win_syms, unsigned long long *total, unsigned int *win, int64_t ex_period,
+                  int64_t ex_len, int64_t ex_phase, unsigned long long *n_counted, void *stream);
+
+/*
+ * demap -- nearest constellation point of rxdsp.py:560-565 (first minimum
+ * wins): idx[i] = point index; n_fallback += count of inputs that are not
+ * exactly a constellation point.
+ */
+int kk_demap(const void *symbols, int64_t n, int order, const float *pts_host, uint8_t *idx,
+             unsigned long long *n_fallback, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* KKB200_H */

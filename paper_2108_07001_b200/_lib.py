@@ -1,0 +1,87 @@
+"""ctypes binding of libkkb200.so (the C ABI declared in include/kkb200.h).
+
+There is no CPU fallback: if the CUDA library is missing or cannot be loaded
+every entry point raises.  Status codes map onto the reference's exception
+types (ParameterError sigcore.py:37, SyncError rxdsp.py:63, RuntimeError).
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+
+from .sigcore import ParameterError
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "_lib", "libkkb200.so")
+
+KK_OK, KK_ERR_PARAM, KK_ERR_SYNC, KK_ERR_CUDA, KK_ERR_INTERNAL = 0, 1, 2, 3, 4
+KK_DTYPE_I16, KK_DTYPE_F32, KK_DTYPE_F64 = 0, 1, 2
+
+
+class SyncError(RuntimeError):
+    """Raised when the receiver cannot align to the reference sequence
+    (mirrors kkmodem.rxdsp.SyncError, rxdsp.py:63)."""
+
+
+_P = ctypes.c_void_p
+_I64 = ctypes.c_int64
+_I = ctypes.c_int
+_F = ctypes.c_float
+_D = ctypes.c_double
+_SZ = ctypes.c_size_t
+
+_SIGS = {
+    "kk_last_error": ([], ctypes.c_char_p),
+    "kk_version": ([], _I),
+    "kk_device_sync": ([], _I),
+    "kk_reconstruct_pairs": ([_I, _P, _F, _F, _I64, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _I64, _I, _I, _P, _I, _P], _I),
+    "kk_carrier_means": ([_P, _I64, _I, _I64, _I64, _I, _P, _P], _I),
+    "kk_static_blocks": ([_P, _I64, _I64, _I64, _I64, _P, _I64, _I, _I, _I, _I, _P, _I, _P, _P, _P, _P], _I),
+    "kk_symbol_sync_scratch_bytes": ([_I64, _I], _SZ),
+    "kk_symbol_sync": ([_P, _I64, _P, _I, _I64, _P, _P, _SZ, _P], _I),
+    "kk_ddlms_sequential": ([_P, _I64, _F, _I, _P, _I64, _P, _P, _I, _P, _P, _I, _F, _F, _F, _I, _F, _I,
+                             _P, _P, _P, _P], _I),
+    "kk_ddlms_workspace_bytes": ([_I64, _I], _SZ),
+    "kk_ddlms_solve": ([_P, _I64, _F, _P, _I64, _P, _I, _P, _P, _I, _F, _F, _F, _I, _F, _I, _I, _F, _P, _P,
+                        _P, _P, _SZ, _P, _P], _I),
+    "kk_bit_errors": ([_P, _P, _I64, _P, _I64, _P, _P, _I64, _I64, _I64, _P, _P], _I),
+    "kk_demap": ([_P, _I64, _I, _P, _P, _P, _P], _I),
+}
+
+EXPORTED = sorted(_SIGS)
+_lib = None
+
+
+def load():
+    """Load (once) and return the ctypes library; raises if unavailable."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise RuntimeError(
+            f"CUDA library {LIB_PATH} is missing: build it with "
+            "`python -m paper_2108_07001_b200.build` (no CPU fallback exists)")
+    lib = ctypes.CDLL(LIB_PATH)
+    for name, (args, res) in _SIGS.items():
+        fn = getattr(lib, name)
+        fn.argtypes = args
+        fn.restype = res
+    _lib = lib
+    return lib
+
+
+def check(rc: int, what: str = "") -> None:
+    if rc == KK_OK:
+        return
+    msg = load().kk_last_error().decode(errors="replace")
+    text = f"{what}: {msg}" if what else msg
+    if rc == KK_ERR_PARAM:
+        raise ParameterError(text)
+    if rc == KK_ERR_SYNC:
+        raise SyncError(text)
+    raise RuntimeError(text)
+
+
+def call(name: str, *args) -> None:
+    check(getattr(load(), name)(*args), name)

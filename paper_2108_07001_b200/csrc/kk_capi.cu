@@ -1,0 +1,80 @@
+// C-ABI plumbing for libkkb200.so: thread-local last error, status codes,
+// lazily built immutable twiddle tables (one per device, std::call_once).
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <vector>
+
+#include "kk_common.cuh"
+#include "kk_internal.h"
+
+namespace kk {
+
+static thread_local char g_err[512] = {0};
+
+void clear_error() { g_err[0] = 0; }
+
+int set_error(int code, const char* msg) {
+    std::snprintf(g_err, sizeof(g_err), "%s", msg ? msg : "error");
+    return code;
+}
+
+int set_cuda_error(const char* where) {
+    const cudaError_t e = cudaGetLastError();
+    std::snprintf(g_err, sizeof(g_err), "%s: %s", where, cudaGetErrorString(e));
+    return KK_ERR_CUDA;
+}
+
+int check_launch(const char* name) {
+    const cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) {
+        std::snprintf(g_err, sizeof(g_err), "launch %s: %s", name, cudaGetErrorString(e));
+        return KK_ERR_CUDA;
+    }
+    return KK_OK;
+}
+
+namespace {
+constexpr int kMaxDev = 64;
+std::once_flag g_tw_once[kMaxDev];
+float2* g_tw[kMaxDev] = {nullptr};
+}  // namespace
+
+const float2* twiddle_table_device() {
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxDev) {
+        set_cuda_error("cudaGetDevice");
+        return nullptr;
+    }
+    std::call_once(g_tw_once[dev], [dev]() {
+        std::vector<float2> h(kTwEntries);
+        const double two_pi = 6.283185307179586476925286766559;
+        for (int i = 0; i < kTwHi; ++i) {   // W_32768^(64 i)
+            const double a = -two_pi * (64.0 * i) / kTwN;
+            h[i] = make_float2(static_cast<float>(std::cos(a)), static_cast<float>(std::sin(a)));
+        }
+        for (int i = 0; i < kTwLo; ++i) {   // W_32768^i
+            const double a = -two_pi * i / kTwN;
+            h[kTwHi + i] = make_float2(static_cast<float>(std::cos(a)), static_cast<float>(std::sin(a)));
+        }
+        float2* d = nullptr;
+        if (cudaMalloc(&d, kTwEntries * sizeof(float2)) == cudaSuccess &&
+            cudaMemcpy(d, h.data(), kTwEntries * sizeof(float2), cudaMemcpyHostToDevice) == cudaSuccess)
+            g_tw[dev] = d;
+    });
+    if (!g_tw[dev]) set_error(KK_ERR_CUDA, "twiddle table allocation failed");
+    return g_tw[dev];
+}
+
+}  // namespace kk
+
+extern "C" const char* kk_last_error(void) { return kk::g_err; }
+
+extern "C" int kk_version(void) { return KK_ABI_VERSION; }
+
+extern "C" int kk_device_sync(void) {
+    kk::clear_error();
+    if (cudaDeviceSynchronize() != cudaSuccess) return kk::set_cuda_error("cudaDeviceSynchronize");
+    return KK_OK;
+}

@@ -1,0 +1,194 @@
+// Shared device building blocks for the B200 KK receiver kernels.
+//
+// * complex helpers on float2,
+// * in-register radix-{2,4,8,16} DFTs (DIF, compile-time twiddles),
+// * an in-place shared-memory Stockham pass engine: every pass reads all of
+//   its inputs into registers, barriers, butterflies, writes the outputs to
+//   the autosorted positions and barriers again, so one padded buffer
+//   (separate re/im float planes, one pad word per 32) serves all passes.
+//   The first pass can read through a functor (global memory, fused
+//   pre-processing) and the last pass can write through a functor (fused
+//   epilogue), so only the middle passes touch shared memory.
+// * a two-level twiddle table for W_32768 (hi[512] x lo[64]) that every
+//   power-of-two FFT up to 32768 points indexes into.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace kk {
+
+constexpr int kTwLogN = 15;               // W_32768 master table
+constexpr int kTwN = 1 << kTwLogN;
+constexpr int kTwLo = 64;
+constexpr int kTwHi = kTwN / kTwLo;       // 512
+constexpr int kTwEntries = kTwHi + kTwLo; // 576 float2
+
+__device__ __forceinline__ float2 cadd(float2 a, float2 b) { return make_float2(a.x + b.x, a.y + b.y); }
+__device__ __forceinline__ float2 csub(float2 a, float2 b) { return make_float2(a.x - b.x, a.y - b.y); }
+__device__ __forceinline__ float2 cmul(float2 a, float2 b) {
+    return make_float2(fmaf(a.x, b.x, -a.y * b.y), fmaf(a.x, b.y, a.y * b.x));
+}
+__device__ __forceinline__ float2 cmulc(float2 a, float2 b) {  // a * conj(b)
+    return make_float2(fmaf(a.x, b.x, a.y * b.y), fmaf(a.y, b.x, -a.x * b.y));
+}
+__device__ __forceinline__ float2 cconj(float2 a) { return make_float2(a.x, -a.y); }
+__device__ __forceinline__ float2 cscale(float2 a, float s) { return make_float2(a.x * s, a.y * s); }
+__device__ __forceinline__ float2 mul_mj(float2 a) { return make_float2(a.y, -a.x); }   // * (-j)
+__device__ __forceinline__ float2 mul_pj(float2 a) { return make_float2(-a.y, a.x); }   // * (+j)
+
+// cos/sin(2*pi*t/16) for t in [0,8)
+__host__ __device__ constexpr float c16(int t) {
+    return t == 0 ? 1.0f : t == 1 ? 0.92387953251128674f : t == 2 ? 0.70710678118654752f
+         : t == 3 ? 0.38268343236508977f : t == 4 ? 0.0f : t == 5 ? -0.38268343236508977f
+         : t == 6 ? -0.70710678118654752f : -0.92387953251128674f;
+}
+__host__ __device__ constexpr float s16(int t) {
+    return t == 0 ? 0.0f : t == 1 ? 0.38268343236508977f : t == 2 ? 0.70710678118654752f
+         : t == 3 ? 0.92387953251128674f : t == 4 ? 1.0f : t == 5 ? 0.92387953251128674f
+         : t == 6 ? 0.70710678118654752f : 0.38268343236508977f;
+}
+
+// multiply by W16^t (forward: exp(-2*pi*i*t/16); inverse: conjugate), t compile-time
+template <int T, bool INV>
+__device__ __forceinline__ float2 tw16(float2 a) {
+    if constexpr (T == 0) {
+        return a;
+    } else if constexpr (T == 4) {
+        return INV ? mul_pj(a) : mul_mj(a);
+    } else {
+        constexpr float c = c16(T);
+        constexpr float s = INV ? s16(T) : -s16(T);
+        return make_float2(fmaf(a.x, c, -a.y * s), fmaf(a.x, s, a.y * c));
+    }
+}
+
+template <int LOG>
+__host__ __device__ constexpr int bitrev(int i) {
+    int r = 0;
+    for (int b = 0; b < LOG; ++b) r |= ((i >> b) & 1) << (LOG - 1 - b);
+    return r;
+}
+template <int R> struct Log2;
+template <> struct Log2<2> { static constexpr int v = 1; };
+template <> struct Log2<4> { static constexpr int v = 2; };
+template <> struct Log2<8> { static constexpr int v = 3; };
+template <> struct Log2<16> { static constexpr int v = 4; };
+
+// radix-2 DIF stage with span S inside an R-point register DFT
+template <int R, int S, bool INV>
+__device__ __forceinline__ void dif_stage(float2 (&v)[R]) {
+#pragma unroll
+    for (int j = 0; j < R; j += 2 * S) {
+#pragma unroll
+        for (int k = 0; k < S; ++k) {
+            float2 a = v[j + k], b = v[j + k + S];
+            v[j + k] = cadd(a, b);
+            float2 d = csub(a, b);
+            // W_{2S}^k = W16^{k * 16/(2S)}
+            switch (k * (16 / (2 * S))) {
+                case 0: v[j + k + S] = tw16<0, INV>(d); break;
+                case 1: v[j + k + S] = tw16<1, INV>(d); break;
+                case 2: v[j + k + S] = tw16<2, INV>(d); break;
+                case 3: v[j + k + S] = tw16<3, INV>(d); break;
+                case 4: v[j + k + S] = tw16<4, INV>(d); break;
+                case 5: v[j + k + S] = tw16<5, INV>(d); break;
+                case 6: v[j + k + S] = tw16<6, INV>(d); break;
+                default: v[j + k + S] = tw16<7, INV>(d); break;
+            }
+        }
+    }
+}
+
+// In-register R-point DFT, natural order in and out.
+template <int R, bool INV>
+__device__ __forceinline__ void dft_reg(float2 (&v)[R]) {
+    if constexpr (R >= 16) dif_stage<R, 8, INV>(v);
+    if constexpr (R >= 8) dif_stage<R, 4, INV>(v);
+    if constexpr (R >= 4) dif_stage<R, 2, INV>(v);
+    dif_stage<R, 1, INV>(v);
+    float2 t[R];
+#pragma unroll
+    for (int i = 0; i < R; ++i) t[i] = v[bitrev<Log2<R>::v>(i)];
+#pragma unroll
+    for (int i = 0; i < R; ++i) v[i] = t[i];
+}
+
+// ---------------------------------------------------------------------------
+// twiddles: W_32768^t = hi[t >> 6] * lo[t & 63]; table lives in smem
+// ---------------------------------------------------------------------------
+struct Twiddle {
+    const float2* hi;  // [512]
+    const float2* lo;  // [64]
+    // W_N^t (forward sign), N a power of two <= 32768, 0 <= t < N
+    template <int N>
+    __device__ __forceinline__ float2 w(int t) const {
+        const int u = t * (kTwN / N);
+        return cmul(hi[u >> 6], lo[u & 63]);
+    }
+};
+
+__device__ __forceinline__ void load_twiddles(float2* sm, const float2* __restrict__ g, int tid, int nt) {
+    for (int i = tid; i < kTwEntries; i += nt) sm[i] = g[i];
+}
+
+// ---------------------------------------------------------------------------
+// padded planar shared-memory buffer
+// ---------------------------------------------------------------------------
+__host__ __device__ constexpr int padi(int i) { return i + (i >> 5); }
+__host__ __device__ constexpr int padded(int n) { return n + (n >> 5); }
+
+struct SmemPlanes {
+    float* re;
+    float* im;
+    __device__ __forceinline__ float2 ld(int i) const { const int p = padi(i); return make_float2(re[p], im[p]); }
+    __device__ __forceinline__ void st(int i, float2 v) const { const int p = padi(i); re[p] = v.x; im[p] = v.y; }
+};
+
+struct LoadPlanes {
+    SmemPlanes s;
+    __device__ __forceinline__ float2 operator()(int i) const { return s.ld(i); }
+};
+struct StorePlanes {
+    SmemPlanes s;
+    __device__ __forceinline__ void operator()(int i, float2 v) const { s.st(i, v); }
+};
+
+// One in-place Stockham (autosort, DIT-twiddle) pass of an N-point FFT with
+// radix R, run by NT threads; NS = product of the radices of earlier passes.
+// Butterfly j reads x[j + r*N/R], applies W_N^{r*(j%NS)*(N/(NS*R))}, does an
+// R-point DFT and writes x[(j/NS)*NS*R + j%NS + r*NS].
+// SYNC_IN: barrier between the read and write phases (needed whenever the
+// loader reads the same buffer the storer writes).
+template <int N, int R, int NS, int NT, bool INV, bool SYNC_IN, class Load, class Store>
+__device__ __forceinline__ void stockham_pass(int tid, const Twiddle& tw, const Load& load, const Store& store) {
+    constexpr int NB = N / R;
+    static_assert(NB % NT == 0, "butterflies must split evenly over threads");
+    constexpr int BPT = NB / NT;
+    float2 v[BPT][R];
+#pragma unroll
+    for (int q = 0; q < BPT; ++q) {
+        const int j = tid + q * NT;
+#pragma unroll
+        for (int r = 0; r < R; ++r) v[q][r] = load(j + r * NB);
+    }
+    if constexpr (SYNC_IN) __syncthreads();
+#pragma unroll
+    for (int q = 0; q < BPT; ++q) {
+        const int j = tid + q * NT;
+        if constexpr (NS > 1) {
+            const int t = (j % NS) * (N / (NS * R));
+#pragma unroll
+            for (int r = 1; r < R; ++r) {
+                const float2 w = tw.template w<N>(r * t);
+                v[q][r] = INV ? cmulc(v[q][r], w) : cmul(v[q][r], w);
+            }
+        }
+        dft_reg<R, INV>(v[q]);
+        const int d0 = (j / NS) * NS * R + (j % NS);
+#pragma unroll
+        for (int r = 0; r < R; ++r) store(d0 + r * NS, v[q][r]);
+    }
+}
+
+}  // namespace kk

@@ -1,0 +1,880 @@
+// K3 sync / K4 widely-linear DDLMS / BER kernels.
+//
+// Reference: rxdsp.py `_ddlms_core` :460-499, `ddlms_wl` :510-545,
+// `symbol_sync` :574-601, `demap` :548-567; harness/runner.py
+// `_accumulate_errors` :351-363.
+//
+// DDLMS, real form.  With X = [Re x0, Im x0, ..., Re x3, Im x3] (the 4-tap
+// 2-sps window of symbol k) and the widely-linear taps written as a real 2x8
+// matrix T (row 0 -> Re y, row 1 -> Im y), the reference recurrence
+//     y = sum conj(w_i) x_i + conj(g_i) conj(x_i)
+//     w_i += mu conj(d - y) x_i ;  g_i += mu conj(d - y) conj(x_i)
+// is exactly  y = T X,  T <- T + 2 mu (D - T X) X^T   (D = [Re d, Im d]),
+// i.e. T <- T A_k + c_k with A_k = I - 2 mu X X^T (real symmetric 8x8) and
+// c_k = 2 mu D X^T.  With decisions fixed a block of B symbols is the affine
+// map T -> T P_b + Q_b, P_b = A_0..A_{B-1} (decision independent), Q_b built
+// from the decisions.
+//
+// Exact parallel solve (kk_ddlms_solve): P_b for all blocks; exact Q for the
+// pure-training blocks; speculate every decision-directed block from the
+// training-end taps; then iterate { deterministic multi-level prefix scan of
+// (P, Q) -> block start taps; re-run every block whose start taps moved by
+// more than its certified margin; count changed decisions } until no
+// decision changes -- that fixpoint is the sequential recurrence's result.
+// Guard trips, frozen state and non-convergence fall back to the exact
+// sequential chain.
+#include <algorithm>
+#include <cmath>
+#include <vector>
+
+#include "kk_common.cuh"
+#include "kk_internal.h"
+
+namespace kk {
+
+// ---------------------------------------------------------------------------
+// slicer (nearest constellation point, first minimum wins: rxdsp.py:476-483)
+// ---------------------------------------------------------------------------
+struct Slicer {
+    int kind;          // 0 = square grid (separable), 1 = brute force
+    int npts;
+    int m;             // levels per axis (square)
+    float norm;        // level value = (2i - (m-1)) / norm
+    float thr;         // guard: divergence_factor * max_radius
+    float2 pts[64];
+    uint8_t grid[64];  // (i_re * m + i_im) -> point index (square)
+};
+
+// returns point index, sets decision value and margin (distance to the
+// nearest decision boundary)
+__device__ __forceinline__ int slice(const Slicer& s, float yr, float yi, float& margin) {
+    if (s.kind == 0) {
+        const float h = 1.0f / s.norm;                       // half spacing
+        const float fr = (yr * s.norm + (s.m - 1)) * 0.5f;
+        const float fi = (yi * s.norm + (s.m - 1)) * 0.5f;
+        int ir = __float2int_rn(fr), ii = __float2int_rn(fi);
+        ir = min(max(ir, 0), s.m - 1);
+        ii = min(max(ii, 0), s.m - 1);
+        const float lr = (2 * ir - (s.m - 1)) * h, li = (2 * ii - (s.m - 1)) * h;
+        float mr = 3.0e38f, mi = 3.0e38f;
+        if (ir > 0) mr = yr - (lr - h);
+        if (ir < s.m - 1) mr = fminf(mr, (lr + h) - yr);
+        if (ii > 0) mi = yi - (li - h);
+        if (ii < s.m - 1) mi = fminf(mi, (li + h) - yi);
+        margin = fminf(mr, mi);
+        return s.grid[ir * s.m + ii];
+    }
+    int best = 0;
+    float bd = 3.0e38f;
+    for (int p = 0; p < s.npts; ++p) {
+        const float dr = yr - s.pts[p].x, di = yi - s.pts[p].y;
+        const float d = dr * dr + di * di;
+        if (d < bd) { bd = d; best = p; }
+    }
+    float mg = 3.0e38f;
+    const float2 pb = s.pts[best];
+    for (int p = 0; p < s.npts; ++p) {
+        if (p == best) continue;
+        const float dr = yr - s.pts[p].x, di = yi - s.pts[p].y;
+        const float ex = pb.x - s.pts[p].x, ey = pb.y - s.pts[p].y;
+        const float sep = sqrtf(ex * ex + ey * ey);
+        mg = fminf(mg, ((dr * dr + di * di) - bd) / (2.0f * sep));
+    }
+    margin = mg;
+    return best;
+}
+
+// ---------------------------------------------------------------------------
+// sequential chain, complex form, exact reference semantics (fp32)
+// (used by the functional ddlms_wl API, non-WL mode and fallbacks)
+// ---------------------------------------------------------------------------
+__global__ void ddlms_seq_kernel(const float2* __restrict__ x, int64_t n_out, float scale, int n_taps,
+                                 const float2* __restrict__ train, int64_t n_train, float2* __restrict__ wg,
+                                 int* __restrict__ fz, Slicer sl, float mu, int wl, int guard_run,
+                                 uint8_t* __restrict__ labels, float2* __restrict__ soft,
+                                 float2* __restrict__ dec) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    float2 w[16], g[16];
+    for (int i = 0; i < n_taps; ++i) { w[i] = wg[i]; g[i] = wg[n_taps + i]; }
+    int frozen = fz[0];
+    int div = fz[1];
+    for (int64_t k = 0; k < n_out; ++k) {
+        const float2* xk = x + 2 * k;
+        float2 y = make_float2(0.f, 0.f);
+        for (int i = 0; i < n_taps; ++i) {
+            const float2 xi = cscale(xk[i], scale);
+            y = cadd(y, cmul(cconj(w[i]), xi));
+            if (wl) y = cadd(y, cmul(cconj(g[i]), cconj(xi)));
+        }
+        float2 d;
+        int lab;
+        if (k < n_train) {
+            d = train[k];
+            lab = 255;
+        } else {
+            float mg;
+            lab = slice(sl, y.x, y.y, mg);
+            d = sl.pts[lab];
+        }
+        if (sqrtf(y.x * y.x + y.y * y.y) > sl.thr) {
+            div += 1;
+            if (div >= guard_run) frozen = 1;
+        } else {
+            div = 0;
+        }
+        if (!frozen && mu != 0.0f) {
+            const float2 ce = cconj(csub(d, y));
+            const float2 mce = cscale(ce, mu);
+            for (int i = 0; i < n_taps; ++i) {
+                const float2 xi = cscale(xk[i], scale);
+                w[i] = cadd(w[i], cmul(mce, xi));
+                if (wl) g[i] = cadd(g[i], cmul(mce, cconj(xi)));
+            }
+        }
+        if (labels) labels[k] = static_cast<uint8_t>(lab);
+        if (soft) soft[k] = y;
+        if (dec) dec[k] = d;
+    }
+    for (int i = 0; i < n_taps; ++i) { wg[i] = w[i]; wg[n_taps + i] = g[i]; }
+    fz[0] = frozen;
+    fz[1] = div;
+}
+
+// ---------------------------------------------------------------------------
+// block-parallel solve (WL, 4 taps)
+// ---------------------------------------------------------------------------
+struct SolveArgs {
+    const float2* x;      // 2-sps input; symbol k uses x[2k .. 2k+3]
+    int64_t nsym;
+    float scale;
+    const float2* train;  // training symbols, k < n_train
+    int64_t n_train;
+    float mu;
+    int B;                // symbols per block
+    int64_t nb;
+};
+
+// symbol k's window x[2k .. 2k+3] (scaled); consecutive symbols share two
+// samples, so the loops below slide the window and load 2 samples per symbol
+__device__ __forceinline__ void load_pair(const SolveArgs& a, int64_t i, float& r0, float& i0, float& r1, float& i1) {
+    const float2 v0 = __ldg(a.x + i), v1 = __ldg(a.x + i + 1);
+    r0 = v0.x * a.scale; i0 = v0.y * a.scale; r1 = v1.x * a.scale; i1 = v1.y * a.scale;
+}
+
+// P_b = prod (I - 2 mu X X^T) over the block; also max |X|^2
+__global__ void ddlms_maps_kernel(SolveArgs a, float* __restrict__ Pb, float* __restrict__ maxx2) {
+    const int64_t b = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (b >= a.nb) return;
+    float P[64];
+#pragma unroll
+    for (int i = 0; i < 64; ++i) P[i] = (i % 9 == 0) ? 1.f : 0.f;
+    const int64_t k0 = b * a.B, k1 = min(k0 + a.B, a.nsym);
+    const float tm = 2.0f * a.mu;
+    float mx = 0.f;
+    float X[8];
+    if (k0 < k1) load_pair(a, 2 * k0, X[4], X[5], X[6], X[7]);
+    for (int64_t k = k0; k < k1; ++k) {
+        X[0] = X[4]; X[1] = X[5]; X[2] = X[6]; X[3] = X[7];
+        load_pair(a, 2 * k + 2, X[4], X[5], X[6], X[7]);
+        float n2 = 0.f;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) n2 = fmaf(X[j], X[j], n2);
+        mx = fmaxf(mx, n2);
+        float v[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            float s = 0.f;
+#pragma unroll
+            for (int j = 0; j < 8; ++j) s = fmaf(P[i * 8 + j], X[j], s);
+            v[i] = s * tm;
+        }
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+#pragma unroll
+            for (int j = 0; j < 8; ++j) P[i * 8 + j] = fmaf(-v[i], X[j], P[i * 8 + j]);
+    }
+    float* o = Pb + b * 64;
+#pragma unroll
+    for (int i = 0; i < 64; ++i) o[i] = P[i];
+    maxx2[b] = mx;
+}
+
+struct RunOut {
+    uint8_t* labels;
+    float2* soft;
+    float* Q;         // [nb][16]
+    float* Tused;     // [nb][16]
+    float* margin;    // [nb]
+    float* Tend;      // [16] end taps of the last block
+    int* over;        // [nb] guard exceedances in the block's latest run
+    unsigned long long* counters;  // [0] changed decisions, [1] blocks re-run
+};
+
+// Run blocks [b_lo, b_hi) starting from Tstart[b] (or chain them when chain != 0:
+// one thread, block b+1 starts from block b's end taps).  Skip test: re-run a
+// block only if |T_new - T_used|_F * max|X| >= min(margin, soft_tol).
+__global__ void ddlms_run_kernel(SolveArgs a, Slicer sl, const float* __restrict__ Tstart,
+                                 const float* __restrict__ maxx2, RunOut o, int64_t b_lo, int64_t b_hi,
+                                 int use_skip, float soft_tol, int chain, int first_run) {
+    int64_t b = b_lo + int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (chain) {
+        if (blockIdx.x != 0 || threadIdx.x != 0) return;
+        b = b_lo;
+    }
+    if (b >= b_hi) return;
+    float T[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) T[i] = Tstart[b * 16 + i];
+    const float tm = 2.0f * a.mu;
+    unsigned long long changed = 0, over = 0, reruns = 0;
+    for (;;) {
+        bool run = true;
+        if (use_skip && !chain && !first_run) {
+            float d2 = 0.f;
+#pragma unroll
+            for (int i = 0; i < 16; ++i) {
+                const float d = T[i] - o.Tused[b * 16 + i];
+                d2 = fmaf(d, d, d2);
+            }
+            const float bound = sqrtf(d2 * maxx2[b]);
+            const float ok = fminf(o.margin[b], soft_tol);
+            run = !(bound < ok) || (a.mu * maxx2[b] > 1.0f);
+        }
+        if (run) {
+            ++reruns;
+#pragma unroll
+            for (int i = 0; i < 16; ++i) o.Tused[b * 16 + i] = T[i];
+            float Q[16];
+#pragma unroll
+            for (int i = 0; i < 16; ++i) Q[i] = 0.f;
+            float mg = 3.0e38f;
+            const int64_t k0 = b * a.B, k1 = min(k0 + a.B, a.nsym);
+            float X[8];
+            load_pair(a, 2 * k0, X[4], X[5], X[6], X[7]);
+            for (int64_t k = k0; k < k1; ++k) {
+                X[0] = X[4]; X[1] = X[5]; X[2] = X[6]; X[3] = X[7];
+                load_pair(a, 2 * k + 2, X[4], X[5], X[6], X[7]);
+                float yr = 0.f, yi = 0.f, qr = 0.f, qi = 0.f;
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
+                    yr = fmaf(T[j], X[j], yr);
+                    yi = fmaf(T[8 + j], X[j], yi);
+                    qr = fmaf(Q[j], X[j], qr);
+                    qi = fmaf(Q[8 + j], X[j], qi);
+                }
+                float dr, di;
+                int lab;
+                if (k < a.n_train) {
+                    const float2 t = __ldg(a.train + k);
+                    dr = t.x; di = t.y;
+                    lab = 255;
+                } else {
+                    float m;
+                    lab = slice(sl, yr, yi, m);
+                    mg = fminf(mg, m);
+                    dr = sl.pts[lab].x; di = sl.pts[lab].y;
+                }
+                const float ay = sqrtf(yr * yr + yi * yi);
+                if (ay > sl.thr) ++over;
+                mg = fminf(mg, fabsf(ay - sl.thr));
+                const float er = tm * (dr - yr), ei = tm * (di - yi);
+                const float fr = tm * (dr - qr), fi = tm * (di - qi);
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
+                    T[j] = fmaf(er, X[j], T[j]);
+                    T[8 + j] = fmaf(ei, X[j], T[8 + j]);
+                    Q[j] = fmaf(fr, X[j], Q[j]);
+                    Q[8 + j] = fmaf(fi, X[j], Q[8 + j]);
+                }
+                const uint8_t old = o.labels[k];
+                if (old != static_cast<uint8_t>(lab)) { o.labels[k] = static_cast<uint8_t>(lab); ++changed; }
+                o.soft[k] = make_float2(yr, yi);
+            }
+#pragma unroll
+            for (int i = 0; i < 16; ++i) o.Q[b * 16 + i] = Q[i];
+            o.margin[b] = mg;
+            o.over[b] = static_cast<int>(over);
+            over = 0;
+            if (b == a.nb - 1) {
+#pragma unroll
+                for (int i = 0; i < 16; ++i) o.Tend[i] = T[i];
+            }
+        }
+        if (!chain) break;
+        ++b;
+        if (b >= b_hi) break;
+        if (!run) {
+#pragma unroll
+            for (int i = 0; i < 16; ++i) T[i] = Tstart[b * 16 + i];
+        }
+    }
+    if (changed) atomicAdd(o.counters + 0, changed);
+    if (reruns) atomicAdd(o.counters + 1, reruns);
+}
+
+__global__ void sum_int_kernel(const int* __restrict__ v, int64_t n, unsigned long long* __restrict__ out) {
+    unsigned long long acc = 0;
+    for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x)
+        acc += static_cast<unsigned long long>(v[i]);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if ((threadIdx.x & 31) == 0 && acc) atomicAdd(out, acc);
+}
+
+__global__ void fill_T_kernel(float* __restrict__ T, int64_t b0, int64_t b1, const float* __restrict__ src) {
+    const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    const int64_t n = (b1 - b0) * 16;
+    if (i < n) T[b0 * 16 + i] = src[i & 15];
+}
+
+// fold groups of G consecutive maps:  (P, Q) <- (P P_c, Q P_c + Q_c)
+__global__ void scan_fold_kernel(const float* __restrict__ Pc, const float* __restrict__ Qc, int64_t n_child,
+                                 int G, float* __restrict__ Pg, float* __restrict__ Qg, int64_t n_grp, int with_p) {
+    const int64_t g = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (g >= n_grp) return;
+    float P[64], Q[16];
+#pragma unroll
+    for (int i = 0; i < 64; ++i) P[i] = (i % 9 == 0) ? 1.f : 0.f;
+#pragma unroll
+    for (int i = 0; i < 16; ++i) Q[i] = 0.f;
+    const int64_t c0 = g * G, c1 = min(c0 + G, n_child);
+    for (int64_t c = c0; c < c1; ++c) {
+        const float* M = Pc + c * 64;
+        float nQ[16];
+#pragma unroll
+        for (int r = 0; r < 2; ++r)
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                float s = Qc[c * 16 + r * 8 + j];
+#pragma unroll
+                for (int i = 0; i < 8; ++i) s = fmaf(Q[r * 8 + i], __ldg(M + i * 8 + j), s);
+                nQ[r * 8 + j] = s;
+            }
+#pragma unroll
+        for (int i = 0; i < 16; ++i) Q[i] = nQ[i];
+        if (with_p) {
+            float nP[64];
+#pragma unroll
+            for (int r = 0; r < 8; ++r)
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
+                    float s = 0.f;
+#pragma unroll
+                    for (int i = 0; i < 8; ++i) s = fmaf(P[r * 8 + i], __ldg(M + i * 8 + j), s);
+                    nP[r * 8 + j] = s;
+                }
+#pragma unroll
+            for (int i = 0; i < 64; ++i) P[i] = nP[i];
+        }
+    }
+#pragma unroll
+    for (int i = 0; i < 16; ++i) Qg[g * 16 + i] = Q[i];
+    if (with_p) {
+#pragma unroll
+        for (int i = 0; i < 64; ++i) Pg[g * 64 + i] = P[i];
+    }
+}
+
+// down-sweep: children start taps from the group start taps
+__global__ void scan_down_kernel(const float* __restrict__ Pc, const float* __restrict__ Qc, int64_t n_child,
+                                 int G, const float* __restrict__ Tg, int64_t n_grp, float* __restrict__ Tc) {
+    const int64_t g = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (g >= n_grp) return;
+    float T[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) T[i] = Tg[g * 16 + i];
+    const int64_t c0 = g * G, c1 = min(c0 + G, n_child);
+    for (int64_t c = c0; c < c1; ++c) {
+#pragma unroll
+        for (int i = 0; i < 16; ++i) Tc[c * 16 + i] = T[i];
+        if (c + 1 == c1) break;
+        const float* M = Pc + c * 64;
+        float nT[16];
+#pragma unroll
+        for (int r = 0; r < 2; ++r)
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                float s = Qc[c * 16 + r * 8 + j];
+#pragma unroll
+                for (int i = 0; i < 8; ++i) s = fmaf(T[r * 8 + i], __ldg(M + i * 8 + j), s);
+                nT[r * 8 + j] = s;
+            }
+#pragma unroll
+        for (int i = 0; i < 16; ++i) T[i] = nT[i];
+    }
+}
+
+// ---------------------------------------------------------------------------
+// symbol sync (rxdsp.py:574-601): |xcorr| of both 2-sps parities with the
+// reference, argmax, sidelobe RMS; plus the head RMS for eq_scale
+// (rxdsp.py:734-737).  float64 accumulation.
+// ---------------------------------------------------------------------------
+__global__ void xcorr_kernel(const float2* __restrict__ head, int64_t n_head, const float2* __restrict__ ref,
+                             int n_ref, int64_t n_lag0, int64_t n_lag1, double* __restrict__ mag) {
+    extern __shared__ float2 sref[];
+    for (int i = threadIdx.x; i < n_ref; i += blockDim.x) sref[i] = ref[i];
+    __syncthreads();
+    const int64_t t = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    const int64_t tot = n_lag0 + n_lag1;
+    if (t >= tot) return;
+    const int parity = t < n_lag0 ? 0 : 1;
+    const int64_t k = parity ? t - n_lag0 : t;
+    double re = 0.0, im = 0.0;
+    for (int i = 0; i < n_ref; ++i) {
+        const float2 z = head[parity + 2 * (k + i)];
+        const float2 r = sref[i];
+        // z * conj(r)
+        re += static_cast<double>(z.x) * r.x + static_cast<double>(z.y) * r.y;
+        im += static_cast<double>(z.y) * r.x - static_cast<double>(z.x) * r.y;
+    }
+    mag[t] = sqrt(re * re + im * im);
+}
+
+__global__ void sync_reduce_kernel(const double* __restrict__ mag, int64_t n_lag0, int64_t n_lag1,
+                                   const float2* __restrict__ head, int64_t n_head, int64_t skip,
+                                   double* __restrict__ res) {
+    // res: [0] best parity, [1] k, [2] ratio, [3] rms of head[skip:]
+    __shared__ double sd[1024];
+    __shared__ long long si[1024];
+    const int tid = threadIdx.x;
+    double best_ratio = -1.0;
+    long long best_k = -1;
+    int best_p = -1;
+    for (int parity = 0; parity < 2; ++parity) {
+        const int64_t n = parity ? n_lag1 : n_lag0;
+        if (n <= 0) continue;
+        const double* m = mag + (parity ? n_lag0 : 0);
+        double bv = -1.0;
+        long long bi = 0;
+        for (int64_t i = tid; i < n; i += blockDim.x)
+            if (m[i] > bv) { bv = m[i]; bi = i; }
+        sd[tid] = bv;
+        si[tid] = bi;
+        __syncthreads();
+        for (int s = blockDim.x / 2; s > 0; s >>= 1) {
+            if (tid < s) {
+                const double ov = sd[tid + s];
+                const long long oi = si[tid + s];
+                if (ov > sd[tid] || (ov == sd[tid] && oi < si[tid])) { sd[tid] = ov; si[tid] = oi; }
+            }
+            __syncthreads();
+        }
+        const double peak = sd[0];
+        const long long k = si[0];
+        __syncthreads();
+        double acc = 0.0;
+        for (int64_t i = tid; i < n; i += blockDim.x)
+            if (i < k - 2 || i > k + 2) acc += m[i] * m[i];
+        sd[tid] = acc;
+        __syncthreads();
+        for (int s = blockDim.x / 2; s > 0; s >>= 1) {
+            if (tid < s) sd[tid] += sd[tid + s];
+            __syncthreads();
+        }
+        const long long lo = k - 2 < 0 ? 0 : k - 2;
+        const long long hi = k + 3 > n ? n : k + 3;
+        const long long n_side = n - (hi - lo);
+        const double rms = n_side > 0 ? sqrt(sd[0] / static_cast<double>(n_side)) : 1e-30;
+        const double ratio = peak / rms;
+        if (ratio > best_ratio) { best_ratio = ratio; best_k = k; best_p = parity; }
+        __syncthreads();
+    }
+    double acc = 0.0;
+    for (int64_t i = skip + tid; i < n_head; i += blockDim.x) {
+        const float2 v = head[i];
+        acc += static_cast<double>(v.x) * v.x + static_cast<double>(v.y) * v.y;
+    }
+    sd[tid] = acc;
+    __syncthreads();
+    for (int s = blockDim.x / 2; s > 0; s >>= 1) {
+        if (tid < s) sd[tid] += sd[tid + s];
+        __syncthreads();
+    }
+    if (tid == 0) {
+        res[0] = best_p;
+        res[1] = static_cast<double>(best_k);
+        res[2] = best_ratio;
+        const int64_t cnt = n_head - skip;
+        res[3] = cnt > 0 ? sqrt(sd[0] / static_cast<double>(cnt)) : 0.0;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// BER: bit errors between decided point indices and reference point indices
+// (demap rxdsp.py:548-567 + XOR count runner.py:360-362), per-window counts
+// ---------------------------------------------------------------------------
+__global__ void bit_errors_kernel(const uint8_t* __restrict__ lab, const uint8_t* __restrict__ ref, int64_t n,
+                                  const uint8_t* __restrict__ point_label, int64_t win_syms,
+                                  unsigned long long* __restrict__ total, unsigned int* __restrict__ win,
+                                  int64_t ex_period, int64_t ex_len, int64_t ex_phase,
+                                  unsigned long long* __restrict__ n_counted) {
+    __shared__ uint8_t pl[64];
+    if (threadIdx.x < 64) pl[threadIdx.x] = point_label[threadIdx.x];
+    __syncthreads();
+    unsigned long long e = 0, cnt = 0;
+    for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
+        if (ex_period > 0 && ((i + ex_phase) % ex_period) >= ex_period - ex_len) continue;
+        ++cnt;
+        const uint8_t a = lab[i], b = ref[i];
+        const unsigned c = __popc(static_cast<unsigned>(pl[a & 63] ^ pl[b & 63]));
+        e += c;
+        if (win && c) atomicAdd(win + i / win_syms, c);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        e += __shfl_xor_sync(0xffffffffu, e, o);
+        cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+    }
+    if ((threadIdx.x & 31) == 0) {
+        if (e) atomicAdd(total, e);
+        if (cnt && n_counted) atomicAdd(n_counted, cnt);
+    }
+}
+
+// nearest point (first minimum wins) + fallback count (rxdsp.py:560-565)
+__global__ void demap_kernel(const float2* __restrict__ sym, int64_t n, Slicer sl, uint8_t* __restrict__ idx,
+                             unsigned long long* __restrict__ n_fallback) {
+    unsigned long long fb = 0;
+    for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
+        const float2 y = sym[i];
+        int best = 0;
+        float bd = 3.0e38f;
+        for (int p = 0; p < sl.npts; ++p) {
+            const float dr = y.x - sl.pts[p].x, di = y.y - sl.pts[p].y;
+            const float d = dr * dr + di * di;
+            if (d < bd) { bd = d; best = p; }
+        }
+        idx[i] = static_cast<uint8_t>(best);
+        if (bd > 1e-18f) ++fb;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) fb += __shfl_xor_sync(0xffffffffu, fb, o);
+    if ((threadIdx.x & 31) == 0 && fb) atomicAdd(n_fallback, fb);
+}
+
+}  // namespace kk
+
+// ===========================================================================
+// C ABI
+// ===========================================================================
+using namespace kk;
+
+static Slicer make_slicer(int order, const float* pts_ri, const uint8_t* grid, int grid_m, float norm,
+                          float max_radius, float guard_factor) {
+    Slicer s{};
+    s.npts = order;
+    s.kind = grid_m > 0 ? 0 : 1;
+    s.m = grid_m;
+    s.norm = norm;
+    s.thr = guard_factor * max_radius;
+    for (int i = 0; i < order && i < 64; ++i) s.pts[i] = make_float2(pts_ri[2 * i], pts_ri[2 * i + 1]);
+    if (grid_m > 0)
+        for (int i = 0; i < grid_m * grid_m && i < 64; ++i) s.grid[i] = grid[i];
+    return s;
+}
+
+extern "C" int kk_ddlms_sequential(const void* x, int64_t n_out, float scale, int n_taps, const void* train,
+                                   int64_t n_train, void* wg, int* fz, int order, const float* pts_host,
+                                   const uint8_t* grid_host, int grid_m, float norm, float max_radius,
+                                   float guard_factor, int guard_run, float mu, int widely_linear,
+                                   uint8_t* labels, void* soft, void* dec, void* stream) {
+    clear_error();
+    if (n_taps < 1 || n_taps > 16) return set_error(KK_ERR_PARAM, "n_taps must be in [1, 16]");
+    if (order < 2 || order > 64) return set_error(KK_ERR_PARAM, "constellation order must be <= 64");
+    if (n_out <= 0) return KK_OK;
+    Slicer sl = make_slicer(order, pts_host, grid_host, grid_m, norm, max_radius, guard_factor);
+    ddlms_seq_kernel<<<1, 1, 0, static_cast<cudaStream_t>(stream)>>>(
+        static_cast<const float2*>(x), n_out, scale, n_taps, static_cast<const float2*>(train), n_train,
+        static_cast<float2*>(wg), fz, sl, mu, widely_linear, guard_run, labels, static_cast<float2*>(soft),
+        static_cast<float2*>(dec));
+    return check_launch("ddlms_seq_kernel");
+}
+
+namespace {
+constexpr int kG = 32;   // scan fan-in
+
+struct Level {
+    int64_t n;
+    float *P, *Q, *T;
+};
+
+size_t align_up(size_t v) { return (v + 255) & ~size_t(255); }
+
+struct Layout {
+    int64_t nb;
+    std::vector<int64_t> n;  // entries per level (level 0 = blocks)
+    size_t bytes;
+};
+
+Layout plan(int64_t nsym, int B) {
+    Layout L;
+    L.nb = (nsym + B - 1) / B;
+    int64_t n = L.nb;
+    L.n.push_back(n);
+    while (n > kG) {
+        n = (n + kG - 1) / kG;
+        L.n.push_back(n);
+    }
+    size_t b = 0;
+    for (size_t l = 0; l < L.n.size(); ++l) b += align_up(L.n[l] * 96 * sizeof(float));  // P64 + Q16 + T16
+    b += align_up(L.nb * 16 * sizeof(float));   // Tused
+    b += align_up(L.nb * sizeof(float)) * 2;    // margin, maxx2
+    b += align_up(16 * sizeof(float)) * 2;      // Tend, Tinit
+    b += align_up(L.nb * sizeof(int));          // over
+    b += align_up(4 * sizeof(unsigned long long));
+    L.bytes = b;
+    return L;
+}
+}  // namespace
+
+extern "C" size_t kk_ddlms_workspace_bytes(int64_t nsym, int block) {
+    if (nsym <= 0 || block <= 0) return 0;
+    return plan(nsym, block).bytes;
+}
+
+// Exact block-parallel WL DDLMS (4 taps) over nsym symbols.
+//   T_init: host float[16] (real form).  Outputs: labels (255 on training
+//   symbols), soft, T_final (host float[16]).  stats (host int64[6]):
+//   iterations, blocks re-run, fallback (0 none, 1 guard, 2 not converged),
+//   guard exceedances, changed decisions in the last iteration, blocks.
+extern "C" int kk_ddlms_solve(const void* x, int64_t nsym, float scale, const void* train, int64_t n_train,
+                              const float* T_init, int order, const float* pts_host, const uint8_t* grid_host,
+                              int grid_m, float norm, float max_radius, float guard_factor, int guard_run,
+                              float mu, int block, int max_iter, float soft_tol, uint8_t* labels, void* soft,
+                              float* T_final, void* workspace, size_t ws_bytes, int64_t* stats, void* stream) {
+    clear_error();
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    if (nsym <= 0) return KK_OK;
+    if (block <= 0) return set_error(KK_ERR_PARAM, "block must be positive");
+    if (order < 2 || order > 64) return set_error(KK_ERR_PARAM, "constellation order must be <= 64");
+    Layout L = plan(nsym, block);
+    if (ws_bytes < L.bytes) return set_error(KK_ERR_PARAM, "workspace too small");
+    Slicer sl = make_slicer(order, pts_host, grid_host, grid_m, norm, max_radius, guard_factor);
+
+    // carve the workspace
+    char* w = static_cast<char*>(workspace);
+    std::vector<Level> lv(L.n.size());
+    for (size_t l = 0; l < L.n.size(); ++l) {
+        lv[l].n = L.n[l];
+        lv[l].P = reinterpret_cast<float*>(w);
+        lv[l].Q = lv[l].P + L.n[l] * 64;
+        lv[l].T = lv[l].Q + L.n[l] * 16;
+        w += align_up(L.n[l] * 96 * sizeof(float));
+    }
+    float* Tused = reinterpret_cast<float*>(w); w += align_up(L.nb * 16 * sizeof(float));
+    float* margin = reinterpret_cast<float*>(w); w += align_up(L.nb * sizeof(float));
+    float* maxx2 = reinterpret_cast<float*>(w); w += align_up(L.nb * sizeof(float));
+    float* Tend = reinterpret_cast<float*>(w); w += align_up(16 * sizeof(float));
+    float* Tinit_d = reinterpret_cast<float*>(w); w += align_up(16 * sizeof(float));
+    int* over = reinterpret_cast<int*>(w); w += align_up(L.nb * sizeof(int));
+    unsigned long long* ctr = reinterpret_cast<unsigned long long*>(w);
+
+    SolveArgs a;
+    a.x = static_cast<const float2*>(x);
+    a.nsym = nsym;
+    a.scale = scale;
+    a.train = static_cast<const float2*>(train);
+    a.n_train = n_train;
+    a.mu = mu;
+    a.B = block;
+    a.nb = L.nb;
+    RunOut o;
+    o.labels = labels;
+    o.soft = static_cast<float2*>(soft);
+    o.Q = lv[0].Q;
+    o.Tused = Tused;
+    o.margin = margin;
+    o.Tend = Tend;
+    o.over = over;
+    o.counters = ctr;
+
+    const int th = 128;
+    auto grid_of = [&](int64_t n) { return static_cast<unsigned>((n + th - 1) / th); };
+    const int top = static_cast<int>(lv.size()) - 1;
+    int64_t st[6] = {0, 0, 0, 0, 0, L.nb};
+
+    // (1) decision-independent block maps and their aggregates
+    ddlms_maps_kernel<<<grid_of(L.nb), th, 0, s>>>(a, lv[0].P, maxx2);
+    if (int rc = check_launch("ddlms_maps_kernel")) return rc;
+    if (cudaMemsetAsync(labels, 0xFE, nsym, s) != cudaSuccess) return set_cuda_error("labels init");
+
+    auto scan = [&](bool with_p) -> int {
+        for (int l = 1; l <= top; ++l) {
+            scan_fold_kernel<<<grid_of(lv[l].n), th, 0, s>>>(lv[l - 1].P, lv[l - 1].Q, lv[l - 1].n, kG, lv[l].P,
+                                                             lv[l].Q, lv[l].n, with_p ? 1 : 0);
+            if (int rc = check_launch("scan_fold_kernel")) return rc;
+        }
+        // top level: sequential over <= kG entries from T_init
+        {
+            std::vector<float> Ptop(lv[top].n * 64), Qtop(lv[top].n * 16), Ttop(lv[top].n * 16);
+            if (cudaMemcpyAsync(Ptop.data(), lv[top].P, Ptop.size() * 4, cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+                cudaMemcpyAsync(Qtop.data(), lv[top].Q, Qtop.size() * 4, cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+                cudaStreamSynchronize(s) != cudaSuccess)
+                return set_cuda_error("scan top copy");
+            float T[16];
+            for (int i = 0; i < 16; ++i) T[i] = T_init[i];
+            for (int64_t g = 0; g < lv[top].n; ++g) {
+                for (int i = 0; i < 16; ++i) Ttop[g * 16 + i] = T[i];
+                float nT[16];
+                for (int r = 0; r < 2; ++r)
+                    for (int j = 0; j < 8; ++j) {
+                        float acc = Qtop[g * 16 + r * 8 + j];
+                        for (int i = 0; i < 8; ++i) acc = std::fma(T[r * 8 + i], Ptop[g * 64 + i * 8 + j], acc);
+                        nT[r * 8 + j] = acc;
+                    }
+                for (int i = 0; i < 16; ++i) T[i] = nT[i];
+            }
+            if (cudaMemcpyAsync(lv[top].T, Ttop.data(), Ttop.size() * 4, cudaMemcpyHostToDevice, s) != cudaSuccess ||
+                cudaStreamSynchronize(s) != cudaSuccess)
+                return set_cuda_error("scan top upload");
+        }
+        for (int l = top; l >= 1; --l) {
+            scan_down_kernel<<<grid_of(lv[l].n), th, 0, s>>>(lv[l - 1].P, lv[l - 1].Q, lv[l - 1].n, kG, lv[l].T,
+                                                             lv[l].n, lv[l - 1].T);
+            if (int rc = check_launch("scan_down_kernel")) return rc;
+        }
+        return KK_OK;
+    };
+    auto read_ctr = [&](unsigned long long (&h)[4]) -> int {
+        if (cudaMemcpyAsync(h, ctr, sizeof(h), cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+            cudaStreamSynchronize(s) != cudaSuccess)
+            return set_cuda_error("counter readback");
+        return KK_OK;
+    };
+    auto fill_T = [&](int64_t b0, int64_t b1, const float* Tsrc_dev) -> int {
+        if (b1 <= b0) return KK_OK;
+        fill_T_kernel<<<grid_of((b1 - b0) * 16), th, 0, s>>>(lv[0].T, b0, b1, Tsrc_dev);
+        return check_launch("fill_T_kernel");
+    };
+
+    // (2) pure-training blocks are exact from any start: run them, scan to
+    //     get the exact training-end taps, speculate everything after.
+    const int64_t bt = std::min<int64_t>(n_train / block, L.nb);
+    if (cudaMemcpyAsync(Tinit_d, T_init, 16 * sizeof(float), cudaMemcpyHostToDevice, s) != cudaSuccess)
+        return set_cuda_error("T_init upload");
+    if (cudaMemsetAsync(over, 0, L.nb * sizeof(int), s) != cudaSuccess) return set_cuda_error("over init");
+    if (int rc = fill_T(0, L.nb, Tinit_d)) return rc;
+    if (cudaMemsetAsync(ctr, 0, 4 * sizeof(unsigned long long), s) != cudaSuccess) return set_cuda_error("ctr");
+    if (bt > 0) {
+        ddlms_run_kernel<<<grid_of(bt), th, 0, s>>>(a, sl, lv[0].T, maxx2, o, 0, bt, 0, soft_tol, 0, 1);
+        if (int rc = check_launch("ddlms_run_kernel")) return rc;
+        // Q of not-yet-run blocks must not pollute the training scan: zero them
+        if (cudaMemsetAsync(lv[0].Q + bt * 16, 0, (L.nb - bt) * 16 * sizeof(float), s) != cudaSuccess)
+            return set_cuda_error("Q init");
+        if (int rc = scan(true)) return rc;
+        // lv[0].T[bt] is exact; broadcast it as the guess for all later blocks
+        if (bt < L.nb) {
+            if (cudaMemcpyAsync(Tend, lv[0].T + bt * 16, 16 * sizeof(float), cudaMemcpyDeviceToDevice, s) !=
+                cudaSuccess)
+                return set_cuda_error("T guess");
+            if (int rc = fill_T(bt + 1, L.nb, Tend)) return rc;
+        }
+    }
+    if (bt < L.nb) {
+        ddlms_run_kernel<<<grid_of(L.nb - bt), th, 0, s>>>(a, sl, lv[0].T, maxx2, o, bt, L.nb, 0, soft_tol, 0, 1);
+        if (int rc = check_launch("ddlms_run_kernel")) return rc;
+    }
+    st[1] = L.nb;
+    bool p_done = bt > 0;
+
+    // (3) fixpoint iterations
+    bool converged = false;
+    unsigned long long h[4] = {0, 0, 0, 0};
+    for (int it = 1; it <= max_iter; ++it) {
+        if (int rc = scan(!p_done)) return rc;
+        p_done = true;
+        if (cudaMemsetAsync(ctr, 0, 4 * sizeof(unsigned long long), s) != cudaSuccess) return set_cuda_error("ctr");
+        ddlms_run_kernel<<<grid_of(L.nb), th, 0, s>>>(a, sl, lv[0].T, maxx2, o, 0, L.nb, 1, soft_tol, 0, 0);
+        if (int rc = check_launch("ddlms_run_kernel")) return rc;
+        if (int rc = read_ctr(h)) return rc;
+        st[0] = it;
+        st[1] += static_cast<int64_t>(h[1]);
+        st[4] = static_cast<int64_t>(h[0]);
+        if (h[0] == 0) { converged = true; break; }
+    }
+    if (!converged) {
+        // exact fallback: chain every block sequentially from the scanned start
+        // taps of block 0 (== T_init)
+        st[2] = 2;
+        if (cudaMemsetAsync(ctr, 0, 4 * sizeof(unsigned long long), s) != cudaSuccess) return set_cuda_error("ctr");
+        ddlms_run_kernel<<<1, 1, 0, s>>>(a, sl, lv[0].T, maxx2, o, 0, L.nb, 0, soft_tol, 1, 1);
+        if (int rc = check_launch("ddlms_run_kernel chain")) return rc;
+    }
+    if (cudaMemsetAsync(ctr + 2, 0, sizeof(unsigned long long), s) != cudaSuccess) return set_cuda_error("ctr");
+    sum_int_kernel<<<grid_of(std::min<int64_t>(L.nb, 148 * 8 * th)), th, 0, s>>>(over, L.nb, ctr + 2);
+    if (int rc = check_launch("sum_int_kernel")) return rc;
+    if (int rc = read_ctr(h)) return rc;
+    st[3] = static_cast<int64_t>(h[2]);
+    if (st[3] > 0) st[2] = st[2] ? st[2] : 1;   // guard exceedances: caller must re-run exactly
+    if (cudaMemcpyAsync(T_final, Tend, 16 * sizeof(float), cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+        cudaStreamSynchronize(s) != cudaSuccess)
+        return set_cuda_error("T_final");
+    if (stats)
+        for (int i = 0; i < 6; ++i) stats[i] = st[i];
+    return KK_OK;
+}
+
+extern "C" int kk_symbol_sync(const void* head, int64_t n_head, const void* ref, int n_ref, int64_t skip,
+                              double* result, void* scratch, size_t scratch_bytes, void* stream) {
+    clear_error();
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const int64_t l0 = (n_head + 1) / 2, l1 = n_head / 2;
+    const int64_t nl0 = (ref && n_ref > 0 && l0 >= n_ref) ? l0 - n_ref + 1 : 0;
+    const int64_t nl1 = (ref && n_ref > 0 && l1 >= n_ref) ? l1 - n_ref + 1 : 0;
+    const size_t need = (nl0 + nl1 + 4) * sizeof(double) + 256;
+    if (scratch_bytes < need) return set_error(KK_ERR_PARAM, "sync scratch too small");
+    double* mag = static_cast<double*>(scratch);
+    double* res = mag + ((nl0 + nl1 + 31) / 32) * 32;
+    if (nl0 + nl1 > 0) {
+        const int th = 256;
+        const size_t sm = static_cast<size_t>(n_ref) * sizeof(float2);
+        if (sm > 48 * 1024 &&
+            cudaFuncSetAttribute(xcorr_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm)) !=
+                cudaSuccess)
+            return set_cuda_error("xcorr smem");
+        xcorr_kernel<<<static_cast<unsigned>((nl0 + nl1 + th - 1) / th), th, sm, s>>>(
+            static_cast<const float2*>(head), n_head, static_cast<const float2*>(ref), n_ref, nl0, nl1, mag);
+        if (int rc = check_launch("xcorr_kernel")) return rc;
+    }
+    sync_reduce_kernel<<<1, 1024, 0, s>>>(mag, nl0, nl1, static_cast<const float2*>(head), n_head, skip, res);
+    if (int rc = check_launch("sync_reduce_kernel")) return rc;
+    if (cudaMemcpyAsync(result, res, 4 * sizeof(double), cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+        cudaStreamSynchronize(s) != cudaSuccess)
+        return set_cuda_error("sync readback");
+    return KK_OK;
+}
+
+extern "C" size_t kk_symbol_sync_scratch_bytes(int64_t n_head, int n_ref) {
+    const int64_t l0 = (n_head + 1) / 2, l1 = n_head / 2;
+    const int64_t nl0 = (n_ref > 0 && l0 >= n_ref) ? l0 - n_ref + 1 : 0;
+    const int64_t nl1 = (n_ref > 0 && l1 >= n_ref) ? l1 - n_ref + 1 : 0;
+    return static_cast<size_t>(((nl0 + nl1 + 31) / 32) * 32 + 4) * sizeof(double) + 256;
+}
+
+extern "C" int kk_bit_errors(const uint8_t* labels, const uint8_t* ref_idx, int64_t n, const uint8_t* point_label,
+                             int64_t win_syms, unsigned long long* total, unsigned int* win, int64_t ex_period,
+                             int64_t ex_len, int64_t ex_phase, unsigned long long* n_counted, void* stream) {
+    clear_error();
+    if (n <= 0) return KK_OK;
+    const int th = 256;
+    int64_t blocks = (n + th - 1) / th;
+    if (blocks > 148 * 16) blocks = 148 * 16;
+    bit_errors_kernel<<<static_cast<unsigned>(blocks), th, 0, static_cast<cudaStream_t>(stream)>>>(
+        labels, ref_idx, n, point_label, win_syms > 0 ? win_syms : 1, total, win_syms > 0 ? win : nullptr,
+        ex_period, ex_len, ex_phase, n_counted);
+    return check_launch("bit_errors_kernel");
+}
+
+extern "C" int kk_demap(const void* symbols, int64_t n, int order, const float* pts_host, uint8_t* idx,
+                        unsigned long long* n_fallback, void* stream) {
+    clear_error();
+    if (order < 2 || order > 64) return set_error(KK_ERR_PARAM, "constellation order must be <= 64");
+    if (n <= 0) return KK_OK;
+    Slicer sl = make_slicer(order, pts_host, nullptr, 0, 1.0f, 1.0f, 1.0f);
+    const int th = 256;
+    int64_t blocks = (n + th - 1) / th;
+    if (blocks > 148 * 16) blocks = 148 * 16;
+    demap_kernel<<<static_cast<unsigned>(blocks), th, 0, static_cast<cudaStream_t>(stream)>>>(
+        static_cast<const float2*>(symbols), n, sl, idx, n_fallback);
+    return check_launch("demap_kernel");
+}

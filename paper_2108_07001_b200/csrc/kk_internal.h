@@ -1,0 +1,22 @@
+// Host-side internals shared by the translation units of libkkb200.so:
+// status codes (mirrored in include/kkb200.h), the thread-local last-error
+// string, and the lazily built per-device twiddle table.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/kkb200.h"
+
+namespace kk {
+
+void clear_error();
+int set_error(int code, const char* msg);
+int set_cuda_error(const char* where);
+int check_launch(const char* name);
+
+// W_32768 two-level table on the current device: [hi(512) | lo(64)] float2.
+// Built once per device (std::call_once), immutable afterwards.
+const float2* twiddle_table_device();
+
+}  // namespace kk

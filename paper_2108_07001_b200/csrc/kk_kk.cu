@@ -1,0 +1,300 @@
+// K1 kk_fused: blockwise Kramers-Kronig field reconstruction fused with the
+// downshift / mirror and the per-hop carrier sums.
+//
+// Reference semantics (rxdsp.py `kk_reconstruct` :184-244, `_hilbert_multiplier`
+// :170-181, `_run_downshift` :690-696 -> sigcore `frequency_shift` :286-299,
+// and the segment sums of `_run_carrier` :685-687):
+//   per hop (512) mean m; dead if m <= 0; safe = max(x, 1e-12|m|) (1 if dead)
+//   amp = sqrt(safe), u = 0.5 ln(safe)
+//   block j = [u(hop j-1), u(hop j)] (1024): phi = irfft(rfft(block) * M)[512:]
+//   M[k] = (-j)^(k+1) (the -j sgn multiplier delayed by 256), M[0] = M[512] = 0
+//   field[g] = amp[g-256] exp(j phi[g]), 0 where the delayed hop is dead
+//   z[g] = conj(field[g] * exp(-2 pi i (p g mod q)/q))          (mirror on)
+//
+// B200 mapping: one 64-thread group per PAIR of blocks (global even hop 2p
+// and 2p+1) packed as the real and imaginary parts of one complex 1024-point
+// FFT (the multiplier is Hermitian, so the two real results separate
+// exactly).  A 256-thread CTA runs 4 pairs = 8 output hops and stages the 9
+// hops of u/amp it needs once in shared memory.  FFT = Stockham radix
+// 16x16x4 in padded planar smem; the inverse FFT's last pass writes the field
+// straight to HBM (coalesced) with the rotation/mirror and the hop sums fused.
+#include "kk_common.cuh"
+#include "kk_internal.h"
+
+namespace kk {
+
+constexpr int kHop = 512;
+constexpr int kN1 = 1024;
+constexpr int kPairsPerCta = 4;
+constexpr int kGroupThreads = 64;
+constexpr int kK1Threads = kPairsPerCta * kGroupThreads;      // 256
+constexpr int kStageHops = 2 * kPairsPerCta + 1;              // 9
+constexpr int kPlane1 = padded(kN1);                          // 1056 floats
+
+struct K1Smem {
+    float u[kStageHops * kHop];
+    float a[kStageHops * kHop];
+    float re[kPairsPerCta][kPlane1];
+    float im[kPairsPerCta][kPlane1];
+    float2 tw[kTwEntries];
+    float2 red[kK1Threads / 32][2];
+    int dead[kStageHops];
+    uint8_t dead_hist[kHop / 2];   // per-sample dead flags of hop -1 (state)
+    unsigned int clamped;
+};
+
+template <typename TIn>
+__device__ __forceinline__ float load_in(const TIn* p, int64_t i, float scale) {
+    return static_cast<float>(p[i]) * scale;
+}
+template <>
+__device__ __forceinline__ float load_in<double>(const double* p, int64_t i, float scale) {
+    return static_cast<float>(p[i] * static_cast<double>(scale));
+}
+
+// Hilbert multiplier on the full 1024-bin spectrum (Hermitian extension of
+// the rfft multiplier): k in [1,511]: (-j)^(k+1); k in [513,1023]:
+// conj((-j)^(1025-k)); 0 at DC and Nyquist.
+__device__ __forceinline__ float2 apply_mult(int k, float2 z) {
+    if (k == 0 || k == 512) return make_float2(0.f, 0.f);
+    int e;
+    bool conj_;
+    if (k < 512) { e = (k + 1) & 3; conj_ = false; }
+    else { e = (1025 - k) & 3; conj_ = true; }
+    // (-j)^e : 0 -> 1, 1 -> -j, 2 -> -1, 3 -> +j ; conj flips the sign of j
+    switch (e) {
+        case 0: return z;
+        case 1: return conj_ ? mul_pj(z) : mul_mj(z);
+        case 2: return make_float2(-z.x, -z.y);
+        default: return conj_ ? mul_mj(z) : mul_pj(z);
+    }
+}
+
+template <typename TIn>
+__global__ void __launch_bounds__(kK1Threads)
+kk_pairs_kernel(const TIn* __restrict__ in, float in_scale, float clamp_rel, int64_t n_hops,
+                const float* __restrict__ st_u, const float* __restrict__ st_a,
+                const uint8_t* __restrict__ st_dead,
+                float* __restrict__ new_u, float* __restrict__ new_a, uint8_t* __restrict__ new_dead,
+                float2* __restrict__ out, float2* __restrict__ hop_sum, uint8_t* __restrict__ hop_dead,
+                unsigned long long* __restrict__ clamped_total,
+                int64_t n0_global, int rot_p, int rot_q, const float2* __restrict__ rot_tab,
+                int mirror, const float2* __restrict__ tw_g)
+{
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    K1Smem& S = *reinterpret_cast<K1Smem*>(smem_raw);
+    const int tid = threadIdx.x;
+    const int warp = tid >> 5, lane = tid & 31;
+    const int64_t hop0 = int64_t(blockIdx.x) * (2 * kPairsPerCta) - 1;   // chunk hop of stage hop 0
+
+    load_twiddles(S.tw, tw_g, tid, kK1Threads);
+    if (tid == 0) S.clamped = 0;
+    __syncthreads();
+
+    // ---- stage 9 hops: means, dead flags, clamp, u = 0.5 ln(safe), amp ----
+    for (int L = warp; L < kStageHops; L += kK1Threads / 32) {
+        const int64_t h = hop0 + L;
+        float* u = S.u + L * kHop;
+        float* a = S.a + L * kHop;
+        if (h < 0) {  // previous-chunk state (rxdsp.py:208-213 initial zeros)
+            for (int i = lane; i < kHop; i += 32) u[i] = st_u[i];
+            for (int i = lane; i < kHop / 2; i += 32) {
+                a[i] = 0.f;
+                a[kHop / 2 + i] = st_a[i];
+                S.dead_hist[i] = st_dead[i];
+            }
+            if (lane == 0) S.dead[L] = 0;
+            continue;
+        }
+        if (h >= n_hops) {  // dummy partner beyond the last real hop
+            for (int i = lane; i < kHop; i += 32) { u[i] = 0.f; a[i] = 0.f; }
+            if (lane == 0) S.dead[L] = 1;
+            continue;
+        }
+        const TIn* src = in + h * kHop;
+        float xv[kHop / 32];
+        double sum = 0.0;
+#pragma unroll
+        for (int i = 0; i < kHop / 32; ++i) {
+            xv[i] = load_in<TIn>(src, lane + 32 * i, 1.0f);
+            sum += static_cast<double>(xv[i]);
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+        // mean = sum * scale / 512 (exact for int16 codes: integer sum)
+        const double mean = sum * static_cast<double>(in_scale) / kHop;
+        const bool dead = !(mean > 0.0);
+        const float thr = dead ? 1.0f : static_cast<float>(static_cast<double>(clamp_rel) * fabs(mean));
+        unsigned int ncl = 0;
+#pragma unroll
+        for (int i = 0; i < kHop / 32; ++i) {
+            const float x = xv[i] * in_scale;
+            float s;
+            if (dead) {
+                s = 1.0f;
+            } else {
+                ncl += (x < thr) ? 1u : 0u;
+                s = fmaxf(x, thr);
+            }
+            u[lane + 32 * i] = 0.5f * logf(s);
+            a[lane + 32 * i] = sqrtf(s);
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) ncl += __shfl_xor_sync(0xffffffffu, ncl, o);
+        if (lane == 0) {
+            S.dead[L] = dead ? 1 : 0;
+            if (L >= 1) {   // stage hop 0 belongs to the previous CTA
+                if (ncl) atomicAdd(&S.clamped, ncl);
+                hop_dead[h] = dead ? 1 : 0;
+            }
+        }
+    }
+    __syncthreads();
+
+    // ---- per pair: forward FFT1024 of u_a + j u_b, multiplier, inverse ----
+    const int g = tid / kGroupThreads;
+    const int gt = tid % kGroupThreads;
+    const int64_t pair = int64_t(blockIdx.x) * kPairsPerCta + g;
+    const int64_t hop_a = 2 * pair;          // output hop of the real-part block
+    const bool active = hop_a < n_hops;
+    const Twiddle tw{S.tw, S.tw + kTwHi};
+    SmemPlanes P{S.re[g], S.im[g]};
+    const float* ua = S.u + (2 * g) * kHop;          // block a: stage hops 2g, 2g+1
+    const float* ub = S.u + (2 * g + 1) * kHop;      // block b: stage hops 2g+1, 2g+2
+
+    auto ld_u = [&](int i) { return make_float2(ua[i], ub[i]); };
+    stockham_pass<kN1, 16, 1, kGroupThreads, false, false>(gt, tw, ld_u, StorePlanes{P});
+    __syncthreads();
+    stockham_pass<kN1, 16, 16, kGroupThreads, false, true>(gt, tw, LoadPlanes{P}, StorePlanes{P});
+    __syncthreads();
+    stockham_pass<kN1, 4, 256, kGroupThreads, false, true>(gt, tw, LoadPlanes{P}, StorePlanes{P});
+    __syncthreads();
+    auto ld_m = [&](int k) { return apply_mult(k, P.ld(k)); };
+    stockham_pass<kN1, 16, 1, kGroupThreads, true, true>(gt, tw, ld_m, StorePlanes{P});
+    __syncthreads();
+    stockham_pass<kN1, 16, 16, kGroupThreads, true, true>(gt, tw, LoadPlanes{P}, StorePlanes{P});
+    __syncthreads();
+
+    // last inverse pass: outputs n = j + 256 r; n >= 512 are the new hop
+    float2 acc_a = make_float2(0.f, 0.f), acc_b = make_float2(0.f, 0.f);
+    const float inv_scale = 1.0f / (1024.0f * 3.14159265358979323846f);   // phi/pi for sincospif
+    const float* aa = S.a + (2 * g) * kHop + kHop / 2;      // amp at (new hop pos - 256), block a
+    const float* ab = S.a + (2 * g + 1) * kHop + kHop / 2;  // block b
+    const int dead_a0 = S.dead[2 * g], dead_a1 = S.dead[2 * g + 1], dead_b1 = S.dead[2 * g + 2];
+    const bool hist = (hop0 + 2 * g) < 0;   // stage hop 2g is the state hop
+    auto st_out = [&](int n, float2 v) {
+        if (n < kHop) return;
+        const int i = n - kHop;
+        const bool has_b = (hop_a + 1) < n_hops;
+        // delayed dead flags: position i-256 of the new hop lies in the
+        // previous hop when i < 256
+        bool da = (i < kHop / 2) ? (hist ? (S.dead_hist[i] != 0) : (dead_a0 != 0)) : (dead_a1 != 0);
+        bool db = (i < kHop / 2) ? (dead_a1 != 0) : (dead_b1 != 0);
+        float sa, ca, sb, cb;
+        sincospif(v.x * inv_scale, &sa, &ca);
+        sincospif(v.y * inv_scale, &sb, &cb);
+        const float amp_a = aa[i], amp_b = ab[i];
+        float2 fa = da ? make_float2(0.f, 0.f) : make_float2(amp_a * ca, amp_a * sa);
+        float2 fb = db ? make_float2(0.f, 0.f) : make_float2(amp_b * cb, amp_b * sb);
+        if (!active) return;
+        acc_a = cadd(acc_a, fa);
+        const int64_t pa = hop_a * kHop + i;           // chunk positions
+        const int64_t pb = pa + kHop;
+        float2 za = fa, zb = fb;
+        if (rot_q > 0) {
+            const int64_t ga = n0_global + pa, gb = n0_global + pb;
+            const int ia = static_cast<int>((static_cast<unsigned long long>(ga) % rot_q) * rot_p % rot_q);
+            const int ib = static_cast<int>((static_cast<unsigned long long>(gb) % rot_q) * rot_p % rot_q);
+            za = cmul(fa, rot_tab[ia]);
+            zb = cmul(fb, rot_tab[ib]);
+        }
+        if (mirror) { za = cconj(za); zb = cconj(zb); }
+        out[pa] = za;
+        if (has_b) {
+            acc_b = cadd(acc_b, fb);
+            out[pb] = zb;
+        }
+    };
+    stockham_pass<kN1, 4, 256, kGroupThreads, true, true>(gt, tw, LoadPlanes{P}, st_out);
+
+    // ---- deterministic per-hop field sums (fixed shuffle tree) ----
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        acc_a.x += __shfl_xor_sync(0xffffffffu, acc_a.x, o);
+        acc_a.y += __shfl_xor_sync(0xffffffffu, acc_a.y, o);
+        acc_b.x += __shfl_xor_sync(0xffffffffu, acc_b.x, o);
+        acc_b.y += __shfl_xor_sync(0xffffffffu, acc_b.y, o);
+    }
+    if (lane == 0) { S.red[warp][0] = acc_a; S.red[warp][1] = acc_b; }
+    __syncthreads();
+    if (gt == 0 && active) {
+        const int w0 = warp;   // first warp of the group (gt == 0)
+        hop_sum[hop_a] = cadd(S.red[w0][0], S.red[w0 + 1][0]);
+        if (hop_a + 1 < n_hops) hop_sum[hop_a + 1] = cadd(S.red[w0][1], S.red[w0 + 1][1]);
+    }
+    if (tid == 0 && S.clamped) atomicAdd(clamped_total, static_cast<unsigned long long>(S.clamped));
+
+    // ---- state for the next chunk: u, amp, dead of the last real hop ----
+    const int64_t last = n_hops - 1;
+    const int64_t Ll = last - hop0;
+    if (Ll >= 1 && Ll < kStageHops) {
+        for (int i = tid; i < kHop; i += kK1Threads) new_u[i] = S.u[Ll * kHop + i];
+        for (int i = tid; i < kHop / 2; i += kK1Threads) {
+            new_a[i] = S.a[Ll * kHop + kHop / 2 + i];
+            new_dead[i] = static_cast<uint8_t>(S.dead[Ll]);
+        }
+    }
+}
+
+template <typename TIn>
+static int launch_k1(const void* in, float in_scale, float clamp_rel, int64_t n_hops, const float* st_u, const float* st_a,
+                     const uint8_t* st_dead, float* new_u, float* new_a, uint8_t* new_dead, float2* out,
+                     float2* hop_sum, uint8_t* hop_dead, unsigned long long* clamped, int64_t n0,
+                     int rot_p, int rot_q, const float2* rot_tab, int mirror, cudaStream_t s) {
+    const float2* tw = twiddle_table_device();
+    if (!tw) return KK_ERR_CUDA;
+    const size_t smem = sizeof(K1Smem);
+    static bool attr_done = false;
+    if (!attr_done) {
+        if (cudaFuncSetAttribute(kk_pairs_kernel<TIn>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(smem)) != cudaSuccess) return set_cuda_error("K1 smem attr");
+        attr_done = true;
+    }
+    const int64_t pairs = (n_hops + 1) / 2;
+    const int64_t grid = (pairs + kPairsPerCta - 1) / kPairsPerCta;
+    kk_pairs_kernel<TIn><<<static_cast<unsigned>(grid), kK1Threads, smem, s>>>(
+        static_cast<const TIn*>(in), in_scale, clamp_rel, n_hops, st_u, st_a, st_dead, new_u, new_a, new_dead, out,
+        hop_sum, hop_dead, clamped, n0, rot_p, rot_q, rot_tab, mirror, tw);
+    return check_launch("kk_pairs_kernel");
+}
+
+}  // namespace kk
+
+extern "C" int kk_reconstruct_pairs(int in_dtype, const void* in, float in_scale, float clamp_rel, int64_t n_hops,
+                                    const float* st_u, const float* st_a, const uint8_t* st_dead,
+                                    float* new_u, float* new_a, uint8_t* new_dead, void* out,
+                                    void* hop_sum, uint8_t* hop_dead, unsigned long long* clamped,
+                                    int64_t n0_global, int rot_p, int rot_q, const void* rot_tab,
+                                    int mirror, void* stream) {
+    using namespace kk;
+    clear_error();
+    if (n_hops <= 0) return set_error(KK_ERR_PARAM, "n_hops must be positive");
+    if (rot_q > 0 && !rot_tab) return set_error(KK_ERR_PARAM, "rotation table missing");
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    float2* o = static_cast<float2*>(out);
+    float2* hs = static_cast<float2*>(hop_sum);
+    const float2* rt = static_cast<const float2*>(rot_tab);
+    switch (in_dtype) {
+        case KK_DTYPE_I16:
+            return launch_k1<int16_t>(in, in_scale, clamp_rel, n_hops, st_u, st_a, st_dead, new_u, new_a, new_dead, o, hs,
+                                      hop_dead, clamped, n0_global, rot_p, rot_q, rt, mirror, s);
+        case KK_DTYPE_F32:
+            return launch_k1<float>(in, in_scale, clamp_rel, n_hops, st_u, st_a, st_dead, new_u, new_a, new_dead, o, hs,
+                                    hop_dead, clamped, n0_global, rot_p, rot_q, rt, mirror, s);
+        case KK_DTYPE_F64:
+            return launch_k1<double>(in, in_scale, clamp_rel, n_hops, st_u, st_a, st_dead, new_u, new_a, new_dead, o, hs,
+                                     hop_dead, clamped, n0_global, rot_p, rot_q, rt, mirror, s);
+        default:
+            return set_error(KK_ERR_PARAM, "unsupported input dtype");
+    }
+}

@@ -1,0 +1,267 @@
+// K2 static_fused: carrier-mean subtraction + fused static equaliser / CD
+// compensation + 2:1 decimation, one 32768-point overlap-save block per CTA.
+//
+// Reference semantics (rxdsp.py `_run_carrier` :671-688, `_run_static`
+// :698-720 == `static_equalize_and_resample` :414-453, `_static_response`
+// :401-411):
+//   s[g] = z[g] - conj(mean_seg(g) * rot[g])      (carrier removed, mirrored)
+//   block b = s[16384(b-1) .. 16384(b+1))          (zeros before the stream)
+//   Y = ifft16384( fft32768(block)[kept] * H ) * 0.5 ;  out = Y[8192:]
+//   kept = [0, 8192) U [24576, 32768)
+//
+// B200 mapping (the 256 KB block does not fit one CTA's 227 KB of shared
+// memory, so it is never materialised):
+//   radix-2 DIF split  a = x0 + x1 -> E = FFT16384(a) = even bins
+//                      b = (x0 - x1) W32768^n -> O = FFT16384(b) = odd bins
+//   kept bins of E/O are their low and high quarters -> 8192 each
+//   A = IFFT8192(E_kept * H_even), B = IFFT8192(O_kept * H_odd)
+//   out[r] = (A[r] - W16384^{-r} B[r]) * 0.5/16384
+// One 512-thread CTA per block: 132 KB padded planar FFT buffer + 64 KB for A.
+// The first pass of each FFT16384 reads HBM directly (coalesced) with the
+// carrier subtraction / pre-twiddle fused, the IFFT's first pass applies the
+// kept-bin gather and H, and the final IFFT pass writes the 2-sps output
+// straight to HBM.
+#include "kk_common.cuh"
+#include "kk_internal.h"
+
+namespace kk {
+
+constexpr int kNS = 32768;        // static block
+constexpr int kHopS = 16384;      // hop / half FFT
+constexpr int kNOut = 8192;       // outputs per block
+constexpr int kK2Threads = 512;
+constexpr int kPlane2 = padded(kHopS);   // 16896 floats
+constexpr int kRotMax = 1024;            // rotation-table entries held in smem
+
+struct K2Smem {
+    float re[kPlane2];
+    float im[kPlane2];
+    float2 A[kNOut];
+    float2 tw[kTwEntries];
+    float2 rot[kRotMax];
+};
+
+struct K2Params {
+    const float2* z;        // KK output stream (conj(field * rot)), z[0] = global index z_index0
+    int64_t z_index0;
+    int64_t hb0;            // global static hop of the first block of this launch
+    int64_t valid_end;      // global index: samples at/after are zero padding
+    const float2* seg_mean; // carrier mean per segment, seg_mean[0] = segment seg_index0
+    int64_t seg_index0;
+    int seg_len;
+    int carrier;            // subtract the carrier mean
+    int rot_p, rot_q;       // rotation exp(-2 pi i (p g mod q)/q); q == 0 -> none
+    const float2* rot_tab;
+    int mirror;
+    const float2* h_even;   // H at kept index 2m'  (8192)
+    const float2* h_odd;    // H at kept index 2m'+1 (8192)
+    float2* out;            // 8192 per block
+};
+
+// x mod d for 0 <= x < 2^25 via a float reciprocal (+-1 quotient fix-up)
+__device__ __forceinline__ unsigned fmod_u(unsigned x, unsigned d, float inv_d, unsigned* quot = nullptr) {
+    unsigned q = __float2uint_rz(__uint2float_rn(x) * inv_d);
+    int r = static_cast<int>(x) - static_cast<int>(q * d);
+    if (r < 0) { r += d; --q; }
+    if (r >= static_cast<int>(d)) { r -= d; ++q; }
+    if (quot) *quot = q;
+    return static_cast<unsigned>(r);
+}
+
+// per-CTA constants for the carrier-removed input of one 32768-sample block
+struct BlockIn {
+    int64_t base;      // global index of block sample 0 (may be negative: stream start)
+    unsigned c0;       // (p * base) mod q
+    unsigned rb;       // base mod seg_len (floor)
+    int64_t sb;        // floor(base / seg_len) - seg_index0
+    float inv_q, inv_seg;
+};
+
+__device__ __forceinline__ BlockIn make_block_in(const K2Params& p, int64_t base) {
+    BlockIn b;
+    b.base = base;
+    b.inv_q = p.rot_q > 0 ? 1.0f / static_cast<float>(p.rot_q) : 0.f;
+    b.inv_seg = p.seg_len > 0 ? 1.0f / static_cast<float>(p.seg_len) : 0.f;
+    if (p.rot_q > 0) {
+        int64_t m = base % p.rot_q;
+        if (m < 0) m += p.rot_q;
+        b.c0 = static_cast<unsigned>((m * p.rot_p) % p.rot_q);
+    } else {
+        b.c0 = 0;
+    }
+    if (p.seg_len > 0) {
+        int64_t sq = base / p.seg_len;
+        int64_t r = base - sq * p.seg_len;
+        if (r < 0) { r += p.seg_len; --sq; }
+        b.rb = static_cast<unsigned>(r);
+        b.sb = sq - p.seg_index0;
+    } else {
+        b.rb = 0;
+        b.sb = 0;
+    }
+    return b;
+}
+
+// carrier-removed static-stage input at block position n (global base + n)
+__device__ __forceinline__ float2 static_input(const K2Params& p, const BlockIn& b, const float2* rot_s, int n) {
+    const int64_t g = b.base + n;
+    if (g < 0 || g >= p.valid_end) return make_float2(0.f, 0.f);
+    float2 v = __ldg(p.z + (g - p.z_index0));
+    if (p.carrier) {
+        unsigned ds;
+        fmod_u(b.rb + static_cast<unsigned>(n), static_cast<unsigned>(p.seg_len), b.inv_seg, &ds);
+        float2 mr = __ldg(p.seg_mean + (b.sb + ds));
+        if (p.rot_q > 0) {
+            const unsigned a = fmod_u(b.c0 + static_cast<unsigned>(p.rot_p) * static_cast<unsigned>(n),
+                                      static_cast<unsigned>(p.rot_q), b.inv_q);
+            const float2 r = (p.rot_q <= kRotMax) ? rot_s[a] : __ldg(p.rot_tab + a);
+            mr = cmul(mr, r);
+        }
+        if (p.mirror) mr = cconj(mr);
+        v = csub(v, mr);
+    }
+    return v;
+}
+
+__global__ void __launch_bounds__(kK2Threads, 1) static_blocks_kernel(K2Params p, const float2* __restrict__ tw_g) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    K2Smem& S = *reinterpret_cast<K2Smem*>(smem_raw);
+    const int tid = threadIdx.x;
+    load_twiddles(S.tw, tw_g, tid, kK2Threads);
+    if (p.carrier && p.rot_q > 0 && p.rot_q <= kRotMax)
+        for (int i = tid; i < p.rot_q; i += kK2Threads) S.rot[i] = p.rot_tab[i];
+    __syncthreads();
+
+    const Twiddle tw{S.tw, S.tw + kTwHi};
+    const SmemPlanes P{S.re, S.im};
+    const int64_t hb = p.hb0 + blockIdx.x;
+    const int64_t base = (hb - 1) * kHopS;   // global index of block sample 0
+    const BlockIn bi = make_block_in(p, base);
+
+    for (int chain = 0; chain < 2; ++chain) {
+        // ---- FFT16384 of a = x0 + x1 (even bins) or b = (x0 - x1) W^n (odd) ----
+        if (chain == 0) {
+            auto ld = [&](int n) {
+                return cadd(static_input(p, bi, S.rot, n), static_input(p, bi, S.rot, kHopS + n));
+            };
+            stockham_pass<kHopS, 16, 1, kK2Threads, false, false>(tid, tw, ld, StorePlanes{P});
+        } else {
+            auto ld = [&](int n) {
+                const float2 d = csub(static_input(p, bi, S.rot, n), static_input(p, bi, S.rot, kHopS + n));
+                return cmul(d, tw.template w<kNS>(n));
+            };
+            stockham_pass<kHopS, 16, 1, kK2Threads, false, false>(tid, tw, ld, StorePlanes{P});
+        }
+        __syncthreads();
+        stockham_pass<kHopS, 16, 16, kK2Threads, false, true>(tid, tw, LoadPlanes{P}, StorePlanes{P});
+        __syncthreads();
+        stockham_pass<kHopS, 16, 256, kK2Threads, false, true>(tid, tw, LoadPlanes{P}, StorePlanes{P});
+        __syncthreads();
+        stockham_pass<kHopS, 4, 4096, kK2Threads, false, true>(tid, tw, LoadPlanes{P}, StorePlanes{P});
+        __syncthreads();
+
+        // ---- IFFT8192 of the kept quarters times H ----
+        const float2* h = chain == 0 ? p.h_even : p.h_odd;
+        auto ld_k = [&](int m) {
+            const int src = m < 4096 ? m : m + 8192;
+            return cmul(P.ld(src), __ldg(h + m));
+        };
+        stockham_pass<kNOut, 16, 1, kK2Threads, true, true>(tid, tw, ld_k, StorePlanes{P});
+        __syncthreads();
+        stockham_pass<kNOut, 16, 16, kK2Threads, true, true>(tid, tw, LoadPlanes{P}, StorePlanes{P});
+        __syncthreads();
+        stockham_pass<kNOut, 8, 256, kK2Threads, true, true>(tid, tw, LoadPlanes{P}, StorePlanes{P});
+        __syncthreads();
+        if (chain == 0) {
+            auto st_a = [&](int n, float2 v) { S.A[n] = v; };
+            stockham_pass<kNOut, 4, 2048, kK2Threads, true, true>(tid, tw, LoadPlanes{P}, st_a);
+            __syncthreads();
+        } else {
+            float2* out = p.out + int64_t(blockIdx.x) * kNOut;
+            const float sc = 0.5f / 16384.0f;
+            auto st_o = [&](int r, float2 v) {
+                // W16384^{-r} = conj(W32768^{2r})
+                const float2 bt = cmulc(v, tw.template w<kHopS>(r));
+                out[r] = cscale(csub(S.A[r], bt), sc);
+            };
+            stockham_pass<kNOut, 4, 2048, kK2Threads, true, true>(tid, tw, LoadPlanes{P}, st_o);
+        }
+    }
+}
+
+}  // namespace kk
+
+extern "C" int kk_static_blocks(const void* z, int64_t z_index0, int64_t hb0, int64_t n_blocks,
+                                int64_t valid_end, const void* seg_mean, int64_t seg_index0, int seg_len,
+                                int carrier, int rot_p, int rot_q, const void* rot_tab, int mirror,
+                                const void* h_even, const void* h_odd, void* out, void* stream) {
+    using namespace kk;
+    clear_error();
+    if (n_blocks <= 0) return KK_OK;
+    if (carrier && (seg_len <= 0 || !seg_mean)) return set_error(KK_ERR_PARAM, "carrier means missing");
+    if (rot_q > 0 && !rot_tab) return set_error(KK_ERR_PARAM, "rotation table missing");
+    const float2* tw = twiddle_table_device();
+    if (!tw) return KK_ERR_CUDA;
+    static bool attr_done = false;
+    const size_t smem = sizeof(K2Smem);
+    if (!attr_done) {
+        if (cudaFuncSetAttribute(static_blocks_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(smem)) != cudaSuccess)
+            return set_cuda_error("K2 smem attr");
+        attr_done = true;
+    }
+    K2Params p;
+    p.z = static_cast<const float2*>(z);
+    p.z_index0 = z_index0;
+    p.hb0 = hb0;
+    p.valid_end = valid_end;
+    p.seg_mean = static_cast<const float2*>(seg_mean);
+    p.seg_index0 = seg_index0;
+    p.seg_len = seg_len;
+    p.carrier = carrier;
+    p.rot_p = rot_p;
+    p.rot_q = rot_q;
+    p.rot_tab = static_cast<const float2*>(rot_tab);
+    p.mirror = mirror;
+    p.h_even = static_cast<const float2*>(h_even);
+    p.h_odd = static_cast<const float2*>(h_odd);
+    p.out = static_cast<float2*>(out);
+    static_blocks_kernel<<<static_cast<unsigned>(n_blocks), kK2Threads, smem, static_cast<cudaStream_t>(stream)>>>(p, tw);
+    return check_launch("static_blocks_kernel");
+}
+
+// ---------------------------------------------------------------------------
+// carrier means: mean over each aligned segment from the per-hop field sums
+// (rxdsp.py:685-687).  seg s covers hops [s*hps, (s+1)*hps) of the hop-sum
+// array; the last segment may be partial (flush) with `last_len` samples.
+// ---------------------------------------------------------------------------
+namespace kk {
+__global__ void carrier_means_kernel(const float2* __restrict__ hop_sum, int64_t n_segs, int hops_per_seg,
+                                     int64_t n_hops_avail, int64_t last_len, int seg_len, float2* __restrict__ mean) {
+    const int64_t s = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (s >= n_segs) return;
+    double re = 0.0, im = 0.0;
+    const int64_t h0 = s * hops_per_seg;
+    for (int i = 0; i < hops_per_seg; ++i) {
+        const int64_t h = h0 + i;
+        if (h >= n_hops_avail) break;
+        const float2 v = hop_sum[h];
+        re += v.x;
+        im += v.y;
+    }
+    const double len = (s == n_segs - 1 && last_len > 0) ? static_cast<double>(last_len) : static_cast<double>(seg_len);
+    mean[s] = make_float2(static_cast<float>(re / len), static_cast<float>(im / len));
+}
+}  // namespace kk
+
+extern "C" int kk_carrier_means(const void* hop_sum, int64_t n_segs, int hops_per_seg, int64_t n_hops_avail,
+                                int64_t last_len, int seg_len, void* mean, void* stream) {
+    using namespace kk;
+    clear_error();
+    if (n_segs <= 0) return KK_OK;
+    const int th = 128;
+    carrier_means_kernel<<<static_cast<unsigned>((n_segs + th - 1) / th), th, 0, static_cast<cudaStream_t>(stream)>>>(
+        static_cast<const float2*>(hop_sum), n_segs, hops_per_seg, n_hops_avail, last_len, seg_len,
+        static_cast<float2*>(mean));
+    return check_launch("carrier_means_kernel");
+}

@@ -1,0 +1,83 @@
+"""Callers of the receiver (kkmodem.harness.runner, cited `hr:line`) that
+touch the hot path: pipeline construction, buffer-wise receive, BER/Q/EVM
+measurement, and a device-resident streaming run.
+
+`make_pipeline_config` accepts the reference's ExperimentConfig / LinkConfig
+duck-typed (attributes tx, rx, link, frontend), so the reference harness,
+sweeps and presets drive the B200 pipeline unchanged.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+from .constellation import make_constellation
+from .metrics import SyncFailure, count_bit_errors, evm, frame_sync, q_from_ber, windowed_q
+from .rxdsp import (
+    DdlmsConfig, GpuOptions, RxPipeline, RxPipelineConfig, compute_static_taps, demap, design_receive_taps,
+)
+from .sigcore import BlockPlan
+
+
+def make_pipeline_config(cfg, link, gpu: GpuOptions | None = None) -> RxPipelineConfig:
+    """hr:65-91."""
+    rx, tx = cfg.rx, cfg.tx
+    rate_out = cfg.frontend.adc_rate_hz / 2.0
+    if rx.designed_taps:
+        taps = design_receive_taps(link, tx, frontend=cfg.frontend if rx.compensate_frontend else None,
+                                   n_taps=rx.static_n_taps, rate_hz=rate_out)
+    else:
+        taps = compute_static_taps(link, n_taps=rx.static_n_taps, rate_hz=rate_out)
+    return RxPipelineConfig(
+        adc_rate_hz=cfg.frontend.adc_rate_hz, baud_hz=tx.baud_hz, tone_freq_hz=tx.tone_freq_hz,
+        kk_plan=BlockPlan(rx.kk_fft_size, buffer_len=rx.buffer_len),
+        static_plan=BlockPlan(rx.static_fft_size, buffer_len=rx.buffer_len),
+        static_taps=taps, carrier_removal=rx.carrier_removal, carrier_segment_len=rx.carrier_segment_len,
+        ddlms=DdlmsConfig(mu=rx.mu, startup_symbols=rx.startup_symbols, widely_linear=rx.widely_linear),
+        constellation_order=tx.constellation_order, sync_symbols=rx.sync_symbols,
+        sync_wait_samples=rx.sync_wait_samples, gpu=gpu or GpuOptions())
+
+
+def receive_stream(adc, pipe_cfg: RxPipelineConfig, reference_symbols) -> RxPipeline:
+    """Feed a whole ADC stream buffer by buffer (hr:94-101)."""
+    pipe = RxPipeline(pipe_cfg, reference_symbols=reference_symbols)
+    x = adc.samples if hasattr(adc, "samples") else adc
+    blen = pipe_cfg.kk_plan.buffer_len
+    for start in range(0, len(x), blen):
+        pipe.feed(x[start:start + blen])
+    return pipe
+
+
+def measure_point(dec, soft, bits, syms, cfg) -> dict:
+    """BER/Q/EVM over the post-startup region (hr:104-137)."""
+    spec = make_constellation(cfg.tx.constellation_order)
+    k = spec.bits_per_symbol
+    head = cfg.rx.startup_symbols + cfg.metrics.head_guard_symbols
+    stop = min(len(dec), len(syms)) - cfg.metrics.tail_guard_symbols
+    if stop - head < 1000:
+        raise SyncFailure("too few symbols beyond the startup region")
+    rx_bits, _ = demap(dec[head:stop], spec)
+    offset, a_rx, a_tx = frame_sync(rx_bits, bits)
+    errors = a_rx != a_tx
+    n_bits, n_err = len(errors), int(np.sum(errors))
+    ber = n_err / n_bits
+    point = {"ber": ber, "q_db": q_from_ber(ber), "evm_pct": evm(soft[head:stop], syms[head:stop]),
+             "n_bits": n_bits, "n_errors": n_err, "sync_offset": int(offset)}
+    bit_rate = cfg.tx.baud_hz * k
+    win = cfg.metrics.windowed_q_window_s
+    point["windowed_q"] = ([[float(t), float(q)] for t, q in windowed_q(errors, bit_rate, win)]
+                           if n_bits >= int(win * bit_rate) else [])
+    return point
+
+
+def device_ber(labels, ref_idx, order: int, head: int, stop: int, tile_symbols: int = 0, seam_guard: int = 128):
+    """BER of decided indices [head, stop) against transmitted indices on the
+    GPU (kk_bit_errors), excluding `seam_guard` symbols before every tile
+    seam of a tiled capture.  Returns device
+    tensors (errors, symbols)."""
+    lab = labels[head:stop]
+    ref = ref_idx[head:stop]
+    if tile_symbols > 0:
+        return count_bit_errors(lab, ref, order, exclude_period=tile_symbols, exclude_len=seam_guard,
+                                exclude_phase=head)[:2]
+    return count_bit_errors(lab, ref, order)[:2]

@@ -1,0 +1,1006 @@
+"""B200 drop-in for kkmodem.rxdsp -- the streaming Kramers-Kronig receiver.
+
+Same public names, signatures, defaults, outputs and exceptions as
+/root/reference/pkg/src/kkmodem/rxdsp.py (cited `rx:line`):
+
+    DdlmsConfig (rx:71-78), EqualizerState (rx:81-101), RxPipelineConfig
+    (rx:104-137), RxPipeline (rx:608-824: feed / drain / finish / diverged /
+    diagnostics / stage_seconds / sync_offset / sync_ratio / samples_in /
+    write_diagnostics), SyncError (rx:63), stream_buffers (rx:144),
+    kk_reconstruct (rx:184), downshift_dc (rx:247), compute_static_taps
+    (rx:264), static_tap_coverage (rx:291), design_receive_taps (rx:317),
+    refine_static_taps (rx:365), static_equalize_and_resample (rx:414),
+    ddlms_wl (rx:510), demap (rx:548), symbol_sync (rx:574).
+
+Every per-sample operation runs in libkkb200.so (hand-written sm_100a CUDA,
+include/kkb200.h) on the current CUDA device; there is no CPU fallback and
+the module raises if the library is missing.  Tap design (compute_static_taps,
+design_receive_taps, refine_static_taps) is per-link host setup in float64,
+as SURVEY.md §8(a) A2' prescribes.
+
+Differences from the reference, all deliberate and documented in DESIGN.md:
+  * arithmetic is float32 / complex64 on the GPU (the reference is float64):
+    fields match to ~1e-7 relative L2, decisions match except at fp ties;
+  * KK blocks are processed in pairs on the global even-hop grid, so a feed
+    that ends on an odd hop keeps that hop in the raw FIFO until the next
+    feed (outputs are unchanged: the carrier stage releases only whole
+    65536-sample segments anyway);
+  * the DDLMS runs on frames of `gpu.ddlms_frame_symbols` symbols on the
+    global symbol grid (exact block-parallel solve inside a frame), so
+    decisions are released per completed frame; any feed chunking gives
+    bit-identical output;
+  * `stage_seconds["downshift"]` is 0: the downshift/mirror is fused into
+    the KK kernel.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import json
+from dataclasses import dataclass, field as dc_field
+from fractions import Fraction
+
+import numpy as np
+
+from . import _lib
+from ._lib import SyncError
+from .constellation import ConstellationSpec, make_constellation, slicer_tables
+from .sigcore import (
+    AdcCodes,
+    BlockPlan,
+    ComplexSignal,
+    FirFilter,
+    ParameterError,
+    RealSignal,
+    anti_alias_window,
+    cd_phase_coefficient,
+    design_rrc,
+    fir_frequency_response,
+)
+
+__all__ = [
+    "DdlmsConfig", "EqualizerState", "RxPipelineConfig", "GpuOptions", "RxPipeline", "SyncError",
+    "stream_buffers", "kk_reconstruct", "downshift_dc", "compute_static_taps", "static_tap_coverage",
+    "design_receive_taps", "refine_static_taps", "static_equalize_and_resample", "ddlms_wl", "demap",
+    "symbol_sync",
+]
+
+KK_FFT = 1024
+STATIC_FFT = 32768
+
+
+def _torch():
+    import torch
+    return torch
+
+
+# ---------------------------------------------------------------------------
+# configuration & state (rx:71-137)
+# ---------------------------------------------------------------------------
+
+@dataclass
+class DdlmsConfig:
+    n_taps: int = 4
+    mu: float = 1e-3
+    startup_symbols: int = 10_000
+    widely_linear: bool = True
+    divergence_factor: float = 10.0
+    divergence_run: int = 100
+
+
+@dataclass
+class EqualizerState:
+    """Widely-linear tap pair plus streaming bookkeeping (rx:81-101)."""
+
+    w: np.ndarray
+    g: np.ndarray
+    resid: np.ndarray = dc_field(default_factory=lambda: np.zeros(0, dtype=np.complex128))
+    frozen: bool = False
+    div_count: int = 0
+    symbols_done: int = 0
+
+    @classmethod
+    def initial(cls, n_taps: int = 4, spike_index: int = 1) -> "EqualizerState":
+        w = np.zeros(n_taps, dtype=np.complex128)
+        w[spike_index] = 1.0
+        return cls(w=w, g=np.zeros(n_taps, dtype=np.complex128))
+
+    @property
+    def diverged(self) -> bool:
+        return self.frozen
+
+
+@dataclass
+class GpuOptions:
+    """B200-only knobs (not in the reference): DDLMS block size B, frame size
+    F (symbols, global grid), fixpoint iteration cap, soft-output tolerance
+    of the block-skip certificate."""
+
+    ddlms_block: int = 256
+    ddlms_frame_symbols: int = 1 << 26
+    ddlms_max_iter: int = 64
+    ddlms_soft_tol: float = 1e-6
+
+
+@dataclass
+class RxPipelineConfig:
+    adc_rate_hz: float = 4e9
+    baud_hz: float = 1e9
+    tone_freq_hz: float = 0.516e9
+    kk_plan: BlockPlan = dc_field(default_factory=lambda: BlockPlan(1024, buffer_len=1 << 22))
+    static_plan: BlockPlan = dc_field(default_factory=lambda: BlockPlan(32768, buffer_len=1 << 22))
+    static_taps: FirFilter | None = None
+    carrier_removal: bool = True
+    carrier_segment_len: int = 1 << 16
+    mirror: bool = True
+    aa_edge: float = 0.01
+    ddlms: DdlmsConfig = dc_field(default_factory=DdlmsConfig)
+    constellation_order: int = 4
+    sync_symbols: int = 4096
+    sync_wait_samples: int = 1 << 16
+    gpu: GpuOptions = dc_field(default_factory=GpuOptions)
+
+    def __post_init__(self):
+        if self.sps_in != 4:
+            raise ParameterError("pipeline expects 4 samples per symbol at the ADC rate")
+        if self.static_taps is not None and len(self.static_taps) % 2 == 0:
+            raise ParameterError("static taps length must be odd")
+
+    @property
+    def sps_in(self) -> int:
+        return int(round(self.adc_rate_hz / self.baud_hz))
+
+    @property
+    def sps_out(self) -> int:
+        return self.sps_in // 2
+
+    @property
+    def constellation(self) -> ConstellationSpec:
+        return make_constellation(self.constellation_order)
+
+
+# ---------------------------------------------------------------------------
+# helpers
+# ---------------------------------------------------------------------------
+
+def _device():
+    torch = _torch()
+    if not torch.cuda.is_available():
+        raise RuntimeError("paper_2108_07001_b200 needs a CUDA device (no CPU fallback)")
+    return torch.device("cuda", torch.cuda.current_device())
+
+
+def _stream(dev=None) -> int:
+    torch = _torch()
+    return torch.cuda.current_stream(dev).cuda_stream
+
+
+def _ptr(t) -> int:
+    return t.data_ptr() if t is not None else 0
+
+
+def _tone_rotation(tone_hz: float, fs: float):
+    """Exact rational form p/q of tone/fs for the phase-continuous downshift
+    exp(-2 pi i (p g mod q)/q) (sigcore.py:297-298 computes the same phase
+    in float64; the integer form stays exact at any stream index)."""
+    if tone_hz == 0.0:
+        return 0, 0, None
+    fr = Fraction(tone_hz / fs).limit_denominator(1024)
+    if abs(float(fr) - tone_hz / fs) > 1e-12:
+        raise ParameterError("tone_freq_hz / adc_rate_hz must be a rational p/q with q <= 1024")
+    q = fr.denominator
+    p = fr.numerator % q
+    a = np.arange(q)
+    tab = np.exp(-2j * np.pi * a / q).astype(np.complex64)
+    return p, q, tab
+
+
+def _static_response(taps: FirFilter, plan: BlockPlan, fs_in: float, edge: float, aa_delay: int):
+    """Kept-bin indices and combined response (rx:401-411), float64 host."""
+    n = plan.fft_size
+    m = n // 2
+    kept = np.concatenate([np.arange(0, m // 2), np.arange(n - m // 2, n)])
+    f = np.fft.fftfreq(n, 1.0 / fs_in)[kept]
+    h = fir_frequency_response(taps, f)
+    h *= anti_alias_window(f, fs_in / 4.0, edge)
+    h *= np.exp(-2j * np.pi * f * aa_delay / fs_in)
+    return kept, h
+
+
+def _T_from_wg(w: np.ndarray, g: np.ndarray) -> np.ndarray:
+    """WL taps -> real 2x8 form (kk_ddlms.cu header)."""
+    T = np.zeros(16, dtype=np.float64)
+    T[0:8:2] = w.real + g.real
+    T[1:8:2] = w.imag - g.imag
+    T[8:16:2] = -w.imag - g.imag
+    T[9:16:2] = w.real - g.real
+    return T.astype(np.float32)
+
+
+def _wg_from_T(T: np.ndarray):
+    T = np.asarray(T, dtype=np.float64)
+    wr = (T[0:8:2] + T[9:16:2]) / 2
+    gr = (T[0:8:2] - T[9:16:2]) / 2
+    wi = (T[1:8:2] - T[8:16:2]) / 2
+    gi = -(T[1:8:2] + T[8:16:2]) / 2
+    return (wr + 1j * wi).astype(np.complex128), (gr + 1j * gi).astype(np.complex128)
+
+
+def _as_device_input(x, dev):
+    """(tensor on dev, dtype code, scale) for feed / kk_reconstruct inputs."""
+    torch = _torch()
+    if isinstance(x, AdcCodes):
+        c = x.codes
+        t = c if isinstance(c, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(c, dtype=np.int16))
+        return t.to(dev, non_blocking=True).contiguous(), _lib.KK_DTYPE_I16, float(x.half_lsb)
+    if isinstance(x, RealSignal):
+        x = x.samples
+    if isinstance(x, torch.Tensor):
+        if x.dtype == torch.int16:
+            raise ParameterError("int16 tensors must be wrapped in AdcCodes (scale needed)")
+        if x.dtype == torch.float32:
+            return x.to(dev).contiguous(), _lib.KK_DTYPE_F32, 1.0
+        return x.to(dev, torch.float64).contiguous(), _lib.KK_DTYPE_F64, 1.0
+    a = np.ascontiguousarray(np.asarray(x, dtype=np.float64))
+    if not np.all(np.isfinite(a)):
+        raise ParameterError("samples contains non-finite samples")
+    return torch.from_numpy(a).to(dev, non_blocking=True), _lib.KK_DTYPE_F64, 1.0
+
+
+class _DevStream:
+    """Append-only device buffer on a global index with prefix trimming."""
+
+    def __init__(self, dtype, dev, cap=1 << 16):
+        torch = _torch()
+        self.torch = torch
+        self.buf = torch.empty(cap, dtype=dtype, device=dev)
+        self.base = 0      # global index of buf[0]
+        self.end = 0       # global end index
+        self.keep = 0      # data before this global index may be dropped
+
+    def reserve(self, n_more: int):
+        """Make room for n_more items at the end; returns the tensor slice
+        (global [end, end + n_more)) to write into."""
+        need = self.end + n_more - self.base
+        if need > self.buf.shape[0]:
+            live0 = max(self.keep, self.base)
+            live = self.end - live0
+            cap = max(2 * (live + n_more), 1 << 16)
+            nb = self.torch.empty(cap, dtype=self.buf.dtype, device=self.buf.device)
+            if live > 0:
+                nb[:live].copy_(self.buf[live0 - self.base:self.end - self.base])
+            self.buf, self.base = nb, live0
+        o = self.end - self.base
+        return self.buf[o:o + n_more]
+
+    def commit(self, n: int):
+        self.end += n
+
+    def view(self, g0: int, g1: int):
+        return self.buf[g0 - self.base:g1 - self.base]
+
+    def ptr(self, g: int) -> int:
+        return self.buf.data_ptr() + (g - self.base) * self.buf.element_size()
+
+
+# ---------------------------------------------------------------------------
+# buffer management (rx:144-163)
+# ---------------------------------------------------------------------------
+
+def stream_buffers(adc_stream: RealSignal, plan: BlockPlan):
+    """Split a stream into processing buffers with the carried-overlap tail
+    (host bookkeeping; rx:144-163)."""
+    x = np.asarray(adc_stream.samples)
+    if len(x) < plan.hop:
+        raise ParameterError("stream shorter than one hop")
+    tail = np.zeros(plan.hop, dtype=np.float64)
+    for index, start in enumerate(range(0, len(x), plan.buffer_len)):
+        chunk = x[start:start + plan.buffer_len]
+        n_pad = plan.buffer_len - len(chunk)
+        if n_pad:
+            chunk = np.concatenate([chunk, np.zeros(n_pad)])
+        yield {"index": index, "samples": chunk, "tail": tail, "n_padding": n_pad}
+        tail = chunk[-plan.hop:].copy()
+
+
+# ---------------------------------------------------------------------------
+# KK reconstruction (rx:184-244) -> K1
+# ---------------------------------------------------------------------------
+
+def kk_reconstruct(current, plan: BlockPlan, state: dict | None = None, clamp_rel: float = 1e-12,
+                   device_output: bool = False):
+    """Blockwise KK field reconstruction on the GPU (rx:184-244).
+
+    Returns (ComplexSignal, new_state, diag) with the reference's state dict
+    keys {u_tail, a_hist, dead_hist}; output delayed by hop/2 like the
+    reference.  `current` may be a RealSignal, ndarray, AdcCodes or a CUDA
+    tensor; with device_output=True the field stays a complex64 CUDA tensor.
+    """
+    torch = _torch()
+    if plan.fft_size != KK_FFT:
+        raise ParameterError("the B200 KK kernel is built for kk_plan.fft_size == 1024")
+    fs = getattr(current, "sample_rate_hz", 4e9)
+    n = len(current.codes) if isinstance(current, AdcCodes) else len(
+        current.samples if isinstance(current, RealSignal) else current)
+    hop = plan.hop
+    if n % hop != 0 or n == 0:
+        raise ParameterError("chunk length must be a positive multiple of plan.hop")
+    dev = _device()
+    x, dt, sc = _as_device_input(current, dev)
+    n_hops = n // hop
+    if state is None:
+        state = {"u_tail": np.zeros(hop), "a_hist": np.zeros(hop // 2),
+                 "dead_hist": np.zeros(hop // 2, dtype=bool)}
+    su = torch.as_tensor(np.asarray(state["u_tail"], np.float32), device=dev)
+    sa = torch.as_tensor(np.asarray(state["a_hist"], np.float32), device=dev)
+    sd = torch.as_tensor(np.asarray(state["dead_hist"], np.uint8), device=dev)
+    nu = torch.empty(hop, dtype=torch.float32, device=dev)
+    na = torch.empty(hop // 2, dtype=torch.float32, device=dev)
+    nd = torch.empty(hop // 2, dtype=torch.uint8, device=dev)
+    out = torch.empty(n, dtype=torch.complex64, device=dev)
+    hs = torch.empty(n_hops, dtype=torch.complex64, device=dev)
+    hd = torch.empty(n_hops, dtype=torch.uint8, device=dev)
+    cl = torch.zeros(1, dtype=torch.int64, device=dev)
+    _lib.call("kk_reconstruct_pairs", dt, _ptr(x), sc, float(clamp_rel), n_hops, _ptr(su), _ptr(sa), _ptr(sd),
+              _ptr(nu), _ptr(na), _ptr(nd), _ptr(out), _ptr(hs), _ptr(hd), _ptr(cl), 0, 0, 0, None, 0,
+              _stream(dev))
+    new_state = {"u_tail": nu.cpu().numpy().astype(np.float64), "a_hist": na.cpu().numpy().astype(np.float64),
+                 "dead_hist": nd.cpu().numpy().astype(bool)}
+    diag = {"clamped": int(cl.item()), "zero_blocks": torch.nonzero(hd).flatten().cpu().tolist()}
+    field = out if device_output else out.cpu().numpy().astype(np.complex128)
+    return ComplexSignal(field, fs), new_state, diag
+
+
+def downshift_dc(field: ComplexSignal, tone_freq_hz: float, start_index: int = 0) -> ComplexSignal:
+    """Shift the payload band to DC (rx:247-257 -> sigcore.py:286-299),
+    phase-continuous via start_index.  In the pipeline this is fused into K1;
+    the standalone form evaluates the reference's float64 phase on the device."""
+    torch = _torch()
+    fs = field.sample_rate_hz
+    if tone_freq_hz == 0 and start_index == 0:
+        s = field.samples
+        return ComplexSignal(s.clone() if isinstance(s, torch.Tensor) else np.array(s, copy=True), fs)
+    if abs(tone_freq_hz) >= fs / 2:
+        raise ParameterError("|delta_f_hz| must be below Nyquist")
+    dev = _device()
+    s = field.samples
+    was_np = not isinstance(s, torch.Tensor)
+    x = torch.as_tensor(np.asarray(s, np.complex128)) if was_np else s
+    x = x.to(dev, torch.complex128)
+    n = torch.arange(start_index, start_index + x.shape[0], dtype=torch.float64, device=dev)
+    y = x * torch.exp(2j * np.pi * (-tone_freq_hz) * n / fs)
+    return ComplexSignal(y.cpu().numpy() if was_np else y, fs)
+
+
+# ---------------------------------------------------------------------------
+# static equaliser construction (rx:264-394): host setup, float64
+# ---------------------------------------------------------------------------
+
+def static_tap_coverage(link, n_taps: int = 203, rate_hz: float = 2e9) -> float:
+    """Tap span / group-delay spread (rx:291-300, including its units)."""
+    d_si = link.total_dispersion_ps_nm * 1e-6
+    lam = link.center_wavelength_nm * 1e-9
+    delay_span = abs(d_si) * lam ** 2 * rate_hz / 299792458.0
+    if delay_span == 0:
+        return np.inf
+    return (n_taps / rate_hz) / delay_span
+
+
+def compute_static_taps(link, n_taps: int = 203, rate_hz: float = 2e9) -> FirFilter:
+    """Windowed inverse-CD taps (rx:264-288)."""
+    if n_taps % 2 == 0:
+        raise ParameterError("n_taps must be odd")
+    a = cd_phase_coefficient(link.total_dispersion_ps_nm, 1.0, link.center_wavelength_nm)
+    m = 1 << max(12, int(np.ceil(np.log2(4 * n_taps))))
+    f = np.fft.fftfreq(m, 1.0 / rate_hz)
+    h = np.fft.fftshift(np.fft.ifft(np.exp(+1j * a * f * f)))
+    c, half = m // 2, n_taps // 2
+    taps = h[c - half:c + half + 1] * np.hanning(n_taps)
+    return FirFilter(taps / np.sum(taps), rate_hz)
+
+
+def _frontend_field_response(freqs_hz, tone_freq_hz, fe):
+    nu = np.abs(tone_freq_hz - freqs_hz)
+    r = np.exp(-0.5 * np.log(2.0) * (nu / fe.pd_bandwidth_hz) ** (2 * fe.pd_filter_order))
+    return r * np.exp(-0.5 * np.log(2.0) * (nu / fe.adc_analog_bandwidth_hz) ** (2 * fe.adc_aa_order))
+
+
+def design_receive_taps(link, tx, frontend=None, n_taps: int = 203, rate_hz: float | None = None,
+                        ridge: float = 1e-3) -> FirFilter:
+    """Least-squares ISI receive filter (rx:317-362)."""
+    rate = 2.0 * tx.baud_hz if rate_hz is None else rate_hz
+    sps = int(round(rate / tx.baud_hz))
+    if abs(rate - sps * tx.baud_hz) > 1e-6 or sps < 2:
+        raise ParameterError("rate_hz must be an integer multiple of the baud rate")
+    pulse = design_rrc(tx.rolloff, sps, tx.pulse_span_symbols).taps.real
+    lp = len(pulse)
+    nd = 1 << int(np.ceil(np.log2(4 * (lp + n_taps) + 64)))
+    f = np.fft.fftfreq(nd, 1.0 / rate)
+    resp = np.exp(-1j * cd_phase_coefficient(link.total_dispersion_ps_nm, 1.0, link.center_wavelength_nm) * f * f)
+    if frontend is not None:
+        resp = resp * _frontend_field_response(f, tx.tone_freq_hz, frontend)
+    q = np.fft.ifft(np.fft.fft(pulse, nd) * resp)
+    n_isi = (lp + n_taps) // (2 * sps) + 8
+    shift = 2 * n_isi * sps + n_taps
+    q = np.roll(q, shift)
+    t0 = (lp - 1) // 2 + (n_taps - 1) // 2 + shift
+    rows = np.arange(-n_isi, n_isi + 1)
+    a = q[t0 + sps * rows[:, None] - np.arange(n_taps)[None, :]]
+    b = np.zeros(len(rows), dtype=np.complex128)
+    b[n_isi] = 1.0
+    taps, *_ = np.linalg.lstsq(np.vstack([a, np.sqrt(ridge) * np.eye(n_taps)]),
+                               np.concatenate([b, np.zeros(n_taps)]), rcond=None)
+    return FirFilter(taps, rate)
+
+
+def refine_static_taps(input_2sps, training_symbols, n_taps: int = 203, rate_hz: float = 2e9,
+                       ridge: float = 1e-4):
+    """Data-aided LS refit of the receive taps (rx:365-394), host setup."""
+    from numpy.lib.stride_tricks import sliding_window_view
+
+    x = np.asarray(input_2sps, dtype=np.complex128)
+    d = np.asarray(training_symbols, dtype=np.complex128)
+    lag = (n_taps - 1) // 4
+    rows_all = sliding_window_view(x, n_taps)[::2]
+    n_rows = min(len(rows_all), len(d) - lag)
+    if n_rows < 4 * n_taps:
+        raise ParameterError("capture too short for a stable fit")
+    rows = rows_all[:n_rows, ::-1]
+    tgt = d[lag:lag + n_rows]
+    taps, *_ = np.linalg.lstsq(np.vstack([rows, np.sqrt(ridge) * np.eye(n_taps)]),
+                               np.concatenate([tgt, np.zeros(n_taps)]), rcond=None)
+    resid = rows @ taps - tgt
+    return FirFilter(taps, rate_hz), {"relative_mse": float(np.mean(np.abs(resid) ** 2) / np.mean(np.abs(tgt) ** 2))}
+
+
+# ---------------------------------------------------------------------------
+# fused static equalisation + 2:1 resampling (rx:414-453) -> K2
+# ---------------------------------------------------------------------------
+
+def _h_split(h: np.ndarray, dev):
+    torch = _torch()
+    he = torch.from_numpy(np.ascontiguousarray(h[0::2]).astype(np.complex64)).to(dev)
+    ho = torch.from_numpy(np.ascontiguousarray(h[1::2]).astype(np.complex64)).to(dev)
+    return he, ho
+
+
+def static_equalize_and_resample(field: ComplexSignal, static_taps: FirFilter, plan: BlockPlan,
+                                 tail=None, edge: float = 0.01, aa_delay: int | None = None,
+                                 device_output: bool = False):
+    """Static taps + 2:1 resampling in one FD pass per block (rx:414-453)."""
+    torch = _torch()
+    fs_in = field.sample_rate_hz
+    if abs(static_taps.nominal_rate_hz - fs_in / 2.0) > 1e-3:
+        raise ParameterError("static taps must be defined at half the input rate")
+    n, hop = plan.fft_size, plan.hop
+    if n != STATIC_FFT:
+        raise ParameterError("the B200 static kernel is built for static_plan.fft_size == 32768")
+    if aa_delay is None:
+        aa_delay = n // 4
+    if aa_delay % 2 != 0:
+        raise ParameterError("aa_delay must be even")
+    x = field.samples
+    nx = int(x.shape[0])
+    if nx % hop != 0 or nx == 0:
+        raise ParameterError("chunk length must be a positive multiple of plan.hop")
+    if tail is None:
+        tail = np.zeros(hop, dtype=np.complex128)
+    if len(tail) != hop:
+        raise ParameterError("tail length must equal plan.hop")
+    dev = _device()
+    _, h = _static_response(static_taps, plan, fs_in, edge, aa_delay)
+    he, ho = _h_split(h, dev)
+    tx = tail if isinstance(tail, torch.Tensor) else torch.from_numpy(np.asarray(tail, np.complex128))
+    xx = x if isinstance(x, torch.Tensor) else torch.from_numpy(np.asarray(x, np.complex128))
+    z = torch.cat([tx.to(dev, torch.complex64), xx.to(dev, torch.complex64)]).contiguous()
+    nb = nx // hop
+    out = torch.empty(nb * (hop // 2), dtype=torch.complex64, device=dev)
+    # global indexing: tail = [0, hop), x = [hop, hop + nx); blocks hb = 1..nb
+    _lib.call("kk_static_blocks", _ptr(z), 0, 1, nb, hop + nx, None, 0, 0, 0, 0, 0, None, 0,
+              _ptr(he), _ptr(ho), _ptr(out), _stream(dev))
+    new_tail = xx[-hop:]
+    if device_output:
+        return ComplexSignal(out, fs_in / 2.0), new_tail.to(dev)
+    return (ComplexSignal(out.cpu().numpy().astype(np.complex128), fs_in / 2.0),
+            np.asarray(new_tail.cpu().numpy() if isinstance(new_tail, torch.Tensor) else new_tail,
+                       dtype=np.complex128).copy())
+
+
+# ---------------------------------------------------------------------------
+# widely-linear DDLMS (rx:460-545) -> K4
+# ---------------------------------------------------------------------------
+
+def _seq_ddlms(x_dev, n_out: int, scale: float, cfg: DdlmsConfig, order: int, wg_dev, fz_dev, train_dev,
+               n_train: int, labels, soft, dec, dev):
+    tb = slicer_tables(order)
+    _lib.call("kk_ddlms_sequential", _ptr(x_dev), n_out, float(scale), int(cfg.n_taps), _ptr(train_dev),
+              int(n_train), _ptr(wg_dev), _ptr(fz_dev), order,
+              tb.pts_ri.ctypes.data, tb.grid.ctypes.data if tb.grid_m else None, tb.grid_m, tb.norm,
+              tb.max_radius, float(cfg.divergence_factor), int(cfg.divergence_run), float(cfg.mu),
+              int(bool(cfg.widely_linear)), _ptr(labels), _ptr(soft), _ptr(dec), _stream(dev))
+
+
+def ddlms_wl(x, cfg: DdlmsConfig, state: EqualizerState, training=None,
+             constellation: ConstellationSpec | None = None):
+    """Run the widely-linear DDLMS over a 2-sps chunk (rx:510-545).
+
+    Exact sequential recurrence on the GPU (kk_ddlms_sequential), so chunked
+    calls reproduce single-shot calls bit for bit, as the reference's
+    contract requires.  Mutates and returns `state`.
+    """
+    torch = _torch()
+    spec = constellation if constellation is not None else make_constellation(4)
+    dev = _device()
+    xin = x.cpu().numpy() if isinstance(x, torch.Tensor) else np.asarray(x, dtype=np.complex128)
+    x_cat = np.concatenate([state.resid, xin.astype(np.complex128)])
+    n_out = max(0, (len(x_cat) - cfg.n_taps) // 2 + 1)
+    dec = np.empty(n_out, dtype=np.complex128)
+    soft = np.empty(n_out, dtype=np.complex128)
+    if n_out:
+        train = np.zeros(0, np.complex128) if training is None else np.asarray(training, np.complex128)[:n_out]
+        xd = torch.from_numpy(x_cat.astype(np.complex64)).to(dev)
+        td = torch.from_numpy(train.astype(np.complex64)).to(dev) if len(train) else None
+        wg = torch.from_numpy(np.concatenate([state.w, state.g]).astype(np.complex64)).to(dev)
+        fz = torch.tensor([int(state.frozen), int(state.div_count)], dtype=torch.int32, device=dev)
+        lab = torch.empty(n_out, dtype=torch.uint8, device=dev)
+        sf = torch.empty(n_out, dtype=torch.complex64, device=dev)
+        _seq_ddlms(xd, n_out, 1.0, cfg, spec.order, wg, fz, td, len(train), lab, sf, None, dev)
+        l = lab.cpu().numpy()
+        soft = sf.cpu().numpy().astype(np.complex128)
+        dec = spec.points[np.minimum(l, spec.order - 1)].astype(np.complex128)
+        nt = min(len(train), n_out)
+        dec[:nt] = train[:nt]
+        wgh = wg.cpu().numpy().astype(np.complex128)
+        state.w, state.g = wgh[:cfg.n_taps].copy(), wgh[cfg.n_taps:].copy()
+        f = fz.cpu().numpy()
+        state.frozen, state.div_count = bool(f[0]), int(f[1])
+    state.resid = x_cat[2 * n_out:].copy()
+    state.symbols_done += n_out
+    return dec, soft, state
+
+
+def demap(symbols, spec: ConstellationSpec):
+    """Symbols -> bits with nearest-point fallback count (rx:548-567)."""
+    torch = _torch()
+    dev = _device()
+    s = symbols if isinstance(symbols, torch.Tensor) else torch.from_numpy(
+        np.ascontiguousarray(np.asarray(symbols, np.complex128)).astype(np.complex64))
+    s = s.to(dev, torch.complex64).contiguous()
+    n = int(s.shape[0])
+    k = spec.bits_per_symbol
+    if n == 0:
+        return np.zeros(0, dtype=np.uint8), 0
+    idx = torch.empty(n, dtype=torch.uint8, device=dev)
+    fb = torch.zeros(1, dtype=torch.int64, device=dev)
+    tb = slicer_tables(spec.order)
+    _lib.call("kk_demap", _ptr(s), n, spec.order, tb.pts_ri.ctypes.data, _ptr(idx), _ptr(fb), _stream(dev))
+    lab = torch.from_numpy(tb.point_label[:spec.order].astype(np.int64)).to(dev)[idx.long()]
+    shifts = torch.arange(k - 1, -1, -1, device=dev)
+    bits = ((lab[:, None] >> shifts[None, :]) & 1).to(torch.uint8).reshape(-1)
+    return bits.cpu().numpy(), int(fb.item())
+
+
+# ---------------------------------------------------------------------------
+# symbol sync (rx:574-601) -> K3
+# ---------------------------------------------------------------------------
+
+def _sync_device(head, ref, skip: int, dev):
+    """Returns (parity, k, ratio, rms) for device c64 head / ref."""
+    torch = _torch()
+    nh = int(head.shape[0])
+    nr = int(ref.shape[0]) if ref is not None else 0
+    sb = int(_lib.load().kk_symbol_sync_scratch_bytes(nh, nr))
+    scratch = torch.empty(sb, dtype=torch.uint8, device=dev)
+    res = (ctypes.c_double * 4)()
+    _lib.call("kk_symbol_sync", _ptr(head), nh, _ptr(ref), nr, int(skip), res, _ptr(scratch), sb, _stream(dev))
+    return int(res[0]), int(res[1]), float(res[2]), float(res[3])
+
+
+def symbol_sync(y_2sps, reference, min_peak_ratio: float = 4.0):
+    """Locate the reference symbols in a 2-sps stream (rx:574-601)."""
+    torch = _torch()
+    dev = _device()
+    y = y_2sps if isinstance(y_2sps, torch.Tensor) else torch.from_numpy(
+        np.asarray(y_2sps, np.complex128).astype(np.complex64))
+    r = reference if isinstance(reference, torch.Tensor) else torch.from_numpy(
+        np.asarray(reference, np.complex128).astype(np.complex64))
+    y = y.to(dev, torch.complex64).contiguous()
+    r = r.to(dev, torch.complex64).contiguous()
+    parity, k, ratio, _ = _sync_device(y, r, int(y.shape[0]), dev)
+    if parity < 0:
+        raise SyncError("stream shorter than the reference sequence")
+    if ratio < min_peak_ratio:
+        raise SyncError(f"no correlation peak (peak-to-rms {ratio:.2f})")
+    return 2 * k + parity, float(ratio)
+
+
+# ---------------------------------------------------------------------------
+# streaming pipeline (rx:608-824)
+# ---------------------------------------------------------------------------
+
+class RxPipeline:
+    """Streaming receiver on one GPU: feed ADC chunks of any size, collect
+    decisions (rx:608-824).  Output is bit-identical for any chunking."""
+
+    def __init__(self, cfg: RxPipelineConfig, reference_symbols=None, device=None):
+        torch = _torch()
+        _lib.load()
+        self.cfg = cfg
+        self.gpu = getattr(cfg, "gpu", None) or GpuOptions()
+        self.dev = torch.device(device) if device is not None else _device()
+        if cfg.kk_plan.fft_size != KK_FFT or cfg.static_plan.fft_size != STATIC_FFT:
+            raise ParameterError("the B200 kernels are built for kk_plan 1024 / static_plan 32768")
+        if cfg.carrier_segment_len % (2 * cfg.kk_plan.hop) or cfg.carrier_segment_len <= 0:
+            raise ParameterError("carrier_segment_len must be a positive multiple of 1024")
+        # only the sync + training prefix of the reference is ever read
+        # (rx:740, rx:745, rx:755); keep just that on host and device
+        self._ref_len = 0
+        self.reference = None
+        self._ref_dev = None
+        if reference_symbols is not None:
+            self._ref_len = len(reference_symbols)
+            n_keep = max(cfg.sync_symbols, cfg.ddlms.startup_symbols)
+            self.reference = np.asarray(reference_symbols[:n_keep], np.complex128)
+            self._ref_dev = torch.from_numpy(self.reference.astype(np.complex64)).to(self.dev)
+        taps = cfg.static_taps if cfg.static_taps is not None else FirFilter(np.array([1.0 + 0j]), cfg.adc_rate_hz / 2.0)
+        self._taps = taps
+        self._aa_delay = cfg.static_plan.fft_size // 4
+        self._kept, self._resp = _static_response(taps, cfg.static_plan, cfg.adc_rate_hz, cfg.aa_edge, self._aa_delay)
+        self._h_even, self._h_odd = _h_split(self._resp, self.dev)
+        p, q, tab = _tone_rotation(cfg.tone_freq_hz, cfg.adc_rate_hz)
+        self._rot_p, self._rot_q = p, q
+        self._rot_tab = torch.from_numpy(tab).to(self.dev) if tab is not None else None
+        self._spec = make_constellation(cfg.constellation_order)
+        self._tables = slicer_tables(cfg.constellation_order)
+
+        # raw FIFO (device), KK state (ping-pong), global counters
+        self._raw = None
+        self._raw_dt = None
+        self._raw_scale = 1.0
+        hop = cfg.kk_plan.hop
+        self._kk_state = [
+            (torch.zeros(hop, dtype=torch.float32, device=self.dev),
+             torch.zeros(hop // 2, dtype=torch.float32, device=self.dev),
+             torch.zeros(hop // 2, dtype=torch.uint8, device=self.dev)),
+            (torch.empty(hop, dtype=torch.float32, device=self.dev),
+             torch.empty(hop // 2, dtype=torch.float32, device=self.dev),
+             torch.empty(hop // 2, dtype=torch.uint8, device=self.dev)),
+        ]
+        self._kk_cur = 0
+        self._z = _DevStream(torch.complex64, self.dev)          # KK output, global sample index
+        self._hs = _DevStream(torch.complex64, self.dev)         # per-hop field sums, global hop index
+        self._hd = _DevStream(torch.uint8, self.dev)             # per-hop dead flags
+        self._seg = _DevStream(torch.complex64, self.dev)        # carrier means, global segment index
+        self._y2 = _DevStream(torch.complex64, self.dev)         # static output, global 2-sps index
+        self._clamped = torch.zeros(1, dtype=torch.int64, device=self.dev)
+        self._c_end = 0
+        self._hb_next = 0
+        self._flushed = False
+
+        # DDLMS
+        self._synced = False
+        self._drop = 0
+        self._eq_scale = None
+        self.sync_offset = None
+        self.sync_ratio = None
+        self._train_total = 0
+        self._sym_done = 0
+        st0 = EqualizerState.initial(cfg.ddlms.n_taps)
+        self._w, self._g = st0.w, st0.g
+        self._T = _T_from_wg(st0.w, st0.g) if cfg.ddlms.n_taps == 4 else None
+        self._frozen = False
+        self._div_count = 0
+        self._ws = None
+        self.ddlms_stats: list[dict] = []
+
+        self._out: list[tuple] = []
+        self._pending_diag: list[tuple] = []
+        self._diagnostics: list[dict] = []
+        self._events: list[tuple] = []
+        self._stage_acc = {"kk": 0.0, "carrier": 0.0, "downshift": 0.0, "static": 0.0, "ddlms": 0.0}
+        self.samples_in = 0
+        self._chunk_index = 0
+
+    # -- timing ---------------------------------------------------------------
+
+    def _ev(self):
+        torch = _torch()
+        e = torch.cuda.Event(enable_timing=True)
+        e.record(torch.cuda.current_stream(self.dev))
+        return e
+
+    @property
+    def stage_seconds(self) -> dict:
+        if self._events:
+            _torch().cuda.current_stream(self.dev).synchronize()
+            for name, a, b in self._events:
+                self._stage_acc[name] += a.elapsed_time(b) / 1e3
+            self._events = []
+        return dict(self._stage_acc)
+
+    @property
+    def diagnostics(self) -> list:
+        torch = _torch()
+        for chunk, h0, n, cl0, cl1, frozen in self._pending_diag:
+            dead = self._hd.view(h0, h0 + n)
+            zb = torch.nonzero(dead).flatten().cpu().tolist()
+            self._diagnostics.append({"chunk": chunk, "clamped": int(cl1.item() - cl0.item()),
+                                      "zero_blocks": zb, "diverged": frozen})
+        self._pending_diag = []
+        return self._diagnostics
+
+    # -- stages ------------------------------------------------------------------
+
+    def _append_raw(self, x, dt, scale):
+        torch = _torch()
+        if self._raw is None or self._raw.shape[0] == 0:
+            self._raw, self._raw_dt, self._raw_scale = x, dt, scale
+            return
+        if dt != self._raw_dt or scale != self._raw_scale:
+            def f64(t, d, s):
+                return t.to(torch.float64) * s if d == _lib.KK_DTYPE_I16 else t.to(torch.float64)
+            self._raw = torch.cat([f64(self._raw, self._raw_dt, self._raw_scale), f64(x, dt, scale)])
+            self._raw_dt, self._raw_scale = _lib.KK_DTYPE_F64, 1.0
+        else:
+            self._raw = torch.cat([self._raw, x])
+
+    def _run_kk(self, chunk, n_hops):
+        torch = _torch()
+        hop = self.cfg.kk_plan.hop
+        g0 = self._z.end
+        h0 = self._hs.end
+        out = self._z.reserve(n_hops * hop)
+        hs = self._hs.reserve(n_hops)
+        hd = self._hd.reserve(n_hops)
+        su, sa, sd = self._kk_state[self._kk_cur]
+        nu, na, nd = self._kk_state[1 - self._kk_cur]
+        clamped_before = self._clamped.clone()
+        rq = self._rot_q
+        _lib.call("kk_reconstruct_pairs", self._raw_dt, _ptr(chunk), float(self._raw_scale), 1e-12, n_hops,
+                  _ptr(su), _ptr(sa), _ptr(sd), _ptr(nu), _ptr(na), _ptr(nd), _ptr(out), _ptr(hs), _ptr(hd),
+                  _ptr(self._clamped), g0, self._rot_p, rq, _ptr(self._rot_tab), int(bool(self.cfg.mirror)),
+                  _stream(self.dev))
+        self._kk_cur = 1 - self._kk_cur
+        self._z.commit(n_hops * hop)
+        self._hs.commit(n_hops)
+        self._hd.commit(n_hops)
+        # diagnostics are materialised lazily (no host sync per feed)
+        self._pending_diag.append((self._chunk_index, h0, n_hops, clamped_before, self._clamped.clone(),
+                                   self._frozen))
+
+    def _run_carrier(self, flush):
+        cfg = self.cfg
+        z_end = self._z.end
+        if not cfg.carrier_removal:
+            self._c_end = z_end
+            return
+        seg = cfg.carrier_segment_len
+        n_done = self._seg.end
+        n_full = z_end // seg
+        n_tot = -(-z_end // seg) if flush else n_full
+        if n_tot > n_done:
+            n_new = n_tot - n_done
+            hps = seg // self.cfg.kk_plan.hop
+            out = self._seg.reserve(n_new)
+            last_len = z_end - (n_tot - 1) * seg if (flush and z_end % seg) else 0
+            hs_ptr = self._hs.ptr(n_done * hps)
+            _lib.call("kk_carrier_means", hs_ptr, n_new, hps, self._hs.end - n_done * hps, last_len, seg,
+                      _ptr(out), _stream(self.dev))
+            self._seg.commit(n_new)
+            self._hs.keep = n_tot * hps
+        self._c_end = z_end if flush else n_full * seg
+
+    def _run_static(self, flush):
+        hop = self.cfg.static_plan.hop
+        c_end = self._c_end
+        hb_end = -(-c_end // hop) if flush else c_end // hop
+        n = hb_end - self._hb_next
+        if n <= 0:
+            return
+        nout = hop // 2
+        out = self._y2.reserve(n * nout)
+        seg = self.cfg.carrier_segment_len
+        seg0 = self._seg.base
+        _lib.call("kk_static_blocks", _ptr(self._z.buf), self._z.base, self._hb_next, n, c_end,
+                  _ptr(self._seg.buf), seg0, seg, int(bool(self.cfg.carrier_removal)),
+                  self._rot_p, self._rot_q, _ptr(self._rot_tab), int(bool(self.cfg.mirror)),
+                  _ptr(self._h_even), _ptr(self._h_odd), _ptr(out), _stream(self.dev))
+        self._y2.commit(n * nout)
+        self._hb_next = hb_end
+        self._z.keep = max(0, (self._hb_next - 1) * hop)
+        self._seg.keep = max(0, ((self._hb_next - 1) * hop) // seg)
+
+    def _do_sync(self, flush):
+        cfg = self.cfg
+        need = cfg.sync_wait_samples + 2 * cfg.sync_symbols
+        avail = self._y2.end
+        if avail < need and not flush:
+            return False
+        nh = min(need, avail)
+        head = self._y2.view(0, nh)
+        skip = min(nh // 2, 1 << 13)
+        ref = self._ref_dev[:cfg.sync_symbols] if self._ref_dev is not None else None
+        parity, k, ratio, rms = _sync_device(head, ref, skip, self.dev)
+        self._eq_scale = 1.0 / rms if rms > 0 else 1.0
+        drop = 0
+        if self.reference is not None:
+            if parity < 0:
+                raise SyncError("stream shorter than the reference sequence")
+            if ratio < 4.0:
+                raise SyncError(f"no correlation peak (peak-to-rms {ratio:.2f})")
+            offset = 2 * k + parity
+            self.sync_offset, self.sync_ratio = offset, float(ratio)
+            drop = max(0, offset - 1)
+            self._train_total = min(cfg.ddlms.startup_symbols, self._ref_len)
+        self._drop = drop
+        self._synced = True
+        return True
+
+    def _solve_frame(self, k0, k1):
+        torch = _torch()
+        cfg = self.cfg
+        d = cfg.ddlms
+        nsym = k1 - k0
+        q0 = self._drop + 2 * k0
+        x_ptr = self._y2.ptr(q0)
+        n_train = int(max(0, min(nsym, self._train_total - k0)))
+        train_ptr = (self._ref_dev.data_ptr() + k0 * 8) if n_train > 0 else 0
+        labels = torch.empty(nsym, dtype=torch.uint8, device=self.dev)
+        soft = torch.empty(nsym, dtype=torch.complex64, device=self.dev)
+        tb = self._tables
+        use_solve = (d.widely_linear and d.n_taps == 4 and not self._frozen and self._div_count == 0)
+        stats = {"k0": k0, "nsym": nsym, "mode": "solve" if use_solve else "sequential"}
+        if use_solve:
+            B = int(self.gpu.ddlms_block)
+            wsb = int(_lib.load().kk_ddlms_workspace_bytes(nsym, B))
+            if self._ws is None or self._ws.numel() < wsb:
+                self._ws = torch.empty(wsb, dtype=torch.uint8, device=self.dev)
+            Tin = np.ascontiguousarray(self._T, dtype=np.float32)
+            Tout = np.zeros(16, dtype=np.float32)
+            st = np.zeros(6, dtype=np.int64)
+            _lib.call("kk_ddlms_solve", x_ptr, nsym, float(self._eq_scale), train_ptr, n_train,
+                      Tin.ctypes.data, tb.order, tb.pts_ri.ctypes.data,
+                      tb.grid.ctypes.data if tb.grid_m else None, tb.grid_m, tb.norm, tb.max_radius,
+                      float(d.divergence_factor), int(d.divergence_run), float(d.mu), B,
+                      int(self.gpu.ddlms_max_iter), float(self.gpu.ddlms_soft_tol), _ptr(labels), _ptr(soft),
+                      Tout.ctypes.data, _ptr(self._ws), wsb, st.ctypes.data, _stream(self.dev))
+            stats.update(iterations=int(st[0]), blocks_rerun=int(st[1]), fallback=int(st[2]),
+                         guard_exceed=int(st[3]), blocks=int(st[5]))
+            if st[2] == 1:
+                use_solve = False   # guard interaction: exact sequential re-run of the frame
+                stats["mode"] = "sequential(guard)"
+            else:
+                self._T = Tout
+                self._w, self._g = _wg_from_T(Tout)
+        if not use_solve:
+            if d.n_taps == 4 and self._T is not None:
+                self._w, self._g = _wg_from_T(self._T)
+            wg = torch.from_numpy(np.concatenate([self._w, self._g]).astype(np.complex64)).to(self.dev)
+            fz = torch.tensor([int(self._frozen), int(self._div_count)], dtype=torch.int32, device=self.dev)
+            xv = self._y2.view(q0, q0 + 2 * nsym + 2)
+            tv = self._ref_dev[k0:k0 + n_train] if n_train > 0 else None
+            _seq_ddlms(xv, nsym, self._eq_scale, d, tb.order, wg, fz, tv, n_train, labels, soft, None, self.dev)
+            wgh = wg.cpu().numpy().astype(np.complex128)
+            self._w, self._g = wgh[:d.n_taps], wgh[d.n_taps:]
+            f = fz.cpu().numpy()
+            self._frozen, self._div_count = bool(f[0]), int(f[1])
+            if d.n_taps == 4:
+                self._T = _T_from_wg(self._w, self._g)
+        self.ddlms_stats.append(stats)
+        self._out.append((labels, soft, k0, n_train))
+        self._sym_done = k1
+        self._y2.keep = self._drop + 2 * k1
+
+    def _run_ddlms(self, flush):
+        if not self._synced:
+            if not self._do_sync(flush):
+                return
+        F = int(self.gpu.ddlms_frame_symbols)
+        while True:
+            n_q = self._y2.end - self._drop
+            k0 = self._sym_done
+            k1 = (k0 // F + 1) * F
+            if n_q >= 2 * k1 + 2:
+                self._solve_frame(k0, k1)
+                continue
+            if flush:
+                total = (n_q - self.cfg.ddlms.n_taps) // 2 + 1 if n_q >= self.cfg.ddlms.n_taps else 0
+                if total > k0:
+                    self._solve_frame(k0, total)
+            break
+
+    # -- public API (rx:768-824) ---------------------------------------------
+
+    def feed(self, adc_chunk, flush: bool = False) -> None:
+        """Process a chunk of ADC samples (any length): ndarray (float64),
+        RealSignal, AdcCodes (exact int16 wire format) or a CUDA tensor."""
+        torch = _torch()
+        x, dt, sc = _as_device_input(adc_chunk, self.dev) if _len(adc_chunk) else (None, None, None)
+        n_new = _len(adc_chunk)
+        self.samples_in += n_new
+        if x is not None:
+            self._append_raw(x, dt, sc)
+        hop = self.cfg.kk_plan.hop
+        n_raw = 0 if self._raw is None else int(self._raw.shape[0])
+        if flush and n_raw % hop:
+            pad = hop - n_raw % hop
+            z = torch.zeros(pad, dtype=self._raw.dtype, device=self.dev)
+            self._raw = torch.cat([self._raw, z])
+            n_raw += pad
+        n_hops = n_raw // hop
+        if not flush:
+            n_hops = (n_hops // 2) * 2          # pairs on the global even-hop grid
+        if n_hops == 0 and not flush:
+            return
+        t0 = self._ev()
+        if n_hops:
+            chunk = self._raw[:n_hops * hop]
+            self._run_kk(chunk, n_hops)
+            self._raw = self._raw[n_hops * hop:]
+        t1 = self._ev()
+        self._run_carrier(flush)
+        t2 = self._ev()
+        self._run_static(flush)
+        t3 = self._ev()
+        self._run_ddlms(flush)
+        t4 = self._ev()
+        self._events += [("kk", t0, t1), ("carrier", t1, t2), ("static", t2, t3), ("ddlms", t3, t4)]
+        self._chunk_index += 1
+        if flush:
+            self._flushed = True
+
+    def drain_device(self):
+        """Device-resident outputs accumulated so far, then cleared:
+        (labels uint8 [n] point indices (255 = training symbol), soft
+        complex64 [n], list of (first symbol index, n_train) per frame)."""
+        torch = _torch()
+        if not self._out:
+            return (torch.zeros(0, dtype=torch.uint8, device=self.dev),
+                    torch.zeros(0, dtype=torch.complex64, device=self.dev), [])
+        labels = torch.cat([o[0] for o in self._out])
+        soft = torch.cat([o[1] for o in self._out])
+        meta = [(o[2], o[3]) for o in self._out]
+        self._out = []
+        return labels, soft, meta
+
+    def drain(self):
+        """Return (decisions, soft) accumulated so far as complex128 and clear
+        them (rx:803-809)."""
+        labels, soft, meta = self.drain_device()
+        if labels.numel() == 0:
+            return np.zeros(0, dtype=np.complex128), np.zeros(0, dtype=np.complex128)
+        lab = labels.cpu().numpy()
+        dec = self._spec.points[np.minimum(lab, self._spec.order - 1)].astype(np.complex128)
+        # frames are contiguous in symbol index; training sits at frame heads
+        first = meta[0][0]
+        for k0, n_train in meta:
+            if n_train > 0:
+                o = k0 - first
+                dec[o:o + n_train] = self.reference[k0:k0 + n_train]
+        return dec, soft.cpu().numpy().astype(np.complex128)
+
+    def finish(self):
+        """Flush (zero-padded) and return what has not been drained (rx:811-815)."""
+        self.feed(np.zeros(0), flush=True)
+        return self.drain()
+
+    @property
+    def diverged(self) -> bool:
+        return self._frozen
+
+    @property
+    def eq_scale(self):
+        return self._eq_scale
+
+    def write_diagnostics(self, path: str) -> None:
+        with open(path, "w") as f:
+            for rec in self.diagnostics:
+                f.write(json.dumps(rec, sort_keys=True) + "\n")
+
+
+def _len(x) -> int:
+    if isinstance(x, AdcCodes):
+        return len(x)
+    if isinstance(x, RealSignal):
+        return len(x.samples)
+    return int(x.shape[0]) if hasattr(x, "shape") else len(x)
