@@ -48,6 +48,8 @@ extern "C" {
 const char *kk_last_error(void);
 int kk_version(void);
 int kk_device_sync(void);
+/* number of kernels this library has launched (process-wide counter) */
+unsigned long long kk_launch_count(void);
 
 /*
  * K1 kk_fused -- replaces rxdsp.py:184-244 `kk_reconstruct` (+ the downshift

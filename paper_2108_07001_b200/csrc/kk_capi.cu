@@ -12,6 +12,7 @@
 namespace kk {
 
 static thread_local char g_err[512] = {0};
+static unsigned long long g_launches = 0;   // kernels launched through this library
 
 void clear_error() { g_err[0] = 0; }
 
@@ -27,6 +28,7 @@ int set_cuda_error(const char* where) {
 }
 
 int check_launch(const char* name) {
+    __atomic_fetch_add(&g_launches, 1ull, __ATOMIC_RELAXED);
     const cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) {
         std::snprintf(g_err, sizeof(g_err), "launch %s: %s", name, cudaGetErrorString(e));
@@ -72,6 +74,8 @@ const float2* twiddle_table_device() {
 extern "C" const char* kk_last_error(void) { return kk::g_err; }
 
 extern "C" int kk_version(void) { return KK_ABI_VERSION; }
+
+extern "C" unsigned long long kk_launch_count(void) { return __atomic_load_n(&kk::g_launches, __ATOMIC_RELAXED); }
 
 extern "C" int kk_device_sync(void) {
     kk::clear_error();

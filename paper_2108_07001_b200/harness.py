@@ -70,14 +70,16 @@ def measure_point(dec, soft, bits, syms, cfg) -> dict:
     return point
 
 
-def device_ber(labels, ref_idx, order: int, head: int, stop: int, tile_symbols: int = 0, seam_guard: int = 128):
+def device_ber(labels, ref_idx, order: int, head: int, stop: int, tile_symbols: int = 0, seam_guard: int = 128,
+               index0: int = 0):
     """BER of decided indices [head, stop) against transmitted indices on the
     GPU (kk_bit_errors), excluding `seam_guard` symbols before every tile
     seam of a tiled capture.  Returns device
-    tensors (errors, symbols)."""
+    tensors (errors, symbols).  index0: absolute symbol index of labels[0]
+    (sets the seam phase)."""
     lab = labels[head:stop]
     ref = ref_idx[head:stop]
     if tile_symbols > 0:
         return count_bit_errors(lab, ref, order, exclude_period=tile_symbols, exclude_len=seam_guard,
-                                exclude_phase=head)[:2]
+                                exclude_phase=index0 + head)[:2]
     return count_bit_errors(lab, ref, order)[:2]

@@ -195,8 +195,17 @@ def _tone_rotation(tone_hz: float, fs: float):
     return p, q, tab
 
 
+_RESP_CACHE: dict = {}
+
+
 def _static_response(taps: FirFilter, plan: BlockPlan, fs_in: float, edge: float, aa_delay: int):
-    """Kept-bin indices and combined response (rx:401-411), float64 host."""
+    """Kept-bin indices and combined response (rx:401-411), float64 host
+    (memoised per taps/plan: it is a per-link constant)."""
+    key = (np.asarray(taps.taps).tobytes(), float(taps.nominal_rate_hz), plan.fft_size, float(fs_in), float(edge),
+           int(aa_delay))
+    hit = _RESP_CACHE.get(key)
+    if hit is not None:
+        return hit[0].copy(), hit[1].copy()
     n = plan.fft_size
     m = n // 2
     kept = np.concatenate([np.arange(0, m // 2), np.arange(n - m // 2, n)])
@@ -204,6 +213,9 @@ def _static_response(taps: FirFilter, plan: BlockPlan, fs_in: float, edge: float
     h = fir_frequency_response(taps, f)
     h *= anti_alias_window(f, fs_in / 4.0, edge)
     h *= np.exp(-2j * np.pi * f * aa_delay / fs_in)
+    if len(_RESP_CACHE) > 16:
+        _RESP_CACHE.clear()
+    _RESP_CACHE[key] = (kept.copy(), h.copy())
     return kept, h
 
 
@@ -978,6 +990,13 @@ class RxPipeline:
                 o = k0 - first
                 dec[o:o + n_train] = self.reference[k0:k0 + n_train]
         return dec, soft.cpu().numpy().astype(np.complex128)
+
+    def release_buffers(self) -> None:
+        """Free the device stream buffers of a finished pipeline (outputs
+        already drained); timing events and statistics stay valid."""
+        self._z = self._hs = self._hd = self._seg = self._y2 = None
+        self._raw = None
+        self._ws = None
 
     def finish(self):
         """Flush (zero-padded) and return what has not been drained (rx:811-815)."""
