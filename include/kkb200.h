@@ -120,7 +120,8 @@ int kk_ddlms_sequential(const void *x, int64_t n_out, float scale, int n_taps, c
  * taps in real 2x8 form.  stats_host[6] = {iterations, blocks re-run,
  * fallback (0 none, 1 guard exceeded -> caller re-runs sequentially,
  * 2 not converged -> chained), guard exceedances, changed decisions in the
- * last iteration, blocks}.
+ * last iteration, blocks, then for iterations 1..16: (changed, re-run)}:
+ * the buffer must hold 38 int64.
  */
 size_t kk_ddlms_workspace_bytes(int64_t nsym, int block);
 int kk_ddlms_solve(const void *x, int64_t nsym, float scale, const void *train, int64_t n_train,

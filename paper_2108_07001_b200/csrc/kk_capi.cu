@@ -52,13 +52,16 @@ const float2* twiddle_table_device() {
     std::call_once(g_tw_once[dev], [dev]() {
         std::vector<float2> h(kTwEntries);
         const double two_pi = 6.283185307179586476925286766559;
-        for (int i = 0; i < kTwHi; ++i) {   // W_32768^(64 i)
-            const double a = -two_pi * (64.0 * i) / kTwN;
-            h[i] = make_float2(static_cast<float>(std::cos(a)), static_cast<float>(std::sin(a)));
-        }
-        for (int i = 0; i < kTwLo; ++i) {   // W_32768^i
-            const double a = -two_pi * i / kTwN;
-            h[kTwHi + i] = make_float2(static_cast<float>(std::cos(a)), static_cast<float>(std::sin(a)));
+        for (int M = 256; M <= 32768; M *= 2) {
+            const int o = tw_offset(M);
+            for (int i = 0; i < 32; ++i) {          // L_M[i] = W_M^i
+                const double a = -two_pi * i / M;
+                h[o + i] = make_float2(static_cast<float>(std::cos(a)), static_cast<float>(std::sin(a)));
+            }
+            for (int i = 0; i < M / 32; ++i) {      // H_M[i] = W_M^(32 i)
+                const double a = -two_pi * (32.0 * i) / M;
+                h[o + 32 + i] = make_float2(static_cast<float>(std::cos(a)), static_cast<float>(std::sin(a)));
+            }
         }
         float2* d = nullptr;
         if (cudaMalloc(&d, kTwEntries * sizeof(float2)) == cudaSuccess &&

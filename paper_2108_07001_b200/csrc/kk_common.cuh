@@ -18,11 +18,6 @@
 
 namespace kk {
 
-constexpr int kTwLogN = 15;               // W_32768 master table
-constexpr int kTwN = 1 << kTwLogN;
-constexpr int kTwLo = 64;
-constexpr int kTwHi = kTwN / kTwLo;       // 512
-constexpr int kTwEntries = kTwHi + kTwLo; // 576 float2
 
 __device__ __forceinline__ float2 cadd(float2 a, float2 b) { return make_float2(a.x + b.x, a.y + b.y); }
 __device__ __forceinline__ float2 csub(float2 a, float2 b) { return make_float2(a.x - b.x, a.y - b.y); }
@@ -36,6 +31,16 @@ __device__ __forceinline__ float2 cconj(float2 a) { return make_float2(a.x, -a.y
 __device__ __forceinline__ float2 cscale(float2 a, float s) { return make_float2(a.x * s, a.y * s); }
 __device__ __forceinline__ float2 mul_mj(float2 a) { return make_float2(a.y, -a.x); }   // * (-j)
 __device__ __forceinline__ float2 mul_pj(float2 a) { return make_float2(-a.y, a.x); }   // * (+j)
+
+// x mod d for 0 <= x < 2^25 via a float reciprocal (+-1 quotient fix-up)
+__device__ __forceinline__ unsigned fmod_u(unsigned x, unsigned d, float inv_d, unsigned* quot = nullptr) {
+    unsigned q = __float2uint_rz(__uint2float_rn(x) * inv_d);
+    int r = static_cast<int>(x) - static_cast<int>(q * d);
+    if (r < 0) { r += d; --q; }
+    if (r >= static_cast<int>(d)) { r -= d; ++q; }
+    if (quot) *quot = q;
+    return static_cast<unsigned>(r);
+}
 
 // cos/sin(2*pi*t/16) for t in [0,8)
 __host__ __device__ constexpr float c16(int t) {
@@ -115,21 +120,50 @@ __device__ __forceinline__ void dft_reg(float2 (&v)[R]) {
 }
 
 // ---------------------------------------------------------------------------
-// twiddles: W_32768^t = hi[t >> 6] * lo[t & 63]; table lives in smem
+// twiddles: for every power of two M in [256, 32768] a two-level table
+//   W_M^k = H_M[k >> 5] * L_M[k & 31],  L_M[i] = W_M^i, H_M[i] = W_M^(32 i)
+// so that 32 consecutive k (the lanes of a Stockham pass) read 32
+// consecutive L entries (conflict-free) and one or two broadcast H entries.
+// Packed [L_256 H_256 | L_512 H_512 | ... | L_32768 H_32768], built once per
+// device on the host in float64 (kk_capi.cu) and staged into smem.
 // ---------------------------------------------------------------------------
+__host__ __device__ constexpr int ilog2c(int m) { return m <= 1 ? 0 : 1 + ilog2c(m >> 1); }
+__host__ __device__ constexpr int tw_offset(int M) { return 32 * (ilog2c(M) - 8) + M / 32 - 8; }
+constexpr int kTwEntries = tw_offset(65536);   // 2296 float2 = 18.4 KB
+
 struct Twiddle {
-    const float2* hi;  // [512]
-    const float2* lo;  // [64]
-    // W_N^t (forward sign), N a power of two <= 32768, 0 <= t < N
-    template <int N>
-    __device__ __forceinline__ float2 w(int t) const {
-        const int u = t * (kTwN / N);
-        return cmul(hi[u >> 6], lo[u & 63]);
+    const float2* t;
+    // W_M^k (forward sign), 0 <= k < M
+    template <int M>
+    __device__ __forceinline__ float2 w(int k) const {
+        static_assert(M >= 256 && M <= 32768, "twiddle size");
+        constexpr int o = tw_offset(M);
+        return cmul(t[o + 32 + (k >> 5)], t[o + (k & 31)]);
     }
 };
 
 __device__ __forceinline__ void load_twiddles(float2* sm, const float2* __restrict__ g, int tid, int nt) {
     for (int i = tid; i < kTwEntries; i += nt) sm[i] = g[i];
+}
+
+// w[r] = w1^r for r in [0, R), by a power tree of depth <= 4 (accuracy ~1e-7)
+template <int R>
+__device__ __forceinline__ void twiddle_powers(float2 w1, float2 (&w)[R]) {
+    w[0] = make_float2(1.f, 0.f);
+    if constexpr (R > 1) w[1] = w1;
+    if constexpr (R > 2) w[2] = cmul(w1, w1);
+    if constexpr (R > 3) w[3] = cmul(w[2], w1);
+    if constexpr (R > 4) {
+        w[4] = cmul(w[2], w[2]);
+        w[5] = cmul(w[4], w1);
+        w[6] = cmul(w[4], w[2]);
+        w[7] = cmul(w[4], w[3]);
+    }
+    if constexpr (R > 8) {
+        w[8] = cmul(w[4], w[4]);
+#pragma unroll
+        for (int r = 1; r < 8; ++r) w[8 + r] = cmul(w[8], w[r]);
+    }
 }
 
 // ---------------------------------------------------------------------------
@@ -156,38 +190,70 @@ struct StorePlanes {
 
 // One in-place Stockham (autosort, DIT-twiddle) pass of an N-point FFT with
 // radix R, run by NT threads; NS = product of the radices of earlier passes.
-// Butterfly j reads x[j + r*N/R], applies W_N^{r*(j%NS)*(N/(NS*R))}, does an
+// Butterfly j reads x[j + r*N/R], applies W_{NS*R}^{r*(j%NS)}, does an
 // R-point DFT and writes x[(j/NS)*NS*R + j%NS + r*NS].
-// SYNC_IN: barrier between the read and write phases (needed whenever the
-// loader reads the same buffer the storer writes).
-template <int N, int R, int NS, int NT, bool INV, bool SYNC_IN, class Load, class Store>
-__device__ __forceinline__ void stockham_pass(int tid, const Twiddle& tw, const Load& load, const Store& store) {
-    constexpr int NB = N / R;
+template <int N, int R, int NT>
+struct PassShape {
+    static constexpr int NB = N / R;
     static_assert(NB % NT == 0, "butterflies must split evenly over threads");
-    constexpr int BPT = NB / NT;
-    float2 v[BPT][R];
+    static constexpr int BPT = NB / NT;
+};
+
+template <int N, int R, int NT, class Load>
+__device__ __forceinline__ void stockham_load(int tid, const Load& load, float2 (&v)[PassShape<N, R, NT>::BPT][R]) {
+    constexpr int NB = PassShape<N, R, NT>::NB;
 #pragma unroll
-    for (int q = 0; q < BPT; ++q) {
+    for (int q = 0; q < PassShape<N, R, NT>::BPT; ++q) {
         const int j = tid + q * NT;
 #pragma unroll
         for (int r = 0; r < R; ++r) v[q][r] = load(j + r * NB);
     }
-    if constexpr (SYNC_IN) __syncthreads();
+}
+
+template <int N, int R, int NS, int NT, bool INV, int NBF = PassShape<N, R, NT>::BPT, class Store>
+__device__ __forceinline__ void stockham_compute_store(int tid, const Twiddle& tw, float2 (&v)[NBF][R],
+                                                       const Store& store) {
 #pragma unroll
-    for (int q = 0; q < BPT; ++q) {
+    for (int q = 0; q < NBF; ++q) {
         const int j = tid + q * NT;
         if constexpr (NS > 1) {
-            const int t = (j % NS) * (N / (NS * R));
+            // w_r = w1^r by a running product (2 live registers; error <= R ulp)
+            const float2 w1 = tw.template w<NS * R>(j % NS);
+            float2 wr = w1;
 #pragma unroll
             for (int r = 1; r < R; ++r) {
-                const float2 w = tw.template w<N>(r * t);
-                v[q][r] = INV ? cmulc(v[q][r], w) : cmul(v[q][r], w);
+                v[q][r] = INV ? cmulc(v[q][r], wr) : cmul(v[q][r], wr);
+                if (r + 1 < R) wr = cmul(wr, w1);
             }
         }
         dft_reg<R, INV>(v[q]);
         const int d0 = (j / NS) * NS * R + (j % NS);
 #pragma unroll
         for (int r = 0; r < R; ++r) store(d0 + r * NS, v[q][r]);
+    }
+}
+
+// SYNC_IN: barrier between the read and write phases (needed whenever the
+// loader reads the same buffer the storer writes).
+// SYNC_IN == false means the pass is out of place (loader and storer touch
+// different memory): butterflies then stream one at a time (R live values).
+template <int N, int R, int NS, int NT, bool INV, bool SYNC_IN, class Load, class Store>
+__device__ __forceinline__ void stockham_pass(int tid, const Twiddle& tw, const Load& load, const Store& store) {
+    if constexpr (SYNC_IN) {
+        float2 v[PassShape<N, R, NT>::BPT][R];
+        stockham_load<N, R, NT>(tid, load, v);
+        __syncthreads();
+        stockham_compute_store<N, R, NS, NT, INV>(tid, tw, v, store);
+    } else {
+        constexpr int NB = PassShape<N, R, NT>::NB;
+#pragma unroll 1
+        for (int q = 0; q < PassShape<N, R, NT>::BPT; ++q) {
+            float2 v[1][R];
+            const int j = tid + q * NT;
+#pragma unroll
+            for (int r = 0; r < R; ++r) v[0][r] = load(j + r * NB);
+            stockham_compute_store<N, R, NS, NT, INV, 1>(tid + q * NT, tw, v, store);
+        }
     }
 }
 

@@ -207,6 +207,7 @@ struct RunOut {
     float* margin;    // [nb]
     float* Tend;      // [16] end taps of the last block
     int* over;        // [nb] guard exceedances in the block's latest run
+    unsigned long long* hash;  // [nb] hash of the block's latest label sequence
     unsigned long long* counters;  // [0] changed decisions, [1] blocks re-run
 };
 
@@ -327,80 +328,310 @@ __global__ void fill_T_kernel(float* __restrict__ T, int64_t b0, int64_t b1, con
     if (i < n) T[b0 * 16 + i] = src[i & 15];
 }
 
-// fold groups of G consecutive maps:  (P, Q) <- (P P_c, Q P_c + Q_c)
-__global__ void scan_fold_kernel(const float* __restrict__ Pc, const float* __restrict__ Qc, int64_t n_child,
-                                 int G, float* __restrict__ Pg, float* __restrict__ Qg, int64_t n_grp, int with_p) {
-    const int64_t g = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (g >= n_grp) return;
-    float P[64], Q[16];
+// Block-parallel DDLMS pass, one thread per block of B symbols, 128 blocks per
+// CTA.  Each thread's recurrence is sequential, so the inputs are staged per
+// chunk of C symbols through shared memory (a warp loads each of its threads'
+// contiguous 2C+2-sample segments coalesced) and the outputs (labels, soft)
+// are written back the same way.  WITH_P additionally accumulates the
+// decision-independent block map P_b and max|X|^2 (fused first pass).
+constexpr size_t block_kernel_smem(int C) {
+    return 2 * size_t(128) * ((2 * C + 2) | 1) * 8 + size_t(128) * (C | 1) * 8 + 128 * 4;
+}
+
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
+    const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+
+// Block-parallel DDLMS pass, one thread per block of B symbols, 128 blocks per
+// CTA.  Each thread's recurrence is sequential, so its input is staged per
+// chunk of C symbols through shared memory with cp.async (a warp copies each
+// of its threads' contiguous 2C+2-sample segments, coalesced; double
+// buffered so chunk c+1 streams in while chunk c is computed) and the soft
+// outputs are written back the same way.  Decision changes are detected per
+// block with a 64-bit hash of its label sequence (no label re-read).  WITH_P
+// additionally accumulates the decision-independent block map P_b and
+// max|X|^2 (fused first pass).
+template <int C, bool WITH_P>
+__global__ void __launch_bounds__(128)
+ddlms_block_kernel(SolveArgs a, Slicer sl, const float* __restrict__ Tstart, float* __restrict__ Pb,
+                   float* __restrict__ maxx2, RunOut o, int64_t b_lo, int64_t b_hi, int use_skip, float soft_tol) {
+    constexpr int NT = 128;
+    constexpr int SEG = 2 * C + 2;
+    constexpr int SEGP = SEG | 1;      // odd float2 stride: conflict-free per-thread reads
+    constexpr int CS = C | 1;
+    static_assert(C == 8, "labels are packed 8 per 64-bit store");
+    extern __shared__ __align__(16) unsigned char dsm[];
+    float2* xs = reinterpret_cast<float2*>(dsm);                  // [2][NT * SEGP]
+    float2* ss = xs + 2 * NT * SEGP;                               // [NT * CS]
+    int* run_s = reinterpret_cast<int*>(ss + NT * CS);             // [NT]
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int64_t bcta = b_lo + int64_t(blockIdx.x) * NT;
+    const int64_t b = bcta + tid;
+    bool run = b < b_hi;
+    float T[16];
+    if (run) {
 #pragma unroll
-    for (int i = 0; i < 64; ++i) P[i] = (i % 9 == 0) ? 1.f : 0.f;
+        for (int i = 0; i < 16; ++i) T[i] = Tstart[b * 16 + i];
+        if (use_skip && !WITH_P) {
+            float d2 = 0.f;
 #pragma unroll
-    for (int i = 0; i < 16; ++i) Q[i] = 0.f;
-    const int64_t c0 = g * G, c1 = min(c0 + G, n_child);
-    for (int64_t c = c0; c < c1; ++c) {
-        const float* M = Pc + c * 64;
-        float nQ[16];
-#pragma unroll
-        for (int r = 0; r < 2; ++r)
-#pragma unroll
-            for (int j = 0; j < 8; ++j) {
-                float s = Qc[c * 16 + r * 8 + j];
-#pragma unroll
-                for (int i = 0; i < 8; ++i) s = fmaf(Q[r * 8 + i], __ldg(M + i * 8 + j), s);
-                nQ[r * 8 + j] = s;
+            for (int i = 0; i < 16; ++i) {
+                const float d = T[i] - o.Tused[b * 16 + i];
+                d2 = fmaf(d, d, d2);
             }
-#pragma unroll
-        for (int i = 0; i < 16; ++i) Q[i] = nQ[i];
-        if (with_p) {
-            float nP[64];
-#pragma unroll
-            for (int r = 0; r < 8; ++r)
-#pragma unroll
-                for (int j = 0; j < 8; ++j) {
-                    float s = 0.f;
-#pragma unroll
-                    for (int i = 0; i < 8; ++i) s = fmaf(P[r * 8 + i], __ldg(M + i * 8 + j), s);
-                    nP[r * 8 + j] = s;
-                }
-#pragma unroll
-            for (int i = 0; i < 64; ++i) P[i] = nP[i];
+            const float bound = sqrtf(d2 * maxx2[b]);
+            run = !(bound < fminf(o.margin[b], soft_tol)) || (a.mu * maxx2[b] > 1.0f);
         }
     }
+    run_s[tid] = run ? 1 : 0;
+    if (!__syncthreads_or(run ? 1 : 0)) return;
+    const int64_t k0 = b * a.B;
+    const int64_t k1 = run ? min(k0 + a.B, a.nsym) : k0;
+    const int nchunk = (a.B + C - 1) / C;
+
+    auto prefetch = [&](int c) {
+        float2* dst = xs + (c & 1) * NT * SEGP;
+        for (int tt = 0; tt < 32; ++tt) {
+            const int t = warp * 32 + tt;
+            if (!run_s[t]) continue;
+            const int64_t bt = bcta + t;
+            const int64_t kb = bt * a.B + int64_t(c) * C;
+            const int64_t ke = min((bt + 1) * a.B, a.nsym);
+            if (kb >= ke) continue;
+            const int n = 2 * static_cast<int>(min(static_cast<int64_t>(C), ke - kb)) + 2;
+            const float2* src = a.x + 2 * kb;
+            if (lane < n) cp_async8(dst + t * SEGP + lane, src + lane);
+            if (lane + 32 < n) cp_async8(dst + t * SEGP + lane + 32, src + lane + 32);
+        }
+        cp_async_commit();
+    };
+
+    float Q[16];
 #pragma unroll
-    for (int i = 0; i < 16; ++i) Qg[g * 16 + i] = Q[i];
-    if (with_p) {
+    for (int i = 0; i < 16; ++i) Q[i] = 0.f;
+    float P[WITH_P ? 64 : 1];
+    if constexpr (WITH_P) {
 #pragma unroll
-        for (int i = 0; i < 64; ++i) Pg[g * 64 + i] = P[i];
+        for (int i = 0; i < 64; ++i) P[i] = (i % 9 == 0) ? 1.f : 0.f;
+    }
+    const float tm = 2.0f * a.mu;
+    float mg = 3.0e38f, mx = 0.f;
+    int over = 0;
+    unsigned long long hsh = 1469598103934665603ull;
+
+    prefetch(0);
+    for (int c = 0; c < nchunk; ++c) {
+        if (c + 1 < nchunk) {
+            prefetch(c + 1);
+            cp_async_wait<1>();
+        } else {
+            cp_async_wait<0>();
+        }
+        __syncthreads();
+        // ---- sequential recurrence over this chunk ----
+        const int64_t kc = k0 + int64_t(c) * C;
+        if (run && kc < k1) {
+            const float2* xv = xs + (c & 1) * NT * SEGP + tid * SEGP;
+            unsigned long long packed = 0;
+            const int nk = static_cast<int>(min(static_cast<int64_t>(C), k1 - kc));
+            for (int i = 0; i < nk; ++i) {
+                const int64_t k = kc + i;
+                float X[8];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const float2 v = xv[2 * i + u];
+                    X[2 * u] = v.x * a.scale;
+                    X[2 * u + 1] = v.y * a.scale;
+                }
+                // y = T X and Q X with split accumulators (short dependency chain)
+                float ya = 0.f, yb = 0.f, za = 0.f, zb = 0.f, qa = 0.f, qb = 0.f, wa = 0.f, wb = 0.f;
+#pragma unroll
+                for (int j = 0; j < 8; j += 2) {
+                    ya = fmaf(T[j], X[j], ya);
+                    yb = fmaf(T[j + 1], X[j + 1], yb);
+                    za = fmaf(T[8 + j], X[j], za);
+                    zb = fmaf(T[9 + j], X[j + 1], zb);
+                    qa = fmaf(Q[j], X[j], qa);
+                    qb = fmaf(Q[j + 1], X[j + 1], qb);
+                    wa = fmaf(Q[8 + j], X[j], wa);
+                    wb = fmaf(Q[9 + j], X[j + 1], wb);
+                }
+                const float yr = ya + yb, yi = za + zb, qr = qa + qb, qi = wa + wb;
+                float dr, di;
+                int lab;
+                if (k < a.n_train) {
+                    const float2 t = __ldg(a.train + k);
+                    dr = t.x; di = t.y;
+                    lab = 255;
+                } else {
+                    float m;
+                    lab = slice(sl, yr, yi, m);
+                    mg = fminf(mg, m);
+                    dr = sl.pts[lab].x; di = sl.pts[lab].y;
+                }
+                const float ay = sqrtf(yr * yr + yi * yi);
+                over += (ay > sl.thr) ? 1 : 0;
+                mg = fminf(mg, fabsf(ay - sl.thr));
+                const float er = tm * (dr - yr), ei = tm * (di - yi);
+                const float fr = tm * (dr - qr), fi = tm * (di - qi);
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
+                    T[j] = fmaf(er, X[j], T[j]);
+                    T[8 + j] = fmaf(ei, X[j], T[8 + j]);
+                    Q[j] = fmaf(fr, X[j], Q[j]);
+                    Q[8 + j] = fmaf(fi, X[j], Q[8 + j]);
+                }
+                if constexpr (WITH_P) {
+                    float n2 = 0.f;
+#pragma unroll
+                    for (int j = 0; j < 8; ++j) n2 = fmaf(X[j], X[j], n2);
+                    mx = fmaxf(mx, n2);
+                    float v[8];
+#pragma unroll
+                    for (int r = 0; r < 8; ++r) {
+                        float sacc = 0.f;
+#pragma unroll
+                        for (int j = 0; j < 8; ++j) sacc = fmaf(P[r * 8 + j], X[j], sacc);
+                        v[r] = sacc * tm;
+                    }
+#pragma unroll
+                    for (int r = 0; r < 8; ++r)
+#pragma unroll
+                        for (int j = 0; j < 8; ++j) P[r * 8 + j] = fmaf(-v[r], X[j], P[r * 8 + j]);
+                }
+                hsh = (hsh ^ static_cast<unsigned long long>(lab)) * 1099511628211ull;
+                packed |= static_cast<unsigned long long>(lab & 0xff) << (8 * i);
+                ss[tid * CS + i] = make_float2(yr, yi);
+            }
+            // labels: C == 8 symbols -> one 8-byte store (chunk-aligned)
+            if (nk == C) *reinterpret_cast<unsigned long long*>(o.labels + kc) = packed;
+            else
+                for (int i = 0; i < nk; ++i) o.labels[kc + i] = static_cast<uint8_t>(packed >> (8 * i));
+        }
+        __syncthreads();
+        // ---- soft outputs, coalesced per thread segment ----
+        for (int tt = 0; tt < 32; ++tt) {
+            const int t = warp * 32 + tt;
+            if (!run_s[t]) continue;
+            const int64_t bt = bcta + t;
+            const int64_t kb = bt * a.B + int64_t(c) * C;
+            const int64_t ke = min((bt + 1) * a.B, a.nsym);
+            if (kb >= ke) continue;
+            const int cnt = static_cast<int>(min(static_cast<int64_t>(C), ke - kb));
+            if (lane < cnt) o.soft[kb + lane] = ss[t * CS + lane];
+        }
+    }
+    unsigned long long changed = 0;
+    if (run) {
+        changed = (o.hash[b] != hsh) ? 1ull : 0ull;
+        o.hash[b] = hsh;
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+            o.Q[b * 16 + i] = Q[i];
+            o.Tused[b * 16 + i] = Tstart[b * 16 + i];
+        }
+        o.margin[b] = mg;
+        o.over[b] = over;
+        if (b == a.nb - 1) {
+#pragma unroll
+            for (int i = 0; i < 16; ++i) o.Tend[i] = T[i];
+        }
+        if constexpr (WITH_P) {
+#pragma unroll
+            for (int i = 0; i < 64; ++i) Pb[b * 64 + i] = P[i];
+            maxx2[b] = mx;
+        }
+    }
+    unsigned long long rr = run ? 1ull : 0ull;
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+        changed += __shfl_xor_sync(0xffffffffu, changed, off);
+        rr += __shfl_xor_sync(0xffffffffu, rr, off);
+    }
+    if (lane == 0) {
+        if (changed) atomicAdd(o.counters + 0, changed);
+        if (rr) atomicAdd(o.counters + 1, rr);
     }
 }
 
-// down-sweep: children start taps from the group start taps
-__global__ void scan_down_kernel(const float* __restrict__ Pc, const float* __restrict__ Qc, int64_t n_child,
-                                 int G, const float* __restrict__ Tg, int64_t n_grp, float* __restrict__ Tc) {
-    const int64_t g = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+// fold groups of G consecutive maps:  (P, Q) <- (P P_c, Q P_c + Q_c)
+// One warp per group; the running P (8x8) / Q (2x8) live in shared memory,
+// lane l owns P entries 2l, 2l+1 and (l < 16) Q entry l.
+constexpr int kScanWarps = 4;
+
+__global__ void __launch_bounds__(32 * kScanWarps)
+scan_fold_kernel(const float* __restrict__ Pc, const float* __restrict__ Qc, int64_t n_child, int G,
+                 float* __restrict__ Pg, float* __restrict__ Qg, int64_t n_grp, int with_p) {
+    __shared__ float sP[kScanWarps][64];
+    __shared__ float sQ[kScanWarps][16];
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    const int64_t g = int64_t(blockIdx.x) * kScanWarps + w;
     if (g >= n_grp) return;
-    float T[16];
-#pragma unroll
-    for (int i = 0; i < 16; ++i) T[i] = Tg[g * 16 + i];
+    float* P = sP[w];
+    float* Q = sQ[w];
+    P[2 * l] = ((2 * l) % 9 == 0) ? 1.f : 0.f;
+    P[2 * l + 1] = ((2 * l + 1) % 9 == 0) ? 1.f : 0.f;
+    if (l < 16) Q[l] = 0.f;
+    __syncwarp();
+    const int pi = (2 * l) >> 3, pj = (2 * l) & 7;   // P entries (pi, pj), (pi, pj+1)
+    const int qr = l >> 3, qj = l & 7;               // Q entry (qr, qj) for l < 16
     const int64_t c0 = g * G, c1 = min(c0 + G, n_child);
     for (int64_t c = c0; c < c1; ++c) {
+        const float* M = Pc + c * 64;
+        float q = 0.f, p0 = 0.f, p1 = 0.f;
+        if (l < 16) {
+            q = __ldg(Qc + c * 16 + l);
 #pragma unroll
-        for (int i = 0; i < 16; ++i) Tc[c * 16 + i] = T[i];
+            for (int k = 0; k < 8; ++k) q = fmaf(Q[qr * 8 + k], __ldg(M + k * 8 + qj), q);
+        }
+        if (with_p) {
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+                const float a = P[pi * 8 + k];
+                p0 = fmaf(a, __ldg(M + k * 8 + pj), p0);
+                p1 = fmaf(a, __ldg(M + k * 8 + pj + 1), p1);
+            }
+        }
+        __syncwarp();
+        if (l < 16) Q[l] = q;
+        if (with_p) { P[2 * l] = p0; P[2 * l + 1] = p1; }
+        __syncwarp();
+    }
+    if (l < 16) Qg[g * 16 + l] = Q[l];
+    if (with_p) { Pg[g * 64 + 2 * l] = P[2 * l]; Pg[g * 64 + 2 * l + 1] = P[2 * l + 1]; }
+}
+
+// down-sweep: children start taps from the group start taps, one warp per
+// group (lanes 0..15 own T entries)
+__global__ void __launch_bounds__(32 * kScanWarps)
+scan_down_kernel(const float* __restrict__ Pc, const float* __restrict__ Qc, int64_t n_child, int G,
+                 const float* __restrict__ Tg, int64_t n_grp, float* __restrict__ Tc) {
+    __shared__ float sT[kScanWarps][16];
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    const int64_t g = int64_t(blockIdx.x) * kScanWarps + w;
+    if (g >= n_grp) return;
+    float* T = sT[w];
+    if (l < 16) T[l] = Tg[g * 16 + l];
+    __syncwarp();
+    const int r = l >> 3, j = l & 7;
+    const int64_t c0 = g * G, c1 = min(c0 + G, n_child);
+    for (int64_t c = c0; c < c1; ++c) {
+        if (l < 16) Tc[c * 16 + l] = T[l];
         if (c + 1 == c1) break;
         const float* M = Pc + c * 64;
-        float nT[16];
+        float t = 0.f;
+        if (l < 16) {
+            t = __ldg(Qc + c * 16 + l);
 #pragma unroll
-        for (int r = 0; r < 2; ++r)
-#pragma unroll
-            for (int j = 0; j < 8; ++j) {
-                float s = Qc[c * 16 + r * 8 + j];
-#pragma unroll
-                for (int i = 0; i < 8; ++i) s = fmaf(T[r * 8 + i], __ldg(M + i * 8 + j), s);
-                nT[r * 8 + j] = s;
-            }
-#pragma unroll
-        for (int i = 0; i < 16; ++i) T[i] = nT[i];
+            for (int k = 0; k < 8; ++k) t = fmaf(T[r * 8 + k], __ldg(M + k * 8 + j), t);
+        }
+        __syncwarp();
+        if (l < 16) T[l] = t;
+        __syncwarp();
     }
 }
 
@@ -419,15 +650,27 @@ __global__ void xcorr_kernel(const float2* __restrict__ head, int64_t n_head, co
     if (t >= tot) return;
     const int parity = t < n_lag0 ? 0 : 1;
     const int64_t k = parity ? t - n_lag0 : t;
-    double re = 0.0, im = 0.0;
-    for (int i = 0; i < n_ref; ++i) {
-        const float2 z = head[parity + 2 * (k + i)];
-        const float2 r = sref[i];
-        // z * conj(r)
-        re += static_cast<double>(z.x) * r.x + static_cast<double>(z.y) * r.y;
-        im += static_cast<double>(z.y) * r.x - static_cast<double>(z.x) * r.y;
+    float re[4] = {0.f, 0.f, 0.f, 0.f}, im[4] = {0.f, 0.f, 0.f, 0.f};
+    const float2* zp = head + parity + 2 * k;
+    int i = 0;
+    for (; i + 4 <= n_ref; i += 4) {
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const float2 z = __ldg(zp + 2 * (i + u));
+            const float2 r = sref[i + u];
+            re[u] = fmaf(z.x, r.x, fmaf(z.y, r.y, re[u]));      // z * conj(r)
+            im[u] = fmaf(z.y, r.x, fmaf(-z.x, r.y, im[u]));
+        }
     }
-    mag[t] = sqrt(re * re + im * im);
+    for (; i < n_ref; ++i) {
+        const float2 z = __ldg(zp + 2 * i);
+        const float2 r = sref[i];
+        re[0] = fmaf(z.x, r.x, fmaf(z.y, r.y, re[0]));
+        im[0] = fmaf(z.y, r.x, fmaf(-z.x, r.y, im[0]));
+    }
+    const double R = (static_cast<double>(re[0]) + re[1]) + (static_cast<double>(re[2]) + re[3]);
+    const double I = (static_cast<double>(im[0]) + im[1]) + (static_cast<double>(im[2]) + im[3]);
+    mag[t] = sqrt(R * R + I * I);
 }
 
 __global__ void sync_reduce_kernel(const double* __restrict__ mag, int64_t n_lag0, int64_t n_lag1,
@@ -621,6 +864,7 @@ Layout plan(int64_t nsym, int B) {
     b += align_up(L.nb * sizeof(float)) * 2;    // margin, maxx2
     b += align_up(16 * sizeof(float)) * 2;      // Tend, Tinit
     b += align_up(L.nb * sizeof(int));          // over
+    b += align_up(L.nb * sizeof(unsigned long long));   // label hashes
     b += align_up(4 * sizeof(unsigned long long));
     L.bytes = b;
     return L;
@@ -667,6 +911,7 @@ extern "C" int kk_ddlms_solve(const void* x, int64_t nsym, float scale, const vo
     float* Tend = reinterpret_cast<float*>(w); w += align_up(16 * sizeof(float));
     float* Tinit_d = reinterpret_cast<float*>(w); w += align_up(16 * sizeof(float));
     int* over = reinterpret_cast<int*>(w); w += align_up(L.nb * sizeof(int));
+    unsigned long long* hsh = reinterpret_cast<unsigned long long*>(w); w += align_up(L.nb * 8);
     unsigned long long* ctr = reinterpret_cast<unsigned long long*>(w);
 
     SolveArgs a;
@@ -686,6 +931,7 @@ extern "C" int kk_ddlms_solve(const void* x, int64_t nsym, float scale, const vo
     o.margin = margin;
     o.Tend = Tend;
     o.over = over;
+    o.hash = hsh;
     o.counters = ctr;
 
     const int th = 128;
@@ -693,43 +939,22 @@ extern "C" int kk_ddlms_solve(const void* x, int64_t nsym, float scale, const vo
     const int top = static_cast<int>(lv.size()) - 1;
     int64_t st[6] = {0, 0, 0, 0, 0, L.nb};
 
-    // (1) decision-independent block maps and their aggregates
-    ddlms_maps_kernel<<<grid_of(L.nb), th, 0, s>>>(a, lv[0].P, maxx2);
-    if (int rc = check_launch("ddlms_maps_kernel")) return rc;
     if (cudaMemsetAsync(labels, 0xFE, nsym, s) != cudaSuccess) return set_cuda_error("labels init");
 
     auto scan = [&](bool with_p) -> int {
+        const unsigned wblk = 32 * kScanWarps;
+        auto wgrid = [&](int64_t n) { return static_cast<unsigned>((n + kScanWarps - 1) / kScanWarps); };
         for (int l = 1; l <= top; ++l) {
-            scan_fold_kernel<<<grid_of(lv[l].n), th, 0, s>>>(lv[l - 1].P, lv[l - 1].Q, lv[l - 1].n, kG, lv[l].P,
+            scan_fold_kernel<<<wgrid(lv[l].n), wblk, 0, s>>>(lv[l - 1].P, lv[l - 1].Q, lv[l - 1].n, kG, lv[l].P,
                                                              lv[l].Q, lv[l].n, with_p ? 1 : 0);
             if (int rc = check_launch("scan_fold_kernel")) return rc;
         }
-        // top level: sequential over <= kG entries from T_init
-        {
-            std::vector<float> Ptop(lv[top].n * 64), Qtop(lv[top].n * 16), Ttop(lv[top].n * 16);
-            if (cudaMemcpyAsync(Ptop.data(), lv[top].P, Ptop.size() * 4, cudaMemcpyDeviceToHost, s) != cudaSuccess ||
-                cudaMemcpyAsync(Qtop.data(), lv[top].Q, Qtop.size() * 4, cudaMemcpyDeviceToHost, s) != cudaSuccess ||
-                cudaStreamSynchronize(s) != cudaSuccess)
-                return set_cuda_error("scan top copy");
-            float T[16];
-            for (int i = 0; i < 16; ++i) T[i] = T_init[i];
-            for (int64_t g = 0; g < lv[top].n; ++g) {
-                for (int i = 0; i < 16; ++i) Ttop[g * 16 + i] = T[i];
-                float nT[16];
-                for (int r = 0; r < 2; ++r)
-                    for (int j = 0; j < 8; ++j) {
-                        float acc = Qtop[g * 16 + r * 8 + j];
-                        for (int i = 0; i < 8; ++i) acc = std::fma(T[r * 8 + i], Ptop[g * 64 + i * 8 + j], acc);
-                        nT[r * 8 + j] = acc;
-                    }
-                for (int i = 0; i < 16; ++i) T[i] = nT[i];
-            }
-            if (cudaMemcpyAsync(lv[top].T, Ttop.data(), Ttop.size() * 4, cudaMemcpyHostToDevice, s) != cudaSuccess ||
-                cudaStreamSynchronize(s) != cudaSuccess)
-                return set_cuda_error("scan top upload");
-        }
+        // top level: one warp folds the <= kG top entries from T_init
+        scan_down_kernel<<<1, wblk, 0, s>>>(lv[top].P, lv[top].Q, lv[top].n, static_cast<int>(lv[top].n), Tinit_d,
+                                            1, lv[top].T);
+        if (int rc = check_launch("scan_down_kernel")) return rc;
         for (int l = top; l >= 1; --l) {
-            scan_down_kernel<<<grid_of(lv[l].n), th, 0, s>>>(lv[l - 1].P, lv[l - 1].Q, lv[l - 1].n, kG, lv[l].T,
+            scan_down_kernel<<<wgrid(lv[l].n), wblk, 0, s>>>(lv[l - 1].P, lv[l - 1].Q, lv[l - 1].n, kG, lv[l].T,
                                                              lv[l].n, lv[l - 1].T);
             if (int rc = check_launch("scan_down_kernel")) return rc;
         }
@@ -746,6 +971,27 @@ extern "C" int kk_ddlms_solve(const void* x, int64_t nsym, float scale, const vo
         fill_T_kernel<<<grid_of((b1 - b0) * 16), th, 0, s>>>(lv[0].T, b0, b1, Tsrc_dev);
         return check_launch("fill_T_kernel");
     };
+    constexpr int kC = 8;
+    const size_t bsm = block_kernel_smem(kC);
+    static bool attr_done = false;
+    if (!attr_done) {
+        if (cudaFuncSetAttribute(ddlms_block_kernel<kC, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(bsm)) != cudaSuccess ||
+            cudaFuncSetAttribute(ddlms_block_kernel<kC, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(bsm)) != cudaSuccess)
+            return set_cuda_error("ddlms smem attr");
+        attr_done = true;
+    }
+    auto run_blocks = [&](bool with_p, int64_t b0, int64_t b1, int use_skip) -> int {
+        if (b1 <= b0) return KK_OK;
+        const unsigned g = static_cast<unsigned>((b1 - b0 + 127) / 128);
+        if (with_p)
+            ddlms_block_kernel<kC, true><<<g, 128, bsm, s>>>(a, sl, lv[0].T, lv[0].P, maxx2, o, b0, b1, 0, soft_tol);
+        else
+            ddlms_block_kernel<kC, false><<<g, 128, bsm, s>>>(a, sl, lv[0].T, lv[0].P, maxx2, o, b0, b1, use_skip,
+                                                              soft_tol);
+        return check_launch("ddlms_block_kernel");
+    };
 
     // (2) pure-training blocks are exact from any start: run them, scan to
     //     get the exact training-end taps, speculate everything after.
@@ -753,13 +999,15 @@ extern "C" int kk_ddlms_solve(const void* x, int64_t nsym, float scale, const vo
     if (cudaMemcpyAsync(Tinit_d, T_init, 16 * sizeof(float), cudaMemcpyHostToDevice, s) != cudaSuccess)
         return set_cuda_error("T_init upload");
     if (cudaMemsetAsync(over, 0, L.nb * sizeof(int), s) != cudaSuccess) return set_cuda_error("over init");
+    if (cudaMemsetAsync(hsh, 0, L.nb * 8, s) != cudaSuccess) return set_cuda_error("hash init");
     if (int rc = fill_T(0, L.nb, Tinit_d)) return rc;
     if (cudaMemsetAsync(ctr, 0, 4 * sizeof(unsigned long long), s) != cudaSuccess) return set_cuda_error("ctr");
     if (bt > 0) {
-        ddlms_run_kernel<<<grid_of(bt), th, 0, s>>>(a, sl, lv[0].T, maxx2, o, 0, bt, 0, soft_tol, 0, 1);
-        if (int rc = check_launch("ddlms_run_kernel")) return rc;
+        // first pass fused with the block maps P_b (decision independent)
+        if (int rc = run_blocks(true, 0, bt, 0)) return rc;
         // Q of not-yet-run blocks must not pollute the training scan: zero them
-        if (cudaMemsetAsync(lv[0].Q + bt * 16, 0, (L.nb - bt) * 16 * sizeof(float), s) != cudaSuccess)
+        if (bt < L.nb &&
+            cudaMemsetAsync(lv[0].Q + bt * 16, 0, (L.nb - bt) * 16 * sizeof(float), s) != cudaSuccess)
             return set_cuda_error("Q init");
         if (int rc = scan(true)) return rc;
         // lv[0].T[bt] is exact; broadcast it as the guess for all later blocks
@@ -770,12 +1018,9 @@ extern "C" int kk_ddlms_solve(const void* x, int64_t nsym, float scale, const vo
             if (int rc = fill_T(bt + 1, L.nb, Tend)) return rc;
         }
     }
-    if (bt < L.nb) {
-        ddlms_run_kernel<<<grid_of(L.nb - bt), th, 0, s>>>(a, sl, lv[0].T, maxx2, o, bt, L.nb, 0, soft_tol, 0, 1);
-        if (int rc = check_launch("ddlms_run_kernel")) return rc;
-    }
+    if (int rc = run_blocks(true, bt, L.nb, 0)) return rc;
     st[1] = L.nb;
-    bool p_done = bt > 0;
+    bool p_done = false;   // the training scan saw only the training blocks' maps
 
     // (3) fixpoint iterations
     bool converged = false;
@@ -784,12 +1029,15 @@ extern "C" int kk_ddlms_solve(const void* x, int64_t nsym, float scale, const vo
         if (int rc = scan(!p_done)) return rc;
         p_done = true;
         if (cudaMemsetAsync(ctr, 0, 4 * sizeof(unsigned long long), s) != cudaSuccess) return set_cuda_error("ctr");
-        ddlms_run_kernel<<<grid_of(L.nb), th, 0, s>>>(a, sl, lv[0].T, maxx2, o, 0, L.nb, 1, soft_tol, 0, 0);
-        if (int rc = check_launch("ddlms_run_kernel")) return rc;
+        if (int rc = run_blocks(false, 0, L.nb, 1)) return rc;
         if (int rc = read_ctr(h)) return rc;
         st[0] = it;
         st[1] += static_cast<int64_t>(h[1]);
         st[4] = static_cast<int64_t>(h[0]);
+        if (it <= 16 && stats) {   // per-iteration detail: stats[6 + 2(it-1)] = changed, reruns
+            stats[6 + 2 * (it - 1)] = static_cast<int64_t>(h[0]);
+            stats[7 + 2 * (it - 1)] = static_cast<int64_t>(h[1]);
+        }
         if (h[0] == 0) { converged = true; break; }
     }
     if (!converged) {

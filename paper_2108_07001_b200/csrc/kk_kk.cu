@@ -157,7 +157,7 @@ kk_pairs_kernel(const TIn* __restrict__ in, float in_scale, float clamp_rel, int
     const int64_t pair = int64_t(blockIdx.x) * kPairsPerCta + g;
     const int64_t hop_a = 2 * pair;          // output hop of the real-part block
     const bool active = hop_a < n_hops;
-    const Twiddle tw{S.tw, S.tw + kTwHi};
+    const Twiddle tw{S.tw};
     SmemPlanes P{S.re[g], S.im[g]};
     const float* ua = S.u + (2 * g) * kHop;          // block a: stage hops 2g, 2g+1
     const float* ub = S.u + (2 * g + 1) * kHop;      // block b: stage hops 2g+1, 2g+2
@@ -182,6 +182,11 @@ kk_pairs_kernel(const TIn* __restrict__ in, float in_scale, float clamp_rel, int
     const float* ab = S.a + (2 * g + 1) * kHop + kHop / 2;  // block b
     const int dead_a0 = S.dead[2 * g], dead_a1 = S.dead[2 * g + 1], dead_b1 = S.dead[2 * g + 2];
     const bool hist = (hop0 + 2 * g) < 0;   // stage hop 2g is the state hop
+    // rotation index (rot_p * g mod rot_q) of the pair's first output sample
+    unsigned rot_base = 0;
+    const float inv_q = rot_q > 0 ? 1.0f / static_cast<float>(rot_q) : 0.f;
+    if (rot_q > 0 && active)
+        rot_base = static_cast<unsigned>((static_cast<unsigned long long>(n0_global + hop_a * kHop) % rot_q));
     auto st_out = [&](int n, float2 v) {
         if (n < kHop) return;
         const int i = n - kHop;
@@ -202,11 +207,11 @@ kk_pairs_kernel(const TIn* __restrict__ in, float in_scale, float clamp_rel, int
         const int64_t pb = pa + kHop;
         float2 za = fa, zb = fb;
         if (rot_q > 0) {
-            const int64_t ga = n0_global + pa, gb = n0_global + pb;
-            const int ia = static_cast<int>((static_cast<unsigned long long>(ga) % rot_q) * rot_p % rot_q);
-            const int ib = static_cast<int>((static_cast<unsigned long long>(gb) % rot_q) * rot_p % rot_q);
-            za = cmul(fa, rot_tab[ia]);
-            zb = cmul(fb, rot_tab[ib]);
+            const unsigned Q = static_cast<unsigned>(rot_q), P = static_cast<unsigned>(rot_p);
+            const unsigned ia = fmod_u((rot_base + i) * P, Q, inv_q);
+            const unsigned ib = fmod_u((rot_base + kHop + i) * P, Q, inv_q);
+            za = cmul(fa, __ldg(rot_tab + ia));
+            zb = cmul(fb, __ldg(rot_tab + ib));
         }
         if (mirror) { za = cconj(za); zb = cconj(zb); }
         out[pa] = za;

@@ -21,6 +21,8 @@
 // carrier subtraction / pre-twiddle fused, the IFFT's first pass applies the
 // kept-bin gather and H, and the final IFFT pass writes the 2-sps output
 // straight to HBM.
+#include <algorithm>
+
 #include "kk_common.cuh"
 #include "kk_internal.h"
 
@@ -57,16 +59,6 @@ struct K2Params {
     const float2* h_odd;    // H at kept index 2m'+1 (8192)
     float2* out;            // 8192 per block
 };
-
-// x mod d for 0 <= x < 2^25 via a float reciprocal (+-1 quotient fix-up)
-__device__ __forceinline__ unsigned fmod_u(unsigned x, unsigned d, float inv_d, unsigned* quot = nullptr) {
-    unsigned q = __float2uint_rz(__uint2float_rn(x) * inv_d);
-    int r = static_cast<int>(x) - static_cast<int>(q * d);
-    if (r < 0) { r += d; --q; }
-    if (r >= static_cast<int>(d)) { r -= d; ++q; }
-    if (quot) *quot = q;
-    return static_cast<unsigned>(r);
-}
 
 // per-CTA constants for the carrier-removed input of one 32768-sample block
 struct BlockIn {
@@ -123,6 +115,55 @@ __device__ __forceinline__ float2 static_input(const K2Params& p, const BlockIn&
     return v;
 }
 
+// Pass 1 of the chain-c FFT16384, butterfly j: v[r] = a(n) (c = 0) or b(n)
+// (c = 1) at n = j + 1024 r.  FAST: interior block with at most one carrier
+// segment boundary (incremental indices); otherwise the generic path.
+template <int CHAIN, bool FAST>
+__device__ __forceinline__ void k2_load_bfly(const K2Params& p, const BlockIn& b, const float2* rot_s,
+                                             const Twiddle& tw, int j, float2 mA, float2 mB, int bnd,
+                                             unsigned s1024, unsigned s16384, float2 (&v)[1][16]) {
+    if constexpr (FAST) {
+        const float2* z0 = p.z + (b.base - p.z_index0) + j;
+        const unsigned Q = static_cast<unsigned>(p.rot_q);
+        unsigned a0 = 0, a1 = 0;
+        if (p.carrier && Q) {
+            a0 = fmod_u(b.c0 + static_cast<unsigned>(p.rot_p) * static_cast<unsigned>(j), Q, b.inv_q);
+            a1 = a0 + s16384;
+            a1 -= (a1 >= Q) ? Q : 0u;
+        }
+#pragma unroll
+        for (int r = 0; r < 16; ++r) {
+            const int n = j + 1024 * r;
+            float2 x0 = __ldg(z0 + 1024 * r);
+            float2 x1 = __ldg(z0 + kHopS + 1024 * r);
+            if (p.carrier) {
+                float2 m0 = n < bnd ? mA : mB;
+                float2 m1 = (n + kHopS) < bnd ? mA : mB;
+                if (Q) {
+                    m0 = cmul(m0, rot_s[a0]);
+                    m1 = cmul(m1, rot_s[a1]);
+                    a0 += s1024; a0 -= (a0 >= Q) ? Q : 0u;
+                    a1 += s1024; a1 -= (a1 >= Q) ? Q : 0u;
+                }
+                if (p.mirror) { m0 = cconj(m0); m1 = cconj(m1); }
+                x0 = csub(x0, m0);
+                x1 = csub(x1, m1);
+            }
+            if constexpr (CHAIN == 0) v[0][r] = cadd(x0, x1);
+            else v[0][r] = cmul(csub(x0, x1), tw.template w<kNS>(n));
+        }
+    } else {
+#pragma unroll
+        for (int r = 0; r < 16; ++r) {
+            const int n = j + 1024 * r;
+            const float2 x0 = static_input(p, b, rot_s, n), x1 = static_input(p, b, rot_s, kHopS + n);
+            if constexpr (CHAIN == 0) v[0][r] = cadd(x0, x1);
+            else v[0][r] = cmul(csub(x0, x1), tw.template w<kNS>(n));
+        }
+    }
+}
+
+template <bool FAST>
 __global__ void __launch_bounds__(kK2Threads, 1) static_blocks_kernel(K2Params p, const float2* __restrict__ tw_g) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     K2Smem& S = *reinterpret_cast<K2Smem*>(smem_raw);
@@ -132,25 +173,33 @@ __global__ void __launch_bounds__(kK2Threads, 1) static_blocks_kernel(K2Params p
         for (int i = tid; i < p.rot_q; i += kK2Threads) S.rot[i] = p.rot_tab[i];
     __syncthreads();
 
-    const Twiddle tw{S.tw, S.tw + kTwHi};
+    const Twiddle tw{S.tw};
     const SmemPlanes P{S.re, S.im};
     const int64_t hb = p.hb0 + blockIdx.x;
     const int64_t base = (hb - 1) * kHopS;   // global index of block sample 0
     const BlockIn bi = make_block_in(p, base);
+    float2 mA = make_float2(0.f, 0.f), mB = mA;
+    int bnd = kNS;
+    unsigned s1024 = 0, s16384 = 0;
+    if (FAST && p.carrier) {
+        mA = __ldg(p.seg_mean + bi.sb);
+        bnd = p.seg_len - static_cast<int>(bi.rb);
+        if (bnd < kNS) mB = __ldg(p.seg_mean + bi.sb + 1);
+        if (p.rot_q > 0) {
+            s1024 = static_cast<unsigned>((1024ll * p.rot_p) % p.rot_q);
+            s16384 = static_cast<unsigned>((16384ll * p.rot_p) % p.rot_q);
+        }
+    }
 
     for (int chain = 0; chain < 2; ++chain) {
         // ---- FFT16384 of a = x0 + x1 (even bins) or b = (x0 - x1) W^n (odd) ----
-        if (chain == 0) {
-            auto ld = [&](int n) {
-                return cadd(static_input(p, bi, S.rot, n), static_input(p, bi, S.rot, kHopS + n));
-            };
-            stockham_pass<kHopS, 16, 1, kK2Threads, false, false>(tid, tw, ld, StorePlanes{P});
-        } else {
-            auto ld = [&](int n) {
-                const float2 d = csub(static_input(p, bi, S.rot, n), static_input(p, bi, S.rot, kHopS + n));
-                return cmul(d, tw.template w<kNS>(n));
-            };
-            stockham_pass<kHopS, 16, 1, kK2Threads, false, false>(tid, tw, ld, StorePlanes{P});
+#pragma unroll 1
+        for (int q = 0; q < 2; ++q) {
+            float2 v[1][16];
+            const int j = tid + q * kK2Threads;
+            if (chain == 0) k2_load_bfly<0, FAST>(p, bi, S.rot, tw, j, mA, mB, bnd, s1024, s16384, v);
+            else k2_load_bfly<1, FAST>(p, bi, S.rot, tw, j, mA, mB, bnd, s1024, s16384, v);
+            stockham_compute_store<kHopS, 16, 1, kK2Threads, false, 1>(j, tw, v, StorePlanes{P});
         }
         __syncthreads();
         stockham_pass<kHopS, 16, 16, kK2Threads, false, true>(tid, tw, LoadPlanes{P}, StorePlanes{P});
@@ -174,7 +223,7 @@ __global__ void __launch_bounds__(kK2Threads, 1) static_blocks_kernel(K2Params p
         __syncthreads();
         if (chain == 0) {
             auto st_a = [&](int n, float2 v) { S.A[n] = v; };
-            stockham_pass<kNOut, 4, 2048, kK2Threads, true, true>(tid, tw, LoadPlanes{P}, st_a);
+            stockham_pass<kNOut, 4, 2048, kK2Threads, true, false>(tid, tw, LoadPlanes{P}, st_a);
             __syncthreads();
         } else {
             float2* out = p.out + int64_t(blockIdx.x) * kNOut;
@@ -184,7 +233,7 @@ __global__ void __launch_bounds__(kK2Threads, 1) static_blocks_kernel(K2Params p
                 const float2 bt = cmulc(v, tw.template w<kHopS>(r));
                 out[r] = cscale(csub(S.A[r], bt), sc);
             };
-            stockham_pass<kNOut, 4, 2048, kK2Threads, true, true>(tid, tw, LoadPlanes{P}, st_o);
+            stockham_pass<kNOut, 4, 2048, kK2Threads, true, false>(tid, tw, LoadPlanes{P}, st_o);
         }
     }
 }
@@ -205,11 +254,14 @@ extern "C" int kk_static_blocks(const void* z, int64_t z_index0, int64_t hb0, in
     static bool attr_done = false;
     const size_t smem = sizeof(K2Smem);
     if (!attr_done) {
-        if (cudaFuncSetAttribute(static_blocks_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        if (cudaFuncSetAttribute(static_blocks_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(smem)) != cudaSuccess ||
+            cudaFuncSetAttribute(static_blocks_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  static_cast<int>(smem)) != cudaSuccess)
             return set_cuda_error("K2 smem attr");
         attr_done = true;
     }
+    if (rot_q > kRotMax) return set_error(KK_ERR_PARAM, "rotation denominator must be <= 1024");
     K2Params p;
     p.z = static_cast<const float2*>(z);
     p.z_index0 = z_index0;
@@ -226,8 +278,32 @@ extern "C" int kk_static_blocks(const void* z, int64_t z_index0, int64_t hb0, in
     p.h_even = static_cast<const float2*>(h_even);
     p.h_odd = static_cast<const float2*>(h_odd);
     p.out = static_cast<float2*>(out);
-    static_blocks_kernel<<<static_cast<unsigned>(n_blocks), kK2Threads, smem, static_cast<cudaStream_t>(stream)>>>(p, tw);
-    return check_launch("static_blocks_kernel");
+    // interior blocks (inside [0, valid_end), <= 1 carrier boundary) take the
+    // FAST specialisation; the stream-edge blocks the generic one
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const int64_t hb1 = hb0 + n_blocks;
+    int64_t lo = hb0, hi = hb1;
+    if (!carrier || seg_len >= kNS) {
+        lo = std::max<int64_t>(hb0, 1);
+        hi = std::min<int64_t>(hb1, valid_end / kHopS);
+        if (hi < lo) { lo = hb0; hi = hb0; }
+    } else {
+        lo = hi = hb0;
+    }
+    auto launch = [&](bool fast, int64_t a, int64_t b) -> int {
+        if (b <= a) return KK_OK;
+        K2Params q = p;
+        q.hb0 = a;
+        q.out = p.out + (a - hb0) * kNOut;
+        if (fast)
+            static_blocks_kernel<true><<<static_cast<unsigned>(b - a), kK2Threads, smem, s>>>(q, tw);
+        else
+            static_blocks_kernel<false><<<static_cast<unsigned>(b - a), kK2Threads, smem, s>>>(q, tw);
+        return check_launch("static_blocks_kernel");
+    };
+    if (int rc = launch(false, hb0, lo)) return rc;
+    if (int rc = launch(true, lo, hi)) return rc;
+    return launch(false, hi, hb1);
 }
 
 // ---------------------------------------------------------------------------

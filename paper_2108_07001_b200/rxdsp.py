@@ -277,7 +277,8 @@ class _DevStream:
         if need > self.buf.shape[0]:
             live0 = max(self.keep, self.base)
             live = self.end - live0
-            cap = max(2 * (live + n_more), 1 << 16)
+            # exact fit for a first (one-shot) fill, geometric growth when streaming
+            cap = n_more if live == 0 else max(2 * (live + n_more), 1 << 16)
             nb = self.torch.empty(cap, dtype=self.buf.dtype, device=self.buf.device)
             if live > 0:
                 nb[:live].copy_(self.buf[live0 - self.base:self.end - self.base])
@@ -869,15 +870,17 @@ class RxPipeline:
                 self._ws = torch.empty(wsb, dtype=torch.uint8, device=self.dev)
             Tin = np.ascontiguousarray(self._T, dtype=np.float32)
             Tout = np.zeros(16, dtype=np.float32)
-            st = np.zeros(6, dtype=np.int64)
+            st = np.zeros(38, dtype=np.int64)
             _lib.call("kk_ddlms_solve", x_ptr, nsym, float(self._eq_scale), train_ptr, n_train,
                       Tin.ctypes.data, tb.order, tb.pts_ri.ctypes.data,
                       tb.grid.ctypes.data if tb.grid_m else None, tb.grid_m, tb.norm, tb.max_radius,
                       float(d.divergence_factor), int(d.divergence_run), float(d.mu), B,
                       int(self.gpu.ddlms_max_iter), float(self.gpu.ddlms_soft_tol), _ptr(labels), _ptr(soft),
                       Tout.ctypes.data, _ptr(self._ws), wsb, st.ctypes.data, _stream(self.dev))
-            stats.update(iterations=int(st[0]), blocks_rerun=int(st[1]), fallback=int(st[2]),
-                         guard_exceed=int(st[3]), blocks=int(st[5]))
+            it = int(st[0])
+            stats.update(iterations=it, blocks_rerun=int(st[1]), fallback=int(st[2]),
+                         guard_exceed=int(st[3]), blocks=int(st[5]),
+                         per_iter=[(int(st[6 + 2 * i]), int(st[7 + 2 * i])) for i in range(min(it, 16))])
             if st[2] == 1:
                 use_solve = False   # guard interaction: exact sequential re-run of the frame
                 stats["mode"] = "sequential(guard)"
