@@ -334,43 +334,108 @@ __global__ void fill_T_kernel(float* __restrict__ T, int64_t b0, int64_t b1, con
 // contiguous 2C+2-sample segments coalesced) and the outputs (labels, soft)
 // are written back the same way.  WITH_P additionally accumulates the
 // decision-independent block map P_b and max|X|^2 (fused first pass).
-constexpr size_t block_kernel_smem(int C) {
-    return 2 * size_t(128) * ((2 * C + 2) | 1) * 8 + size_t(128) * (C | 1) * 8 + 128 * 4;
+// ---------------------------------------------------------------------------
+// Block-interleaved ("transposed") layout for the block-parallel passes:
+// XT[i * nb + b] = (x[2(bB+i)], x[2(bB+i)+1]) (one float4 = two 2-sps samples)
+// for pair i in [0, B] of block b, so that thread b's sequential recurrence
+// reads XT[i][b] while its 31 warp neighbours read XT[i][b+1..b+31]: every
+// load is a fully coalesced 512-byte warp transaction, with no staging.
+// Outputs are written the same way (ST / LT) and un-transposed once.
+// ---------------------------------------------------------------------------
+__global__ void ddlms_transpose_in(const float2* __restrict__ x, int64_t nsym, int B, int64_t nb,
+                                   float4* __restrict__ XT) {
+    __shared__ float4 tile[32][33];
+    const int tx = threadIdx.x, ty = threadIdx.y;
+    const int64_t b0 = int64_t(blockIdx.x) * 32;
+    const int i0 = blockIdx.y * 32;
+    for (int bb = ty; bb < 32; bb += 8) {
+        const int64_t b = b0 + bb;
+        const int i = i0 + tx;
+        float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (b < nb && i <= B) {
+            const int64_t g = b * B + i;           // pair index: samples 2g, 2g+1
+            if (g <= nsym) {
+                const float2 a = __ldg(x + 2 * g), c = __ldg(x + 2 * g + 1);
+                v = make_float4(a.x, a.y, c.x, c.y);
+            }
+        }
+        tile[bb][tx] = v;
+    }
+    __syncthreads();
+    for (int ii = ty; ii < 32; ii += 8) {
+        const int i = i0 + ii;
+        const int64_t b = b0 + tx;
+        if (i <= B && b < nb) XT[int64_t(i) * nb + b] = tile[tx][ii];
+    }
 }
 
-__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
-    const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(smem));
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(gmem));
+__global__ void ddlms_transpose_out(const float2* __restrict__ ST, const uint8_t* __restrict__ LT, int64_t nsym,
+                                    int B, int64_t nb, float2* __restrict__ soft, uint8_t* __restrict__ labels) {
+    __shared__ float2 ts[32][33];
+    __shared__ uint8_t tl[32][33];
+    const int tx = threadIdx.x, ty = threadIdx.y;
+    const int64_t b0 = int64_t(blockIdx.x) * 32;
+    const int i0 = blockIdx.y * 32;
+    for (int ii = ty; ii < 32; ii += 8) {
+        const int i = i0 + ii;
+        const int64_t b = b0 + tx;
+        if (i < B && b < nb) {
+            ts[ii][tx] = ST[int64_t(i) * nb + b];
+            tl[ii][tx] = LT[int64_t(i) * nb + b];
+        }
+    }
+    __syncthreads();
+    for (int bb = ty; bb < 32; bb += 8) {
+        const int64_t b = b0 + bb;
+        const int i = i0 + tx;
+        const int64_t k = b * B + i;
+        if (b < nb && i < B && k < nsym) {
+            soft[k] = ts[tx][bb];
+            labels[k] = tl[tx][bb];
+        }
+    }
 }
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
 
-// Block-parallel DDLMS pass, one thread per block of B symbols, 128 blocks per
-// CTA.  Each thread's recurrence is sequential, so its input is staged per
-// chunk of C symbols through shared memory with cp.async (a warp copies each
-// of its threads' contiguous 2C+2-sample segments, coalesced; double
-// buffered so chunk c+1 streams in while chunk c is computed) and the soft
-// outputs are written back the same way.  Decision changes are detected per
-// block with a 64-bit hash of its label sequence (no label re-read).  WITH_P
-// additionally accumulates the decision-independent block map P_b and
-// max|X|^2 (fused first pass).
-template <int C, bool WITH_P>
+struct LeanSlicer {
+    int square, m;
+    float half_norm, off, h;     // v = y*half_norm + off: level index; h = half level spacing
+};
+
+struct TOut {
+    float2* ST;       // [B][nb] transposed soft
+    uint8_t* LT;      // [B][nb] transposed labels
+};
+
+// Block-parallel DDLMS pass, one thread per block of B symbols.  Lean
+// per-symbol work (~70 instructions): the input scale s is folded into the
+// taps (T' = s T, mu' = mu s^2, so y = T' x_raw); Q_b is recovered once per
+// block as T_end - T_start P_b; decision changes are detected with a 32-bit
+// hash of the block's label sequence; the guard is tracked as max |y|^2.
+// WITH_P (first pass) also accumulates P_b = prod (I - 2 mu' x x^T) and
+// max |x|^2.  Reads / writes use the block-interleaved layout (coalesced).
+template <bool WITH_P>
 __global__ void __launch_bounds__(128)
-ddlms_block_kernel(SolveArgs a, Slicer sl, const float* __restrict__ Tstart, float* __restrict__ Pb,
-                   float* __restrict__ maxx2, RunOut o, int64_t b_lo, int64_t b_hi, int use_skip, float soft_tol) {
-    constexpr int NT = 128;
-    constexpr int SEG = 2 * C + 2;
-    constexpr int SEGP = SEG | 1;      // odd float2 stride: conflict-free per-thread reads
-    constexpr int CS = C | 1;
-    static_assert(C == 8, "labels are packed 8 per 64-bit store");
-    extern __shared__ __align__(16) unsigned char dsm[];
-    float2* xs = reinterpret_cast<float2*>(dsm);                  // [2][NT * SEGP]
-    float2* ss = xs + 2 * NT * SEGP;                               // [NT * CS]
-    int* run_s = reinterpret_cast<int*>(ss + NT * CS);             // [NT]
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int64_t bcta = b_lo + int64_t(blockIdx.x) * NT;
-    const int64_t b = bcta + tid;
+ddlms_block_kernel(SolveArgs a, Slicer sl, const float4* __restrict__ XT, const float* __restrict__ Tstart,
+                   float* __restrict__ Pb, float* __restrict__ maxx2, RunOut o, TOut to, int64_t b_lo,
+                   int64_t b_hi, int use_skip, float soft_tol) {
+    __shared__ float2 pts[64];
+    __shared__ uint8_t grid[64];
+    const int tid = threadIdx.x, lane = tid & 31;
+    if (tid < 64) {
+        pts[tid] = sl.pts[tid];
+        grid[tid] = sl.grid[tid];
+    }
+    __syncthreads();
+    LeanSlicer ls;
+    ls.square = sl.kind == 0;
+    ls.m = sl.m;
+    ls.half_norm = 0.5f * sl.norm;
+    ls.off = 0.5f * (sl.m - 1);
+    ls.h = 1.0f / sl.norm;
+    const float thr2 = sl.thr * sl.thr;
+    const int64_t nb = a.nb;
+
+    const int64_t b = b_lo + int64_t(blockIdx.x) * blockDim.x + tid;
     bool run = b < b_hi;
     float T[16];
     if (run) {
@@ -387,155 +452,117 @@ ddlms_block_kernel(SolveArgs a, Slicer sl, const float* __restrict__ Tstart, flo
             run = !(bound < fminf(o.margin[b], soft_tol)) || (a.mu * maxx2[b] > 1.0f);
         }
     }
-    run_s[tid] = run ? 1 : 0;
-    if (!__syncthreads_or(run ? 1 : 0)) return;
-    const int64_t k0 = b * a.B;
-    const int64_t k1 = run ? min(k0 + a.B, a.nsym) : k0;
-    const int nchunk = (a.B + C - 1) / C;
-
-    auto prefetch = [&](int c) {
-        float2* dst = xs + (c & 1) * NT * SEGP;
-        for (int tt = 0; tt < 32; ++tt) {
-            const int t = warp * 32 + tt;
-            if (!run_s[t]) continue;
-            const int64_t bt = bcta + t;
-            const int64_t kb = bt * a.B + int64_t(c) * C;
-            const int64_t ke = min((bt + 1) * a.B, a.nsym);
-            if (kb >= ke) continue;
-            const int n = 2 * static_cast<int>(min(static_cast<int64_t>(C), ke - kb)) + 2;
-            const float2* src = a.x + 2 * kb;
-            if (lane < n) cp_async8(dst + t * SEGP + lane, src + lane);
-            if (lane + 32 < n) cp_async8(dst + t * SEGP + lane + 32, src + lane + 32);
-        }
-        cp_async_commit();
-    };
-
-    float Q[16];
-#pragma unroll
-    for (int i = 0; i < 16; ++i) Q[i] = 0.f;
-    float P[WITH_P ? 64 : 1];
-    if constexpr (WITH_P) {
-#pragma unroll
-        for (int i = 0; i < 64; ++i) P[i] = (i % 9 == 0) ? 1.f : 0.f;
-    }
-    const float tm = 2.0f * a.mu;
-    float mg = 3.0e38f, mx = 0.f;
-    int over = 0;
-    unsigned long long hsh = 1469598103934665603ull;
-
-    prefetch(0);
-    for (int c = 0; c < nchunk; ++c) {
-        if (c + 1 < nchunk) {
-            prefetch(c + 1);
-            cp_async_wait<1>();
-        } else {
-            cp_async_wait<0>();
-        }
-        __syncthreads();
-        // ---- sequential recurrence over this chunk ----
-        const int64_t kc = k0 + int64_t(c) * C;
-        if (run && kc < k1) {
-            const float2* xv = xs + (c & 1) * NT * SEGP + tid * SEGP;
-            unsigned long long packed = 0;
-            const int nk = static_cast<int>(min(static_cast<int64_t>(C), k1 - kc));
-            for (int i = 0; i < nk; ++i) {
-                const int64_t k = kc + i;
-                float X[8];
-#pragma unroll
-                for (int u = 0; u < 4; ++u) {
-                    const float2 v = xv[2 * i + u];
-                    X[2 * u] = v.x * a.scale;
-                    X[2 * u + 1] = v.y * a.scale;
-                }
-                // y = T X and Q X with split accumulators (short dependency chain)
-                float ya = 0.f, yb = 0.f, za = 0.f, zb = 0.f, qa = 0.f, qb = 0.f, wa = 0.f, wb = 0.f;
-#pragma unroll
-                for (int j = 0; j < 8; j += 2) {
-                    ya = fmaf(T[j], X[j], ya);
-                    yb = fmaf(T[j + 1], X[j + 1], yb);
-                    za = fmaf(T[8 + j], X[j], za);
-                    zb = fmaf(T[9 + j], X[j + 1], zb);
-                    qa = fmaf(Q[j], X[j], qa);
-                    qb = fmaf(Q[j + 1], X[j + 1], qb);
-                    wa = fmaf(Q[8 + j], X[j], wa);
-                    wb = fmaf(Q[9 + j], X[j + 1], wb);
-                }
-                const float yr = ya + yb, yi = za + zb, qr = qa + qb, qi = wa + wb;
-                float dr, di;
-                int lab;
-                if (k < a.n_train) {
-                    const float2 t = __ldg(a.train + k);
-                    dr = t.x; di = t.y;
-                    lab = 255;
-                } else {
-                    float m;
-                    lab = slice(sl, yr, yi, m);
-                    mg = fminf(mg, m);
-                    dr = sl.pts[lab].x; di = sl.pts[lab].y;
-                }
-                const float ay = sqrtf(yr * yr + yi * yi);
-                over += (ay > sl.thr) ? 1 : 0;
-                mg = fminf(mg, fabsf(ay - sl.thr));
-                const float er = tm * (dr - yr), ei = tm * (di - yi);
-                const float fr = tm * (dr - qr), fi = tm * (di - qi);
-#pragma unroll
-                for (int j = 0; j < 8; ++j) {
-                    T[j] = fmaf(er, X[j], T[j]);
-                    T[8 + j] = fmaf(ei, X[j], T[8 + j]);
-                    Q[j] = fmaf(fr, X[j], Q[j]);
-                    Q[8 + j] = fmaf(fi, X[j], Q[8 + j]);
-                }
-                if constexpr (WITH_P) {
-                    float n2 = 0.f;
-#pragma unroll
-                    for (int j = 0; j < 8; ++j) n2 = fmaf(X[j], X[j], n2);
-                    mx = fmaxf(mx, n2);
-                    float v[8];
-#pragma unroll
-                    for (int r = 0; r < 8; ++r) {
-                        float sacc = 0.f;
-#pragma unroll
-                        for (int j = 0; j < 8; ++j) sacc = fmaf(P[r * 8 + j], X[j], sacc);
-                        v[r] = sacc * tm;
-                    }
-#pragma unroll
-                    for (int r = 0; r < 8; ++r)
-#pragma unroll
-                        for (int j = 0; j < 8; ++j) P[r * 8 + j] = fmaf(-v[r], X[j], P[r * 8 + j]);
-                }
-                hsh = (hsh ^ static_cast<unsigned long long>(lab)) * 1099511628211ull;
-                packed |= static_cast<unsigned long long>(lab & 0xff) << (8 * i);
-                ss[tid * CS + i] = make_float2(yr, yi);
-            }
-            // labels: C == 8 symbols -> one 8-byte store (chunk-aligned)
-            if (nk == C) *reinterpret_cast<unsigned long long*>(o.labels + kc) = packed;
-            else
-                for (int i = 0; i < nk; ++i) o.labels[kc + i] = static_cast<uint8_t>(packed >> (8 * i));
-        }
-        __syncthreads();
-        // ---- soft outputs, coalesced per thread segment ----
-        for (int tt = 0; tt < 32; ++tt) {
-            const int t = warp * 32 + tt;
-            if (!run_s[t]) continue;
-            const int64_t bt = bcta + t;
-            const int64_t kb = bt * a.B + int64_t(c) * C;
-            const int64_t ke = min((bt + 1) * a.B, a.nsym);
-            if (kb >= ke) continue;
-            const int cnt = static_cast<int>(min(static_cast<int64_t>(C), ke - kb));
-            if (lane < cnt) o.soft[kb + lane] = ss[t * CS + lane];
-        }
-    }
     unsigned long long changed = 0;
     if (run) {
-        changed = (o.hash[b] != hsh) ? 1ull : 0ull;
-        o.hash[b] = hsh;
+        const int64_t k0 = b * a.B;
+        const int nk = static_cast<int>(min(static_cast<int64_t>(a.B), a.nsym - k0));
+        float P[WITH_P ? 64 : 1];
+        if constexpr (WITH_P) {
 #pragma unroll
-        for (int i = 0; i < 16; ++i) {
-            o.Q[b * 16 + i] = Q[i];
-            o.Tused[b * 16 + i] = Tstart[b * 16 + i];
+            for (int i = 0; i < 64; ++i) P[i] = (i % 9 == 0) ? 1.f : 0.f;
         }
-        o.margin[b] = mg;
-        o.over[b] = over;
+        const float tm = 2.0f * a.mu;      // mu' (scale folded in)
+        float mg = 3.0e38f, mx = 0.f, my2 = 0.f;
+        unsigned hsh = 2166136261u;
+        float X[8];
+        const float4* xp = XT + b;
+        {
+            const float4 w = __ldg(xp);
+            X[4] = w.x; X[5] = w.y; X[6] = w.z; X[7] = w.w;
+        }
+        // software pipeline: 4 pair loads in flight
+        float4 q0 = __ldg(xp + 1 * nb), q1 = __ldg(xp + 2 * nb), q2 = __ldg(xp + 3 * nb), q3;
+        for (int i = 0; i < nk; ++i) {
+            q3 = (i + 4 <= a.B) ? __ldg(xp + int64_t(i + 4) * nb) : make_float4(0.f, 0.f, 0.f, 0.f);
+            X[0] = X[4]; X[1] = X[5]; X[2] = X[6]; X[3] = X[7];
+            X[4] = q0.x; X[5] = q0.y; X[6] = q0.z; X[7] = q0.w;
+            q0 = q1; q1 = q2; q2 = q3;
+            const int64_t k = k0 + i;
+            float ya = 0.f, yb = 0.f, za = 0.f, zb = 0.f;
+#pragma unroll
+            for (int j = 0; j < 8; j += 2) {
+                ya = fmaf(T[j], X[j], ya);
+                yb = fmaf(T[j + 1], X[j + 1], yb);
+                za = fmaf(T[8 + j], X[j], za);
+                zb = fmaf(T[9 + j], X[j + 1], zb);
+            }
+            const float yr = ya + yb, yi = za + zb;
+            float dr, di;
+            int lab;
+            if (k < a.n_train) {
+                const float2 t = __ldg(a.train + k);
+                dr = t.x; di = t.y;
+                lab = 255;
+            } else if (ls.square) {
+                const float vr = fmaf(yr, ls.half_norm, ls.off), vi = fmaf(yi, ls.half_norm, ls.off);
+                const int ir = min(max(__float2int_rn(vr), 0), ls.m - 1);
+                const int ii = min(max(__float2int_rn(vi), 0), ls.m - 1);
+                const float fr = vr - static_cast<float>(ir), fi = vi - static_cast<float>(ii);
+                // distance (level units) to the nearest decision boundary
+                const float mr = (ir == 0) ? 0.5f - fr : (ir == ls.m - 1) ? 0.5f + fr : 0.5f - fabsf(fr);
+                const float mi = (ii == 0) ? 0.5f - fi : (ii == ls.m - 1) ? 0.5f + fi : 0.5f - fabsf(fi);
+                mg = fminf(mg, fminf(mr, mi) * (2.0f * ls.h));
+                lab = grid[ir * ls.m + ii];
+                const float2 pp = pts[lab];
+                dr = pp.x; di = pp.y;
+            } else {
+                float m_;
+                lab = slice(sl, yr, yi, m_);
+                mg = fminf(mg, m_);
+                const float2 pp = pts[lab];
+                dr = pp.x; di = pp.y;
+            }
+            my2 = fmaxf(my2, fmaf(yr, yr, yi * yi));
+            const float er = tm * (dr - yr), ei = tm * (di - yi);
+            if constexpr (WITH_P) {
+                float n2 = 0.f;
+#pragma unroll
+                for (int j = 0; j < 8; ++j) n2 = fmaf(X[j], X[j], n2);
+                mx = fmaxf(mx, n2);
+                float v[8];
+#pragma unroll
+                for (int r = 0; r < 8; ++r) {
+                    float sacc = 0.f;
+#pragma unroll
+                    for (int j = 0; j < 8; ++j) sacc = fmaf(P[r * 8 + j], X[j], sacc);
+                    v[r] = sacc * tm;
+                }
+#pragma unroll
+                for (int r = 0; r < 8; ++r)
+#pragma unroll
+                    for (int j = 0; j < 8; ++j) P[r * 8 + j] = fmaf(-v[r], X[j], P[r * 8 + j]);
+            }
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                T[j] = fmaf(er, X[j], T[j]);
+                T[8 + j] = fmaf(ei, X[j], T[8 + j]);
+            }
+            hsh = (hsh ^ static_cast<unsigned>(lab)) * 16777619u;
+            to.ST[int64_t(i) * nb + b] = make_float2(yr, yi);
+            to.LT[int64_t(i) * nb + b] = static_cast<uint8_t>(lab);
+        }
+        changed = (o.hash[b] != static_cast<unsigned long long>(hsh)) ? 1ull : 0ull;
+        o.hash[b] = hsh;
+        // Q_b = T_end - T_start P_b
+        const float* Pm = Pb + b * 64;
+#pragma unroll
+        for (int r = 0; r < 2; ++r)
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                float acc = T[r * 8 + j];
+#pragma unroll
+                for (int i = 0; i < 8; ++i) {
+                    float pij;
+                    if constexpr (WITH_P) pij = P[i * 8 + j];
+                    else pij = __ldg(Pm + i * 8 + j);
+                    acc = fmaf(-Tstart[b * 16 + r * 8 + i], pij, acc);
+                }
+                o.Q[b * 16 + r * 8 + j] = acc;
+            }
+#pragma unroll
+        for (int i = 0; i < 16; ++i) o.Tused[b * 16 + i] = Tstart[b * 16 + i];
+        o.margin[b] = fminf(mg, fabsf(sl.thr - sqrtf(my2)));
+        o.over[b] = my2 > thr2 ? 1 : 0;
         if (b == a.nb - 1) {
 #pragma unroll
             for (int i = 0; i < 16; ++i) o.Tend[i] = T[i];
@@ -865,6 +892,9 @@ Layout plan(int64_t nsym, int B) {
     b += align_up(16 * sizeof(float)) * 2;      // Tend, Tinit
     b += align_up(L.nb * sizeof(int));          // over
     b += align_up(L.nb * sizeof(unsigned long long));   // label hashes
+    b += align_up(size_t(B + 1) * L.nb * 16);            // XT (block-interleaved input)
+    b += align_up(size_t(B) * L.nb * 8);                 // ST
+    b += align_up(size_t(B) * L.nb);                     // LT
     b += align_up(4 * sizeof(unsigned long long));
     L.bytes = b;
     return L;
@@ -912,15 +942,23 @@ extern "C" int kk_ddlms_solve(const void* x, int64_t nsym, float scale, const vo
     float* Tinit_d = reinterpret_cast<float*>(w); w += align_up(16 * sizeof(float));
     int* over = reinterpret_cast<int*>(w); w += align_up(L.nb * sizeof(int));
     unsigned long long* hsh = reinterpret_cast<unsigned long long*>(w); w += align_up(L.nb * 8);
+    float4* XT = reinterpret_cast<float4*>(w); w += align_up(size_t(block + 1) * L.nb * 16);
+    TOut to;
+    to.ST = reinterpret_cast<float2*>(w); w += align_up(size_t(block) * L.nb * 8);
+    to.LT = reinterpret_cast<uint8_t*>(w); w += align_up(size_t(block) * L.nb);
     unsigned long long* ctr = reinterpret_cast<unsigned long long*>(w);
 
+    // the block kernels work on the raw input with the scale folded into the
+    // taps: T' = s T, mu' = mu s^2 (y = T' x_raw exactly as y = T (s x_raw))
     SolveArgs a;
     a.x = static_cast<const float2*>(x);
     a.nsym = nsym;
-    a.scale = scale;
+    a.scale = 1.0f;
     a.train = static_cast<const float2*>(train);
     a.n_train = n_train;
-    a.mu = mu;
+    a.mu = mu * scale * scale;
+    float T_init_s[16];
+    for (int i = 0; i < 16; ++i) T_init_s[i] = T_init[i] * scale;
     a.B = block;
     a.nb = L.nb;
     RunOut o;
@@ -939,7 +977,6 @@ extern "C" int kk_ddlms_solve(const void* x, int64_t nsym, float scale, const vo
     const int top = static_cast<int>(lv.size()) - 1;
     int64_t st[6] = {0, 0, 0, 0, 0, L.nb};
 
-    if (cudaMemsetAsync(labels, 0xFE, nsym, s) != cudaSuccess) return set_cuda_error("labels init");
 
     auto scan = [&](bool with_p) -> int {
         const unsigned wblk = 32 * kScanWarps;
@@ -971,32 +1008,28 @@ extern "C" int kk_ddlms_solve(const void* x, int64_t nsym, float scale, const vo
         fill_T_kernel<<<grid_of((b1 - b0) * 16), th, 0, s>>>(lv[0].T, b0, b1, Tsrc_dev);
         return check_launch("fill_T_kernel");
     };
-    constexpr int kC = 8;
-    const size_t bsm = block_kernel_smem(kC);
-    static bool attr_done = false;
-    if (!attr_done) {
-        if (cudaFuncSetAttribute(ddlms_block_kernel<kC, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 static_cast<int>(bsm)) != cudaSuccess ||
-            cudaFuncSetAttribute(ddlms_block_kernel<kC, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 static_cast<int>(bsm)) != cudaSuccess)
-            return set_cuda_error("ddlms smem attr");
-        attr_done = true;
-    }
     auto run_blocks = [&](bool with_p, int64_t b0, int64_t b1, int use_skip) -> int {
         if (b1 <= b0) return KK_OK;
         const unsigned g = static_cast<unsigned>((b1 - b0 + 127) / 128);
         if (with_p)
-            ddlms_block_kernel<kC, true><<<g, 128, bsm, s>>>(a, sl, lv[0].T, lv[0].P, maxx2, o, b0, b1, 0, soft_tol);
+            ddlms_block_kernel<true><<<g, 128, 0, s>>>(a, sl, XT, lv[0].T, lv[0].P, maxx2, o, to, b0, b1, 0,
+                                                       soft_tol);
         else
-            ddlms_block_kernel<kC, false><<<g, 128, bsm, s>>>(a, sl, lv[0].T, lv[0].P, maxx2, o, b0, b1, use_skip,
-                                                              soft_tol);
+            ddlms_block_kernel<false><<<g, 128, 0, s>>>(a, sl, XT, lv[0].T, lv[0].P, maxx2, o, to, b0, b1, use_skip,
+                                                        soft_tol);
         return check_launch("ddlms_block_kernel");
     };
+    {   // block-interleaved copy of the input
+        dim3 tb(32, 8), tg(static_cast<unsigned>((L.nb + 31) / 32), static_cast<unsigned>((block + 1 + 31) / 32));
+        ddlms_transpose_in<<<tg, tb, 0, s>>>(a.x, nsym, block, L.nb, XT);
+        if (int rc = check_launch("ddlms_transpose_in")) return rc;
+    }
 
     // (2) pure-training blocks are exact from any start: run them, scan to
     //     get the exact training-end taps, speculate everything after.
     const int64_t bt = std::min<int64_t>(n_train / block, L.nb);
-    if (cudaMemcpyAsync(Tinit_d, T_init, 16 * sizeof(float), cudaMemcpyHostToDevice, s) != cudaSuccess)
+    if (cudaMemcpyAsync(Tinit_d, T_init_s, 16 * sizeof(float), cudaMemcpyHostToDevice, s) != cudaSuccess ||
+        cudaStreamSynchronize(s) != cudaSuccess)
         return set_cuda_error("T_init upload");
     if (cudaMemsetAsync(over, 0, L.nb * sizeof(int), s) != cudaSuccess) return set_cuda_error("over init");
     if (cudaMemsetAsync(hsh, 0, L.nb * 8, s) != cudaSuccess) return set_cuda_error("hash init");
@@ -1040,7 +1073,11 @@ extern "C" int kk_ddlms_solve(const void* x, int64_t nsym, float scale, const vo
         }
         if (h[0] == 0) { converged = true; break; }
     }
-    if (!converged) {
+    if (converged) {
+        dim3 tb(32, 8), tg(static_cast<unsigned>((L.nb + 31) / 32), static_cast<unsigned>((block + 31) / 32));
+        ddlms_transpose_out<<<tg, tb, 0, s>>>(to.ST, to.LT, nsym, block, L.nb, static_cast<float2*>(soft), labels);
+        if (int rc = check_launch("ddlms_transpose_out")) return rc;
+    } else {
         // exact fallback: chain every block sequentially from the scanned start
         // taps of block 0 (== T_init)
         st[2] = 2;
@@ -1057,6 +1094,7 @@ extern "C" int kk_ddlms_solve(const void* x, int64_t nsym, float scale, const vo
     if (cudaMemcpyAsync(T_final, Tend, 16 * sizeof(float), cudaMemcpyDeviceToHost, s) != cudaSuccess ||
         cudaStreamSynchronize(s) != cudaSuccess)
         return set_cuda_error("T_final");
+    for (int i = 0; i < 16; ++i) T_final[i] /= scale;
     if (stats)
         for (int i = 0; i < 6; ++i) stats[i] = st[i];
     return KK_OK;

@@ -119,7 +119,7 @@ class GpuOptions:
     ddlms_block: int = 256
     ddlms_frame_symbols: int = 1 << 26
     ddlms_max_iter: int = 64
-    ddlms_soft_tol: float = 1e-6
+    ddlms_soft_tol: float = 1e-5
 
 
 @dataclass
