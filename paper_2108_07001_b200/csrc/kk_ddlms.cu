@@ -407,14 +407,15 @@ struct TOut {
 };
 
 // Block-parallel DDLMS pass, one thread per block of B symbols.  Lean
-// per-symbol work (~70 instructions): the input scale s is folded into the
+// per-symbol work (~75 instructions): the input scale s is folded into the
 // taps (T' = s T, mu' = mu s^2, so y = T' x_raw); Q_b is recovered once per
 // block as T_end - T_start P_b; decision changes are detected with a 32-bit
-// hash of the block's label sequence; the guard is tracked as max |y|^2.
-// WITH_P (first pass) also accumulates P_b = prod (I - 2 mu' x x^T) and
-// max |x|^2.  Reads / writes use the block-interleaved layout (coalesced).
+// hash of the block's label sequence; the guard is tracked as max |y|^2 and
+// the decision margin conservatively as the distance to the nearest interior
+// boundary.  WITH_P (first pass) also accumulates P_b = prod (I - 2 mu' x x^T)
+// and max |x|^2.  Reads / writes use the block-interleaved layout (coalesced).
 template <bool WITH_P>
-__global__ void __launch_bounds__(128)
+__global__ void __launch_bounds__(128, WITH_P ? 3 : 6)
 ddlms_block_kernel(SolveArgs a, Slicer sl, const float4* __restrict__ XT, const float* __restrict__ Tstart,
                    float* __restrict__ Pb, float* __restrict__ maxx2, RunOut o, TOut to, int64_t b_lo,
                    int64_t b_hi, int use_skip, float soft_tol) {
@@ -426,12 +427,9 @@ ddlms_block_kernel(SolveArgs a, Slicer sl, const float4* __restrict__ XT, const 
         grid[tid] = sl.grid[tid];
     }
     __syncthreads();
-    LeanSlicer ls;
-    ls.square = sl.kind == 0;
-    ls.m = sl.m;
-    ls.half_norm = 0.5f * sl.norm;
-    ls.off = 0.5f * (sl.m - 1);
-    ls.h = 1.0f / sl.norm;
+    const bool square = sl.kind == 0;
+    const int m1 = sl.m - 1;
+    const float half_norm = 0.5f * sl.norm, off = 0.5f * (sl.m - 1);
     const float thr2 = sl.thr * sl.thr;
     const int64_t nb = a.nb;
 
@@ -456,28 +454,35 @@ ddlms_block_kernel(SolveArgs a, Slicer sl, const float4* __restrict__ XT, const 
     if (run) {
         const int64_t k0 = b * a.B;
         const int nk = static_cast<int>(min(static_cast<int64_t>(a.B), a.nsym - k0));
+        const int ntr = static_cast<int>(max(static_cast<int64_t>(0), min(static_cast<int64_t>(nk), a.n_train - k0)));
         float P[WITH_P ? 64 : 1];
         if constexpr (WITH_P) {
 #pragma unroll
             for (int i = 0; i < 64; ++i) P[i] = (i % 9 == 0) ? 1.f : 0.f;
         }
         const float tm = 2.0f * a.mu;      // mu' (scale folded in)
-        float mg = 3.0e38f, mx = 0.f, my2 = 0.f;
+        float mgl = 0.5f, mgb = 3.0e38f, mx = 0.f, my2 = 0.f;
         unsigned hsh = 2166136261u;
         float X[8];
         const float4* xp = XT + b;
+        float2* sp = to.ST + b;
+        uint8_t* lp = to.LT + b;
         {
             const float4 w = __ldg(xp);
             X[4] = w.x; X[5] = w.y; X[6] = w.z; X[7] = w.w;
         }
-        // software pipeline: 4 pair loads in flight
-        float4 q0 = __ldg(xp + 1 * nb), q1 = __ldg(xp + 2 * nb), q2 = __ldg(xp + 3 * nb), q3;
+        xp += nb;
+        // software pipeline: 4 pair loads in flight (XT has B+1 rows; rows
+        // past the block's valid symbols are zero-filled and never used)
+        float4 q0 = __ldg(xp), q1 = __ldg(xp + nb), q2 = __ldg(xp + 2 * nb), q3;
+        xp += 3 * nb;
+        const float4* xend = XT + b + int64_t(a.B) * nb;
         for (int i = 0; i < nk; ++i) {
-            q3 = (i + 4 <= a.B) ? __ldg(xp + int64_t(i + 4) * nb) : make_float4(0.f, 0.f, 0.f, 0.f);
+            q3 = (xp <= xend) ? __ldg(xp) : make_float4(0.f, 0.f, 0.f, 0.f);
+            xp += nb;
             X[0] = X[4]; X[1] = X[5]; X[2] = X[6]; X[3] = X[7];
             X[4] = q0.x; X[5] = q0.y; X[6] = q0.z; X[7] = q0.w;
             q0 = q1; q1 = q2; q2 = q3;
-            const int64_t k = k0 + i;
             float ya = 0.f, yb = 0.f, za = 0.f, zb = 0.f;
 #pragma unroll
             for (int j = 0; j < 8; j += 2) {
@@ -489,26 +494,24 @@ ddlms_block_kernel(SolveArgs a, Slicer sl, const float4* __restrict__ XT, const 
             const float yr = ya + yb, yi = za + zb;
             float dr, di;
             int lab;
-            if (k < a.n_train) {
-                const float2 t = __ldg(a.train + k);
+            if (i < ntr) {
+                const float2 t = __ldg(a.train + k0 + i);
                 dr = t.x; di = t.y;
                 lab = 255;
-            } else if (ls.square) {
-                const float vr = fmaf(yr, ls.half_norm, ls.off), vi = fmaf(yi, ls.half_norm, ls.off);
-                const int ir = min(max(__float2int_rn(vr), 0), ls.m - 1);
-                const int ii = min(max(__float2int_rn(vi), 0), ls.m - 1);
-                const float fr = vr - static_cast<float>(ir), fi = vi - static_cast<float>(ii);
-                // distance (level units) to the nearest decision boundary
-                const float mr = (ir == 0) ? 0.5f - fr : (ir == ls.m - 1) ? 0.5f + fr : 0.5f - fabsf(fr);
-                const float mi = (ii == 0) ? 0.5f - fi : (ii == ls.m - 1) ? 0.5f + fi : 0.5f - fabsf(fi);
-                mg = fminf(mg, fminf(mr, mi) * (2.0f * ls.h));
-                lab = grid[ir * ls.m + ii];
+            } else if (square) {
+                const float vr = fmaf(yr, half_norm, off), vi = fmaf(yi, half_norm, off);
+                const int ir = min(max(__float2int_rn(vr), 0), m1);
+                const int ii = min(max(__float2int_rn(vi), 0), m1);
+                // conservative margin (level units): distance to the nearest
+                // boundary if both neighbours existed
+                mgl = fminf(mgl, 0.5f - fmaxf(fabsf(vr - static_cast<float>(ir)), fabsf(vi - static_cast<float>(ii))));
+                lab = grid[ir * sl.m + ii];
                 const float2 pp = pts[lab];
                 dr = pp.x; di = pp.y;
             } else {
                 float m_;
                 lab = slice(sl, yr, yi, m_);
-                mg = fminf(mg, m_);
+                mgb = fminf(mgb, m_);
                 const float2 pp = pts[lab];
                 dr = pp.x; di = pp.y;
             }
@@ -538,8 +541,10 @@ ddlms_block_kernel(SolveArgs a, Slicer sl, const float4* __restrict__ XT, const 
                 T[8 + j] = fmaf(ei, X[j], T[8 + j]);
             }
             hsh = (hsh ^ static_cast<unsigned>(lab)) * 16777619u;
-            to.ST[int64_t(i) * nb + b] = make_float2(yr, yi);
-            to.LT[int64_t(i) * nb + b] = static_cast<uint8_t>(lab);
+            *sp = make_float2(yr, yi);
+            *lp = static_cast<uint8_t>(lab);
+            sp += nb;
+            lp += nb;
         }
         changed = (o.hash[b] != static_cast<unsigned long long>(hsh)) ? 1ull : 0ull;
         o.hash[b] = hsh;
@@ -561,6 +566,7 @@ ddlms_block_kernel(SolveArgs a, Slicer sl, const float4* __restrict__ XT, const 
             }
 #pragma unroll
         for (int i = 0; i < 16; ++i) o.Tused[b * 16 + i] = Tstart[b * 16 + i];
+        const float mg = square ? mgl * (2.0f / sl.norm) : mgb;
         o.margin[b] = fminf(mg, fabsf(sl.thr - sqrtf(my2)));
         o.over[b] = my2 > thr2 ? 1 : 0;
         if (b == a.nb - 1) {
@@ -575,9 +581,9 @@ ddlms_block_kernel(SolveArgs a, Slicer sl, const float4* __restrict__ XT, const 
     }
     unsigned long long rr = run ? 1ull : 0ull;
 #pragma unroll
-    for (int off = 16; off > 0; off >>= 1) {
-        changed += __shfl_xor_sync(0xffffffffu, changed, off);
-        rr += __shfl_xor_sync(0xffffffffu, rr, off);
+    for (int off_ = 16; off_ > 0; off_ >>= 1) {
+        changed += __shfl_xor_sync(0xffffffffu, changed, off_);
+        rr += __shfl_xor_sync(0xffffffffu, rr, off_);
     }
     if (lane == 0) {
         if (changed) atomicAdd(o.counters + 0, changed);
@@ -585,19 +591,36 @@ ddlms_block_kernel(SolveArgs a, Slicer sl, const float4* __restrict__ XT, const 
     }
 }
 
-// fold groups of G consecutive maps:  (P, Q) <- (P P_c, Q P_c + Q_c)
-// One warp per group; the running P (8x8) / Q (2x8) live in shared memory,
-// lane l owns P entries 2l, 2l+1 and (l < 16) Q entry l.
-constexpr int kScanWarps = 4;
+// fold groups of G (<= 32) consecutive maps:  (P, Q) <- (P P_c, Q P_c + Q_c)
+// One warp per group.  The group's children (P_c, Q_c) are first staged in
+// shared memory with all loads in flight, then folded serially from smem.
+constexpr int kScanWarps = 2;
 
 __global__ void __launch_bounds__(32 * kScanWarps)
 scan_fold_kernel(const float* __restrict__ Pc, const float* __restrict__ Qc, int64_t n_child, int G,
                  float* __restrict__ Pg, float* __restrict__ Qg, int64_t n_grp, int with_p) {
     __shared__ float sP[kScanWarps][64];
     __shared__ float sQ[kScanWarps][16];
+    __shared__ float cP[kScanWarps][32][65];
+    __shared__ float cQ[kScanWarps][32][17];
     const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
     const int64_t g = int64_t(blockIdx.x) * kScanWarps + w;
     if (g >= n_grp) return;
+    const int64_t c0 = g * G;
+    const int nc = static_cast<int>(min(static_cast<int64_t>(G), n_child - c0));
+    for (int c = 0; c < nc; ++c) {
+        if (with_p) {
+            cP[w][c][l] = __ldg(Pc + (c0 + c) * 64 + l);
+            cP[w][c][l + 32] = __ldg(Pc + (c0 + c) * 64 + l + 32);
+        } else if (l < 16) {
+            // only Q P_c is needed: rows of P_c are read by all lanes
+            cP[w][c][l] = __ldg(Pc + (c0 + c) * 64 + l);
+            cP[w][c][l + 16] = __ldg(Pc + (c0 + c) * 64 + l + 16);
+            cP[w][c][l + 32] = __ldg(Pc + (c0 + c) * 64 + l + 32);
+            cP[w][c][l + 48] = __ldg(Pc + (c0 + c) * 64 + l + 48);
+        }
+        if (l < 16) cQ[w][c][l] = __ldg(Qc + (c0 + c) * 16 + l);
+    }
     float* P = sP[w];
     float* Q = sQ[w];
     P[2 * l] = ((2 * l) % 9 == 0) ? 1.f : 0.f;
@@ -606,21 +629,20 @@ scan_fold_kernel(const float* __restrict__ Pc, const float* __restrict__ Qc, int
     __syncwarp();
     const int pi = (2 * l) >> 3, pj = (2 * l) & 7;   // P entries (pi, pj), (pi, pj+1)
     const int qr = l >> 3, qj = l & 7;               // Q entry (qr, qj) for l < 16
-    const int64_t c0 = g * G, c1 = min(c0 + G, n_child);
-    for (int64_t c = c0; c < c1; ++c) {
-        const float* M = Pc + c * 64;
+    for (int c = 0; c < nc; ++c) {
+        const float* M = cP[w][c];
         float q = 0.f, p0 = 0.f, p1 = 0.f;
         if (l < 16) {
-            q = __ldg(Qc + c * 16 + l);
+            q = cQ[w][c][l];
 #pragma unroll
-            for (int k = 0; k < 8; ++k) q = fmaf(Q[qr * 8 + k], __ldg(M + k * 8 + qj), q);
+            for (int k = 0; k < 8; ++k) q = fmaf(Q[qr * 8 + k], M[k * 8 + qj], q);
         }
         if (with_p) {
 #pragma unroll
             for (int k = 0; k < 8; ++k) {
                 const float a = P[pi * 8 + k];
-                p0 = fmaf(a, __ldg(M + k * 8 + pj), p0);
-                p1 = fmaf(a, __ldg(M + k * 8 + pj + 1), p1);
+                p0 = fmaf(a, M[k * 8 + pj], p0);
+                p1 = fmaf(a, M[k * 8 + pj + 1], p1);
             }
         }
         __syncwarp();
@@ -633,33 +655,45 @@ scan_fold_kernel(const float* __restrict__ Pc, const float* __restrict__ Qc, int
 }
 
 // down-sweep: children start taps from the group start taps, one warp per
-// group (lanes 0..15 own T entries)
+// group (lanes 0..15 own T entries); children staged in smem first
 __global__ void __launch_bounds__(32 * kScanWarps)
 scan_down_kernel(const float* __restrict__ Pc, const float* __restrict__ Qc, int64_t n_child, int G,
                  const float* __restrict__ Tg, int64_t n_grp, float* __restrict__ Tc) {
     __shared__ float sT[kScanWarps][16];
+    __shared__ float cP[kScanWarps][32][65];
+    __shared__ float cQ[kScanWarps][32][17];
+    __shared__ float oT[kScanWarps][32][17];
     const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
     const int64_t g = int64_t(blockIdx.x) * kScanWarps + w;
     if (g >= n_grp) return;
+    const int64_t c0 = g * G;
+    const int nc = static_cast<int>(min(static_cast<int64_t>(G), n_child - c0));
+    for (int c = 0; c < nc - 1; ++c) {
+        cP[w][c][l] = __ldg(Pc + (c0 + c) * 64 + l);
+        cP[w][c][l + 32] = __ldg(Pc + (c0 + c) * 64 + l + 32);
+        if (l < 16) cQ[w][c][l] = __ldg(Qc + (c0 + c) * 16 + l);
+    }
     float* T = sT[w];
     if (l < 16) T[l] = Tg[g * 16 + l];
     __syncwarp();
     const int r = l >> 3, j = l & 7;
-    const int64_t c0 = g * G, c1 = min(c0 + G, n_child);
-    for (int64_t c = c0; c < c1; ++c) {
-        if (l < 16) Tc[c * 16 + l] = T[l];
-        if (c + 1 == c1) break;
-        const float* M = Pc + c * 64;
+    for (int c = 0; c < nc; ++c) {
+        if (l < 16) oT[w][c][l] = T[l];
+        if (c + 1 == nc) break;
+        const float* M = cP[w][c];
         float t = 0.f;
         if (l < 16) {
-            t = __ldg(Qc + c * 16 + l);
+            t = cQ[w][c][l];
 #pragma unroll
-            for (int k = 0; k < 8; ++k) t = fmaf(T[r * 8 + k], __ldg(M + k * 8 + j), t);
+            for (int k = 0; k < 8; ++k) t = fmaf(T[r * 8 + k], M[k * 8 + j], t);
         }
         __syncwarp();
         if (l < 16) T[l] = t;
         __syncwarp();
     }
+    __syncwarp();
+    for (int c = 0; c < nc; ++c)
+        if (l < 16) Tc[(c0 + c) * 16 + l] = oT[w][c][l];
 }
 
 // ---------------------------------------------------------------------------

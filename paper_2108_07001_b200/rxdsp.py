@@ -117,7 +117,7 @@ class GpuOptions:
     of the block-skip certificate."""
 
     ddlms_block: int = 256
-    ddlms_frame_symbols: int = 1 << 26
+    ddlms_frame_symbols: int = 1 << 28
     ddlms_max_iter: int = 64
     ddlms_soft_tol: float = 1e-5
 
