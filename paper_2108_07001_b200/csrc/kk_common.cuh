@@ -5,12 +5,12 @@
 // * an in-place shared-memory Stockham pass engine: every pass reads all of
 //   its inputs into registers, barriers, butterflies, writes the outputs to
 //   the autosorted positions and barriers again, so one padded buffer
-//   (separate re/im float planes, one pad word per 32) serves all passes.
+//   (float2, one pad slot per 16) serves all passes.
 //   The first pass can read through a functor (global memory, fused
 //   pre-processing) and the last pass can write through a functor (fused
 //   epilogue), so only the middle passes touch shared memory.
-// * a two-level twiddle table for W_32768 (hi[512] x lo[64]) that every
-//   power-of-two FFT up to 32768 points indexes into.
+// * per-size two-level twiddle tables W_M^k = H_M[k>>5] L_M[k&31] for
+//   M = 256..32768 (conflict-free for the lanes of a pass).
 #pragma once
 
 #include <cuda_runtime.h>
@@ -169,14 +169,16 @@ __device__ __forceinline__ void twiddle_powers(float2 w1, float2 (&w)[R]) {
 // ---------------------------------------------------------------------------
 // padded planar shared-memory buffer
 // ---------------------------------------------------------------------------
-__host__ __device__ constexpr int padi(int i) { return i + (i >> 5); }
-__host__ __device__ constexpr int padded(int n) { return n + (n >> 5); }
+// float2 elements with one pad slot per 16: every Stockham access pattern
+// used here (consecutive, stride-R with R = 16, the NS = 16 scatter) maps the
+// 16 lanes of each LDS.64/STS.64 wavefront to 16 distinct bank pairs.
+__host__ __device__ constexpr int padi(int i) { return i + (i >> 4); }
+__host__ __device__ constexpr int padded(int n) { return n + (n >> 4); }
 
 struct SmemPlanes {
-    float* re;
-    float* im;
-    __device__ __forceinline__ float2 ld(int i) const { const int p = padi(i); return make_float2(re[p], im[p]); }
-    __device__ __forceinline__ void st(int i, float2 v) const { const int p = padi(i); re[p] = v.x; im[p] = v.y; }
+    float2* d;
+    __device__ __forceinline__ float2 ld(int i) const { return d[padi(i)]; }
+    __device__ __forceinline__ void st(int i, float2 v) const { d[padi(i)] = v; }
 };
 
 struct LoadPlanes {
@@ -195,13 +197,15 @@ struct StorePlanes {
 template <int N, int R, int NT>
 struct PassShape {
     static constexpr int NB = N / R;
-    static_assert(NB % NT == 0, "butterflies must split evenly over threads");
-    static constexpr int BPT = NB / NT;
+    static_assert(NB % NT == 0 || NT % NB == 0, "butterflies must split evenly over threads");
+    static constexpr int BPT = NB >= NT ? NB / NT : 1;
+    static constexpr bool PARTIAL = NB < NT;   // threads tid >= NB idle in this pass
 };
 
 template <int N, int R, int NT, class Load>
 __device__ __forceinline__ void stockham_load(int tid, const Load& load, float2 (&v)[PassShape<N, R, NT>::BPT][R]) {
     constexpr int NB = PassShape<N, R, NT>::NB;
+    if (PassShape<N, R, NT>::PARTIAL && tid >= NB) return;
 #pragma unroll
     for (int q = 0; q < PassShape<N, R, NT>::BPT; ++q) {
         const int j = tid + q * NT;
@@ -213,10 +217,24 @@ __device__ __forceinline__ void stockham_load(int tid, const Load& load, float2 
 template <int N, int R, int NS, int NT, bool INV, int NBF = PassShape<N, R, NT>::BPT, class Store>
 __device__ __forceinline__ void stockham_compute_store(int tid, const Twiddle& tw, float2 (&v)[NBF][R],
                                                        const Store& store) {
+    if (PassShape<N, R, NT>::PARTIAL && tid >= PassShape<N, R, NT>::NB) return;
+    // when NT is a multiple of NS every butterfly of this thread has the same
+    // twiddle index (j % NS == tid % NS): build the chain once, apply to all
+    constexpr bool kShared = (NS > 1) && (NT % NS == 0) && (NBF > 1);
+    if constexpr (kShared) {
+        const float2 w1 = tw.template w<NS * R>(tid % NS);
+        float2 wr = w1;
+#pragma unroll
+        for (int r = 1; r < R; ++r) {
+#pragma unroll
+            for (int q = 0; q < NBF; ++q) v[q][r] = INV ? cmulc(v[q][r], wr) : cmul(v[q][r], wr);
+            if (r + 1 < R) wr = cmul(wr, w1);
+        }
+    }
 #pragma unroll
     for (int q = 0; q < NBF; ++q) {
         const int j = tid + q * NT;
-        if constexpr (NS > 1) {
+        if constexpr (NS > 1 && !kShared) {
             // w_r = w1^r by a running product (2 live registers; error <= R ulp)
             const float2 w1 = tw.template w<NS * R>(j % NS);
             float2 wr = w1;
@@ -246,6 +264,7 @@ __device__ __forceinline__ void stockham_pass(int tid, const Twiddle& tw, const 
         stockham_compute_store<N, R, NS, NT, INV>(tid, tw, v, store);
     } else {
         constexpr int NB = PassShape<N, R, NT>::NB;
+        if (PassShape<N, R, NT>::PARTIAL && tid >= NB) return;
 #pragma unroll 1
         for (int q = 0; q < PassShape<N, R, NT>::BPT; ++q) {
             float2 v[1][R];

@@ -16,7 +16,7 @@
 // FFT (the multiplier is Hermitian, so the two real results separate
 // exactly).  A 256-thread CTA runs 4 pairs = 8 output hops and stages the 9
 // hops of u/amp it needs once in shared memory.  FFT = Stockham radix
-// 16x16x4 in padded planar smem; the inverse FFT's last pass writes the field
+// 16x16x4 in padded float2 smem; the inverse FFT's last pass writes the field
 // straight to HBM (coalesced) with the rotation/mirror and the hop sums fused.
 #include "kk_common.cuh"
 #include "kk_internal.h"
@@ -29,13 +29,12 @@ constexpr int kPairsPerCta = 4;
 constexpr int kGroupThreads = 64;
 constexpr int kK1Threads = kPairsPerCta * kGroupThreads;      // 256
 constexpr int kStageHops = 2 * kPairsPerCta + 1;              // 9
-constexpr int kPlane1 = padded(kN1);                          // 1056 floats
+constexpr int kPlane1 = padded(kN1);                          // 1088 float2
 
 struct K1Smem {
     float u[kStageHops * kHop];
     float a[kStageHops * kHop];
-    float re[kPairsPerCta][kPlane1];
-    float im[kPairsPerCta][kPlane1];
+    float2 buf[kPairsPerCta][kPlane1];
     float2 tw[kTwEntries];
     float2 red[kK1Threads / 32][2];
     int dead[kStageHops];
@@ -158,7 +157,7 @@ kk_pairs_kernel(const TIn* __restrict__ in, float in_scale, float clamp_rel, int
     const int64_t hop_a = 2 * pair;          // output hop of the real-part block
     const bool active = hop_a < n_hops;
     const Twiddle tw{S.tw};
-    SmemPlanes P{S.re[g], S.im[g]};
+    SmemPlanes P{S.buf[g]};
     const float* ua = S.u + (2 * g) * kHop;          // block a: stage hops 2g, 2g+1
     const float* ub = S.u + (2 * g + 1) * kHop;      // block b: stage hops 2g+1, 2g+2
 

@@ -16,7 +16,7 @@
 //   kept bins of E/O are their low and high quarters -> 8192 each
 //   A = IFFT8192(E_kept * H_even), B = IFFT8192(O_kept * H_odd)
 //   out[r] = (A[r] - W16384^{-r} B[r]) * 0.5/16384
-// One 512-thread CTA per block: 132 KB padded planar FFT buffer + 64 KB for A.
+// One 512-thread CTA per block: 136 KB padded float2 FFT buffer + 64 KB for A.
 // The first pass of each FFT16384 reads HBM directly (coalesced) with the
 // carrier subtraction / pre-twiddle fused, the IFFT's first pass applies the
 // kept-bin gather and H, and the final IFFT pass writes the 2-sps output
@@ -32,12 +32,11 @@ constexpr int kNS = 32768;        // static block
 constexpr int kHopS = 16384;      // hop / half FFT
 constexpr int kNOut = 8192;       // outputs per block
 constexpr int kK2Threads = 512;
-constexpr int kPlane2 = padded(kHopS);   // 16896 floats
+constexpr int kPlane2 = padded(kHopS);   // 17408 float2
 constexpr int kRotMax = 1024;            // rotation-table entries held in smem
 
 struct K2Smem {
-    float re[kPlane2];
-    float im[kPlane2];
+    float2 buf[kPlane2];
     float2 A[kNOut];
     float2 tw[kTwEntries];
     float2 rot[kRotMax];
@@ -174,7 +173,7 @@ __global__ void __launch_bounds__(kK2Threads, 1) static_blocks_kernel(K2Params p
     __syncthreads();
 
     const Twiddle tw{S.tw};
-    const SmemPlanes P{S.re, S.im};
+    const SmemPlanes P{S.buf};
     const int64_t hb = p.hb0 + blockIdx.x;
     const int64_t base = (hb - 1) * kHopS;   // global index of block sample 0
     const BlockIn bi = make_block_in(p, base);
@@ -194,7 +193,7 @@ __global__ void __launch_bounds__(kK2Threads, 1) static_blocks_kernel(K2Params p
     for (int chain = 0; chain < 2; ++chain) {
         // ---- FFT16384 of a = x0 + x1 (even bins) or b = (x0 - x1) W^n (odd) ----
 #pragma unroll 1
-        for (int q = 0; q < 2; ++q) {
+        for (int q = 0; q < kHopS / 16 / kK2Threads; ++q) {
             float2 v[1][16];
             const int j = tid + q * kK2Threads;
             if (chain == 0) k2_load_bfly<0, FAST>(p, bi, S.rot, tw, j, mA, mB, bnd, s1024, s16384, v);
