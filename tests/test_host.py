@@ -1,0 +1,131 @@
+"""Host-side logic of the drop-in package (no GPU): constellation tables and
+slicer descriptors, plans/config validation, receive-tap design (checked
+against the taps the reference designed for each golden capture), metrics
+helpers and super-frame planning."""
+
+import numpy as np
+import pytest
+
+from oracle import kkoracle as ko
+from paper_2108_07001_b200 import rxdsp
+from paper_2108_07001_b200.captures import list_captures, load_capture
+from paper_2108_07001_b200.constellation import make_constellation, slicer_tables
+from paper_2108_07001_b200.metrics import frame_sync, q_from_ber, windowed_q
+from paper_2108_07001_b200.sigcore import BlockPlan, FirFilter, ParameterError, RealSignal
+from paper_2108_07001_b200.superframe import HALO_SAMPLES, plan_superframe
+
+
+@pytest.mark.parametrize("order", [4, 8, 16, 32, 64])
+def test_constellations_match_oracle(order):
+    a, b = make_constellation(order), ko.constellation(order)
+    assert np.array_equal(a.points, b.points) and np.array_equal(a.labels, b.labels)
+
+
+@pytest.mark.parametrize("order", [4, 16, 64])
+def test_square_slicer_grid(order):
+    tb = slicer_tables(order)
+    assert tb.grid_m == int(np.sqrt(order))
+    pts = make_constellation(order).points
+    rng = np.random.default_rng(order)
+    y = (rng.standard_normal(5000) + 1j * rng.standard_normal(5000)) * 1.2
+    # the separable rule used on the GPU == the reference's argmin
+    v_r = np.clip(np.rint(y.real * tb.norm / 2 + (tb.grid_m - 1) / 2), 0, tb.grid_m - 1).astype(int)
+    v_i = np.clip(np.rint(y.imag * tb.norm / 2 + (tb.grid_m - 1) / 2), 0, tb.grid_m - 1).astype(int)
+    sep = tb.grid[v_r * tb.grid_m + v_i]
+    brute = np.argmin(np.abs(y[:, None] - pts[None, :]), axis=1)
+    assert np.array_equal(sep, brute)
+
+
+def test_non_square_use_brute_force():
+    for order in (8, 32):
+        assert slicer_tables(order).grid_m == 0
+
+
+def test_plans_and_config_validation():
+    assert BlockPlan(1024, buffer_len=1 << 22).blocks_per_buffer == 8192
+    with pytest.raises(ParameterError):
+        BlockPlan(1000)
+    with pytest.raises(ParameterError):
+        rxdsp.RxPipelineConfig(baud_hz=2e9)
+    with pytest.raises(ParameterError):
+        rxdsp.RxPipelineConfig(static_taps=FirFilter(np.ones(4), 2e9))
+
+
+def test_stream_buffers():
+    plan = BlockPlan(1024, buffer_len=4096)
+    bufs = list(rxdsp.stream_buffers(RealSignal(np.ones(5000), 4e9), plan))
+    assert len(bufs) == 2
+    assert bufs[1]["n_padding"] == 4096 - (5000 - 4096)
+    assert np.array_equal(bufs[0]["tail"], np.zeros(512))
+    with pytest.raises(ParameterError):
+        list(rxdsp.stream_buffers(RealSignal(np.ones(100), 4e9), plan))
+
+
+class _NS:
+    def __init__(self, **kw):
+        self.__dict__.update(kw)
+
+
+def _link_tx_fe(meta):
+    c = meta["config"]
+    L = c["link"]
+    link = _NS(total_dispersion_ps_nm=L["n_spans"] * L["span_length_km"] * L["dispersion_ps_nm_km"],
+               center_wavelength_nm=L["center_wavelength_nm"])
+    tx = _NS(**{k: c["tx"][k] for k in ("baud_hz", "rolloff", "pulse_span_symbols", "tone_freq_hz")})
+    fe = _NS(**{k: c["frontend"][k] for k in ("pd_bandwidth_hz", "pd_filter_order", "adc_analog_bandwidth_hz",
+                                               "adc_aa_order")})
+    return link, tx, fe
+
+
+@pytest.mark.parametrize("name", ["c1_qpsk_b2b", "c4_qpsk_10000km_cspr10", "c3_64qam_1600km_rel-20"])
+def test_receive_tap_design_matches_reference(name):
+    cap = load_capture(name)
+    link, tx, fe = _link_tx_fe(cap.meta)
+    fir = rxdsp.design_receive_taps(link, tx, frontend=fe, n_taps=203, rate_hz=2e9)
+    assert np.max(np.abs(fir.taps - cap.taps)) < 1e-9 * np.max(np.abs(cap.taps))
+
+
+def test_compute_static_taps_zero_link_is_delta():
+    fir = rxdsp.compute_static_taps(_NS(total_dispersion_ps_nm=0.0, center_wavelength_nm=1550.0))
+    c = len(fir.taps) // 2
+    assert abs(fir.taps[c] - 1) < 1e-6 and np.max(np.abs(np.delete(fir.taps, c))) < 1e-6
+    with pytest.raises(ParameterError):
+        rxdsp.compute_static_taps(_NS(total_dispersion_ps_nm=0.0, center_wavelength_nm=1550.0), n_taps=202)
+
+
+def test_static_response_matches_oracle():
+    cap = load_capture("c4_qpsk_10000km_cspr10")
+    kept, h = rxdsp._static_response(FirFilter(cap.taps, 2e9), BlockPlan(32768), 4e9, 0.01, 8192)
+    k2, h2 = ko.static_response(cap.taps, 2e9, 32768, 4e9, 0.01, 8192)
+    assert np.array_equal(kept, k2) and np.max(np.abs(h - h2)) < 1e-12
+
+
+def test_metrics_helpers():
+    assert q_from_ber(0) == np.inf
+    assert q_from_ber(1e-3) == pytest.approx(ko.q_from_ber(1e-3))
+    rng = np.random.default_rng(1)
+    tx = rng.integers(0, 2, 1 << 15).astype(np.uint8)
+    rx = tx[1000:20000].copy()
+    off, a, b = frame_sync(rx, tx)
+    assert off == 1000 and np.array_equal(a, b)
+    q = windowed_q(np.zeros(10000, np.uint8), 1e6, 0.001)
+    assert len(q) == 10 and all(v == q_from_ber(1e-3) for _, v in q)
+
+
+def test_superframe_planning():
+    n = 1 << 30
+    jobs = [plan_superframe(r, 4, n) for r in range(4)]
+    assert jobs[0].load_start == 0 and jobs[-1].load_end == 4 * n
+    for j in jobs[1:]:
+        assert j.core_start - j.load_start == HALO_SAMPLES
+        assert j.load_start % 65536 == 0
+    assert all(a.core_end == b.core_start for a, b in zip(jobs, jobs[1:]))
+
+
+def test_captures_index():
+    names = list_captures()
+    assert "c5_qpsk_10000km_tile" in names
+    cap = load_capture("c1_qpsk_b2b")
+    assert cap.adc_h.dtype == np.int16 and np.all(cap.adc_h % 2 != 0)
+    cfg = cap.pipeline_config()
+    assert cfg.static_taps is not None and cfg.constellation_order == 4
