@@ -119,9 +119,9 @@ int kk_ddlms_sequential(const void *x, int64_t n_out, float scale, int n_taps, c
  * the certified fixpoint).  T_init_host / T_final_host: float[16], the WL
  * taps in real 2x8 form.  stats_host[6] = {iterations, blocks re-run,
  * fallback (0 none, 1 guard exceeded -> caller re-runs sequentially,
- * 2 not converged -> chained), guard exceedances, changed decisions in the
- * last iteration, blocks, then for iterations 1..16: (changed, re-run)}:
- * the buffer must hold 38 int64.
+ * 2 not converged -> chained), guard exceedances, changed blocks in the
+ * last iteration, blocks, then for iterations 1..16: (changed blocks,
+ * re-run blocks)}: the buffer must hold 38 int64.
  */
 size_t kk_ddlms_workspace_bytes(int64_t nsym, int block);
 int kk_ddlms_solve(const void *x, int64_t nsym, float scale, const void *train, int64_t n_train,
@@ -130,6 +130,28 @@ int kk_ddlms_solve(const void *x, int64_t nsym, float scale, const void *train, 
                    float mu, int block, int max_iter, float soft_tol, uint8_t *labels, void *soft,
                    float *T_final_host, void *workspace, size_t ws_bytes, int64_t *stats_host,
                    void *stream);
+
+/*
+ * K4 as a phased solver over one frame, so frames on different GPUs can be
+ * chained exactly (superframe sharding): the host exchanges
+ * frame maps (P, Q) -- T_end = T_start P + Q, map_host = float[64 + 16] --
+ * between ranks.  kk_ddlms_create carves the caller's workspace
+ * (kk_ddlms_workspace_bytes) and returns an opaque handle (NULL on error).
+ *   train(T_start)      exact pure-training blocks -> training-end taps
+ *   speculate(T_guess)  first pass of the decision-directed blocks -> map
+ *   iterate(T_start)    exact frame-start taps: re-run, changed blocks -> map
+ *   finish              labels / soft / end taps / guard exceedances
+ */
+void *kk_ddlms_create(const void *x, int64_t nsym, float scale, const void *train, int64_t n_train, int order,
+                      const float *pts_host, const uint8_t *grid_host, int grid_m, float norm, float max_radius,
+                      float guard_factor, float mu, int block, float soft_tol, void *workspace, size_t ws_bytes,
+                      void *stream);
+int kk_ddlms_train(void *solver, const float *T_start_host, float *T_train_end_host);
+int kk_ddlms_speculate(void *solver, const float *T_guess_host, float *map_host);
+int kk_ddlms_iterate(void *solver, const float *T_start_host, int64_t *changed_blocks, int64_t *rerun_blocks,
+                     float *map_host);
+int kk_ddlms_finish(void *solver, uint8_t *labels, void *soft, float *T_final_host, int64_t *guard_exceed);
+void kk_ddlms_destroy(void *solver);
 
 /*
  * BER -- replaces demap (rxdsp.py:548-567) + the XOR count of

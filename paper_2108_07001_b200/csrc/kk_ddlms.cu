@@ -940,109 +940,109 @@ extern "C" size_t kk_ddlms_workspace_bytes(int64_t nsym, int block) {
     return plan(nsym, block).bytes;
 }
 
-// Exact block-parallel WL DDLMS (4 taps) over nsym symbols.
-//   T_init: host float[16] (real form).  Outputs: labels (255 on training
-//   symbols), soft, T_final (host float[16]).  stats (host int64[6]):
-//   iterations, blocks re-run, fallback (0 none, 1 guard, 2 not converged),
-//   guard exceedances, changed decisions in the last iteration, blocks.
-extern "C" int kk_ddlms_solve(const void* x, int64_t nsym, float scale, const void* train, int64_t n_train,
-                              const float* T_init, int order, const float* pts_host, const uint8_t* grid_host,
-                              int grid_m, float norm, float max_radius, float guard_factor, int guard_run,
-                              float mu, int block, int max_iter, float soft_tol, uint8_t* labels, void* soft,
-                              float* T_final, void* workspace, size_t ws_bytes, int64_t* stats, void* stream) {
-    clear_error();
-    cudaStream_t s = static_cast<cudaStream_t>(stream);
-    if (nsym <= 0) return KK_OK;
-    if (block <= 0) return set_error(KK_ERR_PARAM, "block must be positive");
-    if (order < 2 || order > 64) return set_error(KK_ERR_PARAM, "constellation order must be <= 64");
-    Layout L = plan(nsym, block);
-    if (ws_bytes < L.bytes) return set_error(KK_ERR_PARAM, "workspace too small");
-    Slicer sl = make_slicer(order, pts_host, grid_host, grid_m, norm, max_radius, guard_factor);
-
-    // carve the workspace
-    char* w = static_cast<char*>(workspace);
-    std::vector<Level> lv(L.n.size());
-    for (size_t l = 0; l < L.n.size(); ++l) {
-        lv[l].n = L.n[l];
-        lv[l].P = reinterpret_cast<float*>(w);
-        lv[l].Q = lv[l].P + L.n[l] * 64;
-        lv[l].T = lv[l].Q + L.n[l] * 16;
-        w += align_up(L.n[l] * 96 * sizeof(float));
-    }
-    float* Tused = reinterpret_cast<float*>(w); w += align_up(L.nb * 16 * sizeof(float));
-    float* margin = reinterpret_cast<float*>(w); w += align_up(L.nb * sizeof(float));
-    float* maxx2 = reinterpret_cast<float*>(w); w += align_up(L.nb * sizeof(float));
-    float* Tend = reinterpret_cast<float*>(w); w += align_up(16 * sizeof(float));
-    float* Tinit_d = reinterpret_cast<float*>(w); w += align_up(16 * sizeof(float));
-    int* over = reinterpret_cast<int*>(w); w += align_up(L.nb * sizeof(int));
-    unsigned long long* hsh = reinterpret_cast<unsigned long long*>(w); w += align_up(L.nb * 8);
-    float4* XT = reinterpret_cast<float4*>(w); w += align_up(size_t(block + 1) * L.nb * 16);
-    TOut to;
-    to.ST = reinterpret_cast<float2*>(w); w += align_up(size_t(block) * L.nb * 8);
-    to.LT = reinterpret_cast<uint8_t*>(w); w += align_up(size_t(block) * L.nb);
-    unsigned long long* ctr = reinterpret_cast<unsigned long long*>(w);
-
-    // the block kernels work on the raw input with the scale folded into the
-    // taps: T' = s T, mu' = mu s^2 (y = T' x_raw exactly as y = T (s x_raw))
+// ---------------------------------------------------------------------------
+// DdlmsSolver: exact block-parallel WL DDLMS (4 taps) over one frame of nsym
+// symbols, in phases so that frames on different GPUs can be chained by a
+// host-side exchange of their composed affine maps (superframe / multirank):
+//   train(T_start)      pure-training blocks (exact from any start) -> exact
+//                       training-end taps
+//   speculate(T_guess)  first pass of every decision-directed block from the
+//                       guess, fused with the block maps P_b -> frame map
+//   iterate(T_start)    exact frame start taps: scan, re-run blocks whose start
+//                       moved beyond their certified margin, count changed
+//                       blocks -> frame map
+//   finish()            outputs (labels, soft), end taps, guard check
+// A frame map (P, Q) means T_end = T_start P + Q (host float[64 + 16]).
+// ---------------------------------------------------------------------------
+namespace {
+struct DdlmsSolver {
+    cudaStream_t s;
+    Layout L;
+    std::vector<Level> lv;
+    int top;
+    Slicer sl;
     SolveArgs a;
-    a.x = static_cast<const float2*>(x);
-    a.nsym = nsym;
-    a.scale = 1.0f;
-    a.train = static_cast<const float2*>(train);
-    a.n_train = n_train;
-    a.mu = mu * scale * scale;
-    float T_init_s[16];
-    for (int i = 0; i < 16; ++i) T_init_s[i] = T_init[i] * scale;
-    a.B = block;
-    a.nb = L.nb;
     RunOut o;
-    o.labels = labels;
-    o.soft = static_cast<float2*>(soft);
-    o.Q = lv[0].Q;
-    o.Tused = Tused;
-    o.margin = margin;
-    o.Tend = Tend;
-    o.over = over;
-    o.hash = hsh;
-    o.counters = ctr;
+    TOut to;
+    float scale, soft_tol;
+    float *Tused, *margin, *maxx2, *Tend, *Tinit_d;
+    int* over;
+    unsigned long long *hsh, *ctr;
+    float4* XT;
+    int64_t bt = 0;
+    bool speculated = false;
+    int64_t iters = 0, reruns = 0, last_changed = 0;
 
-    const int th = 128;
-    auto grid_of = [&](int64_t n) { return static_cast<unsigned>((n + th - 1) / th); };
-    const int top = static_cast<int>(lv.size()) - 1;
-    int64_t st[6] = {0, 0, 0, 0, 0, L.nb};
-
-
-    auto scan = [&](bool with_p) -> int {
+    int scan_up(bool with_p) {
         const unsigned wblk = 32 * kScanWarps;
-        auto wgrid = [&](int64_t n) { return static_cast<unsigned>((n + kScanWarps - 1) / kScanWarps); };
         for (int l = 1; l <= top; ++l) {
-            scan_fold_kernel<<<wgrid(lv[l].n), wblk, 0, s>>>(lv[l - 1].P, lv[l - 1].Q, lv[l - 1].n, kG, lv[l].P,
-                                                             lv[l].Q, lv[l].n, with_p ? 1 : 0);
+            const unsigned g = static_cast<unsigned>((lv[l].n + kScanWarps - 1) / kScanWarps);
+            scan_fold_kernel<<<g, wblk, 0, s>>>(lv[l - 1].P, lv[l - 1].Q, lv[l - 1].n, kG, lv[l].P, lv[l].Q,
+                                                lv[l].n, with_p ? 1 : 0);
             if (int rc = check_launch("scan_fold_kernel")) return rc;
         }
-        // top level: one warp folds the <= kG top entries from T_init
-        scan_down_kernel<<<1, wblk, 0, s>>>(lv[top].P, lv[top].Q, lv[top].n, static_cast<int>(lv[top].n), Tinit_d,
-                                            1, lv[top].T);
+        return KK_OK;
+    }
+    int scan_down() {   // from Tinit_d (frame start, scaled)
+        const unsigned wblk = 32 * kScanWarps;
+        scan_down_kernel<<<1, wblk, 0, s>>>(lv[top].P, lv[top].Q, lv[top].n, static_cast<int>(lv[top].n), Tinit_d, 1,
+                                            lv[top].T);
         if (int rc = check_launch("scan_down_kernel")) return rc;
         for (int l = top; l >= 1; --l) {
-            scan_down_kernel<<<wgrid(lv[l].n), wblk, 0, s>>>(lv[l - 1].P, lv[l - 1].Q, lv[l - 1].n, kG, lv[l].T,
-                                                             lv[l].n, lv[l - 1].T);
+            const unsigned g = static_cast<unsigned>((lv[l].n + kScanWarps - 1) / kScanWarps);
+            scan_down_kernel<<<g, wblk, 0, s>>>(lv[l - 1].P, lv[l - 1].Q, lv[l - 1].n, kG, lv[l].T, lv[l].n,
+                                                lv[l - 1].T);
             if (int rc = check_launch("scan_down_kernel")) return rc;
         }
         return KK_OK;
-    };
-    auto read_ctr = [&](unsigned long long (&h)[4]) -> int {
-        if (cudaMemcpyAsync(h, ctr, sizeof(h), cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+    }
+    // frame map from the top-level aggregates (host fold), unscaled Q
+    int frame_map(float* agg) {
+        if (!agg) return KK_OK;
+        const int64_t n = lv[top].n;
+        std::vector<float> P(n * 64), Q(n * 16);
+        if (cudaMemcpyAsync(P.data(), lv[top].P, P.size() * 4, cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+            cudaMemcpyAsync(Q.data(), lv[top].Q, Q.size() * 4, cudaMemcpyDeviceToHost, s) != cudaSuccess ||
             cudaStreamSynchronize(s) != cudaSuccess)
-            return set_cuda_error("counter readback");
+            return set_cuda_error("frame map readback");
+        double Pa[64], Qa[16];
+        for (int i = 0; i < 64; ++i) Pa[i] = (i % 9 == 0) ? 1.0 : 0.0;
+        for (int i = 0; i < 16; ++i) Qa[i] = 0.0;
+        for (int64_t g = 0; g < n; ++g) {
+            double nP[64], nQ[16];
+            for (int r = 0; r < 8; ++r)
+                for (int j = 0; j < 8; ++j) {
+                    double acc = 0.0;
+                    for (int k = 0; k < 8; ++k) acc += Pa[r * 8 + k] * P[g * 64 + k * 8 + j];
+                    nP[r * 8 + j] = acc;
+                }
+            for (int r = 0; r < 2; ++r)
+                for (int j = 0; j < 8; ++j) {
+                    double acc = Q[g * 16 + r * 8 + j];
+                    for (int k = 0; k < 8; ++k) acc += Qa[r * 8 + k] * P[g * 64 + k * 8 + j];
+                    nQ[r * 8 + j] = acc;
+                }
+            for (int i = 0; i < 64; ++i) Pa[i] = nP[i];
+            for (int i = 0; i < 16; ++i) Qa[i] = nQ[i];
+        }
+        for (int i = 0; i < 64; ++i) agg[i] = static_cast<float>(Pa[i]);
+        for (int i = 0; i < 16; ++i) agg[64 + i] = static_cast<float>(Qa[i] / scale);
         return KK_OK;
-    };
-    auto fill_T = [&](int64_t b0, int64_t b1, const float* Tsrc_dev) -> int {
+    }
+    int set_start(const float* T_host) {
+        float Ts[16];
+        for (int i = 0; i < 16; ++i) Ts[i] = T_host[i] * scale;
+        if (cudaMemcpyAsync(Tinit_d, Ts, sizeof(Ts), cudaMemcpyHostToDevice, s) != cudaSuccess ||
+            cudaStreamSynchronize(s) != cudaSuccess)
+            return set_cuda_error("T upload");
+        return KK_OK;
+    }
+    int fill_T(int64_t b0, int64_t b1, const float* src_dev) {
         if (b1 <= b0) return KK_OK;
-        fill_T_kernel<<<grid_of((b1 - b0) * 16), th, 0, s>>>(lv[0].T, b0, b1, Tsrc_dev);
+        fill_T_kernel<<<static_cast<unsigned>(((b1 - b0) * 16 + 127) / 128), 128, 0, s>>>(lv[0].T, b0, b1, src_dev);
         return check_launch("fill_T_kernel");
-    };
-    auto run_blocks = [&](bool with_p, int64_t b0, int64_t b1, int use_skip) -> int {
+    }
+    int run_blocks(bool with_p, int64_t b0, int64_t b1, int use_skip) {
         if (b1 <= b0) return KK_OK;
         const unsigned g = static_cast<unsigned>((b1 - b0 + 127) / 128);
         if (with_p)
@@ -1052,83 +1052,267 @@ extern "C" int kk_ddlms_solve(const void* x, int64_t nsym, float scale, const vo
             ddlms_block_kernel<false><<<g, 128, 0, s>>>(a, sl, XT, lv[0].T, lv[0].P, maxx2, o, to, b0, b1, use_skip,
                                                         soft_tol);
         return check_launch("ddlms_block_kernel");
-    };
-    {   // block-interleaved copy of the input
+    }
+    int read_ctr(unsigned long long (&h)[4]) {
+        if (cudaMemcpyAsync(h, ctr, sizeof(h), cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+            cudaStreamSynchronize(s) != cudaSuccess)
+            return set_cuda_error("counter readback");
+        return KK_OK;
+    }
+
+    int init(const void* x, int64_t nsym, float scale_, const void* train, int64_t n_train, Slicer sl_, float mu,
+             int block, float soft_tol_, void* workspace, size_t ws_bytes, cudaStream_t s_) {
+        s = s_;
+        sl = sl_;
+        scale = scale_;
+        soft_tol = soft_tol_;
+        L = plan(nsym, block);
+        if (ws_bytes < L.bytes) return set_error(KK_ERR_PARAM, "workspace too small");
+        char* w = static_cast<char*>(workspace);
+        lv.resize(L.n.size());
+        for (size_t l = 0; l < L.n.size(); ++l) {
+            lv[l].n = L.n[l];
+            lv[l].P = reinterpret_cast<float*>(w);
+            lv[l].Q = lv[l].P + L.n[l] * 64;
+            lv[l].T = lv[l].Q + L.n[l] * 16;
+            w += align_up(L.n[l] * 96 * sizeof(float));
+        }
+        top = static_cast<int>(lv.size()) - 1;
+        Tused = reinterpret_cast<float*>(w); w += align_up(L.nb * 16 * sizeof(float));
+        margin = reinterpret_cast<float*>(w); w += align_up(L.nb * sizeof(float));
+        maxx2 = reinterpret_cast<float*>(w); w += align_up(L.nb * sizeof(float));
+        Tend = reinterpret_cast<float*>(w); w += align_up(16 * sizeof(float));
+        Tinit_d = reinterpret_cast<float*>(w); w += align_up(16 * sizeof(float));
+        over = reinterpret_cast<int*>(w); w += align_up(L.nb * sizeof(int));
+        hsh = reinterpret_cast<unsigned long long*>(w); w += align_up(L.nb * 8);
+        XT = reinterpret_cast<float4*>(w); w += align_up(size_t(block + 1) * L.nb * 16);
+        to.ST = reinterpret_cast<float2*>(w); w += align_up(size_t(block) * L.nb * 8);
+        to.LT = reinterpret_cast<uint8_t*>(w); w += align_up(size_t(block) * L.nb);
+        ctr = reinterpret_cast<unsigned long long*>(w);
+        // the block kernels work on the raw input with the scale folded into
+        // the taps: T' = s T, mu' = mu s^2 (y = T' x_raw == T (s x_raw))
+        a.x = static_cast<const float2*>(x);
+        a.nsym = nsym;
+        a.scale = 1.0f;
+        a.train = static_cast<const float2*>(train);
+        a.n_train = n_train;
+        a.mu = mu * scale * scale;
+        a.B = block;
+        a.nb = L.nb;
+        o.labels = nullptr;
+        o.soft = nullptr;
+        o.Q = lv[0].Q;
+        o.Tused = Tused;
+        o.margin = margin;
+        o.Tend = Tend;
+        o.over = over;
+        o.hash = hsh;
+        o.counters = ctr;
+        bt = std::min<int64_t>(n_train / block, L.nb);
+        if (cudaMemsetAsync(over, 0, L.nb * sizeof(int), s) != cudaSuccess ||
+            cudaMemsetAsync(hsh, 0, L.nb * 8, s) != cudaSuccess ||
+            cudaMemsetAsync(ctr, 0, 4 * sizeof(unsigned long long), s) != cudaSuccess)
+            return set_cuda_error("solver init");
         dim3 tb(32, 8), tg(static_cast<unsigned>((L.nb + 31) / 32), static_cast<unsigned>((block + 1 + 31) / 32));
         ddlms_transpose_in<<<tg, tb, 0, s>>>(a.x, nsym, block, L.nb, XT);
-        if (int rc = check_launch("ddlms_transpose_in")) return rc;
+        return check_launch("ddlms_transpose_in");
     }
 
-    // (2) pure-training blocks are exact from any start: run them, scan to
-    //     get the exact training-end taps, speculate everything after.
-    const int64_t bt = std::min<int64_t>(n_train / block, L.nb);
-    if (cudaMemcpyAsync(Tinit_d, T_init_s, 16 * sizeof(float), cudaMemcpyHostToDevice, s) != cudaSuccess ||
-        cudaStreamSynchronize(s) != cudaSuccess)
-        return set_cuda_error("T_init upload");
-    if (cudaMemsetAsync(over, 0, L.nb * sizeof(int), s) != cudaSuccess) return set_cuda_error("over init");
-    if (cudaMemsetAsync(hsh, 0, L.nb * 8, s) != cudaSuccess) return set_cuda_error("hash init");
-    if (int rc = fill_T(0, L.nb, Tinit_d)) return rc;
-    if (cudaMemsetAsync(ctr, 0, 4 * sizeof(unsigned long long), s) != cudaSuccess) return set_cuda_error("ctr");
-    if (bt > 0) {
-        // first pass fused with the block maps P_b (decision independent)
-        if (int rc = run_blocks(true, 0, bt, 0)) return rc;
-        // Q of not-yet-run blocks must not pollute the training scan: zero them
-        if (bt < L.nb &&
-            cudaMemsetAsync(lv[0].Q + bt * 16, 0, (L.nb - bt) * 16 * sizeof(float), s) != cudaSuccess)
-            return set_cuda_error("Q init");
-        if (int rc = scan(true)) return rc;
-        // lv[0].T[bt] is exact; broadcast it as the guess for all later blocks
-        if (bt < L.nb) {
-            if (cudaMemcpyAsync(Tend, lv[0].T + bt * 16, 16 * sizeof(float), cudaMemcpyDeviceToDevice, s) !=
-                cudaSuccess)
-                return set_cuda_error("T guess");
-            if (int rc = fill_T(bt + 1, L.nb, Tend)) return rc;
+    // pure-training blocks from T_start; writes the exact training-end taps
+    int train(const float* T_start, float* T_train_end) {
+        if (int rc = set_start(T_start)) return rc;
+        if (int rc = fill_T(0, L.nb, Tinit_d)) return rc;
+        if (bt > 0) {
+            if (int rc = run_blocks(true, 0, bt, 0)) return rc;
+            if (bt < L.nb &&
+                cudaMemsetAsync(lv[0].Q + bt * 16, 0, (L.nb - bt) * 16 * sizeof(float), s) != cudaSuccess)
+                return set_cuda_error("Q init");
+            if (int rc = scan_up(true)) return rc;
+            if (int rc = scan_down()) return rc;
         }
+        if (T_train_end) {
+            float Tt[16];
+            if (bt < L.nb) {
+                if (cudaMemcpyAsync(Tt, lv[0].T + bt * 16, sizeof(Tt), cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+                    cudaStreamSynchronize(s) != cudaSuccess)
+                    return set_cuda_error("T train end");
+                for (int i = 0; i < 16; ++i) T_train_end[i] = Tt[i] / scale;
+            } else {
+                // training covers the frame: its end taps
+                if (cudaMemcpyAsync(Tt, Tend, sizeof(Tt), cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+                    cudaStreamSynchronize(s) != cudaSuccess)
+                    return set_cuda_error("T train end");
+                for (int i = 0; i < 16; ++i) T_train_end[i] = Tt[i] / scale;
+            }
+        }
+        return KK_OK;
     }
-    if (int rc = run_blocks(true, bt, L.nb, 0)) return rc;
-    st[1] = L.nb;
-    bool p_done = false;   // the training scan saw only the training blocks' maps
 
-    // (3) fixpoint iterations
-    bool converged = false;
-    unsigned long long h[4] = {0, 0, 0, 0};
-    for (int it = 1; it <= max_iter; ++it) {
-        if (int rc = scan(!p_done)) return rc;
-        p_done = true;
-        if (cudaMemsetAsync(ctr, 0, 4 * sizeof(unsigned long long), s) != cudaSuccess) return set_cuda_error("ctr");
+    // first pass of the decision-directed blocks from T_guess (+ P_b)
+    int speculate(const float* T_guess, float* agg) {
+        float Tg[16];
+        for (int i = 0; i < 16; ++i) Tg[i] = T_guess[i] * scale;
+        if (cudaMemcpyAsync(Tend, Tg, sizeof(Tg), cudaMemcpyHostToDevice, s) != cudaSuccess)
+            return set_cuda_error("T guess");
+        if (int rc = fill_T(bt, L.nb, Tend)) return rc;
+        if (int rc = run_blocks(true, bt, L.nb, 0)) return rc;
+        reruns += L.nb;
+        speculated = true;
+        if (int rc = scan_up(true)) return rc;
+        return frame_map(agg);
+    }
+
+    // exact frame start taps -> re-run; returns changed blocks
+    int iterate(const float* T_start, int64_t* changed, int64_t* rerun, float* agg) {
+        if (!speculated) return set_error(KK_ERR_PARAM, "speculate() must precede iterate()");
+        if (int rc = set_start(T_start)) return rc;
+        if (int rc = scan_down()) return rc;
+        if (cudaMemsetAsync(ctr, 0, 2 * sizeof(unsigned long long), s) != cudaSuccess) return set_cuda_error("ctr");
         if (int rc = run_blocks(false, 0, L.nb, 1)) return rc;
+        unsigned long long h[4];
         if (int rc = read_ctr(h)) return rc;
-        st[0] = it;
-        st[1] += static_cast<int64_t>(h[1]);
-        st[4] = static_cast<int64_t>(h[0]);
-        if (it <= 16 && stats) {   // per-iteration detail: stats[6 + 2(it-1)] = changed, reruns
-            stats[6 + 2 * (it - 1)] = static_cast<int64_t>(h[0]);
-            stats[7 + 2 * (it - 1)] = static_cast<int64_t>(h[1]);
-        }
-        if (h[0] == 0) { converged = true; break; }
+        ++iters;
+        reruns += static_cast<int64_t>(h[1]);
+        last_changed = static_cast<int64_t>(h[0]);
+        if (changed) *changed = last_changed;
+        if (rerun) *rerun = static_cast<int64_t>(h[1]);
+        if (int rc = scan_up(false)) return rc;
+        return frame_map(agg);
     }
-    if (converged) {
-        dim3 tb(32, 8), tg(static_cast<unsigned>((L.nb + 31) / 32), static_cast<unsigned>((block + 31) / 32));
-        ddlms_transpose_out<<<tg, tb, 0, s>>>(to.ST, to.LT, nsym, block, L.nb, static_cast<float2*>(soft), labels);
-        if (int rc = check_launch("ddlms_transpose_out")) return rc;
-    } else {
-        // exact fallback: chain every block sequentially from the scanned start
-        // taps of block 0 (== T_init)
-        st[2] = 2;
-        if (cudaMemsetAsync(ctr, 0, 4 * sizeof(unsigned long long), s) != cudaSuccess) return set_cuda_error("ctr");
+
+    // chained exact fallback from block 0 (start taps already in lv[0].T[0])
+    int chain(uint8_t* labels, float2* soft) {
+        o.labels = labels;
+        o.soft = soft;
+        if (int rc = scan_down()) return rc;
         ddlms_run_kernel<<<1, 1, 0, s>>>(a, sl, lv[0].T, maxx2, o, 0, L.nb, 0, soft_tol, 1, 1);
-        if (int rc = check_launch("ddlms_run_kernel chain")) return rc;
+        return check_launch("ddlms_run_kernel chain");
     }
-    if (cudaMemsetAsync(ctr + 2, 0, sizeof(unsigned long long), s) != cudaSuccess) return set_cuda_error("ctr");
-    sum_int_kernel<<<grid_of(std::min<int64_t>(L.nb, 148 * 8 * th)), th, 0, s>>>(over, L.nb, ctr + 2);
-    if (int rc = check_launch("sum_int_kernel")) return rc;
-    if (int rc = read_ctr(h)) return rc;
-    st[3] = static_cast<int64_t>(h[2]);
-    if (st[3] > 0) st[2] = st[2] ? st[2] : 1;   // guard exceedances: caller must re-run exactly
-    if (cudaMemcpyAsync(T_final, Tend, 16 * sizeof(float), cudaMemcpyDeviceToHost, s) != cudaSuccess ||
-        cudaStreamSynchronize(s) != cudaSuccess)
-        return set_cuda_error("T_final");
-    for (int i = 0; i < 16; ++i) T_final[i] /= scale;
+
+    int finish(uint8_t* labels, float2* soft, float* T_final, int64_t* guard) {
+        dim3 tb(32, 8), tg(static_cast<unsigned>((L.nb + 31) / 32), static_cast<unsigned>((a.B + 31) / 32));
+        ddlms_transpose_out<<<tg, tb, 0, s>>>(to.ST, to.LT, a.nsym, a.B, L.nb, soft, labels);
+        if (int rc = check_launch("ddlms_transpose_out")) return rc;
+        return end_state(T_final, guard);
+    }
+    int end_state(float* T_final, int64_t* guard) {
+        if (cudaMemsetAsync(ctr + 2, 0, sizeof(unsigned long long), s) != cudaSuccess) return set_cuda_error("ctr");
+        const int64_t gblocks = std::min<int64_t>((L.nb + 127) / 128, 148 * 8);
+        sum_int_kernel<<<static_cast<unsigned>(gblocks), 128, 0, s>>>(over, L.nb, ctr + 2);
+        if (int rc = check_launch("sum_int_kernel")) return rc;
+        unsigned long long h[4];
+        if (int rc = read_ctr(h)) return rc;
+        if (guard) *guard = static_cast<int64_t>(h[2]);
+        if (T_final) {
+            float Tt[16];
+            if (cudaMemcpyAsync(Tt, Tend, sizeof(Tt), cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+                cudaStreamSynchronize(s) != cudaSuccess)
+                return set_cuda_error("T_final");
+            for (int i = 0; i < 16; ++i) T_final[i] = Tt[i] / scale;
+        }
+        return KK_OK;
+    }
+};
+
+int make_solver(DdlmsSolver& sv, const void* x, int64_t nsym, float scale, const void* train, int64_t n_train,
+                int order, const float* pts_host, const uint8_t* grid_host, int grid_m, float norm, float max_radius,
+                float guard_factor, float mu, int block, float soft_tol, void* workspace, size_t ws_bytes,
+                cudaStream_t s) {
+    if (nsym <= 0) return set_error(KK_ERR_PARAM, "nsym must be positive");
+    if (block <= 0) return set_error(KK_ERR_PARAM, "block must be positive");
+    if (order < 2 || order > 64) return set_error(KK_ERR_PARAM, "constellation order must be <= 64");
+    if (!(scale > 0.0f)) return set_error(KK_ERR_PARAM, "scale must be positive");
+    Slicer sl = make_slicer(order, pts_host, grid_host, grid_m, norm, max_radius, guard_factor);
+    return sv.init(x, nsym, scale, train, n_train, sl, mu, block, soft_tol, workspace, ws_bytes, s);
+}
+}  // namespace
+
+extern "C" void* kk_ddlms_create(const void* x, int64_t nsym, float scale, const void* train, int64_t n_train,
+                                 int order, const float* pts_host, const uint8_t* grid_host, int grid_m, float norm,
+                                 float max_radius, float guard_factor, float mu, int block, float soft_tol,
+                                 void* workspace, size_t ws_bytes, void* stream) {
+    clear_error();
+    auto* sv = new DdlmsSolver();
+    if (make_solver(*sv, x, nsym, scale, train, n_train, order, pts_host, grid_host, grid_m, norm, max_radius,
+                    guard_factor, mu, block, soft_tol, workspace, ws_bytes, static_cast<cudaStream_t>(stream))) {
+        delete sv;
+        return nullptr;
+    }
+    return sv;
+}
+
+extern "C" int kk_ddlms_train(void* h, const float* T_start_host, float* T_train_end_host) {
+    clear_error();
+    if (!h) return set_error(KK_ERR_PARAM, "null solver");
+    return static_cast<DdlmsSolver*>(h)->train(T_start_host, T_train_end_host);
+}
+
+extern "C" int kk_ddlms_speculate(void* h, const float* T_guess_host, float* map_host) {
+    clear_error();
+    if (!h) return set_error(KK_ERR_PARAM, "null solver");
+    return static_cast<DdlmsSolver*>(h)->speculate(T_guess_host, map_host);
+}
+
+extern "C" int kk_ddlms_iterate(void* h, const float* T_start_host, int64_t* changed, int64_t* rerun,
+                                float* map_host) {
+    clear_error();
+    if (!h) return set_error(KK_ERR_PARAM, "null solver");
+    return static_cast<DdlmsSolver*>(h)->iterate(T_start_host, changed, rerun, map_host);
+}
+
+extern "C" int kk_ddlms_finish(void* h, uint8_t* labels, void* soft, float* T_final_host, int64_t* guard) {
+    clear_error();
+    if (!h) return set_error(KK_ERR_PARAM, "null solver");
+    return static_cast<DdlmsSolver*>(h)->finish(labels, static_cast<float2*>(soft), T_final_host, guard);
+}
+
+extern "C" void kk_ddlms_destroy(void* h) { delete static_cast<DdlmsSolver*>(h); }
+
+// Single-frame exact solve (T_init = exact frame start taps).  stats (host
+// int64[38]): iterations, blocks re-run, fallback (0 none, 1 guard exceeded
+// -> caller re-runs sequentially, 2 not converged -> chained), guard
+// exceedances, changed blocks in the last iteration, blocks, then
+// per-iteration (changed blocks, re-run blocks) for iterations 1..16.
+extern "C" int kk_ddlms_solve(const void* x, int64_t nsym, float scale, const void* train, int64_t n_train,
+                              const float* T_init, int order, const float* pts_host, const uint8_t* grid_host,
+                              int grid_m, float norm, float max_radius, float guard_factor, int guard_run,
+                              float mu, int block, int max_iter, float soft_tol, uint8_t* labels, void* soft,
+                              float* T_final, void* workspace, size_t ws_bytes, int64_t* stats, void* stream) {
+    clear_error();
+    (void)guard_run;
+    if (nsym <= 0) return KK_OK;
+    DdlmsSolver sv;
+    if (int rc = make_solver(sv, x, nsym, scale, train, n_train, order, pts_host, grid_host, grid_m, norm,
+                             max_radius, guard_factor, mu, block, soft_tol, workspace, ws_bytes,
+                             static_cast<cudaStream_t>(stream)))
+        return rc;
+    float Tg[16];
+    if (int rc = sv.train(T_init, Tg)) return rc;
+    if (int rc = sv.speculate(sv.bt > 0 ? Tg : T_init, nullptr)) return rc;
+    int64_t st[6] = {0, 0, 0, 0, 0, sv.L.nb};
+    bool converged = false;
+    for (int it = 1; it <= max_iter; ++it) {
+        int64_t ch = 0, rr = 0;
+        if (int rc = sv.iterate(T_init, &ch, &rr, nullptr)) return rc;
+        if (stats && it <= 16) {
+            stats[6 + 2 * (it - 1)] = ch;
+            stats[7 + 2 * (it - 1)] = rr;
+        }
+        if (ch == 0) { converged = true; break; }
+    }
+    int64_t guard = 0;
+    if (converged) {
+        if (int rc = sv.finish(labels, static_cast<float2*>(soft), T_final, &guard)) return rc;
+    } else {
+        st[2] = 2;
+        if (int rc = sv.chain(labels, static_cast<float2*>(soft))) return rc;
+        if (int rc = sv.end_state(T_final, &guard)) return rc;
+    }
+    st[0] = sv.iters;
+    st[1] = sv.reruns;
+    st[3] = guard;
+    st[4] = sv.last_changed;
+    if (guard > 0 && st[2] == 0) st[2] = 1;   // guard exceedances: caller must re-run exactly
     if (stats)
         for (int i = 0; i < 6; ++i) stats[i] = st[i];
     return KK_OK;

@@ -262,13 +262,13 @@ def _as_device_input(x, dev):
 class _DevStream:
     """Append-only device buffer on a global index with prefix trimming."""
 
-    def __init__(self, dtype, dev, cap=1 << 16):
+    def __init__(self, dtype, dev, cap=1 << 16, start=0):
         torch = _torch()
         self.torch = torch
         self.buf = torch.empty(cap, dtype=dtype, device=dev)
-        self.base = 0      # global index of buf[0]
-        self.end = 0       # global end index
-        self.keep = 0      # data before this global index may be dropped
+        self.base = start  # global index of buf[0]
+        self.end = start   # global end index
+        self.keep = start  # data before this global index may be dropped
 
     def reserve(self, n_more: int):
         """Make room for n_more items at the end; returns the tensor slice
@@ -635,7 +635,12 @@ class RxPipeline:
     """Streaming receiver on one GPU: feed ADC chunks of any size, collect
     decisions (rx:608-824).  Output is bit-identical for any chunking."""
 
-    def __init__(self, cfg: RxPipelineConfig, reference_symbols=None, device=None):
+    def __init__(self, cfg: RxPipelineConfig, reference_symbols=None, device=None, stream_offset: int = 0,
+                 static_start_hop: int | None = None):
+        """stream_offset: global ADC index of the first sample fed (a multiple
+        of the carrier segment; super-frame shards start mid-stream);
+        static_start_hop: first global static hop to equalise (shards skip
+        their left halo)."""
         torch = _torch()
         _lib.load()
         self.cfg = cfg
@@ -680,14 +685,21 @@ class RxPipeline:
              torch.empty(hop // 2, dtype=torch.uint8, device=self.dev)),
         ]
         self._kk_cur = 0
-        self._z = _DevStream(torch.complex64, self.dev)          # KK output, global sample index
-        self._hs = _DevStream(torch.complex64, self.dev)         # per-hop field sums, global hop index
-        self._hd = _DevStream(torch.uint8, self.dev)             # per-hop dead flags
-        self._seg = _DevStream(torch.complex64, self.dev)        # carrier means, global segment index
-        self._y2 = _DevStream(torch.complex64, self.dev)         # static output, global 2-sps index
+        seg = cfg.carrier_segment_len
+        if stream_offset % seg or stream_offset % cfg.static_plan.hop:
+            raise ParameterError("stream_offset must be a multiple of the carrier segment and static hop")
+        hb0 = stream_offset // cfg.static_plan.hop if static_start_hop is None else int(static_start_hop)
+        if hb0 * cfg.static_plan.hop < stream_offset + (cfg.static_plan.hop if stream_offset else 0):
+            raise ParameterError("static_start_hop must leave one static hop of history inside the stream")
+        self._stream_offset = stream_offset
+        self._z = _DevStream(torch.complex64, self.dev, start=stream_offset)            # KK output, global sample index
+        self._hs = _DevStream(torch.complex64, self.dev, start=stream_offset // hop)    # per-hop field sums, global hop
+        self._hd = _DevStream(torch.uint8, self.dev, start=stream_offset // hop)        # per-hop dead flags
+        self._seg = _DevStream(torch.complex64, self.dev, start=stream_offset // seg)   # carrier means, global segment
+        self._y2 = _DevStream(torch.complex64, self.dev, start=hb0 * (cfg.static_plan.hop // 2))  # static out, 2-sps
         self._clamped = torch.zeros(1, dtype=torch.int64, device=self.dev)
-        self._c_end = 0
-        self._hb_next = 0
+        self._c_end = stream_offset
+        self._hb_next = hb0
         self._flushed = False
 
         # DDLMS
@@ -957,12 +969,22 @@ class RxPipeline:
         t2 = self._ev()
         self._run_static(flush)
         t3 = self._ev()
-        self._run_ddlms(flush)
+        if not getattr(self, "_front_only", False):
+            self._run_ddlms(flush)
         t4 = self._ev()
         self._events += [("kk", t0, t1), ("carrier", t1, t2), ("static", t2, t3), ("ddlms", t3, t4)]
         self._chunk_index += 1
         if flush:
             self._flushed = True
+
+    def front_end(self, adc_chunk, flush: bool = False) -> None:
+        """KK -> carrier -> downshift -> static stages only (the DDLMS is
+        driven externally, e.g. by the multi-GPU super-frame solver)."""
+        self._front_only = True
+        try:
+            self.feed(adc_chunk, flush=flush)
+        finally:
+            self._front_only = False
 
     def drain_device(self):
         """Device-resident outputs accumulated so far, then cleared:
