@@ -51,7 +51,8 @@ class TorchComm:
 
     def __init__(self, dist, device):
         self.dist = dist
-        self.device = device
+        # NCCL collectives take device tensors, gloo host tensors
+        self.device = device if dist.get_backend() == "nccl" else "cpu"
         self.rank = dist.get_rank()
         self.world = dist.get_world_size()
 
