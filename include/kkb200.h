@@ -50,6 +50,9 @@ int kk_version(void);
 int kk_device_sync(void);
 /* number of kernels this library has launched (process-wide counter) */
 unsigned long long kk_launch_count(void);
+/* measured FP32 FFMA throughput of the current device (FLOP/s), for the
+ * roofline of the FP32-bound FFT kernels */
+int kk_fma_peak(double *flops_per_s_host, void *stream);
 
 /*
  * K1 kk_fused -- replaces rxdsp.py:184-244 `kk_reconstruct` (+ the downshift

@@ -85,3 +85,53 @@ extern "C" int kk_device_sync(void) {
     if (cudaDeviceSynchronize() != cudaSuccess) return kk::set_cuda_error("cudaDeviceSynchronize");
     return KK_OK;
 }
+
+// ---------------------------------------------------------------------------
+// FP32 FMA throughput microbenchmark (the roofline denominator for the
+// FP32-bound FFT kernels; MEASURED_PEAKS.json has no FP32 entry).  Each
+// thread runs 8 independent FFMA chains; returns FLOP/s (2 per FFMA).
+// ---------------------------------------------------------------------------
+namespace kk {
+__global__ void fma_peak_kernel(float* out, int iters, float a, float b) {
+    float x0 = threadIdx.x, x1 = x0 + 1, x2 = x0 + 2, x3 = x0 + 3, x4 = x0 + 4, x5 = x0 + 5, x6 = x0 + 6,
+          x7 = x0 + 7;
+    for (int i = 0; i < iters; ++i) {
+#pragma unroll
+        for (int u = 0; u < 16; ++u) {
+            x0 = fmaf(x0, a, b); x1 = fmaf(x1, a, b); x2 = fmaf(x2, a, b); x3 = fmaf(x3, a, b);
+            x4 = fmaf(x4, a, b); x5 = fmaf(x5, a, b); x6 = fmaf(x6, a, b); x7 = fmaf(x7, a, b);
+        }
+    }
+    const float s = x0 + x1 + x2 + x3 + x4 + x5 + x6 + x7;
+    if (s == 1234.5f) out[threadIdx.x] = s;   // keep the chains alive
+}
+}  // namespace kk
+
+extern "C" int kk_fma_peak(double* flops_per_s, void* stream) {
+    kk::clear_error();
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    int dev = 0, sms = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    float* out = nullptr;
+    if (cudaMalloc(&out, 1024 * sizeof(float)) != cudaSuccess) return kk::set_cuda_error("fma peak alloc");
+    const int blocks = sms * 8, threads = 256, iters = 4096;
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    kk::fma_peak_kernel<<<blocks, threads, 0, s>>>(out, 64, 0.999f, 1e-3f);   // warm-up
+    cudaEventRecord(e0, s);
+    kk::fma_peak_kernel<<<blocks, threads, 0, s>>>(out, iters, 0.999f, 1e-3f);
+    cudaEventRecord(e1, s);
+    int rc = kk::check_launch("fma_peak_kernel");
+    cudaEventSynchronize(e1);
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, e0, e1);
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    cudaFree(out);
+    if (rc) return rc;
+    const double flops = 2.0 * 8 * 16 * double(iters) * blocks * threads;
+    *flops_per_s = flops / (ms * 1e-3);
+    return KK_OK;
+}

@@ -815,12 +815,35 @@ __global__ void bit_errors_kernel(const uint8_t* __restrict__ lab, const uint8_t
     __shared__ uint8_t pl[64];
     if (threadIdx.x < 64) pl[threadIdx.x] = point_label[threadIdx.x];
     __syncthreads();
+    // each thread owns a contiguous run of 16 symbols (one uint4 of each
+    // array); the seam phase is tracked incrementally (no 64-bit modulo)
     unsigned long long e = 0, cnt = 0;
-    for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t n16 = n / 16;
+    const uint4* L4 = reinterpret_cast<const uint4*>(lab);
+    const uint4* R4 = reinterpret_cast<const uint4*>(ref);
+    const bool aligned = ((reinterpret_cast<uintptr_t>(lab) | reinterpret_cast<uintptr_t>(ref)) & 15) == 0;
+    const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+    for (int64_t t = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; t < (aligned ? n16 : 0); t += stride) {
+        const uint4 a4 = L4[t], b4 = R4[t];
+        const uint8_t* a = reinterpret_cast<const uint8_t*>(&a4);
+        const uint8_t* b = reinterpret_cast<const uint8_t*>(&b4);
+        int64_t ph = ex_period > 0 ? (16 * t + ex_phase) % ex_period : 0;
+#pragma unroll
+        for (int u = 0; u < 16; ++u) {
+            const bool skip = ex_period > 0 && ph >= ex_period - ex_len;
+            if (ex_period > 0 && ++ph == ex_period) ph = 0;
+            if (skip) continue;
+            ++cnt;
+            const unsigned c = __popc(static_cast<unsigned>(pl[a[u] & 63] ^ pl[b[u] & 63]));
+            e += c;
+            if (win && c) atomicAdd(win + (16 * t + u) / win_syms, c);
+        }
+    }
+    // tail (or the whole range when unaligned)
+    for (int64_t i = (aligned ? n16 * 16 : 0) + int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride) {
         if (ex_period > 0 && ((i + ex_phase) % ex_period) >= ex_period - ex_len) continue;
         ++cnt;
-        const uint8_t a = lab[i], b = ref[i];
-        const unsigned c = __popc(static_cast<unsigned>(pl[a & 63] ^ pl[b & 63]));
+        const unsigned c = __popc(static_cast<unsigned>(pl[lab[i] & 63] ^ pl[ref[i] & 63]));
         e += c;
         if (win && c) atomicAdd(win + i / win_syms, c);
     }
