@@ -182,13 +182,23 @@ struct SmemPlanes {
 };
 
 struct LoadPlanes {
+    static constexpr bool kPlanes = true;
     SmemPlanes s;
     __device__ __forceinline__ float2 operator()(int i) const { return s.ld(i); }
 };
 struct StorePlanes {
+    static constexpr bool kPlanes = true;
     SmemPlanes s;
     __device__ __forceinline__ void operator()(int i, float2 v) const { s.st(i, v); }
 };
+
+// does the functor address the padded smem buffer directly?  Then the pass
+// engine hoists the padding math: padi(x + y) == padi(x) + y + y/16 for y a
+// multiple of 16, and == padi(x) + y when x is a multiple of 16 and y < 16.
+template <class F, class = void>
+struct is_planes { static constexpr bool value = false; };
+template <class F>
+struct is_planes<F, decltype(void(F::kPlanes))> { static constexpr bool value = F::kPlanes; };
 
 // One in-place Stockham (autosort, DIT-twiddle) pass of an N-point FFT with
 // radix R, run by NT threads; NS = product of the radices of earlier passes.
@@ -209,8 +219,14 @@ __device__ __forceinline__ void stockham_load(int tid, const Load& load, float2 
 #pragma unroll
     for (int q = 0; q < PassShape<N, R, NT>::BPT; ++q) {
         const int j = tid + q * NT;
+        if constexpr (is_planes<Load>::value && NB % 16 == 0) {
+            const float2* p = load.s.d + padi(j);
 #pragma unroll
-        for (int r = 0; r < R; ++r) v[q][r] = load(j + r * NB);
+            for (int r = 0; r < R; ++r) v[q][r] = p[r * (NB + NB / 16)];
+        } else {
+#pragma unroll
+            for (int r = 0; r < R; ++r) v[q][r] = load(j + r * NB);
+        }
     }
 }
 
@@ -246,8 +262,18 @@ __device__ __forceinline__ void stockham_compute_store(int tid, const Twiddle& t
         }
         dft_reg<R, INV>(v[q]);
         const int d0 = (j / NS) * NS * R + (j % NS);
+        if constexpr (is_planes<Store>::value && NS % 16 == 0) {
+            float2* p = store.s.d + padi(d0);
 #pragma unroll
-        for (int r = 0; r < R; ++r) store(d0 + r * NS, v[q][r]);
+            for (int r = 0; r < R; ++r) p[r * (NS + NS / 16)] = v[q][r];
+        } else if constexpr (is_planes<Store>::value && NS == 1 && R <= 16 && 16 % R == 0) {
+            float2* p = store.s.d + padi(d0);        // d0 = j*R, R | 16: no pad crossing
+#pragma unroll
+            for (int r = 0; r < R; ++r) p[r] = v[q][r];
+        } else {
+#pragma unroll
+            for (int r = 0; r < R; ++r) store(d0 + r * NS, v[q][r]);
+        }
     }
 }
 
@@ -269,8 +295,14 @@ __device__ __forceinline__ void stockham_pass(int tid, const Twiddle& tw, const 
         for (int q = 0; q < PassShape<N, R, NT>::BPT; ++q) {
             float2 v[1][R];
             const int j = tid + q * NT;
+            if constexpr (is_planes<Load>::value && NB % 16 == 0) {
+                const float2* p = load.s.d + padi(j);
 #pragma unroll
-            for (int r = 0; r < R; ++r) v[0][r] = load(j + r * NB);
+                for (int r = 0; r < R; ++r) v[0][r] = p[r * (NB + NB / 16)];
+            } else {
+#pragma unroll
+                for (int r = 0; r < R; ++r) v[0][r] = load(j + r * NB);
+            }
             stockham_compute_store<N, R, NS, NT, INV, 1>(tid + q * NT, tw, v, store);
         }
     }

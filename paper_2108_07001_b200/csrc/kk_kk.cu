@@ -31,16 +31,25 @@ constexpr int kK1Threads = kPairsPerCta * kGroupThreads;      // 256
 constexpr int kStageHops = 2 * kPairsPerCta + 1;              // 9
 constexpr int kPlane1 = padded(kN1);                          // 1088 float2
 
+// K1 only indexes the W_256 / W_1024 twiddle tables: stage that prefix
+constexpr int kK1TwEntries = tw_offset(2048);
+
 struct K1Smem {
-    float u[kStageHops * kHop];
-    float a[kStageHops * kHop];
+    float u[kStageHops * kHop];          // 0.5 ln(safe); amp = exp(u) is recomputed
+    float ahist[kHop / 2];               // amp of the state hop (initial state: zeros)
     float2 buf[kPairsPerCta][kPlane1];
-    float2 tw[kTwEntries];
+    float2 tw[kK1TwEntries];
     float2 red[kK1Threads / 32][2];
     int dead[kStageHops];
     uint8_t dead_hist[kHop / 2];   // per-sample dead flags of hop -1 (state)
     unsigned int clamped;
 };
+
+// x reduced to [-pi, pi] (exact multiple-of-2pi removal for |x| << 2^20)
+__device__ __forceinline__ float reduce_2pi(float x) {
+    const float k = rintf(x * 0.15915494309189535f);
+    return fmaf(-k, 6.28318548202514648f, fmaf(-k, -1.7484555314695172e-7f, x));
+}
 
 template <typename TIn>
 __device__ __forceinline__ float load_in(const TIn* p, int64_t i, float scale) {
@@ -86,7 +95,7 @@ kk_pairs_kernel(const TIn* __restrict__ in, float in_scale, float clamp_rel, int
     const int warp = tid >> 5, lane = tid & 31;
     const int64_t hop0 = int64_t(blockIdx.x) * (2 * kPairsPerCta) - 1;   // chunk hop of stage hop 0
 
-    load_twiddles(S.tw, tw_g, tid, kK1Threads);
+    for (int i = tid; i < kK1TwEntries; i += kK1Threads) S.tw[i] = tw_g[i];
     if (tid == 0) S.clamped = 0;
     __syncthreads();
 
@@ -94,19 +103,17 @@ kk_pairs_kernel(const TIn* __restrict__ in, float in_scale, float clamp_rel, int
     for (int L = warp; L < kStageHops; L += kK1Threads / 32) {
         const int64_t h = hop0 + L;
         float* u = S.u + L * kHop;
-        float* a = S.a + L * kHop;
         if (h < 0) {  // previous-chunk state (rxdsp.py:208-213 initial zeros)
             for (int i = lane; i < kHop; i += 32) u[i] = st_u[i];
             for (int i = lane; i < kHop / 2; i += 32) {
-                a[i] = 0.f;
-                a[kHop / 2 + i] = st_a[i];
+                S.ahist[i] = st_a[i];
                 S.dead_hist[i] = st_dead[i];
             }
             if (lane == 0) S.dead[L] = 0;
             continue;
         }
         if (h >= n_hops) {  // dummy partner beyond the last real hop
-            for (int i = lane; i < kHop; i += 32) { u[i] = 0.f; a[i] = 0.f; }
+            for (int i = lane; i < kHop; i += 32) u[i] = 0.f;
             if (lane == 0) S.dead[L] = 1;
             continue;
         }
@@ -135,8 +142,7 @@ kk_pairs_kernel(const TIn* __restrict__ in, float in_scale, float clamp_rel, int
                 ncl += (x < thr) ? 1u : 0u;
                 s = fmaxf(x, thr);
             }
-            u[lane + 32 * i] = 0.5f * logf(s);
-            a[lane + 32 * i] = sqrtf(s);
+            u[lane + 32 * i] = 0.5f * __logf(s);
         }
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) ncl += __shfl_xor_sync(0xffffffffu, ncl, o);
@@ -176,14 +182,14 @@ kk_pairs_kernel(const TIn* __restrict__ in, float in_scale, float clamp_rel, int
 
     // last inverse pass: outputs n = j + 256 r; n >= 512 are the new hop
     float2 acc_a = make_float2(0.f, 0.f), acc_b = make_float2(0.f, 0.f);
-    const float inv_scale = 1.0f / (1024.0f * 3.14159265358979323846f);   // phi/pi for sincospif
-    const float* aa = S.a + (2 * g) * kHop + kHop / 2;      // amp at (new hop pos - 256), block a
-    const float* ab = S.a + (2 * g + 1) * kHop + kHop / 2;  // block b
+    const float* ua_d = S.u + (2 * g) * kHop + kHop / 2;      // u at (new hop pos - 256), block a
+    const float* ub_d = S.u + (2 * g + 1) * kHop + kHop / 2;  // block b
     const int dead_a0 = S.dead[2 * g], dead_a1 = S.dead[2 * g + 1], dead_b1 = S.dead[2 * g + 2];
     const bool hist = (hop0 + 2 * g) < 0;   // stage hop 2g is the state hop
     // rotation index (rot_p * g mod rot_q) of the pair's first output sample
     unsigned rot_base = 0;
     const float inv_q = rot_q > 0 ? 1.0f / static_cast<float>(rot_q) : 0.f;
+    const float two_pi_over_q = rot_q > 0 ? 6.283185307179586f / static_cast<float>(rot_q) : 0.f;
     if (rot_q > 0 && active)
         rot_base = static_cast<unsigned>((static_cast<unsigned long long>(n0_global + hop_a * kHop) % rot_q));
     auto st_out = [&](int n, float2 v) {
@@ -194,10 +200,14 @@ kk_pairs_kernel(const TIn* __restrict__ in, float in_scale, float clamp_rel, int
         // previous hop when i < 256
         bool da = (i < kHop / 2) ? (hist ? (S.dead_hist[i] != 0) : (dead_a0 != 0)) : (dead_a1 != 0);
         bool db = (i < kHop / 2) ? (dead_a1 != 0) : (dead_b1 != 0);
+        // phases, reduced to [-pi, pi] for the fast sin/cos (abs err ~1e-6)
+        const float pa_ = reduce_2pi(v.x * (1.0f / 1024.0f));
+        const float pb_ = reduce_2pi(v.y * (1.0f / 1024.0f));
+        const float amp_a = (hist && i < kHop / 2) ? S.ahist[i] : __expf(ua_d[i]);
+        const float amp_b = __expf(ub_d[i]);
         float sa, ca, sb, cb;
-        sincospif(v.x * inv_scale, &sa, &ca);
-        sincospif(v.y * inv_scale, &sb, &cb);
-        const float amp_a = aa[i], amp_b = ab[i];
+        __sincosf(pa_, &sa, &ca);
+        __sincosf(pb_, &sb, &cb);
         float2 fa = da ? make_float2(0.f, 0.f) : make_float2(amp_a * ca, amp_a * sa);
         float2 fb = db ? make_float2(0.f, 0.f) : make_float2(amp_b * cb, amp_b * sb);
         if (!active) return;
@@ -206,11 +216,17 @@ kk_pairs_kernel(const TIn* __restrict__ in, float in_scale, float clamp_rel, int
         const int64_t pb = pa + kHop;
         float2 za = fa, zb = fb;
         if (rot_q > 0) {
+            // field * exp(-2 pi i a/q) = amp exp(i (phi - 2 pi a/q)): one more sincos
             const unsigned Q = static_cast<unsigned>(rot_q), P = static_cast<unsigned>(rot_p);
-            const unsigned ia = fmod_u((rot_base + i) * P, Q, inv_q);
-            const unsigned ib = fmod_u((rot_base + kHop + i) * P, Q, inv_q);
-            za = cmul(fa, __ldg(rot_tab + ia));
-            zb = cmul(fb, __ldg(rot_tab + ib));
+            const int ia = static_cast<int>(fmod_u((rot_base + i) * P, Q, inv_q));
+            const int ib = static_cast<int>(fmod_u((rot_base + kHop + i) * P, Q, inv_q));
+            const float th_a = reduce_2pi(pa_ - two_pi_over_q * static_cast<float>(ia));
+            const float th_b = reduce_2pi(pb_ - two_pi_over_q * static_cast<float>(ib));
+            float sra, cra, srb, crb;
+            __sincosf(th_a, &sra, &cra);
+            __sincosf(th_b, &srb, &crb);
+            za = da ? make_float2(0.f, 0.f) : make_float2(amp_a * cra, amp_a * sra);
+            zb = db ? make_float2(0.f, 0.f) : make_float2(amp_b * crb, amp_b * srb);
         }
         if (mirror) { za = cconj(za); zb = cconj(zb); }
         out[pa] = za;
@@ -244,7 +260,7 @@ kk_pairs_kernel(const TIn* __restrict__ in, float in_scale, float clamp_rel, int
     if (Ll >= 1 && Ll < kStageHops) {
         for (int i = tid; i < kHop; i += kK1Threads) new_u[i] = S.u[Ll * kHop + i];
         for (int i = tid; i < kHop / 2; i += kK1Threads) {
-            new_a[i] = S.a[Ll * kHop + kHop / 2 + i];
+            new_a[i] = (hop0 + Ll < 0) ? S.ahist[i] : __expf(S.u[Ll * kHop + kHop / 2 + i]);
             new_dead[i] = static_cast<uint8_t>(S.dead[Ll]);
         }
     }
