@@ -142,7 +142,10 @@ int kk_ddlms_solve(const void *x, int64_t nsym, float scale, const void *train, 
  * (kk_ddlms_workspace_bytes) and returns an opaque handle (NULL on error).
  *   train(T_start)      exact pure-training blocks -> training-end taps
  *   speculate(T_guess)  first pass of the decision-directed blocks -> map
- *   iterate(T_start)    exact frame-start taps: re-run, changed blocks -> map
+ *   iterate(T_start)    exact frame-start taps: re-run blocks whose decision
+ *                       margin the start move could cross (soft_pass: also
+ *                       those whose soft outputs would move > soft_tol);
+ *                       changed blocks -> map
  *   finish              labels / soft / end taps / guard exceedances
  */
 void *kk_ddlms_create(const void *x, int64_t nsym, float scale, const void *train, int64_t n_train, int order,
@@ -151,8 +154,8 @@ void *kk_ddlms_create(const void *x, int64_t nsym, float scale, const void *trai
                       void *stream);
 int kk_ddlms_train(void *solver, const float *T_start_host, float *T_train_end_host);
 int kk_ddlms_speculate(void *solver, const float *T_guess_host, float *map_host);
-int kk_ddlms_iterate(void *solver, const float *T_start_host, int64_t *changed_blocks, int64_t *rerun_blocks,
-                     float *map_host);
+int kk_ddlms_iterate(void *solver, const float *T_start_host, int soft_pass, int64_t *changed_blocks,
+                     int64_t *rerun_blocks, float *map_host);
 int kk_ddlms_finish(void *solver, uint8_t *labels, void *soft, float *T_final_host, int64_t *guard_exceed);
 void kk_ddlms_destroy(void *solver);
 

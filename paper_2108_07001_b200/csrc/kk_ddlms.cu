@@ -418,7 +418,8 @@ template <bool WITH_P>
 __global__ void __launch_bounds__(128, WITH_P ? 3 : 6)
 ddlms_block_kernel(SolveArgs a, Slicer sl, const float4* __restrict__ XT, const float* __restrict__ Tstart,
                    float* __restrict__ Pb, float* __restrict__ maxx2, RunOut o, TOut to, int64_t b_lo,
-                   int64_t b_hi, int use_skip, float soft_tol) {
+                   int64_t b_hi, int use_skip, float soft_tol, const int* __restrict__ list,
+                   const unsigned long long* __restrict__ list_n, int write_out) {
     __shared__ float2 pts[64];
     __shared__ uint8_t grid[64];
     const int tid = threadIdx.x, lane = tid & 31;
@@ -433,8 +434,15 @@ ddlms_block_kernel(SolveArgs a, Slicer sl, const float4* __restrict__ XT, const 
     const float thr2 = sl.thr * sl.thr;
     const int64_t nb = a.nb;
 
-    const int64_t b = b_lo + int64_t(blockIdx.x) * blockDim.x + tid;
-    bool run = b < b_hi;
+    int64_t b = b_lo + int64_t(blockIdx.x) * blockDim.x + tid;
+    bool run;
+    if (list) {   // compacted list of the blocks to re-run
+        const int64_t t = int64_t(blockIdx.x) * blockDim.x + tid;
+        run = t < static_cast<int64_t>(*list_n);
+        b = run ? list[t] : 0;
+    } else {
+        run = b < b_hi;
+    }
     float T[16];
     if (run) {
 #pragma unroll
@@ -450,6 +458,7 @@ ddlms_block_kernel(SolveArgs a, Slicer sl, const float4* __restrict__ XT, const 
             run = !(bound < fminf(o.margin[b], soft_tol)) || (a.mu * maxx2[b] > 1.0f);
         }
     }
+    if (list && !__syncthreads_or(run ? 1 : 0)) return;
     unsigned long long changed = 0;
     if (run) {
         const int64_t k0 = b * a.B;
@@ -541,10 +550,12 @@ ddlms_block_kernel(SolveArgs a, Slicer sl, const float4* __restrict__ XT, const 
                 T[8 + j] = fmaf(ei, X[j], T[8 + j]);
             }
             hsh = (hsh ^ static_cast<unsigned>(lab)) * 16777619u;
-            *sp = make_float2(yr, yi);
-            *lp = static_cast<uint8_t>(lab);
-            sp += nb;
-            lp += nb;
+            if (write_out) {   // outputs only from the final (full) pass
+                *sp = make_float2(yr, yi);
+                *lp = static_cast<uint8_t>(lab);
+                sp += nb;
+                lp += nb;
+            }
         }
         changed = (o.hash[b] != static_cast<unsigned long long>(hsh)) ? 1ull : 0ull;
         o.hash[b] = hsh;
@@ -589,6 +600,34 @@ ddlms_block_kernel(SolveArgs a, Slicer sl, const float4* __restrict__ XT, const 
         if (changed) atomicAdd(o.counters + 0, changed);
         if (rr) atomicAdd(o.counters + 1, rr);
     }
+}
+
+// Which blocks must re-run: |T_new - T_used|_F * max|x| >= min(margin, tol)
+// (decision / guard margin certificate, soft tolerance), compacted into a
+// list (warp-aggregated append; block order inside a warp preserved).
+__global__ void ddlms_select_kernel(const float* __restrict__ Tstart, const float* __restrict__ Tused,
+                                    const float* __restrict__ margin, const float* __restrict__ maxx2, float mu,
+                                    int64_t nb, float tol, int* __restrict__ list,
+                                    unsigned long long* __restrict__ list_n) {
+    const int64_t b = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    bool run = false;
+    if (b < nb) {
+        float d2 = 0.f;
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+            const float d = Tstart[b * 16 + i] - Tused[b * 16 + i];
+            d2 = fmaf(d, d, d2);
+        }
+        const float bound = sqrtf(d2 * maxx2[b]);
+        run = !(bound < fminf(margin[b], tol)) || (mu * maxx2[b] > 1.0f);
+    }
+    const unsigned m = __ballot_sync(0xffffffffu, run);
+    if (!m) return;
+    const int lane = threadIdx.x & 31;
+    unsigned long long base = 0;
+    if (lane == 0) base = atomicAdd(list_n, static_cast<unsigned long long>(__popc(m)));
+    base = __shfl_sync(0xffffffffu, base, 0);
+    if (run) list[base + __popc(m & ((1u << lane) - 1u))] = static_cast<int>(b);
 }
 
 // fold groups of G (<= 32) consecutive maps:  (P, Q) <- (P P_c, Q P_c + Q_c)
@@ -952,6 +991,7 @@ Layout plan(int64_t nsym, int B) {
     b += align_up(size_t(B + 1) * L.nb * 16);            // XT (block-interleaved input)
     b += align_up(size_t(B) * L.nb * 8);                 // ST
     b += align_up(size_t(B) * L.nb);                     // LT
+    b += align_up(L.nb * sizeof(int));                   // re-run list
     b += align_up(4 * sizeof(unsigned long long));
     L.bytes = b;
     return L;
@@ -992,6 +1032,7 @@ struct DdlmsSolver {
     int* over;
     unsigned long long *hsh, *ctr;
     float4* XT;
+    int* list;
     int64_t bt = 0;
     bool speculated = false;
     int64_t iters = 0, reruns = 0, last_changed = 0;
@@ -1065,15 +1106,22 @@ struct DdlmsSolver {
         fill_T_kernel<<<static_cast<unsigned>(((b1 - b0) * 16 + 127) / 128), 128, 0, s>>>(lv[0].T, b0, b1, src_dev);
         return check_launch("fill_T_kernel");
     }
-    int run_blocks(bool with_p, int64_t b0, int64_t b1, int use_skip) {
+    int run_blocks(bool with_p, int64_t b0, int64_t b1, int use_skip, float tol = 0.f, int write_out = 0) {
         if (b1 <= b0) return KK_OK;
         const unsigned g = static_cast<unsigned>((b1 - b0 + 127) / 128);
         if (with_p)
-            ddlms_block_kernel<true><<<g, 128, 0, s>>>(a, sl, XT, lv[0].T, lv[0].P, maxx2, o, to, b0, b1, 0,
-                                                       soft_tol);
-        else
-            ddlms_block_kernel<false><<<g, 128, 0, s>>>(a, sl, XT, lv[0].T, lv[0].P, maxx2, o, to, b0, b1, use_skip,
-                                                        soft_tol);
+            ddlms_block_kernel<true><<<g, 128, 0, s>>>(a, sl, XT, lv[0].T, lv[0].P, maxx2, o, to, b0, b1, 0, tol,
+                                                       nullptr, nullptr, write_out);
+        else if (!use_skip)
+            ddlms_block_kernel<false><<<g, 128, 0, s>>>(a, sl, XT, lv[0].T, lv[0].P, maxx2, o, to, b0, b1, 0, tol,
+                                                        nullptr, nullptr, write_out);
+        else {
+            // compact the blocks to re-run so that warps only carry live chains
+            ddlms_select_kernel<<<g, 128, 0, s>>>(lv[0].T, Tused, margin, maxx2, a.mu, L.nb, tol, list, ctr + 3);
+            if (int rc = check_launch("ddlms_select_kernel")) return rc;
+            ddlms_block_kernel<false><<<g, 128, 0, s>>>(a, sl, XT, lv[0].T, lv[0].P, maxx2, o, to, b0, b1, 0, tol,
+                                                        list, ctr + 3, write_out);
+        }
         return check_launch("ddlms_block_kernel");
     }
     int read_ctr(unsigned long long (&h)[4]) {
@@ -1111,6 +1159,7 @@ struct DdlmsSolver {
         XT = reinterpret_cast<float4*>(w); w += align_up(size_t(block + 1) * L.nb * 16);
         to.ST = reinterpret_cast<float2*>(w); w += align_up(size_t(block) * L.nb * 8);
         to.LT = reinterpret_cast<uint8_t*>(w); w += align_up(size_t(block) * L.nb);
+        list = reinterpret_cast<int*>(w); w += align_up(L.nb * sizeof(int));
         ctr = reinterpret_cast<unsigned long long*>(w);
         // the block kernels work on the raw input with the scale folded into
         // the taps: T' = s T, mu' = mu s^2 (y = T' x_raw == T (s x_raw))
@@ -1185,13 +1234,23 @@ struct DdlmsSolver {
         return frame_map(agg);
     }
 
-    // exact frame start taps -> re-run; returns changed blocks
-    int iterate(const float* T_start, int64_t* changed, int64_t* rerun, float* agg) {
+    // exact frame start taps -> re-run; returns changed blocks.  A
+    // decision pass re-runs only blocks whose certified decision margin the
+    // start-tap move could cross; a soft pass also refreshes every block
+    // whose soft outputs would move by more than soft_tol.
+    int iterate(const float* T_start, int64_t* changed, int64_t* rerun, float* agg, bool soft_pass) {
         if (!speculated) return set_error(KK_ERR_PARAM, "speculate() must precede iterate()");
         if (int rc = set_start(T_start)) return rc;
         if (int rc = scan_down()) return rc;
-        if (cudaMemsetAsync(ctr, 0, 2 * sizeof(unsigned long long), s) != cudaSuccess) return set_cuda_error("ctr");
-        if (int rc = run_blocks(false, 0, L.nb, 1)) return rc;
+        if (cudaMemsetAsync(ctr, 0, 2 * sizeof(unsigned long long), s) != cudaSuccess ||
+            cudaMemsetAsync(ctr + 3, 0, sizeof(unsigned long long), s) != cudaSuccess)
+            return set_cuda_error("ctr");
+        // decision pass: compacted re-run of the blocks whose certified margin
+        // the start move could cross, no outputs; final pass: every block,
+        // outputs written (soft exact for the final start taps)
+        if (int rc = soft_pass ? run_blocks(false, 0, L.nb, 0, 0.f, 1)
+                               : run_blocks(false, 0, L.nb, 1, 3.0e38f, 0))
+            return rc;
         unsigned long long h[4];
         if (int rc = read_ctr(h)) return rc;
         ++iters;
@@ -1276,11 +1335,11 @@ extern "C" int kk_ddlms_speculate(void* h, const float* T_guess_host, float* map
     return static_cast<DdlmsSolver*>(h)->speculate(T_guess_host, map_host);
 }
 
-extern "C" int kk_ddlms_iterate(void* h, const float* T_start_host, int64_t* changed, int64_t* rerun,
+extern "C" int kk_ddlms_iterate(void* h, const float* T_start_host, int soft_pass, int64_t* changed, int64_t* rerun,
                                 float* map_host) {
     clear_error();
     if (!h) return set_error(KK_ERR_PARAM, "null solver");
-    return static_cast<DdlmsSolver*>(h)->iterate(T_start_host, changed, rerun, map_host);
+    return static_cast<DdlmsSolver*>(h)->iterate(T_start_host, changed, rerun, map_host, soft_pass != 0);
 }
 
 extern "C" int kk_ddlms_finish(void* h, uint8_t* labels, void* soft, float* T_final_host, int64_t* guard) {
@@ -1314,14 +1373,16 @@ extern "C" int kk_ddlms_solve(const void* x, int64_t nsym, float scale, const vo
     if (int rc = sv.speculate(sv.bt > 0 ? Tg : T_init, nullptr)) return rc;
     int64_t st[6] = {0, 0, 0, 0, 0, sv.L.nb};
     bool converged = false;
+    bool soft_pass = false;   // decision passes until nothing changes, then one soft refresh
     for (int it = 1; it <= max_iter; ++it) {
         int64_t ch = 0, rr = 0;
-        if (int rc = sv.iterate(T_init, &ch, &rr, nullptr)) return rc;
+        if (int rc = sv.iterate(T_init, &ch, &rr, nullptr, soft_pass)) return rc;
         if (stats && it <= 16) {
             stats[6 + 2 * (it - 1)] = ch;
             stats[7 + 2 * (it - 1)] = rr;
         }
-        if (ch == 0) { converged = true; break; }
+        if (ch == 0 && soft_pass) { converged = true; break; }
+        soft_pass = (ch == 0);
     }
     int64_t guard = 0;
     if (converged) {

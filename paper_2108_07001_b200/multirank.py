@@ -90,14 +90,16 @@ def solve_chained(solver, comm, T_init, has_training: bool, max_iter: int = 64):
     T_te = comm.broadcast(T_te, src=0).astype(np.float32)
     mp = solver.speculate(T_te)
     per_iter = []
+    soft_pass = False    # decision passes until no rank changed, then one soft refresh
     for it in range(1, max_iter + 1):
         maps = comm.all_gather(mp)
         T_start = compose_start(T_init, maps, rank)
-        changed, rerun, mp = solver.iterate(T_start)
+        changed, rerun, mp = solver.iterate(T_start, soft_pass)
         total = comm.all_reduce_sum(changed)
         per_iter.append((int(changed), int(rerun), int(total)))
-        if total == 0:
+        if total == 0 and soft_pass:
             return it, per_iter
+        soft_pass = total == 0
     raise RuntimeError("multi-rank DDLMS did not converge within max_iter")
 
 
@@ -135,12 +137,13 @@ class GpuFrameSolver:
         _lib.call("kk_ddlms_speculate", self.h, T.ctypes.data, mp.ctypes.data)
         return mp
 
-    def iterate(self, T):
+    def iterate(self, T, soft_pass=False):
         mp = np.zeros(MAP_LEN, np.float32)
         ch = ctypes.c_int64(0)
         rr = ctypes.c_int64(0)
         T = np.ascontiguousarray(T, np.float32)
-        _lib.call("kk_ddlms_iterate", self.h, T.ctypes.data, ctypes.byref(ch), ctypes.byref(rr), mp.ctypes.data)
+        _lib.call("kk_ddlms_iterate", self.h, T.ctypes.data, int(bool(soft_pass)), ctypes.byref(ch),
+                  ctypes.byref(rr), mp.ctypes.data)
         return ch.value, rr.value, mp
 
     def finish(self):

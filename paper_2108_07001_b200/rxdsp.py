@@ -116,7 +116,7 @@ class GpuOptions:
     F (symbols, global grid), fixpoint iteration cap, soft-output tolerance
     of the block-skip certificate."""
 
-    ddlms_block: int = 512
+    ddlms_block: int = 1024
     ddlms_frame_symbols: int = 1 << 28
     ddlms_max_iter: int = 64
     ddlms_soft_tol: float = 1e-5

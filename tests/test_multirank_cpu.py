@@ -85,7 +85,7 @@ class NumpyFrameSolver:
             self._run(b, Tg)
         return self._map()
 
-    def iterate(self, Ts):
+    def iterate(self, Ts, soft_pass=False):
         T = np.asarray(Ts, np.float64).reshape(2, 8)
         changed = 0
         for b in range(len(self.blocks)):
