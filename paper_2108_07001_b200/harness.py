@@ -16,6 +16,7 @@ from .metrics import SyncFailure, count_bit_errors, evm, frame_sync, q_from_ber,
 from .rxdsp import (
     DdlmsConfig, GpuOptions, RxPipeline, RxPipelineConfig, compute_static_taps, demap, design_receive_taps,
 )
+
 from .sigcore import BlockPlan
 
 
@@ -83,3 +84,68 @@ def device_ber(labels, ref_idx, order: int, head: int, stop: int, tile_symbols: 
         return count_bit_errors(lab, ref, order, exclude_period=tile_symbols, exclude_len=seam_guard,
                                 exclude_phase=index0 + head)[:2]
     return count_bit_errors(lab, ref, order)[:2]
+
+
+def receive_host_stream(cfg, host_codes, half_lsb: float, reference_symbols, chunk_samples: int = 1 << 26,
+                        labels_host=None, device=None):
+    """End-to-end receive of an int16 ADC stream in pinned HOST memory.
+
+    The stream is copied in chunks on a side stream (double-buffered) while
+    the compute stream runs the receiver on the previous chunk, and the
+    decided labels of every completed DDLMS frame are copied back to
+    (pinned) host memory as they are released -- PCIe traffic overlaps the
+    GPU work.  Returns (pipe, labels_host[:n], n_decided).
+    """
+    import torch
+
+    from .sigcore import AdcCodes
+
+    dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+    n = int(host_codes.shape[0])
+    comp = torch.cuda.current_stream(dev)
+    copy = torch.cuda.Stream(device=dev)
+    d2h = torch.cuda.Stream(device=dev)
+    bufs = [torch.empty(chunk_samples, dtype=torch.int16, device=dev) for _ in range(3)]
+    ready = [torch.cuda.Event() for _ in range(3)]
+    free = [torch.cuda.Event() for _ in range(3)]
+    pipe = RxPipeline(cfg, reference_symbols=reference_symbols, device=dev)
+    pipe.expect(n, chunk_samples)
+    if labels_host is None:
+        labels_host = torch.empty(n // 4 + 8, dtype=torch.uint8, pin_memory=True)
+    n_out = 0
+    starts = list(range(0, n, chunk_samples))
+
+    def issue_copy(i):
+        a = starts[i]
+        m = min(chunk_samples, n - a)
+        k = i % 3
+        with torch.cuda.stream(copy):
+            if i >= 3:
+                copy.wait_event(free[k])
+            bufs[k][:m].copy_(host_codes[a:a + m], non_blocking=True)
+            ready[k].record(copy)
+
+    issue_copy(0)
+    if len(starts) > 1:
+        issue_copy(1)
+    for i, a in enumerate(starts):
+        k = i % 3
+        m = min(chunk_samples, n - a)
+        comp.wait_event(ready[k])
+        last = i == len(starts) - 1
+        pipe.feed(AdcCodes(bufs[k][:m], half_lsb, cfg.adc_rate_hz), flush=last)
+        # the buffer may still back the raw FIFO tail until the next feed
+        if i >= 1:
+            free[(i - 1) % 3].record(comp)
+        if i + 2 < len(starts):
+            issue_copy(i + 2)
+        lab, _, _ = pipe.drain_device()
+        if lab.numel():
+            # device -> host on its own stream (the other DMA direction)
+            d2h.wait_stream(comp)
+            with torch.cuda.stream(d2h):
+                labels_host[n_out:n_out + lab.numel()].copy_(lab, non_blocking=True)
+            lab.record_stream(d2h)
+            n_out += lab.numel()
+    comp.wait_stream(d2h)
+    return pipe, labels_host, n_out

@@ -289,6 +289,17 @@ class _DevStream:
     def commit(self, n: int):
         self.end += n
 
+    def ensure_capacity(self, n: int):
+        """Pre-size the buffer for n live items (avoids growth copies)."""
+        if self.buf.shape[0] >= n:
+            return
+        live0 = max(self.keep, self.base)
+        live = self.end - live0
+        nb = self.torch.empty(max(n, live), dtype=self.buf.dtype, device=self.buf.device)
+        if live > 0:
+            nb[:live].copy_(self.buf[live0 - self.base:self.end - self.base])
+        self.buf, self.base = nb, live0
+
     def view(self, g0: int, g1: int):
         return self.buf[g0 - self.base:g1 - self.base]
 
@@ -976,6 +987,15 @@ class RxPipeline:
         self._chunk_index += 1
         if flush:
             self._flushed = True
+
+    def expect(self, n_samples: int, chunk_samples: int | None = None) -> None:
+        """Capacity hint for a stream of n_samples fed in chunks of
+        chunk_samples: pre-sizes the 2-sps buffer for one DDLMS frame and the
+        KK output window, so streaming feeds never re-grow device buffers."""
+        F = int(self.gpu.ddlms_frame_symbols)
+        self._y2.ensure_capacity(min(n_samples // 2, 2 * F + 2 * self.cfg.static_plan.hop) + 16)
+        c = chunk_samples or n_samples
+        self._z.ensure_capacity(min(n_samples, c + 2 * self.cfg.carrier_segment_len + self.cfg.static_plan.hop))
 
     def front_end(self, adc_chunk, flush: bool = False) -> None:
         """KK -> carrier -> downshift -> static stages only (the DDLMS is
