@@ -66,11 +66,12 @@ def load():
     global _lib
     if _lib is not None:
         return _lib
-    if not os.path.exists(LIB_PATH):
+    path = os.environ.get("KKB200_LIB") or LIB_PATH   # variant builds (tools/) only
+    if not os.path.exists(path):
         raise RuntimeError(
-            f"CUDA library {LIB_PATH} is missing: build it with "
+            f"CUDA library {path} is missing: build it with "
             "`python -m paper_2108_07001_b200.build` (no CPU fallback exists)")
-    lib = ctypes.CDLL(LIB_PATH)
+    lib = ctypes.CDLL(path)
     for name, (args, res) in _SIGS.items():
         fn = getattr(lib, name)
         fn.argtypes = args

@@ -49,39 +49,48 @@ def _digest() -> str:
     return h.hexdigest()
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    os.makedirs(OUT_DIR, exist_ok=True)
-    stamp = os.path.join(OUT_DIR, "build.sha256")
-    dig = _digest()
-    if not force and os.path.exists(LIB) and os.path.exists(stamp):
+def build(force: bool = False, verbose: bool = False, defines=(), name: str = "") -> str:
+    """Build the library; `defines`/`name` make a tuning variant at
+    _lib/variants/libkkb200_<name>.so (load it with KKB200_LIB=...)."""
+    out_dir = os.path.join(OUT_DIR, "variants", name) if name else OUT_DIR
+    lib_path = os.path.join(out_dir, f"libkkb200_{name}.so") if name else LIB
+    os.makedirs(out_dir, exist_ok=True)
+    stamp = os.path.join(out_dir, "build.sha256")
+    flags = NVCC_FLAGS + [f"-D{d}" for d in defines]
+    dig = _digest() + " ".join(flags)
+    if not force and os.path.exists(lib_path) and os.path.exists(stamp):
         with open(stamp) as f:
             if f.read().strip() == dig:
-                return LIB
+                return lib_path
     nvcc = _nvcc()
     objs = []
     logs = []
     for src in SOURCES:
-        obj = os.path.join(OUT_DIR, src.replace(".cu", ".o"))
-        cmd = [nvcc, *NVCC_FLAGS, "-I", os.path.join(REPO, "include"), "-dc" if False else "-c",
+        obj = os.path.join(out_dir, src.replace(".cu", ".o"))
+        cmd = [nvcc, *flags, "-I", os.path.join(REPO, "include"), "-dc" if False else "-c",
                os.path.join(CSRC, src), "-o", obj]
         r = subprocess.run(cmd, capture_output=True, text=True)
         logs.append(f"$ {' '.join(cmd)}\n{r.stdout}{r.stderr}")
         if r.returncode != 0:
             raise RuntimeError(f"nvcc failed for {src}:\n{r.stdout}\n{r.stderr}")
         objs.append(obj)
-    cmd = [nvcc, "-shared", "-gencode", "arch=compute_100a,code=sm_100a", *objs, "-o", LIB]
+    cmd = [nvcc, "-shared", "-gencode", "arch=compute_100a,code=sm_100a", *objs, "-o", lib_path]
     r = subprocess.run(cmd, capture_output=True, text=True)
     logs.append(f"$ {' '.join(cmd)}\n{r.stdout}{r.stderr}")
     if r.returncode != 0:
         raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")
-    with open(os.path.join(OUT_DIR, "build.log"), "w") as f:
+    with open(os.path.join(out_dir, "build.log"), "w") as f:
         f.write("\n".join(logs))
     with open(stamp, "w") as f:
         f.write(dig)
     if verbose:
         print("\n".join(logs))
-    return LIB
+    return lib_path
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))
+    # python -m paper_2108_07001_b200.build [--force] [-v] [--variant NAME -DX=1 ...]
+    av = sys.argv[1:]
+    nm = av[av.index("--variant") + 1] if "--variant" in av else ""
+    print(build(force="--force" in av, verbose="-v" in av, name=nm,
+                defines=[a[2:] for a in av if a.startswith("-D")]))

@@ -335,13 +335,24 @@ __global__ void fill_T_kernel(float* __restrict__ T, int64_t b0, int64_t b1, con
 // are written back the same way.  WITH_P additionally accumulates the
 // decision-independent block map P_b and max|X|^2 (fused first pass).
 // ---------------------------------------------------------------------------
-// Block-interleaved ("transposed") layout for the block-parallel passes:
-// XT[i * nb + b] = (x[2(bB+i)], x[2(bB+i)+1]) (one float4 = two 2-sps samples)
-// for pair i in [0, B] of block b, so that thread b's sequential recurrence
-// reads XT[i][b] while its 31 warp neighbours read XT[i][b+1..b+31]: every
-// load is a fully coalesced 512-byte warp transaction, with no staging.
-// Outputs are written the same way (ST / LT) and un-transposed once.
+// Warp-tiled block-interleaved layout for the block-parallel passes.  Blocks
+// are grouped in tiles of 32 (one warp); inside a tile, row i holds pair i of
+// the 32 blocks side by side:
+//   XT[tix(b, i, B + 1)] = (x[2(bB+i)], x[2(bB+i)+1])   (one float4 = two 2-sps samples)
+// so thread b's sequential recurrence reads row i while its 31 warp
+// neighbours read the rest of the same 512-byte row (coalesced), and a warp's
+// whole stream is one contiguous (B+1) x 512 B region (TLB-local: a plain
+// [i][b] interleave strides nb x 16 B per symbol and misses the TLB on every
+// load when few warps are resident).  Outputs (ST / LT) use the same tiling
+// and are un-tiled once.
 // ---------------------------------------------------------------------------
+__host__ __device__ __forceinline__ int64_t tix(int64_t b, int i, int rows) {
+    return ((b >> 5) * rows + i) * 32 + (b & 31);
+}
+__host__ __device__ __forceinline__ int64_t tiled_elems(int64_t nb, int rows) {
+    return ((nb + 31) >> 5) * int64_t(rows) * 32;
+}
+
 __global__ void ddlms_transpose_in(const float2* __restrict__ x, int64_t nsym, int B, int64_t nb,
                                    float4* __restrict__ XT) {
     __shared__ float4 tile[32][33];
@@ -365,7 +376,7 @@ __global__ void ddlms_transpose_in(const float2* __restrict__ x, int64_t nsym, i
     for (int ii = ty; ii < 32; ii += 8) {
         const int i = i0 + ii;
         const int64_t b = b0 + tx;
-        if (i <= B && b < nb) XT[int64_t(i) * nb + b] = tile[tx][ii];
+        if (i <= B && b < nb) XT[tix(b, i, B + 1)] = tile[tx][ii];
     }
 }
 
@@ -380,8 +391,8 @@ __global__ void ddlms_transpose_out(const float2* __restrict__ ST, const uint8_t
         const int i = i0 + ii;
         const int64_t b = b0 + tx;
         if (i < B && b < nb) {
-            ts[ii][tx] = ST[int64_t(i) * nb + b];
-            tl[ii][tx] = LT[int64_t(i) * nb + b];
+            ts[ii][tx] = ST[tix(b, i, B)];
+            tl[ii][tx] = LT[tix(b, i, B)];
         }
     }
     __syncthreads();
@@ -395,6 +406,25 @@ __global__ void ddlms_transpose_out(const float2* __restrict__ ST, const uint8_t
         }
     }
 }
+
+#ifndef KK_DD_MINB
+#define KK_DD_MINB 4      // resident CTAs / SM of the decision passes
+#endif
+constexpr int kRing = 16;   // cp.async input ring depth (power of two)
+constexpr int kBlockThreads = 128;
+constexpr size_t kRingSmem = size_t(kRing) * kBlockThreads * (sizeof(float4) + sizeof(float2));
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* g, int src_bytes) {
+    const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(sa), "l"(g), "r"(src_bytes) : "memory");
+}
+__device__ __forceinline__ void cp_async8(void* smem, const void* g) {
+    const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(g) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
 
 struct LeanSlicer {
     int square, m;
@@ -415,7 +445,7 @@ struct TOut {
 // boundary.  WITH_P (first pass) also accumulates P_b = prod (I - 2 mu' x x^T)
 // and max |x|^2.  Reads / writes use the block-interleaved layout (coalesced).
 template <bool WITH_P>
-__global__ void __launch_bounds__(128, WITH_P ? 3 : 6)
+__global__ void __launch_bounds__(kBlockThreads, WITH_P ? 3 : KK_DD_MINB)
 ddlms_block_kernel(SolveArgs a, Slicer sl, const float4* __restrict__ XT, const float* __restrict__ Tstart,
                    float* __restrict__ Pb, float* __restrict__ maxx2, RunOut o, TOut to, int64_t b_lo,
                    int64_t b_hi, int use_skip, float soft_tol, const int* __restrict__ list,
@@ -432,7 +462,6 @@ ddlms_block_kernel(SolveArgs a, Slicer sl, const float4* __restrict__ XT, const 
     const int m1 = sl.m - 1;
     const float half_norm = 0.5f * sl.norm, off = 0.5f * (sl.m - 1);
     const float thr2 = sl.thr * sl.thr;
-    const int64_t nb = a.nb;
 
     int64_t b = b_lo + int64_t(blockIdx.x) * blockDim.x + tid;
     bool run;
@@ -473,25 +502,41 @@ ddlms_block_kernel(SolveArgs a, Slicer sl, const float4* __restrict__ XT, const 
         float mgl = 0.5f, mgb = 3.0e38f, mx = 0.f, my2 = 0.f;
         unsigned hsh = 2166136261u;
         float X[8];
-        const float4* xp = XT + b;
-        float2* sp = to.ST + b;
-        uint8_t* lp = to.LT + b;
+        const float4* xp = XT + tix(b, 0, a.B + 1);
+        float2* sp = to.ST + tix(b, 0, a.B);
+        uint8_t* lp = to.LT + tix(b, 0, a.B);
         {
             const float4 w = __ldg(xp);
             X[4] = w.x; X[5] = w.y; X[6] = w.z; X[7] = w.w;
         }
-        xp += nb;
-        // software pipeline: 4 pair loads in flight (XT has B+1 rows; rows
-        // past the block's valid symbols are zero-filled and never used)
-        float4 q0 = __ldg(xp), q1 = __ldg(xp + nb), q2 = __ldg(xp + 2 * nb), q3;
-        xp += 3 * nb;
-        const float4* xend = XT + b + int64_t(a.B) * nb;
+        // Input pipeline: a per-thread ring of kRing smem slots filled by
+        // cp.async (one commit group per row), kRing - 1 rows in flight.
+        // Register-destination prefetches do not work here: ptxas folds the
+        // ring loads onto shared scoreboards and the chain then waits on the
+        // newest load every symbol (measured: ~1400 cycles / symbol).
+        // Slot r & (kRing-1) holds pair row r and training symbol r - 1, both
+        // consumed by symbol i = r - 1.
+        extern __shared__ float4 ring_sm[];
+        const int nt = blockDim.x;
+        float4* xr = ring_sm + tid;
+        float2* tr = reinterpret_cast<float2*>(ring_sm + kRing * nt) + tid;
+        const float2* tg = a.train + k0 - 1;
+        auto issue = [&](int r) {
+            const int sl_ = r & (kRing - 1);
+            cp_async16(xr + sl_ * nt, xp + int64_t(r) * 32, r <= a.B ? 16 : 0);
+            if (r - 1 < ntr) cp_async8(tr + sl_ * nt, tg + r);
+            cp_async_commit();
+        };
+#pragma unroll 1
+        for (int r = 1; r < kRing; ++r) issue(r);
+#pragma unroll 2
         for (int i = 0; i < nk; ++i) {
-            q3 = (xp <= xend) ? __ldg(xp) : make_float4(0.f, 0.f, 0.f, 0.f);
-            xp += nb;
+            cp_async_wait<kRing - 2>();
+            const int sl_ = (i + 1) & (kRing - 1);
+            const float4 w = xr[sl_ * nt];
+            issue(i + kRing);
             X[0] = X[4]; X[1] = X[5]; X[2] = X[6]; X[3] = X[7];
-            X[4] = q0.x; X[5] = q0.y; X[6] = q0.z; X[7] = q0.w;
-            q0 = q1; q1 = q2; q2 = q3;
+            X[4] = w.x; X[5] = w.y; X[6] = w.z; X[7] = w.w;
             float ya = 0.f, yb = 0.f, za = 0.f, zb = 0.f;
 #pragma unroll
             for (int j = 0; j < 8; j += 2) {
@@ -504,7 +549,7 @@ ddlms_block_kernel(SolveArgs a, Slicer sl, const float4* __restrict__ XT, const 
             float dr, di;
             int lab;
             if (i < ntr) {
-                const float2 t = __ldg(a.train + k0 + i);
+                const float2 t = tr[((i + 1) & (kRing - 1)) * nt];
                 dr = t.x; di = t.y;
                 lab = 255;
             } else if (square) {
@@ -553,10 +598,11 @@ ddlms_block_kernel(SolveArgs a, Slicer sl, const float4* __restrict__ XT, const 
             if (write_out) {   // outputs only from the final (full) pass
                 *sp = make_float2(yr, yi);
                 *lp = static_cast<uint8_t>(lab);
-                sp += nb;
-                lp += nb;
+                sp += 32;
+                lp += 32;
             }
         }
+        cp_async_wait<0>();
         changed = (o.hash[b] != static_cast<unsigned long long>(hsh)) ? 1ull : 0ull;
         o.hash[b] = hsh;
         // Q_b = T_end - T_start P_b
@@ -988,9 +1034,9 @@ Layout plan(int64_t nsym, int B) {
     b += align_up(16 * sizeof(float)) * 2;      // Tend, Tinit
     b += align_up(L.nb * sizeof(int));          // over
     b += align_up(L.nb * sizeof(unsigned long long));   // label hashes
-    b += align_up(size_t(B + 1) * L.nb * 16);            // XT (block-interleaved input)
-    b += align_up(size_t(B) * L.nb * 8);                 // ST
-    b += align_up(size_t(B) * L.nb);                     // LT
+    b += align_up(size_t(tiled_elems(L.nb, B + 1)) * 16);   // XT (warp-tiled input)
+    b += align_up(size_t(tiled_elems(L.nb, B)) * 8);        // ST
+    b += align_up(size_t(tiled_elems(L.nb, B)));            // LT
     b += align_up(L.nb * sizeof(int));                   // re-run list
     b += align_up(4 * sizeof(unsigned long long));
     L.bytes = b;
@@ -1108,18 +1154,29 @@ struct DdlmsSolver {
     }
     int run_blocks(bool with_p, int64_t b0, int64_t b1, int use_skip, float tol = 0.f, int write_out = 0) {
         if (b1 <= b0) return KK_OK;
-        const unsigned g = static_cast<unsigned>((b1 - b0 + 127) / 128);
+        static thread_local int attr_dev = -1;
+        int dev = 0;
+        cudaGetDevice(&dev);
+        if (attr_dev != dev) {
+            if (cudaFuncSetAttribute(ddlms_block_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     static_cast<int>(kRingSmem)) != cudaSuccess ||
+                cudaFuncSetAttribute(ddlms_block_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     static_cast<int>(kRingSmem)) != cudaSuccess)
+                return set_cuda_error("ddlms_block_kernel smem attribute");
+            attr_dev = dev;
+        }
+        const unsigned g = static_cast<unsigned>((b1 - b0 + kBlockThreads - 1) / kBlockThreads);
         if (with_p)
-            ddlms_block_kernel<true><<<g, 128, 0, s>>>(a, sl, XT, lv[0].T, lv[0].P, maxx2, o, to, b0, b1, 0, tol,
+            ddlms_block_kernel<true><<<g, kBlockThreads, kRingSmem, s>>>(a, sl, XT, lv[0].T, lv[0].P, maxx2, o, to, b0, b1, 0, tol,
                                                        nullptr, nullptr, write_out);
         else if (!use_skip)
-            ddlms_block_kernel<false><<<g, 128, 0, s>>>(a, sl, XT, lv[0].T, lv[0].P, maxx2, o, to, b0, b1, 0, tol,
+            ddlms_block_kernel<false><<<g, kBlockThreads, kRingSmem, s>>>(a, sl, XT, lv[0].T, lv[0].P, maxx2, o, to, b0, b1, 0, tol,
                                                         nullptr, nullptr, write_out);
         else {
             // compact the blocks to re-run so that warps only carry live chains
             ddlms_select_kernel<<<g, 128, 0, s>>>(lv[0].T, Tused, margin, maxx2, a.mu, L.nb, tol, list, ctr + 3);
             if (int rc = check_launch("ddlms_select_kernel")) return rc;
-            ddlms_block_kernel<false><<<g, 128, 0, s>>>(a, sl, XT, lv[0].T, lv[0].P, maxx2, o, to, b0, b1, 0, tol,
+            ddlms_block_kernel<false><<<g, kBlockThreads, kRingSmem, s>>>(a, sl, XT, lv[0].T, lv[0].P, maxx2, o, to, b0, b1, 0, tol,
                                                         list, ctr + 3, write_out);
         }
         return check_launch("ddlms_block_kernel");
@@ -1156,9 +1213,9 @@ struct DdlmsSolver {
         Tinit_d = reinterpret_cast<float*>(w); w += align_up(16 * sizeof(float));
         over = reinterpret_cast<int*>(w); w += align_up(L.nb * sizeof(int));
         hsh = reinterpret_cast<unsigned long long*>(w); w += align_up(L.nb * 8);
-        XT = reinterpret_cast<float4*>(w); w += align_up(size_t(block + 1) * L.nb * 16);
-        to.ST = reinterpret_cast<float2*>(w); w += align_up(size_t(block) * L.nb * 8);
-        to.LT = reinterpret_cast<uint8_t*>(w); w += align_up(size_t(block) * L.nb);
+        XT = reinterpret_cast<float4*>(w); w += align_up(size_t(tiled_elems(L.nb, block + 1)) * 16);
+        to.ST = reinterpret_cast<float2*>(w); w += align_up(size_t(tiled_elems(L.nb, block)) * 8);
+        to.LT = reinterpret_cast<uint8_t*>(w); w += align_up(size_t(tiled_elems(L.nb, block)));
         list = reinterpret_cast<int*>(w); w += align_up(L.nb * sizeof(int));
         ctr = reinterpret_cast<unsigned long long*>(w);
         // the block kernels work on the raw input with the scale folded into

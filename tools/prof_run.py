@@ -16,7 +16,10 @@ log2n = int(sys.argv[1]) if len(sys.argv) > 1 else 24
 reps = int(sys.argv[2]) if len(sys.argv) > 2 else 2
 cap = load_capture("c5_qpsk_10000km_tile")
 codes, _ = tile(cap, 1 << log2n)
-cfg = cap.pipeline_config()
+gpu_kw = {}
+if os.environ.get("KK_FRAME_LOG2"):
+    gpu_kw["ddlms_frame_symbols"] = 1 << int(os.environ["KK_FRAME_LOG2"])
+cfg = cap.pipeline_config(**gpu_kw)
 ref = cap.symbols()[:10000]
 dev = torch.device("cuda", 0)
 cd = torch.from_numpy(codes).to(dev)
