@@ -147,6 +147,9 @@ int kk_ddlms_solve(const void *x, int64_t nsym, float scale, const void *train, 
  *                       those whose soft outputs would move > soft_tol);
  *                       changed blocks -> map
  *   finish              labels / soft / end taps / guard exceedances
+ * kk_ddlms_bind_outputs (optional, before the final iterate) makes the final
+ * pass write labels / soft straight into the caller's device arrays; finish
+ * then copies nothing when given the same pointers.
  */
 void *kk_ddlms_create(const void *x, int64_t nsym, float scale, const void *train, int64_t n_train, int order,
                       const float *pts_host, const uint8_t *grid_host, int grid_m, float norm, float max_radius,
@@ -156,6 +159,7 @@ int kk_ddlms_train(void *solver, const float *T_start_host, float *T_train_end_h
 int kk_ddlms_speculate(void *solver, const float *T_guess_host, float *map_host);
 int kk_ddlms_iterate(void *solver, const float *T_start_host, int soft_pass, int64_t *changed_blocks,
                      int64_t *rerun_blocks, float *map_host);
+int kk_ddlms_bind_outputs(void *solver, uint8_t *labels, void *soft);
 int kk_ddlms_finish(void *solver, uint8_t *labels, void *soft, float *T_final_host, int64_t *guard_exceed);
 void kk_ddlms_destroy(void *solver);
 

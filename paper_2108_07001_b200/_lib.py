@@ -51,6 +51,7 @@ _SIGS = {
     "kk_ddlms_train": ([_P, _P, _P], _I),
     "kk_ddlms_speculate": ([_P, _P, _P], _I),
     "kk_ddlms_iterate": ([_P, _P, _I, _P, _P, _P], _I),
+    "kk_ddlms_bind_outputs": ([_P, _P, _P], _I),
     "kk_ddlms_finish": ([_P, _P, _P, _P, _P], _I),
     "kk_ddlms_destroy": ([_P], None),
     "kk_bit_errors": ([_P, _P, _I64, _P, _I64, _P, _P, _I64, _I64, _I64, _P, _P], _I),

@@ -43,6 +43,8 @@ struct Slicer {
     float thr;         // guard: divergence_factor * max_radius
     float2 pts[64];
     uint8_t grid[64];  // (i_re * m + i_im) -> point index (square)
+    int sep;           // square grid whose points are exactly ((2 i_re - (m-1)) h, (2 i_im - (m-1)) h) in fp32
+    float lev_h;
 };
 
 // returns point index, sets decision value and margin (distance to the
@@ -328,99 +330,32 @@ __global__ void fill_T_kernel(float* __restrict__ T, int64_t b0, int64_t b1, con
     if (i < n) T[b0 * 16 + i] = src[i & 15];
 }
 
-// Block-parallel DDLMS pass, one thread per block of B symbols, 128 blocks per
-// CTA.  Each thread's recurrence is sequential, so the inputs are staged per
-// chunk of C symbols through shared memory (a warp loads each of its threads'
-// contiguous 2C+2-sample segments coalesced) and the outputs (labels, soft)
-// are written back the same way.  WITH_P additionally accumulates the
-// decision-independent block map P_b and max|X|^2 (fused first pass).
+// Block-parallel DDLMS passes (ddlms_block_kernel below): one thread per
+// block of B symbols, reading the 2-sps equalizer input in place (no
+// transposition) through a per-thread cp.async ring, and writing the final
+// soft / labels in natural order.
 // ---------------------------------------------------------------------------
-// Warp-tiled block-interleaved layout for the block-parallel passes.  Blocks
-// are grouped in tiles of 32 (one warp); inside a tile, row i holds pair i of
-// the 32 blocks side by side:
-//   XT[tix(b, i, B + 1)] = (x[2(bB+i)], x[2(bB+i)+1])   (one float4 = two 2-sps samples)
-// so thread b's sequential recurrence reads row i while its 31 warp
-// neighbours read the rest of the same 512-byte row (coalesced), and a warp's
-// whole stream is one contiguous (B+1) x 512 B region (TLB-local: a plain
-// [i][b] interleave strides nb x 16 B per symbol and misses the TLB on every
-// load when few warps are resident).  Outputs (ST / LT) use the same tiling
-// and are un-tiled once.
-// ---------------------------------------------------------------------------
-__host__ __device__ __forceinline__ int64_t tix(int64_t b, int i, int rows) {
-    return ((b >> 5) * rows + i) * 32 + (b & 31);
-}
-__host__ __device__ __forceinline__ int64_t tiled_elems(int64_t nb, int rows) {
-    return ((nb + 31) >> 5) * int64_t(rows) * 32;
-}
-
-__global__ void ddlms_transpose_in(const float2* __restrict__ x, int64_t nsym, int B, int64_t nb,
-                                   float4* __restrict__ XT) {
-    __shared__ float4 tile[32][33];
-    const int tx = threadIdx.x, ty = threadIdx.y;
-    const int64_t b0 = int64_t(blockIdx.x) * 32;
-    const int i0 = blockIdx.y * 32;
-    for (int bb = ty; bb < 32; bb += 8) {
-        const int64_t b = b0 + bb;
-        const int i = i0 + tx;
-        float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (b < nb && i <= B) {
-            const int64_t g = b * B + i;           // pair index: samples 2g, 2g+1
-            if (g <= nsym) {
-                const float2 a = __ldg(x + 2 * g), c = __ldg(x + 2 * g + 1);
-                v = make_float4(a.x, a.y, c.x, c.y);
-            }
-        }
-        tile[bb][tx] = v;
-    }
-    __syncthreads();
-    for (int ii = ty; ii < 32; ii += 8) {
-        const int i = i0 + ii;
-        const int64_t b = b0 + tx;
-        if (i <= B && b < nb) XT[tix(b, i, B + 1)] = tile[tx][ii];
-    }
-}
-
-__global__ void ddlms_transpose_out(const float2* __restrict__ ST, const uint8_t* __restrict__ LT, int64_t nsym,
-                                    int B, int64_t nb, float2* __restrict__ soft, uint8_t* __restrict__ labels) {
-    __shared__ float2 ts[32][33];
-    __shared__ uint8_t tl[32][33];
-    const int tx = threadIdx.x, ty = threadIdx.y;
-    const int64_t b0 = int64_t(blockIdx.x) * 32;
-    const int i0 = blockIdx.y * 32;
-    for (int ii = ty; ii < 32; ii += 8) {
-        const int i = i0 + ii;
-        const int64_t b = b0 + tx;
-        if (i < B && b < nb) {
-            ts[ii][tx] = ST[tix(b, i, B)];
-            tl[ii][tx] = LT[tix(b, i, B)];
-        }
-    }
-    __syncthreads();
-    for (int bb = ty; bb < 32; bb += 8) {
-        const int64_t b = b0 + bb;
-        const int i = i0 + tx;
-        const int64_t k = b * B + i;
-        if (b < nb && i < B && k < nsym) {
-            soft[k] = ts[tx][bb];
-            labels[k] = tl[tx][bb];
-        }
-    }
-}
-
 #ifndef KK_DD_MINB
 #define KK_DD_MINB 4      // resident CTAs / SM of the decision passes
 #endif
-constexpr int kRing = 16;   // cp.async input ring depth (power of two)
 constexpr int kBlockThreads = 128;
-constexpr size_t kRingSmem = size_t(kRing) * kBlockThreads * (sizeof(float4) + sizeof(float2));
 
 __device__ __forceinline__ void cp_async16(void* smem, const void* g, int src_bytes) {
     const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(smem));
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(sa), "l"(g), "r"(src_bytes) : "memory");
 }
-__device__ __forceinline__ void cp_async8(void* smem, const void* g) {
+__device__ __forceinline__ void cp_async8z(void* smem, const void* g, int src_bytes) {
     const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(smem));
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(g) : "memory");
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(sa), "l"(g), "r"(src_bytes) : "memory");
+}
+// predicated in PTX (-> SASS predicate, not a branch: a branch would make
+// ptxas wait on every outstanding shared load at the reconvergence point)
+__device__ __forceinline__ void cp_async8_if(bool pred, void* smem, const void* g) {
+    const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+    asm volatile(
+        "{\n .reg .pred p;\n setp.ne.b32 p, %2, 0;\n @p cp.async.ca.shared.global [%0], [%1], 8;\n}\n" ::"r"(sa),
+        "l"(g), "r"(static_cast<int>(pred))
+        : "memory");
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
 template <int N>
@@ -432,36 +367,64 @@ struct LeanSlicer {
 };
 
 struct TOut {
-    float2* ST;       // [B][nb] transposed soft
-    uint8_t* LT;      // [B][nb] transposed labels
+    float2* ST;       // [nsym] soft (final pass)
+    uint8_t* LT;      // [nsym] labels (final pass)
 };
 
 // Block-parallel DDLMS pass, one thread per block of B symbols.  Lean
-// per-symbol work (~75 instructions): the input scale s is folded into the
-// taps (T' = s T, mu' = mu s^2, so y = T' x_raw); Q_b is recovered once per
-// block as T_end - T_start P_b; decision changes are detected with a 32-bit
-// hash of the block's label sequence; the guard is tracked as max |y|^2 and
-// the decision margin conservatively as the distance to the nearest interior
+// per-symbol work: the input scale s is folded into the taps (T' = s T,
+// mu' = mu s^2, so y = T' x_raw); Q_b is recovered once per block as
+// T_end - T_start P_b; decision changes are detected with a 32-bit hash of
+// the block's label sequence; the guard is tracked as max |y|^2 and the
+// decision margin conservatively as the distance to the nearest interior
 // boundary.  WITH_P (first pass) also accumulates P_b = prod (I - 2 mu' x x^T)
-// and max |x|^2.  Reads / writes use the block-interleaved layout (coalesced).
-template <bool WITH_P>
+// and max |x|^2.  SQ > 0: separable square constellation with SQ levels per
+// axis -- branch-free arithmetic slicer; SQ == 0: table / brute-force slicer.
+//
+// Input staging (the 2-sps input x is read in place): a warp's 32 lanes own
+// 32 blocks; the warp loads chunks of 8 pair rows for all of them
+// cooperatively with cp.async (8 lanes x 16 B = one 128 B run of one block
+// per quarter warp), kChunks chunks in flight, into a swizzled smem ring
+// [chunk][row][lane]; each lane then reads its own column (conflict-free).
+// Register-destination prefetches were measured not to work here (ptxas
+// folds them onto shared scoreboards and the chain waits on the newest load).
+// TRAIN (launches covering blocks with training symbols): a per-thread
+// cp.async ring of training symbols as well.  Outputs (final pass) are
+// written per lane in 8-symbol runs (64 B soft, 8 B labels).
+constexpr int kChunkRows = 8;
+constexpr int kChunks = 3;
+constexpr int kTrainRing = 32;   // >= kChunks * kChunkRows symbols in flight
+constexpr size_t kWarpStage = size_t(kChunks) * kChunkRows * 32 * sizeof(float4);
+constexpr size_t kStageSmem = kWarpStage * (kBlockThreads / 32);
+constexpr size_t kTrainSmem = size_t(kTrainRing) * kBlockThreads * sizeof(float2);
+
+__device__ __forceinline__ int stage_idx(int chunk, int row, int col) {
+    return (chunk * kChunkRows + row) * 32 + (col ^ ((row * 4) & 31));
+}
+
+template <bool WITH_P, int SQ, bool AL16, bool TRAIN>
 __global__ void __launch_bounds__(kBlockThreads, WITH_P ? 3 : KK_DD_MINB)
-ddlms_block_kernel(SolveArgs a, Slicer sl, const float4* __restrict__ XT, const float* __restrict__ Tstart,
-                   float* __restrict__ Pb, float* __restrict__ maxx2, RunOut o, TOut to, int64_t b_lo,
-                   int64_t b_hi, int use_skip, float soft_tol, const int* __restrict__ list,
-                   const unsigned long long* __restrict__ list_n, int write_out) {
+ddlms_block_kernel(SolveArgs a, Slicer sl, const float* __restrict__ Tstart, float* __restrict__ Pb,
+                   float* __restrict__ maxx2, RunOut o, TOut to, int64_t b_lo, int64_t b_hi, int use_skip,
+                   float soft_tol, const int* __restrict__ list, const unsigned long long* __restrict__ list_n,
+                   int write_out) {
     __shared__ float2 pts[64];
     __shared__ uint8_t grid[64];
-    const int tid = threadIdx.x, lane = tid & 31;
+    extern __shared__ float4 dyn_sm[];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     if (tid < 64) {
         pts[tid] = sl.pts[tid];
         grid[tid] = sl.grid[tid];
     }
     __syncthreads();
-    const bool square = sl.kind == 0;
-    const int m1 = sl.m - 1;
-    const float half_norm = 0.5f * sl.norm, off = 0.5f * (sl.m - 1);
+    const int m = SQ > 0 ? SQ : sl.m;
+    const int m1 = m - 1;
+    const float half_norm = 0.5f * sl.norm, off = 0.5f * (m - 1);
     const float thr2 = sl.thr * sl.thr;
+    const float lev_h = sl.lev_h;
+    const unsigned glab = SQ == 2 ? (unsigned(sl.grid[0]) | unsigned(sl.grid[1]) << 8 | unsigned(sl.grid[2]) << 16 |
+                                     unsigned(sl.grid[3]) << 24)
+                                  : 0u;
 
     int64_t b = b_lo + int64_t(blockIdx.x) * blockDim.x + tid;
     bool run;
@@ -486,123 +449,203 @@ ddlms_block_kernel(SolveArgs a, Slicer sl, const float4* __restrict__ XT, const 
             const float bound = sqrtf(d2 * maxx2[b]);
             run = !(bound < fminf(o.margin[b], soft_tol)) || (a.mu * maxx2[b] > 1.0f);
         }
-    }
-    if (list && !__syncthreads_or(run ? 1 : 0)) return;
-    unsigned long long changed = 0;
-    if (run) {
-        const int64_t k0 = b * a.B;
-        const int nk = static_cast<int>(min(static_cast<int64_t>(a.B), a.nsym - k0));
-        const int ntr = static_cast<int>(max(static_cast<int64_t>(0), min(static_cast<int64_t>(nk), a.n_train - k0)));
-        float P[WITH_P ? 64 : 1];
-        if constexpr (WITH_P) {
+    } else {
 #pragma unroll
-            for (int i = 0; i < 64; ++i) P[i] = (i % 9 == 0) ? 1.f : 0.f;
+        for (int i = 0; i < 16; ++i) T[i] = 0.f;
+    }
+    const unsigned act = __ballot_sync(0xffffffffu, run);
+    if (!act) return;    // whole warp idle (no block-level barriers below)
+
+    const int64_t k0 = b * a.B;
+    const int nk = run ? static_cast<int>(min(static_cast<int64_t>(a.B), a.nsym - k0)) : 0;
+    const int ntr = TRAIN ? static_cast<int>(max(static_cast<int64_t>(0), min(static_cast<int64_t>(nk), a.n_train - k0))) : 0;
+    const int nk_w = __reduce_max_sync(0xffffffffu, static_cast<unsigned>(nk));
+    const int nchunks = (nk_w + kChunkRows - 1) / kChunkRows;
+    const int bsh = run ? static_cast<int>(b) : -1;   // block index shared with the loader lanes
+
+    float4* stage = dyn_sm + warp * (kWarpStage / sizeof(float4));
+    // loader: rows 8c+1 .. 8c+8 of the warp's 32 blocks (row r of block q =
+    // samples x[2(k0_q + r)], x[2(k0_q + r) + 1]; rows 1..nk_q are valid)
+    const int lrow = lane & 7;
+    auto load_chunk = [&](int c) {
+        const int slot = c % kChunks;
+        const int r = c * kChunkRows + 1 + lrow;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            const int col = q * 4 + (lane >> 3);
+            const int bq = __shfl_sync(0xffffffffu, bsh, col);
+            const int64_t kq = static_cast<int64_t>(bq) * a.B;
+            const bool ok = bq >= 0 && r <= min(static_cast<int64_t>(a.B), a.nsym - kq);
+            const float2* src = a.x + 2 * (ok ? kq + r : 0);
+            float4* dst = stage + stage_idx(slot, lrow, col);
+            if constexpr (AL16) {
+                cp_async16(dst, src, ok ? 16 : 0);
+            } else {
+                cp_async8z(dst, src, ok ? 8 : 0);
+                cp_async8z(reinterpret_cast<float2*>(dst) + 1, src + 1, ok ? 8 : 0);
+            }
         }
-        const float tm = 2.0f * a.mu;      // mu' (scale folded in)
-        float mgl = 0.5f, mgb = 3.0e38f, mx = 0.f, my2 = 0.f;
-        unsigned hsh = 2166136261u;
-        float X[8];
-        const float4* xp = XT + tix(b, 0, a.B + 1);
-        float2* sp = to.ST + tix(b, 0, a.B);
-        uint8_t* lp = to.LT + tix(b, 0, a.B);
-        {
-            const float4 w = __ldg(xp);
-            X[4] = w.x; X[5] = w.y; X[6] = w.z; X[7] = w.w;
+    };
+    // training ring (per thread): slot i & (kTrainRing-1) <- train[k0 + i]
+    float2* trr = reinterpret_cast<float2*>(dyn_sm + kStageSmem / sizeof(float4)) + tid;
+    const float2* tg = a.train + k0;
+    auto load_train = [&](int i) {
+        if constexpr (TRAIN) cp_async8_if(i < ntr, trr + (i & (kTrainRing - 1)) * kBlockThreads, tg + i);
+    };
+    // one commit group per chunk (training symbols of the chunk's 8 symbols ride along)
+    auto issue = [&](int c) {
+        load_chunk(c);
+        if constexpr (TRAIN) {
+#pragma unroll
+            for (int j = 0; j < kChunkRows; ++j) load_train(c * kChunkRows + j);
         }
-        // Input pipeline: a per-thread ring of kRing smem slots filled by
-        // cp.async (one commit group per row), kRing - 1 rows in flight.
-        // Register-destination prefetches do not work here: ptxas folds the
-        // ring loads onto shared scoreboards and the chain then waits on the
-        // newest load every symbol (measured: ~1400 cycles / symbol).
-        // Slot r & (kRing-1) holds pair row r and training symbol r - 1, both
-        // consumed by symbol i = r - 1.
-        extern __shared__ float4 ring_sm[];
-        const int nt = blockDim.x;
-        float4* xr = ring_sm + tid;
-        float2* tr = reinterpret_cast<float2*>(ring_sm + kRing * nt) + tid;
-        const float2* tg = a.train + k0 - 1;
-        auto issue = [&](int r) {
-            const int sl_ = r & (kRing - 1);
-            cp_async16(xr + sl_ * nt, xp + int64_t(r) * 32, r <= a.B ? 16 : 0);
-            if (r - 1 < ntr) cp_async8(tr + sl_ * nt, tg + r);
-            cp_async_commit();
-        };
+        cp_async_commit();
+    };
+
+    float P[WITH_P ? 64 : 1];
+    if constexpr (WITH_P) {
+#pragma unroll
+        for (int i = 0; i < 64; ++i) P[i] = (i % 9 == 0) ? 1.f : 0.f;
+    }
+    const float tm = 2.0f * a.mu;      // mu' (scale folded in)
+    float mgl = 0.5f, mgb = 3.0e38f, mx = 0.f, my2 = 0.f;
+    unsigned hsh = 2166136261u;
+    float X[8];
+    {
+        float2 u0 = make_float2(0.f, 0.f), u1 = u0;
+        if (run) {
+            u0 = __ldg(a.x + 2 * k0);
+            u1 = __ldg(a.x + 2 * k0 + 1);
+        }
+        X[4] = u0.x; X[5] = u0.y; X[6] = u1.x; X[7] = u1.y;
+    }
+    float2* sp = to.ST + k0;
+    uint8_t* lp = to.LT + k0;
+
 #pragma unroll 1
-        for (int r = 1; r < kRing; ++r) issue(r);
-#pragma unroll 2
-        for (int i = 0; i < nk; ++i) {
-            cp_async_wait<kRing - 2>();
-            const int sl_ = (i + 1) & (kRing - 1);
-            const float4 w = xr[sl_ * nt];
-            issue(i + kRing);
+    for (int c = 0; c < kChunks - 1; ++c) issue(c);
+#pragma unroll 1
+    for (int c = 0; c < nchunks; ++c) {
+        __syncwarp();                  // every lane is done with chunk c-1's slot
+        issue(c + kChunks - 1);        // (empty groups past the end keep the count uniform)
+        cp_async_wait<kChunks - 1>();  // this lane's copies of chunk c landed
+        __syncwarp();                  // ... and every other lane's
+        float4 rows[kChunkRows];
+#pragma unroll
+        for (int j = 0; j < kChunkRows; ++j) rows[j] = stage[stage_idx(c % kChunks, j, lane)];
+        float2 soft8[kChunkRows];
+        unsigned lab8[2] = {0u, 0u};
+#pragma unroll
+        for (int j = 0; j < kChunkRows; ++j) {
+            const int i = c * kChunkRows + j;
+            const bool live = i < nk;
             X[0] = X[4]; X[1] = X[5]; X[2] = X[6]; X[3] = X[7];
-            X[4] = w.x; X[5] = w.y; X[6] = w.z; X[7] = w.w;
+            X[4] = rows[j].x; X[5] = rows[j].y; X[6] = rows[j].z; X[7] = rows[j].w;
             float ya = 0.f, yb = 0.f, za = 0.f, zb = 0.f;
 #pragma unroll
-            for (int j = 0; j < 8; j += 2) {
-                ya = fmaf(T[j], X[j], ya);
-                yb = fmaf(T[j + 1], X[j + 1], yb);
-                za = fmaf(T[8 + j], X[j], za);
-                zb = fmaf(T[9 + j], X[j + 1], zb);
+            for (int jj = 0; jj < 8; jj += 2) {
+                ya = fmaf(T[jj], X[jj], ya);
+                yb = fmaf(T[jj + 1], X[jj + 1], yb);
+                za = fmaf(T[8 + jj], X[jj], za);
+                zb = fmaf(T[9 + jj], X[jj + 1], zb);
             }
             const float yr = ya + yb, yi = za + zb;
             float dr, di;
             int lab;
-            if (i < ntr) {
-                const float2 t = tr[((i + 1) & (kRing - 1)) * nt];
-                dr = t.x; di = t.y;
-                lab = 255;
-            } else if (square) {
+            float2 tcur = make_float2(0.f, 0.f);
+            if constexpr (TRAIN) tcur = trr[(i & (kTrainRing - 1)) * kBlockThreads];
+            const bool trn = i < ntr;
+            if constexpr (SQ > 0) {
+                // branch-free: no F2I (MIO) and no control flow on the chain.
+                // (v + 1.5*2^23) - 1.5*2^23 == rint(v) for |v| < 2^22.
+                constexpr float kMagic = 12582912.0f;
                 const float vr = fmaf(yr, half_norm, off), vi = fmaf(yi, half_norm, off);
-                const int ir = min(max(__float2int_rn(vr), 0), m1);
-                const int ii = min(max(__float2int_rn(vi), 0), m1);
-                // conservative margin (level units): distance to the nearest
-                // boundary if both neighbours existed
-                mgl = fminf(mgl, 0.5f - fmaxf(fabsf(vr - static_cast<float>(ir)), fabsf(vi - static_cast<float>(ii))));
-                lab = grid[ir * sl.m + ii];
-                const float2 pp = pts[lab];
-                dr = pp.x; di = pp.y;
+                const float fr = fminf(fmaxf((vr + kMagic) - kMagic, 0.f), static_cast<float>(m1));
+                const float fi = fminf(fmaxf((vi + kMagic) - kMagic, 0.f), static_cast<float>(m1));
+                const float mg_s = 0.5f - fmaxf(fabsf(vr - fr), fabsf(vi - fi));
+                mgl = (live && !trn) ? fminf(mgl, mg_s) : mgl;
+                const int ir = __float_as_int(fr + kMagic) - __float_as_int(kMagic);
+                const int ii = __float_as_int(fi + kMagic) - __float_as_int(kMagic);
+                // level value (2 i - (m-1)) * h: exact for the constellation
+                // (checked on the host, Slicer::sep)
+                dr = trn ? tcur.x : fmaf(2.0f, fr, -static_cast<float>(m1)) * lev_h;
+                di = trn ? tcur.y : fmaf(2.0f, fi, -static_cast<float>(m1)) * lev_h;
+                int sl_lab;
+                if constexpr (SQ == 2) sl_lab = (glab >> (8 * (ir * 2 + ii))) & 0xff;
+                else sl_lab = grid[ir * SQ + ii];
+                lab = trn ? 255 : sl_lab;
             } else {
-                float m_;
-                lab = slice(sl, yr, yi, m_);
-                mgb = fminf(mgb, m_);
-                const float2 pp = pts[lab];
-                dr = pp.x; di = pp.y;
+                if (trn) {
+                    dr = tcur.x; di = tcur.y;
+                    lab = 255;
+                } else if (sl.kind == 0) {
+                    const float vr = fmaf(yr, half_norm, off), vi = fmaf(yi, half_norm, off);
+                    const int ir = min(max(__float2int_rn(vr), 0), m1);
+                    const int ii = min(max(__float2int_rn(vi), 0), m1);
+                    if (live)
+                        mgl = fminf(mgl, 0.5f - fmaxf(fabsf(vr - static_cast<float>(ir)),
+                                                      fabsf(vi - static_cast<float>(ii))));
+                    lab = grid[ir * m + ii];
+                    const float2 pp = pts[lab];
+                    dr = pp.x; di = pp.y;
+                } else {
+                    float m_;
+                    lab = slice(sl, yr, yi, m_);
+                    if (live) mgb = fminf(mgb, m_);
+                    const float2 pp = pts[lab];
+                    dr = pp.x; di = pp.y;
+                }
             }
-            my2 = fmaxf(my2, fmaf(yr, yr, yi * yi));
-            const float er = tm * (dr - yr), ei = tm * (di - yi);
+            my2 = live ? fmaxf(my2, fmaf(yr, yr, yi * yi)) : my2;
+            const float er = live ? tm * (dr - yr) : 0.f, ei = live ? tm * (di - yi) : 0.f;
             if constexpr (WITH_P) {
                 float n2 = 0.f;
 #pragma unroll
-                for (int j = 0; j < 8; ++j) n2 = fmaf(X[j], X[j], n2);
-                mx = fmaxf(mx, n2);
+                for (int jj = 0; jj < 8; ++jj) n2 = fmaf(X[jj], X[jj], n2);
+                mx = fmaxf(mx, n2);     // rows past nk are zero-filled
                 float v[8];
 #pragma unroll
                 for (int r = 0; r < 8; ++r) {
                     float sacc = 0.f;
 #pragma unroll
-                    for (int j = 0; j < 8; ++j) sacc = fmaf(P[r * 8 + j], X[j], sacc);
-                    v[r] = sacc * tm;
+                    for (int jj = 0; jj < 8; ++jj) sacc = fmaf(P[r * 8 + jj], X[jj], sacc);
+                    v[r] = live ? sacc * tm : 0.f;
                 }
 #pragma unroll
                 for (int r = 0; r < 8; ++r)
 #pragma unroll
-                    for (int j = 0; j < 8; ++j) P[r * 8 + j] = fmaf(-v[r], X[j], P[r * 8 + j]);
+                    for (int jj = 0; jj < 8; ++jj) P[r * 8 + jj] = fmaf(-v[r], X[jj], P[r * 8 + jj]);
             }
 #pragma unroll
-            for (int j = 0; j < 8; ++j) {
-                T[j] = fmaf(er, X[j], T[j]);
-                T[8 + j] = fmaf(ei, X[j], T[8 + j]);
+            for (int jj = 0; jj < 8; ++jj) {
+                T[jj] = fmaf(er, X[jj], T[jj]);
+                T[8 + jj] = fmaf(ei, X[jj], T[8 + jj]);
             }
-            hsh = (hsh ^ static_cast<unsigned>(lab)) * 16777619u;
-            if (write_out) {   // outputs only from the final (full) pass
-                *sp = make_float2(yr, yi);
-                *lp = static_cast<uint8_t>(lab);
-                sp += 32;
-                lp += 32;
+            hsh = live ? (hsh ^ static_cast<unsigned>(lab)) * 16777619u : hsh;
+            soft8[j] = make_float2(yr, yi);
+            lab8[j >> 2] |= static_cast<unsigned>(lab & 0xff) << (8 * (j & 3));
+        }
+        if (!WITH_P && write_out) {   // outputs only from the final (full) pass
+            const int i0 = c * kChunkRows;
+            if (i0 + kChunkRows <= nk) {
+                float4* s4 = reinterpret_cast<float4*>(sp + i0);
+#pragma unroll
+                for (int j = 0; j < kChunkRows / 2; ++j)
+                    s4[j] = make_float4(soft8[2 * j].x, soft8[2 * j].y, soft8[2 * j + 1].x, soft8[2 * j + 1].y);
+                *reinterpret_cast<uint2*>(lp + i0) = make_uint2(lab8[0], lab8[1]);
+            } else {
+#pragma unroll
+                for (int j = 0; j < kChunkRows; ++j)
+                    if (i0 + j < nk) {
+                        sp[i0 + j] = soft8[j];
+                        lp[i0 + j] = static_cast<uint8_t>(lab8[j >> 2] >> (8 * (j & 3)));
+                    }
             }
         }
-        cp_async_wait<0>();
+    }
+    cp_async_wait<0>();
+    unsigned long long changed = 0;
+    if (run) {
         changed = (o.hash[b] != static_cast<unsigned long long>(hsh)) ? 1ull : 0ull;
         o.hash[b] = hsh;
         // Q_b = T_end - T_start P_b
@@ -623,7 +666,8 @@ ddlms_block_kernel(SolveArgs a, Slicer sl, const float4* __restrict__ XT, const 
             }
 #pragma unroll
         for (int i = 0; i < 16; ++i) o.Tused[b * 16 + i] = Tstart[b * 16 + i];
-        const float mg = square ? mgl * (2.0f / sl.norm) : mgb;
+        const bool sq = SQ > 0 || sl.kind == 0;
+        const float mg = sq ? mgl * (2.0f / sl.norm) : mgb;
         o.margin[b] = fminf(mg, fabsf(sl.thr - sqrtf(my2)));
         o.over[b] = my2 > thr2 ? 1 : 0;
         if (b == a.nb - 1) {
@@ -653,9 +697,9 @@ ddlms_block_kernel(SolveArgs a, Slicer sl, const float4* __restrict__ XT, const 
 // list (warp-aggregated append; block order inside a warp preserved).
 __global__ void ddlms_select_kernel(const float* __restrict__ Tstart, const float* __restrict__ Tused,
                                     const float* __restrict__ margin, const float* __restrict__ maxx2, float mu,
-                                    int64_t nb, float tol, int* __restrict__ list,
+                                    int64_t b_lo, int64_t nb, float tol, int* __restrict__ list,
                                     unsigned long long* __restrict__ list_n) {
-    const int64_t b = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    const int64_t b = b_lo + int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     bool run = false;
     if (b < nb) {
         float d2 = 0.f;
@@ -982,6 +1026,23 @@ static Slicer make_slicer(int order, const float* pts_ri, const uint8_t* grid, i
     for (int i = 0; i < order && i < 64; ++i) s.pts[i] = make_float2(pts_ri[2 * i], pts_ri[2 * i + 1]);
     if (grid_m > 0)
         for (int i = 0; i < grid_m * grid_m && i < 64; ++i) s.grid[i] = grid[i];
+    s.sep = 0;
+    s.lev_h = 0.f;
+    if (grid_m == 2 || grid_m == 4 || grid_m == 8) {
+        // h = the first positive level (2 i - (m-1) == 1); every point must be
+        // reproduced bit-exactly by the device formula
+        const float h = s.pts[s.grid[(grid_m / 2) * grid_m]].x;
+        bool ok = h > 0.f;
+        for (int i = 0; i < grid_m; ++i)
+            for (int j = 0; j < grid_m; ++j) {
+                const float2 p = s.pts[s.grid[i * grid_m + j]];
+                const volatile float lr = static_cast<float>(2 * i - (grid_m - 1)) * h;
+                const volatile float li = static_cast<float>(2 * j - (grid_m - 1)) * h;
+                ok = ok && p.x == lr && p.y == li;
+            }
+        s.sep = ok ? 1 : 0;
+        s.lev_h = h;
+    }
     return s;
 }
 
@@ -1034,9 +1095,8 @@ Layout plan(int64_t nsym, int B) {
     b += align_up(16 * sizeof(float)) * 2;      // Tend, Tinit
     b += align_up(L.nb * sizeof(int));          // over
     b += align_up(L.nb * sizeof(unsigned long long));   // label hashes
-    b += align_up(size_t(tiled_elems(L.nb, B + 1)) * 16);   // XT (warp-tiled input)
-    b += align_up(size_t(tiled_elems(L.nb, B)) * 8);        // ST
-    b += align_up(size_t(tiled_elems(L.nb, B)));            // LT
+    b += align_up(size_t(nsym) * 8);                     // ST (soft, unless bound to the caller's)
+    b += align_up(size_t(nsym));                         // LT (labels, idem)
     b += align_up(L.nb * sizeof(int));                   // re-run list
     b += align_up(4 * sizeof(unsigned long long));
     L.bytes = b;
@@ -1077,9 +1137,11 @@ struct DdlmsSolver {
     float *Tused, *margin, *maxx2, *Tend, *Tinit_d;
     int* over;
     unsigned long long *hsh, *ctr;
-    float4* XT;
+    float2* ST_own = nullptr;    // workspace soft / labels (outputs not bound)
+    uint8_t* LT_own = nullptr;
     int* list;
-    int64_t bt = 0;
+    int64_t bt = 0;      // pure training blocks
+    int64_t ntb = 0;     // blocks holding any training symbol
     bool speculated = false;
     int64_t iters = 0, reruns = 0, last_changed = 0;
 
@@ -1152,34 +1214,71 @@ struct DdlmsSolver {
         fill_T_kernel<<<static_cast<unsigned>(((b1 - b0) * 16 + 127) / 128), 128, 0, s>>>(lv[0].T, b0, b1, src_dev);
         return check_launch("fill_T_kernel");
     }
+    // Run blocks [b0, b1): the blocks holding training symbols (b < ntb) in a
+    // TRAIN launch (range mode, in-kernel skip test), the rest in a plain
+    // launch -- compacted into a re-run list first when use_skip.
     int run_blocks(bool with_p, int64_t b0, int64_t b1, int use_skip, float tol = 0.f, int write_out = 0) {
         if (b1 <= b0) return KK_OK;
         static thread_local int attr_dev = -1;
         int dev = 0;
         cudaGetDevice(&dev);
         if (attr_dev != dev) {
-            if (cudaFuncSetAttribute(ddlms_block_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     static_cast<int>(kRingSmem)) != cudaSuccess ||
-                cudaFuncSetAttribute(ddlms_block_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     static_cast<int>(kRingSmem)) != cudaSuccess)
-                return set_cuda_error("ddlms_block_kernel smem attribute");
+            struct KS { const void* k; size_t smem; };
+            const KS ks[] = {
+#define KK_DD_K(P_, S_, T_) {reinterpret_cast<const void*>(ddlms_block_kernel<P_, S_, true, T_>), T_ ? kStageSmem + kTrainSmem : kStageSmem}, \
+                            {reinterpret_cast<const void*>(ddlms_block_kernel<P_, S_, false, T_>), T_ ? kStageSmem + kTrainSmem : kStageSmem}
+                KK_DD_K(true, 0, true), KK_DD_K(true, 2, true), KK_DD_K(true, 4, true), KK_DD_K(true, 8, true),
+                KK_DD_K(false, 0, true), KK_DD_K(false, 2, true), KK_DD_K(false, 4, true), KK_DD_K(false, 8, true),
+                KK_DD_K(true, 0, false), KK_DD_K(true, 2, false), KK_DD_K(true, 4, false), KK_DD_K(true, 8, false),
+                KK_DD_K(false, 0, false), KK_DD_K(false, 2, false), KK_DD_K(false, 4, false), KK_DD_K(false, 8, false)
+#undef KK_DD_K
+            };
+            for (const KS& k : ks)
+                if (cudaFuncSetAttribute(k.k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(k.smem)) !=
+                    cudaSuccess)
+                    return set_cuda_error("ddlms_block_kernel smem attribute");
             attr_dev = dev;
         }
-        const unsigned g = static_cast<unsigned>((b1 - b0 + kBlockThreads - 1) / kBlockThreads);
-        if (with_p)
-            ddlms_block_kernel<true><<<g, kBlockThreads, kRingSmem, s>>>(a, sl, XT, lv[0].T, lv[0].P, maxx2, o, to, b0, b1, 0, tol,
-                                                       nullptr, nullptr, write_out);
-        else if (!use_skip)
-            ddlms_block_kernel<false><<<g, kBlockThreads, kRingSmem, s>>>(a, sl, XT, lv[0].T, lv[0].P, maxx2, o, to, b0, b1, 0, tol,
-                                                        nullptr, nullptr, write_out);
-        else {
+        const int sq = sl.sep ? sl.m : 0;
+        const bool al = (reinterpret_cast<uintptr_t>(a.x) & 15) == 0;
+        auto launch = [&](bool train_blocks, int64_t lo, int64_t hi, int skip, const int* lst,
+                          const unsigned long long* lst_n) {
+            const unsigned g = static_cast<unsigned>((hi - lo + kBlockThreads - 1) / kBlockThreads);
+            const size_t smem = train_blocks ? kStageSmem + kTrainSmem : kStageSmem;
+            auto go = [&](auto kern) {
+                kern<<<g, kBlockThreads, smem, s>>>(a, sl, lv[0].T, lv[0].P, maxx2, o, to, lo, hi, skip, tol, lst,
+                                                    lst_n, write_out);
+            };
+#define KK_DD_GO3(P_, S_, T_) (al ? go(ddlms_block_kernel<P_, S_, true, T_>) : go(ddlms_block_kernel<P_, S_, false, T_>))
+#define KK_DD_GO(P_, S_) (train_blocks ? KK_DD_GO3(P_, S_, true) : KK_DD_GO3(P_, S_, false))
+            if (with_p) {
+                if (sq == 2) KK_DD_GO(true, 2);
+                else if (sq == 4) KK_DD_GO(true, 4);
+                else if (sq == 8) KK_DD_GO(true, 8);
+                else KK_DD_GO(true, 0);
+            } else {
+                if (sq == 2) KK_DD_GO(false, 2);
+                else if (sq == 4) KK_DD_GO(false, 4);
+                else if (sq == 8) KK_DD_GO(false, 8);
+                else KK_DD_GO(false, 0);
+            }
+#undef KK_DD_GO
+#undef KK_DD_GO3
+            return check_launch("ddlms_block_kernel");
+        };
+        const int64_t t1 = std::min(b1, ntb);
+        if (b0 < t1)
+            if (int rc = launch(true, b0, t1, (use_skip && !with_p) ? 1 : 0, nullptr, nullptr)) return rc;
+        const int64_t d0 = std::max(b0, ntb);
+        if (d0 >= b1) return KK_OK;
+        if (use_skip && !with_p) {
             // compact the blocks to re-run so that warps only carry live chains
-            ddlms_select_kernel<<<g, 128, 0, s>>>(lv[0].T, Tused, margin, maxx2, a.mu, L.nb, tol, list, ctr + 3);
+            const unsigned g = static_cast<unsigned>((b1 - d0 + 127) / 128);
+            ddlms_select_kernel<<<g, 128, 0, s>>>(lv[0].T, Tused, margin, maxx2, a.mu, d0, b1, tol, list, ctr + 3);
             if (int rc = check_launch("ddlms_select_kernel")) return rc;
-            ddlms_block_kernel<false><<<g, kBlockThreads, kRingSmem, s>>>(a, sl, XT, lv[0].T, lv[0].P, maxx2, o, to, b0, b1, 0, tol,
-                                                        list, ctr + 3, write_out);
+            return launch(false, d0, b1, 0, list, ctr + 3);
         }
-        return check_launch("ddlms_block_kernel");
+        return launch(false, d0, b1, 0, nullptr, nullptr);
     }
     int read_ctr(unsigned long long (&h)[4]) {
         if (cudaMemcpyAsync(h, ctr, sizeof(h), cudaMemcpyDeviceToHost, s) != cudaSuccess ||
@@ -1213,9 +1312,10 @@ struct DdlmsSolver {
         Tinit_d = reinterpret_cast<float*>(w); w += align_up(16 * sizeof(float));
         over = reinterpret_cast<int*>(w); w += align_up(L.nb * sizeof(int));
         hsh = reinterpret_cast<unsigned long long*>(w); w += align_up(L.nb * 8);
-        XT = reinterpret_cast<float4*>(w); w += align_up(size_t(tiled_elems(L.nb, block + 1)) * 16);
-        to.ST = reinterpret_cast<float2*>(w); w += align_up(size_t(tiled_elems(L.nb, block)) * 8);
-        to.LT = reinterpret_cast<uint8_t*>(w); w += align_up(size_t(tiled_elems(L.nb, block)));
+        ST_own = reinterpret_cast<float2*>(w); w += align_up(size_t(nsym) * 8);
+        LT_own = reinterpret_cast<uint8_t*>(w); w += align_up(size_t(nsym));
+        to.ST = ST_own;
+        to.LT = LT_own;
         list = reinterpret_cast<int*>(w); w += align_up(L.nb * sizeof(int));
         ctr = reinterpret_cast<unsigned long long*>(w);
         // the block kernels work on the raw input with the scale folded into
@@ -1238,13 +1338,21 @@ struct DdlmsSolver {
         o.hash = hsh;
         o.counters = ctr;
         bt = std::min<int64_t>(n_train / block, L.nb);
+        ntb = std::min<int64_t>((n_train + block - 1) / block, L.nb);
         if (cudaMemsetAsync(over, 0, L.nb * sizeof(int), s) != cudaSuccess ||
             cudaMemsetAsync(hsh, 0, L.nb * 8, s) != cudaSuccess ||
             cudaMemsetAsync(ctr, 0, 4 * sizeof(unsigned long long), s) != cudaSuccess)
             return set_cuda_error("solver init");
-        dim3 tb(32, 8), tg(static_cast<unsigned>((L.nb + 31) / 32), static_cast<unsigned>((block + 1 + 31) / 32));
-        ddlms_transpose_in<<<tg, tb, 0, s>>>(a.x, nsym, block, L.nb, XT);
-        return check_launch("ddlms_transpose_in");
+        return KK_OK;
+    }
+
+    // the final pass writes straight into the caller's arrays when bound
+    // (8-symbol runs are stored as 16 B soft / 8 B label words: alignment)
+    void bind_outputs(uint8_t* labels, float2* soft) {
+        const bool ok = labels && soft && (reinterpret_cast<uintptr_t>(labels) & 7) == 0 &&
+                        (reinterpret_cast<uintptr_t>(soft) & 15) == 0;
+        to.LT = ok ? labels : LT_own;
+        to.ST = ok ? soft : ST_own;
     }
 
     // pure-training blocks from T_start; writes the exact training-end taps
@@ -1329,9 +1437,12 @@ struct DdlmsSolver {
     }
 
     int finish(uint8_t* labels, float2* soft, float* T_final, int64_t* guard) {
-        dim3 tb(32, 8), tg(static_cast<unsigned>((L.nb + 31) / 32), static_cast<unsigned>((a.B + 31) / 32));
-        ddlms_transpose_out<<<tg, tb, 0, s>>>(to.ST, to.LT, a.nsym, a.B, L.nb, soft, labels);
-        if (int rc = check_launch("ddlms_transpose_out")) return rc;
+        if (labels && labels != to.LT &&
+            cudaMemcpyAsync(labels, to.LT, size_t(a.nsym), cudaMemcpyDeviceToDevice, s) != cudaSuccess)
+            return set_cuda_error("labels copy");
+        if (soft && soft != to.ST &&
+            cudaMemcpyAsync(soft, to.ST, size_t(a.nsym) * 8, cudaMemcpyDeviceToDevice, s) != cudaSuccess)
+            return set_cuda_error("soft copy");
         return end_state(T_final, guard);
     }
     int end_state(float* T_final, int64_t* guard) {
@@ -1405,6 +1516,13 @@ extern "C" int kk_ddlms_finish(void* h, uint8_t* labels, void* soft, float* T_fi
     return static_cast<DdlmsSolver*>(h)->finish(labels, static_cast<float2*>(soft), T_final_host, guard);
 }
 
+extern "C" int kk_ddlms_bind_outputs(void* h, uint8_t* labels, void* soft) {
+    clear_error();
+    if (!h) return set_error(KK_ERR_PARAM, "null solver");
+    static_cast<DdlmsSolver*>(h)->bind_outputs(labels, static_cast<float2*>(soft));
+    return KK_OK;
+}
+
 extern "C" void kk_ddlms_destroy(void* h) { delete static_cast<DdlmsSolver*>(h); }
 
 // Single-frame exact solve (T_init = exact frame start taps).  stats (host
@@ -1425,6 +1543,7 @@ extern "C" int kk_ddlms_solve(const void* x, int64_t nsym, float scale, const vo
                              max_radius, guard_factor, mu, block, soft_tol, workspace, ws_bytes,
                              static_cast<cudaStream_t>(stream)))
         return rc;
+    sv.bind_outputs(labels, static_cast<float2*>(soft));
     float Tg[16];
     if (int rc = sv.train(T_init, Tg)) return rc;
     if (int rc = sv.speculate(sv.bt > 0 ? Tg : T_init, nullptr)) return rc;

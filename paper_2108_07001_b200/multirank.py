@@ -124,6 +124,10 @@ class GpuFrameSolver:
             _stream(dev))
         if not self.h:
             _lib.check(_lib.KK_ERR_PARAM, "kk_ddlms_create")
+        # the final pass writes straight into these
+        self.labels = torch.empty(self.nsym, dtype=torch.uint8, device=dev)
+        self.soft = torch.empty(self.nsym, dtype=torch.complex64, device=dev)
+        _lib.call("kk_ddlms_bind_outputs", self.h, _ptr(self.labels), _ptr(self.soft))
 
     def train(self, T):
         out = np.zeros(16, np.float32)
@@ -147,10 +151,7 @@ class GpuFrameSolver:
         return ch.value, rr.value, mp
 
     def finish(self):
-        import torch
-
-        labels = torch.empty(self.nsym, dtype=torch.uint8, device=self.dev)
-        soft = torch.empty(self.nsym, dtype=torch.complex64, device=self.dev)
+        labels, soft = self.labels, self.soft
         Tf = np.zeros(16, np.float32)
         guard = ctypes.c_int64(0)
         _lib.call("kk_ddlms_finish", self.h, _ptr(labels), _ptr(soft), Tf.ctypes.data, ctypes.byref(guard))
