@@ -324,6 +324,13 @@ __global__ void sum_int_kernel(const int* __restrict__ v, int64_t n, unsigned lo
     if ((threadIdx.x & 31) == 0 && acc) atomicAdd(out, acc);
 }
 
+struct Vec16 {
+    float v[16];
+};
+__global__ void set16_kernel(float* __restrict__ dst, Vec16 v) {
+    if (threadIdx.x < 16) dst[threadIdx.x] = v.v[threadIdx.x];
+}
+
 __global__ void fill_T_kernel(float* __restrict__ T, int64_t b0, int64_t b1, const float* __restrict__ src) {
     const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     const int64_t n = (b1 - b0) * 16;
@@ -1201,14 +1208,16 @@ struct DdlmsSolver {
         for (int i = 0; i < 16; ++i) agg[64 + i] = static_cast<float>(Qa[i] / scale);
         return KK_OK;
     }
-    int set_start(const float* T_host) {
-        float Ts[16];
-        for (int i = 0; i < 16; ++i) Ts[i] = T_host[i] * scale;
-        if (cudaMemcpyAsync(Tinit_d, Ts, sizeof(Ts), cudaMemcpyHostToDevice, s) != cudaSuccess ||
-            cudaStreamSynchronize(s) != cudaSuccess)
-            return set_cuda_error("T upload");
-        return KK_OK;
+    // small host values go down as kernel arguments, not H2D copies: a copy
+    // would queue behind the bulk input transfers of a streaming receive on
+    // the (in-order) host->device copy engine
+    int upload16(float* dst, const float* T_host) {
+        Vec16 v;
+        for (int i = 0; i < 16; ++i) v.v[i] = T_host[i] * scale;
+        set16_kernel<<<1, 16, 0, s>>>(dst, v);
+        return check_launch("set16_kernel");
     }
+    int set_start(const float* T_host) { return upload16(Tinit_d, T_host); }
     int fill_T(int64_t b0, int64_t b1, const float* src_dev) {
         if (b1 <= b0) return KK_OK;
         fill_T_kernel<<<static_cast<unsigned>(((b1 - b0) * 16 + 127) / 128), 128, 0, s>>>(lv[0].T, b0, b1, src_dev);
@@ -1387,10 +1396,7 @@ struct DdlmsSolver {
 
     // first pass of the decision-directed blocks from T_guess (+ P_b)
     int speculate(const float* T_guess, float* agg) {
-        float Tg[16];
-        for (int i = 0; i < 16; ++i) Tg[i] = T_guess[i] * scale;
-        if (cudaMemcpyAsync(Tend, Tg, sizeof(Tg), cudaMemcpyHostToDevice, s) != cudaSuccess)
-            return set_cuda_error("T guess");
+        if (int rc = upload16(Tend, T_guess)) return rc;
         if (int rc = fill_T(bt, L.nb, Tend)) return rc;
         if (int rc = run_blocks(true, bt, L.nb, 0)) return rc;
         reruns += L.nb;

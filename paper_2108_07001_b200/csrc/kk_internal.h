@@ -19,4 +19,7 @@ int check_launch(const char* name);
 // Built once per device (std::call_once), immutable afterwards.
 const float2* twiddle_table_device();
 
+// SM count of the current device (cached per device)
+int num_sms();
+
 }  // namespace kk

@@ -86,15 +86,18 @@ def device_ber(labels, ref_idx, order: int, head: int, stop: int, tile_symbols: 
     return count_bit_errors(lab, ref, order)[:2]
 
 
-def receive_host_stream(cfg, host_codes, half_lsb: float, reference_symbols, chunk_samples: int = 1 << 26,
-                        labels_host=None, device=None):
+def receive_host_stream(cfg, host_codes, half_lsb: float, reference_symbols, chunk_samples: int = 1 << 25,
+                        labels_host=None, device=None, staging=None):
     """End-to-end receive of an int16 ADC stream in pinned HOST memory.
 
-    The stream is copied in chunks on a side stream (double-buffered) while
-    the compute stream runs the receiver on the previous chunk, and the
-    decided labels of every completed DDLMS frame are copied back to
-    (pinned) host memory as they are released -- PCIe traffic overlaps the
-    GPU work.  Returns (pipe, labels_host[:n], n_decided).
+    Every chunk's host->device copy is queued up front on a side stream into
+    one device staging buffer (HBM is plentiful; the copy engine then streams
+    at the full PCIe rate however long the receiver blocks the host), the
+    compute stream waits per chunk on its copy event, and the decided labels
+    of every completed DDLMS frame go back to (pinned) host memory on a third
+    stream as they are released -- both PCIe directions overlap the GPU work.
+    `staging` (optional) is a reusable int16 device buffer of >= n samples.
+    Returns (pipe, labels_host, n_decided).
     """
     import torch
 
@@ -105,40 +108,27 @@ def receive_host_stream(cfg, host_codes, half_lsb: float, reference_symbols, chu
     comp = torch.cuda.current_stream(dev)
     copy = torch.cuda.Stream(device=dev)
     d2h = torch.cuda.Stream(device=dev)
-    bufs = [torch.empty(chunk_samples, dtype=torch.int16, device=dev) for _ in range(3)]
-    ready = [torch.cuda.Event() for _ in range(3)]
-    free = [torch.cuda.Event() for _ in range(3)]
+    if staging is None or staging.numel() < n:
+        staging = torch.empty(n, dtype=torch.int16, device=dev)
+    # the pipeline's own uploads go first: later small H2D copies would queue
+    # behind the bulk transfers on the in-order host->device copy engine
     pipe = RxPipeline(cfg, reference_symbols=reference_symbols, device=dev)
     pipe.expect(n, chunk_samples)
+    starts = list(range(0, n, chunk_samples))
+    ready = [torch.cuda.Event() for _ in starts]
+    copy.wait_stream(comp)          # the staging buffer's previous readers
+    with torch.cuda.stream(copy):
+        for i, a in enumerate(starts):
+            m = min(chunk_samples, n - a)
+            staging[a:a + m].copy_(host_codes[a:a + m], non_blocking=True)
+            ready[i].record(copy)
     if labels_host is None:
         labels_host = torch.empty(n // 4 + 8, dtype=torch.uint8, pin_memory=True)
     n_out = 0
-    starts = list(range(0, n, chunk_samples))
-
-    def issue_copy(i):
-        a = starts[i]
-        m = min(chunk_samples, n - a)
-        k = i % 3
-        with torch.cuda.stream(copy):
-            if i >= 3:
-                copy.wait_event(free[k])
-            bufs[k][:m].copy_(host_codes[a:a + m], non_blocking=True)
-            ready[k].record(copy)
-
-    issue_copy(0)
-    if len(starts) > 1:
-        issue_copy(1)
     for i, a in enumerate(starts):
-        k = i % 3
         m = min(chunk_samples, n - a)
-        comp.wait_event(ready[k])
-        last = i == len(starts) - 1
-        pipe.feed(AdcCodes(bufs[k][:m], half_lsb, cfg.adc_rate_hz), flush=last)
-        # the buffer may still back the raw FIFO tail until the next feed
-        if i >= 1:
-            free[(i - 1) % 3].record(comp)
-        if i + 2 < len(starts):
-            issue_copy(i + 2)
+        comp.wait_event(ready[i])
+        pipe.feed(AdcCodes(staging[a:a + m], half_lsb, cfg.adc_rate_hz), flush=i == len(starts) - 1)
         lab, _, _ = pipe.drain_device()
         if lab.numel():
             # device -> host on its own stream (the other DMA direction)

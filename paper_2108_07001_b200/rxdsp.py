@@ -114,12 +114,16 @@ class EqualizerState:
 class GpuOptions:
     """B200-only knobs (not in the reference): DDLMS block size B, frame size
     F (symbols, global grid), fixpoint iteration cap, soft-output tolerance
-    of the block-skip certificate."""
+    of the block-skip certificate, and the smallest frame of the geometric
+    tail used when the stream length is announced (RxPipeline.expect): the
+    last grid frame is split in halves down to this size so that little
+    DDLMS work (and output transfer) is left once the last input arrives."""
 
     ddlms_block: int = 1024
     ddlms_frame_symbols: int = 1 << 28
     ddlms_max_iter: int = 64
     ddlms_soft_tol: float = 1e-5
+    ddlms_tail_min_symbols: int = 1 << 22
 
 
 @dataclass
@@ -721,6 +725,7 @@ class RxPipeline:
         self.sync_ratio = None
         self._train_total = 0
         self._sym_done = 0
+        self._expected_symbols = None     # set by expect(): geometric DDLMS tail
         st0 = EqualizerState.initial(cfg.ddlms.n_taps)
         self._w, self._g = st0.w, st0.g
         self._T = _T_from_wg(st0.w, st0.g) if cfg.ddlms.n_taps == 4 else None
@@ -933,11 +938,10 @@ class RxPipeline:
         if not self._synced:
             if not self._do_sync(flush):
                 return
-        F = int(self.gpu.ddlms_frame_symbols)
         while True:
             n_q = self._y2.end - self._drop
             k0 = self._sym_done
-            k1 = (k0 // F + 1) * F
+            k1 = self._frame_end(k0)
             if n_q >= 2 * k1 + 2:
                 self._solve_frame(k0, k1)
                 continue
@@ -946,6 +950,23 @@ class RxPipeline:
                 if total > k0:
                     self._solve_frame(k0, total)
             break
+
+    def _frame_end(self, k0: int) -> int:
+        """End of the DDLMS frame starting at symbol k0: the next multiple of
+        F (global grid, independent of the feed chunking); inside the last
+        grid frame of an announced stream (expect), geometric halves of the
+        remainder down to ddlms_tail_min_symbols (multiples of the block)."""
+        F = int(self.gpu.ddlms_frame_symbols)
+        k1 = (k0 // F + 1) * F
+        T = self._expected_symbols
+        if T is None or k1 < T:
+            return k1
+        B = int(self.gpu.ddlms_block)
+        fmin = max(B, int(self.gpu.ddlms_tail_min_symbols))
+        rem = T - k0
+        if rem <= 2 * fmin:
+            return k1
+        return k0 + max(fmin, (rem // 2) // B * B)
 
     # -- public API (rx:768-824) ---------------------------------------------
 
@@ -993,6 +1014,8 @@ class RxPipeline:
         chunk_samples: pre-sizes the 2-sps buffer for one DDLMS frame and the
         KK output window, so streaming feeds never re-grow device buffers."""
         F = int(self.gpu.ddlms_frame_symbols)
+        # symbols the stream will end with (upper bound: 4 samples / symbol)
+        self._expected_symbols = int(n_samples) // 4
         self._y2.ensure_capacity(min(n_samples // 2, 2 * F + 2 * self.cfg.static_plan.hop) + 16)
         c = chunk_samples or n_samples
         self._z.ensure_capacity(min(n_samples, c + 2 * self.cfg.carrier_segment_len + self.cfg.static_plan.hop))
