@@ -16,15 +16,22 @@
 //   kept bins of E/O are their low and high quarters -> 8192 each
 //   A = IFFT8192(E_kept * H_even), B = IFFT8192(O_kept * H_odd)
 //   out[r] = (A[r] - W16384^{-r} B[r]) * 0.5/16384
-// One 512-thread CTA per block: 136 KB padded float2 FFT buffer + 64 KB for A.
-// The first pass of each FFT16384 reads HBM directly (coalesced) with the
-// carrier subtraction / pre-twiddle fused, the IFFT's first pass applies the
-// kept-bin gather and H, and the final IFFT pass writes the 2-sps output
-// straight to HBM.
+// One 512-thread CTA (16 warps) per block, four-step factorisations whose
+// inner transforms are warp-local (kk_warpfft.cuh):
+//   FFT16384 = DFT16 over stride 1024 (fused with the HBM loads, carrier
+//              subtraction, DIF pre-twiddle; then W16384^{n2 k1}) into 16
+//              rows, then one warp_fft1024 per row (warp k1)
+//   IFFT8192 = DFT16 over stride 512 of the kept bins x H (then
+//              W8192^{-m2 p1}) into 16 rows, then one warp_fft512 per row
+// so each transform needs two block barriers instead of one per radix pass.
+// Chain 0's A is parked in smem (natural order, padded); chain 1 combines
+// out = (A - W16384^{-r} B) * 0.5/16384 in place and the block is written
+// to HBM coalesced.
 #include <algorithm>
 
 #include "kk_common.cuh"
 #include "kk_internal.h"
+#include "kk_warpfft.cuh"
 
 namespace kk {
 
@@ -32,15 +39,17 @@ constexpr int kNS = 32768;        // static block
 constexpr int kHopS = 16384;      // hop / half FFT
 constexpr int kNOut = 8192;       // outputs per block
 constexpr int kK2Threads = 512;
-constexpr int kPlane2 = padded(kHopS);   // 17408 float2
+constexpr int kRowE = 1025;              // FFT16384 rows (16 x 1024, +1 pad)
+constexpr int kRowI = 513;               // IFFT8192 rows (16 x 512, +1 pad)
 constexpr int kRotMax = 1024;            // rotation-table entries held in smem
 
 struct K2Smem {
-    float2 buf[kPlane2];
-    float2 A[kNOut];
-    float2 tw[kTwEntries];
-    float2 rot[kRotMax];
+    float2 buf[16 * kRowE];              // 131,200 B
+    float2 A[padded(kNOut)];             // 69,632 B: chain 0 result / output staging
+    float2 tw[kTwEntries];               // 18,368 B
+    float2 rot[kRotMax];                 // 8,192 B
 };
+static_assert(sizeof(K2Smem) <= 232448, "K2 shared memory");
 
 struct K2Params {
     const float2* z;        // KK output stream (conj(field * rot)), z[0] = global index z_index0
@@ -115,50 +124,60 @@ __device__ __forceinline__ float2 static_input(const K2Params& p, const BlockIn&
     return v;
 }
 
-// Pass 1 of the chain-c FFT16384, butterfly j: v[r] = a(n) (c = 0) or b(n)
-// (c = 1) at n = j + 1024 r.  FAST: interior block with at most one carrier
-// segment boundary (incremental indices); otherwise the generic path.
+// Step 1 input of the chain-c FFT16384, column j: v[r] = a(n) (c = 0) or
+// (x0 - x1)(n) W32^r (c = 1) at n = j + 1024 r; the remaining W32768^j of the
+// odd-bin pre-twiddle is common to the column and folded into the post-DFT
+// twiddle chain.  FAST: interior block of a stream whose carrier segments
+// are whole multiples of the hop, so the mean is constant over x0 and over
+// x1 and the carrier conj(mean * rot[n]) is a running product over r
+// (rot(n + 1024) = rot(n) rot(1024)); otherwise the generic per-sample path
+// (with the full W32768^n pre-twiddle applied here, step1_twiddle = false).
 template <int CHAIN, bool FAST>
-__device__ __forceinline__ void k2_load_bfly(const K2Params& p, const BlockIn& b, const float2* rot_s,
-                                             const Twiddle& tw, int j, float2 mA, float2 mB, int bnd,
-                                             unsigned s1024, unsigned s16384, float2 (&v)[1][16]) {
+__device__ __forceinline__ void k2_load_column(const K2Params& p, const BlockIn& b, const float2* rot_s,
+                                               const Twiddle& tw, int j, float2 mA, float2 mB, int bnd,
+                                               unsigned s1024, unsigned s16384, float2 (&v)[16]) {
     if constexpr (FAST) {
         const float2* z0 = p.z + (b.base - p.z_index0) + j;
-        const unsigned Q = static_cast<unsigned>(p.rot_q);
-        unsigned a0 = 0, a1 = 0;
-        if (p.carrier && Q) {
-            a0 = fmod_u(b.c0 + static_cast<unsigned>(p.rot_p) * static_cast<unsigned>(j), Q, b.inv_q);
-            a1 = a0 + s16384;
-            a1 -= (a1 >= Q) ? Q : 0u;
+        float2 c0 = make_float2(0.f, 0.f), c1 = c0, st = make_float2(1.f, 0.f);
+        if (p.carrier) {
+            const float2 m1 = bnd <= kHopS ? mB : mA;
+            c0 = mA;
+            c1 = m1;
+            const unsigned Q = static_cast<unsigned>(p.rot_q);
+            if (Q) {
+                const unsigned a0 = fmod_u(b.c0 + static_cast<unsigned>(p.rot_p) * static_cast<unsigned>(j), Q, b.inv_q);
+                unsigned a1 = a0 + s16384;
+                a1 -= (a1 >= Q) ? Q : 0u;
+                c0 = cmul(c0, rot_s[a0]);
+                c1 = cmul(c1, rot_s[a1]);
+                st = rot_s[s1024];
+            }
+            if (p.mirror) {
+                c0 = cconj(c0);
+                c1 = cconj(c1);
+                st = cconj(st);
+            }
         }
 #pragma unroll
         for (int r = 0; r < 16; ++r) {
-            const int n = j + 1024 * r;
             float2 x0 = __ldg(z0 + 1024 * r);
             float2 x1 = __ldg(z0 + kHopS + 1024 * r);
             if (p.carrier) {
-                float2 m0 = n < bnd ? mA : mB;
-                float2 m1 = (n + kHopS) < bnd ? mA : mB;
-                if (Q) {
-                    m0 = cmul(m0, rot_s[a0]);
-                    m1 = cmul(m1, rot_s[a1]);
-                    a0 += s1024; a0 -= (a0 >= Q) ? Q : 0u;
-                    a1 += s1024; a1 -= (a1 >= Q) ? Q : 0u;
-                }
-                if (p.mirror) { m0 = cconj(m0); m1 = cconj(m1); }
-                x0 = csub(x0, m0);
-                x1 = csub(x1, m1);
+                x0 = csub(x0, c0);
+                x1 = csub(x1, c1);
+                c0 = cmul(c0, st);
+                c1 = cmul(c1, st);
             }
-            if constexpr (CHAIN == 0) v[0][r] = cadd(x0, x1);
-            else v[0][r] = cmul(csub(x0, x1), tw.template w<kNS>(n));
+            if constexpr (CHAIN == 0) v[r] = cadd(x0, x1);
+            else v[r] = tw32<false>(csub(x0, x1), r);
         }
     } else {
 #pragma unroll
         for (int r = 0; r < 16; ++r) {
             const int n = j + 1024 * r;
             const float2 x0 = static_input(p, b, rot_s, n), x1 = static_input(p, b, rot_s, kHopS + n);
-            if constexpr (CHAIN == 0) v[0][r] = cadd(x0, x1);
-            else v[0][r] = cmul(csub(x0, x1), tw.template w<kNS>(n));
+            if constexpr (CHAIN == 0) v[r] = cadd(x0, x1);
+            else v[r] = tw32<false>(csub(x0, x1), r);
         }
     }
 }
@@ -205,49 +224,71 @@ __global__ void __launch_bounds__(kK2Threads, 1) static_blocks_kernel(K2Params p
         }
     }
 
+    const int warp = tid >> 5, lane = tid & 31;
+    float2* E = S.buf;
     for (int chain = 0; chain < 2; ++chain) {
-        // ---- FFT16384 of a = x0 + x1 (even bins) or b = (x0 - x1) W^n (odd) ----
+        // ---- FFT16384 step 1: column n2 = j, DFT16 over n1 (stride 1024),
+        //      W16384^{j k1}, -> row k1, position j ----
 #pragma unroll 1
-        for (int q = 0; q < kHopS / 16 / kK2Threads; ++q) {
-            float2 v[1][16];
+        for (int q = 0; q < 1024 / kK2Threads; ++q) {
+            float2 v[16];
             const int j = tid + q * kK2Threads;
-            if (chain == 0) k2_load_bfly<0, FAST>(p, bi, S.rot, tw, j, mA, mB, bnd, s1024, s16384, v);
-            else k2_load_bfly<1, FAST>(p, bi, S.rot, tw, j, mA, mB, bnd, s1024, s16384, v);
-            stockham_compute_store<kHopS, 16, 1, kK2Threads, false, 1>(j, tw, v, StorePlanes{P});
+            if (chain == 0) k2_load_column<0, FAST>(p, bi, S.rot, tw, j, mA, mB, bnd, s1024, s16384, v);
+            else k2_load_column<1, FAST>(p, bi, S.rot, tw, j, mA, mB, bnd, s1024, s16384, v);
+            dft_reg<16, false>(v);
+            // W16384^{j k1}; chain 1 also W32768^j: W32768^{j (2 k1 + 1)}
+            const float2 s2 = tw.template w<kHopS>(j);
+            float2 wr = s2;
+            if (chain == 1) {
+                wr = tw.template w<kNS>(j);
+                v[0] = cmul(v[0], wr);
+            }
+#pragma unroll
+            for (int k1 = 1; k1 < 16; ++k1) {
+                if (chain == 1 || k1 > 1) wr = cmul(wr, s2);
+                v[k1] = cmul(v[k1], wr);
+            }
+#pragma unroll
+            for (int k1 = 0; k1 < 16; ++k1) E[k1 * kRowE + j] = v[k1];
         }
         __syncthreads();
-        stockham_pass<kHopS, 16, 16, kK2Threads, false, true>(tid, tw, LoadPlanes{P}, StorePlanes{P});
-        __syncthreads();
-        stockham_pass<kHopS, 16, 256, kK2Threads, false, true>(tid, tw, LoadPlanes{P}, StorePlanes{P});
-        __syncthreads();
-        stockham_pass<kHopS, 4, 4096, kK2Threads, false, true>(tid, tw, LoadPlanes{P}, StorePlanes{P});
+        // ---- FFT16384 step 2: warp k1 transforms row k1 -> bin k1 + 16 k2 at [k1][k2] ----
+        warp_fft1024<false>(E + warp * kRowE, lane, tw);
         __syncthreads();
 
-        // ---- IFFT8192 of the kept quarters times H ----
+        // ---- IFFT8192 step 1: column m2 = tid of the kept bins x H (stride 512) ----
         const float2* h = chain == 0 ? p.h_even : p.h_odd;
-        auto ld_k = [&](int m) {
-            const int src = m < 4096 ? m : m + 8192;
-            return cmul(P.ld(src), __ldg(h + m));
-        };
-        stockham_pass<kNOut, 16, 1, kK2Threads, true, true>(tid, tw, ld_k, StorePlanes{P});
+        float2 u[16];
+#pragma unroll
+        for (int r = 0; r < 16; ++r) {
+            const int m = tid + 512 * r;
+            const int k = r < 8 ? m : m + 8192;          // kept bins: low and high quarters
+            u[r] = cmul(E[(k & 15) * kRowE + (k >> 4)], __ldg(h + m));
+        }
         __syncthreads();
-        stockham_pass<kNOut, 16, 16, kK2Threads, true, true>(tid, tw, LoadPlanes{P}, StorePlanes{P});
+        dft_reg<16, true>(u);
+        apply_twiddle_chain<16, true>(u, tw.template w<kNOut>(tid));
+#pragma unroll
+        for (int p1 = 0; p1 < 16; ++p1) E[p1 * kRowI + tid] = u[p1];
         __syncthreads();
-        stockham_pass<kNOut, 8, 256, kK2Threads, true, true>(tid, tw, LoadPlanes{P}, StorePlanes{P});
-        __syncthreads();
+        // ---- IFFT8192 step 2: warp p1 transforms row p1 -> sample p1 + 16 p2 ----
         if (chain == 0) {
-            auto st_a = [&](int n, float2 v) { S.A[n] = v; };
-            stockham_pass<kNOut, 4, 2048, kK2Threads, true, false>(tid, tw, LoadPlanes{P}, st_a);
+            auto st_a = [&](int p2, float2 v) { S.A[padi(warp + 16 * p2)] = v; };
+            warp_fft512<true>(E + warp * kRowI, lane, tw, st_a);
             __syncthreads();
         } else {
-            float2* out = p.out + int64_t(blockIdx.x) * kNOut;
             const float sc = 0.5f / 16384.0f;
-            auto st_o = [&](int r, float2 v) {
-                // W16384^{-r} = conj(W32768^{2r})
+            auto st_o = [&](int p2, float2 v) {
+                const int r = warp + 16 * p2;
+                // W16384^{-r} B[r]
                 const float2 bt = cmulc(v, tw.template w<kHopS>(r));
-                out[r] = cscale(csub(S.A[r], bt), sc);
+                S.A[padi(r)] = cscale(csub(S.A[padi(r)], bt), sc);
             };
-            stockham_pass<kNOut, 4, 2048, kK2Threads, true, false>(tid, tw, LoadPlanes{P}, st_o);
+            warp_fft512<true>(E + warp * kRowI, lane, tw, st_o);
+            __syncthreads();
+            float2* out = p.out + int64_t(blockIdx.x) * kNOut;
+#pragma unroll 4
+            for (int i = tid; i < kNOut; i += kK2Threads) out[i] = S.A[padi(i)];
         }
     }
 }
@@ -298,7 +339,7 @@ extern "C" int kk_static_blocks(const void* z, int64_t z_index0, int64_t hb0, in
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     const int64_t hb1 = hb0 + n_blocks;
     int64_t lo = hb0, hi = hb1;
-    if (!carrier || seg_len >= kNS) {
+    if (!carrier || (seg_len >= kNS && seg_len % kHopS == 0)) {
         lo = std::max<int64_t>(hb0, 1);
         hi = std::min<int64_t>(hb1, valid_end / kHopS);
         if (hi < lo) { lo = hb0; hi = hb0; }
