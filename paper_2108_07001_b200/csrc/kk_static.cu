@@ -138,11 +138,13 @@ __device__ __forceinline__ void k2_load_column(const K2Params& p, const BlockIn&
                                                unsigned s1024, unsigned s16384, float2 (&v)[16]) {
     if constexpr (FAST) {
         const float2* z0 = p.z + (b.base - p.z_index0) + j;
-        float2 c0 = make_float2(0.f, 0.f), c1 = c0, st = make_float2(1.f, 0.f);
+        // carrier over the column: x0 part c0 st^r, x1 part c1 st^r, so the
+        // chain input needs only their sum (c0 + c1) or difference (c0 - c1)
+        // as one running product
+        float2 cc = make_float2(0.f, 0.f), st = make_float2(1.f, 0.f);
         if (p.carrier) {
             const float2 m1 = bnd <= kHopS ? mB : mA;
-            c0 = mA;
-            c1 = m1;
+            float2 c0 = mA, c1 = m1;
             const unsigned Q = static_cast<unsigned>(p.rot_q);
             if (Q) {
                 const unsigned a0 = fmod_u(b.c0 + static_cast<unsigned>(p.rot_p) * static_cast<unsigned>(j), Q, b.inv_q);
@@ -152,24 +154,23 @@ __device__ __forceinline__ void k2_load_column(const K2Params& p, const BlockIn&
                 c1 = cmul(c1, rot_s[a1]);
                 st = rot_s[s1024];
             }
+            cc = CHAIN == 0 ? cadd(c0, c1) : csub(c0, c1);
             if (p.mirror) {
-                c0 = cconj(c0);
-                c1 = cconj(c1);
+                cc = cconj(cc);
                 st = cconj(st);
             }
         }
 #pragma unroll
         for (int r = 0; r < 16; ++r) {
-            float2 x0 = __ldg(z0 + 1024 * r);
-            float2 x1 = __ldg(z0 + kHopS + 1024 * r);
+            const float2 x0 = __ldg(z0 + 1024 * r);
+            const float2 x1 = __ldg(z0 + kHopS + 1024 * r);
+            float2 u = CHAIN == 0 ? cadd(x0, x1) : csub(x0, x1);
             if (p.carrier) {
-                x0 = csub(x0, c0);
-                x1 = csub(x1, c1);
-                c0 = cmul(c0, st);
-                c1 = cmul(c1, st);
+                u = csub(u, cc);
+                cc = cmul(cc, st);
             }
-            if constexpr (CHAIN == 0) v[r] = cadd(x0, x1);
-            else v[r] = tw32<false>(csub(x0, x1), r);
+            if constexpr (CHAIN == 0) v[r] = u;
+            else v[r] = tw32<false>(u, r);
         }
     } else {
 #pragma unroll
