@@ -78,12 +78,15 @@ __device__ __forceinline__ void apply_twiddle_chain(float2 (&v)[R], float2 w1) {
 // conflict-free in-row transpose slot of element (c, a) of a [C][32] tile
 __device__ __forceinline__ int xpose_slot(int c, int a) { return c * 32 + ((a + c) & 31); }
 
-// 1024-point FFT of row[0..1024) (natural order in and out) by one warp.
-template <bool INV>
-__device__ __forceinline__ void warp_fft1024(float2* row, int lane, const Twiddle& tw) {
+// 1024-point FFT by one warp with fused I/O: input element i comes from
+// load(i) (i = lane + 32 b), output k = lane + 32 d goes to store(d, k, v)
+// (d compile-time after unrolling); row[0..1024) is the transpose scratch.
+template <bool INV, class Load, class Store>
+__device__ __forceinline__ void warp_fft1024_io(float2* row, int lane, const Twiddle& tw, const Load& load,
+                                                const Store& store) {
     float2 v[32];
 #pragma unroll
-    for (int b = 0; b < 32; ++b) v[b] = row[lane + 32 * b];
+    for (int b = 0; b < 32; ++b) v[b] = load(lane + 32 * b);
     dft32<INV>(v);
     apply_twiddle_chain<32, INV>(v, tw.template w<1024>(lane));
     __syncwarp();
@@ -95,8 +98,15 @@ __device__ __forceinline__ void warp_fft1024(float2* row, int lane, const Twiddl
     dft32<INV>(v);
     __syncwarp();
 #pragma unroll
-    for (int d = 0; d < 32; ++d) row[lane + 32 * d] = v[d];
+    for (int d = 0; d < 32; ++d) store(d, lane + 32 * d, v[d]);
     __syncwarp();
+}
+
+// 1024-point FFT of row[0..1024) (natural order in and out) by one warp.
+template <bool INV>
+__device__ __forceinline__ void warp_fft1024(float2* row, int lane, const Twiddle& tw) {
+    warp_fft1024_io<INV>(row, lane, tw, [&](int i) { return row[i]; },
+                         [&](int, int k, float2 v) { row[k] = v; });
 }
 
 // 512-point FFT of row[0..512) by one warp; output k = c + 16 (2 d + h) of
