@@ -183,6 +183,14 @@ int kk_bit_errors(const uint8_t *labels, const uint8_t *ref_idx, int64_t n, cons
 int kk_demap(const void *symbols, int64_t n, int order, const float *pts_host, uint8_t *idx,
              unsigned long long *n_fallback, void *stream);
 
+/*
+ * Receiver output bits -- decided labels demapped (rxdsp.py:548-567 bit
+ * order) and packed MSB first (np.packbits layout): out[(n*k + 7) / 8].
+ * Label 255 (training) takes train_idx[sym0 + i] when sym0 + i < n_train.
+ */
+int kk_pack_bits(const uint8_t *labels, int64_t n, int64_t sym0, const uint8_t *train_idx, int64_t n_train,
+                 int bits_per_symbol, const uint8_t *point_label_host, int order, uint8_t *out, void *stream);
+
 #ifdef __cplusplus
 }
 #endif

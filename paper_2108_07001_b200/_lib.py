@@ -56,6 +56,7 @@ _SIGS = {
     "kk_ddlms_destroy": ([_P], None),
     "kk_bit_errors": ([_P, _P, _I64, _P, _I64, _P, _P, _I64, _I64, _I64, _P, _P], _I),
     "kk_demap": ([_P, _I64, _I, _P, _P, _P, _P], _I),
+    "kk_pack_bits": ([_P, _I64, _I64, _P, _I64, _I, _P, _I, _P, _P], _I),
 }
 
 EXPORTED = sorted(_SIGS)

@@ -1648,3 +1648,56 @@ extern "C" int kk_demap(const void* symbols, int64_t n, int order, const float* 
         static_cast<const float2*>(symbols), n, sl, idx, n_fallback);
     return check_launch("demap_kernel");
 }
+
+// ---------------------------------------------------------------------------
+// Decided labels -> demapped bit stream, packed MSB first (the receiver's
+// output: rxdsp.py demap :548-567 bit order, np.packbits layout).  Label 255
+// (training symbol) takes the training symbol's point index train_idx[k].
+// One thread per output byte; bit b belongs to symbol b / k, bit k-1-(b % k).
+// ---------------------------------------------------------------------------
+namespace kk {
+struct PointLabels {
+    uint8_t v[64];
+};
+__global__ void pack_bits_kernel(const uint8_t* __restrict__ lab, int64_t n, int64_t sym0,
+                                 const uint8_t* __restrict__ train_idx, int64_t n_train, PointLabels pl, int k,
+                                 uint8_t* __restrict__ out, int64_t nbytes) {
+    for (int64_t o = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; o < nbytes;
+         o += int64_t(gridDim.x) * blockDim.x) {
+        unsigned byte = 0;
+        int64_t b = o * 8;
+#pragma unroll 1
+        for (int t = 0; t < 8; ++t, ++b) {
+            const int64_t s = b / k;
+            unsigned bit = 0;
+            if (s < n) {
+                int li = lab[s];
+                if (li == 255) li = (sym0 + s < n_train && train_idx) ? train_idx[sym0 + s] : 0;
+                const int word = pl.v[li & 63];
+                bit = (word >> (k - 1 - static_cast<int>(b - s * k))) & 1;
+            }
+            byte |= bit << (7 - t);
+        }
+        out[o] = static_cast<uint8_t>(byte);
+    }
+}
+}  // namespace kk
+
+extern "C" int kk_pack_bits(const uint8_t* labels, int64_t n, int64_t sym0, const uint8_t* train_idx,
+                            int64_t n_train, int bits_per_symbol, const uint8_t* point_label_host, int order,
+                            uint8_t* out, void* stream) {
+    using namespace kk;
+    clear_error();
+    if (bits_per_symbol < 1 || bits_per_symbol > 6 || order > 64 || order < 2)
+        return set_error(KK_ERR_PARAM, "bits_per_symbol must be in [1, 6], order in [2, 64]");
+    if (n <= 0) return KK_OK;
+    PointLabels pl{};
+    for (int i = 0; i < order; ++i) pl.v[i] = point_label_host[i];
+    const int64_t nbytes = (n * bits_per_symbol + 7) / 8;
+    const int th = 256;
+    int64_t blocks = (nbytes + th - 1) / th;
+    if (blocks > 148 * 32) blocks = 148 * 32;
+    pack_bits_kernel<<<static_cast<unsigned>(blocks), th, 0, static_cast<cudaStream_t>(stream)>>>(
+        labels, n, sym0, train_idx, n_train, pl, bits_per_symbol, out, nbytes);
+    return check_launch("pack_bits_kernel");
+}

@@ -11,6 +11,7 @@ from __future__ import annotations
 
 import numpy as np
 
+from . import _lib
 from .constellation import make_constellation
 from .metrics import SyncFailure, count_bit_errors, evm, frame_sync, q_from_ber, windowed_q
 from .rxdsp import (
@@ -87,20 +88,23 @@ def device_ber(labels, ref_idx, order: int, head: int, stop: int, tile_symbols: 
 
 
 def receive_host_stream(cfg, host_codes, half_lsb: float, reference_symbols, chunk_samples: int = 1 << 25,
-                        labels_host=None, device=None, staging=None):
-    """End-to-end receive of an int16 ADC stream in pinned HOST memory.
+                        bits_host=None, device=None, staging=None):
+    """End-to-end receive of an int16 ADC stream in pinned HOST memory; the
+    receiver's output -- the demapped bit stream, packed (np.packbits
+    layout) -- lands in pinned host memory.
 
     Every chunk's host->device copy is queued up front on a side stream into
     one device staging buffer (HBM is plentiful; the copy engine then streams
     at the full PCIe rate however long the receiver blocks the host), the
-    compute stream waits per chunk on its copy event, and the decided labels
-    of every completed DDLMS frame go back to (pinned) host memory on a third
-    stream as they are released -- both PCIe directions overlap the GPU work.
-    `staging` (optional) is a reusable int16 device buffer of >= n samples.
-    Returns (pipe, labels_host, n_decided).
+    compute stream waits per chunk on its copy event, and the bits of every
+    completed DDLMS frame go back on a third stream as they are released --
+    both PCIe directions overlap the GPU work.  `staging` (optional) is a
+    reusable int16 device buffer of >= n samples.
+    Returns (pipe, bits_host, n_symbols_decided).
     """
     import torch
 
+    from .constellation import make_constellation, slicer_tables
     from .sigcore import AdcCodes
 
     dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
@@ -114,28 +118,46 @@ def receive_host_stream(cfg, host_codes, half_lsb: float, reference_symbols, chu
     # behind the bulk transfers on the in-order host->device copy engine
     pipe = RxPipeline(cfg, reference_symbols=reference_symbols, device=dev)
     pipe.expect(n, chunk_samples)
+    order = cfg.constellation_order
+    k = make_constellation(order).bits_per_symbol
+    tb = slicer_tables(order)
+    train_idx = None
+    n_train = 0
+    if reference_symbols is not None:
+        ref = np.asarray(reference_symbols, np.complex128)[:cfg.ddlms.startup_symbols]
+        pts = make_constellation(order).points
+        ti = np.argmin(np.abs(ref[:, None] - pts[None, :]), axis=1).astype(np.uint8)
+        train_idx = torch.from_numpy(ti).to(dev)
+        n_train = len(ti)
     starts = list(range(0, n, chunk_samples))
     ready = [torch.cuda.Event() for _ in starts]
-    copy.wait_stream(comp)          # the staging buffer's previous readers
+    copy.wait_stream(comp)          # the staging buffer's previous readers (and the uploads)
     with torch.cuda.stream(copy):
         for i, a in enumerate(starts):
             m = min(chunk_samples, n - a)
             staging[a:a + m].copy_(host_codes[a:a + m], non_blocking=True)
             ready[i].record(copy)
-    if labels_host is None:
-        labels_host = torch.empty(n // 4 + 8, dtype=torch.uint8, pin_memory=True)
+    if bits_host is None:
+        bits_host = torch.empty((n // 4 + 8) * k // 8 + 8, dtype=torch.uint8, pin_memory=True)
     n_out = 0
+    b_out = 0
     for i, a in enumerate(starts):
         m = min(chunk_samples, n - a)
         comp.wait_event(ready[i])
         pipe.feed(AdcCodes(staging[a:a + m], half_lsb, cfg.adc_rate_hz), flush=i == len(starts) - 1)
         lab, _, _ = pipe.drain_device()
         if lab.numel():
+            nb = (lab.numel() * k + 7) // 8
+            packed = torch.empty(nb, dtype=torch.uint8, device=dev)
+            _lib.call("kk_pack_bits", lab.data_ptr(), lab.numel(), n_out,
+                      train_idx.data_ptr() if train_idx is not None else None, n_train, k,
+                      tb.point_label.ctypes.data, order, packed.data_ptr(), comp.cuda_stream)
             # device -> host on its own stream (the other DMA direction)
             d2h.wait_stream(comp)
             with torch.cuda.stream(d2h):
-                labels_host[n_out:n_out + lab.numel()].copy_(lab, non_blocking=True)
-            lab.record_stream(d2h)
+                bits_host[b_out:b_out + nb].copy_(packed, non_blocking=True)
+            packed.record_stream(d2h)
             n_out += lab.numel()
+            b_out += nb
     comp.wait_stream(d2h)
-    return pipe, labels_host, n_out
+    return pipe, bits_host, n_out
