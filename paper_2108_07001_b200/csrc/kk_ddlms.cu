@@ -25,6 +25,8 @@
 // sequential chain.
 #include <algorithm>
 #include <cmath>
+#include <cstring>
+#include <mutex>
 #include <vector>
 
 #include "kk_common.cuh"
@@ -1070,6 +1072,25 @@ extern "C" int kk_ddlms_sequential(const void* x, int64_t n_out, float scale, in
     return check_launch("ddlms_seq_kernel");
 }
 
+
+// Small device->host reads through a per-thread pinned staging buffer (a
+// copy to pageable memory goes through the driver's shared bounce buffer and
+// stalls other host threads' CUDA calls while it waits on this stream).
+static int d2h_small(void* dst, const void* src, size_t bytes, cudaStream_t s) {
+    static thread_local void* pin = nullptr;
+    constexpr size_t kPin = 64 << 10;
+    if (bytes > kPin) return set_error(KK_ERR_PARAM, "d2h_small: too large");
+    if (!pin && cudaHostAlloc(&pin, kPin, cudaHostAllocDefault) != cudaSuccess) {
+        pin = nullptr;
+        return set_cuda_error("pinned staging");
+    }
+    if (cudaMemcpyAsync(pin, src, bytes, cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+        cudaStreamSynchronize(s) != cudaSuccess)
+        return set_cuda_error("device->host readback");
+    std::memcpy(dst, pin, bytes);
+    return KK_OK;
+}
+
 namespace {
 constexpr int kG = 32;   // scan fan-in
 
@@ -1180,10 +1201,8 @@ struct DdlmsSolver {
         if (!agg) return KK_OK;
         const int64_t n = lv[top].n;
         std::vector<float> P(n * 64), Q(n * 16);
-        if (cudaMemcpyAsync(P.data(), lv[top].P, P.size() * 4, cudaMemcpyDeviceToHost, s) != cudaSuccess ||
-            cudaMemcpyAsync(Q.data(), lv[top].Q, Q.size() * 4, cudaMemcpyDeviceToHost, s) != cudaSuccess ||
-            cudaStreamSynchronize(s) != cudaSuccess)
-            return set_cuda_error("frame map readback");
+        if (int rc = d2h_small(P.data(), lv[top].P, P.size() * 4, s)) return rc;
+        if (int rc = d2h_small(Q.data(), lv[top].Q, Q.size() * 4, s)) return rc;
         double Pa[64], Qa[16];
         for (int i = 0; i < 64; ++i) Pa[i] = (i % 9 == 0) ? 1.0 : 0.0;
         for (int i = 0; i < 16; ++i) Qa[i] = 0.0;
@@ -1228,10 +1247,14 @@ struct DdlmsSolver {
     // launch -- compacted into a re-run list first when use_skip.
     int run_blocks(bool with_p, int64_t b0, int64_t b1, int use_skip, float tol = 0.f, int write_out = 0) {
         if (b1 <= b0) return KK_OK;
-        static thread_local int attr_dev = -1;
+        // kernel attributes once per device and process (cudaFuncSetAttribute
+        // can serialise against work in flight on other threads' streams)
+        static std::once_flag attr_once[64];
+        static int attr_rc[64] = {0};
         int dev = 0;
         cudaGetDevice(&dev);
-        if (attr_dev != dev) {
+        if (dev < 0 || dev >= 64) return set_error(KK_ERR_CUDA, "device index");
+        std::call_once(attr_once[dev], [&]() {
             struct KS { const void* k; size_t smem; };
             const KS ks[] = {
 #define KK_DD_K(P_, S_, T_) {reinterpret_cast<const void*>(ddlms_block_kernel<P_, S_, true, T_>), T_ ? kStageSmem + kTrainSmem : kStageSmem}, \
@@ -1245,9 +1268,9 @@ struct DdlmsSolver {
             for (const KS& k : ks)
                 if (cudaFuncSetAttribute(k.k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(k.smem)) !=
                     cudaSuccess)
-                    return set_cuda_error("ddlms_block_kernel smem attribute");
-            attr_dev = dev;
-        }
+                    attr_rc[dev] = 1;
+        });
+        if (attr_rc[dev]) return set_error(KK_ERR_CUDA, "ddlms_block_kernel smem attribute");
         const int sq = sl.sep ? sl.m : 0;
         const bool al = (reinterpret_cast<uintptr_t>(a.x) & 15) == 0;
         auto launch = [&](bool train_blocks, int64_t lo, int64_t hi, int skip, const int* lst,
@@ -1290,10 +1313,7 @@ struct DdlmsSolver {
         return launch(false, d0, b1, 0, nullptr, nullptr);
     }
     int read_ctr(unsigned long long (&h)[4]) {
-        if (cudaMemcpyAsync(h, ctr, sizeof(h), cudaMemcpyDeviceToHost, s) != cudaSuccess ||
-            cudaStreamSynchronize(s) != cudaSuccess)
-            return set_cuda_error("counter readback");
-        return KK_OK;
+        return d2h_small(h, ctr, sizeof(h), s);
     }
 
     int init(const void* x, int64_t nsym, float scale_, const void* train, int64_t n_train, Slicer sl_, float mu,
@@ -1379,15 +1399,11 @@ struct DdlmsSolver {
         if (T_train_end) {
             float Tt[16];
             if (bt < L.nb) {
-                if (cudaMemcpyAsync(Tt, lv[0].T + bt * 16, sizeof(Tt), cudaMemcpyDeviceToHost, s) != cudaSuccess ||
-                    cudaStreamSynchronize(s) != cudaSuccess)
-                    return set_cuda_error("T train end");
+                if (int rc = d2h_small(Tt, lv[0].T + bt * 16, sizeof(Tt), s)) return rc;
                 for (int i = 0; i < 16; ++i) T_train_end[i] = Tt[i] / scale;
             } else {
                 // training covers the frame: its end taps
-                if (cudaMemcpyAsync(Tt, Tend, sizeof(Tt), cudaMemcpyDeviceToHost, s) != cudaSuccess ||
-                    cudaStreamSynchronize(s) != cudaSuccess)
-                    return set_cuda_error("T train end");
+                if (int rc = d2h_small(Tt, Tend, sizeof(Tt), s)) return rc;
                 for (int i = 0; i < 16; ++i) T_train_end[i] = Tt[i] / scale;
             }
         }
@@ -1461,9 +1477,7 @@ struct DdlmsSolver {
         if (guard) *guard = static_cast<int64_t>(h[2]);
         if (T_final) {
             float Tt[16];
-            if (cudaMemcpyAsync(Tt, Tend, sizeof(Tt), cudaMemcpyDeviceToHost, s) != cudaSuccess ||
-                cudaStreamSynchronize(s) != cudaSuccess)
-                return set_cuda_error("T_final");
+            if (int rc = d2h_small(Tt, Tend, sizeof(Tt), s)) return rc;
             for (int i = 0; i < 16; ++i) T_final[i] = Tt[i] / scale;
         }
         return KK_OK;
@@ -1608,10 +1622,7 @@ extern "C" int kk_symbol_sync(const void* head, int64_t n_head, const void* ref,
     }
     sync_reduce_kernel<<<1, 1024, 0, s>>>(mag, nl0, nl1, static_cast<const float2*>(head), n_head, skip, res);
     if (int rc = check_launch("sync_reduce_kernel")) return rc;
-    if (cudaMemcpyAsync(result, res, 4 * sizeof(double), cudaMemcpyDeviceToHost, s) != cudaSuccess ||
-        cudaStreamSynchronize(s) != cudaSuccess)
-        return set_cuda_error("sync readback");
-    return KK_OK;
+    return d2h_small(result, res, 4 * sizeof(double), s);
 }
 
 extern "C" size_t kk_symbol_sync_scratch_bytes(int64_t n_head, int n_ref) {

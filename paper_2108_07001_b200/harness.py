@@ -14,6 +14,7 @@ import numpy as np
 from . import _lib
 from .constellation import make_constellation
 from .metrics import SyncFailure, count_bit_errors, evm, frame_sync, q_from_ber, windowed_q
+from .rxdsp import side_stream
 from .rxdsp import (
     DdlmsConfig, GpuOptions, RxPipeline, RxPipelineConfig, compute_static_taps, demap, design_receive_taps,
 )
@@ -88,7 +89,7 @@ def device_ber(labels, ref_idx, order: int, head: int, stop: int, tile_symbols: 
 
 
 def receive_host_stream(cfg, host_codes, half_lsb: float, reference_symbols, chunk_samples: int = 1 << 25,
-                        bits_host=None, device=None, staging=None):
+                        bits_host=None, device=None, staging=None, trace=None):
     """End-to-end receive of an int16 ADC stream in pinned HOST memory; the
     receiver's output -- the demapped bit stream, packed (np.packbits
     layout) -- lands in pinned host memory.
@@ -108,14 +109,36 @@ def receive_host_stream(cfg, host_codes, half_lsb: float, reference_symbols, chu
     from .sigcore import AdcCodes
 
     dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+    caller = torch.cuda.current_stream(dev)
+    comp = side_stream(dev, "front")
+    comp.wait_stream(caller)
+    with torch.cuda.stream(comp):
+        out = _receive_host_stream(cfg, host_codes, half_lsb, reference_symbols, chunk_samples, bits_host, dev,
+                                   staging, trace, comp)
+    caller.wait_stream(comp)
+    return out
+
+
+def _receive_host_stream(cfg, host_codes, half_lsb, reference_symbols, chunk_samples, bits_host, dev, staging,
+                         trace, comp):
+    import torch
+
+    from .constellation import make_constellation, slicer_tables
+    from .sigcore import AdcCodes
+
     n = int(host_codes.shape[0])
-    comp = torch.cuda.current_stream(dev)
-    copy = torch.cuda.Stream(device=dev)
-    d2h = torch.cuda.Stream(device=dev)
+    copy = side_stream(dev, "h2d")
+    d2h = side_stream(dev, "d2h")
     if staging is None or staging.numel() < n:
         staging = torch.empty(n, dtype=torch.int16, device=dev)
     # the pipeline's own uploads go first: later small H2D copies would queue
-    # behind the bulk transfers on the in-order host->device copy engine
+    # behind the bulk transfers on the in-order host->device copy engine.
+    # DDLMS frames run asynchronously (worker thread + stream) so the front
+    # end of later chunks overlaps them.
+    import dataclasses
+
+    gpu = dataclasses.replace(cfg.gpu, ddlms_async=True)
+    cfg = dataclasses.replace(cfg, gpu=gpu)
     pipe = RxPipeline(cfg, reference_symbols=reference_symbols, device=dev)
     pipe.expect(n, chunk_samples)
     order = cfg.constellation_order
@@ -145,18 +168,25 @@ def receive_host_stream(cfg, host_codes, half_lsb: float, reference_symbols, chu
         m = min(chunk_samples, n - a)
         comp.wait_event(ready[i])
         pipe.feed(AdcCodes(staging[a:a + m], half_lsb, cfg.adc_rate_hz), flush=i == len(starts) - 1)
-        lab, _, _ = pipe.drain_device()
+        if trace is not None:
+            import time
+
+            ev = torch.cuda.Event(enable_timing=True)
+            ev.record(comp)
+            trace.append((i, time.perf_counter(), ready[i], ev, len(pipe._jobs)))
+        # finished frames, valid on the d2h stream: pack + device -> host there
+        # (the other DMA direction), off the compute stream
+        lab, soft, _ = pipe.drain_device(wait_stream=d2h)
         if lab.numel():
             nb = (lab.numel() * k + 7) // 8
-            packed = torch.empty(nb, dtype=torch.uint8, device=dev)
-            _lib.call("kk_pack_bits", lab.data_ptr(), lab.numel(), n_out,
-                      train_idx.data_ptr() if train_idx is not None else None, n_train, k,
-                      tb.point_label.ctypes.data, order, packed.data_ptr(), comp.cuda_stream)
-            # device -> host on its own stream (the other DMA direction)
-            d2h.wait_stream(comp)
             with torch.cuda.stream(d2h):
+                packed = torch.empty(nb, dtype=torch.uint8, device=dev)
+                _lib.call("kk_pack_bits", lab.data_ptr(), lab.numel(), n_out,
+                          train_idx.data_ptr() if train_idx is not None else None, n_train, k,
+                          tb.point_label.ctypes.data, order, packed.data_ptr(), d2h.cuda_stream)
                 bits_host[b_out:b_out + nb].copy_(packed, non_blocking=True)
-            packed.record_stream(d2h)
+            lab.record_stream(d2h)
+            soft.record_stream(d2h)
             n_out += lab.numel()
             b_out += nb
     comp.wait_stream(d2h)

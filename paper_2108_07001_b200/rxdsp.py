@@ -124,6 +124,9 @@ class GpuOptions:
     ddlms_max_iter: int = 64
     ddlms_soft_tol: float = 1e-5
     ddlms_tail_min_symbols: int = 1 << 22
+    # run the DDLMS frames on a worker thread / CUDA stream so the front end
+    # of later chunks overlaps them (streaming receive, harness.receive_host_stream)
+    ddlms_async: bool = False
 
 
 @dataclass
@@ -263,6 +266,20 @@ def _as_device_input(x, dev):
     return torch.from_numpy(a).to(dev, non_blocking=True), _lib.KK_DTYPE_F64, 1.0
 
 
+_SIDE_STREAMS = {}
+
+
+def side_stream(dev, name: str, priority: int = 0):
+    """A persistent named side stream per device (reused across pipelines:
+    the caching allocator pools memory per stream, so fresh streams per call
+    would strand cached blocks).  priority < 0: scheduled ahead of others."""
+    torch = _torch()
+    key = (str(dev), name, priority)
+    if key not in _SIDE_STREAMS:
+        _SIDE_STREAMS[key] = torch.cuda.Stream(device=dev, priority=priority)
+    return _SIDE_STREAMS[key]
+
+
 class _DevStream:
     """Append-only device buffer on a global index with prefix trimming."""
 
@@ -274,11 +291,15 @@ class _DevStream:
         self.end = start   # global end index
         self.keep = start  # data before this global index may be dropped
 
+    before_realloc = None   # hook: readers of the old buffer must finish first
+
     def reserve(self, n_more: int):
         """Make room for n_more items at the end; returns the tensor slice
         (global [end, end + n_more)) to write into."""
         need = self.end + n_more - self.base
         if need > self.buf.shape[0]:
+            if self.before_realloc is not None:
+                self.before_realloc()
             live0 = max(self.keep, self.base)
             live = self.end - live0
             # exact fit for a first (one-shot) fill, geometric growth when streaming
@@ -297,6 +318,8 @@ class _DevStream:
         """Pre-size the buffer for n live items (avoids growth copies)."""
         if self.buf.shape[0] >= n:
             return
+        if self.before_realloc is not None:
+            self.before_realloc()
         live0 = max(self.keep, self.base)
         live = self.end - live0
         nb = self.torch.empty(max(n, live), dtype=self.buf.dtype, device=self.buf.device)
@@ -726,6 +749,11 @@ class RxPipeline:
         self._train_total = 0
         self._sym_done = 0
         self._expected_symbols = None     # set by expect(): geometric DDLMS tail
+        import collections
+        self._async = bool(getattr(self.gpu, "ddlms_async", False))
+        self._jobs = collections.deque()  # submitted asynchronous frames, in order
+        self._worker = None
+        self._y2.before_realloc = self._wait_frames
         st0 = EqualizerState.initial(cfg.ddlms.n_taps)
         self._w, self._g = st0.w, st0.g
         self._T = _T_from_wg(st0.w, st0.g) if cfg.ddlms.n_taps == 4 else None
@@ -795,7 +823,7 @@ class RxPipeline:
         hd = self._hd.reserve(n_hops)
         su, sa, sd = self._kk_state[self._kk_cur]
         nu, na, nd = self._kk_state[1 - self._kk_cur]
-        clamped_before = self._clamped.clone()
+        clamped_before = self._clamped * 1       # (a kernel, not a D2D memcpy)
         rq = self._rot_q
         _lib.call("kk_reconstruct_pairs", self._raw_dt, _ptr(chunk), float(self._raw_scale), 1e-12, n_hops,
                   _ptr(su), _ptr(sa), _ptr(sd), _ptr(nu), _ptr(na), _ptr(nd), _ptr(out), _ptr(hs), _ptr(hd),
@@ -806,7 +834,7 @@ class RxPipeline:
         self._hs.commit(n_hops)
         self._hd.commit(n_hops)
         # diagnostics are materialised lazily (no host sync per feed)
-        self._pending_diag.append((self._chunk_index, h0, n_hops, clamped_before, self._clamped.clone(),
+        self._pending_diag.append((self._chunk_index, h0, n_hops, clamped_before, self._clamped * 1,
                                    self._frozen))
 
     def _run_carrier(self, flush):
@@ -877,7 +905,7 @@ class RxPipeline:
         self._synced = True
         return True
 
-    def _solve_frame(self, k0, k1):
+    def _solve_frame_impl(self, k0, k1, labels=None, soft=None):
         torch = _torch()
         cfg = self.cfg
         d = cfg.ddlms
@@ -886,8 +914,9 @@ class RxPipeline:
         x_ptr = self._y2.ptr(q0)
         n_train = int(max(0, min(nsym, self._train_total - k0)))
         train_ptr = (self._ref_dev.data_ptr() + k0 * 8) if n_train > 0 else 0
-        labels = torch.empty(nsym, dtype=torch.uint8, device=self.dev)
-        soft = torch.empty(nsym, dtype=torch.complex64, device=self.dev)
+        if labels is None:
+            labels = torch.empty(nsym, dtype=torch.uint8, device=self.dev)
+            soft = torch.empty(nsym, dtype=torch.complex64, device=self.dev)
         tb = self._tables
         use_solve = (d.widely_linear and d.n_taps == 4 and not self._frozen and self._div_count == 0)
         stats = {"k0": k0, "nsym": nsym, "mode": "solve" if use_solve else "sequential"}
@@ -895,6 +924,8 @@ class RxPipeline:
             B = int(self.gpu.ddlms_block)
             wsb = int(_lib.load().kk_ddlms_workspace_bytes(nsym, B))
             if self._ws is None or self._ws.numel() < wsb:
+                if self._async:
+                    raise RuntimeError("asynchronous DDLMS frame without a pre-sized workspace")
                 self._ws = torch.empty(wsb, dtype=torch.uint8, device=self.dev)
             Tin = np.ascontiguousarray(self._T, dtype=np.float32)
             Tout = np.zeros(16, dtype=np.float32)
@@ -929,10 +960,109 @@ class RxPipeline:
             self._frozen, self._div_count = bool(f[0]), int(f[1])
             if d.n_taps == 4:
                 self._T = _T_from_wg(self._w, self._g)
+        return labels, soft, n_train, stats
+
+    def _solve_frame(self, k0, k1):
+        labels, soft, n_train, stats = self._solve_frame_impl(k0, k1)
         self.ddlms_stats.append(stats)
         self._out.append((labels, soft, k0, n_train))
         self._sym_done = k1
         self._y2.keep = self._drop + 2 * k1
+
+    # -- asynchronous DDLMS frames (GpuOptions.ddlms_async) ------------------
+    # The frames form one sequential recurrence (frame f+1 starts from frame
+    # f's end taps), so a single worker thread solves them in order on its
+    # own CUDA stream, each after an event marking that the front end has
+    # produced the frame's input; the host thread keeps feeding.  The worker
+    # owns the equalizer state (_T, _w, _g, _frozen, _div_count, _ws) while
+    # frames are pending.  Outputs are collected in order by drain_device().
+
+    def _submit_frame(self, k0, k1):
+        import queue
+        import threading
+
+        torch = _torch()
+        if self._worker is None:
+            self._job_q = queue.Queue()
+            # high priority: the frame chain is the critical path at the end
+            # of a stream (measured 0.1-0.5 GBaud better end to end)
+            self._worker_stream = side_stream(self.dev, "ddlms", -1)
+            self._worker = threading.Thread(target=self._worker_loop, daemon=True)
+            self._worker.start()
+        # device memory is allocated here, on the host thread's stream (the
+        # caching allocator pools per stream); the worker marks its use
+        nsym = k1 - k0
+        wsb = int(_lib.load().kk_ddlms_workspace_bytes(nsym, int(self.gpu.ddlms_block)))
+        if self._ws is None or self._ws.numel() < wsb:
+            self._wait_frames()          # the worker may still use the old workspace
+            self._ws = None
+            self._ws = torch.empty(wsb, dtype=torch.uint8, device=self.dev)
+        labels = torch.empty(nsym, dtype=torch.uint8, device=self.dev)
+        soft = torch.empty(nsym, dtype=torch.complex64, device=self.dev)
+        ready = torch.cuda.Event()
+        ready.record(torch.cuda.current_stream(self.dev))
+        job = {"k0": k0, "k1": k1, "ready": ready, "finished": threading.Event(), "labels": labels, "soft": soft}
+        self._jobs.append(job)
+        self._job_q.put(job)
+        self._sym_done = k1
+        self._y2.keep = self._drop + 2 * self._jobs[0]["k0"]   # pending frames' input stays
+
+    def _worker_loop(self):
+        torch = _torch()
+        torch.cuda.set_device(self.dev)
+        ws = self._worker_stream
+        while True:
+            job = self._job_q.get()
+            if job is None:
+                return
+            try:
+                with torch.cuda.stream(ws):
+                    ws.wait_event(job["ready"])
+                    e0 = torch.cuda.Event(enable_timing=True)
+                    e0.record(ws)
+                    job["out"] = self._solve_frame_impl(job["k0"], job["k1"], job["labels"], job["soft"])
+                    e1 = torch.cuda.Event(enable_timing=True)
+                    e1.record(ws)
+                    for t in (job["labels"], job["soft"], self._ws):
+                        t.record_stream(ws)
+                    job["events"] = (e0, e1)
+                    job["done"] = e1
+            except BaseException as exc:   # re-raised on the host thread by drain_device
+                job["error"] = exc
+            job["finished"].set()
+
+    def _collect_frames(self, block: bool, wait_stream=None):
+        """Move finished frames (all of them when block) to the outputs, in
+        order; `wait_stream` (default: the current stream) is made to wait for
+        their completion."""
+        torch = _torch()
+        ws = wait_stream if wait_stream is not None else torch.cuda.current_stream(self.dev)
+        while self._jobs:
+            job = self._jobs[0]
+            if not job["finished"].is_set():
+                if not block:
+                    break
+                job["finished"].wait()
+            self._jobs.popleft()
+            if "error" in job:
+                raise job["error"]
+            labels, soft, n_train, stats = job["out"]
+            ws.wait_event(job["done"])
+            self._events.append(("ddlms", *job["events"]))
+            self.ddlms_stats.append(stats)
+            self._out.append((labels, soft, job["k0"], n_train))
+        if self._y2 is not None:
+            self._y2.keep = self._drop + 2 * (self._jobs[0]["k0"] if self._jobs else self._sym_done)
+
+    def _wait_frames(self):
+        if self._jobs:
+            self._collect_frames(block=True)
+
+    def _stop_worker(self):
+        if self._worker is not None:
+            self._job_q.put(None)
+            self._worker.join()
+            self._worker = None
 
     def _run_ddlms(self, flush):
         if not self._synced:
@@ -942,13 +1072,14 @@ class RxPipeline:
             n_q = self._y2.end - self._drop
             k0 = self._sym_done
             k1 = self._frame_end(k0)
+            solve = self._submit_frame if self._async else self._solve_frame
             if n_q >= 2 * k1 + 2:
-                self._solve_frame(k0, k1)
+                solve(k0, k1)
                 continue
             if flush:
                 total = (n_q - self.cfg.ddlms.n_taps) // 2 + 1 if n_q >= self.cfg.ddlms.n_taps else 0
                 if total > k0:
-                    self._solve_frame(k0, total)
+                    solve(k0, total)
             break
 
     def _frame_end(self, k0: int) -> int:
@@ -1029,16 +1160,29 @@ class RxPipeline:
         finally:
             self._front_only = False
 
-    def drain_device(self):
+    def drain_device(self, wait_stream=None):
         """Device-resident outputs accumulated so far, then cleared:
         (labels uint8 [n] point indices (255 = training symbol), soft
-        complex64 [n], list of (first symbol index, n_train) per frame)."""
+        complex64 [n], list of (first symbol index, n_train) per frame).
+        With asynchronous DDLMS frames: the frames finished so far (all of
+        them once the stream is flushed), valid on `wait_stream` (default:
+        the current stream)."""
         torch = _torch()
-        if not self._out:
-            return (torch.zeros(0, dtype=torch.uint8, device=self.dev),
-                    torch.zeros(0, dtype=torch.complex64, device=self.dev), [])
-        labels = torch.cat([o[0] for o in self._out])
-        soft = torch.cat([o[1] for o in self._out])
+        cur = torch.cuda.current_stream(self.dev)
+        ws = wait_stream if wait_stream is not None else cur
+        if ws is not cur:
+            ws.wait_stream(cur)       # outputs of synchronous frames (current stream)
+        if self._async and self._jobs:
+            self._collect_frames(block=self._flushed, wait_stream=ws)
+        with torch.cuda.stream(ws):
+            if not self._out:
+                return (torch.zeros(0, dtype=torch.uint8, device=self.dev),
+                        torch.zeros(0, dtype=torch.complex64, device=self.dev), [])
+            if len(self._out) == 1:
+                labels, soft = self._out[0][0], self._out[0][1]
+            else:
+                labels = torch.cat([o[0] for o in self._out])
+                soft = torch.cat([o[1] for o in self._out])
         meta = [(o[2], o[3]) for o in self._out]
         self._out = []
         return labels, soft, meta
@@ -1062,6 +1206,8 @@ class RxPipeline:
     def release_buffers(self) -> None:
         """Free the device stream buffers of a finished pipeline (outputs
         already drained); timing events and statistics stay valid."""
+        self._wait_frames()
+        self._stop_worker()
         self._z = self._hs = self._hd = self._seg = self._y2 = None
         self._raw = None
         self._ws = None

@@ -10,7 +10,8 @@ sys.path.insert(0, REPO)
 
 import torch  # noqa: E402
 
-from paper_2108_07001_b200 import harness, rxdsp  # noqa: E402
+from paper_2108_07001_b200 import _lib, harness, rxdsp  # noqa: E402
+from paper_2108_07001_b200.constellation import slicer_tables  # noqa: E402
 from paper_2108_07001_b200.captures import load_capture, tile  # noqa: E402
 from paper_2108_07001_b200.sigcore import AdcCodes  # noqa: E402
 
@@ -22,6 +23,7 @@ codes, _ = tile(cap, 1 << log2n)
 cfg = cap.pipeline_config(ddlms_frame_symbols=frame)
 ref = cap.symbols()[:10000]
 dev = torch.device("cuda", 0)
+tb = slicer_tables(4)
 host = torch.from_numpy(codes).pin_memory()
 dst = torch.empty(host.shape[0], dtype=torch.int16, device=dev)
 for _ in range(2):
@@ -62,6 +64,7 @@ for rep in range(3):
             dst[a:a + m].copy_(host[a:a + m], non_blocking=True)
             ready[i].record(copy)
     n_out = 0
+    b_out = 0
     host_t = []
     d2h_ev = []
     for i, a in enumerate(starts):
@@ -72,14 +75,19 @@ for rep in range(3):
         host_t.append(time.perf_counter() - h0)
         lab, _, _ = pipe.drain_device()
         if lab.numel():
+            nb = (lab.numel() * 2 + 7) // 8
+            packed = torch.empty(nb, dtype=torch.uint8, device=dev)
+            _lib.call("kk_pack_bits", lab.data_ptr(), lab.numel(), n_out, None, 0, 2,
+                      tb.point_label.ctypes.data, 4, packed.data_ptr(), comp.cuda_stream)
             d2h.wait_stream(comp)
             with torch.cuda.stream(d2h):
-                lab_host[n_out:n_out + lab.numel()].copy_(lab, non_blocking=True)
+                lab_host[b_out:b_out + nb].copy_(packed, non_blocking=True)
                 ev = torch.cuda.Event(enable_timing=True)
                 ev.record(d2h)
                 d2h_ev.append((i, lab.numel(), ev))
-            lab.record_stream(d2h)
+            packed.record_stream(d2h)
             n_out += lab.numel()
+            b_out += nb
     comp.wait_stream(d2h)
     t_end = torch.cuda.Event(enable_timing=True)
     t_end.record(comp)

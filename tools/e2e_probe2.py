@@ -1,0 +1,69 @@
+"""Timeline of harness.receive_host_stream (async DDLMS) for one 2^N step."""
+import os
+import sys
+import time
+
+REPO = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, REPO)
+import torch  # noqa: E402
+
+from paper_2108_07001_b200.captures import load_capture, tile  # noqa: E402
+from paper_2108_07001_b200.harness import receive_host_stream  # noqa: E402
+
+log2n = int(sys.argv[1]) if len(sys.argv) > 1 else 30
+chunk = 1 << int(sys.argv[2]) if len(sys.argv) > 2 else 1 << 25
+frame = 1 << int(sys.argv[3]) if len(sys.argv) > 3 else 1 << 28
+cap = load_capture("c5_qpsk_10000km_tile")
+codes, _ = tile(cap, 1 << log2n)
+cfg = cap.pipeline_config(ddlms_frame_symbols=frame)
+ref = cap.symbols()[:10000]
+dev = torch.device("cuda", 0)
+host = torch.from_numpy(codes).pin_memory()
+staging = torch.empty(host.shape[0], dtype=torch.int16, device=dev)
+
+# host-side time per pipeline phase (monkeypatched timers)
+from paper_2108_07001_b200 import rxdsp  # noqa: E402
+HT = {}
+
+
+def _wrap(name):
+    f = getattr(rxdsp.RxPipeline, name)
+
+    def g(self, *a, **k):
+        t = time.perf_counter()
+        try:
+            return f(self, *a, **k)
+        finally:
+            HT.setdefault(name, []).append(time.perf_counter() - t)
+    setattr(rxdsp.RxPipeline, name, g)
+
+
+for _n in ("_run_kk", "_run_carrier", "_run_static", "_run_ddlms", "drain_device", "_submit_frame", "_wait_frames"):
+    _wrap(_n)
+for rep in range(3):
+    HT.clear()
+    tr = []
+    ms0 = torch.cuda.memory_stats()
+    t0 = torch.cuda.Event(enable_timing=True)
+    t0.record()
+    h0 = time.perf_counter()
+    pipe, bits, n = receive_host_stream(cfg, host, cap.half_lsb, ref, chunk_samples=chunk, staging=staging, trace=tr)
+    t1 = torch.cuda.Event(enable_timing=True)
+    t1.record()
+    torch.cuda.synchronize()
+    tot = t0.elapsed_time(t1)
+    ms1 = torch.cuda.memory_stats()
+    print(f"rep {rep}: {tot:.2f} ms {n / tot / 1e6:.3f} GBaud host {1e3 * (time.perf_counter() - h0):.2f} ms",
+          "device allocs", ms1.get("num_device_alloc", 0) - ms0.get("num_device_alloc", 0),
+          "frees", ms1.get("num_device_free", 0) - ms0.get("num_device_free", 0),
+          "retries", ms1.get("num_alloc_retries", 0) - ms0.get("num_alloc_retries", 0))
+    if rep == 2:
+        for i, ht, rd, fe, nj in tr:
+            print(f"  chunk {i:3d}: fed @ {t0.elapsed_time(fe):8.2f} "
+                  f"host @ {1e3 * (ht - h0):8.2f} pending {nj}")
+        print("  stats", [(s["k0"], s["nsym"], s.get("iterations")) for s in pipe.ddlms_stats])
+        print("  stages", pipe.stage_seconds)
+        for k_, v_ in HT.items():
+            print("  host", k_, "n", len(v_), "total ms %.2f" % (1e3 * sum(v_)), "max ms %.2f" % (1e3 * max(v_)),
+                  "top", ["%.2f" % (1e3 * x) for x in sorted(v_)[-4:]])
+    pipe.release_buffers()
