@@ -13,7 +13,11 @@ def launch_shares(path, out):
     ki, vi = h.index("Kernel Name"), h.index("Metric Value")
     names = [(r[ki], float(r[vi].replace(",", ""))) for r in data if len(r) > vi]
     starts = [i for i, (n, _) in enumerate(names) if "kk_pairs_kernel" in n]
-    seg = names[starts[-1]:] if len(starts) < 2 else names[starts[-2]:starts[-1]]
+    # one device-resident step: from the longest K1 launch (the whole 2^30
+    # sample super-frame) to the next K1 launch
+    s0 = max(starts, key=lambda i: names[i][1])
+    nxt = [i for i in starts if i > s0]
+    seg = names[s0:nxt[0]] if nxt else names[s0:]
     agg = defaultdict(lambda: [0, 0.0])
     for n, v in seg:
         agg[n.split("(")[0][:60]][0] += 1
