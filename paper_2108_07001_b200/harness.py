@@ -119,11 +119,60 @@ def receive_host_stream(cfg, host_codes, half_lsb: float, reference_symbols, chu
     return out
 
 
+def _stream_receiver(cfg, reference_symbols, n: int, chunk_samples: int, dev):
+    """Pipeline + output packing state of a streaming receive (shared by the
+    pinned-host and raw-file ingest paths)."""
+    import dataclasses
+
+    import torch
+
+    from .constellation import make_constellation, slicer_tables
+
+    # DDLMS frames run asynchronously (worker thread + stream) so the front
+    # end of later chunks overlaps them.
+    gpu = dataclasses.replace(cfg.gpu, ddlms_async=True)
+    cfg = dataclasses.replace(cfg, gpu=gpu)
+    pipe = RxPipeline(cfg, reference_symbols=reference_symbols, device=dev)
+    pipe.expect(n, chunk_samples)
+    order = cfg.constellation_order
+    st = {"cfg": cfg, "pipe": pipe, "order": order, "k": make_constellation(order).bits_per_symbol,
+          "tb": slicer_tables(order), "train_idx": None, "n_train": 0, "n_out": 0, "b_out": 0}
+    if reference_symbols is not None:
+        ref = np.asarray(reference_symbols, np.complex128)[:cfg.ddlms.startup_symbols]
+        pts = make_constellation(order).points
+        ti = np.argmin(np.abs(ref[:, None] - pts[None, :]), axis=1).astype(np.uint8)
+        st["train_idx"] = torch.from_numpy(ti).to(dev)
+        st["n_train"] = len(ti)
+    return st
+
+
+def _drain_bits(st, bits_host, d2h, dev):
+    """Finished frames -> packed bits -> pinned host, on the d2h stream (the
+    other DMA direction), off the compute stream."""
+    import torch
+
+    pipe, k = st["pipe"], st["k"]
+    lab, soft, _ = pipe.drain_device(wait_stream=d2h)
+    if not lab.numel():
+        return
+    nb = (lab.numel() * k + 7) // 8
+    ti = st["train_idx"]
+    with torch.cuda.stream(d2h):
+        packed = torch.empty(nb, dtype=torch.uint8, device=dev)
+        _lib.call("kk_pack_bits", lab.data_ptr(), lab.numel(), st["n_out"],
+                  ti.data_ptr() if ti is not None else None, st["n_train"], k,
+                  st["tb"].point_label.ctypes.data, st["order"], packed.data_ptr(), d2h.cuda_stream)
+        bits_host[st["b_out"]:st["b_out"] + nb].copy_(packed, non_blocking=True)
+    lab.record_stream(d2h)
+    soft.record_stream(d2h)
+    st["n_out"] += lab.numel()
+    st["b_out"] += nb
+
+
 def _receive_host_stream(cfg, host_codes, half_lsb, reference_symbols, chunk_samples, bits_host, dev, staging,
                          trace, comp):
     import torch
 
-    from .constellation import make_constellation, slicer_tables
     from .sigcore import AdcCodes
 
     n = int(host_codes.shape[0])
@@ -132,26 +181,9 @@ def _receive_host_stream(cfg, host_codes, half_lsb, reference_symbols, chunk_sam
     if staging is None or staging.numel() < n:
         staging = torch.empty(n, dtype=torch.int16, device=dev)
     # the pipeline's own uploads go first: later small H2D copies would queue
-    # behind the bulk transfers on the in-order host->device copy engine.
-    # DDLMS frames run asynchronously (worker thread + stream) so the front
-    # end of later chunks overlaps them.
-    import dataclasses
-
-    gpu = dataclasses.replace(cfg.gpu, ddlms_async=True)
-    cfg = dataclasses.replace(cfg, gpu=gpu)
-    pipe = RxPipeline(cfg, reference_symbols=reference_symbols, device=dev)
-    pipe.expect(n, chunk_samples)
-    order = cfg.constellation_order
-    k = make_constellation(order).bits_per_symbol
-    tb = slicer_tables(order)
-    train_idx = None
-    n_train = 0
-    if reference_symbols is not None:
-        ref = np.asarray(reference_symbols, np.complex128)[:cfg.ddlms.startup_symbols]
-        pts = make_constellation(order).points
-        ti = np.argmin(np.abs(ref[:, None] - pts[None, :]), axis=1).astype(np.uint8)
-        train_idx = torch.from_numpy(ti).to(dev)
-        n_train = len(ti)
+    # behind the bulk transfers on the in-order host->device copy engine
+    st = _stream_receiver(cfg, reference_symbols, n, chunk_samples, dev)
+    pipe, cfg = st["pipe"], st["cfg"]
     starts = list(range(0, n, chunk_samples))
     ready = [torch.cuda.Event() for _ in starts]
     copy.wait_stream(comp)          # the staging buffer's previous readers (and the uploads)
@@ -161,9 +193,7 @@ def _receive_host_stream(cfg, host_codes, half_lsb, reference_symbols, chunk_sam
             staging[a:a + m].copy_(host_codes[a:a + m], non_blocking=True)
             ready[i].record(copy)
     if bits_host is None:
-        bits_host = torch.empty((n // 4 + 8) * k // 8 + 8, dtype=torch.uint8, pin_memory=True)
-    n_out = 0
-    b_out = 0
+        bits_host = torch.empty((n // 4 + 8) * st["k"] // 8 + 8, dtype=torch.uint8, pin_memory=True)
     for i, a in enumerate(starts):
         m = min(chunk_samples, n - a)
         comp.wait_event(ready[i])
@@ -174,20 +204,88 @@ def _receive_host_stream(cfg, host_codes, half_lsb, reference_symbols, chunk_sam
             ev = torch.cuda.Event(enable_timing=True)
             ev.record(comp)
             trace.append((i, time.perf_counter(), ready[i], ev, len(pipe._jobs)))
-        # finished frames, valid on the d2h stream: pack + device -> host there
-        # (the other DMA direction), off the compute stream
-        lab, soft, _ = pipe.drain_device(wait_stream=d2h)
-        if lab.numel():
-            nb = (lab.numel() * k + 7) // 8
-            with torch.cuda.stream(d2h):
-                packed = torch.empty(nb, dtype=torch.uint8, device=dev)
-                _lib.call("kk_pack_bits", lab.data_ptr(), lab.numel(), n_out,
-                          train_idx.data_ptr() if train_idx is not None else None, n_train, k,
-                          tb.point_label.ctypes.data, order, packed.data_ptr(), d2h.cuda_stream)
-                bits_host[b_out:b_out + nb].copy_(packed, non_blocking=True)
-            lab.record_stream(d2h)
-            soft.record_stream(d2h)
-            n_out += lab.numel()
-            b_out += nb
+        _drain_bits(st, bits_host, d2h, dev)
     comp.wait_stream(d2h)
-    return pipe, bits_host, n_out
+    return pipe, bits_host, st["n_out"]
+
+
+def receive_raw_file(cfg, path: str, reference_symbols, chunk_samples: int = 1 << 25, device=None,
+                     n_buffers: int = 3):
+    """Real-time ingest of the reference's int16 wire format (raw little-
+    endian samples + JSON sidecar, sigcore.py:357-398): a reader thread
+    reads the file chunk by chunk straight into pinned host buffers (ring of
+    n_buffers), each is copied to the device on a side stream as soon as it
+    is full and the receiver consumes it; disk/page-cache reads, PCIe copies
+    and GPU work all overlap.  Returns (pipe, packed output bits (pinned
+    host tensor), n_symbols_decided)."""
+    import json
+    import queue
+    import threading
+
+    import torch
+
+    from .sigcore import AdcCodes, ParameterError
+
+    with open(path + ".json") as f:
+        meta = json.load(f)
+    if meta.get("kind") != "int16":
+        raise ParameterError("receive_raw_file: only int16 wire-format streams are supported")
+    half_lsb = 1.0 / float(meta["scale"])
+    n = int(meta["length"])
+    dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+    caller = torch.cuda.current_stream(dev)
+    comp = side_stream(dev, "front")
+    copy = side_stream(dev, "h2d")
+    d2h = side_stream(dev, "d2h")
+    comp.wait_stream(caller)
+    pins = [torch.empty(chunk_samples, dtype=torch.int16).pin_memory() for _ in range(n_buffers)]
+    free_q, full_q = queue.Queue(), queue.Queue()
+    for i in range(n_buffers):
+        free_q.put((i, None))
+    starts = list(range(0, n, chunk_samples))
+    err = []
+
+    def reader():
+        try:
+            with open(path, "rb") as f:
+                for a in starts:
+                    m = min(chunk_samples, n - a)
+                    i, ev = free_q.get()
+                    if ev is not None:
+                        ev.synchronize()          # its previous H2D copy has finished
+                    view = pins[i].numpy()[:m]
+                    got = f.readinto(memoryview(view).cast("B"))
+                    if got != 2 * m:
+                        raise ParameterError(f"{path}: short read ({got} of {2 * m} bytes)")
+                    full_q.put((i, m))
+        except BaseException as exc:   # surfaced on the caller thread
+            err.append(exc)
+            full_q.put(None)
+
+    th = threading.Thread(target=reader, daemon=True)
+    with torch.cuda.stream(comp):
+        st = _stream_receiver(cfg, reference_symbols, n, chunk_samples, dev)
+        pipe, cfg = st["pipe"], st["cfg"]
+        staging = torch.empty(n, dtype=torch.int16, device=dev)
+        bits_host = torch.empty((n // 4 + 8) * st["k"] // 8 + 8, dtype=torch.uint8, pin_memory=True)
+        copy.wait_stream(comp)
+        th.start()
+        for ci, a in enumerate(starts):
+            item = full_q.get()
+            if item is None:
+                raise err[0]
+            i, m = item
+            ready = torch.cuda.Event()
+            with torch.cuda.stream(copy):
+                staging[a:a + m].copy_(pins[i][:m], non_blocking=True)
+                ready.record(copy)
+            free_q.put((i, ready))
+            comp.wait_event(ready)
+            pipe.feed(AdcCodes(staging[a:a + m], half_lsb, cfg.adc_rate_hz), flush=ci == len(starts) - 1)
+            _drain_bits(st, bits_host, d2h, dev)
+        comp.wait_stream(d2h)
+    th.join()
+    if err:
+        raise err[0]
+    caller.wait_stream(comp)
+    return pipe, bits_host, st["n_out"]

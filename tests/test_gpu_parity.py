@@ -327,3 +327,28 @@ def test_host_stream_packed_bits_vs_reference():
     dec, _ = pipe2.finish()
     d_idx = to_idx(dec, 4)
     assert np.array_equal(got, np.unpackbits(pl[d_idx][:, None], axis=1)[:, -2:].reshape(-1))
+
+
+def test_raw_file_ingest_matches_host_stream(tmp_path):
+    """the int16 wire format (raw + JSON sidecar) streamed from
+    a file through pinned buffers gives the same packed bits as the pinned
+    host-stream path."""
+    import torch
+
+    from paper_2108_07001_b200.harness import receive_host_stream, receive_raw_file
+    from paper_2108_07001_b200.sigcore import write_adc_raw
+
+    cap = load_capture("c5_qpsk_10000km_tile")
+    reps = cap.meta["tile_reps"]
+    codes, _ = tile(cap, reps * len(cap.adc_h))
+    path = str(tmp_path / "capture.raw")
+    write_adc_raw(path, AdcCodes(codes, cap.half_lsb, 4e9))
+    cfg = cap.pipeline_config(ddlms_frame_symbols=1 << 18)
+    ref_syms = np.tile(cap.symbols(), reps)
+    _, bits_f, n_f = receive_raw_file(cfg, path, ref_syms, chunk_samples=1 << 20)
+    _, bits_h, n_h = receive_host_stream(cfg, torch.from_numpy(codes).pin_memory(), cap.half_lsb, ref_syms,
+                                         chunk_samples=1 << 20)
+    torch.cuda.synchronize()
+    nb = (2 * n_h + 7) // 8
+    assert n_f == n_h == len(cap.arrays["dec4_idx"])
+    assert torch.equal(bits_f[:nb], bits_h[:nb])
