@@ -13,13 +13,14 @@ import numpy as np
 
 from . import _lib
 from .constellation import make_constellation
-from .metrics import SyncFailure, count_bit_errors, evm, frame_sync, q_from_ber, windowed_q
+from .metrics import (SyncFailure, count_bit_errors, evm, frame_sync, q_from_ber, windowed_q,
+                      windowed_q_from_counts)
 from .rxdsp import side_stream
 from .rxdsp import (
     DdlmsConfig, GpuOptions, RxPipeline, RxPipelineConfig, compute_static_taps, demap, design_receive_taps,
 )
 
-from .sigcore import BlockPlan
+from .sigcore import BlockPlan, ParameterError
 
 
 def make_pipeline_config(cfg, link, gpu: GpuOptions | None = None) -> RxPipelineConfig:
@@ -70,6 +71,93 @@ def measure_point(dec, soft, bits, syms, cfg) -> dict:
     win = cfg.metrics.windowed_q_window_s
     point["windowed_q"] = ([[float(t), float(q)] for t, q in windowed_q(errors, bit_rate, win)]
                            if n_bits >= int(win * bit_rate) else [])
+    return point
+
+
+def frame_sync_device(rx_bits, tx_bits, min_peak_ratio: float = 3.0):
+    """GPU frame_sync (metrics.py:69-112 semantics): bipolar cross-correlation
+    of the received and transmitted bit streams (uint8 CUDA tensors) with the
+    FFT on the device (cuFFT, float64), peak-to-sidelobe test excluding +-2
+    lags, linear correlation -- or circular when the lengths are equal.
+    Returns (lag, aligned rx bits, aligned tx bits) as device views."""
+    import torch
+
+    n_rx, n_tx = int(rx_bits.shape[0]), int(tx_bits.shape[0])
+    if n_tx < (1 << 14):
+        raise ParameterError("reference must be at least 2^14 bits")
+    if n_rx < 64:
+        raise SyncFailure("received stream too short")
+    rx = rx_bits.to(torch.float64) * 2 - 1
+    tx = tx_bits.to(torch.float64) * 2 - 1
+    if n_rx == n_tx:
+        c = torch.fft.irfft(torch.fft.rfft(rx) * torch.conj(torch.fft.rfft(tx)), n=n_rx)
+        mag = c.abs()
+        k = int(torch.argmax(mag))
+        m2 = mag.clone()
+        m2[k] = -1.0
+        ratio = float(mag[k] / (m2.max() + 1e-30))
+        if ratio < min_peak_ratio:
+            raise SyncFailure(f"no circular correlation peak (ratio {ratio:.2f})")
+        return k, torch.roll(rx_bits, -k), tx_bits
+    L = n_rx + n_tx - 1
+    nfft = 1 << (L - 1).bit_length()
+    c = torch.fft.irfft(torch.fft.rfft(rx, n=nfft) * torch.fft.rfft(torch.flip(tx, [0]), n=nfft), n=nfft)[:L]
+    mag = c.abs()
+    k = int(torch.argmax(mag))
+    m2 = mag.clone()
+    m2[max(0, k - 2):min(L, k + 3)] = -1.0
+    ratio = float(mag[k] / (m2.max() + 1e-30))
+    if ratio < min_peak_ratio:
+        raise SyncFailure(f"no correlation peak (ratio {ratio:.2f})")
+    lag = (n_tx - 1) - k
+    if lag >= 0:
+        n = min(n_rx, n_tx - lag)
+        return lag, rx_bits[:n], tx_bits[lag:lag + n]
+    n = min(n_rx + lag, n_tx)
+    return lag, rx_bits[-lag:-lag + n], tx_bits[:n]
+
+
+def measure_point_device(labels, soft, bits, syms, cfg) -> dict:
+    """measure_point (hr:104-137) with the decisions left on the GPU: labels
+    (uint8 point indices) and soft (complex64) CUDA tensors, bits / syms the
+    transmitted bits and symbols (host).  Demap, frame sync, error count,
+    windowed Q and EVM all run on the device; only scalars come back."""
+    import torch
+
+    from .constellation import slicer_tables
+
+    spec = make_constellation(cfg.tx.constellation_order)
+    k = spec.bits_per_symbol
+    dev = labels.device
+    head = cfg.rx.startup_symbols + cfg.metrics.head_guard_symbols
+    stop = min(int(labels.shape[0]), len(syms)) - cfg.metrics.tail_guard_symbols
+    if stop - head < 1000:
+        raise SyncFailure("too few symbols beyond the startup region")
+    pl = torch.from_numpy(slicer_tables(spec.order).point_label.astype(np.int64)).to(dev)
+    lab = pl[labels[head:stop].long()]
+    shifts = torch.arange(k - 1, -1, -1, device=dev)
+    rx_bits = ((lab[:, None] >> shifts[None, :]) & 1).to(torch.uint8).reshape(-1)
+    tx_bits = torch.from_numpy(np.ascontiguousarray(bits, dtype=np.uint8)).to(dev)
+    offset, a_rx, a_tx = frame_sync_device(rx_bits, tx_bits)
+    errors = a_rx != a_tx
+    n_bits = int(errors.shape[0])
+    n_err = int(errors.sum())
+    ber = n_err / n_bits
+    s = soft[head:stop]
+    r = torch.from_numpy(np.ascontiguousarray(syms[head:stop], dtype=np.complex128)).to(dev)
+    evm_pct = float(100.0 * torch.sqrt(torch.mean((s.to(torch.complex128) - r).abs() ** 2) /
+                                       torch.mean(r.abs() ** 2)))
+    point = {"ber": ber, "q_db": q_from_ber(ber), "evm_pct": evm_pct, "n_bits": n_bits, "n_errors": n_err,
+             "sync_offset": int(offset)}
+    bit_rate = cfg.tx.baud_hz * k
+    win = cfg.metrics.windowed_q_window_s
+    bpw = int(round(win * bit_rate))
+    if n_bits >= int(win * bit_rate) and bpw >= 1:
+        nw = n_bits // bpw
+        counts = errors[:nw * bpw].view(nw, bpw).sum(1).cpu().numpy()
+        point["windowed_q"] = [[float(t), float(q)] for t, q in windowed_q_from_counts(counts, bpw, win)]
+    else:
+        point["windowed_q"] = []
     return point
 
 

@@ -352,3 +352,38 @@ def test_raw_file_ingest_matches_host_stream(tmp_path):
     nb = (2 * n_h + 7) // 8
     assert n_f == n_h == len(cap.arrays["dec4_idx"])
     assert torch.equal(bits_f[:nb], bits_h[:nb])
+
+
+def test_measure_point_device_vs_host_and_reference():
+    """measure_point on the GPU (demap, frame sync, error
+    count, windowed Q, EVM) equals the host measure_point on the same
+    decisions and the reference's own point on its capture."""
+    from types import SimpleNamespace
+
+    from paper_2108_07001_b200.harness import measure_point, measure_point_device
+
+    cap = load_capture("c4_qpsk_10000km_cspr10")
+    c = cap.meta["config"]
+    cfgx = SimpleNamespace(tx=SimpleNamespace(constellation_order=c["tx"]["constellation_order"],
+                                              baud_hz=c["tx"]["baud_hz"]),
+                           rx=SimpleNamespace(startup_symbols=c["rx"]["startup_symbols"]),
+                           metrics=SimpleNamespace(head_guard_symbols=c["metrics"]["head_guard_symbols"],
+                                                   tail_guard_symbols=c["metrics"]["tail_guard_symbols"],
+                                                   windowed_q_window_s=c["metrics"]["windowed_q_window_s"]))
+    pipe = rxdsp.RxPipeline(cap.pipeline_config(), reference_symbols=cap.symbols())
+    pipe.feed(cap.adc)
+    pipe.feed(np.zeros(0), flush=True)
+    lab, soft, _ = pipe.drain_device()
+    bits = np.unpackbits(cap.arrays["bits_packed"])[: cap.meta["n_bits"]]
+    syms = cap.symbols()
+    got = measure_point_device(lab, soft, bits, syms, cfgx)
+    labh = lab.cpu().numpy()
+    dec = make_constellation(4).points[np.minimum(labh, 3)]
+    want = measure_point(dec, soft.cpu().numpy().astype(np.complex128), bits, syms, cfgx)
+    for key in ("n_bits", "n_errors", "sync_offset"):
+        assert got[key] == want[key], key
+    assert abs(got["evm_pct"] - want["evm_pct"]) < 1e-6 * want["evm_pct"] + 1e-9
+    assert got["windowed_q"] == want["windowed_q"]
+    ref = cap.meta["point"]
+    assert got["n_errors"] == ref["n_errors"] and got["sync_offset"] == ref["sync_offset"]
+    assert abs(got["evm_pct"] - ref["evm_pct"]) < 1e-3 * ref["evm_pct"]
