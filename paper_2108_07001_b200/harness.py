@@ -74,6 +74,56 @@ def measure_point(dec, soft, bits, syms, cfg) -> dict:
     return point
 
 
+def receive_batch(items, device=None, max_concurrency: int = 4):
+    """Batched multi-stream receive (sweeps): independent
+    streams -- (cfg, adc, reference_symbols) each, adc a numpy / CUDA array or
+    AdcCodes -- run concurrently, one host thread and one CUDA stream per
+    stream, so small sweep points together fill the GPU.  Returns, in order,
+    (labels uint8, soft complex64) CUDA tensors per stream (valid on the
+    caller's current stream) and the pipelines."""
+    import threading
+
+    import torch
+
+    dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+    caller = torch.cuda.current_stream(dev)
+    out = [None] * len(items)
+    errs = []
+    sem = threading.Semaphore(max(1, int(max_concurrency)))
+
+    def run(i, cfg, adc, ref):
+        with sem:
+            try:
+                torch.cuda.set_device(dev)
+                s = side_stream(dev, f"batch{i % max_concurrency}")
+                s.wait_stream(caller)
+                with torch.cuda.stream(s):
+                    pipe = RxPipeline(cfg, reference_symbols=ref, device=dev)
+                    pipe.feed(adc)
+                    pipe.feed(np.zeros(0), flush=True)
+                    lab, soft, _ = pipe.drain_device()
+                    ev = torch.cuda.Event()
+                    ev.record(s)
+                out[i] = (lab, soft, pipe, ev, s)
+            except BaseException as exc:
+                errs.append((i, exc))
+
+    threads = [threading.Thread(target=run, args=(i, *it)) for i, it in enumerate(items)]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join()
+    if errs:
+        raise errs[0][1]
+    res = []
+    for lab, soft, pipe, ev, s in out:
+        caller.wait_event(ev)
+        lab.record_stream(caller)
+        soft.record_stream(caller)
+        res.append((lab, soft, pipe))
+    return res
+
+
 def frame_sync_device(rx_bits, tx_bits, min_peak_ratio: float = 3.0):
     """GPU frame_sync (metrics.py:69-112 semantics): bipolar cross-correlation
     of the received and transmitted bit streams (uint8 CUDA tensors) with the

@@ -267,6 +267,9 @@ def _as_device_input(x, dev):
 
 
 _SIDE_STREAMS = {}
+import threading as _threading
+
+_SIDE_LOCK = _threading.Lock()
 
 
 def side_stream(dev, name: str, priority: int = 0):
@@ -275,9 +278,10 @@ def side_stream(dev, name: str, priority: int = 0):
     would strand cached blocks).  priority < 0: scheduled ahead of others."""
     torch = _torch()
     key = (str(dev), name, priority)
-    if key not in _SIDE_STREAMS:
-        _SIDE_STREAMS[key] = torch.cuda.Stream(device=dev, priority=priority)
-    return _SIDE_STREAMS[key]
+    with _SIDE_LOCK:
+        if key not in _SIDE_STREAMS:
+            _SIDE_STREAMS[key] = torch.cuda.Stream(device=dev, priority=priority)
+        return _SIDE_STREAMS[key]
 
 
 class _DevStream:

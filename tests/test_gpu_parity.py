@@ -387,3 +387,26 @@ def test_measure_point_device_vs_host_and_reference():
     ref = cap.meta["point"]
     assert got["n_errors"] == ref["n_errors"] and got["sync_offset"] == ref["sync_offset"]
     assert abs(got["evm_pct"] - ref["evm_pct"]) < 1e-3 * ref["evm_pct"]
+
+
+def test_receive_batch_equals_single_streams():
+    """a batch of independent sweep points received
+    concurrently gives each stream's single-stream decisions exactly."""
+    from paper_2108_07001_b200.harness import receive_batch
+
+    names = ["c4_qpsk_10000km_cspr4", "c4_qpsk_10000km_cspr8", "c4_qpsk_10000km_cspr12",
+             "c2_16qam_5600km_rel-20"]
+    caps = [load_capture(n) for n in names]
+    res = receive_batch([(c.pipeline_config(), c.adc, c.symbols()) for c in caps])
+    for cap, (lab, soft, pipe) in zip(caps, res):
+        p1 = rxdsp.RxPipeline(cap.pipeline_config(), reference_symbols=cap.symbols())
+        p1.feed(cap.adc)
+        p1.feed(np.zeros(0), flush=True)
+        l1, s1, _ = p1.drain_device()
+        assert torch_equal(lab, l1) and torch_equal(soft, s1)
+        assert pipe.sync_offset == cap.meta["sync_offset"]
+
+
+def torch_equal(a, b):
+    import torch
+    return bool(torch.equal(a, b))
