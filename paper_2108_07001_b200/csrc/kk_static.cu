@@ -124,24 +124,46 @@ __device__ __forceinline__ float2 static_input(const K2Params& p, const BlockIn&
     return v;
 }
 
-// Step 1 input of the chain-c FFT16384, column j: v[r] = a(n) (c = 0) or
-// (x0 - x1)(n) W32^r (c = 1) at n = j + 1024 r; the remaining W32768^j of the
-// odd-bin pre-twiddle is common to the column and folded into the post-DFT
-// twiddle chain.  FAST: interior block of a stream whose carrier segments
-// are whole multiples of the hop, so the mean is constant over x0 and over
-// x1 and the carrier conj(mean * rot[n]) is a running product over r
-// (rot(n + 1024) = rot(n) rot(1024)); otherwise the generic per-sample path
-// (with the full W32768^n pre-twiddle applied here, step1_twiddle = false).
-template <int CHAIN, bool FAST>
-__device__ __forceinline__ void k2_load_column(const K2Params& p, const BlockIn& b, const float2* rot_s,
-                                               const Twiddle& tw, int j, float2 mA, float2 mB, int bnd,
-                                               unsigned s1024, unsigned s16384, float2 (&v)[16]) {
+// ---------------------------------------------------------------------------
+// TMEM as a per-thread scratch: chain 0's first pass also forms the odd
+// chain's column input b and parks it in tensor memory (256 KB/SM, unused by
+// this kernel otherwise); chain 1 reads it back instead of re-reading HBM/L2
+// and recomputing the carrier.  Warp w owns TMEM lanes 32 (w % 4) .. +32 and
+// columns 64 (w / 4) .. +64: 16 complex per column j, 2 columns per thread.
+// ---------------------------------------------------------------------------
+constexpr int kTmemCols = 256;
+
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const float2 (&v)[8]) {
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
+        "%15, %16};\n" ::"r"(taddr),
+        "f"(v[0].x), "f"(v[0].y), "f"(v[1].x), "f"(v[1].y), "f"(v[2].x), "f"(v[2].y), "f"(v[3].x), "f"(v[3].y),
+        "f"(v[4].x), "f"(v[4].y), "f"(v[5].x), "f"(v[5].y), "f"(v[6].x), "f"(v[6].y), "f"(v[7].x), "f"(v[7].y)
+        : "memory");
+}
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float2 (&v)[8]) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
+        "%15}, [%16];\n"
+        : "=f"(v[0].x), "=f"(v[0].y), "=f"(v[1].x), "=f"(v[1].y), "=f"(v[2].x), "=f"(v[2].y), "=f"(v[3].x),
+          "=f"(v[3].y), "=f"(v[4].x), "=f"(v[4].y), "=f"(v[5].x), "=f"(v[5].y), "=f"(v[6].x), "=f"(v[6].y),
+          "=f"(v[7].x), "=f"(v[7].y)
+        : "r"(taddr)
+        : "memory");
+}
+__device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory"); }
+__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory"); }
+
+// Chain 0 column j: v[r] = a(n), and the odd chain's b(n) W32^r parked in
+// TMEM at taddr (+16 columns for r >= 8).
+template <bool FAST>
+__device__ __forceinline__ void k2_load_column_ab(const K2Params& p, const BlockIn& b, const float2* rot_s, int j,
+                                                  float2 mA, float2 mB, int bnd, unsigned s1024, unsigned s16384,
+                                                  float2 (&v)[16], uint32_t taddr) {
+    float2 w[8];
     if constexpr (FAST) {
         const float2* z0 = p.z + (b.base - p.z_index0) + j;
-        // carrier over the column: x0 part c0 st^r, x1 part c1 st^r, so the
-        // chain input needs only their sum (c0 + c1) or difference (c0 - c1)
-        // as one running product
-        float2 cc = make_float2(0.f, 0.f), st = make_float2(1.f, 0.f);
+        float2 ca = make_float2(0.f, 0.f), cb = ca, st = make_float2(1.f, 0.f);
         if (p.carrier) {
             const float2 m1 = bnd <= kHopS ? mB : mA;
             float2 c0 = mA, c1 = m1;
@@ -154,9 +176,11 @@ __device__ __forceinline__ void k2_load_column(const K2Params& p, const BlockIn&
                 c1 = cmul(c1, rot_s[a1]);
                 st = rot_s[s1024];
             }
-            cc = CHAIN == 0 ? cadd(c0, c1) : csub(c0, c1);
+            ca = cadd(c0, c1);
+            cb = csub(c0, c1);
             if (p.mirror) {
-                cc = cconj(cc);
+                ca = cconj(ca);
+                cb = cconj(cb);
                 st = cconj(st);
             }
         }
@@ -164,21 +188,31 @@ __device__ __forceinline__ void k2_load_column(const K2Params& p, const BlockIn&
         for (int r = 0; r < 16; ++r) {
             const float2 x0 = __ldg(z0 + 1024 * r);
             const float2 x1 = __ldg(z0 + kHopS + 1024 * r);
-            float2 u = CHAIN == 0 ? cadd(x0, x1) : csub(x0, x1);
+            float2 ua = cadd(x0, x1), ub = csub(x0, x1);
             if (p.carrier) {
-                u = csub(u, cc);
-                cc = cmul(cc, st);
+                ua = csub(ua, ca);
+                ub = csub(ub, cb);
+                ca = cmul(ca, st);
+                cb = cmul(cb, st);
             }
-            if constexpr (CHAIN == 0) v[r] = u;
-            else v[r] = tw32<false>(u, r);
+            v[r] = ua;
+            w[r & 7] = tw32<false>(ub, r);
+            if ((r & 7) == 7) {
+                tmem_st16(taddr + (r >> 3) * 16, w);
+                tmem_wait_st();
+            }
         }
     } else {
 #pragma unroll
         for (int r = 0; r < 16; ++r) {
             const int n = j + 1024 * r;
             const float2 x0 = static_input(p, b, rot_s, n), x1 = static_input(p, b, rot_s, kHopS + n);
-            if constexpr (CHAIN == 0) v[r] = cadd(x0, x1);
-            else v[r] = tw32<false>(csub(x0, x1), r);
+            v[r] = cadd(x0, x1);
+            w[r & 7] = tw32<false>(csub(x0, x1), r);
+            if ((r & 7) == 7) {
+                tmem_st16(taddr + (r >> 3) * 16, w);
+                tmem_wait_st();
+            }
         }
     }
 }
@@ -227,6 +261,19 @@ __global__ void __launch_bounds__(kK2Threads, 1) static_blocks_kernel(K2Params p
 
     const int warp = tid >> 5, lane = tid & 31;
     float2* E = S.buf;
+    // TMEM scratch (one CTA per SM: the allocation always succeeds)
+    __shared__ uint32_t tmem_base_sh;
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(
+                         static_cast<uint32_t>(__cvta_generic_to_shared(&tmem_base_sh))),
+                     "n"(kTmemCols));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;\n");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;\n");
+    const uint32_t tmem_thread = tmem_base_sh + (static_cast<uint32_t>(32 * (warp & 3)) << 16) +
+                                 static_cast<uint32_t>(64 * (warp >> 2));
     for (int chain = 0; chain < 2; ++chain) {
         // ---- FFT16384 step 1: column n2 = j, DFT16 over n1 (stride 1024),
         //      W16384^{j k1}, -> row k1, position j ----
@@ -234,8 +281,20 @@ __global__ void __launch_bounds__(kK2Threads, 1) static_blocks_kernel(K2Params p
         for (int q = 0; q < 1024 / kK2Threads; ++q) {
             float2 v[16];
             const int j = tid + q * kK2Threads;
-            if (chain == 0) k2_load_column<0, FAST>(p, bi, S.rot, tw, j, mA, mB, bnd, s1024, s16384, v);
-            else k2_load_column<1, FAST>(p, bi, S.rot, tw, j, mA, mB, bnd, s1024, s16384, v);
+            const uint32_t taddr = tmem_thread + 32 * q;
+            if (chain == 0) {
+                k2_load_column_ab<FAST>(p, bi, S.rot, j, mA, mB, bnd, s1024, s16384, v, taddr);
+            } else {
+                float2 h0[8], h1[8];
+                tmem_ld16(taddr, h0);
+                tmem_ld16(taddr + 16, h1);
+                tmem_wait_ld();
+#pragma unroll
+                for (int r = 0; r < 8; ++r) {
+                    v[r] = h0[r];
+                    v[8 + r] = h1[r];
+                }
+            }
             dft_reg<16, false>(v);
             // W16384^{j k1}; chain 1 also W32768^j: W32768^{j (2 k1 + 1)}
             const float2 s2 = tw.template w<kHopS>(j);
@@ -292,6 +351,10 @@ __global__ void __launch_bounds__(kK2Threads, 1) static_blocks_kernel(K2Params p
             for (int i = tid; i < kNOut; i += kK2Threads) out[i] = S.A[padi(i)];
         }
     }
+    asm volatile("tcgen05.fence::before_thread_sync;\n");
+    __syncthreads();
+    if (warp == 0)
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem_base_sh), "n"(kTmemCols));
 }
 
 }  // namespace kk
