@@ -119,7 +119,7 @@ class GpuOptions:
     last grid frame is split in halves down to this size so that little
     DDLMS work (and output transfer) is left once the last input arrives."""
 
-    ddlms_block: int = 1024
+    ddlms_block: int = 512
     ddlms_frame_symbols: int = 1 << 28
     ddlms_max_iter: int = 64
     ddlms_soft_tol: float = 1e-5
