@@ -207,7 +207,8 @@ struct RunOut {
     uint8_t* labels;
     float2* soft;
     float* Q;         // [nb][16]
-    float* Tused;     // [nb][16]
+    float* Tused;     // [nb][16] start taps of the block's latest run
+    float* Twritten;  // [nb][16] start taps of its latest output-writing run (NaN: never)
     float* margin;    // [nb]
     float* Tend;      // [16] end taps of the last block
     int* over;        // [nb] guard exceedances in the block's latest run
@@ -456,7 +457,16 @@ ddlms_block_kernel(SolveArgs a, Slicer sl, const float* __restrict__ Tstart, flo
                 d2 = fmaf(d, d, d2);
             }
             const float bound = sqrtf(d2 * maxx2[b]);
-            run = !(bound < fminf(o.margin[b], soft_tol)) || (a.mu * maxx2[b] > 1.0f);
+            run = !(bound < fminf(o.margin[b], write_out ? 3.0e38f : soft_tol)) || (a.mu * maxx2[b] > 1.0f);
+            if (write_out) {   // outputs valid within soft_tol since their last write?
+                float w2 = 0.f;
+#pragma unroll
+                for (int i = 0; i < 16; ++i) {
+                    const float d = T[i] - o.Twritten[b * 16 + i];
+                    w2 = fmaf(d, d, w2);
+                }
+                run = run || !(sqrtf(w2 * maxx2[b]) < soft_tol);   // NaN (never written) -> run
+            }
         }
     } else {
 #pragma unroll
@@ -675,6 +685,10 @@ ddlms_block_kernel(SolveArgs a, Slicer sl, const float* __restrict__ Tstart, flo
             }
 #pragma unroll
         for (int i = 0; i < 16; ++i) o.Tused[b * 16 + i] = Tstart[b * 16 + i];
+        if (!WITH_P && write_out) {
+#pragma unroll
+            for (int i = 0; i < 16; ++i) o.Twritten[b * 16 + i] = Tstart[b * 16 + i];
+        }
         const bool sq = SQ > 0 || sl.kind == 0;
         const float mg = sq ? mgl * (2.0f / sl.norm) : mgb;
         o.margin[b] = fminf(mg, fabsf(sl.thr - sqrtf(my2)));
@@ -704,10 +718,12 @@ ddlms_block_kernel(SolveArgs a, Slicer sl, const float* __restrict__ Tstart, flo
 // Which blocks must re-run: |T_new - T_used|_F * max|x| >= min(margin, tol)
 // (decision / guard margin certificate, soft tolerance), compacted into a
 // list (warp-aggregated append; block order inside a warp preserved).
+// Output passes (Twritten != null): also re-run every block whose start moved
+// by more than tol since its outputs were last written (or never were).
 __global__ void ddlms_select_kernel(const float* __restrict__ Tstart, const float* __restrict__ Tused,
                                     const float* __restrict__ margin, const float* __restrict__ maxx2, float mu,
-                                    int64_t b_lo, int64_t nb, float tol, int* __restrict__ list,
-                                    unsigned long long* __restrict__ list_n) {
+                                    int64_t b_lo, int64_t nb, float tol, const float* __restrict__ Twritten,
+                                    int* __restrict__ list, unsigned long long* __restrict__ list_n) {
     const int64_t b = b_lo + int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     bool run = false;
     if (b < nb) {
@@ -718,7 +734,16 @@ __global__ void ddlms_select_kernel(const float* __restrict__ Tstart, const floa
             d2 = fmaf(d, d, d2);
         }
         const float bound = sqrtf(d2 * maxx2[b]);
-        run = !(bound < fminf(margin[b], tol)) || (mu * maxx2[b] > 1.0f);
+        run = !(bound < fminf(margin[b], Twritten ? 3.0e38f : tol)) || (mu * maxx2[b] > 1.0f);
+        if (Twritten) {
+            float w2 = 0.f;
+#pragma unroll
+            for (int i = 0; i < 16; ++i) {
+                const float d = Tstart[b * 16 + i] - Twritten[b * 16 + i];
+                w2 = fmaf(d, d, w2);
+            }
+            run = run || !(sqrtf(w2 * maxx2[b]) < tol);
+        }
     }
     const unsigned m = __ballot_sync(0xffffffffu, run);
     if (!m) return;
@@ -1119,6 +1144,7 @@ Layout plan(int64_t nsym, int B) {
     size_t b = 0;
     for (size_t l = 0; l < L.n.size(); ++l) b += align_up(L.n[l] * 96 * sizeof(float));  // P64 + Q16 + T16
     b += align_up(L.nb * 16 * sizeof(float));   // Tused
+    b += align_up(L.nb * 16 * sizeof(float));   // Twritten
     b += align_up(L.nb * sizeof(float)) * 2;    // margin, maxx2
     b += align_up(16 * sizeof(float)) * 2;      // Tend, Tinit
     b += align_up(L.nb * sizeof(int));          // over
@@ -1162,7 +1188,7 @@ struct DdlmsSolver {
     RunOut o;
     TOut to;
     float scale, soft_tol;
-    float *Tused, *margin, *maxx2, *Tend, *Tinit_d;
+    float *Tused, *Twritten, *margin, *maxx2, *Tend, *Tinit_d;
     int* over;
     unsigned long long *hsh, *ctr;
     float2* ST_own = nullptr;    // workspace soft / labels (outputs not bound)
@@ -1306,7 +1332,8 @@ struct DdlmsSolver {
         if (use_skip && !with_p) {
             // compact the blocks to re-run so that warps only carry live chains
             const unsigned g = static_cast<unsigned>((b1 - d0 + 127) / 128);
-            ddlms_select_kernel<<<g, 128, 0, s>>>(lv[0].T, Tused, margin, maxx2, a.mu, d0, b1, tol, list, ctr + 3);
+            ddlms_select_kernel<<<g, 128, 0, s>>>(lv[0].T, Tused, margin, maxx2, a.mu, d0, b1, tol,
+                                                  write_out ? Twritten : nullptr, list, ctr + 3);
             if (int rc = check_launch("ddlms_select_kernel")) return rc;
             return launch(false, d0, b1, 0, list, ctr + 3);
         }
@@ -1335,6 +1362,7 @@ struct DdlmsSolver {
         }
         top = static_cast<int>(lv.size()) - 1;
         Tused = reinterpret_cast<float*>(w); w += align_up(L.nb * 16 * sizeof(float));
+        Twritten = reinterpret_cast<float*>(w); w += align_up(L.nb * 16 * sizeof(float));
         margin = reinterpret_cast<float*>(w); w += align_up(L.nb * sizeof(float));
         maxx2 = reinterpret_cast<float*>(w); w += align_up(L.nb * sizeof(float));
         Tend = reinterpret_cast<float*>(w); w += align_up(16 * sizeof(float));
@@ -1361,6 +1389,7 @@ struct DdlmsSolver {
         o.soft = nullptr;
         o.Q = lv[0].Q;
         o.Tused = Tused;
+        o.Twritten = Twritten;
         o.margin = margin;
         o.Tend = Tend;
         o.over = over;
@@ -1370,6 +1399,7 @@ struct DdlmsSolver {
         ntb = std::min<int64_t>((n_train + block - 1) / block, L.nb);
         if (cudaMemsetAsync(over, 0, L.nb * sizeof(int), s) != cudaSuccess ||
             cudaMemsetAsync(hsh, 0, L.nb * 8, s) != cudaSuccess ||
+            cudaMemsetAsync(Twritten, 0xFF, L.nb * 16 * sizeof(float), s) != cudaSuccess ||   // NaN: never written
             cudaMemsetAsync(ctr, 0, 4 * sizeof(unsigned long long), s) != cudaSuccess)
             return set_cuda_error("solver init");
         return KK_OK;
@@ -1433,9 +1463,11 @@ struct DdlmsSolver {
             cudaMemsetAsync(ctr + 3, 0, sizeof(unsigned long long), s) != cudaSuccess)
             return set_cuda_error("ctr");
         // decision pass: compacted re-run of the blocks whose certified margin
-        // the start move could cross, no outputs; final pass: every block,
-        // outputs written (soft exact for the final start taps)
-        if (int rc = soft_pass ? run_blocks(false, 0, L.nb, 0, 0.f, 1)
+        // the start move could cross, no outputs; output pass: the blocks
+        // whose outputs are missing or were written from a start more than
+        // soft_tol away (the first output pass of a frame runs every block; a
+        // later one, after a late decision change, only its wake)
+        if (int rc = soft_pass ? run_blocks(false, 0, L.nb, 1, soft_tol, 1)
                                : run_blocks(false, 0, L.nb, 1, 3.0e38f, 0))
             return rc;
         unsigned long long h[4];

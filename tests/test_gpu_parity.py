@@ -410,3 +410,35 @@ def test_receive_batch_equals_single_streams():
 def torch_equal(a, b):
     import torch
     return bool(torch.equal(a, b))
+
+
+def test_capture_generator_statistics_vs_reference():
+    """the GPU capture generator (capgen) on the reference's
+    10,000 km QPSK config: the bit/symbol sequence is the reference's exactly,
+    and the received capture matches the reference capture statistically
+    (sync found, EVM within 10 %, BER within 3x of the reference point)."""
+    from paper_2108_07001_b200 import capgen
+    from paper_2108_07001_b200.harness import measure_point_device
+    from types import SimpleNamespace
+
+    cap = load_capture("c4_qpsk_10000km_cspr10")
+    c = cap.meta["config"]
+    n = 1 << 18
+    g = capgen.CaptureGenerator(capgen.GenParams.from_config(c), seed=1)
+    codes, half, idx, bits = g.generate(n, chunk_symbols=1 << 16)
+    ref_bits = np.unpackbits(cap.arrays["bits_packed"])[: cap.meta["n_bits"]]
+    assert np.array_equal(bits[: len(ref_bits)], ref_bits)
+    assert np.array_equal(idx[: len(cap.sym_idx)], cap.sym_idx)
+    pts = make_constellation(4).points
+    pipe = rxdsp.RxPipeline(cap.pipeline_config(), reference_symbols=pts[idx])
+    pipe.feed(AdcCodes(codes, half, 4e9))
+    pipe.feed(np.zeros(0), flush=True)
+    lab, soft, _ = pipe.drain_device()
+    cfgx = SimpleNamespace(tx=SimpleNamespace(constellation_order=4, baud_hz=1e9),
+                           rx=SimpleNamespace(startup_symbols=c["rx"]["startup_symbols"]),
+                           metrics=SimpleNamespace(head_guard_symbols=2048, tail_guard_symbols=4096,
+                                                   windowed_q_window_s=0.021))
+    pt = measure_point_device(lab, soft, bits, pts[idx], cfgx)
+    ref = cap.meta["point"]
+    assert abs(pt["evm_pct"] - ref["evm_pct"]) < 0.1 * ref["evm_pct"], (pt["evm_pct"], ref["evm_pct"])
+    assert pt["ber"] < 3 * max(ref["ber"], 1e-4), pt
