@@ -442,3 +442,30 @@ def test_capture_generator_statistics_vs_reference():
     ref = cap.meta["point"]
     assert abs(pt["evm_pct"] - ref["evm_pct"]) < 0.1 * ref["evm_pct"], (pt["evm_pct"], ref["evm_pct"])
     assert pt["ber"] < 3 * max(ref["ber"], 1e-4), pt
+
+
+@pytest.mark.parametrize("name", ["c2_16qam_5600km_rel-20", "c3_64qam_1600km_rel-20"])
+def test_host_stream_bits_multilevel(name):
+    """The e2e path's packed-bit output for 16-QAM (4 bits/symbol) and 64-QAM
+    (6 bits/symbol, bits straddling bytes): identical to demapping the
+    device-path decisions, training symbols from the reference."""
+    import torch
+
+    from paper_2108_07001_b200.constellation import slicer_tables
+    from paper_2108_07001_b200.harness import receive_host_stream
+
+    cap = load_capture(name)
+    k = {16: 4, 64: 6}[cap.order]
+    cfg = cap.pipeline_config(ddlms_frame_symbols=1 << 14)
+    host = torch.from_numpy(cap.adc_h).pin_memory()
+    _, bits_host, n = receive_host_stream(cfg, host, cap.half_lsb, cap.symbols(), chunk_samples=1 << 16)
+    torch.cuda.synchronize()
+    p2 = rxdsp.RxPipeline(cap.pipeline_config(), reference_symbols=cap.symbols())
+    p2.feed(cap.adc)
+    dec, _ = p2.finish()
+    assert n == len(dec)
+    d_idx = to_idx(dec, cap.order)
+    pl = slicer_tables(cap.order).point_label[: cap.order]
+    want = np.unpackbits(pl[d_idx][:, None], axis=1)[:, -k:].reshape(-1)
+    got = np.unpackbits(bits_host[: (k * n + 7) // 8].numpy())[: k * n]
+    assert np.array_equal(got, want)
