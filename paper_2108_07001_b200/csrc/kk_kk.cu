@@ -192,6 +192,11 @@ kk_pairs_kernel(const TIn* __restrict__ in, float in_scale, float clamp_rel, int
     const float two_pi_over_q = rot_q > 0 ? 6.283185307179586f / static_cast<float>(rot_q) : 0.f;
     if (rot_q > 0 && active)
         rot_base = static_cast<unsigned>((static_cast<unsigned long long>(n0_global + hop_a * kHop) % rot_q));
+    float2 rot_cache = make_float2(1.f, 0.f), r256 = rot_cache, r512 = rot_cache;
+    if (rot_q > 0) {
+        r256 = __ldg(rot_tab + (256ll * rot_p) % rot_q);     // exp(-2 pi i (256 p mod q) / q)
+        r512 = __ldg(rot_tab + (512ll * rot_p) % rot_q);
+    }
     auto st_out = [&](int n, float2 v) {
         if (n < kHop) return;
         const int i = n - kHop;
@@ -216,17 +221,21 @@ kk_pairs_kernel(const TIn* __restrict__ in, float in_scale, float clamp_rel, int
         const int64_t pb = pa + kHop;
         float2 za = fa, zb = fb;
         if (rot_q > 0) {
-            // field * exp(-2 pi i a/q) = amp exp(i (phi - 2 pi a/q)): one more sincos
-            const unsigned Q = static_cast<unsigned>(rot_q), P = static_cast<unsigned>(rot_p);
-            const int ia = static_cast<int>(fmod_u((rot_base + i) * P, Q, inv_q));
-            const int ib = static_cast<int>(fmod_u((rot_base + kHop + i) * P, Q, inv_q));
-            const float th_a = reduce_2pi(pa_ - two_pi_over_q * static_cast<float>(ia));
-            const float th_b = reduce_2pi(pb_ - two_pi_over_q * static_cast<float>(ib));
-            float sra, cra, srb, crb;
-            __sincosf(th_a, &sra, &cra);
-            __sincosf(th_b, &srb, &crb);
-            za = da ? make_float2(0.f, 0.f) : make_float2(amp_a * cra, amp_a * sra);
-            zb = db ? make_float2(0.f, 0.f) : make_float2(amp_b * crb, amp_b * srb);
+            // field * exp(-2 pi i a/q).  A butterfly's outputs i = j and
+            // j + 256 of hops a and b are 256 / 512 samples apart: one sincos
+            // for the first, exact constant rotations (table entries) for the
+            // others
+            if (i < kHop / 2) {
+                const unsigned Q = static_cast<unsigned>(rot_q), P = static_cast<unsigned>(rot_p);
+                const int ia = static_cast<int>(fmod_u((rot_base + i) * P, Q, inv_q));
+                float sr, cr;
+                __sincosf(reduce_2pi(-two_pi_over_q * static_cast<float>(ia)), &sr, &cr);
+                rot_cache = make_float2(cr, sr);
+            } else {
+                rot_cache = cmul(rot_cache, r256);
+            }
+            za = cmul(fa, rot_cache);
+            zb = cmul(fb, cmul(rot_cache, r512));
         }
         if (mirror) { za = cconj(za); zb = cconj(zb); }
         out[pa] = za;
