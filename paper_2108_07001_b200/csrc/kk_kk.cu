@@ -18,6 +18,8 @@
 // hops of u/amp it needs once in shared memory.  FFT = Stockham radix
 // 16x16x4 in padded float2 smem; the inverse FFT's last pass writes the field
 // straight to HBM (coalesced) with the rotation/mirror and the hop sums fused.
+#include <type_traits>
+
 #include "kk_common.cuh"
 #include "kk_internal.h"
 
@@ -40,6 +42,7 @@ struct K1Smem {
     float2 buf[kPairsPerCta][kPlane1];
     float2 tw[kK1TwEntries];
     float2 red[kK1Threads / 32][2];
+    double h0part[kK1Threads / 32];
     int dead[kStageHops];
     uint8_t dead_hist[kHop / 2];   // per-sample dead flags of hop -1 (state)
     unsigned int clamped;
@@ -79,7 +82,7 @@ __device__ __forceinline__ float2 apply_mult(int k, float2 z) {
 }
 
 template <typename TIn>
-__global__ void __launch_bounds__(kK1Threads)
+__global__ void __launch_bounds__(kK1Threads, 4)
 kk_pairs_kernel(const TIn* __restrict__ in, float in_scale, float clamp_rel, int64_t n_hops,
                 const float* __restrict__ st_u, const float* __restrict__ st_a,
                 const uint8_t* __restrict__ st_dead,
@@ -99,59 +102,102 @@ kk_pairs_kernel(const TIn* __restrict__ in, float in_scale, float clamp_rel, int
     if (tid == 0) S.clamped = 0;
     __syncthreads();
 
-    // ---- stage 9 hops: means, dead flags, clamp, u = 0.5 ln(safe), amp ----
-    for (int L = warp; L < kStageHops; L += kK1Threads / 32) {
+    // ---- stage 9 hops: means, dead flags, clamp, u = 0.5 ln(safe) ----
+    // Warp w stages hop w + 1 whole; hop 0 (the previous CTA's last hop,
+    // needed for the first block's history half) is shared by all 8 warps,
+    // 64 samples each, so no warp stages two hops.  Sums of int16 codes are
+    // exact integers.
+    using Acc = typename std::conditional<std::is_same<TIn, int16_t>::value, int, double>::type;
+    auto hop_params = [&](int64_t h, double sum, int& dead, float& thr) {
+        // mean = sum * scale / 512 (exact for int16 codes: integer sum)
+        const double mean = sum * static_cast<double>(in_scale) / kHop;
+        dead = !(mean > 0.0) ? 1 : 0;
+        thr = dead ? 1.0f : static_cast<float>(static_cast<double>(clamp_rel) * fabs(mean));
+    };
+    auto stage_val = [&](float xin, int dead, float thr, unsigned& ncl) {
+        const float x = xin * in_scale;
+        float sv;
+        if (dead) {
+            sv = 1.0f;
+        } else {
+            ncl += (x < thr) ? 1u : 0u;
+            sv = fmaxf(x, thr);
+        }
+        return 0.5f * __logf(sv);
+    };
+    const int64_t h0 = hop0;                       // stage hop 0
+    const bool h0_real = h0 >= 0 && h0 < n_hops;
+    float x0v[2];
+    {
+        // (a) own hop L = warp + 1, (b) this warp's 64 samples of hop 0
+        const int L = warp + 1;
         const int64_t h = hop0 + L;
         float* u = S.u + L * kHop;
-        if (h < 0) {  // previous-chunk state (rxdsp.py:208-213 initial zeros)
-            for (int i = lane; i < kHop; i += 32) u[i] = st_u[i];
-            for (int i = lane; i < kHop / 2; i += 32) {
-                S.ahist[i] = st_a[i];
-                S.dead_hist[i] = st_dead[i];
-            }
-            if (lane == 0) S.dead[L] = 0;
-            continue;
-        }
         if (h >= n_hops) {  // dummy partner beyond the last real hop
             for (int i = lane; i < kHop; i += 32) u[i] = 0.f;
             if (lane == 0) S.dead[L] = 1;
-            continue;
-        }
-        const TIn* src = in + h * kHop;
-        float xv[kHop / 32];
-        double sum = 0.0;
+        } else {
+            const TIn* src = in + h * kHop;
+            float xv[kHop / 32];
+            Acc sum = 0;
 #pragma unroll
-        for (int i = 0; i < kHop / 32; ++i) {
-            xv[i] = load_in<TIn>(src, lane + 32 * i, 1.0f);
-            sum += static_cast<double>(xv[i]);
-        }
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
-        // mean = sum * scale / 512 (exact for int16 codes: integer sum)
-        const double mean = sum * static_cast<double>(in_scale) / kHop;
-        const bool dead = !(mean > 0.0);
-        const float thr = dead ? 1.0f : static_cast<float>(static_cast<double>(clamp_rel) * fabs(mean));
-        unsigned int ncl = 0;
-#pragma unroll
-        for (int i = 0; i < kHop / 32; ++i) {
-            const float x = xv[i] * in_scale;
-            float s;
-            if (dead) {
-                s = 1.0f;
-            } else {
-                ncl += (x < thr) ? 1u : 0u;
-                s = fmaxf(x, thr);
+            for (int i = 0; i < kHop / 32; ++i) {
+                xv[i] = load_in<TIn>(src, lane + 32 * i, 1.0f);
+                sum += static_cast<Acc>(src[lane + 32 * i]);
             }
-            u[lane + 32 * i] = 0.5f * __logf(s);
-        }
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) ncl += __shfl_xor_sync(0xffffffffu, ncl, o);
-        if (lane == 0) {
-            S.dead[L] = dead ? 1 : 0;
-            if (L >= 1) {   // stage hop 0 belongs to the previous CTA
+            for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+            int dead;
+            float thr;
+            hop_params(h, static_cast<double>(sum), dead, thr);
+            unsigned int ncl = 0;
+#pragma unroll
+            for (int i = 0; i < kHop / 32; ++i) u[lane + 32 * i] = stage_val(xv[i], dead, thr, ncl);
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) ncl += __shfl_xor_sync(0xffffffffu, ncl, o);
+            if (lane == 0) {
+                S.dead[L] = dead;
                 if (ncl) atomicAdd(&S.clamped, ncl);
-                hop_dead[h] = dead ? 1 : 0;
+                hop_dead[h] = static_cast<uint8_t>(dead);
             }
+        }
+        Acc p0 = 0;
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+            const int i = warp * 64 + lane + 32 * e;
+            x0v[e] = 0.f;
+            if (h0_real) {
+                x0v[e] = load_in<TIn>(in + h0 * kHop, i, 1.0f);
+                p0 += static_cast<Acc>(in[h0 * kHop + i]);
+            }
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) p0 += __shfl_xor_sync(0xffffffffu, p0, o);
+        if (lane == 0) S.h0part[warp] = static_cast<double>(p0);
+    }
+    __syncthreads();
+    {
+        float* u = S.u;
+        if (h0 < 0) {   // previous-chunk state (rxdsp.py:208-213 initial zeros)
+            for (int i = tid; i < kHop; i += kK1Threads) u[i] = st_u[i];
+            for (int i = tid; i < kHop / 2; i += kK1Threads) {
+                S.ahist[i] = st_a[i];
+                S.dead_hist[i] = st_dead[i];
+            }
+            if (tid == 0) S.dead[0] = 0;
+        } else if (!h0_real) {
+            for (int i = tid; i < kHop; i += kK1Threads) u[i] = 0.f;
+            if (tid == 0) S.dead[0] = 1;
+        } else {
+            double sum = 0.0;
+            for (int w = 0; w < kK1Threads / 32; ++w) sum += S.h0part[w];   // fixed order
+            int dead;
+            float thr;
+            hop_params(h0, sum, dead, thr);
+            unsigned int ncl = 0;   // stage hop 0 is counted by the previous CTA
+#pragma unroll
+            for (int e = 0; e < 2; ++e) u[warp * 64 + lane + 32 * e] = stage_val(x0v[e], dead, thr, ncl);
+            if (tid == 0) S.dead[0] = dead;
         }
     }
     __syncthreads();
