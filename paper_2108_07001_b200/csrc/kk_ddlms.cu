@@ -759,6 +759,46 @@ __global__ void ddlms_select_kernel(const float* __restrict__ Tstart, const floa
 // shared memory with all loads in flight, then folded serially from smem.
 constexpr int kScanWarps = 2;
 
+// Stage a group's nc children (P_c: 64 floats, Q_c: 16 floats each, both
+// contiguous in global memory) into the warp's padded smem tiles with all
+// loads issued up front (float4, coalesced): the per-child load loop this
+// replaces serialised ~32 global latencies per group.
+__device__ __forceinline__ void stage_children(const float* __restrict__ Pc, const float* __restrict__ Qc,
+                                               int64_t c0, int nc, int l, float (*cP)[65], float (*cQ)[17]) {
+    if (nc <= 0) return;
+    const float4* p4 = reinterpret_cast<const float4*>(Pc + c0 * 64);
+    const float4* q4 = reinterpret_cast<const float4*>(Qc + c0 * 16);
+    float4 pv[16], qv[4];
+    const int np4 = nc * 16, nq4 = nc * 4;
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
+        const int e = l + 32 * k;
+        pv[k] = e < np4 ? __ldg(p4 + e) : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        const int e = l + 32 * k;
+        qv[k] = e < nq4 ? __ldg(q4 + e) : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
+        const int e = l + 32 * k;
+        if (e < np4) {
+            float* d = &cP[e >> 4][(e & 15) * 4];
+            d[0] = pv[k].x; d[1] = pv[k].y; d[2] = pv[k].z; d[3] = pv[k].w;
+        }
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        const int e = l + 32 * k;
+        if (e < nq4) {
+            float* d = &cQ[e >> 2][(e & 3) * 4];
+            d[0] = qv[k].x; d[1] = qv[k].y; d[2] = qv[k].z; d[3] = qv[k].w;
+        }
+    }
+    __syncwarp();
+}
+
 __global__ void __launch_bounds__(32 * kScanWarps)
 scan_fold_kernel(const float* __restrict__ Pc, const float* __restrict__ Qc, int64_t n_child, int G,
                  float* __restrict__ Pg, float* __restrict__ Qg, int64_t n_grp, int with_p) {
@@ -771,19 +811,7 @@ scan_fold_kernel(const float* __restrict__ Pc, const float* __restrict__ Qc, int
     if (g >= n_grp) return;
     const int64_t c0 = g * G;
     const int nc = static_cast<int>(min(static_cast<int64_t>(G), n_child - c0));
-    for (int c = 0; c < nc; ++c) {
-        if (with_p) {
-            cP[w][c][l] = __ldg(Pc + (c0 + c) * 64 + l);
-            cP[w][c][l + 32] = __ldg(Pc + (c0 + c) * 64 + l + 32);
-        } else if (l < 16) {
-            // only Q P_c is needed: rows of P_c are read by all lanes
-            cP[w][c][l] = __ldg(Pc + (c0 + c) * 64 + l);
-            cP[w][c][l + 16] = __ldg(Pc + (c0 + c) * 64 + l + 16);
-            cP[w][c][l + 32] = __ldg(Pc + (c0 + c) * 64 + l + 32);
-            cP[w][c][l + 48] = __ldg(Pc + (c0 + c) * 64 + l + 48);
-        }
-        if (l < 16) cQ[w][c][l] = __ldg(Qc + (c0 + c) * 16 + l);
-    }
+    stage_children(Pc, Qc, c0, nc, l, cP[w], cQ[w]);
     float* P = sP[w];
     float* Q = sQ[w];
     P[2 * l] = ((2 * l) % 9 == 0) ? 1.f : 0.f;
@@ -831,11 +859,7 @@ scan_down_kernel(const float* __restrict__ Pc, const float* __restrict__ Qc, int
     if (g >= n_grp) return;
     const int64_t c0 = g * G;
     const int nc = static_cast<int>(min(static_cast<int64_t>(G), n_child - c0));
-    for (int c = 0; c < nc - 1; ++c) {
-        cP[w][c][l] = __ldg(Pc + (c0 + c) * 64 + l);
-        cP[w][c][l + 32] = __ldg(Pc + (c0 + c) * 64 + l + 32);
-        if (l < 16) cQ[w][c][l] = __ldg(Qc + (c0 + c) * 16 + l);
-    }
+    stage_children(Pc, Qc, c0, nc - 1, l, cP[w], cQ[w]);
     float* T = sT[w];
     if (l < 16) T[l] = Tg[g * 16 + l];
     __syncwarp();
@@ -855,8 +879,8 @@ scan_down_kernel(const float* __restrict__ Pc, const float* __restrict__ Qc, int
         __syncwarp();
     }
     __syncwarp();
-    for (int c = 0; c < nc; ++c)
-        if (l < 16) Tc[(c0 + c) * 16 + l] = oT[w][c][l];
+    // the group's children are contiguous: one coalesced sweep
+    for (int e = l; e < nc * 16; e += 32) Tc[c0 * 16 + e] = oT[w][e >> 4][e & 15];
 }
 
 // ---------------------------------------------------------------------------
