@@ -1151,7 +1151,10 @@ class RxPipeline:
         F = int(self.gpu.ddlms_frame_symbols)
         # symbols the stream will end with (upper bound: 4 samples / symbol)
         self._expected_symbols = int(n_samples) // 4
-        self._y2.ensure_capacity(min(n_samples // 2, 2 * F + 2 * self.cfg.static_plan.hop) + 16)
+        # asynchronous frames keep their input live until solved: hold the
+        # whole announced stream (a window slide would wait for the worker)
+        y2_cap = n_samples // 2 if self._async else min(n_samples // 2, 2 * F + 2 * self.cfg.static_plan.hop)
+        self._y2.ensure_capacity(y2_cap + 16)
         c = chunk_samples or n_samples
         self._z.ensure_capacity(min(n_samples, c + 2 * self.cfg.carrier_segment_len + self.cfg.static_plan.hop))
 

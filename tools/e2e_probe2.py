@@ -48,6 +48,7 @@ for rep in range(3):
     t0.record()
     h0 = time.perf_counter()
     pipe, bits, n = receive_host_stream(cfg, host, cap.half_lsb, ref, chunk_samples=chunk, staging=staging, trace=tr)
+    evs = list(pipe._events)
     t1 = torch.cuda.Event(enable_timing=True)
     t1.record()
     torch.cuda.synchronize()
@@ -62,6 +63,13 @@ for rep in range(3):
             print(f"  chunk {i:3d}: fed @ {t0.elapsed_time(fe):8.2f} "
                   f"host @ {1e3 * (ht - h0):8.2f} pending {nj}")
         print("  stats", [(s["k0"], s["nsym"], s.get("iterations")) for s in pipe.ddlms_stats])
+        for name, e0, e1 in pipe._events:
+            if name == "ddlms" and e1.query():
+                try:
+                    print(f"  frame: start {t0.elapsed_time(e0):8.2f} end {t0.elapsed_time(e1):8.2f}")
+                except Exception:
+                    pass
+        pipe._events = evs
         print("  stages", pipe.stage_seconds)
         for k_, v_ in HT.items():
             print("  host", k_, "n", len(v_), "total ms %.2f" % (1e3 * sum(v_)), "max ms %.2f" % (1e3 * max(v_)),
