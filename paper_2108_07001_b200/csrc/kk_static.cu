@@ -434,19 +434,31 @@ extern "C" int kk_static_blocks(const void* z, int64_t z_index0, int64_t hb0, in
 namespace kk {
 __global__ void carrier_means_kernel(const float2* __restrict__ hop_sum, int64_t n_segs, int hops_per_seg,
                                      int64_t n_hops_avail, int64_t last_len, int seg_len, float2* __restrict__ mean) {
-    const int64_t s = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    // one warp per segment: lane-strided fp64 partial sums (all loads
+    // independent), fixed shuffle tree -- a deterministic order that does not
+    // depend on how the stream was chunked
+    const int64_t s = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
     if (s >= n_segs) return;
     double re = 0.0, im = 0.0;
     const int64_t h0 = s * hops_per_seg;
-    for (int i = 0; i < hops_per_seg; ++i) {
+    for (int i = lane; i < hops_per_seg; i += 32) {
         const int64_t h = h0 + i;
-        if (h >= n_hops_avail) break;
-        const float2 v = hop_sum[h];
-        re += v.x;
-        im += v.y;
+        if (h < n_hops_avail) {
+            const float2 v = __ldg(hop_sum + h);
+            re += v.x;
+            im += v.y;
+        }
     }
-    const double len = (s == n_segs - 1 && last_len > 0) ? static_cast<double>(last_len) : static_cast<double>(seg_len);
-    mean[s] = make_float2(static_cast<float>(re / len), static_cast<float>(im / len));
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        re += __shfl_xor_sync(0xffffffffu, re, o);
+        im += __shfl_xor_sync(0xffffffffu, im, o);
+    }
+    if (lane == 0) {
+        const double len = (s == n_segs - 1 && last_len > 0) ? static_cast<double>(last_len) : static_cast<double>(seg_len);
+        mean[s] = make_float2(static_cast<float>(re / len), static_cast<float>(im / len));
+    }
 }
 }  // namespace kk
 
@@ -455,8 +467,8 @@ extern "C" int kk_carrier_means(const void* hop_sum, int64_t n_segs, int hops_pe
     using namespace kk;
     clear_error();
     if (n_segs <= 0) return KK_OK;
-    const int th = 128;
-    carrier_means_kernel<<<static_cast<unsigned>((n_segs + th - 1) / th), th, 0, static_cast<cudaStream_t>(stream)>>>(
+    const int th = 128;   // 4 segments per CTA (one warp each)
+    carrier_means_kernel<<<static_cast<unsigned>((n_segs * 32 + th - 1) / th), th, 0, static_cast<cudaStream_t>(stream)>>>(
         static_cast<const float2*>(hop_sum), n_segs, hops_per_seg, n_hops_avail, last_len, seg_len,
         static_cast<float2*>(mean));
     return check_launch("carrier_means_kernel");
