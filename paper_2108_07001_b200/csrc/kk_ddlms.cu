@@ -165,43 +165,6 @@ __device__ __forceinline__ void load_pair(const SolveArgs& a, int64_t i, float& 
     r0 = v0.x * a.scale; i0 = v0.y * a.scale; r1 = v1.x * a.scale; i1 = v1.y * a.scale;
 }
 
-// P_b = prod (I - 2 mu X X^T) over the block; also max |X|^2
-__global__ void ddlms_maps_kernel(SolveArgs a, float* __restrict__ Pb, float* __restrict__ maxx2) {
-    const int64_t b = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (b >= a.nb) return;
-    float P[64];
-#pragma unroll
-    for (int i = 0; i < 64; ++i) P[i] = (i % 9 == 0) ? 1.f : 0.f;
-    const int64_t k0 = b * a.B, k1 = min(k0 + a.B, a.nsym);
-    const float tm = 2.0f * a.mu;
-    float mx = 0.f;
-    float X[8];
-    if (k0 < k1) load_pair(a, 2 * k0, X[4], X[5], X[6], X[7]);
-    for (int64_t k = k0; k < k1; ++k) {
-        X[0] = X[4]; X[1] = X[5]; X[2] = X[6]; X[3] = X[7];
-        load_pair(a, 2 * k + 2, X[4], X[5], X[6], X[7]);
-        float n2 = 0.f;
-#pragma unroll
-        for (int j = 0; j < 8; ++j) n2 = fmaf(X[j], X[j], n2);
-        mx = fmaxf(mx, n2);
-        float v[8];
-#pragma unroll
-        for (int i = 0; i < 8; ++i) {
-            float s = 0.f;
-#pragma unroll
-            for (int j = 0; j < 8; ++j) s = fmaf(P[i * 8 + j], X[j], s);
-            v[i] = s * tm;
-        }
-#pragma unroll
-        for (int i = 0; i < 8; ++i)
-#pragma unroll
-            for (int j = 0; j < 8; ++j) P[i * 8 + j] = fmaf(-v[i], X[j], P[i * 8 + j]);
-    }
-    float* o = Pb + b * 64;
-#pragma unroll
-    for (int i = 0; i < 64; ++i) o[i] = P[i];
-    maxx2[b] = mx;
-}
 
 struct RunOut {
     uint8_t* labels;
@@ -371,10 +334,6 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
 
-struct LeanSlicer {
-    int square, m;
-    float half_norm, off, h;     // v = y*half_norm + off: level index; h = half level spacing
-};
 
 struct TOut {
     float2* ST;       // [nsym] soft (final pass)
