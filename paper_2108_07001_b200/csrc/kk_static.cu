@@ -222,9 +222,38 @@ __global__ void __launch_bounds__(kK2Threads, 1) static_blocks_kernel(K2Params p
     extern __shared__ __align__(16) unsigned char smem_raw[];
     K2Smem& S = *reinterpret_cast<K2Smem*>(smem_raw);
     const int tid = threadIdx.x;
-    load_twiddles(S.tw, tw_g, tid, kK2Threads);
-    if (p.carrier && p.rot_q > 0 && p.rot_q <= kRotMax)
-        for (int i = tid; i < p.rot_q; i += kK2Threads) S.rot[i] = p.rot_tab[i];
+    // twiddle + rotation tables (26 KB from L2): every load issued before
+    // any store, so the CTA pays one latency instead of one per loop trip
+    {
+        constexpr int kTw4 = kTwEntries / 2;                      // float4 = 2 entries
+        static_assert(kTwEntries % 2 == 0, "twiddle table");
+        constexpr int kPer = (kTw4 + kK2Threads - 1) / kK2Threads;
+        const float4* g4 = reinterpret_cast<const float4*>(tw_g);
+        float4* s4 = reinterpret_cast<float4*>(S.tw);
+        float4 tv[kPer];
+#pragma unroll
+        for (int k = 0; k < kPer; ++k) {
+            const int i = tid + k * kK2Threads;
+            tv[k] = i < kTw4 ? __ldg(g4 + i) : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+        float2 rv[(kRotMax + kK2Threads - 1) / kK2Threads];
+        const bool rot = p.carrier && p.rot_q > 0 && p.rot_q <= kRotMax;
+#pragma unroll
+        for (int k = 0; k < (kRotMax + kK2Threads - 1) / kK2Threads; ++k) {
+            const int i = tid + k * kK2Threads;
+            rv[k] = (rot && i < p.rot_q) ? __ldg(p.rot_tab + i) : make_float2(0.f, 0.f);
+        }
+#pragma unroll
+        for (int k = 0; k < kPer; ++k) {
+            const int i = tid + k * kK2Threads;
+            if (i < kTw4) s4[i] = tv[k];
+        }
+#pragma unroll
+        for (int k = 0; k < (kRotMax + kK2Threads - 1) / kK2Threads; ++k) {
+            const int i = tid + k * kK2Threads;
+            if (rot && i < p.rot_q) S.rot[i] = rv[k];
+        }
+    }
     __syncthreads();
 
     const Twiddle tw{S.tw};
