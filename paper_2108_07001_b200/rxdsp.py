@@ -266,6 +266,11 @@ def _as_device_input(x, dev):
     return torch.from_numpy(a).to(dev, non_blocking=True), _lib.KK_DTYPE_F64, 1.0
 
 
+# NVTX ranges around the pipeline stages (KK_NVTX=1; for nsys/ncu range filters)
+import os as _os
+
+_NVTX = _os.environ.get("KK_NVTX", "0") == "1"
+
 _SIDE_STREAMS = {}
 import threading as _threading
 
@@ -1126,18 +1131,27 @@ class RxPipeline:
             n_hops = (n_hops // 2) * 2          # pairs on the global even-hop grid
         if n_hops == 0 and not flush:
             return
+        nv = _NVTX
         t0 = self._ev()
         if n_hops:
             chunk = self._raw[:n_hops * hop]
+            nv and torch.cuda.nvtx.range_push("kk")
             self._run_kk(chunk, n_hops)
+            nv and torch.cuda.nvtx.range_pop()
             self._raw = self._raw[n_hops * hop:]
         t1 = self._ev()
+        nv and torch.cuda.nvtx.range_push("carrier")
         self._run_carrier(flush)
+        nv and torch.cuda.nvtx.range_pop()
         t2 = self._ev()
+        nv and torch.cuda.nvtx.range_push("static")
         self._run_static(flush)
+        nv and torch.cuda.nvtx.range_pop()
         t3 = self._ev()
         if not getattr(self, "_front_only", False):
+            nv and torch.cuda.nvtx.range_push("ddlms")
             self._run_ddlms(flush)
+            nv and torch.cuda.nvtx.range_pop()
         t4 = self._ev()
         self._events += [("kk", t0, t1), ("carrier", t1, t2), ("static", t2, t3), ("ddlms", t3, t4)]
         self._chunk_index += 1
