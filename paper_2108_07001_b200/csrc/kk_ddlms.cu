@@ -1690,19 +1690,26 @@ __global__ void pack_bits_kernel(const uint8_t* __restrict__ lab, int64_t n, int
                                  uint8_t* __restrict__ out, int64_t nbytes) {
     for (int64_t o = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; o < nbytes;
          o += int64_t(gridDim.x) * blockDim.x) {
+        // first symbol touching byte o and the bit offset inside it: one
+        // 64-bit division per byte, then incremental (no per-bit divisions)
+        const int64_t b0 = o * 8;
+        int64_t s = b0 / k;
+        int bit = static_cast<int>(b0 - s * k);       // bits of symbol s already consumed
         unsigned byte = 0;
-        int64_t b = o * 8;
-#pragma unroll 1
-        for (int t = 0; t < 8; ++t, ++b) {
-            const int64_t s = b / k;
-            unsigned bit = 0;
+        int filled = 0;
+        while (filled < 8) {
+            unsigned word = 0;
             if (s < n) {
                 int li = lab[s];
                 if (li == 255) li = (sym0 + s < n_train && train_idx) ? train_idx[sym0 + s] : 0;
-                const int word = pl.v[li & 63];
-                bit = (word >> (k - 1 - static_cast<int>(b - s * k))) & 1;
+                word = pl.v[li & 63];
             }
-            byte |= bit << (7 - t);
+            const int take = min(k - bit, 8 - filled);          // bits of this symbol in this byte
+            const unsigned chunk = (word >> (k - bit - take)) & ((1u << take) - 1u);
+            byte |= chunk << (8 - filled - take);
+            filled += take;
+            bit += take;
+            if (bit == k) { bit = 0; ++s; }
         }
         out[o] = static_cast<uint8_t>(byte);
     }

@@ -284,13 +284,13 @@ def _stream_receiver(cfg, reference_symbols, n: int, chunk_samples: int, dev):
     return st
 
 
-def _drain_bits(st, bits_host, d2h, dev):
+def _drain_bits(st, bits_host, d2h, dev, max_frames=None):
     """Finished frames -> packed bits -> pinned host, on the d2h stream (the
     other DMA direction), off the compute stream."""
     import torch
 
     pipe, k = st["pipe"], st["k"]
-    lab, soft, _ = pipe.drain_device(wait_stream=d2h)
+    lab, soft, _ = pipe.drain_device(wait_stream=d2h, want_soft=False, max_frames=max_frames)
     if not lab.numel():
         return
     nb = (lab.numel() * k + 7) // 8
@@ -342,7 +342,16 @@ def _receive_host_stream(cfg, host_codes, half_lsb, reference_symbols, chunk_sam
             ev = torch.cuda.Event(enable_timing=True)
             ev.record(comp)
             trace.append((i, time.perf_counter(), ready[i], ev, len(pipe._jobs)))
-        _drain_bits(st, bits_host, d2h, dev)
+        # after the last chunk: ship each remaining frame as soon as it is
+        # solved (its transfer overlaps the next frames' solves)
+        while True:
+            _drain_bits(st, bits_host, d2h, dev, max_frames=1 if i == len(starts) - 1 else None)
+            if trace is not None:
+                ev2 = torch.cuda.Event(enable_timing=True)
+                ev2.record(d2h)
+                trace.append(("d2h", time.perf_counter(), ev2))
+            if i < len(starts) - 1 or not pipe.frames_pending:
+                break
     comp.wait_stream(d2h)
     return pipe, bits_host, st["n_out"]
 
@@ -419,8 +428,11 @@ def receive_raw_file(cfg, path: str, reference_symbols, chunk_samples: int = 1 <
                 ready.record(copy)
             free_q.put((i, ready))
             comp.wait_event(ready)
-            pipe.feed(AdcCodes(staging[a:a + m], half_lsb, cfg.adc_rate_hz), flush=ci == len(starts) - 1)
-            _drain_bits(st, bits_host, d2h, dev)
+            last = ci == len(starts) - 1
+            pipe.feed(AdcCodes(staging[a:a + m], half_lsb, cfg.adc_rate_hz), flush=last)
+            _drain_bits(st, bits_host, d2h, dev, max_frames=1 if last else None)
+            while last and pipe.frames_pending:
+                _drain_bits(st, bits_host, d2h, dev, max_frames=1)
         comp.wait_stream(d2h)
     th.join()
     if err:

@@ -106,6 +106,11 @@ class EqualizerState:
         return cls(w=w, g=np.zeros(n_taps, dtype=np.complex128))
 
     @property
+    def frames_pending(self) -> int:
+        """Asynchronous DDLMS frames submitted but not yet drained."""
+        return len(self._jobs)
+
+    @property
     def diverged(self) -> bool:
         return self.frozen
 
@@ -1040,13 +1045,15 @@ class RxPipeline:
                 job["error"] = exc
             job["finished"].set()
 
-    def _collect_frames(self, block: bool, wait_stream=None):
+    def _collect_frames(self, block: bool, wait_stream=None, max_frames: int | None = None):
         """Move finished frames (all of them when block) to the outputs, in
         order; `wait_stream` (default: the current stream) is made to wait for
         their completion."""
         torch = _torch()
         ws = wait_stream if wait_stream is not None else torch.cuda.current_stream(self.dev)
-        while self._jobs:
+        got = 0
+        while self._jobs and (max_frames is None or got < max_frames):
+            got += 1
             job = self._jobs[0]
             if not job["finished"].is_set():
                 if not block:
@@ -1181,7 +1188,7 @@ class RxPipeline:
         finally:
             self._front_only = False
 
-    def drain_device(self, wait_stream=None):
+    def drain_device(self, wait_stream=None, want_soft: bool = True, max_frames: int | None = None):
         """Device-resident outputs accumulated so far, then cleared:
         (labels uint8 [n] point indices (255 = training symbol), soft
         complex64 [n], list of (first symbol index, n_train) per frame).
@@ -1194,7 +1201,7 @@ class RxPipeline:
         if ws is not cur:
             ws.wait_stream(cur)       # outputs of synchronous frames (current stream)
         if self._async and self._jobs:
-            self._collect_frames(block=self._flushed, wait_stream=ws)
+            self._collect_frames(block=self._flushed, wait_stream=ws, max_frames=max_frames)
         with torch.cuda.stream(ws):
             if not self._out:
                 return (torch.zeros(0, dtype=torch.uint8, device=self.dev),
@@ -1203,7 +1210,9 @@ class RxPipeline:
                 labels, soft = self._out[0][0], self._out[0][1]
             else:
                 labels = torch.cat([o[0] for o in self._out])
-                soft = torch.cat([o[1] for o in self._out])
+                # (callers that only ship bits skip the soft concatenation)
+                soft = (torch.cat([o[1] for o in self._out]) if want_soft
+                        else torch.zeros(0, dtype=torch.complex64, device=self.dev))
         meta = [(o[2], o[3]) for o in self._out]
         self._out = []
         return labels, soft, meta
@@ -1237,6 +1246,11 @@ class RxPipeline:
         """Flush (zero-padded) and return what has not been drained (rx:811-815)."""
         self.feed(np.zeros(0), flush=True)
         return self.drain()
+
+    @property
+    def frames_pending(self) -> int:
+        """Asynchronous DDLMS frames submitted but not yet drained."""
+        return len(self._jobs)
 
     @property
     def diverged(self) -> bool:

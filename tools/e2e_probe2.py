@@ -59,7 +59,11 @@ for rep in range(3):
           "frees", ms1.get("num_device_free", 0) - ms0.get("num_device_free", 0),
           "retries", ms1.get("num_alloc_retries", 0) - ms0.get("num_alloc_retries", 0))
     if rep == 2:
-        for i, ht, rd, fe, nj in tr:
+        for item in tr:
+            if item[0] == "d2h":
+                print(f"  d2h done @ {t0.elapsed_time(item[2]):8.2f} host @ {1e3 * (item[1] - h0):8.2f}")
+                continue
+            i, ht, rd, fe, nj = item
             print(f"  chunk {i:3d}: fed @ {t0.elapsed_time(fe):8.2f} "
                   f"host @ {1e3 * (ht - h0):8.2f} pending {nj}")
         print("  stats", [(s["k0"], s["nsym"], s.get("iterations")) for s in pipe.ddlms_stats])
