@@ -128,7 +128,7 @@ class GpuOptions:
     ddlms_frame_symbols: int = 1 << 28
     ddlms_max_iter: int = 64
     ddlms_soft_tol: float = 1e-5
-    ddlms_tail_min_symbols: int = 1 << 22
+    ddlms_tail_min_symbols: int = 1 << 24
     # run the DDLMS frames on a worker thread / CUDA stream so the front end
     # of later chunks overlaps them (streaming receive, harness.receive_host_stream)
     ddlms_async: bool = False
