@@ -311,6 +311,9 @@ __global__ void fill_T_kernel(float* __restrict__ T, int64_t b0, int64_t b1, con
 #ifndef KK_DD_MINB
 #define KK_DD_MINB 4      // resident CTAs / SM of the decision passes
 #endif
+#ifndef KK_DD_MINB_P
+#define KK_DD_MINB_P 3    // resident CTAs / SM of the P pass
+#endif
 constexpr int kBlockThreads = 128;
 
 __device__ __forceinline__ void cp_async16(void* smem, const void* g, int src_bytes) {
@@ -372,7 +375,7 @@ __device__ __forceinline__ int stage_idx(int chunk, int row, int col) {
 }
 
 template <bool WITH_P, int SQ, bool AL16, bool TRAIN>
-__global__ void __launch_bounds__(kBlockThreads, WITH_P ? 3 : KK_DD_MINB)
+__global__ void __launch_bounds__(kBlockThreads, WITH_P ? KK_DD_MINB_P : KK_DD_MINB)
 ddlms_block_kernel(SolveArgs a, Slicer sl, const float* __restrict__ Tstart, float* __restrict__ Pb,
                    float* __restrict__ maxx2, RunOut o, TOut to, int64_t b_lo, int64_t b_hi, int use_skip,
                    float soft_tol, const int* __restrict__ list, const unsigned long long* __restrict__ list_n,
@@ -508,9 +511,13 @@ ddlms_block_kernel(SolveArgs a, Slicer sl, const float* __restrict__ Tstart, flo
         issue(c + kChunks - 1);        // (empty groups past the end keep the count uniform)
         cp_async_wait<kChunks - 1>();  // this lane's copies of chunk c landed
         __syncwarp();                  // ... and every other lane's
-        float4 rows[kChunkRows];
+        // decision passes preload the chunk's 8 rows (ILP); the P pass reads
+        // each row when it is needed (32 fewer live registers: 4 CTAs / SM)
+        float4 rows[WITH_P ? 1 : kChunkRows];
+        if constexpr (!WITH_P) {
 #pragma unroll
-        for (int j = 0; j < kChunkRows; ++j) rows[j] = stage[stage_idx(c % kChunks, j, lane)];
+            for (int j = 0; j < kChunkRows; ++j) rows[j] = stage[stage_idx(c % kChunks, j, lane)];
+        }
         float2 soft8[kChunkRows];
         unsigned lab8[2] = {0u, 0u};
 #pragma unroll
@@ -518,7 +525,8 @@ ddlms_block_kernel(SolveArgs a, Slicer sl, const float* __restrict__ Tstart, flo
             const int i = c * kChunkRows + j;
             const bool live = i < nk;
             X[0] = X[4]; X[1] = X[5]; X[2] = X[6]; X[3] = X[7];
-            X[4] = rows[j].x; X[5] = rows[j].y; X[6] = rows[j].z; X[7] = rows[j].w;
+            const float4 rw = WITH_P ? stage[stage_idx(c % kChunks, j, lane)] : rows[WITH_P ? 0 : j];
+            X[4] = rw.x; X[5] = rw.y; X[6] = rw.z; X[7] = rw.w;
             float ya = 0.f, yb = 0.f, za = 0.f, zb = 0.f;
 #pragma unroll
             for (int jj = 0; jj < 8; jj += 2) {
