@@ -281,12 +281,24 @@ __device__ __forceinline__ void stockham_compute_store(int tid, const Twiddle& t
 // loader reads the same buffer the storer writes).
 // SYNC_IN == false means the pass is out of place (loader and storer touch
 // different memory): butterflies then stream one at a time (R live values).
-template <int N, int R, int NS, int NT, bool INV, bool SYNC_IN, class Load, class Store>
-__device__ __forceinline__ void stockham_pass(int tid, const Twiddle& tw, const Load& load, const Store& store) {
+struct BlockBarrier {
+    __device__ __forceinline__ void operator()() const { __syncthreads(); }
+};
+// named barrier over the NT threads of one sub-group (id 1..15) of the CTA
+struct GroupBarrier {
+    int id, nt;
+    __device__ __forceinline__ void operator()() const {
+        asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nt) : "memory");
+    }
+};
+
+template <int N, int R, int NS, int NT, bool INV, bool SYNC_IN, class Load, class Store, class Bar = BlockBarrier>
+__device__ __forceinline__ void stockham_pass(int tid, const Twiddle& tw, const Load& load, const Store& store,
+                                              const Bar& bar = Bar{}) {
     if constexpr (SYNC_IN) {
         float2 v[PassShape<N, R, NT>::BPT][R];
         stockham_load<N, R, NT>(tid, load, v);
-        __syncthreads();
+        bar();
         stockham_compute_store<N, R, NS, NT, INV>(tid, tw, v, store);
     } else {
         constexpr int NB = PassShape<N, R, NT>::NB;

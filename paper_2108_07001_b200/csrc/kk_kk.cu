@@ -214,17 +214,20 @@ kk_pairs_kernel(const TIn* __restrict__ in, float in_scale, float clamp_rel, int
     const float* ub = S.u + (2 * g + 1) * kHop;      // block b: stage hops 2g+1, 2g+2
 
     auto ld_u = [&](int i) { return make_float2(ua[i], ub[i]); };
+    // the four pairs of the CTA are independent: each 64-thread group syncs
+    // on its own named barrier between passes
+    const GroupBarrier gb{g + 1, kGroupThreads};
     stockham_pass<kN1, 16, 1, kGroupThreads, false, false>(gt, tw, ld_u, StorePlanes{P});
-    __syncthreads();
-    stockham_pass<kN1, 16, 16, kGroupThreads, false, true>(gt, tw, LoadPlanes{P}, StorePlanes{P});
-    __syncthreads();
-    stockham_pass<kN1, 4, 256, kGroupThreads, false, true>(gt, tw, LoadPlanes{P}, StorePlanes{P});
-    __syncthreads();
+    gb();
+    stockham_pass<kN1, 16, 16, kGroupThreads, false, true>(gt, tw, LoadPlanes{P}, StorePlanes{P}, gb);
+    gb();
+    stockham_pass<kN1, 4, 256, kGroupThreads, false, true>(gt, tw, LoadPlanes{P}, StorePlanes{P}, gb);
+    gb();
     auto ld_m = [&](int k) { return apply_mult(k, P.ld(k)); };
-    stockham_pass<kN1, 16, 1, kGroupThreads, true, true>(gt, tw, ld_m, StorePlanes{P});
-    __syncthreads();
-    stockham_pass<kN1, 16, 16, kGroupThreads, true, true>(gt, tw, LoadPlanes{P}, StorePlanes{P});
-    __syncthreads();
+    stockham_pass<kN1, 16, 1, kGroupThreads, true, true>(gt, tw, ld_m, StorePlanes{P}, gb);
+    gb();
+    stockham_pass<kN1, 16, 16, kGroupThreads, true, true>(gt, tw, LoadPlanes{P}, StorePlanes{P}, gb);
+    gb();
 
     // last inverse pass: outputs n = j + 256 r; n >= 512 are the new hop
     float2 acc_a = make_float2(0.f, 0.f), acc_b = make_float2(0.f, 0.f);
@@ -290,7 +293,7 @@ kk_pairs_kernel(const TIn* __restrict__ in, float in_scale, float clamp_rel, int
             out[pb] = zb;
         }
     };
-    stockham_pass<kN1, 4, 256, kGroupThreads, true, true>(gt, tw, LoadPlanes{P}, st_out);
+    stockham_pass<kN1, 4, 256, kGroupThreads, true, true>(gt, tw, LoadPlanes{P}, st_out, gb);
 
     // ---- deterministic per-hop field sums (fixed shuffle tree) ----
 #pragma unroll
