@@ -1069,6 +1069,8 @@ class RxPipeline:
             self._out.append((labels, soft, job["k0"], n_train))
         if self._y2 is not None:
             self._y2.keep = self._drop + 2 * (self._jobs[0]["k0"] if self._jobs else self._sym_done)
+        if self._flushed and not self._jobs:
+            self._stop_worker()       # no frame can follow a flush: release the thread
 
     def _wait_frames(self):
         if self._jobs:
