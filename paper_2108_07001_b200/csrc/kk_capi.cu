@@ -4,6 +4,8 @@
 #include <cstdio>
 #include <cstring>
 #include <mutex>
+#include <set>
+#include <utility>
 #include <vector>
 
 #include "kk_common.cuh"
@@ -42,6 +44,19 @@ constexpr int kMaxDev = 64;
 std::once_flag g_tw_once[kMaxDev];
 float2* g_tw[kMaxDev] = {nullptr};
 }  // namespace
+
+int ensure_smem_attr(const void* fn, size_t smem, const char* what) {
+    static std::mutex mu;
+    static std::set<std::pair<int, const void*>> done;
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return set_cuda_error("cudaGetDevice");
+    std::lock_guard<std::mutex> lock(mu);
+    if (done.count({dev, fn})) return KK_OK;
+    if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)) != cudaSuccess)
+        return set_cuda_error(what);
+    done.insert({dev, fn});
+    return KK_OK;
+}
 
 int num_sms() {
     static int cached[64] = {0};

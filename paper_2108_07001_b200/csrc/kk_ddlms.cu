@@ -1264,14 +1264,8 @@ struct DdlmsSolver {
     // launch -- compacted into a re-run list first when use_skip.
     int run_blocks(bool with_p, int64_t b0, int64_t b1, int use_skip, float tol = 0.f, int write_out = 0) {
         if (b1 <= b0) return KK_OK;
-        // kernel attributes once per device and process (cudaFuncSetAttribute
-        // can serialise against work in flight on other threads' streams)
-        static std::once_flag attr_once[64];
-        static int attr_rc[64] = {0};
-        int dev = 0;
-        cudaGetDevice(&dev);
-        if (dev < 0 || dev >= 64) return set_error(KK_ERR_CUDA, "device index");
-        std::call_once(attr_once[dev], [&]() {
+        // kernel attributes once per device and process (ensure_smem_attr)
+        {
             struct KS { const void* k; size_t smem; };
             const KS ks[] = {
 #define KK_DD_K(P_, S_, T_) {reinterpret_cast<const void*>(ddlms_block_kernel<P_, S_, true, T_>), T_ ? kStageSmem + kTrainSmem : kStageSmem}, \
@@ -1283,11 +1277,8 @@ struct DdlmsSolver {
 #undef KK_DD_K
             };
             for (const KS& k : ks)
-                if (cudaFuncSetAttribute(k.k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(k.smem)) !=
-                    cudaSuccess)
-                    attr_rc[dev] = 1;
-        });
-        if (attr_rc[dev]) return set_error(KK_ERR_CUDA, "ddlms_block_kernel smem attribute");
+                if (int rc = ensure_smem_attr(k.k, k.smem, "ddlms_block_kernel smem attribute")) return rc;
+        }
         const int sq = sl.sep ? sl.m : 0;
         const bool al = (reinterpret_cast<uintptr_t>(a.x) & 15) == 0;
         auto launch = [&](bool train_blocks, int64_t lo, int64_t hi, int skip, const int* lst,

@@ -22,4 +22,8 @@ const float2* twiddle_table_device();
 // SM count of the current device (cached per device)
 int num_sms();
 
+// cudaFuncAttributeMaxDynamicSharedMemorySize for `fn` on the current device,
+// set once per (device, kernel) for the whole process (thread-safe)
+int ensure_smem_attr(const void* fn, size_t smem, const char* what);
+
 }  // namespace kk

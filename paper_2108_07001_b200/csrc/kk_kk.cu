@@ -332,12 +332,8 @@ static int launch_k1(const void* in, float in_scale, float clamp_rel, int64_t n_
     const float2* tw = twiddle_table_device();
     if (!tw) return KK_ERR_CUDA;
     const size_t smem = sizeof(K1Smem);
-    static bool attr_done = false;
-    if (!attr_done) {
-        if (cudaFuncSetAttribute(kk_pairs_kernel<TIn>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 static_cast<int>(smem)) != cudaSuccess) return set_cuda_error("K1 smem attr");
-        attr_done = true;
-    }
+    if (int rc = ensure_smem_attr(reinterpret_cast<const void*>(kk_pairs_kernel<TIn>), smem, "K1 smem attr"))
+        return rc;
     const int64_t pairs = (n_hops + 1) / 2;
     const int64_t grid = (pairs + kPairsPerCta - 1) / kPairsPerCta;
     kk_pairs_kernel<TIn><<<static_cast<unsigned>(grid), kK1Threads, smem, s>>>(

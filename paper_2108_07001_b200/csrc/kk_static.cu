@@ -399,16 +399,11 @@ extern "C" int kk_static_blocks(const void* z, int64_t z_index0, int64_t hb0, in
     if (rot_q > 0 && !rot_tab) return set_error(KK_ERR_PARAM, "rotation table missing");
     const float2* tw = twiddle_table_device();
     if (!tw) return KK_ERR_CUDA;
-    static bool attr_done = false;
     const size_t smem = sizeof(K2Smem);
-    if (!attr_done) {
-        if (cudaFuncSetAttribute(static_blocks_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 static_cast<int>(smem)) != cudaSuccess ||
-            cudaFuncSetAttribute(static_blocks_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 static_cast<int>(smem)) != cudaSuccess)
-            return set_cuda_error("K2 smem attr");
-        attr_done = true;
-    }
+    if (int rc = ensure_smem_attr(reinterpret_cast<const void*>(static_blocks_kernel<true>), smem, "K2 smem attr"))
+        return rc;
+    if (int rc = ensure_smem_attr(reinterpret_cast<const void*>(static_blocks_kernel<false>), smem, "K2 smem attr"))
+        return rc;
     if (rot_q > kRotMax) return set_error(KK_ERR_PARAM, "rotation denominator must be <= 1024");
     K2Params p;
     p.z = static_cast<const float2*>(z);
