@@ -613,7 +613,9 @@ ddlms_block_kernel(SolveArgs a, Slicer sl, const float* __restrict__ Tstart, flo
         }
         if (!WITH_P && write_out) {   // outputs only from the final (full) pass
             const int i0 = c * kChunkRows;
-            if (i0 + kChunkRows <= nk) {
+            // vector stores need 16 B (soft) / 8 B (labels) alignment of the
+            // run: block starts k0 = b B are multiples of 8 when B is
+            if ((a.B & 7) == 0 && i0 + kChunkRows <= nk) {
                 float4* s4 = reinterpret_cast<float4*>(sp + i0);
 #pragma unroll
                 for (int j = 0; j < kChunkRows / 2; ++j)
