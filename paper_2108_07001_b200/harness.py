@@ -284,6 +284,14 @@ def _stream_receiver(cfg, reference_symbols, n: int, chunk_samples: int, dev):
     return st
 
 
+def _bits_capacity(cfg, n: int, k: int) -> int:
+    """Upper bound of the packed output bytes of an n-sample stream: the flush
+    zero-pads the KK and static hops, so up to (n + both FFT sizes) / 4
+    symbols are decided."""
+    n_sym = (n + cfg.static_plan.fft_size + cfg.kk_plan.fft_size) // 4 + 16
+    return (n_sym * k + 7) // 8 + 8
+
+
 def _drain_bits(st, bits_host, d2h, dev, max_frames=None):
     """Finished frames -> packed bits -> pinned host, on the d2h stream (the
     other DMA direction), off the compute stream."""
@@ -300,6 +308,9 @@ def _drain_bits(st, bits_host, d2h, dev, max_frames=None):
         _lib.call("kk_pack_bits", lab.data_ptr(), lab.numel(), st["n_out"],
                   ti.data_ptr() if ti is not None else None, st["n_train"], k,
                   st["tb"].point_label.ctypes.data, st["order"], packed.data_ptr(), d2h.cuda_stream)
+        if st["b_out"] + nb > bits_host.numel():
+            raise ParameterError(f"bits_host holds {bits_host.numel()} bytes, the stream needs more "
+                                 f"(>= {st['b_out'] + nb})")
         bits_host[st["b_out"]:st["b_out"] + nb].copy_(packed, non_blocking=True)
     lab.record_stream(d2h)
     soft.record_stream(d2h)
@@ -331,7 +342,7 @@ def _receive_host_stream(cfg, host_codes, half_lsb, reference_symbols, chunk_sam
             staging[a:a + m].copy_(host_codes[a:a + m], non_blocking=True)
             ready[i].record(copy)
     if bits_host is None:
-        bits_host = torch.empty((n // 4 + 8) * st["k"] // 8 + 8, dtype=torch.uint8, pin_memory=True)
+        bits_host = torch.empty(_bits_capacity(cfg, n, st["k"]), dtype=torch.uint8, pin_memory=True)
     for i, a in enumerate(starts):
         m = min(chunk_samples, n - a)
         comp.wait_event(ready[i])
@@ -414,7 +425,7 @@ def receive_raw_file(cfg, path: str, reference_symbols, chunk_samples: int = 1 <
         st = _stream_receiver(cfg, reference_symbols, n, chunk_samples, dev)
         pipe, cfg = st["pipe"], st["cfg"]
         staging = torch.empty(n, dtype=torch.int16, device=dev)
-        bits_host = torch.empty((n // 4 + 8) * st["k"] // 8 + 8, dtype=torch.uint8, pin_memory=True)
+        bits_host = torch.empty(_bits_capacity(cfg, n, st["k"]), dtype=torch.uint8, pin_memory=True)
         copy.wait_stream(comp)
         th.start()
         for ci, a in enumerate(starts):

@@ -526,3 +526,29 @@ def test_parallel_solver_equals_sequential_kernel(order, noise, B):
     # fp32 ties, the same bar as against the float64 reference
     assert len(mism) <= max(1, int(1e-4 * dd.sum()))
     assert np.median(np.abs(soft - s_seq)) < 1e-5
+
+
+def test_host_stream_ragged_length_and_chunks():
+    """Streaming receive of a ragged stream (length not a multiple of the
+    chunk, the KK hop or the static hop; ragged chunk size): the same bits as
+    the single-shot device path on the same samples."""
+    import torch
+
+    from paper_2108_07001_b200.constellation import slicer_tables
+    from paper_2108_07001_b200.harness import receive_host_stream
+
+    cap = load_capture("c4_qpsk_10000km_cspr6")
+    n = len(cap.adc_h) - 12345
+    codes = np.ascontiguousarray(cap.adc_h[:n])
+    cfg = cap.pipeline_config(ddlms_frame_symbols=1 << 13)
+    _, bits_host, n_sym = receive_host_stream(cfg, torch.from_numpy(codes).pin_memory(), cap.half_lsb,
+                                              cap.symbols(), chunk_samples=50001)
+    torch.cuda.synchronize()
+    p2 = rxdsp.RxPipeline(cap.pipeline_config(), reference_symbols=cap.symbols())
+    p2.feed(AdcCodes(codes, cap.half_lsb))
+    dec, _ = p2.finish()
+    assert n_sym == len(dec)
+    pl = slicer_tables(4).point_label[:4]
+    want = np.unpackbits(pl[to_idx(dec, 4)][:, None], axis=1)[:, -2:].reshape(-1)
+    got = np.unpackbits(bits_host[: (2 * n_sym + 7) // 8].numpy())[: 2 * n_sym]
+    assert np.array_equal(got, want)
