@@ -552,3 +552,44 @@ def test_host_stream_ragged_length_and_chunks():
     want = np.unpackbits(pl[to_idx(dec, 4)][:, None], axis=1)[:, -2:].reshape(-1)
     got = np.unpackbits(bits_host[: (2 * n_sym + 7) // 8].numpy())[: 2 * n_sym]
     assert np.array_equal(got, want)
+
+
+@pytest.mark.parametrize("n", [30000, 47000, 70001])
+def test_short_streams_vs_oracle(n):
+    """Streams shorter than the sync wait (the head is synchronised on what
+    the flush provides), ragged lengths: same sync offset and decisions as the
+    CPU oracle on the same samples."""
+    cap = load_capture("c1_qpsk_b2b")
+    x = cap.adc_float()[:n]
+    syms = cap.symbols()
+    ref = ko.OraclePipeline(ko.OracleConfig(taps=cap.taps), syms)
+    ref.feed(x, flush=True)
+    d_ref, _ = ref.finish()
+    pipe = rxdsp.RxPipeline(cap.pipeline_config(), reference_symbols=syms)
+    pipe.feed(x)
+    dec, _ = pipe.finish()
+    assert pipe.sync_offset == ref.sync_offset
+    assert len(dec) == len(d_ref)
+    # symbols decided past the end of the samples (the flush's zero padding
+    # up to the static hop) are ties around 0 in both; the reference's own
+    # measurement excludes them with its 4096-symbol tail guard
+    valid = (n // 2 - pipe.sync_offset) // 2 - 128
+    assert valid > 1000
+    assert np.mean(to_idx(dec[:valid], 4) == to_idx(d_ref[:valid], 4)) >= DEC_AGREE
+
+
+def test_wrong_reference_raises_sync_error():
+    """A reference sequence the stream does not contain: no correlation peak
+    (peak-to-rms < 4), SyncError -- as the reference (rx:596-600) and the
+    oracle raise."""
+    cap = load_capture("c1_qpsk_b2b")
+    rng = np.random.default_rng(5)
+    wrong = make_constellation(4).points[rng.integers(0, 4, len(cap.sym_idx))]
+    pipe = rxdsp.RxPipeline(cap.pipeline_config(), reference_symbols=wrong)
+    with pytest.raises(rxdsp.SyncError):
+        pipe.feed(cap.adc_float())
+        pipe.finish()
+    ref = ko.OraclePipeline(ko.OracleConfig(taps=cap.taps), wrong)
+    with pytest.raises(ko.OracleSyncError):
+        ref.feed(cap.adc_float(), flush=True)
+        ref.finish()
