@@ -53,6 +53,11 @@ unsigned long long kk_launch_count(void);
 /* measured FP32 FFMA throughput of the current device (FLOP/s), for the
  * roofline of the FP32-bound FFT kernels */
 int kk_fma_peak(double *flops_per_s_host, void *stream);
+/* Stream-ordered host->device upload of a small host buffer through kernel
+ * parameters (16 KB per launch): unlike a DMA copy it never queues behind
+ * bulk host->device transfers already in flight.  The host buffer may be
+ * reused on return.  (B200 addition; the reference has no device.) */
+int kk_upload(void *dst_dev, const void *src_host, int64_t bytes, void *stream);
 
 /*
  * K1 kk_fused -- replaces rxdsp.py:184-244 `kk_reconstruct` (+ the downshift

@@ -37,6 +37,7 @@ _SIGS = {
     "kk_device_sync": ([], _I),
     "kk_launch_count": ([], ctypes.c_ulonglong),
     "kk_fma_peak": ([_P, _P], _I),
+    "kk_upload": ([_P, _P, _I64, _P], _I),
     "kk_reconstruct_pairs": ([_I, _P, _F, _F, _I64, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _I64, _I, _I, _P, _I, _P], _I),
     "kk_carrier_means": ([_P, _I64, _I, _I64, _I64, _I, _P, _P], _I),
     "kk_static_blocks": ([_P, _I64, _I64, _I64, _I64, _P, _I64, _I, _I, _I, _I, _P, _I, _P, _P, _P, _P], _I),

@@ -1,5 +1,6 @@
 // C-ABI plumbing for libkkb200.so: thread-local last error, status codes,
 // lazily built immutable twiddle tables (one per device, std::call_once).
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -110,6 +111,40 @@ extern "C" unsigned long long kk_launch_count(void) { return __atomic_load_n(&kk
 extern "C" int kk_device_sync(void) {
     kk::clear_error();
     if (cudaDeviceSynchronize() != cudaSuccess) return kk::set_cuda_error("cudaDeviceSynchronize");
+    return KK_OK;
+}
+
+// ---------------------------------------------------------------------------
+// Small host->device uploads through kernel parameters.  A DMA copy (pinned
+// or pageable above 64 KB) issued while bulk input copies are queued waits
+// for them on the host->device copy engine; kernel parameters travel in the
+// launch itself, so per-stream set-up data (equaliser tables, reference
+// symbols) lands in order on its own stream.  16 KB per launch.
+// ---------------------------------------------------------------------------
+namespace kk {
+constexpr int kUpBlob = 16384;
+struct UpBlob {
+    unsigned char b[kUpBlob];
+};
+__global__ void upload_blob_kernel(unsigned char* __restrict__ dst, const UpBlob blob, int nbytes) {
+    for (int i = threadIdx.x; i < nbytes; i += blockDim.x) dst[i] = blob.b[i];
+}
+}  // namespace kk
+
+extern "C" int kk_upload(void* dst, const void* src, int64_t bytes, void* stream) {
+    kk::clear_error();
+    if (bytes < 0 || (bytes > 0 && (!dst || !src))) return kk::set_error(KK_ERR_PARAM, "kk_upload: bad arguments");
+    static kk::UpBlob blob;   // staging for the launch arguments (copied at launch)
+    static std::mutex mu;
+    std::lock_guard<std::mutex> lock(mu);
+    const auto* s = static_cast<const unsigned char*>(src);
+    auto* d = static_cast<unsigned char*>(dst);
+    for (int64_t off = 0; off < bytes; off += kk::kUpBlob) {
+        const int n = static_cast<int>(std::min<int64_t>(kk::kUpBlob, bytes - off));
+        std::memcpy(blob.b, s + off, n);
+        kk::upload_blob_kernel<<<1, 1024, 0, static_cast<cudaStream_t>(stream)>>>(d + off, blob, n);
+        if (int rc = kk::check_launch("upload_blob_kernel")) return rc;
+    }
     return KK_OK;
 }
 

@@ -290,6 +290,40 @@ __global__ void sum_int_kernel(const int* __restrict__ v, int64_t n, unsigned lo
     if ((threadIdx.x & 31) == 0 && acc) atomicAdd(out, acc);
 }
 
+// Device-driven fixpoint iteration (kk_ddlms_solve): the pass mode lives in
+// device memory, every kernel of an iteration reads it and a done frame's
+// remaining (pre-queued) iterations return at once; the host reads the
+// control block back once per batch of iterations instead of once per pass.
+constexpr int kModeDecision = 0, kModeOutput = 1, kModeDone = 2;
+constexpr int kMaxStatIters = 64;
+struct ReadBack {
+    unsigned long long ctr[4];   // [0] changed blocks, [1] blocks re-run, [2] guard sum, [3] list length
+    int ctl[4];                  // [0] mode, [1] iterations run
+    unsigned long long it_stats[2 * kMaxStatIters];   // per iteration (changed, re-run)
+    float Tend[16];              // end taps of the frame (scaled)
+};
+
+__device__ __forceinline__ bool ctl_done(const int* ctl) { return ctl && *ctl == kModeDone; }
+
+// end of one iteration: record its counts, pick the next pass (decision
+// passes until nothing changes, then one output pass; an output pass that
+// changes nothing ends the frame)
+__global__ void ddlms_advance_kernel(ReadBack* rb) {
+    const int mode = rb->ctl[0];
+    if (mode == kModeDone) return;
+    const unsigned long long ch = rb->ctr[0], rr = rb->ctr[1];
+    const int it = rb->ctl[1];
+    if (it < kMaxStatIters) {
+        rb->it_stats[2 * it] = ch;
+        rb->it_stats[2 * it + 1] = rr;
+    }
+    rb->ctl[1] = it + 1;
+    rb->ctl[0] = ch ? kModeDecision : (mode == kModeOutput ? kModeDone : kModeOutput);
+    rb->ctr[0] = 0;
+    rb->ctr[1] = 0;
+    rb->ctr[3] = 0;
+}
+
 struct Vec16 {
     float v[16];
 };
@@ -379,7 +413,13 @@ __global__ void __launch_bounds__(kBlockThreads, WITH_P ? KK_DD_MINB_P : KK_DD_M
 ddlms_block_kernel(SolveArgs a, Slicer sl, const float* __restrict__ Tstart, float* __restrict__ Pb,
                    float* __restrict__ maxx2, RunOut o, TOut to, int64_t b_lo, int64_t b_hi, int use_skip,
                    float soft_tol, const int* __restrict__ list, const unsigned long long* __restrict__ list_n,
-                   int write_out) {
+                   int write_out, const int* __restrict__ ctl) {
+    if (ctl) {   // device-driven pass mode
+        const int mode = *ctl;
+        if (mode == kModeDone) return;
+        write_out = mode == kModeOutput;
+        if (!write_out) soft_tol = 3.0e38f;
+    }
     __shared__ float2 pts[64];
     __shared__ uint8_t grid[64];
     extern __shared__ float4 dyn_sm[];
@@ -692,7 +732,16 @@ ddlms_block_kernel(SolveArgs a, Slicer sl, const float* __restrict__ Tstart, flo
 __global__ void ddlms_select_kernel(const float* __restrict__ Tstart, const float* __restrict__ Tused,
                                     const float* __restrict__ margin, const float* __restrict__ maxx2, float mu,
                                     int64_t b_lo, int64_t nb, float tol, const float* __restrict__ Twritten,
-                                    int* __restrict__ list, unsigned long long* __restrict__ list_n) {
+                                    int* __restrict__ list, unsigned long long* __restrict__ list_n,
+                                    const int* __restrict__ ctl) {
+    if (ctl) {   // device-driven pass mode: output passes check Twritten against tol
+        const int mode = *ctl;
+        if (mode == kModeDone) return;
+        if (mode != kModeOutput) {
+            Twritten = nullptr;
+            tol = 3.0e38f;
+        }
+    }
     const int64_t b = b_lo + int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     bool run = false;
     if (b < nb) {
@@ -770,7 +819,9 @@ __device__ __forceinline__ void stage_children(const float* __restrict__ Pc, con
 
 __global__ void __launch_bounds__(32 * kScanWarps)
 scan_fold_kernel(const float* __restrict__ Pc, const float* __restrict__ Qc, int64_t n_child, int G,
-                 float* __restrict__ Pg, float* __restrict__ Qg, int64_t n_grp, int with_p) {
+                 float* __restrict__ Pg, float* __restrict__ Qg, int64_t n_grp, int with_p,
+                 const int* __restrict__ ctl) {
+    if (ctl_done(ctl)) return;
     __shared__ float sP[kScanWarps][64];
     __shared__ float sQ[kScanWarps][16];
     __shared__ float cP[kScanWarps][32][65];
@@ -818,7 +869,9 @@ scan_fold_kernel(const float* __restrict__ Pc, const float* __restrict__ Qc, int
 // group (lanes 0..15 own T entries); children staged in smem first
 __global__ void __launch_bounds__(32 * kScanWarps)
 scan_down_kernel(const float* __restrict__ Pc, const float* __restrict__ Qc, int64_t n_child, int G,
-                 const float* __restrict__ Tg, int64_t n_grp, float* __restrict__ Tc) {
+                 const float* __restrict__ Tg, int64_t n_grp, float* __restrict__ Tc,
+                 const int* __restrict__ ctl) {
+    if (ctl_done(ctl)) return;
     __shared__ float sT[kScanWarps][16];
     __shared__ float cP[kScanWarps][32][65];
     __shared__ float cQ[kScanWarps][32][17];
@@ -1139,13 +1192,13 @@ Layout plan(int64_t nsym, int B) {
     b += align_up(L.nb * 16 * sizeof(float));   // Tused
     b += align_up(L.nb * 16 * sizeof(float));   // Twritten
     b += align_up(L.nb * sizeof(float)) * 2;    // margin, maxx2
-    b += align_up(16 * sizeof(float)) * 2;      // Tend, Tinit
+    b += align_up(16 * sizeof(float));          // Tinit
     b += align_up(L.nb * sizeof(int));          // over
     b += align_up(L.nb * sizeof(unsigned long long));   // label hashes
     b += align_up(size_t(nsym) * 8);                     // ST (soft, unless bound to the caller's)
     b += align_up(size_t(nsym));                         // LT (labels, idem)
     b += align_up(L.nb * sizeof(int));                   // re-run list
-    b += align_up(4 * sizeof(unsigned long long));
+    b += align_up(sizeof(ReadBack));                     // counters, pass control, end taps
     L.bytes = b;
     return L;
 }
@@ -1187,6 +1240,8 @@ struct DdlmsSolver {
     float2* ST_own = nullptr;    // workspace soft / labels (outputs not bound)
     uint8_t* LT_own = nullptr;
     int* list;
+    ReadBack* rb;
+    const int* ctl_d = nullptr;   // device pass control while a device-driven loop is queued
     int64_t bt = 0;      // pure training blocks
     int64_t ntb = 0;     // blocks holding any training symbol
     bool speculated = false;
@@ -1197,7 +1252,7 @@ struct DdlmsSolver {
         for (int l = 1; l <= top; ++l) {
             const unsigned g = static_cast<unsigned>((lv[l].n + kScanWarps - 1) / kScanWarps);
             scan_fold_kernel<<<g, wblk, 0, s>>>(lv[l - 1].P, lv[l - 1].Q, lv[l - 1].n, kG, lv[l].P, lv[l].Q,
-                                                lv[l].n, with_p ? 1 : 0);
+                                                lv[l].n, with_p ? 1 : 0, ctl_d);
             if (int rc = check_launch("scan_fold_kernel")) return rc;
         }
         return KK_OK;
@@ -1205,12 +1260,12 @@ struct DdlmsSolver {
     int scan_down() {   // from Tinit_d (frame start, scaled)
         const unsigned wblk = 32 * kScanWarps;
         scan_down_kernel<<<1, wblk, 0, s>>>(lv[top].P, lv[top].Q, lv[top].n, static_cast<int>(lv[top].n), Tinit_d, 1,
-                                            lv[top].T);
+                                            lv[top].T, ctl_d);
         if (int rc = check_launch("scan_down_kernel")) return rc;
         for (int l = top; l >= 1; --l) {
             const unsigned g = static_cast<unsigned>((lv[l].n + kScanWarps - 1) / kScanWarps);
             scan_down_kernel<<<g, wblk, 0, s>>>(lv[l - 1].P, lv[l - 1].Q, lv[l - 1].n, kG, lv[l].T, lv[l].n,
-                                                lv[l - 1].T);
+                                                lv[l - 1].T, ctl_d);
             if (int rc = check_launch("scan_down_kernel")) return rc;
         }
         return KK_OK;
@@ -1289,7 +1344,7 @@ struct DdlmsSolver {
             const size_t smem = train_blocks ? kStageSmem + kTrainSmem : kStageSmem;
             auto go = [&](auto kern) {
                 kern<<<g, kBlockThreads, smem, s>>>(a, sl, lv[0].T, lv[0].P, maxx2, o, to, lo, hi, skip, tol, lst,
-                                                    lst_n, write_out);
+                                                    lst_n, write_out, with_p ? nullptr : ctl_d);
             };
 #define KK_DD_GO3(P_, S_, T_) (al ? go(ddlms_block_kernel<P_, S_, true, T_>) : go(ddlms_block_kernel<P_, S_, false, T_>))
 #define KK_DD_GO(P_, S_) (train_blocks ? KK_DD_GO3(P_, S_, true) : KK_DD_GO3(P_, S_, false))
@@ -1317,7 +1372,7 @@ struct DdlmsSolver {
             // compact the blocks to re-run so that warps only carry live chains
             const unsigned g = static_cast<unsigned>((b1 - d0 + 127) / 128);
             ddlms_select_kernel<<<g, 128, 0, s>>>(lv[0].T, Tused, margin, maxx2, a.mu, d0, b1, tol,
-                                                  write_out ? Twritten : nullptr, list, ctr + 3);
+                                                  (write_out || ctl_d) ? Twritten : nullptr, list, ctr + 3, ctl_d);
             if (int rc = check_launch("ddlms_select_kernel")) return rc;
             return launch(false, d0, b1, 0, list, ctr + 3);
         }
@@ -1349,7 +1404,6 @@ struct DdlmsSolver {
         Twritten = reinterpret_cast<float*>(w); w += align_up(L.nb * 16 * sizeof(float));
         margin = reinterpret_cast<float*>(w); w += align_up(L.nb * sizeof(float));
         maxx2 = reinterpret_cast<float*>(w); w += align_up(L.nb * sizeof(float));
-        Tend = reinterpret_cast<float*>(w); w += align_up(16 * sizeof(float));
         Tinit_d = reinterpret_cast<float*>(w); w += align_up(16 * sizeof(float));
         over = reinterpret_cast<int*>(w); w += align_up(L.nb * sizeof(int));
         hsh = reinterpret_cast<unsigned long long*>(w); w += align_up(L.nb * 8);
@@ -1358,7 +1412,9 @@ struct DdlmsSolver {
         to.ST = ST_own;
         to.LT = LT_own;
         list = reinterpret_cast<int*>(w); w += align_up(L.nb * sizeof(int));
-        ctr = reinterpret_cast<unsigned long long*>(w);
+        rb = reinterpret_cast<ReadBack*>(w);
+        ctr = rb->ctr;
+        Tend = rb->Tend;
         // the block kernels work on the raw input with the scale folded into
         // the taps: T' = s T, mu' = mu s^2 (y = T' x_raw == T (s x_raw))
         a.x = static_cast<const float2*>(x);
@@ -1410,7 +1466,9 @@ struct DdlmsSolver {
             if (int rc = scan_up(true)) return rc;
             if (int rc = scan_down()) return rc;
         }
-        if (T_train_end) {
+        if (T_train_end && bt == 0) {   // no training blocks: the start taps themselves
+            for (int i = 0; i < 16; ++i) T_train_end[i] = T_start[i];
+        } else if (T_train_end) {
             float Tt[16];
             if (bt < L.nb) {
                 if (int rc = d2h_small(Tt, lv[0].T + bt * 16, sizeof(Tt), s)) return rc;
@@ -1465,6 +1523,82 @@ struct DdlmsSolver {
         return frame_map(agg);
     }
 
+    // Up to max_iter fixpoint iterations from the exact frame start taps,
+    // queued in batches with the pass mode kept on the device (see
+    // ddlms_advance_kernel): one host readback per batch, not per pass.  On
+    // convergence the guard count and end taps come back in the same read.
+    int solve_loop(const float* T_start, int max_iter, int64_t* it_stats, bool* converged, int64_t* guard,
+                   float* T_final) {
+        if (!speculated) return set_error(KK_ERR_PARAM, "speculate() must precede solve_loop()");
+        if (int rc = set_start(T_start)) return rc;
+        if (cudaMemsetAsync(ctr, 0, 4 * sizeof(unsigned long long), s) != cudaSuccess ||
+            cudaMemsetAsync(rb->ctl, 0, sizeof(rb->ctl), s) != cudaSuccess)
+            return set_cuda_error("solve_loop init");
+        *converged = false;
+        ReadBack h;
+        int queued = 0;
+        int batch = 4;   // the bench streams converge in 4 iterations
+        ctl_d = rb->ctl;
+        while (queued < max_iter) {
+            const int n = std::min(batch, max_iter - queued);
+            int rc = KK_OK;
+            for (int i = 0; i < n && rc == KK_OK; ++i) {
+                rc = scan_down();
+                if (rc == KK_OK) rc = run_blocks(false, 0, L.nb, 1, soft_tol, 1);
+                if (rc == KK_OK) rc = scan_up(false);
+                if (rc == KK_OK) {
+                    ddlms_advance_kernel<<<1, 1, 0, s>>>(rb);
+                    rc = check_launch("ddlms_advance_kernel");
+                }
+            }
+            if (rc == KK_OK) {
+                const int64_t gblocks = std::min<int64_t>((L.nb + 127) / 128, 148 * 8);
+                if (cudaMemsetAsync(ctr + 2, 0, sizeof(unsigned long long), s) != cudaSuccess) {
+                    rc = set_cuda_error("ctr");
+                } else {
+                    sum_int_kernel<<<static_cast<unsigned>(gblocks), 128, 0, s>>>(over, L.nb, ctr + 2);
+                    rc = check_launch("sum_int_kernel");
+                }
+            }
+            if (rc == KK_OK) rc = d2h_small(&h, rb, sizeof(h), s);
+            if (rc != KK_OK) {
+                ctl_d = nullptr;
+                return rc;
+            }
+            queued += n;
+            batch = 8;
+            if (h.ctl[0] == kModeDone) break;
+        }
+        ctl_d = nullptr;
+        const int it = h.ctl[1];
+        iters += it;
+        for (int i = 0; i < std::min(it, kMaxStatIters); ++i) {
+            reruns += static_cast<int64_t>(h.it_stats[2 * i + 1]);
+            if (it_stats && i < 16) {
+                it_stats[2 * i] = static_cast<int64_t>(h.it_stats[2 * i]);
+                it_stats[2 * i + 1] = static_cast<int64_t>(h.it_stats[2 * i + 1]);
+            }
+        }
+        if (it > 0 && it <= kMaxStatIters) last_changed = static_cast<int64_t>(h.it_stats[2 * (it - 1)]);
+        *converged = h.ctl[0] == kModeDone;
+        if (*converged) {
+            if (guard) *guard = static_cast<int64_t>(h.ctr[2]);
+            if (T_final)
+                for (int i = 0; i < 16; ++i) T_final[i] = h.Tend[i] / scale;
+        }
+        return KK_OK;
+    }
+
+    int copy_outputs(uint8_t* labels, float2* soft) {
+        if (labels && labels != to.LT &&
+            cudaMemcpyAsync(labels, to.LT, size_t(a.nsym), cudaMemcpyDeviceToDevice, s) != cudaSuccess)
+            return set_cuda_error("labels copy");
+        if (soft && soft != to.ST &&
+            cudaMemcpyAsync(soft, to.ST, size_t(a.nsym) * 8, cudaMemcpyDeviceToDevice, s) != cudaSuccess)
+            return set_cuda_error("soft copy");
+        return KK_OK;
+    }
+
     // chained exact fallback from block 0 (start taps already in lv[0].T[0])
     int chain(uint8_t* labels, float2* soft) {
         o.labels = labels;
@@ -1475,12 +1609,7 @@ struct DdlmsSolver {
     }
 
     int finish(uint8_t* labels, float2* soft, float* T_final, int64_t* guard) {
-        if (labels && labels != to.LT &&
-            cudaMemcpyAsync(labels, to.LT, size_t(a.nsym), cudaMemcpyDeviceToDevice, s) != cudaSuccess)
-            return set_cuda_error("labels copy");
-        if (soft && soft != to.ST &&
-            cudaMemcpyAsync(soft, to.ST, size_t(a.nsym) * 8, cudaMemcpyDeviceToDevice, s) != cudaSuccess)
-            return set_cuda_error("soft copy");
+        if (int rc = copy_outputs(labels, soft)) return rc;
         return end_state(T_final, guard);
     }
     int end_state(float* T_final, int64_t* guard) {
@@ -1585,20 +1714,12 @@ extern "C" int kk_ddlms_solve(const void* x, int64_t nsym, float scale, const vo
     if (int rc = sv.speculate(sv.bt > 0 ? Tg : T_init, nullptr)) return rc;
     int64_t st[6] = {0, 0, 0, 0, 0, sv.L.nb};
     bool converged = false;
-    bool soft_pass = false;   // decision passes until nothing changes, then one soft refresh
-    for (int it = 1; it <= max_iter; ++it) {
-        int64_t ch = 0, rr = 0;
-        if (int rc = sv.iterate(T_init, &ch, &rr, nullptr, soft_pass)) return rc;
-        if (stats && it <= 16) {
-            stats[6 + 2 * (it - 1)] = ch;
-            stats[7 + 2 * (it - 1)] = rr;
-        }
-        if (ch == 0 && soft_pass) { converged = true; break; }
-        soft_pass = (ch == 0);
-    }
     int64_t guard = 0;
+    // decision passes until nothing changes, then one output pass (device-driven)
+    if (int rc = sv.solve_loop(T_init, max_iter, stats ? stats + 6 : nullptr, &converged, &guard, T_final))
+        return rc;
     if (converged) {
-        if (int rc = sv.finish(labels, static_cast<float2*>(soft), T_final, &guard)) return rc;
+        if (int rc = sv.copy_outputs(labels, static_cast<float2*>(soft))) return rc;
     } else {
         st[2] = 2;
         if (int rc = sv.chain(labels, static_cast<float2*>(soft))) return rc;

@@ -15,7 +15,7 @@ from . import _lib
 from .constellation import make_constellation
 from .metrics import (SyncFailure, count_bit_errors, evm, frame_sync, q_from_ber, windowed_q,
                       windowed_q_from_counts)
-from .rxdsp import side_stream
+from .rxdsp import _upload, side_stream
 from .rxdsp import (
     DdlmsConfig, GpuOptions, RxPipeline, RxPipelineConfig, compute_static_taps, demap, design_receive_taps,
 )
@@ -279,7 +279,7 @@ def _stream_receiver(cfg, reference_symbols, n: int, chunk_samples: int, dev):
         ref = np.asarray(reference_symbols, np.complex128)[:cfg.ddlms.startup_symbols]
         pts = make_constellation(order).points
         ti = np.argmin(np.abs(ref[:, None] - pts[None, :]), axis=1).astype(np.uint8)
-        st["train_idx"] = torch.from_numpy(ti).to(dev)
+        st["train_idx"] = _upload(ti, dev)
         st["n_train"] = len(ti)
     return st
 
@@ -329,20 +329,34 @@ def _receive_host_stream(cfg, host_codes, half_lsb, reference_symbols, chunk_sam
     d2h = side_stream(dev, "d2h")
     if staging is None or staging.numel() < n:
         staging = torch.empty(n, dtype=torch.int16, device=dev)
-    # the pipeline's own uploads go first: later small H2D copies would queue
-    # behind the bulk transfers on the in-order host->device copy engine
+    starts = list(range(0, n, chunk_samples))
+    ready = [torch.cuda.Event(enable_timing=trace is not None) for _ in starts]
+    copy.wait_stream(comp)          # the staging buffer's previous readers
+    if trace is not None:
+        import time
+
+        ev0 = torch.cuda.Event(enable_timing=True)
+        ev0.record(copy)
+        trace.append(("copy_start", time.perf_counter(), ev0))
+
+    def queue_copies(lo, hi):
+        with torch.cuda.stream(copy):
+            for i in range(lo, hi):
+                a = starts[i]
+                m = min(chunk_samples, n - a)
+                staging[a:a + m].copy_(host_codes[a:a + m], non_blocking=True)
+                ready[i].record(copy)
+
+    # Every chunk's copy is queued first; the pipeline's set-up overlaps
+    # them.  Its table uploads travel as kernel parameters (kk_upload): a DMA
+    # copy issued now would wait for the whole queued stream on the
+    # host->device copy engine.
+    if bits_host is None:   # (pinned allocation before the copies are queued)
+        k = make_constellation(cfg.constellation_order).bits_per_symbol
+        bits_host = torch.empty(_bits_capacity(cfg, n, k), dtype=torch.uint8, pin_memory=True)
+    queue_copies(0, len(starts))
     st = _stream_receiver(cfg, reference_symbols, n, chunk_samples, dev)
     pipe, cfg = st["pipe"], st["cfg"]
-    starts = list(range(0, n, chunk_samples))
-    ready = [torch.cuda.Event() for _ in starts]
-    copy.wait_stream(comp)          # the staging buffer's previous readers (and the uploads)
-    with torch.cuda.stream(copy):
-        for i, a in enumerate(starts):
-            m = min(chunk_samples, n - a)
-            staging[a:a + m].copy_(host_codes[a:a + m], non_blocking=True)
-            ready[i].record(copy)
-    if bits_host is None:
-        bits_host = torch.empty(_bits_capacity(cfg, n, st["k"]), dtype=torch.uint8, pin_memory=True)
     for i, a in enumerate(starts):
         m = min(chunk_samples, n - a)
         comp.wait_event(ready[i])

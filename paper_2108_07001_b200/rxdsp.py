@@ -42,6 +42,8 @@ from fractions import Fraction
 
 import numpy as np
 
+import os as _os
+
 from . import _lib
 from ._lib import SyncError
 from .constellation import ConstellationSpec, make_constellation, slicer_tables
@@ -125,10 +127,15 @@ class GpuOptions:
     DDLMS work (and output transfer) is left once the last input arrives."""
 
     ddlms_block: int = 512
+    # smaller frames (stream tails) use smaller blocks, down to this size:
+    # B = clamp(2^floor(log2(nsym / 2^15)), ddlms_block_min, ddlms_block) --
+    # a pass costs ~B sequential symbol steps of latency, which a small frame
+    # cannot hide (measured: 2^22-symbol frame 0.47 ms at B=128, 0.61 at 512)
+    ddlms_block_min: int = 128
     ddlms_frame_symbols: int = 1 << 28
     ddlms_max_iter: int = 64
     ddlms_soft_tol: float = 1e-5
-    ddlms_tail_min_symbols: int = 1 << 24
+    ddlms_tail_min_symbols: int = 1 << 22
     # run the DDLMS frames on a worker thread / CUDA stream so the front end
     # of later chunks overlaps them (streaming receive, harness.receive_host_stream)
     ddlms_async: bool = False
@@ -189,6 +196,18 @@ def _stream(dev=None) -> int:
 
 def _ptr(t) -> int:
     return t.data_ptr() if t is not None else 0
+
+
+def _upload(a: np.ndarray, dev):
+    """Small host array -> device tensor, ordered on the current stream via
+    kk_upload (kernel parameters): a DMA copy issued while a streaming
+    receive's bulk input copies are queued would wait for all of them."""
+    torch = _torch()
+    a = np.ascontiguousarray(a)
+    t = torch.empty(a.shape, dtype=torch.from_numpy(a[:0]).dtype, device=dev)
+    if a.nbytes:
+        _lib.call("kk_upload", t.data_ptr(), a.ctypes.data, a.nbytes, _stream(dev))
+    return t
 
 
 def _tone_rotation(tone_hz: float, fs: float):
@@ -272,8 +291,6 @@ def _as_device_input(x, dev):
 
 
 # NVTX ranges around the pipeline stages (KK_NVTX=1; for nsys/ncu range filters)
-import os as _os
-
 _NVTX = _os.environ.get("KK_NVTX", "0") == "1"
 
 _SIDE_STREAMS = {}
@@ -523,9 +540,8 @@ def refine_static_taps(input_2sps, training_symbols, n_taps: int = 203, rate_hz:
 # ---------------------------------------------------------------------------
 
 def _h_split(h: np.ndarray, dev):
-    torch = _torch()
-    he = torch.from_numpy(np.ascontiguousarray(h[0::2]).astype(np.complex64)).to(dev)
-    ho = torch.from_numpy(np.ascontiguousarray(h[1::2]).astype(np.complex64)).to(dev)
+    he = _upload(h[0::2].astype(np.complex64), dev)
+    ho = _upload(h[1::2].astype(np.complex64), dev)
     return he, ho
 
 
@@ -711,7 +727,7 @@ class RxPipeline:
             self._ref_len = len(reference_symbols)
             n_keep = max(cfg.sync_symbols, cfg.ddlms.startup_symbols)
             self.reference = np.asarray(reference_symbols[:n_keep], np.complex128)
-            self._ref_dev = torch.from_numpy(self.reference.astype(np.complex64)).to(self.dev)
+            self._ref_dev = _upload(self.reference.astype(np.complex64), self.dev)
         taps = cfg.static_taps if cfg.static_taps is not None else FirFilter(np.array([1.0 + 0j]), cfg.adc_rate_hz / 2.0)
         self._taps = taps
         self._aa_delay = cfg.static_plan.fft_size // 4
@@ -719,7 +735,7 @@ class RxPipeline:
         self._h_even, self._h_odd = _h_split(self._resp, self.dev)
         p, q, tab = _tone_rotation(cfg.tone_freq_hz, cfg.adc_rate_hz)
         self._rot_p, self._rot_q = p, q
-        self._rot_tab = torch.from_numpy(tab).to(self.dev) if tab is not None else None
+        self._rot_tab = _upload(tab, self.dev) if tab is not None else None
         self._spec = make_constellation(cfg.constellation_order)
         self._tables = slicer_tables(cfg.constellation_order)
 
@@ -763,6 +779,7 @@ class RxPipeline:
         self._train_total = 0
         self._sym_done = 0
         self._expected_symbols = None     # set by expect(): geometric DDLMS tail
+        self._expected_chunk = None
         import collections
         self._async = bool(getattr(self.gpu, "ddlms_async", False))
         self._jobs = collections.deque()  # submitted asynchronous frames, in order
@@ -935,7 +952,8 @@ class RxPipeline:
         use_solve = (d.widely_linear and d.n_taps == 4 and not self._frozen and self._div_count == 0)
         stats = {"k0": k0, "nsym": nsym, "mode": "solve" if use_solve else "sequential"}
         if use_solve:
-            B = int(self.gpu.ddlms_block)
+            B = self._frame_block(nsym)
+            stats["block"] = B
             wsb = int(_lib.load().kk_ddlms_workspace_bytes(nsym, B))
             if self._ws is None or self._ws.numel() < wsb:
                 if self._async:
@@ -1006,7 +1024,7 @@ class RxPipeline:
         # device memory is allocated here, on the host thread's stream (the
         # caching allocator pools per stream); the worker marks its use
         nsym = k1 - k0
-        wsb = int(_lib.load().kk_ddlms_workspace_bytes(nsym, int(self.gpu.ddlms_block)))
+        wsb = int(_lib.load().kk_ddlms_workspace_bytes(nsym, self._frame_block(nsym)))
         if self._ws is None or self._ws.numel() < wsb:
             self._wait_frames()          # the worker may still use the old workspace
             self._ws = None
@@ -1091,6 +1109,12 @@ class RxPipeline:
             k0 = self._sym_done
             k1 = self._frame_end(k0)
             solve = self._submit_frame if self._async else self._solve_frame
+            if flush:
+                # nothing follows a flush: a short remainder (e.g. the grid
+                # lead) joins this frame instead of forming its own
+                total = (n_q - self.cfg.ddlms.n_taps) // 2 + 1 if n_q >= self.cfg.ddlms.n_taps else 0
+                if k0 < k1 < total and total - k1 < int(self.gpu.ddlms_frame_symbols) // 4:
+                    k1 = total
             if n_q >= 2 * k1 + 2:
                 solve(k0, k1)
                 continue
@@ -1100,22 +1124,46 @@ class RxPipeline:
                     solve(k0, total)
             break
 
+    def _frame_block(self, nsym: int) -> int:
+        """DDLMS block size of an nsym-symbol frame (GpuOptions.ddlms_block_min)."""
+        B = int(self.gpu.ddlms_block)
+        lo = min(B, max(1, int(self.gpu.ddlms_block_min)))
+        fit = 1 << max(0, (int(nsym) >> 15).bit_length() - 1)
+        return max(lo, min(B, fit))
+
     def _frame_end(self, k0: int) -> int:
         """End of the DDLMS frame starting at symbol k0: the next multiple of
         F (global grid, independent of the feed chunking); inside the last
         grid frame of an announced stream (expect), geometric halves of the
         remainder down to ddlms_tail_min_symbols (multiples of the block)."""
         F = int(self.gpu.ddlms_frame_symbols)
-        k1 = (k0 // F + 1) * F
+        lead = self._frame_lead(F)
+        k1 = ((k0 + lead) // F + 1) * F - lead
         T = self._expected_symbols
-        if T is None or k1 < T:
+        if T is None or T - k0 > F + lead:
             return k1
-        B = int(self.gpu.ddlms_block)
-        fmin = max(B, int(self.gpu.ddlms_tail_min_symbols))
+        # the last grid frame (with the lead's remainder) is split on the tail grid: multiples of fmin (>= one feed chunk's symbols, so
+        # that only the last chunk's frame is left when the flush arrives)
+        fmin = max(int(self.gpu.ddlms_block), int(self.gpu.ddlms_tail_min_symbols))
+        if self._expected_chunk:
+            fmin = max(fmin, 1 << (max(1, self._expected_chunk // self.cfg.sps_in) - 1).bit_length())
         rem = T - k0
         if rem <= 2 * fmin:
-            return k1
-        return k0 + max(fmin, (rem // 2) // B * B)
+            return max(k1, T)
+        lead = self._frame_lead(fmin)
+        end = ((k0 + lead + rem // 2) // fmin) * fmin - lead
+        return end if k0 < end and T - end >= fmin else max(k1, T)
+
+    def _frame_lead(self, grid: int) -> int:
+        """Frames end `lead` symbols before their grid points: more than the
+        front end holds back (KK block, carrier segment, static block, sync
+        offset), so a frame's input is complete as soon as the feed holding
+        its grid point is processed -- not one feed later.  0 on fine grids."""
+        cfg = self.cfg
+        lead = ((cfg.kk_plan.fft_size + cfg.carrier_segment_len + cfg.static_plan.fft_size) // cfg.sps_in
+                + (cfg.sync_wait_samples + 2 * cfg.sync_symbols) // 2 + 1024)
+        lead = -(-lead // 1024) * 1024
+        return lead if 4 * lead <= grid else 0
 
     # -- public API (rx:768-824) ---------------------------------------------
 
@@ -1174,10 +1222,20 @@ class RxPipeline:
         F = int(self.gpu.ddlms_frame_symbols)
         # symbols the stream will end with (upper bound: 4 samples / symbol)
         self._expected_symbols = int(n_samples) // 4
+        self._expected_chunk = int(chunk_samples) if chunk_samples else None
         # asynchronous frames keep their input live until solved: hold the
         # whole announced stream (a window slide would wait for the worker)
         y2_cap = n_samples // 2 if self._async else min(n_samples // 2, 2 * F + 2 * self.cfg.static_plan.hop)
         self._y2.ensure_capacity(y2_cap + 16)
+        if self._async and self.cfg.ddlms.n_taps == 4:
+            # the largest frame's solver workspace up front: growing it later
+            # would wait for the worker's frames in flight
+            nmax = max(1, min(F + self._frame_lead(F), self._expected_symbols + 1))
+            wsb = int(_lib.load().kk_ddlms_workspace_bytes(nmax, self._frame_block(nmax)))
+            if self._ws is None or self._ws.numel() < wsb:
+                self._wait_frames()
+                self._ws = None
+                self._ws = _torch().empty(wsb, dtype=_torch().uint8, device=self.dev)
         c = chunk_samples or n_samples
         self._z.ensure_capacity(min(n_samples, c + 2 * self.cfg.carrier_segment_len + self.cfg.static_plan.hop))
 

@@ -16,6 +16,9 @@ frame = 1 << int(sys.argv[3]) if len(sys.argv) > 3 else 1 << 28
 cap = load_capture("c5_qpsk_10000km_tile")
 codes, _ = tile(cap, 1 << log2n)
 cfg = cap.pipeline_config(ddlms_frame_symbols=frame)
+if len(sys.argv) > 4:
+    import dataclasses
+    cfg = dataclasses.replace(cfg, gpu=dataclasses.replace(cfg.gpu, ddlms_tail_min_symbols=1 << int(sys.argv[4])))
 ref = cap.symbols()[:10000]
 dev = torch.device("cuda", 0)
 host = torch.from_numpy(codes).pin_memory()
@@ -38,9 +41,53 @@ def _wrap(name):
     setattr(rxdsp.RxPipeline, name, g)
 
 
-for _n in ("_run_kk", "_run_carrier", "_run_static", "_run_ddlms", "drain_device", "_submit_frame", "_wait_frames"):
+from paper_2108_07001_b200 import harness  # noqa: E402
+
+
+def _wrap_mod(mod, name):
+    f = getattr(mod, name)
+
+    def g(*a, **k):
+        t = time.perf_counter()
+        try:
+            return f(*a, **k)
+        finally:
+            HT.setdefault(name, []).append(time.perf_counter() - t)
+    setattr(mod, name, g)
+
+
+_wrap_mod(harness, "_stream_receiver")
+from paper_2108_07001_b200 import _lib  # noqa: E402
+_orig_call = _lib.call
+
+
+def _timed_call(name, *a):
+    t = time.perf_counter()
+    try:
+        return _orig_call(name, *a)
+    finally:
+        dt = time.perf_counter() - t
+        if dt > 5e-4:
+            HT.setdefault("lib:" + name, []).append(dt)
+
+
+_lib.call = _timed_call
+_orig_sync = rxdsp._sync_device
+
+
+def _sync_dbg(head, ref, skip, dev):
+    t = time.perf_counter()
+    e = torch.cuda.Event()
+    e.record(torch.cuda.current_stream(dev))
+    e.synchronize()
+    HT.setdefault("sync:stream_before", []).append(time.perf_counter() - t)
+    return _orig_sync(head, ref, skip, dev)
+
+
+rxdsp._sync_device = _sync_dbg
+for _n in ("__init__", "expect", "_do_sync", "_run_kk", "_run_carrier", "_run_static", "_run_ddlms", "drain_device", "_submit_frame", "_wait_frames"):
     _wrap(_n)
-for rep in range(3):
+for rep in range(4):
     HT.clear()
     tr = []
     ms0 = torch.cuda.memory_stats()
@@ -58,15 +105,23 @@ for rep in range(3):
           "device allocs", ms1.get("num_device_alloc", 0) - ms0.get("num_device_alloc", 0),
           "frees", ms1.get("num_device_free", 0) - ms0.get("num_device_free", 0),
           "retries", ms1.get("num_alloc_retries", 0) - ms0.get("num_alloc_retries", 0))
-    if rep == 2:
+    if rep in (1, 3):
         for item in tr:
+            if item[0] == "mark":
+                print(f"  mark {item[1]} @ {t0.elapsed_time(item[3]):8.2f} host @ {1e3 * (item[2] - h0):8.2f}")
+                continue
+            if item[0] == "copy_start":
+                print(f"  copies start @ {t0.elapsed_time(item[2]):8.2f} host @ {1e3 * (item[1] - h0):8.2f}")
+                continue
             if item[0] == "d2h":
                 print(f"  d2h done @ {t0.elapsed_time(item[2]):8.2f} host @ {1e3 * (item[1] - h0):8.2f}")
                 continue
             i, ht, rd, fe, nj = item
-            print(f"  chunk {i:3d}: fed @ {t0.elapsed_time(fe):8.2f} "
+            print(f"  chunk {i:3d}: copied @ {t0.elapsed_time(rd):8.2f} fed @ {t0.elapsed_time(fe):8.2f} "
                   f"host @ {1e3 * (ht - h0):8.2f} pending {nj}")
         print("  stats", [(s["k0"], s["nsym"], s.get("iterations")) for s in pipe.ddlms_stats])
+        for name, e0, e1 in evs[:8]:
+            print(f"  first events: {name} start {t0.elapsed_time(e0):8.2f} end {t0.elapsed_time(e1):8.2f}")
         for name, e0, e1 in pipe._events:
             if name == "ddlms" and e1.query():
                 try:
