@@ -164,16 +164,53 @@ class GpuFrameSolver:
         self.ws = None
 
 
-def receive_rank(cfg, adc, reference_prefix, job: SuperframeJob, dist) -> SuperframeResult:
+def _front_end_host(pipe, adc, chunk_samples: int, flush: bool, dev) -> None:
+    """Front end of a pinned-host shard, chunk by chunk: every chunk's H2D
+    copy is queued up front on a side stream (into one device staging
+    buffer), the front end of each chunk waits only for its own copy."""
+    import torch
+
+    from .rxdsp import side_stream
+    from .sigcore import AdcCodes
+
+    codes = adc.codes
+    n = int(codes.shape[0])
+    comp = torch.cuda.current_stream(dev)
+    copy = side_stream(dev, "h2d")
+    staging = torch.empty(n, dtype=torch.int16, device=dev)
+    starts = list(range(0, n, chunk_samples))
+    ready = [torch.cuda.Event() for _ in starts]
+    copy.wait_stream(comp)
+    with torch.cuda.stream(copy):
+        for i, a in enumerate(starts):
+            m = min(chunk_samples, n - a)
+            staging[a:a + m].copy_(codes[a:a + m], non_blocking=True)
+            ready[i].record(copy)
+    pipe.expect(n, chunk_samples)
+    for i, a in enumerate(starts):
+        m = min(chunk_samples, n - a)
+        comp.wait_event(ready[i])
+        pipe.front_end(AdcCodes(staging[a:a + m], adc.half_lsb, adc.sample_rate_hz), flush=flush and i == len(starts) - 1)
+    staging.record_stream(comp)
+
+
+def receive_rank(cfg, adc, reference_prefix, job: SuperframeJob, dist, chunk_samples: int | None = None
+                 ) -> SuperframeResult:
     """Receive this rank's super-frame of a multi-GPU stream."""
     import torch
+
+    from .sigcore import AdcCodes
 
     dev = _device()
     comm = TorchComm(dist, dev)
     hop = cfg.static_plan.hop
     pipe = RxPipeline(cfg, reference_symbols=reference_prefix if job.rank == 0 else None,
                       stream_offset=job.load_start, static_start_hop=job.core_start // hop)
-    pipe.front_end(adc, flush=job.last)
+    if (chunk_samples and isinstance(adc, AdcCodes) and isinstance(adc.codes, torch.Tensor)
+            and not adc.codes.is_cuda):
+        _front_end_host(pipe, adc, int(chunk_samples), job.last, dev)
+    else:
+        pipe.front_end(adc, flush=job.last)
     # ---- sync + eq scale on rank 0 (stream head), broadcast ----
     info = np.zeros(4)
     if job.rank == 0:

@@ -64,9 +64,12 @@ class SuperframeResult:
         return self.pipe.stage_seconds if self.pipe is not None else {}
 
 
-def receive_superframe(cfg, adc, reference_prefix, job: SuperframeJob, dist=None) -> SuperframeResult:
+def receive_superframe(cfg, adc, reference_prefix, job: SuperframeJob, dist=None,
+                       chunk_samples: int | None = None) -> SuperframeResult:
     """Receive this rank's super-frame.  adc: AdcCodes / ndarray / CUDA tensor
-    covering [job.load_start, job.load_end)."""
+    covering [job.load_start, job.load_end).  Multi-rank with AdcCodes over a
+    pinned HOST tensor and chunk_samples: the shard is ingested chunk by chunk
+    (H2D copies overlapped with the front end)."""
     from .rxdsp import RxPipeline
 
     if job.world == 1:
@@ -76,4 +79,4 @@ def receive_superframe(cfg, adc, reference_prefix, job: SuperframeJob, dist=None
         pipe.release_buffers()
         return SuperframeResult(labels, soft, meta[0][0] if meta else 0, pipe, pipe.ddlms_stats, pipe.sync_offset)
     from .multirank import receive_rank
-    return receive_rank(cfg, adc, reference_prefix, job, dist)
+    return receive_rank(cfg, adc, reference_prefix, job, dist, chunk_samples=chunk_samples)

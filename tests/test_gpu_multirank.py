@@ -27,7 +27,7 @@ def _stream():
     return cap, codes, syms
 
 
-def _worker(rank, world, port, q):
+def _worker(rank, world, port, q, host_chunk=None):
     import torch.distributed as dist
 
     os.environ["MASTER_ADDR"] = "127.0.0.1"
@@ -42,7 +42,10 @@ def _worker(rank, world, port, q):
         cfg = cap.pipeline_config()
         job = plan_superframe(rank, world, SPR)
         ref = cap.symbols()[:10000]
-        r = receive_superframe(cfg, AdcCodes(codes[job.load_start:job.load_end], cap.half_lsb), ref, job, dist=dist)
+        shard = codes[job.load_start:job.load_end]
+        if host_chunk:       # pinned host shard, chunked ingest (the bench's e2e leg at N > 1)
+            shard = torch.from_numpy(np.ascontiguousarray(shard)).pin_memory()
+        r = receive_superframe(cfg, AdcCodes(shard, cap.half_lsb), ref, job, dist=dist, chunk_samples=host_chunk)
         q.put((rank, r.first_symbol, r.labels.cpu().numpy(), r.ddlms_stats))
     finally:
         dist.destroy_process_group()
@@ -56,7 +59,8 @@ def _port():
     return p
 
 
-def test_two_rank_superframes_equal_single_rank():
+@pytest.mark.parametrize("host_chunk", [None, 300_000])
+def test_two_rank_superframes_equal_single_rank(host_chunk):
     import torch.multiprocessing as mp
 
     from paper_2108_07001_b200.sigcore import AdcCodes
@@ -65,7 +69,7 @@ def test_two_rank_superframes_equal_single_rank():
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _port()
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, q, host_chunk)) for r in range(2)]
     for p in procs:
         p.start()
     res = sorted([q.get(timeout=600) for _ in range(2)], key=lambda t: t[0])
