@@ -238,7 +238,8 @@ def receive_host_stream(cfg, host_codes, half_lsb: float, reference_symbols, chu
     compute stream waits per chunk on its copy event, and the bits of every
     completed DDLMS frame go back on a third stream as they are released --
     both PCIe directions overlap the GPU work.  `staging` (optional) is a
-    reusable int16 device buffer of >= n samples.
+    reusable int16 device buffer of >= n samples.  The DDLMS tail frames
+    are aligned to the chunk ends (RxPipeline.expect(chunk_ends=...)).
     Returns (pipe, bits_host, n_symbols_decided).
     """
     import torch
@@ -257,7 +258,7 @@ def receive_host_stream(cfg, host_codes, half_lsb: float, reference_symbols, chu
     return out
 
 
-def _stream_receiver(cfg, reference_symbols, n: int, chunk_samples: int, dev):
+def _stream_receiver(cfg, reference_symbols, n: int, chunk_samples: int, dev, chunk_ends=None):
     """Pipeline + output packing state of a streaming receive (shared by the
     pinned-host and raw-file ingest paths)."""
     import dataclasses
@@ -271,7 +272,7 @@ def _stream_receiver(cfg, reference_symbols, n: int, chunk_samples: int, dev):
     gpu = dataclasses.replace(cfg.gpu, ddlms_async=True)
     cfg = dataclasses.replace(cfg, gpu=gpu)
     pipe = RxPipeline(cfg, reference_symbols=reference_symbols, device=dev)
-    pipe.expect(n, chunk_samples)
+    pipe.expect(n, chunk_samples, chunk_ends=chunk_ends)
     order = cfg.constellation_order
     st = {"cfg": cfg, "pipe": pipe, "order": order, "k": make_constellation(order).bits_per_symbol,
           "tb": slicer_tables(order), "train_idx": None, "n_train": 0, "n_out": 0, "b_out": 0}
@@ -329,7 +330,10 @@ def _receive_host_stream(cfg, host_codes, half_lsb, reference_symbols, chunk_sam
     d2h = side_stream(dev, "d2h")
     if staging is None or staging.numel() < n:
         staging = torch.empty(n, dtype=torch.int16, device=dev)
+    # (feeding the last chunk in smaller pieces was measured slower: the
+    # DDLMS tail frames then form a longer chain of ~0.5 ms frame latencies)
     starts = list(range(0, n, chunk_samples))
+    sizes = [b - a for a, b in zip(starts, starts[1:] + [n])]
     ready = [torch.cuda.Event(enable_timing=trace is not None) for _ in starts]
     copy.wait_stream(comp)          # the staging buffer's previous readers
     if trace is not None:
@@ -342,8 +346,7 @@ def _receive_host_stream(cfg, host_codes, half_lsb, reference_symbols, chunk_sam
     def queue_copies(lo, hi):
         with torch.cuda.stream(copy):
             for i in range(lo, hi):
-                a = starts[i]
-                m = min(chunk_samples, n - a)
+                a, m = starts[i], sizes[i]
                 staging[a:a + m].copy_(host_codes[a:a + m], non_blocking=True)
                 ready[i].record(copy)
 
@@ -355,10 +358,11 @@ def _receive_host_stream(cfg, host_codes, half_lsb, reference_symbols, chunk_sam
         k = make_constellation(cfg.constellation_order).bits_per_symbol
         bits_host = torch.empty(_bits_capacity(cfg, n, k), dtype=torch.uint8, pin_memory=True)
     queue_copies(0, len(starts))
-    st = _stream_receiver(cfg, reference_symbols, n, chunk_samples, dev)
+    st = _stream_receiver(cfg, reference_symbols, n, chunk_samples, dev, chunk_ends=[a + m for a, m in
+                                                                                   zip(starts, sizes)])
     pipe, cfg = st["pipe"], st["cfg"]
     for i, a in enumerate(starts):
-        m = min(chunk_samples, n - a)
+        m = sizes[i]
         comp.wait_event(ready[i])
         pipe.feed(AdcCodes(staging[a:a + m], half_lsb, cfg.adc_rate_hz), flush=i == len(starts) - 1)
         if trace is not None:

@@ -780,6 +780,8 @@ class RxPipeline:
         self._sym_done = 0
         self._expected_symbols = None     # set by expect(): geometric DDLMS tail
         self._expected_chunk = None
+        self._tail_ends = None            # symbol positions of announced feed ends
+        self._tail_gap = 0
         import collections
         self._async = bool(getattr(self.gpu, "ddlms_async", False))
         self._jobs = collections.deque()  # submitted asynchronous frames, in order
@@ -1142,12 +1144,24 @@ class RxPipeline:
         T = self._expected_symbols
         if T is None or T - k0 > F + lead:
             return k1
-        # the last grid frame (with the lead's remainder) is split on the tail grid: multiples of fmin (>= one feed chunk's symbols, so
+        rem = T - k0
+        if self._tail_ends:
+            # announced feed boundaries: halve the remainder at the boundary
+            # (minus the lead) nearest below the middle, so each tail frame
+            # is complete as soon as its feed is processed and the last one
+            # holds only the last feed
+            lead_t = self._frame_lead(self._tail_gap)
+            ends = [e - lead_t for e in self._tail_ends if k0 < e - lead_t < T]
+            if not ends:
+                return max(k1, T)
+            below = [e for e in ends if e <= k0 + rem // 2]
+            return below[-1] if below else ends[0]
+        # otherwise the last grid frame (with the lead's remainder) is split on
+        # the tail grid: multiples of fmin (>= one feed chunk's symbols, so
         # that only the last chunk's frame is left when the flush arrives)
         fmin = max(int(self.gpu.ddlms_block), int(self.gpu.ddlms_tail_min_symbols))
         if self._expected_chunk:
             fmin = max(fmin, 1 << (max(1, self._expected_chunk // self.cfg.sps_in) - 1).bit_length())
-        rem = T - k0
         if rem <= 2 * fmin:
             return max(k1, T)
         lead = self._frame_lead(fmin)
@@ -1215,14 +1229,22 @@ class RxPipeline:
         if flush:
             self._flushed = True
 
-    def expect(self, n_samples: int, chunk_samples: int | None = None) -> None:
+    def expect(self, n_samples: int, chunk_samples: int | None = None, chunk_ends=None) -> None:
         """Capacity hint for a stream of n_samples fed in chunks of
         chunk_samples: pre-sizes the 2-sps buffer for one DDLMS frame and the
-        KK output window, so streaming feeds never re-grow device buffers."""
+        KK output window, so streaming feeds never re-grow device buffers.
+        chunk_ends (optional): the sample positions where the feeds will end;
+        the DDLMS tail frames are then aligned to them."""
         F = int(self.gpu.ddlms_frame_symbols)
         # symbols the stream will end with (upper bound: 4 samples / symbol)
         self._expected_symbols = int(n_samples) // 4
         self._expected_chunk = int(chunk_samples) if chunk_samples else None
+        if chunk_ends is not None:
+            e = sorted({int(v) for v in chunk_ends if 0 < int(v) < n_samples})
+            sps = self.cfg.sps_in
+            self._tail_ends = [v // sps for v in e]
+            gaps = [b - a for a, b in zip([0] + e, e + [int(n_samples)])]
+            self._tail_gap = min(gaps) // sps if gaps else 0
         # asynchronous frames keep their input live until solved: hold the
         # whole announced stream (a window slide would wait for the worker)
         y2_cap = n_samples // 2 if self._async else min(n_samples // 2, 2 * F + 2 * self.cfg.static_plan.hop)
