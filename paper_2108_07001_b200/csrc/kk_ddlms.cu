@@ -25,6 +25,8 @@
 // sequential chain.
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <vector>
@@ -1703,6 +1705,19 @@ extern "C" int kk_ddlms_solve(const void* x, int64_t nsym, float scale, const vo
     clear_error();
     (void)guard_run;
     if (nsym <= 0) return KK_OK;
+    // KK_DDLMS_TRACE=1: per-phase device times of each solve on stderr
+    static const bool trace = [] {
+        const char* e = std::getenv("KK_DDLMS_TRACE");
+        return e && e[0] == '1';
+    }();
+    cudaEvent_t ev[5] = {};
+    auto mark = [&](int i) {
+        if (trace) {
+            if (!ev[i]) cudaEventCreate(&ev[i]);
+            cudaEventRecord(ev[i], static_cast<cudaStream_t>(stream));
+        }
+    };
+    mark(0);
     DdlmsSolver sv;
     if (int rc = make_solver(sv, x, nsym, scale, train, n_train, order, pts_host, grid_host, grid_m, norm,
                              max_radius, guard_factor, mu, block, soft_tol, workspace, ws_bytes,
@@ -1711,13 +1726,25 @@ extern "C" int kk_ddlms_solve(const void* x, int64_t nsym, float scale, const vo
     sv.bind_outputs(labels, static_cast<float2*>(soft));
     float Tg[16];
     if (int rc = sv.train(T_init, Tg)) return rc;
+    mark(1);
     if (int rc = sv.speculate(sv.bt > 0 ? Tg : T_init, nullptr)) return rc;
+    mark(2);
     int64_t st[6] = {0, 0, 0, 0, 0, sv.L.nb};
     bool converged = false;
     int64_t guard = 0;
     // decision passes until nothing changes, then one output pass (device-driven)
     if (int rc = sv.solve_loop(T_init, max_iter, stats ? stats + 6 : nullptr, &converged, &guard, T_final))
         return rc;
+    mark(3);
+    if (trace) {
+        cudaEventSynchronize(ev[3]);
+        float t[3];
+        for (int i = 0; i < 3; ++i) cudaEventElapsedTime(&t[i], ev[i], ev[i + 1]);
+        std::fprintf(stderr, "[kk_ddlms_solve] nsym %lld B %d: init+train %.3f ms, speculate %.3f ms, loop %.3f ms\n",
+                     static_cast<long long>(nsym), block, t[0], t[1], t[2]);
+        for (cudaEvent_t e : ev)
+            if (e) cudaEventDestroy(e);
+    }
     if (converged) {
         if (int rc = sv.copy_outputs(labels, static_cast<float2*>(soft))) return rc;
     } else {

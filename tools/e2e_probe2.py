@@ -61,8 +61,19 @@ from paper_2108_07001_b200 import _lib  # noqa: E402
 _orig_call = _lib.call
 
 
+SOLVES = []
+
+
 def _timed_call(name, *a):
     t = time.perf_counter()
+    if name == "kk_ddlms_solve":
+        ea, eb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ea.record(torch.cuda.current_stream())
+        try:
+            return _orig_call(name, *a)
+        finally:
+            eb.record(torch.cuda.current_stream())
+            SOLVES.append((t, time.perf_counter(), ea, eb, a[1]))
     try:
         return _orig_call(name, *a)
     finally:
@@ -120,6 +131,9 @@ for rep in range(4):
             print(f"  chunk {i:3d}: copied @ {t0.elapsed_time(rd):8.2f} fed @ {t0.elapsed_time(fe):8.2f} "
                   f"host @ {1e3 * (ht - h0):8.2f} pending {nj}")
         print("  stats", [(s["k0"], s["nsym"], s.get("iterations")) for s in pipe.ddlms_stats])
+        for (ht0, ht1, ea, eb, ns) in SOLVES[-4:]:
+            print(f"  solve nsym {ns}: gpu {t0.elapsed_time(ea):8.2f} - {t0.elapsed_time(eb):8.2f}  "
+                  f"host {1e3 * (ht0 - h0):8.2f} - {1e3 * (ht1 - h0):8.2f}")
         for name, e0, e1 in evs[:8]:
             print(f"  first events: {name} start {t0.elapsed_time(e0):8.2f} end {t0.elapsed_time(e1):8.2f}")
         for name, e0, e1 in pipe._events:
