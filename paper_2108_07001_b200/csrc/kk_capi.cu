@@ -123,11 +123,19 @@ extern "C" int kk_device_sync(void) {
 // ---------------------------------------------------------------------------
 namespace kk {
 constexpr int kUpBlob = 16384;
-struct UpBlob {
+struct alignas(16) UpBlob {
     unsigned char b[kUpBlob];
 };
-__global__ void upload_blob_kernel(unsigned char* __restrict__ dst, const UpBlob blob, int nbytes) {
-    for (int i = threadIdx.x; i < nbytes; i += blockDim.x) dst[i] = blob.b[i];
+// __grid_constant__: indexed straight from the parameter bank (a plain by-
+// value struct indexed dynamically is first copied to local memory per thread)
+__global__ void upload_blob_kernel(unsigned char* __restrict__ dst, const __grid_constant__ UpBlob blob,
+                                   int nbytes) {
+    const int i = threadIdx.x * 16;
+    if ((reinterpret_cast<uintptr_t>(dst) & 15) == 0 && i + 16 <= nbytes) {
+        *reinterpret_cast<uint4*>(dst + i) = *reinterpret_cast<const uint4*>(blob.b + i);
+    } else {
+        for (int k = i; k < min(i + 16, nbytes); ++k) dst[k] = blob.b[k];
+    }
 }
 }  // namespace kk
 
@@ -142,7 +150,7 @@ extern "C" int kk_upload(void* dst, const void* src, int64_t bytes, void* stream
     for (int64_t off = 0; off < bytes; off += kk::kUpBlob) {
         const int n = static_cast<int>(std::min<int64_t>(kk::kUpBlob, bytes - off));
         std::memcpy(blob.b, s + off, n);
-        kk::upload_blob_kernel<<<1, 1024, 0, static_cast<cudaStream_t>(stream)>>>(d + off, blob, n);
+        kk::upload_blob_kernel<<<1, kk::kUpBlob / 16, 0, static_cast<cudaStream_t>(stream)>>>(d + off, blob, n);
         if (int rc = kk::check_launch("upload_blob_kernel")) return rc;
     }
     return KK_OK;
