@@ -179,6 +179,7 @@ struct RunOut {
     int* over;        // [nb] guard exceedances in the block's latest run
     unsigned long long* hash;  // [nb] hash of the block's latest label sequence
     unsigned long long* counters;  // [0] changed decisions, [1] blocks re-run
+    unsigned int* first_changed;   // lowest block index whose decisions changed (atomicMin)
 };
 
 // Run blocks [b_lo, b_hi) starting from Tstart[b] (or chain them when chain != 0:
@@ -301,6 +302,8 @@ constexpr int kMaxStatIters = 64;
 struct ReadBack {
     unsigned long long ctr[4];   // [0] changed blocks, [1] blocks re-run, [2] guard sum, [3] list length
     int ctl[4];                  // [0] mode, [1] iterations run
+    unsigned int first_changed;  // lowest changed block of the running iteration (~0: none)
+    unsigned int last_first;     // the same for the last finished iteration
     unsigned long long it_stats[2 * kMaxStatIters];   // per iteration (changed, re-run)
     float Tend[16];              // end taps of the frame (scaled)
 };
@@ -321,6 +324,8 @@ __global__ void ddlms_advance_kernel(ReadBack* rb) {
     }
     rb->ctl[1] = it + 1;
     rb->ctl[0] = ch ? kModeDecision : (mode == kModeOutput ? kModeDone : kModeOutput);
+    rb->last_first = rb->first_changed;
+    rb->first_changed = 0xffffffffu;
     rb->ctr[0] = 0;
     rb->ctr[1] = 0;
     rb->ctr[3] = 0;
@@ -715,13 +720,17 @@ ddlms_block_kernel(SolveArgs a, Slicer sl, const float* __restrict__ Tstart, flo
         }
     }
     unsigned long long rr = run ? 1ull : 0ull;
+    const unsigned first = __reduce_min_sync(0xffffffffu, changed ? static_cast<unsigned>(b) : 0xffffffffu);
 #pragma unroll
     for (int off_ = 16; off_ > 0; off_ >>= 1) {
         changed += __shfl_xor_sync(0xffffffffu, changed, off_);
         rr += __shfl_xor_sync(0xffffffffu, rr, off_);
     }
     if (lane == 0) {
-        if (changed) atomicAdd(o.counters + 0, changed);
+        if (changed) {
+            atomicAdd(o.counters + 0, changed);
+            atomicMin(o.first_changed, first);
+        }
         if (rr) atomicAdd(o.counters + 1, rr);
     }
 }
@@ -1248,6 +1257,7 @@ struct DdlmsSolver {
     int64_t ntb = 0;     // blocks holding any training symbol
     bool speculated = false;
     int64_t iters = 0, reruns = 0, last_changed = 0;
+    unsigned int last_first_changed = 0;   // lowest changed block of the last iteration (solve_loop)
 
     int scan_up(bool with_p) {
         const unsigned wblk = 32 * kScanWarps;
@@ -1437,12 +1447,14 @@ struct DdlmsSolver {
         o.over = over;
         o.hash = hsh;
         o.counters = ctr;
+        o.first_changed = &rb->first_changed;
         bt = std::min<int64_t>(n_train / block, L.nb);
         ntb = std::min<int64_t>((n_train + block - 1) / block, L.nb);
         if (cudaMemsetAsync(over, 0, L.nb * sizeof(int), s) != cudaSuccess ||
             cudaMemsetAsync(hsh, 0, L.nb * 8, s) != cudaSuccess ||
             cudaMemsetAsync(Twritten, 0xFF, L.nb * 16 * sizeof(float), s) != cudaSuccess ||   // NaN: never written
-            cudaMemsetAsync(ctr, 0, 4 * sizeof(unsigned long long), s) != cudaSuccess)
+            cudaMemsetAsync(ctr, 0, 4 * sizeof(unsigned long long), s) != cudaSuccess ||
+            cudaMemsetAsync(&rb->first_changed, 0xFF, 2 * sizeof(unsigned int), s) != cudaSuccess)
             return set_cuda_error("solver init");
         return KK_OK;
     }
@@ -1534,7 +1546,8 @@ struct DdlmsSolver {
         if (!speculated) return set_error(KK_ERR_PARAM, "speculate() must precede solve_loop()");
         if (int rc = set_start(T_start)) return rc;
         if (cudaMemsetAsync(ctr, 0, 4 * sizeof(unsigned long long), s) != cudaSuccess ||
-            cudaMemsetAsync(rb->ctl, 0, sizeof(rb->ctl), s) != cudaSuccess)
+            cudaMemsetAsync(rb->ctl, 0, sizeof(rb->ctl), s) != cudaSuccess ||
+            cudaMemsetAsync(&rb->first_changed, 0xFF, 2 * sizeof(unsigned int), s) != cudaSuccess)
             return set_cuda_error("solve_loop init");
         *converged = false;
         ReadBack h;
@@ -1583,6 +1596,7 @@ struct DdlmsSolver {
         }
         if (it > 0 && it <= kMaxStatIters) last_changed = static_cast<int64_t>(h.it_stats[2 * (it - 1)]);
         *converged = h.ctl[0] == kModeDone;
+        last_first_changed = h.last_first;
         if (*converged) {
             if (guard) *guard = static_cast<int64_t>(h.ctr[2]);
             if (T_final)
@@ -1602,11 +1616,28 @@ struct DdlmsSolver {
     }
 
     // chained exact fallback from block 0 (start taps already in lv[0].T[0])
-    int chain(uint8_t* labels, float2* soft) {
+    // Non-converged frame: blocks before the lowest block m whose decisions
+    // changed in the last iteration ran from exact start taps with exact
+    // decisions (induction from the exact frame start: none of them changed,
+    // so the scan reproduces their starts).  They get an output pass from
+    // those starts; the sequential chain covers [m, nb) only.
+    int chain(uint8_t* labels, float2* soft, int64_t m = 0) {
+        m = std::max<int64_t>(0, std::min<int64_t>(m, L.nb));
         o.labels = labels;
         o.soft = soft;
         if (int rc = scan_down()) return rc;
-        ddlms_run_kernel<<<1, 1, 0, s>>>(a, sl, lv[0].T, maxx2, o, 0, L.nb, 0, soft_tol, 1, 1);
+        if (m > 0) {
+            if (int rc = run_blocks(false, 0, m, 1, soft_tol, 1)) return rc;
+            const size_t n0 = static_cast<size_t>(std::min<int64_t>(m * a.B, a.nsym));
+            if (labels && labels != to.LT &&
+                cudaMemcpyAsync(labels, to.LT, n0, cudaMemcpyDeviceToDevice, s) != cudaSuccess)
+                return set_cuda_error("labels copy");
+            if (soft && soft != to.ST &&
+                cudaMemcpyAsync(soft, to.ST, n0 * 8, cudaMemcpyDeviceToDevice, s) != cudaSuccess)
+                return set_cuda_error("soft copy");
+        }
+        if (m >= L.nb) return KK_OK;
+        ddlms_run_kernel<<<1, 1, 0, s>>>(a, sl, lv[0].T, maxx2, o, m, L.nb, 0, soft_tol, 1, 1);
         return check_launch("ddlms_run_kernel chain");
     }
 
@@ -1749,7 +1780,7 @@ extern "C" int kk_ddlms_solve(const void* x, int64_t nsym, float scale, const vo
         if (int rc = sv.copy_outputs(labels, static_cast<float2*>(soft))) return rc;
     } else {
         st[2] = 2;
-        if (int rc = sv.chain(labels, static_cast<float2*>(soft))) return rc;
+        if (int rc = sv.chain(labels, static_cast<float2*>(soft), sv.last_first_changed)) return rc;
         if (int rc = sv.end_state(T_final, &guard)) return rc;
     }
     st[0] = sv.iters;
