@@ -1134,10 +1134,12 @@ class RxPipeline:
         return max(lo, min(B, fit))
 
     def _frame_end(self, k0: int) -> int:
-        """End of the DDLMS frame starting at symbol k0: the next multiple of
-        F (global grid, independent of the feed chunking); inside the last
-        grid frame of an announced stream (expect), geometric halves of the
-        remainder down to ddlms_tail_min_symbols (multiples of the block)."""
+        """End of the DDLMS frame starting at symbol k0: the next point of the
+        global grid m*F - lead (independent of the feed chunking; `lead`
+        covers the front end's hold-back, see _frame_lead); inside the last
+        grid frame of an announced stream (expect), halves of the remainder
+        at the announced feed ends, else on a grid of max(one chunk's
+        symbols, ddlms_tail_min_symbols)."""
         F = int(self.gpu.ddlms_frame_symbols)
         lead = self._frame_lead(F)
         k1 = ((k0 + lead) // F + 1) * F - lead
