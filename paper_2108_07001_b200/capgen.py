@@ -121,6 +121,10 @@ class GenParams:
     adc_bits: int
     aa_hz: float
     aa_order: int
+    # OSNR noise loading of the streaming back-to-back front end (runner.py
+    # _StreamingFrontend, hr:257-264) instead of per-span ASE; None: off
+    osnr_db: float | None = None
+    obpf_enabled: bool = True
 
     @classmethod
     def from_config(cls, c: dict) -> "GenParams":
@@ -194,6 +198,8 @@ class CaptureGenerator:
         fp = half * 0.95
         af = np.abs(f)
         ob = np.where(af <= fp, 1.0, np.where(af < half, 0.5 * (1 + np.cos(np.pi * (af - fp) / (half - fp))), 0.0))
+        if not p.obpf_enabled:
+            ob = np.ones_like(af)
         # the zero-phase / symmetric responses are delayed by half the overlap
         # so they are causal inside the overlap-save window
         delay = np.exp(-2j * np.pi * f * (self.ov // 2) / fs)
@@ -240,6 +246,11 @@ class CaptureGenerator:
             # EDFAs restore the total power: signal share shrinks by the noise share
             self.scale_sig *= np.sqrt(max(launch_mw - sig2, 0.0) / launch_mw)
             self.noise_std = np.sqrt(sig2 / 2.0)
+            if p.osnr_db is not None:
+                # white field noise at the OSNR (12.5 GHz reference bandwidth)
+                # relative to the total (signal + carrier) power, hr:257-264
+                density = ps * (1.0 + 10.0 ** (p.cspr_db / 10.0)) / (10.0 ** (p.osnr_db / 10.0) * 12.5e9)
+                self.noise_std = np.sqrt(density * p.sim_rate_hz / 2.0) * self.scale_sig
         k = torch.arange(self.sim_pos, self.sim_pos + n, device=self.dev, dtype=torch.int64)
         ph = 2.0 * np.pi * ((k * self.tone_p) % self.tone_q).to(torch.float64) / self.tone_q
         field = y + (self.amp_tone * torch.polar(torch.ones_like(ph), ph)).to(torch.complex64)

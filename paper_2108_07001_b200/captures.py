@@ -70,7 +70,8 @@ class Capture:
 
 
 def list_captures() -> list[str]:
-    return sorted(f[:-5] for f in os.listdir(GOLDEN) if f.endswith(".json"))
+    return sorted(f[:-5] for f in os.listdir(GOLDEN)
+                  if f.endswith(".json") and os.path.exists(os.path.join(GOLDEN, f[:-5] + ".npz")))
 
 
 def load_capture(name: str, directory: str = GOLDEN) -> Capture:

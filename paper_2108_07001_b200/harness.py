@@ -12,7 +12,7 @@ from __future__ import annotations
 import numpy as np
 
 from . import _lib
-from .constellation import make_constellation
+from .constellation import make_constellation, slicer_tables
 from .metrics import (SyncFailure, count_bit_errors, evm, frame_sync, q_from_ber, windowed_q,
                       windowed_q_from_counts)
 from .rxdsp import _upload, side_stream
@@ -50,6 +50,151 @@ def receive_stream(adc, pipe_cfg: RxPipelineConfig, reference_symbols) -> RxPipe
     for start in range(0, len(x), blen):
         pipe.feed(x[start:start + blen])
     return pipe
+
+
+def _namespace(d):
+    """Attribute view of an ExperimentConfig.to_dict() layout."""
+    from types import SimpleNamespace
+
+    if isinstance(d, dict):
+        return SimpleNamespace(**{k: _namespace(v) for k, v in d.items()})
+    return d
+
+
+def bench_throughput(cfg, n_samples: int, repeats: int = 3) -> dict:
+    """Wall-clock throughput of the receiver chain over pre-generated input
+    (runner.py:370-415, same arguments, errors and result keys).  `cfg` is an
+    ExperimentConfig (anything with .to_dict()) or its dict layout.
+
+    As in the reference, the input is a back-to-back capture of
+    buffer_len/4 symbols tiled to n_samples (content does not change the
+    arithmetic; the tiled decisions are meaningless).  Here the capture is
+    generated on the GPU (capgen: the reference's TX/PD/ADC model) and stays
+    resident in HBM as int16 wire codes; each repeat feeds it buffer by
+    buffer through a fresh RxPipeline and finishes it (decisions returned to
+    the host), timed with the device synchronised."""
+    import copy
+    import time
+
+    import torch
+
+    from . import capgen
+    from .sigcore import AdcCodes
+
+    c = copy.deepcopy(cfg.to_dict() if hasattr(cfg, "to_dict") else cfg)
+    blen = int(c["rx"]["buffer_len"])
+    if n_samples < 4 * blen:
+        raise ValueError("need at least 4 buffers of samples")
+    c["tx"]["n_symbols"] = blen // 4
+    c["link"].update(n_spans=1, span_length_km=0.0, ase_enabled=False)
+    gen = capgen.CaptureGenerator(capgen.GenParams.from_config(c), seed=int(c.get("seed", 0)))
+    codes, half_lsb, idx, _ = gen.generate(blen // 4)
+    reps = -(-n_samples // int(codes.shape[0]))
+    stream = codes.repeat(reps)[:n_samples].contiguous()
+    ref = make_constellation(c["tx"]["constellation_order"]).points[np.tile(idx, reps)[:n_samples // 4]]
+    ns = _namespace(c)
+    link = _namespace({"total_dispersion_ps_nm": 0.0, "center_wavelength_nm": c["link"]["center_wavelength_nm"]})
+    pipe_cfg = make_pipeline_config(ns, link)
+    results, last_pipe = [], None
+    for _ in range(repeats):
+        pipe = RxPipeline(pipe_cfg, reference_symbols=ref)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for start in range(0, n_samples, blen):
+            pipe.feed(AdcCodes(stream[start:start + blen], half_lsb, pipe_cfg.adc_rate_hz))
+        pipe.finish()
+        torch.cuda.synchronize()
+        elapsed = time.perf_counter() - t0
+        results.append(n_samples / elapsed)
+        last_pipe = pipe
+    sps = float(np.median(results))
+    stage = dict(last_pipe.stage_seconds)
+    return {
+        "samples_per_second": sps,
+        "ratio_to_adc_rate": sps / float(c["frontend"]["adc_rate_hz"]),
+        "repeats": results,
+        "stage_seconds": stage,
+        "stage_total_seconds": sum(stage.values()),
+        "wall_seconds_last": n_samples / results[-1],
+    }
+
+
+def run_sustained(cfg, n_adc_samples: int, osnr_db: float | None = None, chunk_symbols: int = 1 << 16) -> dict:
+    """Back-to-back contiguous streaming run with bounded memory
+    (runner.py:290-348, same arguments and result keys).  The ADC stream is
+    generated chunk by chunk on the GPU (capgen with the streaming front
+    end's model: RRC shaping, carrier, optional OSNR noise loading, PD + ADC
+    response, 12-bit quantizer; no dispersion, no phase noise, no OBPF),
+    each chunk is fed to the receiver and its released decisions are scored
+    against the transmitted PRBS bits; BER/Q over [startup + head guard,
+    n - tail guard) and the windowed-Q trace, as in the reference."""
+    import copy
+
+    import torch
+
+    from . import capgen
+
+    c = copy.deepcopy(cfg.to_dict() if hasattr(cfg, "to_dict") else cfg)
+    order = int(c["tx"]["constellation_order"])
+    spec = make_constellation(order)
+    k = spec.bits_per_symbol
+    n_symbols = int(n_adc_samples) // 4
+    c["tx"]["n_symbols"] = n_symbols
+    c["link"].update(n_spans=1, span_length_km=0.0, ase_enabled=False, phase_noise_linewidth_hz=0.0)
+    gp = capgen.GenParams.from_config(c)
+    gp.osnr_db = osnr_db
+    gp.obpf_enabled = False
+    seed = int(np.random.SeedSequence(int(c.get("seed", 0))).generate_state(4)[0])   # hr:41-48 "link"
+    gen = capgen.CaptureGenerator(gp, seed=seed)
+    rx = c["rx"]
+    n_ref = max(int(rx["sync_symbols"]), int(rx["startup_symbols"]))
+    per = gen.period_bits
+    ref_bits = np.take(per, np.arange(min(n_ref, n_symbols) * k) % len(per))
+    ref = spec.points[capgen.map_symbols(ref_bits, order)]
+    link = _namespace({"total_dispersion_ps_nm": 0.0, "center_wavelength_nm": c["link"]["center_wavelength_nm"]})
+    pipe_cfg = make_pipeline_config(_namespace(c), link)
+    pipe = RxPipeline(pipe_cfg, reference_symbols=ref)
+    dev = pipe.dev
+    labels, tx_idx = [], []
+    for start in range(0, n_symbols, chunk_symbols):
+        m = min(chunk_symbols, n_symbols - start)
+        adc, idx, _ = gen.next_chunk(m)
+        tx_idx.append(idx)
+        pipe.feed(adc)
+        lab, _, _ = pipe.drain_device(want_soft=False)
+        labels.append(lab)
+    pipe.feed(np.zeros(0), flush=True)
+    lab, _, _ = pipe.drain_device(want_soft=False)
+    labels.append(lab)
+    lab = torch.cat(labels)[:n_symbols]
+    txi = torch.from_numpy(np.concatenate(tx_idx)[:lab.shape[0]].astype(np.int64)).to(dev)
+    # decisions -> bits on the device (training symbols are the reference's)
+    dec_idx = torch.where(lab == 255, txi, lab.long())
+    pl = torch.from_numpy(slicer_tables(order).point_label[:order].astype(np.int64)).to(dev)
+    shifts = torch.arange(k - 1, -1, -1, device=dev)
+    rx_bits = (pl[dec_idx][:, None] >> shifts) & 1
+    tx_bits = (pl[txi][:, None] >> shifts) & 1
+    flags = (rx_bits != tx_bits).to(torch.uint8).reshape(-1).cpu().numpy()
+    error_flags = np.zeros(k * n_symbols, dtype=np.uint8)
+    error_flags[:len(flags)] = flags
+    m_cfg = c["metrics"]
+    head = int(rx["startup_symbols"]) + int(m_cfg["head_guard_symbols"])
+    stop_sym = n_symbols - int(m_cfg["tail_guard_symbols"])
+    region = error_flags[head * k:stop_sym * k]
+    n_errors = int(np.sum(region))
+    ber = n_errors / len(region)
+    series = windowed_q(region, float(c["tx"]["baud_hz"]) * k, float(m_cfg["windowed_q_window_s"]))
+    qs = [q for _, q in series]
+    return {
+        "n_symbols": int(stop_sym - head),
+        "n_bits": int(len(region)),
+        "n_errors": n_errors,
+        "ber": ber,
+        "q_db": q_from_ber(ber) if ber > 0 else np.inf,
+        "diverged": pipe.diverged,
+        "windowed_q": series,
+        "windowed_q_std_db": float(np.std(qs)) if len(qs) > 1 else 0.0,
+    }
 
 
 def measure_point(dec, soft, bits, syms, cfg) -> dict:

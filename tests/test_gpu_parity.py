@@ -620,3 +620,43 @@ def test_wrong_reference_raises_sync_error():
     with pytest.raises(ko.OracleSyncError):
         ref.feed(cap.adc_float(), flush=True)
         ref.finish()
+
+
+def test_bench_throughput_reports():
+    """harness.bench_throughput mirrors runner.py:370-415 (test_harness.py:
+    180-189): positive rate, ratio to the ADC rate, the five stage keys, and
+    stage time within the wall time of the last repeat."""
+    import copy
+
+    from paper_2108_07001_b200.harness import bench_throughput
+
+    cfg = copy.deepcopy(load_capture("c1_qpsk_b2b").meta["config"])
+    cfg["rx"]["buffer_len"] = 1 << 16
+    result = bench_throughput(cfg, n_samples=1 << 19, repeats=2)
+    assert result["samples_per_second"] > 0
+    assert result["ratio_to_adc_rate"] == pytest.approx(result["samples_per_second"] / 4e9)
+    assert set(result["stage_seconds"]) == {"kk", "carrier", "downshift", "static", "ddlms"}
+    assert result["stage_total_seconds"] <= result["wall_seconds_last"] * 1.05
+
+
+def test_run_sustained_ber_vs_reference():
+    """harness.run_sustained (runner.py:290-348) on the reference test's
+    configuration (16-QAM b2b, OSNR 22 dB, 2^21 samples): same result keys,
+    no divergence, and BER inside the statistical interval of the
+    reference's own run (tests/golden/harness/sustained_16qam_osnr22.json; the noise
+    realisations differ, so the bar is 4 sigma of the two binomial counts)."""
+    import json
+    import os
+
+    from paper_2108_07001_b200.harness import run_sustained
+
+    with open(os.path.join(os.path.dirname(__file__), "golden", "harness", "sustained_16qam_osnr22.json")) as f:
+        g = json.load(f)
+    ref = g["result"]
+    r = run_sustained(g["config"], g["n_adc_samples"], osnr_db=g["osnr_db"])
+    assert set(r) == set(ref)
+    assert not r["diverged"]
+    assert r["n_bits"] == ref["n_bits"] and len(r["windowed_q"]) == len(ref["windowed_q"])
+    sigma = np.sqrt(ref["n_errors"] + max(r["n_errors"], 1))
+    print("errors", r["n_errors"], "reference", ref["n_errors"], "ber", r["ber"], ref["ber"])
+    assert abs(r["n_errors"] - ref["n_errors"]) < 4 * sigma

@@ -129,3 +129,13 @@ def test_captures_index():
     assert cap.adc_h.dtype == np.int16 and np.all(cap.adc_h % 2 != 0)
     cfg = cap.pipeline_config()
     assert cfg.static_taps is not None and cfg.constellation_order == 4
+
+
+def test_bench_throughput_needs_enough_samples():
+    """runner.py:379-380 (test_harness.py:191-194): fewer than 4 buffers of
+    samples raise ValueError before any work."""
+    from paper_2108_07001_b200.harness import bench_throughput
+
+    cfg = load_capture("c1_qpsk_b2b").meta["config"]
+    with pytest.raises(ValueError):
+        bench_throughput(cfg, n_samples=1 << 10)
