@@ -66,19 +66,17 @@ __device__ __forceinline__ float load_in<double>(const double* p, int64_t i, flo
 // Hilbert multiplier on the full 1024-bin spectrum (Hermitian extension of
 // the rfft multiplier): k in [1,511]: (-j)^(k+1); k in [513,1023]:
 // conj((-j)^(1025-k)); 0 at DC and Nyquist.
+// Branch-free (the lanes of a pass hold different k: a switch diverged).
+// (-j)^e z for e = 0..3: (x, y), (y, -x), (-x, -y), (-y, x); the conjugated
+// multiplier (+j)^e is (-j)^{-e}.
 __device__ __forceinline__ float2 apply_mult(int k, float2 z) {
-    if (k == 0 || k == 512) return make_float2(0.f, 0.f);
-    int e;
-    bool conj_;
-    if (k < 512) { e = (k + 1) & 3; conj_ = false; }
-    else { e = (1025 - k) & 3; conj_ = true; }
-    // (-j)^e : 0 -> 1, 1 -> -j, 2 -> -1, 3 -> +j ; conj flips the sign of j
-    switch (e) {
-        case 0: return z;
-        case 1: return conj_ ? mul_pj(z) : mul_mj(z);
-        case 2: return make_float2(-z.x, -z.y);
-        default: return conj_ ? mul_mj(z) : mul_pj(z);
-    }
+    const int e = k < 512 ? ((k + 1) & 3) : ((k - 1025) & 3);     // (1025-k) conj -> -(1025-k)
+    const bool swap = e & 1;
+    const float a = swap ? z.y : z.x, b = swap ? z.x : z.y;
+    const float zero = (k & 511) == 0 ? 0.f : 1.f;                  // DC and Nyquist
+    const float sr = (e & 2) ? -zero : zero;
+    const float si = ((e + 1) & 2) ? -zero : zero;
+    return make_float2(a * sr, b * si);
 }
 
 template <typename TIn>
@@ -239,12 +237,16 @@ kk_pairs_kernel(const TIn* __restrict__ in, float in_scale, float clamp_rel, int
     unsigned rot_base = 0;
     const float inv_q = rot_q > 0 ? 1.0f / static_cast<float>(rot_q) : 0.f;
     const float two_pi_over_q = rot_q > 0 ? 6.283185307179586f / static_cast<float>(rot_q) : 0.f;
-    if (rot_q > 0 && active)
-        rot_base = static_cast<unsigned>((static_cast<unsigned long long>(n0_global + hop_a * kHop) % rot_q));
+    // (32-bit arithmetic: n0_global arrives reduced mod q, hop_a < 2^31)
+    if (rot_q > 0 && active) {
+        const unsigned Q = static_cast<unsigned>(rot_q);
+        rot_base = (static_cast<unsigned>(n0_global) + (static_cast<unsigned>(hop_a) % Q) * (512u % Q)) % Q;
+    }
     float2 rot_cache = make_float2(1.f, 0.f), r256 = rot_cache, r512 = rot_cache;
     if (rot_q > 0) {
-        r256 = __ldg(rot_tab + (256ll * rot_p) % rot_q);     // exp(-2 pi i (256 p mod q) / q)
-        r512 = __ldg(rot_tab + (512ll * rot_p) % rot_q);
+        const unsigned Q = static_cast<unsigned>(rot_q), Pp = static_cast<unsigned>(rot_p);
+        r256 = __ldg(rot_tab + (256u * Pp) % Q);     // exp(-2 pi i (256 p mod q) / q)
+        r512 = __ldg(rot_tab + (512u * Pp) % Q);
     }
     auto st_out = [&](int n, float2 v) {
         if (n < kHop) return;
@@ -334,11 +336,14 @@ static int launch_k1(const void* in, float in_scale, float clamp_rel, int64_t n_
     const size_t smem = sizeof(K1Smem);
     if (int rc = ensure_smem_attr(reinterpret_cast<const void*>(kk_pairs_kernel<TIn>), smem, "K1 smem attr"))
         return rc;
+    if (n_hops >= (int64_t(1) << 31)) return set_error(KK_ERR_PARAM, "n_hops must be < 2^31 per call");
     const int64_t pairs = (n_hops + 1) / 2;
     const int64_t grid = (pairs + kPairsPerCta - 1) / kPairsPerCta;
+    // the kernel only needs the stream index modulo the rotation period
+    const int64_t n0m = rot_q > 0 ? ((n0 % rot_q) + rot_q) % rot_q : 0;
     kk_pairs_kernel<TIn><<<static_cast<unsigned>(grid), kK1Threads, smem, s>>>(
         static_cast<const TIn*>(in), in_scale, clamp_rel, n_hops, st_u, st_a, st_dead, new_u, new_a, new_dead, out,
-        hop_sum, hop_dead, clamped, n0, rot_p, rot_q, rot_tab, mirror, tw);
+        hop_sum, hop_dead, clamped, n0m, rot_p, rot_q, rot_tab, mirror, tw);
     return check_launch("kk_pairs_kernel");
 }
 
