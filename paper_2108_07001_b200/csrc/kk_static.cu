@@ -304,19 +304,6 @@ __global__ void __launch_bounds__(kK2Threads, 1) static_blocks_kernel(K2Params p
     asm volatile("tcgen05.fence::after_thread_sync;\n");
     const uint32_t tmem_thread = tmem_base_sh + (static_cast<uint32_t>(32 * (warp & 3)) << 16) +
                                  static_cast<uint32_t>(64 * (warp >> 2));
-    // the second column's x0 half (16 x 8 B per thread) is copied into the
-    // (still unused) A buffer while the first column is transformed (K2
-    // 11.83 -> 11.71 ms per 2^30 samples: fewer global loads in flight when
-    // the second column starts)
-    if (FAST) {
-        const float2* zq1 = p.z + (bi.base - p.z_index0) + tid + kK2Threads;
-#pragma unroll
-        for (int r = 0; r < 16; ++r) {
-            const uint32_t sa = static_cast<uint32_t>(__cvta_generic_to_shared(S.A + r * kK2Threads + tid));
-            asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(zq1 + 1024 * r) : "memory");
-        }
-        asm volatile("cp.async.commit_group;\n" ::: "memory");
-    }
     for (int chain = 0; chain < 2; ++chain) {
         // ---- FFT16384 step 1: column n2 = j, DFT16 over n1 (stride 1024),
         //      W16384^{j k1}, -> row k1, position j ----
@@ -332,6 +319,20 @@ __global__ void __launch_bounds__(kK2Threads, 1) static_blocks_kernel(K2Params p
                     x0s = S.A + tid;
                 }
                 k2_load_column_ab<FAST>(p, bi, S.rot, j, mA, mB, bnd, s1024, s16384, v, taddr, x0s);
+                if (FAST && q == 0) {
+                    // the second column's x0 half (16 x 8 B per thread) is copied into
+                    // the (still unused) A buffer while the first column is transformed
+                    // (K2 11.83 -> 11.54 ms per 2^30 samples; issuing it before the first
+                    // column's loads gained less, also staging x1 into the FFT buffer lost)
+                    const float2* zq1 = p.z + (bi.base - p.z_index0) + tid + kK2Threads;
+#pragma unroll
+                    for (int r = 0; r < 16; ++r) {
+                        const uint32_t sa = static_cast<uint32_t>(__cvta_generic_to_shared(S.A + r * kK2Threads + tid));
+                        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(zq1 + 1024 * r)
+                                     : "memory");
+                    }
+                    asm volatile("cp.async.commit_group;\n" ::: "memory");
+                }
             } else {
                 float2 h0[8], h1[8];
                 tmem_ld16(taddr, h0);
