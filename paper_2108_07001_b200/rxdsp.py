@@ -135,7 +135,7 @@ class GpuOptions:
     ddlms_frame_symbols: int = 1 << 28
     ddlms_max_iter: int = 64
     ddlms_soft_tol: float = 1e-5
-    ddlms_tail_min_symbols: int = 1 << 22
+    ddlms_tail_min_symbols: int = 1 << 24
     # run the DDLMS frames on a worker thread / CUDA stream so the front end
     # of later chunks overlaps them (streaming receive, harness.receive_host_stream)
     ddlms_async: bool = False
@@ -1147,6 +1147,8 @@ class RxPipeline:
         if T is None or T - k0 > F + lead:
             return k1
         rem = T - k0
+        if rem <= 2 * max(int(self.gpu.ddlms_block), int(self.gpu.ddlms_tail_min_symbols)):
+            return max(k1, T)
         if self._tail_ends:
             # announced feed boundaries: halve the remainder at the boundary
             # (minus the lead) nearest below the middle, so each tail frame
