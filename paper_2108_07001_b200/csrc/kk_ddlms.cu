@@ -24,6 +24,7 @@
 // Guard trips, frozen state and non-convergence fall back to the exact
 // sequential chain.
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -1742,10 +1743,13 @@ extern "C" int kk_ddlms_solve(const void* x, int64_t nsym, float scale, const vo
         return e && e[0] == '1';
     }();
     cudaEvent_t ev[5] = {};
+    double host_ms[5] = {};
+    const auto h0 = std::chrono::steady_clock::now();
     auto mark = [&](int i) {
         if (trace) {
             if (!ev[i]) cudaEventCreate(&ev[i]);
             cudaEventRecord(ev[i], static_cast<cudaStream_t>(stream));
+            host_ms[i] = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - h0).count();
         }
     };
     mark(0);
@@ -1771,8 +1775,11 @@ extern "C" int kk_ddlms_solve(const void* x, int64_t nsym, float scale, const vo
         cudaEventSynchronize(ev[3]);
         float t[3];
         for (int i = 0; i < 3; ++i) cudaEventElapsedTime(&t[i], ev[i], ev[i + 1]);
-        std::fprintf(stderr, "[kk_ddlms_solve] nsym %lld B %d: init+train %.3f ms, speculate %.3f ms, loop %.3f ms\n",
-                     static_cast<long long>(nsym), block, t[0], t[1], t[2]);
+        std::fprintf(stderr,
+                     "[kk_ddlms_solve] nsym %lld B %d: device init+train %.3f ms, speculate %.3f ms, loop %.3f ms; "
+                     "host marks %.3f %.3f %.3f %.3f ms\n",
+                     static_cast<long long>(nsym), block, t[0], t[1], t[2], host_ms[0], host_ms[1], host_ms[2],
+                     host_ms[3]);
         for (cudaEvent_t e : ev)
             if (e) cudaEventDestroy(e);
     }
@@ -1865,33 +1872,31 @@ namespace kk {
 struct PointLabels {
     uint8_t v[64];
 };
+// One thread per group of 8 symbols: 8 k bits = exactly k output bytes (no
+// per-byte divisions; the label table is read from the parameter bank).
 __global__ void pack_bits_kernel(const uint8_t* __restrict__ lab, int64_t n, int64_t sym0,
-                                 const uint8_t* __restrict__ train_idx, int64_t n_train, PointLabels pl, int k,
-                                 uint8_t* __restrict__ out, int64_t nbytes) {
-    for (int64_t o = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; o < nbytes;
-         o += int64_t(gridDim.x) * blockDim.x) {
-        // first symbol touching byte o and the bit offset inside it: one
-        // 64-bit division per byte, then incremental (no per-bit divisions)
-        const int64_t b0 = o * 8;
-        int64_t s = b0 / k;
-        int bit = static_cast<int>(b0 - s * k);       // bits of symbol s already consumed
-        unsigned byte = 0;
-        int filled = 0;
-        while (filled < 8) {
-            unsigned word = 0;
+                                 const uint8_t* __restrict__ train_idx, int64_t n_train,
+                                 const __grid_constant__ PointLabels pl, int k, uint8_t* __restrict__ out,
+                                 int64_t nbytes) {
+    const int64_t ngroups = (n + 7) / 8;
+    for (int64_t g = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; g < ngroups;
+         g += int64_t(gridDim.x) * blockDim.x) {
+        unsigned long long bits = 0;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            const int64_t s = 8 * g + j;
+            unsigned w = 0;
             if (s < n) {
                 int li = lab[s];
                 if (li == 255) li = (sym0 + s < n_train && train_idx) ? train_idx[sym0 + s] : 0;
-                word = pl.v[li & 63];
+                w = pl.v[li & 63];
             }
-            const int take = min(k - bit, 8 - filled);          // bits of this symbol in this byte
-            const unsigned chunk = (word >> (k - bit - take)) & ((1u << take) - 1u);
-            byte |= chunk << (8 - filled - take);
-            filled += take;
-            bit += take;
-            if (bit == k) { bit = 0; ++s; }
+            bits = (bits << k) | w;
         }
-        out[o] = static_cast<uint8_t>(byte);
+        for (int b = 0; b < k; ++b) {
+            const int64_t o = g * k + b;
+            if (o < nbytes) out[o] = static_cast<uint8_t>(bits >> (8 * (k - 1 - b)));
+        }
     }
 }
 }  // namespace kk
@@ -1908,7 +1913,7 @@ extern "C" int kk_pack_bits(const uint8_t* labels, int64_t n, int64_t sym0, cons
     for (int i = 0; i < order; ++i) pl.v[i] = point_label_host[i];
     const int64_t nbytes = (n * bits_per_symbol + 7) / 8;
     const int th = 256;
-    int64_t blocks = (nbytes + th - 1) / th;
+    int64_t blocks = ((n + 7) / 8 + th - 1) / th;
     if (blocks > 148 * 32) blocks = 148 * 32;
     pack_bits_kernel<<<static_cast<unsigned>(blocks), th, 0, static_cast<cudaStream_t>(stream)>>>(
         labels, n, sym0, train_idx, n_train, pl, bits_per_symbol, out, nbytes);

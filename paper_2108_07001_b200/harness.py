@@ -438,29 +438,40 @@ def _bits_capacity(cfg, n: int, k: int) -> int:
     return (n_sym * k + 7) // 8 + 8
 
 
-def _drain_bits(st, bits_host, d2h, dev, max_frames=None):
+def _drain_bits(st, bits_host, d2h, dev, max_frames=None, final: bool = False):
     """Finished frames -> packed bits -> pinned host, on the d2h stream (the
-    other DMA direction), off the compute stream."""
+    other DMA direction), off the compute stream.  Whole groups of 8 symbols
+    (k whole bytes) are packed; the remainder is carried to the next call so
+    the byte stream is continuous whatever the frame sizes (final=True packs
+    it)."""
     import torch
 
     pipe, k = st["pipe"], st["k"]
     lab, soft, _ = pipe.drain_device(wait_stream=d2h, want_soft=False, max_frames=max_frames)
-    if not lab.numel():
+    if lab.numel():
+        lab.record_stream(d2h)
+        soft.record_stream(d2h)
+    carry = st.get("carry")
+    if carry is not None and carry.numel():
+        with torch.cuda.stream(d2h):
+            lab = torch.cat([carry, lab]) if lab.numel() else carry
+    n = int(lab.numel())
+    n_pack = n if final else (n // 8) * 8
+    st["carry"] = lab[n_pack:] if n_pack < n else None
+    if n_pack == 0:
         return
-    nb = (lab.numel() * k + 7) // 8
+    nb = (n_pack * k + 7) // 8
     ti = st["train_idx"]
     with torch.cuda.stream(d2h):
         packed = torch.empty(nb, dtype=torch.uint8, device=dev)
-        _lib.call("kk_pack_bits", lab.data_ptr(), lab.numel(), st["n_out"],
+        _lib.call("kk_pack_bits", lab.data_ptr(), n_pack, st["n_out"],
                   ti.data_ptr() if ti is not None else None, st["n_train"], k,
                   st["tb"].point_label.ctypes.data, st["order"], packed.data_ptr(), d2h.cuda_stream)
         if st["b_out"] + nb > bits_host.numel():
             raise ParameterError(f"bits_host holds {bits_host.numel()} bytes, the stream needs more "
                                  f"(>= {st['b_out'] + nb})")
         bits_host[st["b_out"]:st["b_out"] + nb].copy_(packed, non_blocking=True)
-    lab.record_stream(d2h)
-    soft.record_stream(d2h)
-    st["n_out"] += lab.numel()
+    st["n_out"] += n_pack
     st["b_out"] += nb
 
 
@@ -526,6 +537,7 @@ def _receive_host_stream(cfg, host_codes, half_lsb, reference_symbols, chunk_sam
                 trace.append(("d2h", time.perf_counter(), ev2))
             if i < len(starts) - 1 or not pipe.frames_pending:
                 break
+    _drain_bits(st, bits_host, d2h, dev, final=True)      # the last < 8 symbols
     comp.wait_stream(d2h)
     return pipe, bits_host, st["n_out"]
 
@@ -607,6 +619,8 @@ def receive_raw_file(cfg, path: str, reference_symbols, chunk_samples: int = 1 <
             _drain_bits(st, bits_host, d2h, dev, max_frames=1 if last else None)
             while last and pipe.frames_pending:
                 _drain_bits(st, bits_host, d2h, dev, max_frames=1)
+            if last:
+                _drain_bits(st, bits_host, d2h, dev, final=True)
         comp.wait_stream(d2h)
     th.join()
     if err:

@@ -555,10 +555,13 @@ def test_parallel_solver_fallback_equals_sequential(max_iter):
     assert np.median(np.abs(soft - s_seq)) < 1e-5
 
 
-def test_host_stream_ragged_length_and_chunks():
+@pytest.mark.parametrize("tail_min", [1 << 24, 64])
+def test_host_stream_ragged_length_and_chunks(tail_min):
     """Streaming receive of a ragged stream (length not a multiple of the
     chunk, the KK hop or the static hop; ragged chunk size): the same bits as
-    the single-shot device path on the same samples."""
+    the single-shot device path on the same samples.  tail_min=64 splits the
+    tail frames at the ragged feed ends (frame sizes not multiples of 8
+    symbols: the packed byte stream must stay continuous)."""
     import torch
 
     from paper_2108_07001_b200.constellation import slicer_tables
@@ -567,7 +570,7 @@ def test_host_stream_ragged_length_and_chunks():
     cap = load_capture("c4_qpsk_10000km_cspr6")
     n = len(cap.adc_h) - 12345
     codes = np.ascontiguousarray(cap.adc_h[:n])
-    cfg = cap.pipeline_config(ddlms_frame_symbols=1 << 13)
+    cfg = cap.pipeline_config(ddlms_frame_symbols=1 << 15, ddlms_tail_min_symbols=tail_min)
     _, bits_host, n_sym = receive_host_stream(cfg, torch.from_numpy(codes).pin_memory(), cap.half_lsb,
                                               cap.symbols(), chunk_samples=50001)
     torch.cuda.synchronize()

@@ -33,13 +33,19 @@ total = (pipe._y2.end - pipe._drop - 4) // 2 + 1
 tb = pipe._tables
 d = cfg.ddlms
 s = torch.cuda.current_stream(dev)
+if os.environ.get("KK_LAT_PRIO"):
+    s = torch.cuda.Stream(device=dev, priority=int(os.environ["KK_LAT_PRIO"]))
 flush_buf = torch.empty(1 << 26, dtype=torch.float32, device=dev)
+if os.environ.get("KK_LAT_HEAT") == "1":
+    heat_codes = torch.from_numpy(codes).to(dev)
 for lg in sizes:
     nsym = 1 << lg
     if AT_END:
         k0 = total - nsym
     for B in blocks:
         wsb = int(_lib.load().kk_ddlms_workspace_bytes(nsym, B))
+        if os.environ.get("KK_LAT_BIG_WS"):
+            wsb = max(wsb, int(_lib.load().kk_ddlms_workspace_bytes(1 << 26, 512)))
         ws = torch.empty(wsb, dtype=torch.uint8, device=dev)
         lab = torch.empty(nsym, dtype=torch.uint8, device=dev)
         soft = torch.empty(nsym, dtype=torch.complex64, device=dev)
@@ -52,6 +58,15 @@ for lg in sizes:
             if os.environ.get("KK_LAT_FLUSH_L2") == "1":
                 flush_buf.fill_(rep)      # evict L2 (256 MB > 126 MB)
             torch.cuda.synchronize()
+            if os.environ.get("KK_LAT_HEAT") == "1":
+                # ~40 ms of the receiver's own front end right before the solve
+                # (is the frame slower on a GPU that just ran the full chain?)
+                for _ in range(4):
+                    heat = rxdsp.RxPipeline(cfg, reference_symbols=cap.symbols()[:10000], device=dev)
+                    heat.front_end(AdcCodes(heat_codes, cap.half_lsb, cfg.adc_rate_hz), flush=False)
+                    heat.release_buffers()
+            else:
+                torch.cuda.synchronize()
             h0 = time.perf_counter()
             e0.record(s)
             _lib.call("kk_ddlms_solve", pipe._y2.ptr(pipe._drop + 2 * k0), nsym, float(pipe._eq_scale), None, 0,

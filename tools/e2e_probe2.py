@@ -57,6 +57,26 @@ def _wrap_mod(mod, name):
 
 
 _wrap_mod(harness, "_stream_receiver")
+if os.environ.get("KK_PROBE_NO_D2H") == "1":      # collect frames without packing / shipping bits
+    def _collect_only(st, bits_host, d2h, dev, max_frames=None, final=False):
+        st["pipe"].drain_device(wait_stream=d2h, want_soft=False, max_frames=max_frames)
+    harness._drain_bits = _collect_only
+_MODE = os.environ.get("KK_PROBE_D2H_MODE")
+if _MODE:
+    def _partial(st, bits_host, d2h, dev, max_frames=None, final=False):
+        lab, soft, _ = st["pipe"].drain_device(wait_stream=d2h, want_soft=False, max_frames=max_frames)
+        if not lab.numel():
+            return
+        nb = (lab.numel() * 2 + 7) // 8
+        with torch.cuda.stream(d2h):
+            packed = torch.empty(nb, dtype=torch.uint8, device=dev)
+            if _MODE in ("pack", "both"):
+                _lib.call("kk_pack_bits", lab.data_ptr(), lab.numel(), 0, None, 0, 2,
+                          st["tb"].point_label.ctypes.data, st["order"], packed.data_ptr(), d2h.cuda_stream)
+            if _MODE in ("copy", "both"):
+                bits_host[:nb].copy_(packed, non_blocking=True)
+        lab.record_stream(d2h)
+    harness._drain_bits = _partial
 from paper_2108_07001_b200 import _lib  # noqa: E402
 _orig_call = _lib.call
 
