@@ -15,6 +15,7 @@ from . import _lib
 from .constellation import make_constellation, slicer_tables
 from .metrics import (SyncFailure, count_bit_errors, evm, frame_sync, q_from_ber, windowed_q,
                       windowed_q_from_counts)
+from ._lib import SyncError
 from .rxdsp import _upload, side_stream
 from .rxdsp import (
     DdlmsConfig, GpuOptions, RxPipeline, RxPipelineConfig, compute_static_taps, demap, design_receive_taps,
@@ -117,6 +118,85 @@ def bench_throughput(cfg, n_samples: int, repeats: int = 3) -> dict:
         "stage_total_seconds": sum(stage.values()),
         "wall_seconds_last": n_samples / results[-1],
     }
+
+
+REPORT_SCHEMA_VERSION = 1   # runner.py:38
+
+
+def run_single(cfg, output_dir: str | None = None, save_captures: bool = False) -> dict:
+    """tx -> link (with monitors) -> front end -> rx -> metrics (runner.py:
+    140-196, same report schema: config echo and one point per monitored
+    distance; a sync failure marks that point "failed").  The capture of
+    each monitored distance is generated on the GPU (capgen: the reference's
+    TX, linear link with per-span ASE and laser phase noise, PD and ADC;
+    nonlinear links raise ParameterError) and received and measured on the
+    device; noise realisations differ from the reference's, the statistics
+    do not (test_capture_generator_statistics_vs_reference)."""
+    import copy
+    import json
+    import os
+
+    from . import capgen
+    from .sigcore import AdcCodes, write_adc_raw
+
+    c = copy.deepcopy(cfg.to_dict() if hasattr(cfg, "to_dict") else cfg)
+    ln = c["link"]
+    if ln.get("nonlinearity_enabled"):
+        raise ParameterError("run_single on the GPU models the linear link only")
+    order = int(c["tx"]["constellation_order"])
+    pts = make_constellation(order).points
+    n_symbols = int(c["tx"]["n_symbols"])
+    n_spans, every = int(ln["n_spans"]), max(1, int(ln["monitor_every_n_spans"]))
+    monitors = [m for m in range(1, n_spans + 1) if m % every == 0 or m == n_spans]
+    state = np.random.SeedSequence(int(c.get("seed", 0))).generate_state(4)          # hr:41-48
+    link = _namespace({"total_dispersion_ps_nm": float(ln["dispersion_ps_nm_km"]) * n_spans
+                       * float(ln["span_length_km"]), "center_wavelength_nm": ln["center_wavelength_nm"]})
+    ns = _namespace(c)
+    pipe_cfg = make_pipeline_config(ns, link)
+    points = []
+    for m in monitors:
+        dist = m * float(ln["span_length_km"])
+        point = {"distance_km": dist, "status": "ok"}
+        cm = copy.deepcopy(c)
+        cm["link"]["n_spans"] = m
+        gp = capgen.GenParams.from_config(cm)
+        gp.osnr_db = c["rx"].get("osnr_override_db")
+        gen = capgen.CaptureGenerator(gp, seed=int(state[0]))
+        codes, half, idx, bits = gen.generate(n_symbols)
+        try:
+            pipe = RxPipeline(pipe_cfg, reference_symbols=pts[idx])
+            pipe.feed(AdcCodes(codes, half, pipe_cfg.adc_rate_hz))
+            pipe.feed(np.zeros(0), flush=True)
+            lab, soft, _ = pipe.drain_device()
+            point.update(measure_point_device(lab, soft, bits, pts[idx], ns))
+            full = (1 << int(c["frontend"]["adc_bits"])) - 1          # odd codes at the clip levels
+            point["clip_fraction"] = float((codes.abs() >= full).float().mean())
+            point["diverged"] = pipe.diverged
+            if save_captures and output_dir:
+                ddir = os.path.join(output_dir, f"dist_{int(dist):06d}km")
+                os.makedirs(ddir, exist_ok=True)
+                spec = make_constellation(order)
+                k = spec.bits_per_symbol
+                li = lab.cpu().numpy()
+                li = np.where(li == 255, idx[:len(li)], li)
+                pl = slicer_tables(order).point_label[:order]
+                dbits = np.unpackbits(pl[li][:, None], axis=1)[:, -k:].reshape(-1)
+                np.packbits(dbits).tofile(os.path.join(ddir, "decided_bits.bin"))
+                soft.cpu().numpy().astype(np.complex64).view(np.float32).tofile(
+                    os.path.join(ddir, "soft_symbols.f32"))
+                pipe.write_diagnostics(os.path.join(ddir, "rx_diagnostics.jsonl"))
+                write_adc_raw(os.path.join(ddir, "adc_stream.raw"),
+                              AdcCodes(codes.cpu().numpy(), half, pipe_cfg.adc_rate_hz))
+        except (SyncError, SyncFailure) as exc:
+            point["status"] = "failed"
+            point["reason"] = str(exc)
+        points.append(point)
+    report = {"schema_version": REPORT_SCHEMA_VERSION, "config": c, "points": points}
+    if output_dir:
+        os.makedirs(output_dir, exist_ok=True)
+        with open(os.path.join(output_dir, "report.json"), "w") as f:
+            json.dump(report, f, indent=2, sort_keys=True, default=float)
+    return report
 
 
 def run_sustained(cfg, n_adc_samples: int, osnr_db: float | None = None, chunk_symbols: int = 1 << 16) -> dict:

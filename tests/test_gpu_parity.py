@@ -663,3 +663,31 @@ def test_run_sustained_ber_vs_reference():
     sigma = np.sqrt(ref["n_errors"] + max(r["n_errors"], 1))
     print("errors", r["n_errors"], "reference", ref["n_errors"], "ber", r["ber"], ref["ber"])
     assert abs(r["n_errors"] - ref["n_errors"]) < 4 * sigma
+
+
+@pytest.mark.parametrize("name", ["c2_16qam_5600km_rel-20", "c4_qpsk_10000km_cspr10"])
+def test_run_single_report_vs_reference(name, tmp_path):
+    """harness.run_single (runner.py:140-196) on a golden capture's config:
+    the reference's report schema, one point at the monitored distance, and
+    the point statistics of the reference's own run (EVM within 10 %, BER
+    within a factor 3 -- different noise realisations); captures written in
+    the reference's layout when asked."""
+    import os
+
+    from paper_2108_07001_b200.harness import run_single
+    from paper_2108_07001_b200.sigcore import read_adc_raw
+
+    cap = load_capture(name)
+    rep = run_single(cap.meta["config"], output_dir=str(tmp_path), save_captures=True)
+    assert rep["schema_version"] == 1 and len(rep["points"]) == 1
+    pt, ref = rep["points"][0], cap.meta["point"]
+    assert pt["status"] == "ok" and not pt["diverged"]
+    assert set(ref) <= set(pt) | {"distance_km", "status"}, set(ref) - set(pt)
+    assert abs(pt["evm_pct"] - ref["evm_pct"]) < 0.1 * ref["evm_pct"], (pt["evm_pct"], ref["evm_pct"])
+    assert max(ref["ber"], 1e-4) / 3 < max(pt["ber"], 1e-4) < 3 * max(ref["ber"], 1e-4), (pt["ber"], ref["ber"])
+    d = os.path.join(str(tmp_path), f"dist_{int(pt['distance_km']):06d}km")
+    assert os.path.exists(os.path.join(str(tmp_path), "report.json"))
+    assert len(read_adc_raw(os.path.join(d, "adc_stream.raw"))) == 4 * cap.meta["config"]["tx"]["n_symbols"]
+    k = {4: 2, 16: 4}[cap.order]
+    n_dec = os.path.getsize(os.path.join(d, "decided_bits.bin")) * 8 // k       # decided symbols (sync drop)
+    assert cap.meta["config"]["tx"]["n_symbols"] - 8192 < n_dec <= cap.meta["config"]["tx"]["n_symbols"]
