@@ -691,3 +691,27 @@ def test_run_single_report_vs_reference(name, tmp_path):
     k = {4: 2, 16: 4}[cap.order]
     n_dec = os.path.getsize(os.path.join(d, "decided_bits.bin")) * 8 // k       # decided symbols (sync drop)
     assert cap.meta["config"]["tx"]["n_symbols"] - 8192 < n_dec <= cap.meta["config"]["tx"]["n_symbols"]
+
+
+def test_run_sweep_cspr_vs_reference(tmp_path):
+    """harness.run_sweep over CSPR on the 10,000 km QPSK config (BASELINE
+    configs[3], sweep.py:41-83): rows/summary/CSV layout of the reference,
+    and each point's BER within 3x of the reference's own capture at that
+    CSPR (tests/golden c4_qpsk_10000km_cspr*)."""
+    import copy
+    import os
+
+    from paper_2108_07001_b200.harness import run_sweep
+
+    c = copy.deepcopy(load_capture("c4_qpsk_10000km_cspr10").meta["config"])
+    c["sweep"] = {"axis": "cspr_db", "values": [6.0, 10.0, 14.0]}
+    res = run_sweep(c, output_dir=str(tmp_path))
+    assert set(res) == {"axis", "values", "rows", "summary", "reports"}
+    assert len(res["rows"]) == 3 and all(r["status"] == "ok" for r in res["rows"])
+    assert os.path.exists(os.path.join(str(tmp_path), "sweep.csv"))
+    assert os.path.exists(os.path.join(str(tmp_path), "sweep_optimum.csv"))
+    for r in res["rows"]:
+        ref = load_capture(f"c4_qpsk_10000km_cspr{int(r['value'])}").meta["point"]
+        print(r["value"], r["ber"], ref["ber"])
+        assert max(ref["ber"], 1e-4) / 3 < max(r["ber"], 1e-4) < 3 * max(ref["ber"], 1e-4)
+    assert len(res["summary"]) == 1

@@ -139,3 +139,26 @@ def test_bench_throughput_needs_enough_samples():
     cfg = load_capture("c1_qpsk_b2b").meta["config"]
     with pytest.raises(ValueError):
         bench_throughput(cfg, n_samples=1 << 10)
+
+
+def test_sweep_axis_and_summary():
+    """sweep.py:20-38 axis application and :86-98 argmax summary (host logic
+    of harness.run_sweep); a config without a sweep section raises."""
+    from paper_2108_07001_b200.harness import _apply_axis, run_sweep, sweep_argmax_summary
+
+    c = load_capture("c4_qpsk_10000km_cspr10").meta["config"]
+    assert _apply_axis(c, "cspr_db", 6)["tx"]["cspr_db"] == 6.0
+    assert _apply_axis(c, "format", 16)["tx"]["constellation_order"] == 16
+    d = _apply_axis(c, "distance_km", 2000)["link"]
+    assert d["n_spans"] == 20 and d["monitor_every_n_spans"] == 20
+    assert c["tx"]["cspr_db"] == 10.0                       # input untouched
+    with pytest.raises(ParameterError):
+        _apply_axis(c, "distance_km", 10)
+    with pytest.raises(ParameterError):
+        _apply_axis(c, "nonsense", 1)
+    rows = [{"status": "ok", "q_db": 9.0, "distance_km": 1e4, "value": 6},
+            {"status": "ok", "q_db": 11.0, "distance_km": 1e4, "value": 10},
+            {"status": "failed", "q_db": "", "distance_km": 1e4, "value": 4}]
+    assert sweep_argmax_summary(rows) == [{"distance_km": 1e4, "best_value": 10, "best_q_db": 11.0}]
+    with pytest.raises(ParameterError):
+        run_sweep(dict(c, sweep=None))
