@@ -162,3 +162,77 @@ def test_sweep_axis_and_summary():
     assert sweep_argmax_summary(rows) == [{"distance_km": 1e4, "best_value": 10, "best_q_db": 11.0}]
     with pytest.raises(ParameterError):
         run_sweep(dict(c, sweep=None))
+
+
+# --- the reference's host-side tap criteria (kkmodem test_rxdsp.py:158-385),
+# restated against this package's float64 host setup code ---------------------
+
+def _link_10000km():
+    """LinkConfig() defaults: 100 x 100 km at 20 ps/nm/km, 1550.116 nm."""
+    from types import SimpleNamespace
+
+    return SimpleNamespace(total_dispersion_ps_nm=20.0 * 10000.0, center_wavelength_nm=1550.116)
+
+
+def test_static_tap_coverage_and_even_taps():
+    """test_rxdsp.py:168-172, :194-196: tap span covers the 10,000 km delay
+    spread (the reference's units included); an even tap count is rejected."""
+    assert rxdsp.static_tap_coverage(_link_10000km(), n_taps=203, rate_hz=2e9) > 10.0
+    with pytest.raises(ParameterError):
+        rxdsp.compute_static_taps(_link_10000km(), n_taps=202)
+
+
+def test_static_taps_cascade_flat():
+    """test_rxdsp.py:174-192 (cascade frequency-response oracle): taps x fiber
+    CD is flat within 0.2 dB and 0.05 rad of linear phase over +-0.5 GHz."""
+    from paper_2108_07001_b200.sigcore import cd_phase_coefficient, fir_frequency_response
+
+    link = _link_10000km()
+    fir = rxdsp.compute_static_taps(link, n_taps=203)
+    f = np.linspace(-0.5e9, 0.5e9, 501)
+    a = cd_phase_coefficient(link.total_dispersion_ps_nm, 1.0, link.center_wavelength_nm)
+    cascade = fir_frequency_response(fir, f) * np.exp(-1j * a * f * f)
+    mag_db = 20 * np.log10(np.abs(cascade))
+    phase = np.unwrap(np.angle(cascade))
+    resid = phase - np.polyval(np.polyfit(f, phase, 1), f)
+    assert np.max(np.abs(mag_db - np.mean(mag_db))) < 0.2
+    assert np.max(np.abs(resid)) < 0.05
+
+
+def test_receive_taps_undo_dispersion():
+    """test_rxdsp.py:359-375: TX pulse -> 10,000 km CD -> designed receive
+    taps, sampled at the symbol period, has ISI below 3 %."""
+    from types import SimpleNamespace
+
+    from paper_2108_07001_b200.sigcore import cd_phase_coefficient, design_rrc
+
+    link = _link_10000km()
+    tx = SimpleNamespace(baud_hz=1e9, rolloff=0.01, pulse_span_symbols=256, tone_freq_hz=0.516e9)
+    fir = rxdsp.design_receive_taps(link, tx)
+    assert len(fir.taps) == 203
+    pulse = design_rrc(0.01, 2, 256).taps.real
+    x = np.concatenate([pulse, np.zeros(4096 - len(pulse))])
+    f = np.fft.fftfreq(len(x), 1 / 2e9)
+    a = cd_phase_coefficient(20.0, 10000.0, link.center_wavelength_nm)
+    dispersed = np.fft.ifft(np.fft.fft(x) * np.exp(-1j * a * f * f))
+    composite = np.convolve(dispersed, fir.taps)
+    peak = int(np.argmax(np.abs(composite)))
+    vals = np.abs(composite[peak % 2::2])
+    ci = (peak - peak % 2) // 2
+    assert np.sqrt(np.sum(np.delete(vals, ci) ** 2)) / vals[ci] < 0.03
+
+
+def test_refine_static_taps_fits_capture():
+    """test_rxdsp.py:377-384: the data-aided refit absorbs a mild unknown
+    3-tap channel (relative MSE below 1e-2)."""
+    from paper_2108_07001_b200.sigcore import design_rrc
+
+    rng = np.random.default_rng(12)
+    syms = make_constellation(4).points[rng.integers(0, 4, 6000)]
+    rc = np.convolve(design_rrc(0.01, 2, 256).taps.real, design_rrc(0.01, 2, 256).taps.real)
+    up = np.zeros(2 * len(syms), dtype=complex)
+    up[::2] = syms
+    y2 = np.convolve(up, rc)[len(rc) // 2:len(rc) // 2 + len(up)]
+    x = np.convolve(y2, np.array([0.05 - 0.02j, 1.0, -0.08 + 0.03j]), mode="same")
+    _, diag = rxdsp.refine_static_taps(x, syms, n_taps=31, rate_hz=2e9)
+    assert diag["relative_mse"] < 1e-2
