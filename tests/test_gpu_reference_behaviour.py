@@ -173,3 +173,60 @@ def test_ddlms_widely_linear_corrects_conjugate_crosstalk():
     err_lin, _ = run(False)
     assert sym_err_wl == 0
     assert err_lin >= 10 * err_wl
+
+
+# --- the reference runner's criteria (kkmodem tests/test_harness.py:99-163) ----
+
+def _small_b2b(n_symbols=1 << 15):
+    """small_b2b_config (test_harness.py:24-33) on the dict layout: the
+    back-to-back QPSK golden config, shorter, faster sync/training."""
+    import copy
+
+    from paper_2108_07001_b200.captures import load_capture
+
+    c = copy.deepcopy(load_capture("c1_qpsk_b2b").meta["config"])
+    c["tx"]["n_symbols"] = n_symbols
+    c["rx"]["sync_wait_samples"] = 1 << 14
+    c["rx"]["startup_symbols"] = 4000
+    return c
+
+
+def test_run_single_noiseless_loopback_ber_zero():
+    """test_harness.py:100-106: a noiseless back-to-back run decodes without
+    a single bit error (BER 0, Q infinite)."""
+    from paper_2108_07001_b200.harness import run_single
+
+    (point,) = run_single(_small_b2b())["points"]
+    assert point["status"] == "ok" and point["ber"] == 0.0 and point["q_db"] == np.inf
+
+
+def test_run_single_monitors_and_deterministic_reports(tmp_path):
+    """test_harness.py:108-130: a 10-span link monitored every 2 spans
+    reports at 200..1000 km; two runs of the same config write
+    byte-identical reports."""
+    from paper_2108_07001_b200.harness import run_single
+
+    c = _small_b2b()
+    c["link"].update(n_spans=10, span_length_km=100.0, monitor_every_n_spans=2, ase_enabled=True)
+    rep = run_single(c, output_dir=str(tmp_path / "a"))
+    assert [p["distance_km"] for p in rep["points"]] == [200.0, 400.0, 600.0, 800.0, 1000.0]
+    run_single(c, output_dir=str(tmp_path / "b"))
+    assert (tmp_path / "a" / "report.json").read_bytes() == (tmp_path / "b" / "report.json").read_bytes()
+
+
+def test_run_sweep_rows_and_csv(tmp_path):
+    """test_harness.py:133-157: values x monitored distances rows, the CSV
+    with a header, the optimum file; a one-value sweep succeeds."""
+    from paper_2108_07001_b200.harness import run_sweep
+
+    c = _small_b2b()
+    c["link"].update(n_spans=2, span_length_km=100.0, monitor_every_n_spans=1, ase_enabled=True)
+    c["sweep"] = {"axis": "cspr_db", "values": [8.0, 10.0, 12.0]}
+    res = run_sweep(c, output_dir=str(tmp_path))
+    assert len(res["rows"]) == 3 * 2
+    assert len((tmp_path / "sweep.csv").read_text().strip().splitlines()) == 1 + 6
+    assert (tmp_path / "sweep_optimum.csv").exists()
+    c1 = _small_b2b()
+    c1["sweep"] = {"axis": "cspr_db", "values": [12.0]}
+    res1 = run_sweep(c1)
+    assert len(res1["rows"]) == 1 and res1["rows"][0]["status"] == "ok"
