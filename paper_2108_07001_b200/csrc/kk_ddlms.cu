@@ -1159,17 +1159,34 @@ extern "C" int kk_ddlms_sequential(const void* x, int64_t n_out, float scale, in
 // Small device->host reads through a per-thread pinned staging buffer (a
 // copy to pageable memory goes through the driver's shared bounce buffer and
 // stalls other host threads' CUDA calls while it waits on this stream).
+// The copy is a kernel writing into mapped pinned memory, not a DMA: a
+// DMA readback would queue behind bulk device->host transfers (the packed
+// output bits of a streaming receive) on the copy engine, idling the solver
+// between its passes.
+__global__ void readback_kernel(const uint4* __restrict__ src, uint4* __restrict__ dst, int n16) {
+    for (int i = threadIdx.x; i < n16; i += blockDim.x) dst[i] = src[i];
+}
+
 static int d2h_small(void* dst, const void* src, size_t bytes, cudaStream_t s) {
     static thread_local void* pin = nullptr;
+    static thread_local void* pin_dev = nullptr;
     constexpr size_t kPin = 64 << 10;
     if (bytes > kPin) return set_error(KK_ERR_PARAM, "d2h_small: too large");
-    if (!pin && cudaHostAlloc(&pin, kPin, cudaHostAllocDefault) != cudaSuccess) {
-        pin = nullptr;
-        return set_cuda_error("pinned staging");
+    if (!pin) {
+        if (cudaHostAlloc(&pin, kPin, cudaHostAllocMapped) != cudaSuccess ||
+            cudaHostGetDevicePointer(&pin_dev, pin, 0) != cudaSuccess) {
+            pin = pin_dev = nullptr;
+            return set_cuda_error("mapped pinned staging");
+        }
     }
-    if (cudaMemcpyAsync(pin, src, bytes, cudaMemcpyDeviceToHost, s) != cudaSuccess ||
-        cudaStreamSynchronize(s) != cudaSuccess)
+    if ((reinterpret_cast<uintptr_t>(src) & 15) == 0) {
+        const int n16 = static_cast<int>((bytes + 15) / 16);   // src regions are 256 B-aligned workspace slots
+        readback_kernel<<<1, 256, 0, s>>>(static_cast<const uint4*>(src), static_cast<uint4*>(pin_dev), n16);
+        if (int rc = check_launch("readback_kernel")) return rc;
+    } else if (cudaMemcpyAsync(pin, src, bytes, cudaMemcpyDeviceToHost, s) != cudaSuccess) {
         return set_cuda_error("device->host readback");
+    }
+    if (cudaStreamSynchronize(s) != cudaSuccess) return set_cuda_error("device->host readback");
     std::memcpy(dst, pin, bytes);
     return KK_OK;
 }
