@@ -1599,7 +1599,7 @@ struct DdlmsSolver {
                 return rc;
             }
             queued += n;
-            batch = 8;
+            batch = std::min(2 * batch, 32);   // long decision cascades (64-QAM): fewer readbacks
             if (h.ctl[0] == kModeDone) break;
         }
         ctl_d = nullptr;

@@ -133,7 +133,7 @@ class GpuOptions:
     # cannot hide (measured: 2^22-symbol frame 0.47 ms at B=128, 0.61 at 512)
     ddlms_block_min: int = 128
     ddlms_frame_symbols: int = 1 << 28
-    ddlms_max_iter: int = 64
+    ddlms_max_iter: int = 1024
     ddlms_soft_tol: float = 1e-5
     ddlms_tail_min_symbols: int = 1 << 24
     # run the DDLMS frames on a worker thread / CUDA stream so the front end
