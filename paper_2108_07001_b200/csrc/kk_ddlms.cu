@@ -299,6 +299,11 @@ __global__ void sum_int_kernel(const int* __restrict__ v, int64_t n, unsigned lo
 // remaining (pre-queued) iterations return at once; the host reads the
 // control block back once per batch of iterations instead of once per pass.
 constexpr int kModeDecision = 0, kModeOutput = 1, kModeDone = 2;
+#ifndef KK_CASCADE_W
+#define KK_CASCADE_W 8
+#endif
+constexpr int kCascadeW = KK_CASCADE_W;                        // blocks the exact frontier advances per step set
+constexpr unsigned long long kCascadeMaxChanged = 64; // "a cascade": at most this many changed blocks
 constexpr int kMaxStatIters = 64;
 struct ReadBack {
     unsigned long long ctr[4];   // [0] changed blocks, [1] blocks re-run, [2] guard sum, [3] list length
@@ -330,6 +335,44 @@ __global__ void ddlms_advance_kernel(ReadBack* rb) {
     rb->ctr[0] = 0;
     rb->ctr[1] = 0;
     rb->ctr[3] = 0;
+}
+
+// Decision cascades (64-QAM): late iterations change a few blocks, one block
+// further per iteration.  After an iteration's pass changed at most
+// max_changed blocks, the lowest changed block m ran from its exact start, so
+// the starts of m+1 .. m+W follow exactly from the maps of m .. m+W-1; W
+// repetitions of {these starts -> re-run the W blocks} move the exact
+// frontier W blocks ahead inside one iteration (step = repetition index).
+__global__ void cascade_prep_kernel(ReadBack* rb, const float* __restrict__ Pb, const float* __restrict__ Qb,
+                                    const float* __restrict__ Tused, float* __restrict__ Tstart, int* __restrict__ list,
+                                    int64_t nb, int64_t ntb, int W, int step, unsigned long long max_changed) {
+    if (threadIdx.x != 0) return;
+    if (step == 0)
+        rb->ctl[2] = (rb->ctl[0] != kModeDone && rb->ctr[0] > 0 && rb->ctr[0] <= max_changed) ? 1 : 0;
+    rb->ctr[3] = 0;
+    if (!rb->ctl[2]) return;
+    const int64_t m = rb->first_changed;
+    if (m < ntb || m + 1 >= nb) return;
+    float T[16];
+    for (int i = 0; i < 16; ++i) T[i] = Tused[m * 16 + i];
+    int n = 0;
+    for (int64_t b = m; b + 1 < nb && n < W; ++b) {
+        const float* P = Pb + b * 64;
+        const float* Q = Qb + b * 16;
+        float U[16];
+        for (int r = 0; r < 2; ++r)
+            for (int j = 0; j < 8; ++j) {
+                float acc = Q[r * 8 + j];
+                for (int k = 0; k < 8; ++k) acc = fmaf(T[r * 8 + k], P[k * 8 + j], acc);
+                U[r * 8 + j] = acc;
+            }
+        for (int i = 0; i < 16; ++i) {
+            T[i] = U[i];
+            Tstart[(b + 1) * 16 + i] = U[i];
+        }
+        list[n++] = static_cast<int>(b + 1);
+    }
+    rb->ctr[3] = static_cast<unsigned long long>(n);
 }
 
 struct Vec16 {
@@ -1349,7 +1392,8 @@ struct DdlmsSolver {
     // Run blocks [b0, b1): the blocks holding training symbols (b < ntb) in a
     // TRAIN launch (range mode, in-kernel skip test), the rest in a plain
     // launch -- compacted into a re-run list first when use_skip.
-    int run_blocks(bool with_p, int64_t b0, int64_t b1, int use_skip, float tol = 0.f, int write_out = 0) {
+    int run_blocks(bool with_p, int64_t b0, int64_t b1, int use_skip, float tol = 0.f, int write_out = 0,
+                   const int* ext_list = nullptr) {
         if (b1 <= b0) return KK_OK;
         // kernel attributes once per device and process (ensure_smem_attr)
         {
@@ -1393,6 +1437,7 @@ struct DdlmsSolver {
 #undef KK_DD_GO3
             return check_launch("ddlms_block_kernel");
         };
+        if (ext_list) return launch(false, b0, b1, 0, ext_list, ctr + 3);   // device-built list (cascades)
         const int64_t t1 = std::min(b1, ntb);
         if (b0 < t1)
             if (int rc = launch(true, b0, t1, (use_skip && !with_p) ? 1 : 0, nullptr, nullptr)) return rc;
@@ -1578,6 +1623,14 @@ struct DdlmsSolver {
             for (int i = 0; i < n && rc == KK_OK; ++i) {
                 rc = scan_down();
                 if (rc == KK_OK) rc = run_blocks(false, 0, L.nb, 1, soft_tol, 1);
+                // cascade window steps from the fifth iteration on (frames that
+                // converge in four, the QPSK/16-QAM norm, never queue them)
+                for (int step = 0; rc == KK_OK && queued + i >= 4 && step < kCascadeW; ++step) {
+                    cascade_prep_kernel<<<1, 32, 0, s>>>(rb, lv[0].P, lv[0].Q, Tused, lv[0].T, list, L.nb, ntb,
+                                                         kCascadeW, step, kCascadeMaxChanged);
+                    rc = check_launch("cascade_prep_kernel");
+                    if (rc == KK_OK) rc = run_blocks(false, 0, kCascadeW, 0, soft_tol, 1, list);
+                }
                 if (rc == KK_OK) rc = scan_up(false);
                 if (rc == KK_OK) {
                     ddlms_advance_kernel<<<1, 1, 0, s>>>(rb);
