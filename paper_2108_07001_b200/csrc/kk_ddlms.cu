@@ -1984,7 +1984,10 @@ extern "C" int kk_pack_bits(const uint8_t* labels, int64_t n, int64_t sym0, cons
     const int64_t nbytes = (n * bits_per_symbol + 7) / 8;
     const int th = 256;
     int64_t blocks = ((n + 7) / 8 + th - 1) / th;
-    if (blocks > 148 * 32) blocks = 148 * 32;
+#ifndef KK_PACK_CTAS
+#define KK_PACK_CTAS (148 * 32)
+#endif
+    if (blocks > KK_PACK_CTAS) blocks = KK_PACK_CTAS;
     pack_bits_kernel<<<static_cast<unsigned>(blocks), th, 0, static_cast<cudaStream_t>(stream)>>>(
         labels, n, sym0, train_idx, n_train, pl, bits_per_symbol, out, nbytes);
     return check_launch("pack_bits_kernel");
