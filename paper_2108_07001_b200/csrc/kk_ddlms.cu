@@ -1517,7 +1517,8 @@ struct DdlmsSolver {
             cudaMemsetAsync(hsh, 0, L.nb * 8, s) != cudaSuccess ||
             cudaMemsetAsync(Twritten, 0xFF, L.nb * 16 * sizeof(float), s) != cudaSuccess ||   // NaN: never written
             cudaMemsetAsync(ctr, 0, 4 * sizeof(unsigned long long), s) != cudaSuccess ||
-            cudaMemsetAsync(&rb->first_changed, 0xFF, 2 * sizeof(unsigned int), s) != cudaSuccess)
+            cudaMemsetAsync(&rb->first_changed, 0xFF, 2 * sizeof(unsigned int), s) != cudaSuccess ||
+            cudaMemsetAsync(rb->ctl, 0, sizeof(rb->ctl), s) != cudaSuccess)
             return set_cuda_error("solver init");
         return KK_OK;
     }
@@ -1579,7 +1580,8 @@ struct DdlmsSolver {
         if (int rc = set_start(T_start)) return rc;
         if (int rc = scan_down()) return rc;
         if (cudaMemsetAsync(ctr, 0, 2 * sizeof(unsigned long long), s) != cudaSuccess ||
-            cudaMemsetAsync(ctr + 3, 0, sizeof(unsigned long long), s) != cudaSuccess)
+            cudaMemsetAsync(ctr + 3, 0, sizeof(unsigned long long), s) != cudaSuccess ||
+            cudaMemsetAsync(&rb->first_changed, 0xFF, sizeof(unsigned int), s) != cudaSuccess)
             return set_cuda_error("ctr");
         // decision pass: compacted re-run of the blocks whose certified margin
         // the start move could cross, no outputs; output pass: the blocks
@@ -1589,6 +1591,14 @@ struct DdlmsSolver {
         if (int rc = soft_pass ? run_blocks(false, 0, L.nb, 1, soft_tol, 1)
                                : run_blocks(false, 0, L.nb, 1, 3.0e38f, 0))
             return rc;
+        // decision cascades: as in solve_loop (rb->ctl[0] stays "decision" here)
+        for (int step = 0; iters >= 4 && step < kCascadeW; ++step) {
+            cascade_prep_kernel<<<1, 32, 0, s>>>(rb, lv[0].P, lv[0].Q, Tused, lv[0].T, list, L.nb, ntb, kCascadeW,
+                                                 step, kCascadeMaxChanged);
+            if (int rc = check_launch("cascade_prep_kernel")) return rc;
+            if (int rc = run_blocks(false, 0, kCascadeW, 0, soft_pass ? soft_tol : 3.0e38f, soft_pass ? 1 : 0, list))
+                return rc;
+        }
         unsigned long long h[4];
         if (int rc = read_ctr(h)) return rc;
         ++iters;
