@@ -299,6 +299,9 @@ __global__ void sum_int_kernel(const int* __restrict__ v, int64_t n, unsigned lo
 // remaining (pre-queued) iterations return at once; the host reads the
 // control block back once per batch of iterations instead of once per pass.
 constexpr int kModeDecision = 0, kModeOutput = 1, kModeDone = 2;
+#ifndef KK_CASCADE_FROM
+#define KK_CASCADE_FROM 4   // first 0-based iteration that queues cascade steps
+#endif
 #ifndef KK_CASCADE_W
 #define KK_CASCADE_W 8
 #endif
@@ -1635,7 +1638,7 @@ struct DdlmsSolver {
                 if (rc == KK_OK) rc = run_blocks(false, 0, L.nb, 1, soft_tol, 1);
                 // cascade window steps from the fifth iteration on (frames that
                 // converge in four, the QPSK/16-QAM norm, never queue them)
-                for (int step = 0; rc == KK_OK && queued + i >= 4 && step < kCascadeW; ++step) {
+                for (int step = 0; rc == KK_OK && queued + i >= KK_CASCADE_FROM && step < kCascadeW; ++step) {
                     cascade_prep_kernel<<<1, 32, 0, s>>>(rb, lv[0].P, lv[0].Q, Tused, lv[0].T, list, L.nb, ntb,
                                                          kCascadeW, step, kCascadeMaxChanged);
                     rc = check_launch("cascade_prep_kernel");
