@@ -44,6 +44,9 @@ extern "C" {
 #define KK_DTYPE_I16 0 /* ADC codes; value = code * in_scale (odd half-LSB codes) */
 #define KK_DTYPE_F32 1
 #define KK_DTYPE_F64 2
+/* or-ed into in_dtype of kk_reconstruct_pairs: correctly rounded
+ * logf/expf/sincosf instead of the SFU approximations (functional API) */
+#define KK_DTYPE_PRECISE 0x100
 
 const char *kk_last_error(void);
 int kk_version(void);

@@ -10,18 +10,23 @@ from __future__ import annotations
 import ctypes
 import os
 
-from .sigcore import ParameterError
+from .sigcore import ParameterError, kkmodem_class
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "_lib", "libkkb200.so")
 
 KK_OK, KK_ERR_PARAM, KK_ERR_SYNC, KK_ERR_CUDA, KK_ERR_INTERNAL = 0, 1, 2, 3, 4
 KK_DTYPE_I16, KK_DTYPE_F32, KK_DTYPE_F64 = 0, 1, 2
+KK_DTYPE_PRECISE = 0x100   # or-ed flag: correctly rounded transcendental functions
 
 
-class SyncError(RuntimeError):
+_KK_SYNC_ERROR = kkmodem_class("kkmodem.rxdsp", "SyncError")
+
+
+class SyncError(*((_KK_SYNC_ERROR,) if _KK_SYNC_ERROR else (RuntimeError,))):
     """Raised when the receiver cannot align to the reference sequence
-    (mirrors kkmodem.rxdsp.SyncError, rxdsp.py:63)."""
+    (kkmodem.rxdsp.SyncError, rxdsp.py:63; a subclass of it when kkmodem is
+    importable)."""
 
 
 _P = ctypes.c_void_p

@@ -20,7 +20,6 @@ CSRC = os.path.join(PKG, "csrc")
 OUT_DIR = os.path.join(PKG, "_lib")
 LIB = os.path.join(OUT_DIR, "libkkb200.so")
 SOURCES = ["kk_capi.cu", "kk_kk.cu", "kk_static.cu", "kk_ddlms.cu"]
-HEADERS = ["kk_common.cuh", "kk_internal.h"]
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
@@ -40,7 +39,11 @@ def _nvcc() -> str:
 
 def _digest() -> str:
     h = hashlib.sha256()
-    for f in SOURCES + HEADERS:
+    # every file under csrc/ (sources and all headers they may include)
+    for f in sorted(os.listdir(CSRC)):
+        if not f.endswith((".cu", ".cuh", ".h", ".hpp")):
+            continue
+        h.update(f.encode())
         with open(os.path.join(CSRC, f), "rb") as fh:
             h.update(fh.read())
     with open(os.path.join(REPO, "include", "kkb200.h"), "rb") as fh:

@@ -434,7 +434,7 @@ struct TOut {
 // Block-parallel DDLMS pass, one thread per block of B symbols.  Lean
 // per-symbol work: the input scale s is folded into the taps (T' = s T,
 // mu' = mu s^2, so y = T' x_raw); Q_b is recovered once per block as
-// T_end - T_start P_b; decision changes are detected with a 32-bit hash of
+// T_end - T_start P_b; decision changes are detected with a 64-bit hash of
 // the block's label sequence; the guard is tracked as max |y|^2 and the
 // decision margin conservatively as the distance to the nearest interior
 // boundary.  WITH_P (first pass) also accumulates P_b = prod (I - 2 mu' x x^T)
@@ -584,7 +584,7 @@ ddlms_block_kernel(SolveArgs a, Slicer sl, const float* __restrict__ Tstart, flo
     }
     const float tm = 2.0f * a.mu;      // mu' (scale folded in)
     float mgl = 0.5f, mgb = 3.0e38f, mx = 0.f, my2 = 0.f;
-    unsigned hsh = 2166136261u;
+    unsigned long long hsh = 14695981039346656037ull;   // 64-bit FNV-1a of the block's labels
     float X[8];
     {
         float2 u0 = make_float2(0.f, 0.f), u1 = u0;
@@ -701,7 +701,7 @@ ddlms_block_kernel(SolveArgs a, Slicer sl, const float* __restrict__ Tstart, flo
                 T[jj] = fmaf(er, X[jj], T[jj]);
                 T[8 + jj] = fmaf(ei, X[jj], T[8 + jj]);
             }
-            hsh = live ? (hsh ^ static_cast<unsigned>(lab)) * 16777619u : hsh;
+            hsh = live ? (hsh ^ static_cast<unsigned long long>(lab & 0xff)) * 1099511628211ull : hsh;
             soft8[j] = make_float2(yr, yi);
             lab8[j >> 2] |= static_cast<unsigned>(lab & 0xff) << (8 * (j & 3));
         }
@@ -728,7 +728,7 @@ ddlms_block_kernel(SolveArgs a, Slicer sl, const float* __restrict__ Tstart, flo
     cp_async_wait<0>();
     unsigned long long changed = 0;
     if (run) {
-        changed = (o.hash[b] != static_cast<unsigned long long>(hsh)) ? 1ull : 0ull;
+        changed = (o.hash[b] != hsh) ? 1ull : 0ull;
         o.hash[b] = hsh;
         // Q_b = T_end - T_start P_b
         const float* Pm = Pb + b * 64;

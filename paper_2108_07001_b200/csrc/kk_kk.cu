@@ -79,7 +79,22 @@ __device__ __forceinline__ float2 apply_mult(int k, float2 z) {
     return make_float2(a * sr, b * si);
 }
 
-template <typename TIn>
+// PRECISE: correctly-rounded logf/expf/sincosf instead of the SFU
+// approximations (the functional kk_reconstruct API, whose reference tests
+// demand e.g. a constant current reconstructed to 1e-8 absolute,
+// test_rxdsp.py:83-89); the streaming pipeline uses the fast variant.
+template <bool PRECISE>
+__device__ __forceinline__ float k1_log(float x) { return PRECISE ? logf(x) : __logf(x); }
+template <bool PRECISE>
+__device__ __forceinline__ float k1_exp(float x) { return PRECISE ? expf(x) : __expf(x); }
+// sin/cos of a phase; the fast form first reduces to [-pi, pi]
+template <bool PRECISE>
+__device__ __forceinline__ void k1_sincos(float x, float* s, float* c) {
+    if (PRECISE) sincosf(x, s, c);
+    else __sincosf(reduce_2pi(x), s, c);
+}
+
+template <typename TIn, bool PRECISE>
 __global__ void __launch_bounds__(kK1Threads, 4)
 kk_pairs_kernel(const TIn* __restrict__ in, float in_scale, float clamp_rel, int64_t n_hops,
                 const float* __restrict__ st_u, const float* __restrict__ st_a,
@@ -121,7 +136,7 @@ kk_pairs_kernel(const TIn* __restrict__ in, float in_scale, float clamp_rel, int
             ncl += (x < thr) ? 1u : 0u;
             sv = fmaxf(x, thr);
         }
-        return 0.5f * __logf(sv);
+        return 0.5f * k1_log<PRECISE>(sv);
     };
     const int64_t h0 = hop0;                       // stage hop 0
     const bool h0_real = h0 >= 0 && h0 < n_hops;
@@ -211,7 +226,12 @@ kk_pairs_kernel(const TIn* __restrict__ in, float in_scale, float clamp_rel, int
     const float* ua = S.u + (2 * g) * kHop;          // block a: stage hops 2g, 2g+1
     const float* ub = S.u + (2 * g + 1) * kHop;      // block b: stage hops 2g+1, 2g+2
 
-    auto ld_u = [&](int i) { return make_float2(ua[i], ub[i]); };
+    // The Hilbert multiplier is 0 at DC (M[0] = 0), so a constant shift of a
+    // block's u leaves phi unchanged: subtract u at the first sample of stage
+    // hop 2g+1 (common to both blocks of the pair).  This keeps the transform
+    // at the block's AC level (a constant current gives phi == 0 exactly).
+    const float u_ref = S.u[(2 * g + 1) * kHop];
+    auto ld_u = [&](int i) { return make_float2(ua[i] - u_ref, ub[i] - u_ref); };
     // the four pairs of the CTA are independent: each 64-thread group syncs
     // on its own named barrier between passes
     const GroupBarrier gb{g + 1, kGroupThreads};
@@ -256,14 +276,12 @@ kk_pairs_kernel(const TIn* __restrict__ in, float in_scale, float clamp_rel, int
         // previous hop when i < 256
         bool da = (i < kHop / 2) ? (hist ? (S.dead_hist[i] != 0) : (dead_a0 != 0)) : (dead_a1 != 0);
         bool db = (i < kHop / 2) ? (dead_a1 != 0) : (dead_b1 != 0);
-        // phases, reduced to [-pi, pi] for the fast sin/cos (abs err ~1e-6)
-        const float pa_ = reduce_2pi(v.x * (1.0f / 1024.0f));
-        const float pb_ = reduce_2pi(v.y * (1.0f / 1024.0f));
-        const float amp_a = (hist && i < kHop / 2) ? S.ahist[i] : __expf(ua_d[i]);
-        const float amp_b = __expf(ub_d[i]);
+        // phases (the fast sin/cos reduces to [-pi, pi]: abs err ~1e-6)
+        const float amp_a = (hist && i < kHop / 2) ? S.ahist[i] : k1_exp<PRECISE>(ua_d[i]);
+        const float amp_b = k1_exp<PRECISE>(ub_d[i]);
         float sa, ca, sb, cb;
-        __sincosf(pa_, &sa, &ca);
-        __sincosf(pb_, &sb, &cb);
+        k1_sincos<PRECISE>(v.x * (1.0f / 1024.0f), &sa, &ca);
+        k1_sincos<PRECISE>(v.y * (1.0f / 1024.0f), &sb, &cb);
         float2 fa = da ? make_float2(0.f, 0.f) : make_float2(amp_a * ca, amp_a * sa);
         float2 fb = db ? make_float2(0.f, 0.f) : make_float2(amp_b * cb, amp_b * sb);
         if (!active) return;
@@ -280,7 +298,7 @@ kk_pairs_kernel(const TIn* __restrict__ in, float in_scale, float clamp_rel, int
                 const unsigned Q = static_cast<unsigned>(rot_q), P = static_cast<unsigned>(rot_p);
                 const int ia = static_cast<int>(fmod_u((rot_base + i) * P, Q, inv_q));
                 float sr, cr;
-                __sincosf(reduce_2pi(-two_pi_over_q * static_cast<float>(ia)), &sr, &cr);
+                k1_sincos<PRECISE>(-two_pi_over_q * static_cast<float>(ia), &sr, &cr);
                 rot_cache = make_float2(cr, sr);
             } else {
                 rot_cache = cmul(rot_cache, r256);
@@ -320,13 +338,13 @@ kk_pairs_kernel(const TIn* __restrict__ in, float in_scale, float clamp_rel, int
     if (Ll >= 1 && Ll < kStageHops) {
         for (int i = tid; i < kHop; i += kK1Threads) new_u[i] = S.u[Ll * kHop + i];
         for (int i = tid; i < kHop / 2; i += kK1Threads) {
-            new_a[i] = (hop0 + Ll < 0) ? S.ahist[i] : __expf(S.u[Ll * kHop + kHop / 2 + i]);
+            new_a[i] = (hop0 + Ll < 0) ? S.ahist[i] : k1_exp<PRECISE>(S.u[Ll * kHop + kHop / 2 + i]);
             new_dead[i] = static_cast<uint8_t>(S.dead[Ll]);
         }
     }
 }
 
-template <typename TIn>
+template <typename TIn, bool PRECISE>
 static int launch_k1(const void* in, float in_scale, float clamp_rel, int64_t n_hops, const float* st_u, const float* st_a,
                      const uint8_t* st_dead, float* new_u, float* new_a, uint8_t* new_dead, float2* out,
                      float2* hop_sum, uint8_t* hop_dead, unsigned long long* clamped, int64_t n0,
@@ -334,14 +352,14 @@ static int launch_k1(const void* in, float in_scale, float clamp_rel, int64_t n_
     const float2* tw = twiddle_table_device();
     if (!tw) return KK_ERR_CUDA;
     const size_t smem = sizeof(K1Smem);
-    if (int rc = ensure_smem_attr(reinterpret_cast<const void*>(kk_pairs_kernel<TIn>), smem, "K1 smem attr"))
+    if (int rc = ensure_smem_attr(reinterpret_cast<const void*>(kk_pairs_kernel<TIn, PRECISE>), smem, "K1 smem attr"))
         return rc;
     if (n_hops >= (int64_t(1) << 31)) return set_error(KK_ERR_PARAM, "n_hops must be < 2^31 per call");
     const int64_t pairs = (n_hops + 1) / 2;
     const int64_t grid = (pairs + kPairsPerCta - 1) / kPairsPerCta;
     // the kernel only needs the stream index modulo the rotation period
     const int64_t n0m = rot_q > 0 ? ((n0 % rot_q) + rot_q) % rot_q : 0;
-    kk_pairs_kernel<TIn><<<static_cast<unsigned>(grid), kK1Threads, smem, s>>>(
+    kk_pairs_kernel<TIn, PRECISE><<<static_cast<unsigned>(grid), kK1Threads, smem, s>>>(
         static_cast<const TIn*>(in), in_scale, clamp_rel, n_hops, st_u, st_a, st_dead, new_u, new_a, new_dead, out,
         hop_sum, hop_dead, clamped, n0m, rot_p, rot_q, rot_tab, mirror, tw);
     return check_launch("kk_pairs_kernel");
@@ -363,17 +381,22 @@ extern "C" int kk_reconstruct_pairs(int in_dtype, const void* in, float in_scale
     float2* o = static_cast<float2*>(out);
     float2* hs = static_cast<float2*>(hop_sum);
     const float2* rt = static_cast<const float2*>(rot_tab);
-    switch (in_dtype) {
+    const bool precise = (in_dtype & KK_DTYPE_PRECISE) != 0;
+#define KK_LAUNCH_K1(T, PR)                                                                                    \
+    return launch_k1<T, PR>(in, in_scale, clamp_rel, n_hops, st_u, st_a, st_dead, new_u, new_a, new_dead, o, hs, \
+                            hop_dead, clamped, n0_global, rot_p, rot_q, rt, mirror, s)
+    switch (in_dtype & ~KK_DTYPE_PRECISE) {
         case KK_DTYPE_I16:
-            return launch_k1<int16_t>(in, in_scale, clamp_rel, n_hops, st_u, st_a, st_dead, new_u, new_a, new_dead, o, hs,
-                                      hop_dead, clamped, n0_global, rot_p, rot_q, rt, mirror, s);
+            if (precise) KK_LAUNCH_K1(int16_t, true);
+            KK_LAUNCH_K1(int16_t, false);
         case KK_DTYPE_F32:
-            return launch_k1<float>(in, in_scale, clamp_rel, n_hops, st_u, st_a, st_dead, new_u, new_a, new_dead, o, hs,
-                                    hop_dead, clamped, n0_global, rot_p, rot_q, rt, mirror, s);
+            if (precise) KK_LAUNCH_K1(float, true);
+            KK_LAUNCH_K1(float, false);
         case KK_DTYPE_F64:
-            return launch_k1<double>(in, in_scale, clamp_rel, n_hops, st_u, st_a, st_dead, new_u, new_a, new_dead, o, hs,
-                                     hop_dead, clamped, n0_global, rot_p, rot_q, rt, mirror, s);
+            if (precise) KK_LAUNCH_K1(double, true);
+            KK_LAUNCH_K1(double, false);
         default:
             return set_error(KK_ERR_PARAM, "unsupported input dtype");
     }
+#undef KK_LAUNCH_K1
 }

@@ -58,6 +58,7 @@ from .sigcore import (
     cd_phase_coefficient,
     design_rrc,
     fir_frequency_response,
+    is_signal,
 )
 
 __all__ = [
@@ -106,11 +107,6 @@ class EqualizerState:
         w = np.zeros(n_taps, dtype=np.complex128)
         w[spike_index] = 1.0
         return cls(w=w, g=np.zeros(n_taps, dtype=np.complex128))
-
-    @property
-    def frames_pending(self) -> int:
-        """Asynchronous DDLMS frames submitted but not yet drained."""
-        return len(self._jobs)
 
     @property
     def diverged(self) -> bool:
@@ -276,7 +272,7 @@ def _as_device_input(x, dev):
         c = x.codes
         t = c if isinstance(c, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(c, dtype=np.int16))
         return t.to(dev, non_blocking=True).contiguous(), _lib.KK_DTYPE_I16, float(x.half_lsb)
-    if isinstance(x, RealSignal):
+    if is_signal(x):
         x = x.samples
     if isinstance(x, torch.Tensor):
         if x.dtype == torch.int16:
@@ -403,7 +399,7 @@ def kk_reconstruct(current, plan: BlockPlan, state: dict | None = None, clamp_re
         raise ParameterError("the B200 KK kernel is built for kk_plan.fft_size == 1024")
     fs = getattr(current, "sample_rate_hz", 4e9)
     n = len(current.codes) if isinstance(current, AdcCodes) else len(
-        current.samples if isinstance(current, RealSignal) else current)
+        current.samples if is_signal(current) else current)
     hop = plan.hop
     if n % hop != 0 or n == 0:
         raise ParameterError("chunk length must be a positive multiple of plan.hop")
@@ -423,7 +419,10 @@ def kk_reconstruct(current, plan: BlockPlan, state: dict | None = None, clamp_re
     hs = torch.empty(n_hops, dtype=torch.complex64, device=dev)
     hd = torch.empty(n_hops, dtype=torch.uint8, device=dev)
     cl = torch.zeros(1, dtype=torch.int64, device=dev)
-    _lib.call("kk_reconstruct_pairs", dt, _ptr(x), sc, float(clamp_rel), n_hops, _ptr(su), _ptr(sa), _ptr(sd),
+    # the functional API runs K1's precise variant (correctly rounded
+    # log/exp/sincos; the pipeline uses the SFU approximations)
+    _lib.call("kk_reconstruct_pairs", dt | _lib.KK_DTYPE_PRECISE, _ptr(x), sc, float(clamp_rel), n_hops,
+              _ptr(su), _ptr(sa), _ptr(sd),
               _ptr(nu), _ptr(na), _ptr(nd), _ptr(out), _ptr(hs), _ptr(hd), _ptr(cl), 0, 0, 0, None, 0,
               _stream(dev))
     new_state = {"u_tail": nu.cpu().numpy().astype(np.float64), "a_hist": na.cpu().numpy().astype(np.float64),
@@ -1355,6 +1354,6 @@ class RxPipeline:
 def _len(x) -> int:
     if isinstance(x, AdcCodes):
         return len(x)
-    if isinstance(x, RealSignal):
+    if is_signal(x):
         return len(x.samples)
     return int(x.shape[0]) if hasattr(x, "shape") else len(x)

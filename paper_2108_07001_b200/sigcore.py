@@ -13,15 +13,44 @@ streams never round-trip through host memory.
 
 from __future__ import annotations
 
+import importlib
+import importlib.util
 import json
+import os
 from dataclasses import dataclass, field
 
 import numpy as np
 
 
-class ParameterError(ValueError):
+def kkmodem_class(module: str, name: str):
+    """kkmodem's own class `module.name` when the reference package is
+    importable (so errors raised here are caught by the reference's callers,
+    e.g. runner.py:182 `except (SyncError, SyncFailure)`), else None.
+    KKB200_NO_KKMODEM=1 disables the lookup."""
+    if os.environ.get("KKB200_NO_KKMODEM") == "1":
+        return None
+    try:
+        if importlib.util.find_spec("kkmodem") is None:
+            return None
+        return getattr(importlib.import_module(module), name)
+    except Exception:   # a broken or partial kkmodem install: stand alone
+        return None
+
+
+_KK_PARAMETER_ERROR = kkmodem_class("kkmodem.sigcore", "ParameterError")
+
+
+class ParameterError(*((_KK_PARAMETER_ERROR,) if _KK_PARAMETER_ERROR else (ValueError,))):
     """Raised when an operation receives arguments violating its contract
-    (kkmodem.sigcore.ParameterError, sigcore.py:37)."""
+    (kkmodem.sigcore.ParameterError, sigcore.py:37; a subclass of it when
+    kkmodem is importable)."""
+
+
+def is_signal(x) -> bool:
+    """Duck-typed signal container (this package's or kkmodem's
+    RealSignal/ComplexSignal, sigcore.py:46-99): has .samples and
+    .sample_rate_hz."""
+    return hasattr(x, "samples") and hasattr(x, "sample_rate_hz")
 
 
 def _is_torch(x) -> bool:
@@ -127,7 +156,7 @@ class BlockPlan:
 
 def fir_frequency_response(fir, freqs_hz, rate_hz: float | None = None) -> np.ndarray:
     """DTFT of causal taps at the given frequencies (sigcore.py:217-230)."""
-    if isinstance(fir, FirFilter):
+    if hasattr(fir, "taps") and hasattr(fir, "nominal_rate_hz"):   # this package's or kkmodem's FirFilter
         taps, rate = fir.taps, (fir.nominal_rate_hz if rate_hz is None else rate_hz)
     else:
         if rate_hz is None:

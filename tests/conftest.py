@@ -17,3 +17,7 @@ def pytest_configure(config):
 def golden_names():
     from paper_2108_07001_b200.captures import list_captures
     return list_captures()
+
+
+# run only inside the reference-suite subprocess (tests/test_reference_suite.py)
+collect_ignore = ["reference_switch"]

@@ -111,6 +111,11 @@ for _c in (4.0, 6.0, 8.0, 10.0, 12.0, 14.0):
 CONFIGS["c5_qpsk_10000km_tile"] = (
     cfg_link, dict(order=4, n_spans=100, rel_db=-26.0, cspr_db=10.0, n_symbols=262_000))
 
+# 64-QAM 1,600 km tile (BASELINE configs[2]) for the bench's second format:
+# same k*1000-sample tiling rule
+CONFIGS["c3_64qam_1600km_tile"] = (
+    cfg_link, dict(order=64, n_spans=16, rel_db=-20.0, cspr_db=10.0, n_symbols=262_000))
+
 PREFIX = 1 << 15          # ADC samples of per-stage intermediates kept
 SOFT_KEEP = 1 << 12       # soft symbols kept (head and tail) for soft-value parity
 # configs that also carry per-stage intermediates (size budget)
@@ -250,7 +255,7 @@ def gen_one(name):
         rx_seconds=round(t2 - t1, 2),
         config=cfg.to_dict(),
     )
-    if name == "c5_qpsk_10000km_tile":
+    if name.endswith("_tile"):
         # reference decisions on a 4-tile stream (the bench stream pattern,
         # runner.py:389-391 np.tile) -- checks seams end to end
         reps = 4
