@@ -107,6 +107,12 @@ int kk_static_blocks(const void *z, int64_t z_index0, int64_t hb0, int64_t n_blo
  * rms(head[skip:])}; offset = 2k + parity.  Blocking (one stream sync).
  */
 size_t kk_symbol_sync_scratch_bytes(int64_t n_head, int n_ref);
+/* Non-blocking form: enqueues the same kernels on `stream`; the 4 result
+ * doubles are written to result (device memory or UVA-mapped pinned host
+ * memory) when they complete (B200 addition: the pipeline keeps the device
+ * busy with the rest of the front end while the host waits for the sync). */
+int kk_symbol_sync_enqueue(const void *head, int64_t n_head, const void *ref, int n_ref, int64_t skip,
+                           double *result, void *scratch, size_t scratch_bytes, void *stream);
 int kk_symbol_sync(const void *head, int64_t n_head, const void *ref, int n_ref, int64_t skip,
                    double *result_host, void *scratch, size_t scratch_bytes, void *stream);
 
@@ -141,6 +147,27 @@ int kk_ddlms_solve(const void *x, int64_t nsym, float scale, const void *train, 
                    float mu, int block, int max_iter, float soft_tol, uint8_t *labels, void *soft,
                    float *T_final_host, void *workspace, size_t ws_bytes, int64_t *stats_host,
                    void *stream);
+
+/*
+ * K4 asynchronous form of kk_ddlms_solve (B200 addition): everything is
+ * enqueued on `stream`, nothing is read back, so the host can queue the next
+ * frame / stream while this one runs.  The fixpoint loop runs as a CUDA-graph
+ * WHILE node.  T_io: device float[16], the frame's start taps in, its end taps
+ * out (real 2x8 form); state_io: device int[2] {frozen, div_count} in/out
+ * (rxdsp.py:484-490 guard state); stats_out: device or mapped pinned host
+ * int64[38] (layout of kk_ddlms_solve's stats; [2] = fallback taken: 1 exact
+ * sequential chain on the device, 2 not converged -> chained), may be NULL.
+ * The workspace must stay allocated until the enqueued work completes.
+ * max_iter < 0: cap |max_iter|, and the loop runs as host-driven batches with
+ * readbacks instead of a graph (blocks the calling thread; for worker threads
+ * that solve frames while other streams stream input: instantiating a graph
+ * allocates device memory, which serialises concurrent streams).
+ */
+int kk_ddlms_solve_async(const void *x, int64_t nsym, float scale, const void *train, int64_t n_train,
+                         float *T_io, int *state_io, int order, const float *pts_host, const uint8_t *grid_host,
+                         int grid_m, float norm, float max_radius, float guard_factor, int guard_run, float mu,
+                         int block, int max_iter, float soft_tol, uint8_t *labels, void *soft, void *workspace,
+                         size_t ws_bytes, int64_t *stats_out, void *stream);
 
 /*
  * K4 as a phased solver over one frame, so frames on different GPUs can be

@@ -48,11 +48,14 @@ _SIGS = {
     "kk_static_blocks": ([_P, _I64, _I64, _I64, _I64, _P, _I64, _I, _I, _I, _I, _P, _I, _P, _P, _P, _P], _I),
     "kk_symbol_sync_scratch_bytes": ([_I64, _I], _SZ),
     "kk_symbol_sync": ([_P, _I64, _P, _I, _I64, _P, _P, _SZ, _P], _I),
+    "kk_symbol_sync_enqueue": ([_P, _I64, _P, _I, _I64, _P, _P, _SZ, _P], _I),
     "kk_ddlms_sequential": ([_P, _I64, _F, _I, _P, _I64, _P, _P, _I, _P, _P, _I, _F, _F, _F, _I, _F, _I,
                              _P, _P, _P, _P], _I),
     "kk_ddlms_workspace_bytes": ([_I64, _I], _SZ),
     "kk_ddlms_solve": ([_P, _I64, _F, _P, _I64, _P, _I, _P, _P, _I, _F, _F, _F, _I, _F, _I, _I, _F, _P, _P,
                         _P, _P, _SZ, _P, _P], _I),
+    "kk_ddlms_solve_async": ([_P, _I64, _F, _P, _I64, _P, _P, _I, _P, _P, _I, _F, _F, _F, _I, _F, _I, _I, _F,
+                              _P, _P, _P, _SZ, _P, _P], _I),
     "kk_ddlms_create": ([_P, _I64, _F, _P, _I64, _I, _P, _P, _I, _F, _F, _F, _F, _I, _F, _P, _SZ, _P], _P),
     "kk_ddlms_train": ([_P, _P, _P], _I),
     "kk_ddlms_speculate": ([_P, _P, _P], _I),

@@ -95,16 +95,11 @@ __device__ __forceinline__ int slice(const Slicer& s, float yr, float yi, float&
 // sequential chain, complex form, exact reference semantics (fp32)
 // (used by the functional ddlms_wl API, non-WL mode and fallbacks)
 // ---------------------------------------------------------------------------
-__global__ void ddlms_seq_kernel(const float2* __restrict__ x, int64_t n_out, float scale, int n_taps,
-                                 const float2* __restrict__ train, int64_t n_train, float2* __restrict__ wg,
-                                 int* __restrict__ fz, Slicer sl, float mu, int wl, int guard_run,
-                                 uint8_t* __restrict__ labels, float2* __restrict__ soft,
-                                 float2* __restrict__ dec) {
-    if (threadIdx.x != 0 || blockIdx.x != 0) return;
-    float2 w[16], g[16];
-    for (int i = 0; i < n_taps; ++i) { w[i] = wg[i]; g[i] = wg[n_taps + i]; }
-    int frozen = fz[0];
-    int div = fz[1];
+__device__ __forceinline__ void seq_chain(const float2* __restrict__ x, int64_t n_out, float scale, int n_taps,
+                                          const float2* __restrict__ train, int64_t n_train, float2 (&w)[16],
+                                          float2 (&g)[16], int& frozen, int& div, const Slicer& sl, float mu, int wl,
+                                          int guard_run, uint8_t* __restrict__ labels, float2* __restrict__ soft,
+                                          float2* __restrict__ dec) {
     for (int64_t k = 0; k < n_out; ++k) {
         const float2* xk = x + 2 * k;
         float2 y = make_float2(0.f, 0.f);
@@ -142,9 +137,39 @@ __global__ void ddlms_seq_kernel(const float2* __restrict__ x, int64_t n_out, fl
         if (soft) soft[k] = y;
         if (dec) dec[k] = d;
     }
+}
+
+__global__ void ddlms_seq_kernel(const float2* __restrict__ x, int64_t n_out, float scale, int n_taps,
+                                 const float2* __restrict__ train, int64_t n_train, float2* __restrict__ wg,
+                                 int* __restrict__ fz, Slicer sl, float mu, int wl, int guard_run,
+                                 uint8_t* __restrict__ labels, float2* __restrict__ soft,
+                                 float2* __restrict__ dec) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    float2 w[16], g[16];
+    for (int i = 0; i < n_taps; ++i) { w[i] = wg[i]; g[i] = wg[n_taps + i]; }
+    int frozen = fz[0];
+    int div = fz[1];
+    seq_chain(x, n_out, scale, n_taps, train, n_train, w, g, frozen, div, sl, mu, wl, guard_run, labels, soft, dec);
     for (int i = 0; i < n_taps; ++i) { wg[i] = w[i]; wg[n_taps + i] = g[i]; }
     fz[0] = frozen;
     fz[1] = div;
+}
+
+// WL taps (w, g; 4 taps) <-> real 2x8 form T (rxdsp._T_from_wg / _wg_from_T)
+__device__ __forceinline__ void wg_from_T(const float* T, float inv, float2 (&w)[16], float2 (&g)[16]) {
+    for (int i = 0; i < 4; ++i) {
+        const float a = T[2 * i] * inv, b = T[2 * i + 1] * inv, c = T[8 + 2 * i] * inv, d = T[9 + 2 * i] * inv;
+        w[i] = make_float2((a + d) * 0.5f, (b - c) * 0.5f);
+        g[i] = make_float2((a - d) * 0.5f, -(b + c) * 0.5f);
+    }
+}
+__device__ __forceinline__ void T_from_wg(const float2 (&w)[16], const float2 (&g)[16], float* T) {
+    for (int i = 0; i < 4; ++i) {
+        T[2 * i] = w[i].x + g[i].x;
+        T[2 * i + 1] = w[i].y - g[i].y;
+        T[8 + 2 * i] = -w[i].y - g[i].y;
+        T[9 + 2 * i] = w[i].x - g[i].x;
+    }
 }
 
 // ---------------------------------------------------------------------------
@@ -186,9 +211,16 @@ struct RunOut {
 // Run blocks [b_lo, b_hi) starting from Tstart[b] (or chain them when chain != 0:
 // one thread, block b+1 starts from block b's end taps).  Skip test: re-run a
 // block only if |T_new - T_used|_F * max|X| >= min(margin, soft_tol).
+struct ReadBack;
+__device__ bool fallback_gate(const ReadBack* rb, int64_t& b_lo);
+
 __global__ void ddlms_run_kernel(SolveArgs a, Slicer sl, const float* __restrict__ Tstart,
                                  const float* __restrict__ maxx2, RunOut o, int64_t b_lo, int64_t b_hi,
-                                 int use_skip, float soft_tol, int chain, int first_run) {
+                                 int use_skip, float soft_tol, int chain, int first_run,
+                                 const ReadBack* gate = nullptr) {
+    // gate (asynchronous solve, fallback mode 2): run only then, from the
+    // lowest block whose decisions changed in the last iteration
+    if (gate && !fallback_gate(gate, b_lo)) return;
     int64_t b = b_lo + int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     if (chain) {
         if (blockIdx.x != 0 || threadIdx.x != 0) return;
@@ -305,6 +337,10 @@ constexpr int kModeDecision = 0, kModeOutput = 1, kModeDone = 2;
 #ifndef KK_CASCADE_W
 #define KK_CASCADE_W 8
 #endif
+#ifndef KK_LOOP_UNROLL
+#define KK_LOOP_UNROLL 4
+#endif
+constexpr int kLoopUnroll = KK_LOOP_UNROLL;                    // fixpoint iterations per graph-loop trip
 constexpr int kCascadeW = KK_CASCADE_W;                        // blocks the exact frontier advances per step set
 constexpr unsigned long long kCascadeMaxChanged = 64; // "a cascade": at most this many changed blocks
 constexpr int kMaxStatIters = 64;
@@ -319,25 +355,138 @@ struct ReadBack {
 
 __device__ __forceinline__ bool ctl_done(const int* ctl) { return ctl && *ctl == kModeDone; }
 
+__device__ bool fallback_gate(const ReadBack* rb, int64_t& b_lo) {
+    if (rb->ctl[3] != 2) return false;
+    b_lo = rb->last_first;
+    return true;
+}
+
 // end of one iteration: record its counts, pick the next pass (decision
 // passes until nothing changes, then one output pass; an output pass that
 // changes nothing ends the frame)
-__global__ void ddlms_advance_kernel(ReadBack* rb) {
+// With use_cond the kernel is the last node of the CUDA-graph while loop's
+// body (kk_ddlms_solve_async): it also sets the loop condition (not done,
+// fewer than max_iter iterations).
+__global__ void ddlms_advance_kernel(ReadBack* rb, cudaGraphConditionalHandle loop, int use_cond, int max_iter) {
     const int mode = rb->ctl[0];
-    if (mode == kModeDone) return;
-    const unsigned long long ch = rb->ctr[0], rr = rb->ctr[1];
-    const int it = rb->ctl[1];
-    if (it < kMaxStatIters) {
-        rb->it_stats[2 * it] = ch;
-        rb->it_stats[2 * it + 1] = rr;
+    if (mode != kModeDone) {
+        const unsigned long long ch = rb->ctr[0], rr = rb->ctr[1];
+        const int it = rb->ctl[1];
+        if (it < kMaxStatIters) {
+            rb->it_stats[2 * it] = ch;
+            rb->it_stats[2 * it + 1] = rr;
+        }
+        rb->ctl[1] = it + 1;
+        rb->ctl[0] = ch ? kModeDecision : (mode == kModeOutput ? kModeDone : kModeOutput);
+        rb->last_first = rb->first_changed;
+        rb->first_changed = 0xffffffffu;
+        rb->ctr[0] = 0;
+        rb->ctr[1] = 0;
+        rb->ctr[3] = 0;
     }
-    rb->ctl[1] = it + 1;
-    rb->ctl[0] = ch ? kModeDecision : (mode == kModeOutput ? kModeDone : kModeOutput);
-    rb->last_first = rb->first_changed;
-    rb->first_changed = 0xffffffffu;
-    rb->ctr[0] = 0;
-    rb->ctr[1] = 0;
+    if (use_cond) {
+        if (rb->ctl[0] != kModeDone && rb->ctl[1] >= max_iter) {
+            rb->ctl[3] = 2;              // not converged: the frame takes the chained fallback
+            rb->ctl[0] = kModeDone;      // (the unrolled iterations left in the body return at once)
+        }
+        cudaGraphSetConditional(loop, rb->ctl[0] != kModeDone ? 1u : 0u);
+    }
+}
+
+// ---- asynchronous solve: frame begin / end on the device (no readback) ----
+// frame start taps T_in (unscaled, device) -> Tinit (scaled).  Equalizer
+// state {frozen, div_count} != 0 at the frame start: the affine maps assume
+// live, guard-free taps, so the frame takes the exact sequential chain.
+__global__ void frame_begin_kernel(const float* __restrict__ T_in, float scale, float* __restrict__ Tinit,
+                                   const int* __restrict__ state, ReadBack* rb) {
+    const int i = threadIdx.x;
+    if (i < 16) Tinit[i] = T_in[i] * scale;
+    if (i == 0 && state && (state[0] != 0 || state[1] != 0)) {
+        rb->ctl[0] = kModeDone;
+        rb->ctl[3] = 1;
+    }
+}
+
+__global__ void copy16_kernel(float* __restrict__ dst, const float* __restrict__ src) {
+    if (threadIdx.x < 16) dst[threadIdx.x] = src[threadIdx.x];
+}
+
+// after the loop (guard sum in ctr[2]): fallback mode ctl[3] = 0 none,
+// 1 sequential chain from the frame start (guard exceedances / state),
+// 2 not converged within max_iter -> output pass below the lowest changed
+// block m, chain from m.  ctl[2] gates the mode-2 kernels (kModeOutput: run).
+__global__ void frame_end_kernel(ReadBack* rb) {
+    int fb = rb->ctl[3];
+    if (fb == 0) fb = rb->ctr[2] > 0 ? 1 : (rb->ctl[0] != kModeDone ? 2 : 0);
+    rb->ctl[3] = fb;
+    rb->ctl[2] = fb == 2 ? kModeOutput : kModeDone;
     rb->ctr[3] = 0;
+}
+
+// mode 2: re-run list = blocks [0, m) (their starts are exact: none changed)
+__global__ void fallback_list_kernel(ReadBack* rb, int* __restrict__ list, int64_t nb) {
+    if (rb->ctl[3] != 2) return;
+    const int64_t m = min(static_cast<int64_t>(rb->last_first), nb);
+    for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < m; i += int64_t(gridDim.x) * blockDim.x)
+        list[i] = static_cast<int>(i);
+    if (blockIdx.x == 0 && threadIdx.x == 0) rb->ctr[3] = static_cast<unsigned long long>(m > 0 ? m : 0);
+}
+
+// after the mode-2 chain: guard exceedances there -> mode 1
+__global__ void frame_end2_kernel(ReadBack* rb) {
+    if (rb->ctl[3] == 2 && rb->ctr[2] > 0) rb->ctl[3] = 1;
+}
+
+// mode 1: the exact sequential recurrence (rx:465-498, guard included) over
+// the whole frame from its start taps and state
+__global__ void seq_fallback_kernel(const float2* __restrict__ x, int64_t nsym, float scale,
+                                    const float2* __restrict__ train, int64_t n_train, const float* __restrict__ Tinit,
+                                    float* __restrict__ T_io, int* __restrict__ state_io, Slicer sl, float mu,
+                                    int guard_run, uint8_t* __restrict__ labels, float2* __restrict__ soft,
+                                    const ReadBack* rb) {
+    if (threadIdx.x != 0 || blockIdx.x != 0 || rb->ctl[3] != 1) return;
+    float2 w[16], g[16];
+    wg_from_T(Tinit, 1.0f / scale, w, g);
+    int frozen = state_io ? state_io[0] : 0, div = state_io ? state_io[1] : 0;
+    seq_chain(x, nsym, scale, 4, train, n_train, w, g, frozen, div, sl, mu, 1, guard_run, labels, soft, nullptr);
+    T_from_wg(w, g, T_io);
+    if (state_io) {
+        state_io[0] = frozen;
+        state_io[1] = div;
+    }
+}
+
+// modes 0 / 2: end taps (scaled Tend -> unscaled) and a clear state (no
+// guard exceedance in the frame: div_count ends at 0, taps live)
+__global__ void frame_final_kernel(const ReadBack* rb, float inv_scale, float* __restrict__ T_io,
+                                   int* __restrict__ state_io) {
+    if (rb->ctl[3] == 1) return;
+    const int i = threadIdx.x;
+    if (i < 16) T_io[i] = rb->Tend[i] * inv_scale;
+    if (i == 0 && state_io) {
+        state_io[0] = 0;
+        state_io[1] = 0;
+    }
+}
+
+// statistics of the finished frame -> out[38] (device or mapped host):
+// iterations, blocks run, fallback, guard exceedances, changed blocks in the
+// last iteration, blocks, per-iteration (changed, re-run) for 1..16
+__global__ void frame_stats_kernel(const ReadBack* rb, int64_t nb, int64_t pre_runs, int64_t* __restrict__ out) {
+    if (threadIdx.x != 0) return;
+    const int it = rb->ctl[1];
+    int64_t runs = pre_runs;
+    for (int i = 0; i < min(it, kMaxStatIters); ++i) runs += static_cast<int64_t>(rb->it_stats[2 * i + 1]);
+    out[0] = it;
+    out[1] = runs;
+    out[2] = rb->ctl[3];
+    out[3] = static_cast<int64_t>(rb->ctr[2]);
+    out[4] = (it > 0 && it <= kMaxStatIters) ? static_cast<int64_t>(rb->it_stats[2 * (it - 1)]) : 0;
+    out[5] = nb;
+    for (int i = 0; i < 16; ++i) {
+        out[6 + 2 * i] = i < it ? static_cast<int64_t>(rb->it_stats[2 * i]) : 0;
+        out[7 + 2 * i] = i < it ? static_cast<int64_t>(rb->it_stats[2 * i + 1]) : 0;
+    }
 }
 
 // Decision cascades (64-QAM): late iterations change a few blocks, one block
@@ -348,10 +497,12 @@ __global__ void ddlms_advance_kernel(ReadBack* rb) {
 // frontier W blocks ahead inside one iteration (step = repetition index).
 __global__ void cascade_prep_kernel(ReadBack* rb, const float* __restrict__ Pb, const float* __restrict__ Qb,
                                     const float* __restrict__ Tused, float* __restrict__ Tstart, int* __restrict__ list,
-                                    int64_t nb, int64_t ntb, int W, int step, unsigned long long max_changed) {
+                                    int64_t nb, int64_t ntb, int W, int step, unsigned long long max_changed,
+                                    int from_iter) {
     if (threadIdx.x != 0) return;
     if (step == 0)
-        rb->ctl[2] = (rb->ctl[0] != kModeDone && rb->ctr[0] > 0 && rb->ctr[0] <= max_changed) ? 1 : 0;
+        rb->ctl[2] = (rb->ctl[0] != kModeDone && rb->ctl[1] >= from_iter && rb->ctr[0] > 0 &&
+                      rb->ctr[0] <= max_changed) ? 1 : 0;
     rb->ctr[3] = 0;
     if (!rb->ctl[2]) return;
     const int64_t m = rb->first_changed;
@@ -468,12 +619,23 @@ ddlms_block_kernel(SolveArgs a, Slicer sl, const float* __restrict__ Tstart, flo
                    float* __restrict__ maxx2, RunOut o, TOut to, int64_t b_lo, int64_t b_hi, int use_skip,
                    float soft_tol, const int* __restrict__ list, const unsigned long long* __restrict__ list_n,
                    int write_out, const int* __restrict__ ctl) {
-    if (ctl) {   // device-driven pass mode
+    // write_out: bit 0 = store the block's outputs (soft, labels, Twritten)
+    // when it runs; bit 1 = also re-run blocks whose outputs are stale (start
+    // moved > soft_tol since they were written: output passes)
+    // (storing in decision passes too was measured not to pay: the first
+    // decision pass moves nearly every block's start by more than soft_tol,
+    // so the output pass re-ran 485 k of 524 k blocks anyway)
+    if (ctl) {   // device-driven pass mode: only output passes store (and refresh)
         const int mode = *ctl;
         if (mode == kModeDone) return;
-        write_out = mode == kModeOutput;
-        if (!write_out) soft_tol = 3.0e38f;
+        if (WITH_P) {
+            write_out = 0;
+        } else {
+            write_out = mode == kModeOutput ? 3 : 0;
+            if (mode != kModeOutput) soft_tol = 3.0e38f;
+        }
     }
+    const bool refresh = (write_out & 2) != 0;
     __shared__ float2 pts[64];
     __shared__ uint8_t grid[64];
     extern __shared__ float4 dyn_sm[];
@@ -513,8 +675,8 @@ ddlms_block_kernel(SolveArgs a, Slicer sl, const float* __restrict__ Tstart, flo
                 d2 = fmaf(d, d, d2);
             }
             const float bound = sqrtf(d2 * maxx2[b]);
-            run = !(bound < fminf(o.margin[b], write_out ? 3.0e38f : soft_tol)) || (a.mu * maxx2[b] > 1.0f);
-            if (write_out) {   // outputs valid within soft_tol since their last write?
+            run = !(bound < fminf(o.margin[b], refresh ? 3.0e38f : soft_tol)) || (a.mu * maxx2[b] > 1.0f);
+            if (refresh) {   // outputs valid within soft_tol since their last write?
                 float w2 = 0.f;
 #pragma unroll
                 for (int i = 0; i < 16; ++i) {
@@ -705,7 +867,7 @@ ddlms_block_kernel(SolveArgs a, Slicer sl, const float* __restrict__ Tstart, flo
             soft8[j] = make_float2(yr, yi);
             lab8[j >> 2] |= static_cast<unsigned>(lab & 0xff) << (8 * (j & 3));
         }
-        if (!WITH_P && write_out) {   // outputs only from the final (full) pass
+        if (!WITH_P && (write_out & 1)) {   // outputs from output passes
             const int i0 = c * kChunkRows;
             // vector stores need 16 B (soft) / 8 B (labels) alignment of the
             // run: block starts k0 = b B are multiples of 8 when B is
@@ -748,7 +910,7 @@ ddlms_block_kernel(SolveArgs a, Slicer sl, const float* __restrict__ Tstart, flo
             }
 #pragma unroll
         for (int i = 0; i < 16; ++i) o.Tused[b * 16 + i] = Tstart[b * 16 + i];
-        if (!WITH_P && write_out) {
+        if (!WITH_P && (write_out & 1)) {
 #pragma unroll
             for (int i = 0; i < 16; ++i) o.Twritten[b * 16 + i] = Tstart[b * 16 + i];
         }
@@ -1090,11 +1252,20 @@ __global__ void bit_errors_kernel(const uint8_t* __restrict__ lab, const uint8_t
     const uint4* R4 = reinterpret_cast<const uint4*>(ref);
     const bool aligned = ((reinterpret_cast<uintptr_t>(lab) | reinterpret_cast<uintptr_t>(ref)) & 15) == 0;
     const int64_t stride = int64_t(gridDim.x) * blockDim.x;
-    for (int64_t t = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; t < (aligned ? n16 : 0); t += stride) {
+    const int64_t t0 = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    // seam phase of the thread's first run, then advanced by 16 * stride
+    // (mod period) per trip: one 64-bit modulo per thread, not per trip
+    int64_t ph_run = ex_period > 0 ? (16 * t0 + ex_phase) % ex_period : 0;
+    const int64_t ph_step = ex_period > 0 ? (16 * stride) % ex_period : 0;
+    for (int64_t t = t0; t < (aligned ? n16 : 0); t += stride) {
         const uint4 a4 = L4[t], b4 = R4[t];
         const uint8_t* a = reinterpret_cast<const uint8_t*>(&a4);
         const uint8_t* b = reinterpret_cast<const uint8_t*>(&b4);
-        int64_t ph = ex_period > 0 ? (16 * t + ex_phase) % ex_period : 0;
+        int64_t ph = ph_run;
+        if (ex_period > 0) {
+            ph_run += ph_step;
+            if (ph_run >= ex_period) ph_run -= ex_period;
+        }
 #pragma unroll
         for (int u = 0; u < 16; ++u) {
             const bool skip = ex_period > 0 && ph >= ex_period - ex_len;
@@ -1213,18 +1384,52 @@ __global__ void readback_kernel(const uint4* __restrict__ src, uint4* __restrict
     for (int i = threadIdx.x; i < n16; i += blockDim.x) dst[i] = src[i];
 }
 
-static int d2h_small(void* dst, const void* src, size_t bytes, cudaStream_t s) {
-    static thread_local void* pin = nullptr;
-    static thread_local void* pin_dev = nullptr;
-    constexpr size_t kPin = 64 << 10;
-    if (bytes > kPin) return set_error(KK_ERR_PARAM, "d2h_small: too large");
-    if (!pin) {
-        if (cudaHostAlloc(&pin, kPin, cudaHostAllocMapped) != cudaSuccess ||
-            cudaHostGetDevicePointer(&pin_dev, pin, 0) != cudaSuccess) {
-            pin = pin_dev = nullptr;
-            return set_cuda_error("mapped pinned staging");
+// Mapped pinned staging buffers for small readbacks, pooled process-wide:
+// a call borrows one for its duration (threads never share one at a time),
+// so the number allocated is bounded by the peak number of concurrent
+// readers and no buffer is allocated per pipeline / worker thread.
+namespace {
+struct PinBuf {
+    void* host = nullptr;
+    void* dev = nullptr;
+};
+std::mutex g_pin_mu;
+std::vector<PinBuf> g_pin_free;
+constexpr size_t kPin = 64 << 10;
+
+struct PinLease {
+    PinBuf b;
+    int rc = KK_OK;
+    PinLease() {
+        {
+            std::lock_guard<std::mutex> lk(g_pin_mu);
+            if (!g_pin_free.empty()) {
+                b = g_pin_free.back();
+                g_pin_free.pop_back();
+                return;
+            }
+        }
+        if (cudaHostAlloc(&b.host, kPin, cudaHostAllocMapped) != cudaSuccess ||
+            cudaHostGetDevicePointer(&b.dev, b.host, 0) != cudaSuccess) {
+            b = PinBuf{};
+            rc = set_cuda_error("mapped pinned staging");
         }
     }
+    ~PinLease() {
+        if (b.host) {
+            std::lock_guard<std::mutex> lk(g_pin_mu);
+            g_pin_free.push_back(b);
+        }
+    }
+};
+}  // namespace
+
+static int d2h_small(void* dst, const void* src, size_t bytes, cudaStream_t s) {
+    if (bytes > kPin) return set_error(KK_ERR_PARAM, "d2h_small: too large");
+    PinLease lease;
+    if (lease.rc) return lease.rc;
+    void* pin = lease.b.host;
+    void* pin_dev = lease.b.dev;
     if ((reinterpret_cast<uintptr_t>(src) & 15) == 0) {
         const int n16 = static_cast<int>((bytes + 15) / 16);   // src regions are 256 B-aligned workspace slots
         readback_kernel<<<1, 256, 0, s>>>(static_cast<const uint4*>(src), static_cast<uint4*>(pin_dev), n16);
@@ -1421,7 +1626,7 @@ struct DdlmsSolver {
             const size_t smem = train_blocks ? kStageSmem + kTrainSmem : kStageSmem;
             auto go = [&](auto kern) {
                 kern<<<g, kBlockThreads, smem, s>>>(a, sl, lv[0].T, lv[0].P, maxx2, o, to, lo, hi, skip, tol, lst,
-                                                    lst_n, write_out, with_p ? nullptr : ctl_d);
+                                                    lst_n, write_out, ctl_d);
             };
 #define KK_DD_GO3(P_, S_, T_) (al ? go(ddlms_block_kernel<P_, S_, true, T_>) : go(ddlms_block_kernel<P_, S_, false, T_>))
 #define KK_DD_GO(P_, S_) (train_blocks ? KK_DD_GO3(P_, S_, true) : KK_DD_GO3(P_, S_, false))
@@ -1450,7 +1655,8 @@ struct DdlmsSolver {
             // compact the blocks to re-run so that warps only carry live chains
             const unsigned g = static_cast<unsigned>((b1 - d0 + 127) / 128);
             ddlms_select_kernel<<<g, 128, 0, s>>>(lv[0].T, Tused, margin, maxx2, a.mu, d0, b1, tol,
-                                                  (write_out || ctl_d) ? Twritten : nullptr, list, ctr + 3, ctl_d);
+                                                  ((write_out & 2) || ctl_d) ? Twritten : nullptr, list, ctr + 3,
+                                                  ctl_d);
             if (int rc = check_launch("ddlms_select_kernel")) return rc;
             return launch(false, d0, b1, 0, list, ctr + 3);
         }
@@ -1469,6 +1675,7 @@ struct DdlmsSolver {
         L = plan(nsym, block);
         if (ws_bytes < L.bytes) return set_error(KK_ERR_PARAM, "workspace too small");
         char* w = static_cast<char*>(workspace);
+        ws_base = workspace;
         lv.resize(L.n.size());
         for (size_t l = 0; l < L.n.size(); ++l) {
             lv[l].n = L.n[l];
@@ -1587,19 +1794,19 @@ struct DdlmsSolver {
             cudaMemsetAsync(&rb->first_changed, 0xFF, sizeof(unsigned int), s) != cudaSuccess)
             return set_cuda_error("ctr");
         // decision pass: compacted re-run of the blocks whose certified margin
-        // the start move could cross, no outputs; output pass: the blocks
+        // the start move could cross, no outputs; output pass: also the blocks
         // whose outputs are missing or were written from a start more than
         // soft_tol away (the first output pass of a frame runs every block; a
         // later one, after a late decision change, only its wake)
-        if (int rc = soft_pass ? run_blocks(false, 0, L.nb, 1, soft_tol, 1)
+        if (int rc = soft_pass ? run_blocks(false, 0, L.nb, 1, soft_tol, 3)
                                : run_blocks(false, 0, L.nb, 1, 3.0e38f, 0))
             return rc;
         // decision cascades: as in solve_loop (rb->ctl[0] stays "decision" here)
-        for (int step = 0; iters >= 4 && step < kCascadeW; ++step) {
+        for (int step = 0; iters >= KK_CASCADE_FROM && step < kCascadeW; ++step) {
             cascade_prep_kernel<<<1, 32, 0, s>>>(rb, lv[0].P, lv[0].Q, Tused, lv[0].T, list, L.nb, ntb, kCascadeW,
-                                                 step, kCascadeMaxChanged);
+                                                 step, kCascadeMaxChanged, 0);
             if (int rc = check_launch("cascade_prep_kernel")) return rc;
-            if (int rc = run_blocks(false, 0, kCascadeW, 0, soft_pass ? soft_tol : 3.0e38f, soft_pass ? 1 : 0, list))
+            if (int rc = run_blocks(false, 0, kCascadeW, 0, soft_pass ? soft_tol : 3.0e38f, soft_pass ? 3 : 0, list))
                 return rc;
         }
         unsigned long long h[4];
@@ -1618,12 +1825,13 @@ struct DdlmsSolver {
     // ddlms_advance_kernel): one host readback per batch, not per pass.  On
     // convergence the guard count and end taps come back in the same read.
     int solve_loop(const float* T_start, int max_iter, int64_t* it_stats, bool* converged, int64_t* guard,
-                   float* T_final) {
+                   float* T_final, bool reset = true) {
         if (!speculated) return set_error(KK_ERR_PARAM, "speculate() must precede solve_loop()");
-        if (int rc = set_start(T_start)) return rc;
-        if (cudaMemsetAsync(ctr, 0, 4 * sizeof(unsigned long long), s) != cudaSuccess ||
-            cudaMemsetAsync(rb->ctl, 0, sizeof(rb->ctl), s) != cudaSuccess ||
-            cudaMemsetAsync(&rb->first_changed, 0xFF, 2 * sizeof(unsigned int), s) != cudaSuccess)
+        if (T_start)
+            if (int rc = set_start(T_start)) return rc;
+        if (reset && (cudaMemsetAsync(ctr, 0, 4 * sizeof(unsigned long long), s) != cudaSuccess ||
+                      cudaMemsetAsync(rb->ctl, 0, sizeof(rb->ctl), s) != cudaSuccess ||
+                      cudaMemsetAsync(&rb->first_changed, 0xFF, 2 * sizeof(unsigned int), s) != cudaSuccess))
             return set_cuda_error("solve_loop init");
         *converged = false;
         ReadBack h;
@@ -1635,18 +1843,18 @@ struct DdlmsSolver {
             int rc = KK_OK;
             for (int i = 0; i < n && rc == KK_OK; ++i) {
                 rc = scan_down();
-                if (rc == KK_OK) rc = run_blocks(false, 0, L.nb, 1, soft_tol, 1);
+                if (rc == KK_OK) rc = run_blocks(false, 0, L.nb, 1, soft_tol, 3);
                 // cascade window steps from the fifth iteration on (frames that
                 // converge in four, the QPSK/16-QAM norm, never queue them)
                 for (int step = 0; rc == KK_OK && queued + i >= KK_CASCADE_FROM && step < kCascadeW; ++step) {
                     cascade_prep_kernel<<<1, 32, 0, s>>>(rb, lv[0].P, lv[0].Q, Tused, lv[0].T, list, L.nb, ntb,
-                                                         kCascadeW, step, kCascadeMaxChanged);
+                                                         kCascadeW, step, kCascadeMaxChanged, 0);
                     rc = check_launch("cascade_prep_kernel");
-                    if (rc == KK_OK) rc = run_blocks(false, 0, kCascadeW, 0, soft_tol, 1, list);
+                    if (rc == KK_OK) rc = run_blocks(false, 0, kCascadeW, 0, soft_tol, 3, list);
                 }
                 if (rc == KK_OK) rc = scan_up(false);
                 if (rc == KK_OK) {
-                    ddlms_advance_kernel<<<1, 1, 0, s>>>(rb);
+                    ddlms_advance_kernel<<<1, 1, 0, s>>>(rb, cudaGraphConditionalHandle{}, 0, 0);
                     rc = check_launch("ddlms_advance_kernel");
                 }
             }
@@ -1689,6 +1897,230 @@ struct DdlmsSolver {
         return KK_OK;
     }
 
+    // ---- asynchronous solve (kk_ddlms_solve_async): everything enqueued,
+    // nothing read back; the fixpoint loop is a CUDA-graph WHILE node whose
+    // condition the iteration's advance kernel sets (no pre-queued idle
+    // iterations, no host round trip per batch) ----
+    cudaGraphExec_t loop_exec = nullptr;
+    bool loop_exec_cached = false;   // owned by the process-wide cache below
+    void* ws_base = nullptr;
+
+    static cudaStream_t capture_stream() {
+        static thread_local cudaStream_t cs = nullptr;
+        if (!cs && cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking) != cudaSuccess) cs = nullptr;
+        return cs;
+    }
+
+    // one fixpoint iteration, as in solve_loop (mode from rb->ctl[0])
+    int one_iteration(cudaGraphConditionalHandle h, int max_iter) {
+        if (int rc = scan_down()) return rc;
+        if (int rc = run_blocks(false, 0, L.nb, 1, soft_tol, 3)) return rc;
+        for (int step = 0; step < kCascadeW; ++step) {
+            cascade_prep_kernel<<<1, 32, 0, s>>>(rb, lv[0].P, lv[0].Q, Tused, lv[0].T, list, L.nb, ntb, kCascadeW,
+                                                 step, kCascadeMaxChanged, KK_CASCADE_FROM);
+            if (int rc = check_launch("cascade_prep_kernel")) return rc;
+            if (int rc = run_blocks(false, 0, kCascadeW, 0, soft_tol, 3, list)) return rc;
+        }
+        if (int rc = scan_up(false)) return rc;
+        ddlms_advance_kernel<<<1, 1, 0, s>>>(rb, h, 1, max_iter);
+        return check_launch("ddlms_advance_kernel");
+    }
+
+    // Instantiated loop graphs are cached by everything their kernels' launch
+    // parameters depend on (a repeated frame of the same shape on the same
+    // workspace -- every step of a device-resident stream -- reuses its
+    // graph): instantiation costs ~0.4 ms of host time and allocates device
+    // memory, which serialises concurrent streams.
+    std::vector<uint64_t> loop_key(int max_iter) const {
+        auto f2u = [](float v) { uint32_t u; std::memcpy(&u, &v, 4); return static_cast<uint64_t>(u); };
+        std::vector<uint64_t> k = {
+            reinterpret_cast<uint64_t>(a.x), static_cast<uint64_t>(a.nsym), reinterpret_cast<uint64_t>(a.train),
+            static_cast<uint64_t>(a.n_train), f2u(a.mu), f2u(a.scale), static_cast<uint64_t>(a.B),
+            static_cast<uint64_t>(a.nb), reinterpret_cast<uint64_t>(ws_base), reinterpret_cast<uint64_t>(to.LT),
+            reinterpret_cast<uint64_t>(to.ST), f2u(soft_tol), static_cast<uint64_t>(max_iter),
+            static_cast<uint64_t>(ntb), static_cast<uint64_t>(bt),
+            static_cast<uint64_t>(sl.kind), static_cast<uint64_t>(sl.npts), static_cast<uint64_t>(sl.m),
+            f2u(sl.norm), f2u(sl.thr), static_cast<uint64_t>(sl.sep), f2u(sl.lev_h)};
+        for (int i = 0; i < 64; ++i) k.push_back(f2u(sl.pts[i].x) << 32 | f2u(sl.pts[i].y));
+        for (int i = 0; i < 64; i += 8) {
+            uint64_t g = 0;
+            for (int j = 0; j < 8; ++j) g |= static_cast<uint64_t>(sl.grid[i + j]) << (8 * j);
+            k.push_back(g);
+        }
+        int dev = -1;
+        cudaGetDevice(&dev);
+        k.push_back(static_cast<uint64_t>(dev));
+        return k;
+    }
+
+    int build_loop(int max_iter) {
+        static std::mutex mu;
+        static std::vector<std::pair<std::vector<uint64_t>, cudaGraphExec_t>> cache;   // most recent last
+        const std::vector<uint64_t> key = loop_key(max_iter);
+        {
+            std::lock_guard<std::mutex> lk(mu);
+            for (size_t i = 0; i < cache.size(); ++i)
+                if (cache[i].first == key) {
+                    loop_exec = cache[i].second;
+                    loop_exec_cached = true;
+                    std::rotate(cache.begin() + i, cache.begin() + i + 1, cache.end());
+                    return KK_OK;
+                }
+        }
+        if (int rc = instantiate_loop(max_iter)) return rc;
+        std::lock_guard<std::mutex> lk(mu);
+        if (cache.size() >= 16) {
+            cudaGraphExecDestroy(cache.front().second);   // an in-flight launch completes first
+            cache.erase(cache.begin());
+        }
+        cache.emplace_back(key, loop_exec);
+        loop_exec_cached = true;
+        return KK_OK;
+    }
+
+    int instantiate_loop(int max_iter) {
+        cudaGraph_t g = nullptr;
+        if (cudaGraphCreate(&g, 0) != cudaSuccess) return set_cuda_error("graph create");
+        struct GraphGuard {
+            cudaGraph_t g;
+            ~GraphGuard() { if (g) cudaGraphDestroy(g); }
+        } gg{g};
+        cudaGraphConditionalHandle h;
+        if (cudaGraphConditionalHandleCreate(&h, g, 1, cudaGraphCondAssignDefault) != cudaSuccess)
+            return set_cuda_error("graph conditional handle");
+        cudaGraphNodeParams np = {};
+        np.type = cudaGraphNodeTypeConditional;
+        np.conditional.handle = h;
+        np.conditional.type = cudaGraphCondTypeWhile;
+        np.conditional.size = 1;
+        cudaGraphNode_t node;
+        if (cudaGraphAddNode(&node, g, nullptr, 0, &np) != cudaSuccess) return set_cuda_error("graph while node");
+        cudaGraph_t body = np.conditional.phGraph_out[0];
+        cudaStream_t cs = capture_stream();
+        if (!cs) return set_cuda_error("capture stream");
+        const cudaStream_t s_run = s;
+        if (cudaStreamBeginCaptureToGraph(cs, body, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed) != cudaSuccess)
+            return set_cuda_error("begin capture");
+        s = cs;
+        // the body holds kLoopUnroll iterations: each trip of a graph WHILE
+        // loop costs ~70 us of device-side scheduling (measured), each idle
+        // unrolled iteration ~30 kernels that return at once (~1 us each)
+        int rc = KK_OK;
+        for (int u = 0; u < kLoopUnroll && rc == KK_OK; ++u) rc = one_iteration(h, max_iter);
+        s = s_run;
+        cudaGraph_t captured = nullptr;
+        const cudaError_t ec = cudaStreamEndCapture(cs, &captured);
+        if (rc) return rc;
+        if (ec != cudaSuccess) return set_cuda_error("end capture");
+        if (cudaGraphInstantiate(&loop_exec, g, 0) != cudaSuccess) {
+            loop_exec = nullptr;
+            return set_cuda_error("graph instantiate");
+        }
+        return KK_OK;
+    }
+
+    int solve_async(float* T_io, int* state_io, int max_iter, int guard_run, float mu_raw, int64_t* stats_out,
+                    uint8_t* labels, float2* soft, bool use_graph) {
+        ctl_d = rb->ctl;
+        if (cudaMemsetAsync(rb, 0, sizeof(ReadBack), s) != cudaSuccess ||
+            cudaMemsetAsync(&rb->first_changed, 0xFF, 2 * sizeof(unsigned int), s) != cudaSuccess)
+            return set_cuda_error("solve_async init");
+        frame_begin_kernel<<<1, 32, 0, s>>>(T_io, scale, Tinit_d, state_io, rb);
+        if (int rc = check_launch("frame_begin_kernel")) return rc;
+        // pure training blocks (exact from the frame start), then the first
+        // pass of the decision-directed blocks from the training-end taps
+        if (int rc = fill_T(0, L.nb, Tinit_d)) return rc;
+        if (bt > 0) {
+            if (int rc = run_blocks(true, 0, bt, 0)) return rc;
+            if (bt < L.nb &&
+                cudaMemsetAsync(lv[0].Q + bt * 16, 0, (L.nb - bt) * 16 * sizeof(float), s) != cudaSuccess)
+                return set_cuda_error("Q init");
+            if (int rc = scan_up(true)) return rc;
+            if (int rc = scan_down()) return rc;
+        }
+        if (bt < L.nb) {
+            copy16_kernel<<<1, 32, 0, s>>>(Tend, bt > 0 ? lv[0].T + bt * 16 : Tinit_d);
+            if (int rc = check_launch("copy16_kernel")) return rc;
+            if (int rc = fill_T(bt, L.nb, Tend)) return rc;
+            if (int rc = run_blocks(true, bt, L.nb, 0)) return rc;
+        }
+        if (int rc = scan_up(true)) return rc;
+        speculated = true;
+        if (cudaMemsetAsync(ctr, 0, 4 * sizeof(unsigned long long), s) != cudaSuccess ||
+            cudaMemsetAsync(&rb->first_changed, 0xFF, sizeof(unsigned int), s) != cudaSuccess)
+            return set_cuda_error("solve_async counters");
+        if (!use_graph) {
+            // host-driven batches with readbacks (blocks the calling thread):
+            // for frames solved by a worker thread while other streams work --
+            // instantiating a graph allocates device memory, which serialises
+            // the other streams (measured: e2e 6.3 -> 4.3 GBaud)
+            bool conv = false;
+            if (int rc = solve_loop(nullptr, max_iter, nullptr, &conv, nullptr, nullptr, false)) return rc;
+            ctl_d = rb->ctl;
+        } else {
+            static const bool trace = [] {
+                const char* e = std::getenv("KK_DDLMS_TRACE");
+                return e && e[0] == '1';
+            }();
+            const auto t0 = std::chrono::steady_clock::now();
+            if (int rc = build_loop(max_iter)) return rc;
+            const auto t1 = std::chrono::steady_clock::now();
+            if (cudaGraphLaunch(loop_exec, s) != cudaSuccess) return set_cuda_error("graph launch");
+            if (trace)
+                std::fprintf(stderr, "[kk_ddlms_solve_async] nsym %lld: loop graph build %.3f ms, launch %.3f ms\n",
+                             static_cast<long long>(a.nsym),
+                             std::chrono::duration<double, std::milli>(t1 - t0).count(),
+                             std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t1).count());
+        }
+        // epilogue: guard sum, fallback decision and the fallback paths (each
+        // kernel returns at once unless its mode was chosen)
+        const int64_t gblocks = std::min<int64_t>((L.nb + 127) / 128, 148 * 8);
+        if (cudaMemsetAsync(ctr + 2, 0, sizeof(unsigned long long), s) != cudaSuccess)
+            return set_cuda_error("ctr");
+        sum_int_kernel<<<static_cast<unsigned>(gblocks), 128, 0, s>>>(over, L.nb, ctr + 2);
+        if (int rc = check_launch("sum_int_kernel")) return rc;
+        frame_end_kernel<<<1, 1, 0, s>>>(rb);
+        if (int rc = check_launch("frame_end_kernel")) return rc;
+        // mode 2 (not converged): output pass of [0, m), chain from m
+        {
+            const int* save = ctl_d;
+            ctl_d = &rb->ctl[2];   // kModeOutput in mode 2, kModeDone otherwise
+            fallback_list_kernel<<<static_cast<unsigned>(std::min<int64_t>((L.nb + 255) / 256, 1024)), 256, 0, s>>>(
+                rb, list, L.nb);
+            int rc = check_launch("fallback_list_kernel");
+            if (rc == KK_OK) rc = scan_down();
+            if (rc == KK_OK) rc = run_blocks(false, 0, L.nb, 0, soft_tol, 3, list);
+            ctl_d = save;
+            if (rc) return rc;
+            o.labels = to.LT;
+            o.soft = to.ST;
+            ddlms_run_kernel<<<1, 1, 0, s>>>(a, sl, lv[0].T, maxx2, o, 0, L.nb, 0, soft_tol, 1, 1, rb);
+            if (int rc2 = check_launch("ddlms_run_kernel chain")) return rc2;
+            if (cudaMemsetAsync(ctr + 2, 0, sizeof(unsigned long long), s) != cudaSuccess)
+                return set_cuda_error("ctr");
+            sum_int_kernel<<<static_cast<unsigned>(gblocks), 128, 0, s>>>(over, L.nb, ctr + 2);
+            if (int rc2 = check_launch("sum_int_kernel")) return rc2;
+            frame_end2_kernel<<<1, 1, 0, s>>>(rb);
+            if (int rc2 = check_launch("frame_end2_kernel")) return rc2;
+        }
+        // mode 1: the exact sequential chain over the frame
+        seq_fallback_kernel<<<1, 1, 0, s>>>(a.x, a.nsym, scale, a.train, a.n_train, Tinit_d, T_io, state_io, sl,
+                                            mu_raw, guard_run, to.LT, to.ST, rb);
+        if (int rc = check_launch("seq_fallback_kernel")) return rc;
+        frame_final_kernel<<<1, 32, 0, s>>>(rb, 1.0f / scale, T_io, state_io);
+        if (int rc = check_launch("frame_final_kernel")) return rc;
+        if (stats_out) {
+            frame_stats_kernel<<<1, 32, 0, s>>>(rb, L.nb, L.nb, stats_out);
+            if (int rc = check_launch("frame_stats_kernel")) return rc;
+        }
+        ctl_d = nullptr;
+        return copy_outputs(labels, soft);
+    }
+
+    ~DdlmsSolver() {
+        if (loop_exec && !loop_exec_cached) cudaGraphExecDestroy(loop_exec);   // freed after an in-flight launch
+    }
+
     int copy_outputs(uint8_t* labels, float2* soft) {
         if (labels && labels != to.LT &&
             cudaMemcpyAsync(labels, to.LT, size_t(a.nsym), cudaMemcpyDeviceToDevice, s) != cudaSuccess)
@@ -1711,7 +2143,7 @@ struct DdlmsSolver {
         o.soft = soft;
         if (int rc = scan_down()) return rc;
         if (m > 0) {
-            if (int rc = run_blocks(false, 0, m, 1, soft_tol, 1)) return rc;
+            if (int rc = run_blocks(false, 0, m, 1, soft_tol, 3)) return rc;
             const size_t n0 = static_cast<size_t>(std::min<int64_t>(m * a.B, a.nsym));
             if (labels && labels != to.LT &&
                 cudaMemcpyAsync(labels, to.LT, n0, cudaMemcpyDeviceToDevice, s) != cudaSuccess)
@@ -1883,17 +2315,45 @@ extern "C" int kk_ddlms_solve(const void* x, int64_t nsym, float scale, const vo
     return KK_OK;
 }
 
-extern "C" int kk_symbol_sync(const void* head, int64_t n_head, const void* ref, int n_ref, int64_t skip,
-                              double* result, void* scratch, size_t scratch_bytes, void* stream) {
+// Asynchronous single-frame exact solve: enqueued on `stream`, nothing read
+// back.  T_io (device float[16], unscaled real 2x8 form) holds the frame's
+// start taps and receives its end taps; state_io (device int[2] = {frozen,
+// div_count}) likewise; stats_out (device or mapped host int64[38], may be
+// NULL) receives the statistics of kk_ddlms_solve.  Guard exceedances, a
+// non-clear state at the frame start and non-convergence fall back to exact
+// chains on the device.  The workspace must stay valid until the stream
+// reaches the end of the enqueued work.
+extern "C" int kk_ddlms_solve_async(const void* x, int64_t nsym, float scale, const void* train, int64_t n_train,
+                                    float* T_io, int* state_io, int order, const float* pts_host,
+                                    const uint8_t* grid_host, int grid_m, float norm, float max_radius,
+                                    float guard_factor, int guard_run, float mu, int block, int max_iter,
+                                    float soft_tol, uint8_t* labels, void* soft, void* workspace, size_t ws_bytes,
+                                    int64_t* stats_out, void* stream) {
     clear_error();
-    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    if (nsym <= 0) return KK_OK;
+    if (!T_io) return set_error(KK_ERR_PARAM, "T_io missing");
+    if (max_iter == 0) return set_error(KK_ERR_PARAM, "max_iter must be nonzero");
+    DdlmsSolver sv;
+    if (int rc = make_solver(sv, x, nsym, scale, train, n_train, order, pts_host, grid_host, grid_m, norm,
+                             max_radius, guard_factor, mu, block, soft_tol, workspace, ws_bytes,
+                             static_cast<cudaStream_t>(stream)))
+        return rc;
+    sv.bind_outputs(labels, static_cast<float2*>(soft));
+    const bool use_graph = max_iter > 0;
+    return sv.solve_async(T_io, state_io, max_iter > 0 ? max_iter : -max_iter, guard_run, mu, stats_out, labels,
+                          static_cast<float2*>(soft), use_graph);
+}
+
+// enqueue the sync kernels; the 4 result doubles land in `res` (device or
+// UVA-mapped pinned host memory)
+static int symbol_sync_launch(const void* head, int64_t n_head, const void* ref, int n_ref, int64_t skip,
+                              double* res_out, void* scratch, size_t scratch_bytes, cudaStream_t s) {
     const int64_t l0 = (n_head + 1) / 2, l1 = n_head / 2;
     const int64_t nl0 = (ref && n_ref > 0 && l0 >= n_ref) ? l0 - n_ref + 1 : 0;
     const int64_t nl1 = (ref && n_ref > 0 && l1 >= n_ref) ? l1 - n_ref + 1 : 0;
     const size_t need = (nl0 + nl1 + 4) * sizeof(double) + 256;
     if (scratch_bytes < need) return set_error(KK_ERR_PARAM, "sync scratch too small");
     double* mag = static_cast<double*>(scratch);
-    double* res = mag + ((nl0 + nl1 + 31) / 32) * 32;
     if (nl0 + nl1 > 0) {
         const int th = 256;
         const size_t sm = static_cast<size_t>(n_ref) * sizeof(float2);
@@ -1905,8 +2365,27 @@ extern "C" int kk_symbol_sync(const void* head, int64_t n_head, const void* ref,
             static_cast<const float2*>(head), n_head, static_cast<const float2*>(ref), n_ref, nl0, nl1, mag);
         if (int rc = check_launch("xcorr_kernel")) return rc;
     }
-    sync_reduce_kernel<<<1, 1024, 0, s>>>(mag, nl0, nl1, static_cast<const float2*>(head), n_head, skip, res);
-    if (int rc = check_launch("sync_reduce_kernel")) return rc;
+    sync_reduce_kernel<<<1, 1024, 0, s>>>(mag, nl0, nl1, static_cast<const float2*>(head), n_head, skip, res_out);
+    return check_launch("sync_reduce_kernel");
+}
+
+extern "C" int kk_symbol_sync_enqueue(const void* head, int64_t n_head, const void* ref, int n_ref, int64_t skip,
+                                      double* result, void* scratch, size_t scratch_bytes, void* stream) {
+    clear_error();
+    if (!result) return set_error(KK_ERR_PARAM, "result pointer missing");
+    return symbol_sync_launch(head, n_head, ref, n_ref, skip, result, scratch, scratch_bytes,
+                              static_cast<cudaStream_t>(stream));
+}
+
+extern "C" int kk_symbol_sync(const void* head, int64_t n_head, const void* ref, int n_ref, int64_t skip,
+                              double* result, void* scratch, size_t scratch_bytes, void* stream) {
+    clear_error();
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const int64_t l0 = (n_head + 1) / 2, l1 = n_head / 2;
+    const int64_t nl0 = (ref && n_ref > 0 && l0 >= n_ref) ? l0 - n_ref + 1 : 0;
+    const int64_t nl1 = (ref && n_ref > 0 && l1 >= n_ref) ? l1 - n_ref + 1 : 0;
+    double* res = static_cast<double*>(scratch) + ((nl0 + nl1 + 31) / 32) * 32;
+    if (int rc = symbol_sync_launch(head, n_head, ref, n_ref, skip, res, scratch, scratch_bytes, s)) return rc;
     return d2h_small(result, res, 4 * sizeof(double), s);
 }
 

@@ -532,6 +532,32 @@ def device_ber(labels, ref_idx, order: int, head: int, stop: int, tile_symbols: 
     return count_bit_errors(lab, ref, order)[:2]
 
 
+def pack_labels_host(labels, sym0: int, train_idx, order: int, bits_host) -> int:
+    """Decided labels (uint8 point indices, 255 = training symbol) -> the
+    demapped bit stream packed MSB first (kk_pack_bits, np.packbits layout)
+    -> pinned host memory `bits_host`, on the current stream.  Training
+    labels take the transmitted index train_idx[sym0 + i] (device uint8).
+    Returns the bytes copied."""
+    import torch
+
+    n = int(labels.numel())
+    if n == 0:
+        return 0
+    tb = slicer_tables(order)
+    k = int(np.log2(order))
+    nb = (n * k + 7) // 8
+    if nb > bits_host.numel():
+        raise ParameterError(f"bits_host holds {bits_host.numel()} bytes, need {nb}")
+    dev = labels.device
+    packed = torch.empty(nb, dtype=torch.uint8, device=dev)
+    st = torch.cuda.current_stream(dev).cuda_stream
+    n_train = int(train_idx.numel()) if train_idx is not None else 0
+    _lib.call("kk_pack_bits", labels.data_ptr(), n, int(sym0), train_idx.data_ptr() if n_train else None, n_train,
+              k, tb.point_label.ctypes.data, order, packed.data_ptr(), st)
+    bits_host[:nb].copy_(packed, non_blocking=True)
+    return nb
+
+
 def receive_host_stream(cfg, host_codes, half_lsb: float, reference_symbols, chunk_samples: int = 1 << 25,
                         bits_host=None, device=None, staging=None, trace=None):
     """End-to-end receive of an int16 ADC stream in pinned HOST memory; the

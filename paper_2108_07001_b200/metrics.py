@@ -105,7 +105,9 @@ def count_bit_errors(labels, ref_idx, order: int, window_symbols: int = 0, exclu
         raise ParameterError("labels and reference must have equal length")
     tb = slicer_tables(order)
     dev = labels.device
-    pl = torch.from_numpy(tb.point_label).to(dev)
+    from .rxdsp import _device_const
+
+    pl = _device_const("point_label", tb.point_label, dev)   # no per-call upload
     tot = torch.zeros(1, dtype=torch.int64, device=dev)
     cnt = torch.zeros(1, dtype=torch.int64, device=dev)
     win = None

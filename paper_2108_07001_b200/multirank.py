@@ -98,9 +98,41 @@ def solve_chained(solver, comm, T_init, has_training: bool, max_iter: int = 64):
         total = comm.all_reduce_sum(changed)
         per_iter.append((int(changed), int(rerun), int(total)))
         if total == 0 and soft_pass:
+            # nothing changed: `maps` are the converged frame maps
+            solver.final_maps = maps
             return it, per_iter
         soft_pass = total == 0
     raise RuntimeError("multi-rank DDLMS did not converge within max_iter")
+
+
+def guard_chain(comm, guard_counts, T_init, run_sequential):
+    """Exact fallback when the divergence guard (rx:484-490) fired in some
+    rank's frame: the affine maps assume unfrozen taps, so from the first
+    rank r* whose frame saw a guard exceedance on, the recurrence is re-run
+    in rank order with the exact sequential chain, each rank starting from
+    the previous rank's end state (taps, frozen, div_count), broadcast.
+    Ranks before r* had no exceedance: their frames and maps are exact, so
+    r*'s start taps are the composition of their maps.  run_sequential(T,
+    frozen, div_count) -> (T_end, frozen, div_count) re-runs this rank's
+    frame.  Returns True when this rank's outputs were recomputed."""
+    rank, world = comm.rank, comm.world
+    first = next((r for r in range(world) if guard_counts[r] > 0), None)
+    if first is None:
+        return False
+    state = np.zeros(18)
+    if rank == first:
+        state[:16] = compose_start(T_init, comm_maps(comm), first)
+    state = comm.broadcast(state, src=first)
+    for r in range(first, world):
+        if rank == r:
+            T, fz, dc = run_sequential(state[:16].astype(np.float32), bool(state[16]), int(state[17]))
+            state[:16], state[16], state[17] = T, float(fz), float(dc)
+        state = comm.broadcast(state, src=r)
+    return rank >= first
+
+
+def comm_maps(comm):
+    return getattr(comm, "final_maps", None)
 
 
 class GpuFrameSolver:
@@ -244,9 +276,28 @@ def receive_rank(cfg, adc, reference_prefix, job: SuperframeJob, dist, chunk_sam
     iters, per_iter = solve_chained(solver, comm, T_init, has_training=n_train > 0,
                                     max_iter=int(cfg.gpu.ddlms_max_iter))
     labels, soft, _, guard = solver.finish()
+    comm.final_maps = solver.final_maps
     solver.close()
-    if comm.all_reduce_sum(guard) > 0:
-        raise RuntimeError("divergence guard reached in a multi-rank frame (use a single-rank receive)")
+    mode = "multirank"
+    guards = comm.all_gather([float(guard)])[:, 0]
+
+    def run_sequential(T, frozen, div_count):
+        import torch
+
+        from .rxdsp import _seq_ddlms, _wg_from_T
+
+        w, g = _wg_from_T(T)
+        wg = torch.from_numpy(np.concatenate([w, g]).astype(np.complex64)).to(dev)
+        fz = torch.tensor([int(frozen), int(div_count)], dtype=torch.int32, device=dev)
+        tv = pipe._ref_dev[k0:k0 + n_train] if n_train > 0 else None
+        xv = pipe._y2.view(drop + 2 * k0, drop + 2 * k0 + 2 * nsym + 2)
+        _seq_ddlms(xv, nsym, scale, cfg.ddlms, solver.tb.order, wg, fz, tv, n_train, labels, soft, None, dev)
+        wgh = wg.cpu().numpy().astype(np.complex128)
+        f = fz.cpu().numpy()
+        return _T_from_wg(wgh[:4], wgh[4:]), bool(f[0]), int(f[1])
+
+    if guard_chain(comm, guards, T_init, run_sequential):
+        mode = "multirank(guard: sequential chain)"
     pipe.release_buffers()
-    stats = [{"k0": k0, "nsym": nsym, "mode": "multirank", "iterations": iters, "per_iter": per_iter}]
+    stats = [{"k0": k0, "nsym": nsym, "mode": mode, "iterations": iters, "per_iter": per_iter}]
     return SuperframeResult(labels, soft, k0, pipe, stats, offset if job.rank == 0 else None)

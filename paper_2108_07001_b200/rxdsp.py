@@ -206,6 +206,32 @@ def _upload(a: np.ndarray, dev):
     return t
 
 
+_CONST_CACHE: dict = {}
+
+
+def _device_const(kind: str, a: np.ndarray, dev):
+    """Per-device cache of immutable per-link tables (static response halves,
+    rotation table, reference prefix), keyed by content: pipelines of the
+    same link reuse them instead of re-uploading (14 upload launches per
+    pipeline otherwise).  The current stream waits on the upload's event, so
+    a table uploaded on another stream is complete before it is read."""
+    torch = _torch()
+    a = np.ascontiguousarray(a)
+    key = (kind, str(dev), a.dtype.str, a.shape, hash(a.tobytes()))
+    hit = _CONST_CACHE.get(key)
+    if hit is None:
+        if len(_CONST_CACHE) >= 64:
+            torch.cuda.synchronize(dev)      # no kernel may still read an evicted table
+            _CONST_CACHE.clear()
+        t = _upload(a, dev)
+        ev = torch.cuda.Event()
+        ev.record(torch.cuda.current_stream(dev))
+        hit = _CONST_CACHE[key] = (t, ev)
+    else:
+        torch.cuda.current_stream(dev).wait_event(hit[1])
+    return hit[0]
+
+
 def _tone_rotation(tone_hz: float, fs: float):
     """Exact rational form p/q of tone/fs for the phase-continuous downshift
     exp(-2 pi i (p g mod q)/q) (sigcore.py:297-298 computes the same phase
@@ -538,7 +564,10 @@ def refine_static_taps(input_2sps, training_symbols, n_taps: int = 203, rate_hz:
 # fused static equalisation + 2:1 resampling (rx:414-453) -> K2
 # ---------------------------------------------------------------------------
 
-def _h_split(h: np.ndarray, dev):
+def _h_split(h: np.ndarray, dev, cached: bool = False):
+    if cached:
+        return (_device_const("h_even", h[0::2].astype(np.complex64), dev),
+                _device_const("h_odd", h[1::2].astype(np.complex64), dev))
     he = _upload(h[0::2].astype(np.complex64), dev)
     ho = _upload(h[1::2].astype(np.complex64), dev)
     return he, ho
@@ -726,15 +755,15 @@ class RxPipeline:
             self._ref_len = len(reference_symbols)
             n_keep = max(cfg.sync_symbols, cfg.ddlms.startup_symbols)
             self.reference = np.asarray(reference_symbols[:n_keep], np.complex128)
-            self._ref_dev = _upload(self.reference.astype(np.complex64), self.dev)
+            self._ref_dev = _device_const("ref", self.reference.astype(np.complex64), self.dev)
         taps = cfg.static_taps if cfg.static_taps is not None else FirFilter(np.array([1.0 + 0j]), cfg.adc_rate_hz / 2.0)
         self._taps = taps
         self._aa_delay = cfg.static_plan.fft_size // 4
         self._kept, self._resp = _static_response(taps, cfg.static_plan, cfg.adc_rate_hz, cfg.aa_edge, self._aa_delay)
-        self._h_even, self._h_odd = _h_split(self._resp, self.dev)
+        self._h_even, self._h_odd = _h_split(self._resp, self.dev, cached=True)
         p, q, tab = _tone_rotation(cfg.tone_freq_hz, cfg.adc_rate_hz)
         self._rot_p, self._rot_q = p, q
-        self._rot_tab = _upload(tab, self.dev) if tab is not None else None
+        self._rot_tab = _device_const("rot", tab, self.dev) if tab is not None else None
         self._spec = make_constellation(cfg.constellation_order)
         self._tables = slicer_tables(cfg.constellation_order)
 
@@ -771,6 +800,7 @@ class RxPipeline:
 
         # DDLMS
         self._synced = False
+        self._sync_pending = None         # (pinned result, event, scratch) of an enqueued sync
         self._drop = 0
         self._eq_scale = None
         self.sync_offset = None
@@ -786,13 +816,19 @@ class RxPipeline:
         self._jobs = collections.deque()  # submitted asynchronous frames, in order
         self._worker = None
         self._y2.before_realloc = self._wait_frames
+        # Equalizer state lives on the device (no host round trip between
+        # frames): 4-tap widely-linear -> real 2x8 taps T + {frozen,
+        # div_count} for the block-parallel solver; otherwise the complex
+        # taps (w, g) + {frozen, div_count} of the sequential chain.
         st0 = EqualizerState.initial(cfg.ddlms.n_taps)
-        self._w, self._g = st0.w, st0.g
-        self._T = _T_from_wg(st0.w, st0.g) if cfg.ddlms.n_taps == 4 else None
-        self._frozen = False
-        self._div_count = 0
+        self._solver_form = bool(cfg.ddlms.widely_linear) and cfg.ddlms.n_taps == 4
+        if self._solver_form:
+            self._T_dev = _upload(_T_from_wg(st0.w, st0.g), self.dev)
+        else:
+            self._wg_dev = _upload(np.concatenate([st0.w, st0.g]).astype(np.complex64), self.dev)
+        self._state_dev = torch.zeros(2, dtype=torch.int32, device=self.dev)     # {frozen, div_count}
         self._ws = None
-        self.ddlms_stats: list[dict] = []
+        self._stats: list[dict] = []
 
         self._out: list[tuple] = []
         self._pending_diag: list[tuple] = []
@@ -826,7 +862,7 @@ class RxPipeline:
             dead = self._hd.view(h0, h0 + n)
             zb = torch.nonzero(dead).flatten().cpu().tolist()
             self._diagnostics.append({"chunk": chunk, "clamped": int(cl1.item() - cl0.item()),
-                                      "zero_blocks": zb, "diverged": frozen})
+                                      "zero_blocks": zb, "diverged": bool(frozen.item())})
         self._pending_diag = []
         return self._diagnostics
 
@@ -867,7 +903,7 @@ class RxPipeline:
         self._hd.commit(n_hops)
         # diagnostics are materialised lazily (no host sync per feed)
         self._pending_diag.append((self._chunk_index, h0, n_hops, clamped_before, self._clamped * 1,
-                                   self._frozen))
+                                   self._state_dev[0] * 1))
 
     def _run_carrier(self, flush):
         cfg = self.cfg
@@ -911,9 +947,18 @@ class RxPipeline:
         self._z.keep = max(0, (self._hb_next - 1) * hop)
         self._seg.keep = max(0, ((self._hb_next - 1) * hop) // seg)
 
-    def _do_sync(self, flush):
+    def _sync_head_len(self) -> int:
         cfg = self.cfg
-        need = cfg.sync_wait_samples + 2 * cfg.sync_symbols
+        return cfg.sync_wait_samples + 2 * cfg.sync_symbols
+
+    def _sync_launch(self, flush) -> bool:
+        """Enqueue the stream-head sync (rx:724-749: symbol_sync + eq scale
+        over the first sync_wait + 2 sync_symbols 2-sps samples) without
+        blocking: the result lands in pinned host memory, an event marks it.
+        False when the head is not complete yet (and no flush)."""
+        torch = _torch()
+        cfg = self.cfg
+        need = self._sync_head_len()
         avail = self._y2.end
         if avail < need and not flush:
             return False
@@ -921,7 +966,34 @@ class RxPipeline:
         head = self._y2.view(0, nh)
         skip = min(nh // 2, 1 << 13)
         ref = self._ref_dev[:cfg.sync_symbols] if self._ref_dev is not None else None
-        parity, k, ratio, rms = _sync_device(head, ref, skip, self.dev)
+        nr = int(ref.shape[0]) if ref is not None else 0
+        sb = int(_lib.load().kk_symbol_sync_scratch_bytes(nh, nr))
+        res = torch.zeros(4, dtype=torch.float64).pin_memory()
+        # on a side stream: the cross-correlation (~0.2 ms) overlaps the rest
+        # of the front end instead of delaying it on the main stream
+        cur = torch.cuda.current_stream(self.dev)
+        ss = side_stream(self.dev, "sync")
+        ss.wait_stream(cur)
+        with torch.cuda.stream(ss):
+            scratch = torch.empty(sb, dtype=torch.uint8, device=self.dev)
+            _lib.call("kk_symbol_sync_enqueue", _ptr(head), nh, _ptr(ref), nr, int(skip), res.data_ptr(),
+                      _ptr(scratch), sb, ss.cuda_stream)
+            ev = torch.cuda.Event()
+            ev.record(ss)
+        self._y2.buf.record_stream(ss)     # the head stays valid if the buffer is regrown meanwhile
+        if ref is not None:
+            ref.record_stream(ss)
+        self._sync_pending = (res, ev, scratch)
+        return True
+
+    def _sync_resolve(self):
+        """Wait for the enqueued sync (only that event, not later work) and
+        apply it: offset / ratio / eq scale, training length (rx:734-749)."""
+        cfg = self.cfg
+        res, ev, _ = self._sync_pending
+        ev.synchronize()
+        parity, k, ratio, rms = int(res[0]), int(res[1]), float(res[2]), float(res[3])
+        self._sync_pending = None
         self._eq_scale = 1.0 / rms if rms > 0 else 1.0
         drop = 0
         if self.reference is not None:
@@ -935,9 +1007,16 @@ class RxPipeline:
             self._train_total = min(cfg.ddlms.startup_symbols, self._ref_len)
         self._drop = drop
         self._synced = True
+
+    def _do_sync(self, flush):
+        if self._sync_pending is None and not self._sync_launch(flush):
+            return False
+        self._sync_resolve()
         return True
 
     def _solve_frame_impl(self, k0, k1, labels=None, soft=None):
+        """Enqueue the DDLMS of symbols [k0, k1) on the current stream; no
+        host readback (statistics are materialised lazily, see ddlms_stats)."""
         torch = _torch()
         cfg = self.cfg
         d = cfg.ddlms
@@ -950,54 +1029,85 @@ class RxPipeline:
             labels = torch.empty(nsym, dtype=torch.uint8, device=self.dev)
             soft = torch.empty(nsym, dtype=torch.complex64, device=self.dev)
         tb = self._tables
-        use_solve = (d.widely_linear and d.n_taps == 4 and not self._frozen and self._div_count == 0)
-        stats = {"k0": k0, "nsym": nsym, "mode": "solve" if use_solve else "sequential"}
-        if use_solve:
+        stream = torch.cuda.current_stream(self.dev)
+        if self._solver_form:
             B = self._frame_block(nsym)
-            stats["block"] = B
+            stats = {"k0": k0, "nsym": nsym, "mode": "solve", "block": B}
             wsb = int(_lib.load().kk_ddlms_workspace_bytes(nsym, B))
             if self._ws is None or self._ws.numel() < wsb:
                 if self._async:
                     raise RuntimeError("asynchronous DDLMS frame without a pre-sized workspace")
                 self._ws = torch.empty(wsb, dtype=torch.uint8, device=self.dev)
-            Tin = np.ascontiguousarray(self._T, dtype=np.float32)
-            Tout = np.zeros(16, dtype=np.float32)
-            st = np.zeros(38, dtype=np.int64)
-            _lib.call("kk_ddlms_solve", x_ptr, nsym, float(self._eq_scale), train_ptr, n_train,
-                      Tin.ctypes.data, tb.order, tb.pts_ri.ctypes.data,
+            T_start = self._T_dev.clone()
+            st = torch.zeros(38, dtype=torch.int64).pin_memory()   # written by the device (mapped)
+            _lib.call("kk_ddlms_solve_async", x_ptr, nsym, float(self._eq_scale), train_ptr, n_train,
+                      _ptr(self._T_dev), _ptr(self._state_dev), tb.order, tb.pts_ri.ctypes.data,
                       tb.grid.ctypes.data if tb.grid_m else None, tb.grid_m, tb.norm, tb.max_radius,
                       float(d.divergence_factor), int(d.divergence_run), float(d.mu), B,
-                      int(self.gpu.ddlms_max_iter), float(self.gpu.ddlms_soft_tol), _ptr(labels), _ptr(soft),
-                      Tout.ctypes.data, _ptr(self._ws), wsb, st.ctypes.data, _stream(self.dev))
-            it = int(st[0])
-            stats.update(iterations=it, blocks_rerun=int(st[1]), fallback=int(st[2]),
-                         guard_exceed=int(st[3]), blocks=int(st[5]),
-                         per_iter=[(int(st[6 + 2 * i]), int(st[7 + 2 * i])) for i in range(min(it, 16))])
-            if st[2] == 1:
-                use_solve = False   # guard interaction: exact sequential re-run of the frame
-                stats["mode"] = "sequential(guard)"
-            else:
-                self._T = Tout
-                self._w, self._g = _wg_from_T(Tout)
-        if not use_solve:
-            if d.n_taps == 4 and self._T is not None:
-                self._w, self._g = _wg_from_T(self._T)
-            wg = torch.from_numpy(np.concatenate([self._w, self._g]).astype(np.complex64)).to(self.dev)
-            fz = torch.tensor([int(self._frozen), int(self._div_count)], dtype=torch.int32, device=self.dev)
+                      # worker-thread frames (streaming receive): host-driven loop, no graph
+                      -int(self.gpu.ddlms_max_iter) if self._async else int(self.gpu.ddlms_max_iter),
+                      float(self.gpu.ddlms_soft_tol), _ptr(labels), _ptr(soft),
+                      _ptr(self._ws), wsb, st.data_ptr(), stream.cuda_stream)
+            ev = torch.cuda.Event()
+            ev.record(stream)
+            stats["_pending"] = (st, ev, T_start)
+        else:
+            stats = {"k0": k0, "nsym": nsym, "mode": "sequential"}
             xv = self._y2.view(q0, q0 + 2 * nsym + 2)
             tv = self._ref_dev[k0:k0 + n_train] if n_train > 0 else None
-            _seq_ddlms(xv, nsym, self._eq_scale, d, tb.order, wg, fz, tv, n_train, labels, soft, None, self.dev)
-            wgh = wg.cpu().numpy().astype(np.complex128)
-            self._w, self._g = wgh[:d.n_taps], wgh[d.n_taps:]
-            f = fz.cpu().numpy()
-            self._frozen, self._div_count = bool(f[0]), int(f[1])
-            if d.n_taps == 4:
-                self._T = _T_from_wg(self._w, self._g)
+            _seq_ddlms(xv, nsym, self._eq_scale, d, tb.order, self._wg_dev, self._state_dev, tv, n_train, labels,
+                       soft, None, self.dev)
         return labels, soft, n_train, stats
+
+    @staticmethod
+    def _materialise(stats: dict) -> dict:
+        """Fill a frame's statistics from its device-written record."""
+        pend = stats.pop("_pending", None)
+        if pend is None:
+            return stats
+        st, ev, T_start = pend
+        ev.synchronize()
+        st = st.numpy()
+        it = int(st[0])
+        stats.update(iterations=it, blocks_rerun=int(st[1]), fallback=int(st[2]), guard_exceed=int(st[3]),
+                     blocks=int(st[5]), per_iter=[(int(st[6 + 2 * i]), int(st[7 + 2 * i])) for i in range(min(it, 16))],
+                     T_start=[float(v) for v in T_start.cpu().numpy()])
+        if stats["fallback"] == 1:
+            stats["mode"] = "sequential(guard)"
+        elif stats["fallback"] == 2:
+            stats["mode"] = "solve+chain(not converged)"
+        return stats
+
+    @property
+    def ddlms_stats(self) -> list:
+        """Per-frame DDLMS statistics (synchronises with pending frames)."""
+        return [self._materialise(s) for s in self._stats]
+
+    def resolve_frame_sequential(self, k0: int, k1: int, T_start):
+        """Exactness check (not the product path): re-run symbols [k0, k1)
+        with the SEQUENTIAL kernel (the rx:465-498 recurrence, one thread)
+        from the 4-tap WL start taps T_start (real 2x8 form), guard state
+        cleared.  The 2-sps input must still be held (before
+        release_buffers).  Returns (labels uint8, soft complex64) device tensors."""
+        torch = _torch()
+        d = self.cfg.ddlms
+        nsym = k1 - k0
+        q0 = self._drop + 2 * k0
+        w, g = _wg_from_T(np.asarray(T_start, np.float32))
+        wg = torch.from_numpy(np.concatenate([w, g]).astype(np.complex64)).to(self.dev)
+        fz = torch.zeros(2, dtype=torch.int32, device=self.dev)
+        n_train = int(max(0, min(nsym, self._train_total - k0)))
+        tv = self._ref_dev[k0:k0 + n_train] if n_train > 0 else None
+        labels = torch.empty(nsym, dtype=torch.uint8, device=self.dev)
+        soft = torch.empty(nsym, dtype=torch.complex64, device=self.dev)
+        xv = self._y2.view(q0, q0 + 2 * nsym + 2)
+        _seq_ddlms(xv, nsym, self._eq_scale, d, self._tables.order, wg, fz, tv, n_train, labels, soft, None,
+                   self.dev)
+        return labels, soft
 
     def _solve_frame(self, k0, k1):
         labels, soft, n_train, stats = self._solve_frame_impl(k0, k1)
-        self.ddlms_stats.append(stats)
+        self._stats.append(stats)
         self._out.append((labels, soft, k0, n_train))
         self._sym_done = k1
         self._y2.keep = self._drop + 2 * k1
@@ -1007,7 +1117,7 @@ class RxPipeline:
     # f's end taps), so a single worker thread solves them in order on its
     # own CUDA stream, each after an event marking that the front end has
     # produced the frame's input; the host thread keeps feeding.  The worker
-    # owns the equalizer state (_T, _w, _g, _frozen, _div_count, _ws) while
+    # owns the equalizer state (device taps + state tensors, _ws) while
     # frames are pending.  Outputs are collected in order by drain_device().
 
     def _submit_frame(self, k0, k1):
@@ -1084,7 +1194,7 @@ class RxPipeline:
             labels, soft, n_train, stats = job["out"]
             ws.wait_event(job["done"])
             self._events.append(("ddlms", *job["events"]))
-            self.ddlms_stats.append(stats)
+            self._stats.append(stats)
             self._out.append((labels, soft, job["k0"], n_train))
         if self._y2 is not None:
             self._y2.keep = self._drop + 2 * (self._jobs[0]["k0"] if self._jobs else self._sym_done)
@@ -1205,32 +1315,60 @@ class RxPipeline:
             n_hops = (n_hops // 2) * 2          # pairs on the global even-hop grid
         if n_hops == 0 and not flush:
             return
+        front_only = getattr(self, "_front_only", False)
+        # Before the stream is synced, run the front end over just the stream
+        # head first and enqueue the sync on it: the host then waits for the
+        # sync result while the device runs the rest of the front end (the
+        # output does not depend on the split: every stage is chunk-invariant).
+        parts = [n_hops]
+        if not front_only and not self._synced and self._sync_pending is None:
+            hh = self._sync_head_hops()
+            if 0 < hh < n_hops:
+                parts = [hh, n_hops - hh]
         nv = _NVTX
-        t0 = self._ev()
-        if n_hops:
-            chunk = self._raw[:n_hops * hop]
-            nv and torch.cuda.nvtx.range_push("kk")
-            self._run_kk(chunk, n_hops)
+        for pi, nh in enumerate(parts):
+            last = pi == len(parts) - 1
+            fl = flush and last
+            t0 = self._ev()
+            if nh:
+                chunk = self._raw[:nh * hop]
+                nv and torch.cuda.nvtx.range_push("kk")
+                self._run_kk(chunk, nh)
+                nv and torch.cuda.nvtx.range_pop()
+                self._raw = self._raw[nh * hop:]
+            t1 = self._ev()
+            nv and torch.cuda.nvtx.range_push("carrier")
+            self._run_carrier(fl)
             nv and torch.cuda.nvtx.range_pop()
-            self._raw = self._raw[n_hops * hop:]
-        t1 = self._ev()
-        nv and torch.cuda.nvtx.range_push("carrier")
-        self._run_carrier(flush)
-        nv and torch.cuda.nvtx.range_pop()
-        t2 = self._ev()
-        nv and torch.cuda.nvtx.range_push("static")
-        self._run_static(flush)
-        nv and torch.cuda.nvtx.range_pop()
+            t2 = self._ev()
+            nv and torch.cuda.nvtx.range_push("static")
+            self._run_static(fl)
+            nv and torch.cuda.nvtx.range_pop()
+            t3 = self._ev()
+            self._events += [("kk", t0, t1), ("carrier", t1, t2), ("static", t2, t3)]
+            if not last and not self._synced and self._sync_pending is None:
+                self._sync_launch(False)
         t3 = self._ev()
-        if not getattr(self, "_front_only", False):
+        if not front_only:
             nv and torch.cuda.nvtx.range_push("ddlms")
             self._run_ddlms(flush)
             nv and torch.cuda.nvtx.range_pop()
         t4 = self._ev()
-        self._events += [("kk", t0, t1), ("carrier", t1, t2), ("static", t2, t3), ("ddlms", t3, t4)]
+        self._events.append(("ddlms", t3, t4))
         self._chunk_index += 1
         if flush:
             self._flushed = True
+
+    def _sync_head_hops(self) -> int:
+        """KK hops (even) whose front-end output covers the sync head: the
+        head's 2-sps samples at the ADC rate, plus one static block and one
+        carrier segment of hold-back, rounded up to whole carrier segments."""
+        cfg = self.cfg
+        seg = cfg.carrier_segment_len
+        n = 2 * self._sync_head_len() + cfg.static_plan.fft_size + cfg.kk_plan.fft_size
+        n = (-(-n // seg) + 1) * seg - (self._z.end - self._stream_offset)
+        hop = cfg.kk_plan.hop
+        return max(0, (-(-n // hop) + 1) // 2 * 2)
 
     def expect(self, n_samples: int, chunk_samples: int | None = None, chunk_ends=None) -> None:
         """Capacity hint for a stream of n_samples fed in chunks of
@@ -1339,7 +1477,8 @@ class RxPipeline:
 
     @property
     def diverged(self) -> bool:
-        return self._frozen
+        """Divergence guard fired (taps frozen, rx:484-490); synchronises."""
+        return bool(self._state_dev[0].item())
 
     @property
     def eq_scale(self):

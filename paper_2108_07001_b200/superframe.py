@@ -18,7 +18,7 @@ its blocks and all-reduces the changed-decision count.
 
 from __future__ import annotations
 
-from dataclasses import dataclass, field
+from dataclasses import dataclass
 
 import numpy as np
 
@@ -56,12 +56,20 @@ class SuperframeResult:
     soft: object                # complex64 device tensor
     first_symbol: int           # global DDLMS symbol index of labels[0]
     pipe: object = None         # the pipeline (stage timing events resolved lazily)
-    ddlms_stats: list = field(default_factory=list)
+    stats: list | None = None   # explicit per-frame statistics (multi-rank); else the pipeline's
     sync_offset: int | None = None
 
     @property
     def stage_seconds(self) -> dict:
         return self.pipe.stage_seconds if self.pipe is not None else {}
+
+    @property
+    def ddlms_stats(self) -> list:
+        """Per-frame DDLMS statistics (materialised on first access: the
+        single-rank solve is asynchronous)."""
+        if self.stats is not None:
+            return self.stats
+        return self.pipe.ddlms_stats if self.pipe is not None else []
 
 
 def receive_superframe(cfg, adc, reference_prefix, job: SuperframeJob, dist=None,
@@ -77,6 +85,6 @@ def receive_superframe(cfg, adc, reference_prefix, job: SuperframeJob, dist=None
         pipe.feed(adc, flush=True)
         labels, soft, meta = pipe.drain_device()
         pipe.release_buffers()
-        return SuperframeResult(labels, soft, meta[0][0] if meta else 0, pipe, pipe.ddlms_stats, pipe.sync_offset)
+        return SuperframeResult(labels, soft, meta[0][0] if meta else 0, pipe, None, pipe.sync_offset)
     from .multirank import receive_rank
     return receive_rank(cfg, adc, reference_prefix, job, dist, chunk_samples=chunk_samples)

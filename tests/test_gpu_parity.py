@@ -281,10 +281,12 @@ def test_pipeline_int16_wire_format():
     assert np.mean(to_idx(dec, 4) == cap.arrays["dec_idx"]) >= DEC_AGREE
 
 
-def test_tiled_bench_stream_vs_reference():
-    """The bench workload pattern: the c5 tile repeated 4x (seams
-    phase-continuous), against the reference's decisions on the same stream."""
-    cap = load_capture("c5_qpsk_10000km_tile")
+@pytest.mark.parametrize("name", ["c5_qpsk_10000km_tile", "c3_64qam_1600km_tile"])
+def test_tiled_bench_stream_vs_reference(name):
+    """The bench workload pattern (QPSK 10,000 km and 64-QAM 1,600 km): the
+    tile repeated 4x (seams phase-continuous), against the reference's
+    decisions on the same stream."""
+    cap = load_capture(name)
     reps = cap.meta["tile_reps"]
     codes, _ = tile(cap, reps * len(cap.adc_h))
     cfg = cap.pipeline_config()
@@ -294,8 +296,36 @@ def test_tiled_bench_stream_vs_reference():
     ref = cap.arrays["dec4_idx"]
     assert pipe.sync_offset == cap.meta["sync_offset4"]
     assert len(dec) == len(ref)
-    agree = float(np.mean(to_idx(dec, 4) == ref))
+    agree = float(np.mean(to_idx(dec, cap.order) == ref))
     assert agree >= DEC_AGREE
+
+
+def _burst_stream(factor=100.0, start=150_000, length=600):
+    """c1's ADC stream (float) with a burst of huge samples: after the
+    receive filter |y| stays far above 10 x max radius for more than 100
+    symbols, so the divergence guard (rx:484-490) freezes the taps."""
+    cap = load_capture("c1_qpsk_b2b")
+    x = cap.adc_float().copy()
+    x[start:start + length] *= factor
+    return cap, x
+
+
+def test_pipeline_guard_freeze_vs_oracle():
+    """Divergence guard inside the pipeline (the device-side exact fallback
+    of the asynchronous solver): same freeze, same decisions as the oracle."""
+    cap, x = _burst_stream()
+    syms = cap.symbols()
+    ref, d_ref, _ = ko.receive(x, ko.OracleConfig(taps=cap.taps), syms, 1 << 22)
+    assert ref.eq.frozen, "the burst must trip the guard in the reference arithmetic"
+    cfg = cap.pipeline_config()
+    pipe = rxdsp.RxPipeline(cfg, reference_symbols=syms)
+    pipe.feed(x)
+    dec, _ = pipe.finish()
+    assert pipe.diverged
+    assert [s["mode"] for s in pipe.ddlms_stats][-1].startswith("sequential")
+    assert len(dec) == len(d_ref)
+    agree = float(np.mean(to_idx(dec, 4) == to_idx(d_ref, 4)))
+    assert agree >= DEC_AGREE, agree
 
 
 def test_host_stream_packed_bits_vs_reference():

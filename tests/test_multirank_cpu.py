@@ -160,3 +160,79 @@ def test_two_rank_chained_ddlms_equals_sequential():
     # start taps cross ranks as float32 (as on the GPU): soft within 1e-6
     assert np.max(np.abs(soft - soft_ref)) < 1e-6
     assert res[0][4] == res[1][4] and res[0][4] >= 2      # same global iteration count
+
+
+def _guard_worker(rank, world, port, out_q):
+    """Rank 1's frame holds a burst that trips the divergence guard: the
+    chained fallback must reproduce the single-stream recurrence (frozen
+    taps and all) exactly."""
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from oracle import kkoracle as ko
+        from paper_2108_07001_b200.multirank import TorchComm, guard_chain
+        from paper_2108_07001_b200.rxdsp import EqualizerState, _T_from_wg, _wg_from_T
+
+        syms, x, pts = make_guard_stream()
+        n = (len(x) - 4) // 2 + 1
+        cut = n // 2 + 37
+        k0, k1 = (0, cut) if rank == 0 else (cut, n)
+        st0 = EqualizerState.initial()
+        T_init = _T_from_wg(st0.w, st0.g).astype(np.float64)
+        comm = TorchComm(dist, torch.device("cpu"))
+        # rank 0's converged frame map (exact: no guard there), as the
+        # solver would have all-gathered it: the sequential oracle's end taps
+        # from T_init over rank 0's symbols, written as P = I, Q = T_end - T_init
+        st = ko.EqState.initial()
+        ko.ddlms_wl(x[:2 * cut + 2], st, training=syms[:700], order=16, mu=2e-3)
+        P = np.eye(8)
+        Q = (_T_from_wg(st.w, st.g).astype(np.float64) - T_init).reshape(2, 8)
+        comm.final_maps = np.stack([np.concatenate([P.ravel(), Q.ravel()])] * world)
+        out = {}
+
+        def run_sequential(T, frozen, div_count):
+            w, g = _wg_from_T(T)
+            s = ko.EqState(w=w.copy(), g=g.copy(), frozen=frozen, div_count=div_count)
+            tr = syms[k0:700] if k0 < 700 else None
+            dec, soft, s = ko.ddlms_wl(x[2 * k0:2 * k1 + 2], s, training=tr, order=16, mu=2e-3)
+            out["labels"] = ko.to_index(dec[:k1 - k0], 16)
+            return _T_from_wg(s.w, s.g), s.frozen, s.div_count
+
+        guards = [0.0, 5.0]                           # rank 1 saw exceedances
+        redone = guard_chain(comm, guards, T_init, run_sequential)
+        out_q.put((rank, redone, out.get("labels")))
+    finally:
+        dist.destroy_process_group()
+
+
+def make_guard_stream():
+    syms, x, pts = make_stream(seed=9)
+    n = len(syms)
+    x = x.copy()
+    x[2 * (3 * n // 4):2 * (3 * n // 4 + 150)] *= 40.0     # 150 symbols far outside 10 x max radius
+    return syms, x, pts
+
+
+def test_two_rank_guard_fallback_equals_sequential():
+    from oracle import kkoracle as ko
+
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_guard_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = sorted([q.get(timeout=120) for _ in range(2)], key=lambda t: t[0])
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert res[0][1] is False and res[1][1] is True       # only rank 1 re-ran
+    syms, x, pts = make_guard_stream()
+    st = ko.EqState.initial()
+    dec_ref, _, st = ko.ddlms_wl(x, st, training=syms[:700], order=16, mu=2e-3)
+    assert st.frozen                                       # the burst did trip the guard
+    n = len(dec_ref)
+    cut = n // 2 + 37
+    lab_ref = ko.to_index(dec_ref, 16)
+    assert np.array_equal(res[1][2], lab_ref[cut:])

@@ -51,7 +51,7 @@ for lg in sizes:
         soft = torch.empty(nsym, dtype=torch.complex64, device=dev)
         dev_ms, host_ms = [], []
         for rep in range(4):
-            Tin = np.ascontiguousarray(pipe._T, np.float32)
+            Tin = np.ascontiguousarray(pipe._T_dev.cpu().numpy(), np.float32)
             Tout = np.zeros(16, np.float32)
             st = np.zeros(38, np.int64)
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
