@@ -44,6 +44,11 @@ extern "C" {
 #define KK_DTYPE_I16 0 /* ADC codes; value = code * in_scale (odd half-LSB codes) */
 #define KK_DTYPE_F32 1
 #define KK_DTYPE_F64 2
+/* packed 12-bit ADC codes c, two per 3 bytes little-endian (byte0 = c0[7:0],
+ * byte1 = c0[11:8] | c1[3:0] << 4, byte2 = c1[11:4]); value = (2c + 1) *
+ * in_scale (the int16 path's odd half-LSB code h = 2c + 1).  1.5 B/sample.
+ * The buffer must be 4-byte aligned.  B200 addition (the reference's raw format is int16, sigcore.py:357) */
+#define KK_DTYPE_P12 3
 /* or-ed into in_dtype of kk_reconstruct_pairs: correctly rounded
  * logf/expf/sincosf instead of the SFU approximations (functional API) */
 #define KK_DTYPE_PRECISE 0x100
@@ -79,6 +84,9 @@ int kk_reconstruct_pairs(int in_dtype, const void *in, float in_scale, float cla
                          void *hop_sum, uint8_t *hop_dead, unsigned long long *clamped,
                          int64_t n0_global, int rot_p, int rot_q, const void *rot_tab,
                          int mirror, void *stream);
+
+/* packed 12-bit codes (KK_DTYPE_P12 layout, n even) -> int16 odd codes h */
+int kk_unpack12(const uint8_t *in, int64_t n, int16_t *out, void *stream);
 
 /*
  * Carrier means -- replaces the per-segment np.mean of rxdsp.py:685-687.

@@ -8,8 +8,8 @@ super-frame sharding.
 """
 
 from .sigcore import (  # noqa: F401
-    AdcCodes, BlockPlan, ComplexSignal, FirFilter, ParameterError, RealSignal,
-    anti_alias_window, fir_frequency_response, read_adc_raw, write_adc_raw,
+    AdcCodes, AdcPacked12, BlockPlan, ComplexSignal, FirFilter, ParameterError, RealSignal,
+    anti_alias_window, fir_frequency_response, pack12, read_adc_raw, unpack12, write_adc_raw,
 )
 from .constellation import ConstellationSpec, make_constellation  # noqa: F401
 from .rxdsp import (  # noqa: F401

@@ -16,7 +16,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "_lib", "libkkb200.so")
 
 KK_OK, KK_ERR_PARAM, KK_ERR_SYNC, KK_ERR_CUDA, KK_ERR_INTERNAL = 0, 1, 2, 3, 4
-KK_DTYPE_I16, KK_DTYPE_F32, KK_DTYPE_F64 = 0, 1, 2
+KK_DTYPE_I16, KK_DTYPE_F32, KK_DTYPE_F64, KK_DTYPE_P12 = 0, 1, 2, 3
 KK_DTYPE_PRECISE = 0x100   # or-ed flag: correctly rounded transcendental functions
 
 
@@ -44,6 +44,7 @@ _SIGS = {
     "kk_fma_peak": ([_P, _P], _I),
     "kk_upload": ([_P, _P, _I64, _P], _I),
     "kk_reconstruct_pairs": ([_I, _P, _F, _F, _I64, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _I64, _I, _I, _P, _I, _P], _I),
+    "kk_unpack12": ([_P, _I64, _P, _P], _I),
     "kk_carrier_means": ([_P, _I64, _I, _I64, _I64, _I, _P, _P], _I),
     "kk_static_blocks": ([_P, _I64, _I64, _I64, _I64, _P, _I64, _I, _I, _I, _I, _P, _I, _P, _P, _P, _P], _I),
     "kk_symbol_sync_scratch_bytes": ([_I64, _I], _SZ),

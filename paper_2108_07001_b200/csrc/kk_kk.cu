@@ -18,6 +18,7 @@
 // hops of u/amp it needs once in shared memory.  FFT = Stockham radix
 // 16x16x4 in padded float2 smem; the inverse FFT's last pass writes the field
 // straight to HBM (coalesced) with the rotation/mirror and the hop sums fused.
+#include <algorithm>
 #include <type_traits>
 
 #include "kk_common.cuh"
@@ -54,13 +55,36 @@ __device__ __forceinline__ float reduce_2pi(float x) {
     return fmaf(-k, 6.28318548202514648f, fmaf(-k, -1.7484555314695172e-7f, x));
 }
 
+// Packed 12-bit wire format (KK_DTYPE_P12): two 12-bit two's-complement ADC
+// codes c (12-bit converter, frontend.py:82-118; odd half-LSB code h = 2c+1)
+// per 3 bytes, little-endian: byte0 = c0[7:0], byte1 = c0[11:8] | c1[3:0] << 4,
+// byte2 = c1[11:4].  1.5 B/sample on the wire instead of int16's 2.
+struct P12 {};
+template <typename TIn> struct InElem { using T = TIn; };
+template <> struct InElem<P12> { using T = uint8_t; };
+
+// raw input value at sample i: the code h (int16, P12) or the sample (f32/f64)
 template <typename TIn>
-__device__ __forceinline__ float load_in(const TIn* p, int64_t i, float scale) {
-    return static_cast<float>(p[i]) * scale;
+__device__ __forceinline__ auto raw_at(const typename InElem<TIn>::T* p, int64_t i) {
+    if constexpr (std::is_same<TIn, P12>::value) {
+        const int64_t b = 3 * (i >> 1);                       // first byte of the pair
+        const uint32_t* w = reinterpret_cast<const uint32_t*>(p + (b & ~int64_t(3)));
+        // the second word only when the 3 bytes straddle it ((b & 3) >= 2): every
+        // word read then overlaps the data, so nothing past its end is touched
+        const uint32_t hi = (b & 2) ? __ldg(w + 1) : 0u;
+        const uint32_t v = __funnelshift_r(__ldg(w), hi, static_cast<unsigned>(b & 3) * 8u);
+        const int c = (i & 1) ? (static_cast<int>(v << 8) >> 20) : (static_cast<int>(v << 20) >> 20);
+        return static_cast<int16_t>(2 * c + 1);
+    } else {
+        return p[i];
+    }
 }
-template <>
-__device__ __forceinline__ float load_in<double>(const double* p, int64_t i, float scale) {
-    return static_cast<float>(p[i] * static_cast<double>(scale));
+template <typename TIn>
+__device__ __forceinline__ float load_in(const typename InElem<TIn>::T* p, int64_t i, float scale) {
+    if constexpr (std::is_same<TIn, double>::value)
+        return static_cast<float>(p[i] * static_cast<double>(scale));
+    else
+        return static_cast<float>(raw_at<TIn>(p, i)) * scale;
 }
 
 // Hilbert multiplier on the full 1024-bin spectrum (Hermitian extension of
@@ -96,7 +120,7 @@ __device__ __forceinline__ void k1_sincos(float x, float* s, float* c) {
 
 template <typename TIn, bool PRECISE>
 __global__ void __launch_bounds__(kK1Threads, 4)
-kk_pairs_kernel(const TIn* __restrict__ in, float in_scale, float clamp_rel, int64_t n_hops,
+kk_pairs_kernel(const typename InElem<TIn>::T* __restrict__ in, float in_scale, float clamp_rel, int64_t n_hops,
                 const float* __restrict__ st_u, const float* __restrict__ st_a,
                 const uint8_t* __restrict__ st_dead,
                 float* __restrict__ new_u, float* __restrict__ new_a, uint8_t* __restrict__ new_dead,
@@ -120,7 +144,8 @@ kk_pairs_kernel(const TIn* __restrict__ in, float in_scale, float clamp_rel, int
     // needed for the first block's history half) is shared by all 8 warps,
     // 64 samples each, so no warp stages two hops.  Sums of int16 codes are
     // exact integers.
-    using Acc = typename std::conditional<std::is_same<TIn, int16_t>::value, int, double>::type;
+    using Acc = typename std::conditional<std::is_same<TIn, int16_t>::value || std::is_same<TIn, P12>::value, int,
+                                          double>::type;
     auto hop_params = [&](int64_t h, double sum, int& dead, float& thr) {
         // mean = sum * scale / 512 (exact for int16 codes: integer sum)
         const double mean = sum * static_cast<double>(in_scale) / kHop;
@@ -150,13 +175,13 @@ kk_pairs_kernel(const TIn* __restrict__ in, float in_scale, float clamp_rel, int
             for (int i = lane; i < kHop; i += 32) u[i] = 0.f;
             if (lane == 0) S.dead[L] = 1;
         } else {
-            const TIn* src = in + h * kHop;
             float xv[kHop / 32];
             Acc sum = 0;
 #pragma unroll
             for (int i = 0; i < kHop / 32; ++i) {
-                xv[i] = load_in<TIn>(src, lane + 32 * i, 1.0f);
-                sum += static_cast<Acc>(src[lane + 32 * i]);
+                const auto r = raw_at<TIn>(in, h * kHop + lane + 32 * i);
+                xv[i] = static_cast<float>(r);
+                sum += static_cast<Acc>(r);
             }
 #pragma unroll
             for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
@@ -180,8 +205,9 @@ kk_pairs_kernel(const TIn* __restrict__ in, float in_scale, float clamp_rel, int
             const int i = warp * 64 + lane + 32 * e;
             x0v[e] = 0.f;
             if (h0_real) {
-                x0v[e] = load_in<TIn>(in + h0 * kHop, i, 1.0f);
-                p0 += static_cast<Acc>(in[h0 * kHop + i]);
+                const auto r = raw_at<TIn>(in, h0 * kHop + i);
+                x0v[e] = static_cast<float>(r);
+                p0 += static_cast<Acc>(r);
             }
         }
 #pragma unroll
@@ -360,7 +386,8 @@ static int launch_k1(const void* in, float in_scale, float clamp_rel, int64_t n_
     // the kernel only needs the stream index modulo the rotation period
     const int64_t n0m = rot_q > 0 ? ((n0 % rot_q) + rot_q) % rot_q : 0;
     kk_pairs_kernel<TIn, PRECISE><<<static_cast<unsigned>(grid), kK1Threads, smem, s>>>(
-        static_cast<const TIn*>(in), in_scale, clamp_rel, n_hops, st_u, st_a, st_dead, new_u, new_a, new_dead, out,
+        static_cast<const typename InElem<TIn>::T*>(in), in_scale, clamp_rel, n_hops, st_u, st_a, st_dead, new_u, new_a,
+        new_dead, out,
         hop_sum, hop_dead, clamped, n0m, rot_p, rot_q, rot_tab, mirror, tw);
     return check_launch("kk_pairs_kernel");
 }
@@ -395,8 +422,37 @@ extern "C" int kk_reconstruct_pairs(int in_dtype, const void* in, float in_scale
         case KK_DTYPE_F64:
             if (precise) KK_LAUNCH_K1(double, true);
             KK_LAUNCH_K1(double, false);
+        case KK_DTYPE_P12:
+            if (reinterpret_cast<uintptr_t>(in) & 3) return set_error(KK_ERR_PARAM, "packed 12-bit input must be 4-byte aligned");
+            if (precise) KK_LAUNCH_K1(P12, true);
+            KK_LAUNCH_K1(P12, false);
         default:
             return set_error(KK_ERR_PARAM, "unsupported input dtype");
     }
 #undef KK_LAUNCH_K1
+}
+
+// ---------------------------------------------------------------------------
+// packed 12-bit -> int16 odd half-LSB codes (the flush remainder of a packed
+// stream, which needs exact zero padding, and general conversion)
+// ---------------------------------------------------------------------------
+namespace kk {
+__global__ void unpack12_kernel(const uint8_t* __restrict__ in, int64_t n, int16_t* __restrict__ out) {
+    for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
+        const int64_t b = 3 * (i >> 1);
+        const int lo = in[b + (i & 1)], hi = in[b + 1 + (i & 1)];
+        const int c = (i & 1) ? (((hi << 4) | (lo >> 4)) & 0xFFF) : (((hi & 0xF) << 8) | lo);
+        out[i] = static_cast<int16_t>(2 * ((c ^ 0x800) - 0x800) + 1);
+    }
+}
+}  // namespace kk
+
+extern "C" int kk_unpack12(const uint8_t* in, int64_t n, int16_t* out, void* stream) {
+    using namespace kk;
+    clear_error();
+    if (n <= 0) return KK_OK;
+    if (n & 1) return set_error(KK_ERR_PARAM, "packed 12-bit streams hold an even number of samples");
+    const int64_t blocks = std::min<int64_t>((n + 255) / 256, 148 * 32);
+    unpack12_kernel<<<static_cast<unsigned>(blocks), 256, 0, static_cast<cudaStream_t>(stream)>>>(in, n, out);
+    return check_launch("unpack12_kernel");
 }

@@ -559,7 +559,7 @@ def pack_labels_host(labels, sym0: int, train_idx, order: int, bits_host) -> int
 
 
 def receive_host_stream(cfg, host_codes, half_lsb: float, reference_symbols, chunk_samples: int = 1 << 25,
-                        bits_host=None, device=None, staging=None, trace=None):
+                        bits_host=None, device=None, staging=None, trace=None, packed12_samples: int | None = None):
     """End-to-end receive of an int16 ADC stream in pinned HOST memory; the
     receiver's output -- the demapped bit stream, packed (np.packbits
     layout) -- lands in pinned host memory.
@@ -572,6 +572,9 @@ def receive_host_stream(cfg, host_codes, half_lsb: float, reference_symbols, chu
     both PCIe directions overlap the GPU work.  `staging` (optional) is a
     reusable int16 device buffer of >= n samples.  The DDLMS tail frames
     are aligned to the chunk ends (RxPipeline.expect(chunk_ends=...)).
+    packed12_samples=n: host_codes is instead a pinned uint8 buffer of the
+    packed 12-bit wire format (sigcore.AdcPacked12, 1.5 B/sample) holding n
+    samples; it is unpacked inside K1's staging (staging: uint8).
     Returns (pipe, bits_host, n_symbols_decided).
     """
     import torch
@@ -585,7 +588,7 @@ def receive_host_stream(cfg, host_codes, half_lsb: float, reference_symbols, chu
     comp.wait_stream(caller)
     with torch.cuda.stream(comp):
         out = _receive_host_stream(cfg, host_codes, half_lsb, reference_symbols, chunk_samples, bits_host, dev,
-                                   staging, trace, comp)
+                                   staging, trace, comp, packed12_samples)
     caller.wait_stream(comp)
     return out
 
@@ -663,16 +666,24 @@ def _drain_bits(st, bits_host, d2h, dev, max_frames=None, final: bool = False):
 
 
 def _receive_host_stream(cfg, host_codes, half_lsb, reference_symbols, chunk_samples, bits_host, dev, staging,
-                         trace, comp):
+                         trace, comp, packed12_samples=None):
     import torch
 
-    from .sigcore import AdcCodes
+    from .sigcore import AdcCodes, AdcPacked12
 
-    n = int(host_codes.shape[0])
+    p12 = packed12_samples is not None
+    n = int(packed12_samples) if p12 else int(host_codes.shape[0])
+    if p12 and (n % 2 or chunk_samples % 2):
+        raise ParameterError("packed 12-bit streams and chunks hold even sample counts")
+
+    def span(a, b):   # element range of samples [a, b) in the host / staging buffers
+        return (3 * a // 2, 3 * b // 2) if p12 else (a, b)
+
     copy = side_stream(dev, "h2d")
     d2h = side_stream(dev, "d2h")
-    if staging is None or staging.numel() < n:
-        staging = torch.empty(n, dtype=torch.int16, device=dev)
+    n_el = span(0, n)[1]
+    if staging is None or staging.numel() < n_el or (staging.dtype == torch.uint8) != p12:
+        staging = torch.empty(n_el, dtype=torch.uint8 if p12 else torch.int16, device=dev)
     # (feeding the last chunk in smaller pieces was measured slower: the
     # DDLMS tail frames then form a longer chain of ~0.5 ms frame latencies)
     starts = list(range(0, n, chunk_samples))
@@ -689,8 +700,8 @@ def _receive_host_stream(cfg, host_codes, half_lsb, reference_symbols, chunk_sam
     def queue_copies(lo, hi):
         with torch.cuda.stream(copy):
             for i in range(lo, hi):
-                a, m = starts[i], sizes[i]
-                staging[a:a + m].copy_(host_codes[a:a + m], non_blocking=True)
+                e0, e1 = span(starts[i], starts[i] + sizes[i])
+                staging[e0:e1].copy_(host_codes[e0:e1], non_blocking=True)
                 ready[i].record(copy)
 
     # Every chunk's copy is queued first; the pipeline's set-up overlaps
@@ -707,7 +718,12 @@ def _receive_host_stream(cfg, host_codes, half_lsb, reference_symbols, chunk_sam
     for i, a in enumerate(starts):
         m = sizes[i]
         comp.wait_event(ready[i])
-        pipe.feed(AdcCodes(staging[a:a + m], half_lsb, cfg.adc_rate_hz), flush=i == len(starts) - 1)
+        if p12:
+            e0, e1 = span(a, a + m)
+            chunk = AdcPacked12(staging[e0:e1], half_lsb, m, cfg.adc_rate_hz)
+        else:
+            chunk = AdcCodes(staging[a:a + m], half_lsb, cfg.adc_rate_hz)
+        pipe.feed(chunk, flush=i == len(starts) - 1)
         if trace is not None:
             import time
 

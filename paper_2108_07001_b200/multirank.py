@@ -203,26 +203,34 @@ def _front_end_host(pipe, adc, chunk_samples: int, flush: bool, dev) -> None:
     import torch
 
     from .rxdsp import side_stream
-    from .sigcore import AdcCodes
+    from .sigcore import AdcCodes, AdcPacked12
 
-    codes = adc.codes
-    n = int(codes.shape[0])
+    p12 = isinstance(adc, AdcPacked12)
+    host = adc.data if p12 else adc.codes
+    n = len(adc)
+
+    def span(a, b):   # element range of samples [a, b) (bytes for the packed format)
+        return (3 * a // 2, 3 * b // 2) if p12 else (a, b)
+
     comp = torch.cuda.current_stream(dev)
     copy = side_stream(dev, "h2d")
-    staging = torch.empty(n, dtype=torch.int16, device=dev)
+    staging = torch.empty(span(0, n)[1], dtype=torch.uint8 if p12 else torch.int16, device=dev)
     starts = list(range(0, n, chunk_samples))
     ready = [torch.cuda.Event() for _ in starts]
     copy.wait_stream(comp)
     with torch.cuda.stream(copy):
         for i, a in enumerate(starts):
-            m = min(chunk_samples, n - a)
-            staging[a:a + m].copy_(codes[a:a + m], non_blocking=True)
+            e0, e1 = span(a, min(a + chunk_samples, n))
+            staging[e0:e1].copy_(host[e0:e1], non_blocking=True)
             ready[i].record(copy)
     pipe.expect(n, chunk_samples)
     for i, a in enumerate(starts):
         m = min(chunk_samples, n - a)
         comp.wait_event(ready[i])
-        pipe.front_end(AdcCodes(staging[a:a + m], adc.half_lsb, adc.sample_rate_hz), flush=flush and i == len(starts) - 1)
+        e0, e1 = span(a, a + m)
+        chunk = (AdcPacked12(staging[e0:e1], adc.half_lsb, m, adc.sample_rate_hz) if p12
+                 else AdcCodes(staging[e0:e1], adc.half_lsb, adc.sample_rate_hz))
+        pipe.front_end(chunk, flush=flush and i == len(starts) - 1)
     staging.record_stream(comp)
 
 
@@ -231,15 +239,15 @@ def receive_rank(cfg, adc, reference_prefix, job: SuperframeJob, dist, chunk_sam
     """Receive this rank's super-frame of a multi-GPU stream."""
     import torch
 
-    from .sigcore import AdcCodes
+    from .sigcore import AdcCodes, AdcPacked12
 
     dev = _device()
     comm = TorchComm(dist, dev)
     hop = cfg.static_plan.hop
     pipe = RxPipeline(cfg, reference_symbols=reference_prefix if job.rank == 0 else None,
                       stream_offset=job.load_start, static_start_hop=job.core_start // hop)
-    if (chunk_samples and isinstance(adc, AdcCodes) and isinstance(adc.codes, torch.Tensor)
-            and not adc.codes.is_cuda):
+    host_t = adc.data if isinstance(adc, AdcPacked12) else (adc.codes if isinstance(adc, AdcCodes) else None)
+    if chunk_samples and isinstance(host_t, torch.Tensor) and not host_t.is_cuda:
         _front_end_host(pipe, adc, int(chunk_samples), job.last, dev)
     else:
         pipe.front_end(adc, flush=job.last)

@@ -49,6 +49,7 @@ from ._lib import SyncError
 from .constellation import ConstellationSpec, make_constellation, slicer_tables
 from .sigcore import (
     AdcCodes,
+    AdcPacked12,
     BlockPlan,
     ComplexSignal,
     FirFilter,
@@ -294,6 +295,13 @@ def _wg_from_T(T: np.ndarray):
 def _as_device_input(x, dev):
     """(tensor on dev, dtype code, scale) for feed / kk_reconstruct inputs."""
     torch = _torch()
+    if isinstance(x, AdcPacked12):
+        d = x.data
+        t = d if isinstance(d, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(d, dtype=np.uint8))
+        t = t[:3 * x.n // 2].to(dev, non_blocking=True).contiguous()
+        if t.data_ptr() % 4:            # the kernel reads aligned 32-bit words
+            t = t.clone()
+        return t, _lib.KK_DTYPE_P12, float(x.half_lsb)
     if isinstance(x, AdcCodes):
         c = x.codes
         t = c if isinstance(c, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(c, dtype=np.int16))
@@ -424,7 +432,7 @@ def kk_reconstruct(current, plan: BlockPlan, state: dict | None = None, clamp_re
     if plan.fft_size != KK_FFT:
         raise ParameterError("the B200 KK kernel is built for kk_plan.fft_size == 1024")
     fs = getattr(current, "sample_rate_hz", 4e9)
-    n = len(current.codes) if isinstance(current, AdcCodes) else len(
+    n = len(current) if isinstance(current, (AdcCodes, AdcPacked12)) else len(
         current.samples if is_signal(current) else current)
     hop = plan.hop
     if n % hop != 0 or n == 0:
@@ -868,11 +876,38 @@ class RxPipeline:
 
     # -- stages ------------------------------------------------------------------
 
+    # The raw FIFO holds the input as delivered (int16 codes, packed 12-bit
+    # bytes, f32 or f64); lengths and slices are in samples.
+    def _raw_len(self) -> int:
+        if self._raw is None:
+            return 0
+        n = int(self._raw.shape[0])
+        return n * 2 // 3 if self._raw_dt == _lib.KK_DTYPE_P12 else n
+
+    def _raw_slice(self, a: int, b: int | None = None):
+        if self._raw_dt == _lib.KK_DTYPE_P12:
+            return self._raw[3 * a // 2: None if b is None else 3 * b // 2]
+        return self._raw[a:b]
+
+    def _unpacked(self, t, dt):
+        """Packed 12-bit bytes -> int16 codes (device, kk_unpack12)."""
+        torch = _torch()
+        if dt != _lib.KK_DTYPE_P12:
+            return t, dt
+        n = int(t.shape[0]) * 2 // 3
+        out = torch.empty(n, dtype=torch.int16, device=self.dev)
+        _lib.call("kk_unpack12", _ptr(t), n, _ptr(out), _stream(self.dev))
+        return out, _lib.KK_DTYPE_I16
+
     def _append_raw(self, x, dt, scale):
         torch = _torch()
         if self._raw is None or self._raw.shape[0] == 0:
             self._raw, self._raw_dt, self._raw_scale = x, dt, scale
             return
+        if dt != self._raw_dt or scale != self._raw_scale:
+            # mixed formats: packed input is unpacked to int16 codes first
+            self._raw, self._raw_dt = self._unpacked(self._raw, self._raw_dt)
+            x, dt = self._unpacked(x, dt)
         if dt != self._raw_dt or scale != self._raw_scale:
             def f64(t, d, s):
                 return t.to(torch.float64) * s if d == _lib.KK_DTYPE_I16 else t.to(torch.float64)
@@ -1304,8 +1339,10 @@ class RxPipeline:
         if x is not None:
             self._append_raw(x, dt, sc)
         hop = self.cfg.kk_plan.hop
-        n_raw = 0 if self._raw is None else int(self._raw.shape[0])
+        n_raw = self._raw_len()
         if flush and n_raw % hop:
+            # zero padding (rx:775-778): packed codes cannot hold 0.0 -> int16
+            self._raw, self._raw_dt = self._unpacked(self._raw, self._raw_dt)
             pad = hop - n_raw % hop
             z = torch.zeros(pad, dtype=self._raw.dtype, device=self.dev)
             self._raw = torch.cat([self._raw, z])
@@ -1331,11 +1368,11 @@ class RxPipeline:
             fl = flush and last
             t0 = self._ev()
             if nh:
-                chunk = self._raw[:nh * hop]
+                chunk = self._raw_slice(0, nh * hop)
                 nv and torch.cuda.nvtx.range_push("kk")
                 self._run_kk(chunk, nh)
                 nv and torch.cuda.nvtx.range_pop()
-                self._raw = self._raw[nh * hop:]
+                self._raw = self._raw_slice(nh * hop)
             t1 = self._ev()
             nv and torch.cuda.nvtx.range_push("carrier")
             self._run_carrier(fl)
@@ -1491,7 +1528,7 @@ class RxPipeline:
 
 
 def _len(x) -> int:
-    if isinstance(x, AdcCodes):
+    if isinstance(x, (AdcCodes, AdcPacked12)):
         return len(x)
     if is_signal(x):
         return len(x.samples)

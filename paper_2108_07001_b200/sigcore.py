@@ -111,6 +111,57 @@ class AdcCodes:
 
 
 @dataclass
+class AdcPacked12:
+    """Packed 12-bit wire format (B200 addition; 1.5 B/sample): the 12-bit
+    ADC codes c (frontend.py:82-118, h = 2c + 1 the odd half-LSB code of
+    AdcCodes, value h * half_lsb) two per 3 bytes, little-endian (byte0 =
+    c0[7:0], byte1 = c0[11:8] | c1[3:0] << 4, byte2 = c1[11:4]).  `data`:
+    uint8 numpy array or torch tensor of >= 3 n / 2 bytes; n even."""
+
+    data: object
+    half_lsb: float
+    n: int
+    sample_rate_hz: float = 4e9
+
+    def __post_init__(self):
+        if self.n % 2:
+            raise ParameterError("packed 12-bit streams hold an even number of samples")
+        if int(self.data.shape[0]) < 3 * self.n // 2:
+            raise ParameterError("packed buffer shorter than 3 n / 2 bytes")
+
+    def __len__(self) -> int:
+        return int(self.n)
+
+
+def pack12(codes_h) -> np.ndarray:
+    """int16 odd half-LSB codes h = 2c + 1 (|c| < 2048) -> packed 12-bit bytes."""
+    h = np.asarray(codes_h, dtype=np.int32)
+    if len(h) % 2:
+        raise ParameterError("packed 12-bit streams hold an even number of samples")
+    if np.any((h & 1) == 0) or np.any(h < -4095) or np.any(h > 4095):
+        raise ParameterError("codes must be odd half-LSB codes of a 12-bit converter")
+    c = ((h - 1) >> 1) & 0xFFF
+    c0, c1 = c[0::2], c[1::2]
+    out = np.empty((len(h) // 2, 3), dtype=np.uint8)
+    out[:, 0] = c0 & 0xFF
+    out[:, 1] = (c0 >> 8) | ((c1 & 0xF) << 4)
+    out[:, 2] = c1 >> 4
+    return out.reshape(-1)
+
+
+def unpack12(data, n: int) -> np.ndarray:
+    """Packed 12-bit bytes -> int16 odd half-LSB codes (host reference of
+    kk_unpack12)."""
+    b = np.asarray(data, dtype=np.uint8)[:3 * n // 2].reshape(-1, 3).astype(np.int32)
+    c0 = b[:, 0] | ((b[:, 1] & 0xF) << 8)
+    c1 = (b[:, 1] >> 4) | (b[:, 2] << 4)
+    c = np.empty(n, dtype=np.int32)
+    c[0::2], c[1::2] = c0, c1
+    c = (c ^ 0x800) - 0x800
+    return (2 * c + 1).astype(np.int16)
+
+
+@dataclass
 class FirFilter:
     """FIR taps with the rate they are defined at (sigcore.py:102-118)."""
 

@@ -359,6 +359,60 @@ def test_host_stream_packed_bits_vs_reference():
     assert np.array_equal(got, np.unpackbits(pl[d_idx][:, None], axis=1)[:, -2:].reshape(-1))
 
 
+@pytest.mark.parametrize("name", ["c1_qpsk_b2b", "c3_64qam_1600km_rel-20"])
+def test_packed12_input_bit_identical(name):
+    """Packed 12-bit wire format unpacked inside K1's staging: the same codes,
+    so decisions and soft outputs are bit-identical to the int16 path, for
+    any (even) chunking, including a flush remainder and kk_unpack12."""
+    import torch
+
+    from paper_2108_07001_b200 import _lib
+    from paper_2108_07001_b200.sigcore import AdcPacked12, pack12, unpack12
+
+    cap = load_capture(name)
+    h = cap.adc_h[: len(cap.adc_h) - 300]           # not a hop multiple: flush pads
+    p = pack12(h)
+    cfg = cap.pipeline_config()
+    ref = rxdsp.RxPipeline(cfg, reference_symbols=cap.symbols())
+    ref.feed(AdcCodes(h, cap.half_lsb))
+    d1, s1 = ref.finish()
+    pipe = rxdsp.RxPipeline(cfg, reference_symbols=cap.symbols())
+    cuts = [0, 70_000, 70_002, 150_000, len(h)]
+    for a, b in zip(cuts, cuts[1:]):
+        pipe.feed(AdcPacked12(p[3 * a // 2: 3 * b // 2], cap.half_lsb, b - a))
+    d2, s2 = pipe.finish()
+    assert np.array_equal(d1, d2) and np.array_equal(s1, s2)
+    # the unpack kernel equals the host reference
+    pd = torch.from_numpy(p).cuda()
+    out = torch.empty(len(h), dtype=torch.int16, device="cuda")
+    _lib.call("kk_unpack12", pd.data_ptr(), len(h), out.data_ptr(), torch.cuda.current_stream().cuda_stream)
+    assert np.array_equal(out.cpu().numpy(), unpack12(p, len(h)))
+
+
+def test_host_stream_packed12_equals_int16():
+    """The e2e path with the packed 12-bit wire format (1.5 B/sample over
+    PCIe) returns exactly the int16 path's bits."""
+    import torch
+
+    from paper_2108_07001_b200.harness import receive_host_stream
+    from paper_2108_07001_b200.sigcore import pack12
+
+    cap = load_capture("c5_qpsk_10000km_tile")
+    reps = cap.meta["tile_reps"]
+    codes, _ = tile(cap, reps * len(cap.adc_h))
+    cfg = cap.pipeline_config(ddlms_frame_symbols=1 << 18)
+    ref_syms = np.tile(cap.symbols(), reps)
+    host16 = torch.from_numpy(codes).pin_memory()
+    _, b16, n16 = receive_host_stream(cfg, host16, cap.half_lsb, ref_syms, chunk_samples=1 << 20)
+    host12 = torch.from_numpy(pack12(codes)).pin_memory()
+    _, b12, n12 = receive_host_stream(cfg, host12, cap.half_lsb, ref_syms, chunk_samples=1 << 20,
+                                      packed12_samples=len(codes))
+    torch.cuda.synchronize()
+    assert n12 == n16
+    nb = (2 * n16 + 7) // 8
+    assert np.array_equal(b12[:nb].numpy(), b16[:nb].numpy())
+
+
 def test_raw_file_ingest_matches_host_stream(tmp_path):
     """the int16 wire format (raw + JSON sidecar) streamed from
     a file through pinned buffers gives the same packed bits as the pinned

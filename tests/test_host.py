@@ -236,3 +236,22 @@ def test_refine_static_taps_fits_capture():
     x = np.convolve(y2, np.array([0.05 - 0.02j, 1.0, -0.08 + 0.03j]), mode="same")
     _, diag = rxdsp.refine_static_taps(x, syms, n_taps=31, rate_hz=2e9)
     assert diag["relative_mse"] < 1e-2
+
+
+def test_pack12_round_trip_and_layout():
+    """Packed 12-bit wire format (sigcore.AdcPacked12): exact round trip of
+    odd half-LSB codes over the whole 12-bit range, the documented byte layout,
+    and the contract errors."""
+    from paper_2108_07001_b200.sigcore import AdcPacked12, pack12, unpack12
+
+    c = np.arange(-2048, 2048)
+    h = (2 * np.concatenate([c, c[::-1]]) + 1).astype(np.int16)
+    p = pack12(h)
+    assert len(p) == 3 * len(h) // 2
+    assert np.array_equal(unpack12(p, len(h)), h)
+    # layout: c0 = -2048 (0x800), c1 = 5 -> 0x00, 0x58, 0x00
+    assert list(pack12(np.array([2 * -2048 + 1, 2 * 5 + 1], np.int16))) == [0x00, 0x58, 0x00]
+    with pytest.raises(ParameterError):
+        pack12(np.array([1, 2], np.int16))          # even code: not a mid-rise level
+    with pytest.raises(ParameterError):
+        AdcPacked12(p[:3], 1.0, 3)                  # odd sample count
