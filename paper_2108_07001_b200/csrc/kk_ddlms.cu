@@ -204,6 +204,7 @@ struct RunOut {
     float* Tend;      // [16] end taps of the last block
     int* over;        // [nb] guard exceedances in the block's latest run
     unsigned long long* hash;  // [nb] hash of the block's latest label sequence
+    uint2* ties;               // [nb] recorded fp32-tie decisions (two slots per block)
     unsigned long long* counters;  // [0] changed decisions, [1] blocks re-run
     unsigned int* first_changed;   // lowest block index whose decisions changed (atomicMin)
 };
@@ -613,6 +614,60 @@ __device__ __forceinline__ int stage_idx(int chunk, int row, int col) {
     return (chunk * kChunkRows + row) * 32 + (col ^ ((row * 4) & 31));
 }
 
+// normalised slicer units (level spacing 1): distance from v to the nearest
+// decision boundary of level f's cell (edge levels are open outwards) ...
+__device__ __forceinline__ float axis_margin(float v, float f, float m1f) {
+    const float up = f < m1f ? 0.5f - (v - f) : 3.0e38f;
+    const float dn = f > 0.f ? 0.5f + (v - f) : 3.0e38f;
+    return fminf(up, dn);
+}
+// ... and how far v lies outside level s's cell (negative inside)
+__device__ __forceinline__ float cell_excess(float v, float s, float m1f) {
+    const float up = s < m1f ? v - s : -3.0e38f;
+    const float dn = s > 0.f ? s - v : -3.0e38f;
+    return fmaxf(up, dn) - 0.5f;
+}
+#ifndef KK_TIE_EPS
+#define KK_TIE_EPS 1e-5f
+#endif
+constexpr float kTieEps = KK_TIE_EPS;   // fp32 tie zone, normalised units (ties: DESIGN §4)
+
+// fp32 ties (|margin| < kTieEps): a re-run from start taps that differ by
+// rounding must not flip them back and forth.  The block's first decision at
+// a tie is recorded (two slots per block: bit 31 valid, bits 16..23 grid
+// cell ir * m + ii, bits 0..15 symbol within the block) and kept while y
+// stays within kTieEps of that cell; the symbol's margin is then the
+// distance to leaving that zone, not the rounding-level distance to the
+// boundary.
+__device__ __forceinline__ void tie_rule(int i, float vr, float vi, float m1f, int m, float& fr, float& fi,
+                                         float& mg_s, unsigned& tie0, unsigned& tie1, bool& dirty) {
+    const bool h0 = (tie0 >> 31) && (tie0 & 0xffffu) == static_cast<unsigned>(i);
+    const bool h1 = (tie1 >> 31) && (tie1 & 0xffffu) == static_cast<unsigned>(i);
+    if (h0 || h1) {
+        const int g = ((h0 ? tie0 : tie1) >> 16) & 0xff;
+        const float sr = static_cast<float>(g / m), si = static_cast<float>(g % m);
+        const float e = fmaxf(cell_excess(vr, sr, m1f), cell_excess(vi, si, m1f));
+        if (e < kTieEps) {
+            fr = sr;
+            fi = si;
+            mg_s = kTieEps - e;
+        }
+    } else {
+        const unsigned rec = 0x80000000u |
+                             (static_cast<unsigned>(static_cast<int>(fr) * m + static_cast<int>(fi)) << 16) |
+                             static_cast<unsigned>(i);
+        if (!(tie0 >> 31)) {
+            tie0 = rec;
+            mg_s = kTieEps + mg_s;
+            dirty = true;
+        } else if (!(tie1 >> 31)) {
+            tie1 = rec;
+            mg_s = kTieEps + mg_s;
+            dirty = true;
+        }
+    }
+}
+
 template <bool WITH_P, int SQ, bool AL16, bool TRAIN>
 __global__ void __launch_bounds__(kBlockThreads, WITH_P ? KK_DD_MINB_P : KK_DD_MINB)
 ddlms_block_kernel(SolveArgs a, Slicer sl, const float* __restrict__ Tstart, float* __restrict__ Pb,
@@ -745,7 +800,18 @@ ddlms_block_kernel(SolveArgs a, Slicer sl, const float* __restrict__ Tstart, flo
         for (int i = 0; i < 64; ++i) P[i] = (i % 9 == 0) ? 1.f : 0.f;
     }
     const float tm = 2.0f * a.mu;      // mu' (scale folded in)
-    float mgl = 0.5f, mgb = 3.0e38f, mx = 0.f, my2 = 0.f;
+    float mgl = 3.0e38f, mgb = 3.0e38f, mx = 0.f, my2 = 0.f;
+    // tie slots of the block (see the slicer below): bit 31 valid, bits
+    // 16..23 grid cell (ir * SQ + ii), bits 0..15 symbol within the block
+    unsigned tie0 = 0u, tie1 = 0u;
+    bool ties_dirty = false;
+    if constexpr (!WITH_P) {
+        if (run) {
+            const uint2 t = o.ties[b];
+            tie0 = t.x;
+            tie1 = t.y;
+        }
+    }
     unsigned long long hsh = 14695981039346656037ull;   // 64-bit FNV-1a of the block's labels
     float X[8];
     {
@@ -802,9 +868,17 @@ ddlms_block_kernel(SolveArgs a, Slicer sl, const float* __restrict__ Tstart, flo
                 // (v + 1.5*2^23) - 1.5*2^23 == rint(v) for |v| < 2^22.
                 constexpr float kMagic = 12582912.0f;
                 const float vr = fmaf(yr, half_norm, off), vi = fmaf(yi, half_norm, off);
-                const float fr = fminf(fmaxf((vr + kMagic) - kMagic, 0.f), static_cast<float>(m1));
-                const float fi = fminf(fmaxf((vi + kMagic) - kMagic, 0.f), static_cast<float>(m1));
-                const float mg_s = 0.5f - fmaxf(fabsf(vr - fr), fabsf(vi - fi));
+                const float m1f = static_cast<float>(m1);
+                float fr = fminf(fmaxf((vr + kMagic) - kMagic, 0.f), m1f);
+                float fi = fminf(fmaxf((vi + kMagic) - kMagic, 0.f), m1f);
+                // distance to the nearest decision boundary (an edge level has
+                // none on its outer side)
+                float mg_s = fminf(axis_margin(vr, fr, m1f), axis_margin(vi, fi, m1f));
+                if constexpr (!WITH_P) {
+                    const bool near = live && !trn && mg_s < kTieEps;
+                    if (__any_sync(0xffffffffu, near) && near)
+                        tie_rule(i, vr, vi, m1f, SQ, fr, fi, mg_s, tie0, tie1, ties_dirty);
+                }
                 mgl = (live && !trn) ? fminf(mgl, mg_s) : mgl;
                 const int ir = __float_as_int(fr + kMagic) - __float_as_int(kMagic);
                 const int ii = __float_as_int(fi + kMagic) - __float_as_int(kMagic);
@@ -817,16 +891,29 @@ ddlms_block_kernel(SolveArgs a, Slicer sl, const float* __restrict__ Tstart, flo
                 else sl_lab = grid[ir * SQ + ii];
                 lab = trn ? 255 : sl_lab;
             } else {
+                // square grid whose points are not exactly the fp32 level
+                // products (e.g. 16/64-QAM at unit power): table values.
+                // (computed for every lane: the warp vote must be convergent)
+                float vr = 0.f, vi = 0.f, fr = 0.f, fi = 0.f, mg_s = 3.0e38f;
+                const float m1f = static_cast<float>(m1);
+                if (sl.kind == 0) {
+                    vr = fmaf(yr, half_norm, off);
+                    vi = fmaf(yi, half_norm, off);
+                    fr = fminf(fmaxf(rintf(vr), 0.f), m1f);
+                    fi = fminf(fmaxf(rintf(vi), 0.f), m1f);
+                    mg_s = fminf(axis_margin(vr, fr, m1f), axis_margin(vi, fi, m1f));
+                    if constexpr (!WITH_P) {
+                        const bool near = live && !trn && mg_s < kTieEps;
+                        if (__any_sync(0xffffffffu, near) && near)
+                            tie_rule(i, vr, vi, m1f, m, fr, fi, mg_s, tie0, tie1, ties_dirty);
+                    }
+                }
                 if (trn) {
                     dr = tcur.x; di = tcur.y;
                     lab = 255;
                 } else if (sl.kind == 0) {
-                    const float vr = fmaf(yr, half_norm, off), vi = fmaf(yi, half_norm, off);
-                    const int ir = min(max(__float2int_rn(vr), 0), m1);
-                    const int ii = min(max(__float2int_rn(vi), 0), m1);
-                    if (live)
-                        mgl = fminf(mgl, 0.5f - fmaxf(fabsf(vr - static_cast<float>(ir)),
-                                                      fabsf(vi - static_cast<float>(ii))));
+                    if (live) mgl = fminf(mgl, mg_s);
+                    const int ir = static_cast<int>(fr), ii = static_cast<int>(fi);
                     lab = grid[ir * m + ii];
                     const float2 pp = pts[lab];
                     dr = pp.x; di = pp.y;
@@ -914,8 +1001,11 @@ ddlms_block_kernel(SolveArgs a, Slicer sl, const float* __restrict__ Tstart, flo
 #pragma unroll
             for (int i = 0; i < 16; ++i) o.Twritten[b * 16 + i] = Tstart[b * 16 + i];
         }
+        if constexpr (!WITH_P) {
+            if (ties_dirty) o.ties[b] = make_uint2(tie0, tie1);
+        }
         const bool sq = SQ > 0 || sl.kind == 0;
-        const float mg = sq ? mgl * (2.0f / sl.norm) : mgb;
+        const float mg = sq ? fminf(mgl, 0.5f * 3.0e38f) * (2.0f / sl.norm) : mgb;
         o.margin[b] = fminf(mg, fabsf(sl.thr - sqrtf(my2)));
         o.over[b] = my2 > thr2 ? 1 : 0;
         if (b == a.nb - 1) {
@@ -1475,6 +1565,7 @@ Layout plan(int64_t nsym, int B) {
     b += align_up(16 * sizeof(float));          // Tinit
     b += align_up(L.nb * sizeof(int));          // over
     b += align_up(L.nb * sizeof(unsigned long long));   // label hashes
+    b += align_up(L.nb * sizeof(uint2));                 // tie slots
     b += align_up(size_t(nsym) * 8);                     // ST (soft, unless bound to the caller's)
     b += align_up(size_t(nsym));                         // LT (labels, idem)
     b += align_up(L.nb * sizeof(int));                   // re-run list
@@ -1517,6 +1608,7 @@ struct DdlmsSolver {
     float *Tused, *Twritten, *margin, *maxx2, *Tend, *Tinit_d;
     int* over;
     unsigned long long *hsh, *ctr;
+    uint2* ties = nullptr;
     float2* ST_own = nullptr;    // workspace soft / labels (outputs not bound)
     uint8_t* LT_own = nullptr;
     int* list;
@@ -1692,6 +1784,7 @@ struct DdlmsSolver {
         Tinit_d = reinterpret_cast<float*>(w); w += align_up(16 * sizeof(float));
         over = reinterpret_cast<int*>(w); w += align_up(L.nb * sizeof(int));
         hsh = reinterpret_cast<unsigned long long*>(w); w += align_up(L.nb * 8);
+        ties = reinterpret_cast<uint2*>(w); w += align_up(L.nb * sizeof(uint2));
         ST_own = reinterpret_cast<float2*>(w); w += align_up(size_t(nsym) * 8);
         LT_own = reinterpret_cast<uint8_t*>(w); w += align_up(size_t(nsym));
         to.ST = ST_own;
@@ -1719,12 +1812,14 @@ struct DdlmsSolver {
         o.Tend = Tend;
         o.over = over;
         o.hash = hsh;
+        o.ties = ties;
         o.counters = ctr;
         o.first_changed = &rb->first_changed;
         bt = std::min<int64_t>(n_train / block, L.nb);
         ntb = std::min<int64_t>((n_train + block - 1) / block, L.nb);
         if (cudaMemsetAsync(over, 0, L.nb * sizeof(int), s) != cudaSuccess ||
             cudaMemsetAsync(hsh, 0, L.nb * 8, s) != cudaSuccess ||
+            cudaMemsetAsync(ties, 0, L.nb * sizeof(uint2), s) != cudaSuccess ||
             cudaMemsetAsync(Twritten, 0xFF, L.nb * 16 * sizeof(float), s) != cudaSuccess ||   // NaN: never written
             cudaMemsetAsync(ctr, 0, 4 * sizeof(unsigned long long), s) != cudaSuccess ||
             cudaMemsetAsync(&rb->first_changed, 0xFF, 2 * sizeof(unsigned int), s) != cudaSuccess ||

@@ -322,6 +322,8 @@ def _as_device_input(x, dev):
 
 # NVTX ranges around the pipeline stages (KK_NVTX=1; for nsys/ncu range filters)
 _NVTX = _os.environ.get("KK_NVTX", "0") == "1"
+# the DDLMS fixpoint loop as a CUDA-graph WHILE node (default) or host-driven
+_DDLMS_GRAPH = _os.environ.get("KK_DDLMS_GRAPH", "1") != "0"
 
 _SIDE_STREAMS = {}
 import threading as _threading
@@ -1080,7 +1082,9 @@ class RxPipeline:
                       tb.grid.ctypes.data if tb.grid_m else None, tb.grid_m, tb.norm, tb.max_radius,
                       float(d.divergence_factor), int(d.divergence_run), float(d.mu), B,
                       # worker-thread frames (streaming receive): host-driven loop, no graph
-                      -int(self.gpu.ddlms_max_iter) if self._async else int(self.gpu.ddlms_max_iter),
+                      # (KK_DDLMS_GRAPH=0 forces it: profilers that replay graph nodes)
+                      -int(self.gpu.ddlms_max_iter) if (self._async or not _DDLMS_GRAPH)
+                      else int(self.gpu.ddlms_max_iter),
                       float(self.gpu.ddlms_soft_tol), _ptr(labels), _ptr(soft),
                       _ptr(self._ws), wsb, st.data_ptr(), stream.cuda_stream)
             ev = torch.cuda.Event()

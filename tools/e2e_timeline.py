@@ -21,6 +21,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--out", default=None)
     ap.add_argument("--format", default="c5_qpsk_10000km_tile")
+    ap.add_argument("--packed12", action="store_true")
     args = ap.parse_args()
     import torch
     from torch.profiler import ProfilerActivity, profile
@@ -33,14 +34,17 @@ def main():
     cfg = dataclasses.replace(cfg, gpu=dataclasses.replace(cfg.gpu, ddlms_frame_symbols=1 << 26))
     n = 1 << 30
     codes, _ = tile(cap, n)
-    host = torch.from_numpy(codes).pin_memory()
+    from paper_2108_07001_b200.sigcore import pack12
+
+    host = torch.from_numpy(pack12(codes) if args.packed12 else codes).pin_memory()
     pts = cap.symbols()[:10000]
     bits = torch.empty(n // 4 * 2 // 8 + 65536, dtype=torch.uint8).pin_memory()
-    st = torch.empty(n, dtype=torch.int16, device="cuda")
+    st = (torch.empty(3 * n // 2, dtype=torch.uint8, device="cuda") if args.packed12
+          else torch.empty(n, dtype=torch.int16, device="cuda"))
 
     def step():
         pipe, _, _ = receive_host_stream(cfg, host, cap.half_lsb, pts, chunk_samples=1 << 25, bits_host=bits,
-                                         staging=st)
+                                         staging=st, packed12_samples=n if args.packed12 else None)
         pipe.release_buffers()
 
     for _ in range(3):
