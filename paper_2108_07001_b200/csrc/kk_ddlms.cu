@@ -25,6 +25,7 @@
 // sequential chain.
 #include <algorithm>
 #include <chrono>
+#include <climits>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -184,6 +185,7 @@ struct SolveArgs {
     float mu;
     int B;                // symbols per block
     int64_t nb;
+    int guard_run = 100;  // divergence guard run length (rx:484-490)
 };
 
 // symbol k's window x[2k .. 2k+3] (scaled); consecutive symbols share two
@@ -205,6 +207,9 @@ struct RunOut {
     int* over;        // [nb] guard exceedances in the block's latest run
     unsigned long long* hash;  // [nb] hash of the block's latest label sequence
     uint2* ties;               // [nb] recorded fp32-tie decisions (two slots per block)
+    int2* grun;                // [nb] guard exceedance runs of the block's latest stored run:
+                               //   x = leading run | trailing run << 16, y = first in-block run
+                               //   reaching guard_run (0xffff: none) | all-exceeded << 16
     unsigned long long* counters;  // [0] changed decisions, [1] blocks re-run
     unsigned int* first_changed;   // lowest block index whose decisions changed (atomicMin)
 };
@@ -352,6 +357,9 @@ struct ReadBack {
     unsigned int last_first;     // the same for the last finished iteration
     unsigned long long it_stats[2 * kMaxStatIters];   // per iteration (changed, re-run)
     float Tend[16];              // end taps of the frame (scaled)
+    float Tfz[16];               // frozen taps (scaled) of a guard freeze
+    long long freeze_k;          // symbol whose exceedance run froze the taps (LLONG_MAX: none)
+    int carry;                   // div_count at the frame end (exceedance run in progress)
 };
 
 __device__ __forceinline__ bool ctl_done(const int* ctl) { return ctl && *ctl == kModeDone; }
@@ -402,9 +410,16 @@ __global__ void frame_begin_kernel(const float* __restrict__ T_in, float scale, 
                                    const int* __restrict__ state, ReadBack* rb) {
     const int i = threadIdx.x;
     if (i < 16) Tinit[i] = T_in[i] * scale;
-    if (i == 0 && state && (state[0] != 0 || state[1] != 0)) {
-        rb->ctl[0] = kModeDone;
-        rb->ctl[3] = 1;
+    if (i < 16) rb->Tfz[i] = T_in[i] * scale;
+    if (i == 0) {
+        rb->freeze_k = LLONG_MAX;
+        rb->carry = 0;
+        // taps frozen by an earlier frame: every decision of this frame is a
+        // parallel map with constant taps (mode 3); the solver stands down
+        if (state && state[0] != 0) {
+            rb->ctl[0] = kModeDone;
+            rb->ctl[3] = 3;
+        }
     }
 }
 
@@ -418,16 +433,155 @@ __global__ void copy16_kernel(float* __restrict__ dst, const float* __restrict__
 // block m, chain from m.  ctl[2] gates the mode-2 kernels (kModeOutput: run).
 __global__ void frame_end_kernel(ReadBack* rb) {
     int fb = rb->ctl[3];
-    if (fb == 0) fb = rb->ctr[2] > 0 ? 1 : (rb->ctl[0] != kModeDone ? 2 : 0);
+    if (fb == 0 && rb->ctl[0] != kModeDone) fb = 2;
     rb->ctl[3] = fb;
-    rb->ctl[2] = fb == 2 ? kModeOutput : kModeDone;
+    rb->ctl[2] = (fb == 2 || fb == 4) ? kModeOutput : kModeDone;
     rb->ctr[3] = 0;
 }
 
-// mode 2: re-run list = blocks [0, m) (their starts are exact: none changed)
-__global__ void fallback_list_kernel(ReadBack* rb, int* __restrict__ list, int64_t nb) {
-    if (rb->ctl[3] != 2) return;
-    const int64_t m = min(static_cast<int64_t>(rb->last_first), nb);
+// Divergence guard (rx:484-490) at the converged fixpoint: the decisions are
+// those of the live-tap recurrence, so they are exact up to the first symbol
+// k* at which an exceedance run reaches guard_run (taps freeze there).  Runs
+// cross blocks: a block's carry-in is the trailing run of the block before,
+// extended through all-exceeded blocks (at most guard_run / B + 1 of them),
+// starting from the frame-start div_count.  One thread per block holding an
+// exceedance; the earliest freeze wins (atomicMin); the last block records
+// the frame-end div_count.
+__global__ void guard_scan_kernel(ReadBack* rb, const int2* __restrict__ grun, const int* __restrict__ over,
+                                  int64_t nb, int B, int64_t nsym, int guard_run, const int* __restrict__ state,
+                                  int final_pass) {
+    // in the fixpoint loop (final_pass 0): only the certified prefix -- the
+    // blocks below the lowest block whose decisions changed this iteration
+    // ran from exact starts -- so a freeze found there is the
+    // stream's; the blocks after it need no further iterations
+    if (rb->ctl[3] != 0 || rb->ctr[2] == 0) return;
+    if (!final_pass && rb->ctl[0] == kModeDone) return;
+    const int64_t limit = final_pass ? nb : min(nb, static_cast<int64_t>(rb->first_changed));
+    for (int64_t b = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; b < nb; b += int64_t(gridDim.x) * blockDim.x) {
+        const bool last = final_pass && b == nb - 1;
+        if (b >= limit || (!over[b] && !last)) continue;
+        int64_t c = 0;
+        for (int64_t j = b - 1;; --j) {
+            if (j < 0) {
+                c += state ? state[1] : 0;
+                break;
+            }
+            const int2 g = grun[j];
+            if ((g.y >> 16) & 1) {                    // all exceeded: the run continues through it
+                c += min(static_cast<int64_t>(B), nsym - j * B);
+                if (c >= guard_run) break;
+            } else {
+                c += (g.x >> 16) & 0xffff;            // trailing run
+                break;
+            }
+        }
+        const int2 g = grun[b];
+        const int pre = g.x & 0xffff, first = g.y & 0xffff;
+        const int64_t k0 = b * B;
+        if (over[b]) {
+            long long cand = LLONG_MAX;
+            if (c + pre >= guard_run) cand = k0 + (guard_run - c - 1);
+            else if (first != 0xffff) cand = k0 + first;
+            if (cand != LLONG_MAX) atomicMin(&rb->freeze_k, cand);
+        }
+        if (last)
+            rb->carry = static_cast<int>(min(static_cast<int64_t>(guard_run),
+                                             ((g.y >> 16) & 1) ? c + (nsym - k0) : ((g.x >> 16) & 0xffff)));
+    }
+}
+
+// a certified freeze ends the fixpoint iteration (mode 4)
+__global__ void guard_decide_kernel(ReadBack* rb) {
+    if (rb->ctl[3] == 0 && rb->freeze_k != LLONG_MAX) {
+        rb->ctl[3] = 4;
+        rb->ctl[0] = kModeDone;
+    }
+}
+
+// mode 4: the exact chain of the freezing block from its (exact) start taps
+// up to the freezing symbol k* (which is decided with the taps it froze,
+// without an update); the frozen taps -> rb->Tfz
+__global__ void freeze_chain_kernel(SolveArgs a, Slicer sl, const float* __restrict__ Tstart, ReadBack* rb,
+                                    uint8_t* __restrict__ labels, float2* __restrict__ soft) {
+    if (threadIdx.x != 0 || blockIdx.x != 0 || rb->ctl[3] != 4) return;
+    const int64_t ks = rb->freeze_k;
+    const int64_t b = ks / a.B;
+    float T[16];
+    for (int i = 0; i < 16; ++i) T[i] = Tstart[b * 16 + i];
+    const float tm = 2.0f * a.mu;
+    for (int64_t k = b * a.B; k <= ks; ++k) {
+        float X[8];
+        for (int u = 0; u < 4; ++u) {
+            const float2 v = a.x[2 * k + u];
+            X[2 * u] = v.x;
+            X[2 * u + 1] = v.y;
+        }
+        float yr = 0.f, yi = 0.f;
+        for (int j = 0; j < 8; ++j) {
+            yr = fmaf(T[j], X[j], yr);
+            yi = fmaf(T[8 + j], X[j], yi);
+        }
+        float dr, di;
+        int lab;
+        if (k < a.n_train) {
+            const float2 t = a.train[k];
+            dr = t.x;
+            di = t.y;
+            lab = 255;
+        } else {
+            float m;
+            lab = slice(sl, yr, yi, m);
+            dr = sl.pts[lab].x;
+            di = sl.pts[lab].y;
+        }
+        labels[k] = static_cast<uint8_t>(lab);
+        soft[k] = make_float2(yr, yi);
+        if (k == ks) break;                        // frozen: no update from here on
+        const float er = tm * (dr - yr), ei = tm * (di - yi);
+        for (int j = 0; j < 8; ++j) {
+            T[j] = fmaf(er, X[j], T[j]);
+            T[8 + j] = fmaf(ei, X[j], T[8 + j]);
+        }
+    }
+    for (int i = 0; i < 16; ++i) rb->Tfz[i] = T[i];
+}
+
+// modes 3 / 4: decisions with frozen taps are independent of each other --
+// a parallel map (rb->Tfz: the frame-start taps in mode 3)
+__global__ void frozen_map_kernel(SolveArgs a, Slicer sl, const ReadBack* rb, uint8_t* __restrict__ labels,
+                                  float2* __restrict__ soft) {
+    const int mode = rb->ctl[3];
+    if (mode != 3 && mode != 4) return;
+    const int64_t k0 = mode == 3 ? 0 : rb->freeze_k + 1;
+    __shared__ float Ts[16];
+    if (threadIdx.x < 16) Ts[threadIdx.x] = rb->Tfz[threadIdx.x];
+    __syncthreads();
+    for (int64_t k = k0 + int64_t(blockIdx.x) * blockDim.x + threadIdx.x; k < a.nsym;
+         k += int64_t(gridDim.x) * blockDim.x) {
+        float yr = 0.f, yi = 0.f;
+        for (int u = 0; u < 4; ++u) {
+            const float2 v = __ldg(a.x + 2 * k + u);
+            yr = fmaf(Ts[2 * u], v.x, fmaf(Ts[2 * u + 1], v.y, yr));
+            yi = fmaf(Ts[8 + 2 * u], v.x, fmaf(Ts[9 + 2 * u], v.y, yi));
+        }
+        int lab = 255;
+        if (k >= a.n_train) {
+            float m;
+            lab = slice(sl, yr, yi, m);
+        }
+        labels[k] = static_cast<uint8_t>(lab);
+        soft[k] = make_float2(yr, yi);
+    }
+}
+
+// modes 2 / 4: output pass over blocks [0, m) -- m the lowest block whose
+// decisions changed in the last iteration (their starts are exact), or the
+// freezing block
+__global__ void fallback_list_kernel(ReadBack* rb, int* __restrict__ list, int64_t nb, int B) {
+    const int mode = rb->ctl[3];
+    if (mode != 2 && mode != 4) return;
+    const int64_t m = mode == 4 ? min(static_cast<int64_t>(rb->freeze_k / B), nb)
+                                : min(static_cast<int64_t>(rb->last_first), nb);
     for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < m; i += int64_t(gridDim.x) * blockDim.x)
         list[i] = static_cast<int>(i);
     if (blockIdx.x == 0 && threadIdx.x == 0) rb->ctr[3] = static_cast<unsigned long long>(m > 0 ? m : 0);
@@ -461,12 +615,14 @@ __global__ void seq_fallback_kernel(const float2* __restrict__ x, int64_t nsym, 
 // guard exceedance in the frame: div_count ends at 0, taps live)
 __global__ void frame_final_kernel(const ReadBack* rb, float inv_scale, float* __restrict__ T_io,
                                    int* __restrict__ state_io) {
-    if (rb->ctl[3] == 1) return;
+    const int mode = rb->ctl[3];
+    if (mode == 1) return;                         // the sequential chain wrote them
+    const bool frozen = mode == 3 || mode == 4;
     const int i = threadIdx.x;
-    if (i < 16) T_io[i] = rb->Tend[i] * inv_scale;
+    if (i < 16) T_io[i] = (frozen ? rb->Tfz[i] : rb->Tend[i]) * inv_scale;
     if (i == 0 && state_io) {
-        state_io[0] = 0;
-        state_io[1] = 0;
+        state_io[0] = frozen ? 1 : 0;
+        state_io[1] = frozen ? 0 : rb->carry;    // (a frozen state never unfreezes: div_count is moot)
     }
 }
 
@@ -805,6 +961,11 @@ ddlms_block_kernel(SolveArgs a, Slicer sl, const float* __restrict__ Tstart, flo
     // 16..23 grid cell (ir * SQ + ii), bits 0..15 symbol within the block
     unsigned tie0 = 0u, tie1 = 0u;
     bool ties_dirty = false;
+    // divergence-guard runs (|y| > thr): leading / current run length and the
+    // first in-block run reaching guard_run; gmt: min | |y|^2 - thr^2 |
+    int g_pre = 0, g_run = 0, g_first = 0xffff;
+    bool g_lead = true;
+    float gmt = 3.0e38f;
     if constexpr (!WITH_P) {
         if (run) {
             const uint2 t = o.ties[b];
@@ -925,7 +1086,25 @@ ddlms_block_kernel(SolveArgs a, Slicer sl, const float* __restrict__ Tstart, flo
                     dr = pp.x; di = pp.y;
                 }
             }
-            my2 = live ? fmaxf(my2, fmaf(yr, yr, yi * yi)) : my2;
+            {
+                const float d2 = fmaf(yr, yr, yi * yi);
+                my2 = live ? fmaxf(my2, d2) : my2;
+                if constexpr (!WITH_P) {
+                    gmt = live ? fminf(gmt, fabsf(d2 - thr2)) : gmt;
+                    if (live) {
+                        if (d2 > thr2) {
+                            ++g_run;
+                            if (!g_lead && g_run == a.guard_run && g_first == 0xffff) g_first = i;
+                        } else {
+                            if (g_lead) {
+                                g_pre = g_run;
+                                g_lead = false;
+                            }
+                            g_run = 0;
+                        }
+                    }
+                }
+            }
             const float er = live ? tm * (dr - yr) : 0.f, ei = live ? tm * (di - yi) : 0.f;
             if constexpr (WITH_P) {
                 float n2 = 0.f;
@@ -1006,8 +1185,17 @@ ddlms_block_kernel(SolveArgs a, Slicer sl, const float* __restrict__ Tstart, flo
         }
         const bool sq = SQ > 0 || sl.kind == 0;
         const float mg = sq ? fminf(mgl, 0.5f * 3.0e38f) * (2.0f / sl.norm) : mgb;
-        o.margin[b] = fminf(mg, fabsf(sl.thr - sqrtf(my2)));
+        // guard certificate: every symbol's side of the threshold, not only
+        // the block maximum's (| |y| - thr | >= | |y|^2 - thr^2 | / (2 max(|y|, thr)))
+        const float gm = WITH_P ? fabsf(sl.thr - sqrtf(my2)) : gmt / (2.0f * sqrtf(fmaxf(my2, thr2)));
+        o.margin[b] = fminf(mg, gm);
         o.over[b] = my2 > thr2 ? 1 : 0;
+        if constexpr (!WITH_P) {
+            const int full = g_lead ? 1 : 0;
+            const int pre = g_lead ? g_run : g_pre;
+            o.grun[b] = make_int2((pre & 0xffff) | ((g_run & 0xffff) << 16), (g_first & 0xffff) | (full << 16));
+            if (my2 > thr2) atomicMax(o.counters + 2, 1ull);   // "an exceedance was seen": guard checks from now on
+        }
         if (b == a.nb - 1) {
 #pragma unroll
             for (int i = 0; i < 16; ++i) o.Tend[i] = T[i];
@@ -1566,6 +1754,7 @@ Layout plan(int64_t nsym, int B) {
     b += align_up(L.nb * sizeof(int));          // over
     b += align_up(L.nb * sizeof(unsigned long long));   // label hashes
     b += align_up(L.nb * sizeof(uint2));                 // tie slots
+    b += align_up(L.nb * sizeof(int2));                  // guard runs
     b += align_up(size_t(nsym) * 8);                     // ST (soft, unless bound to the caller's)
     b += align_up(size_t(nsym));                         // LT (labels, idem)
     b += align_up(L.nb * sizeof(int));                   // re-run list
@@ -1609,6 +1798,7 @@ struct DdlmsSolver {
     int* over;
     unsigned long long *hsh, *ctr;
     uint2* ties = nullptr;
+    int2* grun = nullptr;
     float2* ST_own = nullptr;    // workspace soft / labels (outputs not bound)
     uint8_t* LT_own = nullptr;
     int* list;
@@ -1617,6 +1807,7 @@ struct DdlmsSolver {
     int64_t bt = 0;      // pure training blocks
     int64_t ntb = 0;     // blocks holding any training symbol
     bool speculated = false;
+    bool speculated_async = false;   // solve_async: guard checks inside the loop
     int64_t iters = 0, reruns = 0, last_changed = 0;
     unsigned int last_first_changed = 0;   // lowest changed block of the last iteration (solve_loop)
 
@@ -1785,6 +1976,7 @@ struct DdlmsSolver {
         over = reinterpret_cast<int*>(w); w += align_up(L.nb * sizeof(int));
         hsh = reinterpret_cast<unsigned long long*>(w); w += align_up(L.nb * 8);
         ties = reinterpret_cast<uint2*>(w); w += align_up(L.nb * sizeof(uint2));
+        grun = reinterpret_cast<int2*>(w); w += align_up(L.nb * sizeof(int2));
         ST_own = reinterpret_cast<float2*>(w); w += align_up(size_t(nsym) * 8);
         LT_own = reinterpret_cast<uint8_t*>(w); w += align_up(size_t(nsym));
         to.ST = ST_own;
@@ -1813,6 +2005,7 @@ struct DdlmsSolver {
         o.over = over;
         o.hash = hsh;
         o.ties = ties;
+        o.grun = grun;
         o.counters = ctr;
         o.first_changed = &rb->first_changed;
         bt = std::min<int64_t>(n_train / block, L.nb);
@@ -1947,6 +2140,7 @@ struct DdlmsSolver {
                     rc = check_launch("cascade_prep_kernel");
                     if (rc == KK_OK) rc = run_blocks(false, 0, kCascadeW, 0, soft_tol, 3, list);
                 }
+                if (rc == KK_OK && ctl_d && speculated_async) rc = guard_check();
                 if (rc == KK_OK) rc = scan_up(false);
                 if (rc == KK_OK) {
                     ddlms_advance_kernel<<<1, 1, 0, s>>>(rb, cudaGraphConditionalHandle{}, 0, 0);
@@ -2016,9 +2210,19 @@ struct DdlmsSolver {
             if (int rc = check_launch("cascade_prep_kernel")) return rc;
             if (int rc = run_blocks(false, 0, kCascadeW, 0, soft_tol, 3, list)) return rc;
         }
+        if (int rc = guard_check()) return rc;
         if (int rc = scan_up(false)) return rc;
         ddlms_advance_kernel<<<1, 1, 0, s>>>(rb, h, 1, max_iter);
         return check_launch("ddlms_advance_kernel");
+    }
+
+    // a divergence-guard freeze in the certified prefix ends the iteration
+    // (both kernels return at once unless an exceedance has been seen)
+    int guard_check() {
+        guard_scan_kernel<<<148 * 4, 128, 0, s>>>(rb, grun, over, L.nb, a.B, a.nsym, a.guard_run, nullptr, 0);
+        if (int rc = check_launch("guard_scan_kernel")) return rc;
+        guard_decide_kernel<<<1, 1, 0, s>>>(rb);
+        return check_launch("guard_decide_kernel");
     }
 
     // Instantiated loop graphs are cached by everything their kernels' launch
@@ -2033,7 +2237,7 @@ struct DdlmsSolver {
             static_cast<uint64_t>(a.n_train), f2u(a.mu), f2u(a.scale), static_cast<uint64_t>(a.B),
             static_cast<uint64_t>(a.nb), reinterpret_cast<uint64_t>(ws_base), reinterpret_cast<uint64_t>(to.LT),
             reinterpret_cast<uint64_t>(to.ST), f2u(soft_tol), static_cast<uint64_t>(max_iter),
-            static_cast<uint64_t>(ntb), static_cast<uint64_t>(bt),
+            static_cast<uint64_t>(ntb), static_cast<uint64_t>(bt), static_cast<uint64_t>(a.guard_run),
             static_cast<uint64_t>(sl.kind), static_cast<uint64_t>(sl.npts), static_cast<uint64_t>(sl.m),
             f2u(sl.norm), f2u(sl.thr), static_cast<uint64_t>(sl.sep), f2u(sl.lev_h)};
         for (int i = 0; i < 64; ++i) k.push_back(f2u(sl.pts[i].x) << 32 | f2u(sl.pts[i].y));
@@ -2116,6 +2320,7 @@ struct DdlmsSolver {
 
     int solve_async(float* T_io, int* state_io, int max_iter, int guard_run, float mu_raw, int64_t* stats_out,
                     uint8_t* labels, float2* soft, bool use_graph) {
+        a.guard_run = guard_run;
         ctl_d = rb->ctl;
         if (cudaMemsetAsync(rb, 0, sizeof(ReadBack), s) != cudaSuccess ||
             cudaMemsetAsync(&rb->first_changed, 0xFF, 2 * sizeof(unsigned int), s) != cudaSuccess)
@@ -2141,6 +2346,7 @@ struct DdlmsSolver {
         }
         if (int rc = scan_up(true)) return rc;
         speculated = true;
+        speculated_async = true;
         if (cudaMemsetAsync(ctr, 0, 4 * sizeof(unsigned long long), s) != cudaSuccess ||
             cudaMemsetAsync(&rb->first_changed, 0xFF, sizeof(unsigned int), s) != cudaSuccess)
             return set_cuda_error("solve_async counters");
@@ -2174,14 +2380,19 @@ struct DdlmsSolver {
             return set_cuda_error("ctr");
         sum_int_kernel<<<static_cast<unsigned>(gblocks), 128, 0, s>>>(over, L.nb, ctr + 2);
         if (int rc = check_launch("sum_int_kernel")) return rc;
+        // guard exceedances in a converged frame: the first freeze, if any
+        guard_scan_kernel<<<148 * 4, 128, 0, s>>>(rb, grun, over, L.nb, a.B, a.nsym, a.guard_run, state_io, 1);
+        if (int rc = check_launch("guard_scan_kernel")) return rc;
+        guard_decide_kernel<<<1, 1, 0, s>>>(rb);
+        if (int rc = check_launch("guard_decide_kernel")) return rc;
         frame_end_kernel<<<1, 1, 0, s>>>(rb);
         if (int rc = check_launch("frame_end_kernel")) return rc;
-        // mode 2 (not converged): output pass of [0, m), chain from m
+        // modes 2 (not converged) / 4 (freeze): output pass of [0, m); mode 2: chain from m
         {
             const int* save = ctl_d;
             ctl_d = &rb->ctl[2];   // kModeOutput in mode 2, kModeDone otherwise
             fallback_list_kernel<<<static_cast<unsigned>(std::min<int64_t>((L.nb + 255) / 256, 1024)), 256, 0, s>>>(
-                rb, list, L.nb);
+                rb, list, L.nb, a.B);
             int rc = check_launch("fallback_list_kernel");
             if (rc == KK_OK) rc = scan_down();
             if (rc == KK_OK) rc = run_blocks(false, 0, L.nb, 0, soft_tol, 3, list);
@@ -2202,6 +2413,12 @@ struct DdlmsSolver {
         seq_fallback_kernel<<<1, 1, 0, s>>>(a.x, a.nsym, scale, a.train, a.n_train, Tinit_d, T_io, state_io, sl,
                                             mu_raw, guard_run, to.LT, to.ST, rb);
         if (int rc = check_launch("seq_fallback_kernel")) return rc;
+        // mode 4: the freezing block's chain; modes 3 / 4: frozen-tap map
+        freeze_chain_kernel<<<1, 1, 0, s>>>(a, sl, lv[0].T, rb, to.LT, to.ST);
+        if (int rc = check_launch("freeze_chain_kernel")) return rc;
+        frozen_map_kernel<<<static_cast<unsigned>(std::min<int64_t>((a.nsym + 255) / 256, 148 * 16)), 256, 0, s>>>(
+            a, sl, rb, to.LT, to.ST);
+        if (int rc = check_launch("frozen_map_kernel")) return rc;
         frame_final_kernel<<<1, 32, 0, s>>>(rb, 1.0f / scale, T_io, state_io);
         if (int rc = check_launch("frame_final_kernel")) return rc;
         if (stats_out) {

@@ -1111,10 +1111,8 @@ class RxPipeline:
         stats.update(iterations=it, blocks_rerun=int(st[1]), fallback=int(st[2]), guard_exceed=int(st[3]),
                      blocks=int(st[5]), per_iter=[(int(st[6 + 2 * i]), int(st[7 + 2 * i])) for i in range(min(it, 16))],
                      T_start=[float(v) for v in T_start.cpu().numpy()])
-        if stats["fallback"] == 1:
-            stats["mode"] = "sequential(guard)"
-        elif stats["fallback"] == 2:
-            stats["mode"] = "solve+chain(not converged)"
+        stats["mode"] = {1: "sequential(guard)", 2: "solve+chain(not converged)", 3: "frozen(map)",
+                         4: "solve+freeze(map)"}.get(stats["fallback"], stats["mode"])
         return stats
 
     @property
