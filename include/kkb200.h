@@ -160,7 +160,8 @@ int kk_ddlms_solve(const void *x, int64_t nsym, float scale, const void *train, 
  * K4 asynchronous form of kk_ddlms_solve (B200 addition): everything is
  * enqueued on `stream`, nothing is read back, so the host can queue the next
  * frame / stream while this one runs.  The fixpoint loop runs as a CUDA-graph
- * WHILE node.  T_io: device float[16], the frame's start taps in, its end taps
+ * WHILE node.  widely_linear = 0: the linear equaliser (rxdsp.py:491-497 with
+ * g = 0; T keeps the form T1 = T0 M).  T_io: device float[16], the frame's start taps in, its end taps
  * out (real 2x8 form); state_io: device int[2] {frozen, div_count} in/out
  * (rxdsp.py:484-490 guard state); stats_out: device or mapped pinned host
  * int64[38] (layout of kk_ddlms_solve's stats; [2] = fallback taken: 1 exact
@@ -174,8 +175,8 @@ int kk_ddlms_solve(const void *x, int64_t nsym, float scale, const void *train, 
 int kk_ddlms_solve_async(const void *x, int64_t nsym, float scale, const void *train, int64_t n_train,
                          float *T_io, int *state_io, int order, const float *pts_host, const uint8_t *grid_host,
                          int grid_m, float norm, float max_radius, float guard_factor, int guard_run, float mu,
-                         int block, int max_iter, float soft_tol, uint8_t *labels, void *soft, void *workspace,
-                         size_t ws_bytes, int64_t *stats_out, void *stream);
+                         int widely_linear, int block, int max_iter, float soft_tol, uint8_t *labels, void *soft,
+                         void *workspace, size_t ws_bytes, int64_t *stats_out, void *stream);
 
 /*
  * K4 as a phased solver over one frame, so frames on different GPUs can be

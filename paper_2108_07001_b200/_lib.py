@@ -55,8 +55,8 @@ _SIGS = {
     "kk_ddlms_workspace_bytes": ([_I64, _I], _SZ),
     "kk_ddlms_solve": ([_P, _I64, _F, _P, _I64, _P, _I, _P, _P, _I, _F, _F, _F, _I, _F, _I, _I, _F, _P, _P,
                         _P, _P, _SZ, _P, _P], _I),
-    "kk_ddlms_solve_async": ([_P, _I64, _F, _P, _I64, _P, _P, _I, _P, _P, _I, _F, _F, _F, _I, _F, _I, _I, _F,
-                              _P, _P, _P, _SZ, _P, _P], _I),
+    "kk_ddlms_solve_async": ([_P, _I64, _F, _P, _I64, _P, _P, _I, _P, _P, _I, _F, _F, _F, _I, _F, _I, _I, _I,
+                              _F, _P, _P, _P, _SZ, _P, _P], _I),
     "kk_ddlms_create": ([_P, _I64, _F, _P, _I64, _I, _P, _P, _I, _F, _F, _F, _F, _I, _F, _P, _SZ, _P], _P),
     "kk_ddlms_train": ([_P, _P, _P], _I),
     "kk_ddlms_speculate": ([_P, _P, _P], _I),

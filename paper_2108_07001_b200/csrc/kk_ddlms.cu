@@ -186,6 +186,7 @@ struct SolveArgs {
     int B;                // symbols per block
     int64_t nb;
     int guard_run = 100;  // divergence guard run length (rx:484-490)
+    int lin = 0;          // linear (not widely-linear) equaliser
 };
 
 // symbol k's window x[2k .. 2k+3] (scaled); consecutive symbols share two
@@ -207,9 +208,9 @@ struct RunOut {
     int* over;        // [nb] guard exceedances in the block's latest run
     unsigned long long* hash;  // [nb] hash of the block's latest label sequence
     uint2* ties;               // [nb] recorded fp32-tie decisions (two slots per block)
-    int2* grun;                // [nb] guard exceedance runs of the block's latest stored run:
-                               //   x = leading run | trailing run << 16, y = first in-block run
-                               //   reaching guard_run (0xffff: none) | all-exceeded << 16
+    int2* grun;                // [nb] guard exceedance runs of the block's latest run:
+                               //   x = leading run | trailing run << 16, y = (first in-block run
+                               //   reaching guard_run) + 1 (0: none) | all-exceeded << 16
     unsigned long long* counters;  // [0] changed decisions, [1] blocks re-run
     unsigned int* first_changed;   // lowest block index whose decisions changed (atomicMin)
 };
@@ -219,6 +220,20 @@ struct RunOut {
 // block only if |T_new - T_used|_F * max|X| >= min(margin, soft_tol).
 struct ReadBack;
 __device__ bool fallback_gate(const ReadBack* rb, int64_t& b_lo);
+
+// linear-equaliser update of real-form taps (see ddlms_block_kernel<.., LIN>)
+__device__ __forceinline__ void lin_update(float (&T)[16], const float (&X)[8], float el, float fl) {
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+        const float x0 = X[2 * u], x1 = X[2 * u + 1];
+        const float d0 = fmaf(el, x0, fl * x1);
+        const float d1 = fmaf(el, x1, -fl * x0);
+        T[2 * u] += d0;
+        T[2 * u + 1] += d1;
+        T[8 + 2 * u] -= d1;
+        T[9 + 2 * u] += d0;
+    }
+}
 
 __global__ void ddlms_run_kernel(SolveArgs a, Slicer sl, const float* __restrict__ Tstart,
                                  const float* __restrict__ maxx2, RunOut o, int64_t b_lo, int64_t b_hi,
@@ -290,12 +305,17 @@ __global__ void ddlms_run_kernel(SolveArgs a, Slicer sl, const float* __restrict
                 mg = fminf(mg, fabsf(ay - sl.thr));
                 const float er = tm * (dr - yr), ei = tm * (di - yi);
                 const float fr = tm * (dr - qr), fi = tm * (di - qi);
+                if (a.lin) {
+                    lin_update(T, X, 0.5f * er, 0.5f * ei);
+                    lin_update(Q, X, 0.5f * fr, 0.5f * fi);
+                } else {
 #pragma unroll
-                for (int j = 0; j < 8; ++j) {
-                    T[j] = fmaf(er, X[j], T[j]);
-                    T[8 + j] = fmaf(ei, X[j], T[8 + j]);
-                    Q[j] = fmaf(fr, X[j], Q[j]);
-                    Q[8 + j] = fmaf(fi, X[j], Q[8 + j]);
+                    for (int j = 0; j < 8; ++j) {
+                        T[j] = fmaf(er, X[j], T[j]);
+                        T[8 + j] = fmaf(ei, X[j], T[8 + j]);
+                        Q[j] = fmaf(fr, X[j], Q[j]);
+                        Q[8 + j] = fmaf(fi, X[j], Q[8 + j]);
+                    }
                 }
                 const uint8_t old = o.labels[k];
                 if (old != static_cast<uint8_t>(lab)) { o.labels[k] = static_cast<uint8_t>(lab); ++changed; }
@@ -476,12 +496,12 @@ __global__ void guard_scan_kernel(ReadBack* rb, const int2* __restrict__ grun, c
             }
         }
         const int2 g = grun[b];
-        const int pre = g.x & 0xffff, first = g.y & 0xffff;
+        const int pre = g.x & 0xffff, first1 = g.y & 0xffff;   // first in-block run + 1 (0: none)
         const int64_t k0 = b * B;
         if (over[b]) {
             long long cand = LLONG_MAX;
             if (c + pre >= guard_run) cand = k0 + (guard_run - c - 1);
-            else if (first != 0xffff) cand = k0 + first;
+            else if (first1 != 0) cand = k0 + first1 - 1;
             if (cand != LLONG_MAX) atomicMin(&rb->freeze_k, cand);
         }
         if (last)
@@ -538,9 +558,13 @@ __global__ void freeze_chain_kernel(SolveArgs a, Slicer sl, const float* __restr
         soft[k] = make_float2(yr, yi);
         if (k == ks) break;                        // frozen: no update from here on
         const float er = tm * (dr - yr), ei = tm * (di - yi);
-        for (int j = 0; j < 8; ++j) {
-            T[j] = fmaf(er, X[j], T[j]);
-            T[8 + j] = fmaf(ei, X[j], T[8 + j]);
+        if (a.lin) {
+            lin_update(T, X, 0.5f * er, 0.5f * ei);
+        } else {
+            for (int j = 0; j < 8; ++j) {
+                T[j] = fmaf(er, X[j], T[j]);
+                T[8 + j] = fmaf(ei, X[j], T[8 + j]);
+            }
         }
     }
     for (int i = 0; i < 16; ++i) rb->Tfz[i] = T[i];
@@ -597,13 +621,13 @@ __global__ void frame_end2_kernel(ReadBack* rb) {
 __global__ void seq_fallback_kernel(const float2* __restrict__ x, int64_t nsym, float scale,
                                     const float2* __restrict__ train, int64_t n_train, const float* __restrict__ Tinit,
                                     float* __restrict__ T_io, int* __restrict__ state_io, Slicer sl, float mu,
-                                    int guard_run, uint8_t* __restrict__ labels, float2* __restrict__ soft,
+                                    int guard_run, int wl, uint8_t* __restrict__ labels, float2* __restrict__ soft,
                                     const ReadBack* rb) {
     if (threadIdx.x != 0 || blockIdx.x != 0 || rb->ctl[3] != 1) return;
     float2 w[16], g[16];
     wg_from_T(Tinit, 1.0f / scale, w, g);
     int frozen = state_io ? state_io[0] : 0, div = state_io ? state_io[1] : 0;
-    seq_chain(x, nsym, scale, 4, train, n_train, w, g, frozen, div, sl, mu, 1, guard_run, labels, soft, nullptr);
+    seq_chain(x, nsym, scale, 4, train, n_train, w, g, frozen, div, sl, mu, wl, guard_run, labels, soft, nullptr);
     T_from_wg(w, g, T_io);
     if (state_io) {
         state_io[0] = frozen;
@@ -824,7 +848,12 @@ __device__ __forceinline__ void tie_rule(int i, float vr, float vi, float m1f, i
     }
 }
 
-template <bool WITH_P, int SQ, bool AL16, bool TRAIN>
+// LIN: the linear (not widely-linear) equaliser, rx:491-497 with g == 0.
+// In the real 2x8 form T1 = T0 M (M = blockdiag [[0,1],[-1,0]]) stays true;
+// the update is T0 += mu (e_r X + e_i JX) with JX = (x1, -x0) per tap (the
+// real embedding of w += mu conj(e) x), i.e. the affine map
+// A = I - mu (X X^T + JX JX^T), which commutes with M -- the same 2x8 scan.
+template <bool WITH_P, int SQ, bool AL16, bool TRAIN, bool LIN>
 __global__ void __launch_bounds__(kBlockThreads, WITH_P ? KK_DD_MINB_P : KK_DD_MINB)
 ddlms_block_kernel(SolveArgs a, Slicer sl, const float* __restrict__ Tstart, float* __restrict__ Pb,
                    float* __restrict__ maxx2, RunOut o, TOut to, int64_t b_lo, int64_t b_hi, int use_skip,
@@ -966,6 +995,7 @@ ddlms_block_kernel(SolveArgs a, Slicer sl, const float* __restrict__ Tstart, flo
     int g_pre = 0, g_run = 0, g_first = 0xffff;
     bool g_lead = true;
     float gmt = 3.0e38f;
+    (void)g_pre;
     if constexpr (!WITH_P) {
         if (run) {
             const uint2 t = o.ties[b];
@@ -1089,7 +1119,7 @@ ddlms_block_kernel(SolveArgs a, Slicer sl, const float* __restrict__ Tstart, flo
             {
                 const float d2 = fmaf(yr, yr, yi * yi);
                 my2 = live ? fmaxf(my2, d2) : my2;
-                if constexpr (!WITH_P) {
+                {   // every pass (the P pass too: a block not re-run later keeps these)
                     gmt = live ? fminf(gmt, fabsf(d2 - thr2)) : gmt;
                     if (live) {
                         if (d2 > thr2) {
@@ -1111,23 +1141,65 @@ ddlms_block_kernel(SolveArgs a, Slicer sl, const float* __restrict__ Tstart, flo
 #pragma unroll
                 for (int jj = 0; jj < 8; ++jj) n2 = fmaf(X[jj], X[jj], n2);
                 mx = fmaxf(mx, n2);     // rows past nk are zero-filled
-                float v[8];
+                if constexpr (LIN) {
+                    // P <- P - mu (P X) X^T - mu (P JX) JX^T
+                    float JX[8];
 #pragma unroll
-                for (int r = 0; r < 8; ++r) {
-                    float sacc = 0.f;
+                    for (int u = 0; u < 4; ++u) {
+                        JX[2 * u] = X[2 * u + 1];
+                        JX[2 * u + 1] = -X[2 * u];
+                    }
+                    float v[8], w[8];
 #pragma unroll
-                    for (int jj = 0; jj < 8; ++jj) sacc = fmaf(P[r * 8 + jj], X[jj], sacc);
-                    v[r] = live ? sacc * tm : 0.f;
+                    for (int r = 0; r < 8; ++r) {
+                        float sa = 0.f, sb = 0.f;
+#pragma unroll
+                        for (int jj = 0; jj < 8; ++jj) {
+                            sa = fmaf(P[r * 8 + jj], X[jj], sa);
+                            sb = fmaf(P[r * 8 + jj], JX[jj], sb);
+                        }
+                        v[r] = live ? sa * (0.5f * tm) : 0.f;
+                        w[r] = live ? sb * (0.5f * tm) : 0.f;
+                    }
+#pragma unroll
+                    for (int r = 0; r < 8; ++r)
+#pragma unroll
+                        for (int jj = 0; jj < 8; ++jj)
+                            P[r * 8 + jj] = fmaf(-w[r], JX[jj], fmaf(-v[r], X[jj], P[r * 8 + jj]));
+                } else {
+                    float v[8];
+#pragma unroll
+                    for (int r = 0; r < 8; ++r) {
+                        float sacc = 0.f;
+#pragma unroll
+                        for (int jj = 0; jj < 8; ++jj) sacc = fmaf(P[r * 8 + jj], X[jj], sacc);
+                        v[r] = live ? sacc * tm : 0.f;
+                    }
+#pragma unroll
+                    for (int r = 0; r < 8; ++r)
+#pragma unroll
+                        for (int jj = 0; jj < 8; ++jj) P[r * 8 + jj] = fmaf(-v[r], X[jj], P[r * 8 + jj]);
                 }
-#pragma unroll
-                for (int r = 0; r < 8; ++r)
-#pragma unroll
-                    for (int jj = 0; jj < 8; ++jj) P[r * 8 + jj] = fmaf(-v[r], X[jj], P[r * 8 + jj]);
             }
+            if constexpr (LIN) {
+                // T0 += mu (e_r X + e_i JX), T1 = T0 M
+                const float el = 0.5f * er, fl = 0.5f * ei;
 #pragma unroll
-            for (int jj = 0; jj < 8; ++jj) {
-                T[jj] = fmaf(er, X[jj], T[jj]);
-                T[8 + jj] = fmaf(ei, X[jj], T[8 + jj]);
+                for (int u = 0; u < 4; ++u) {
+                    const float x0 = X[2 * u], x1 = X[2 * u + 1];
+                    const float d0 = fmaf(el, x0, fl * x1);
+                    const float d1 = fmaf(el, x1, -fl * x0);
+                    T[2 * u] += d0;
+                    T[2 * u + 1] += d1;
+                    T[8 + 2 * u] -= d1;
+                    T[9 + 2 * u] += d0;
+                }
+            } else {
+#pragma unroll
+                for (int jj = 0; jj < 8; ++jj) {
+                    T[jj] = fmaf(er, X[jj], T[jj]);
+                    T[8 + jj] = fmaf(ei, X[jj], T[8 + jj]);
+                }
             }
             hsh = live ? (hsh ^ static_cast<unsigned long long>(lab & 0xff)) * 1099511628211ull : hsh;
             soft8[j] = make_float2(yr, yi);
@@ -1187,14 +1259,16 @@ ddlms_block_kernel(SolveArgs a, Slicer sl, const float* __restrict__ Tstart, flo
         const float mg = sq ? fminf(mgl, 0.5f * 3.0e38f) * (2.0f / sl.norm) : mgb;
         // guard certificate: every symbol's side of the threshold, not only
         // the block maximum's (| |y| - thr | >= | |y|^2 - thr^2 | / (2 max(|y|, thr)))
-        const float gm = WITH_P ? fabsf(sl.thr - sqrtf(my2)) : gmt / (2.0f * sqrtf(fmaxf(my2, thr2)));
+        const float gm = gmt / (2.0f * sqrtf(fmaxf(my2, thr2)));
         o.margin[b] = fminf(mg, gm);
         o.over[b] = my2 > thr2 ? 1 : 0;
-        if constexpr (!WITH_P) {
+        {
+            // first in-block run stored +1 (0: none), so a zeroed table means "no runs"
             const int full = g_lead ? 1 : 0;
             const int pre = g_lead ? g_run : g_pre;
-            o.grun[b] = make_int2((pre & 0xffff) | ((g_run & 0xffff) << 16), (g_first & 0xffff) | (full << 16));
-            if (my2 > thr2) atomicMax(o.counters + 2, 1ull);   // "an exceedance was seen": guard checks from now on
+            o.grun[b] = make_int2((pre & 0xffff) | ((g_run & 0xffff) << 16),
+                                  ((g_first == 0xffff ? 0 : g_first + 1) & 0xffff) | (full << 16));
+            if (!WITH_P && my2 > thr2) atomicMax(o.counters + 2, 1ull);   // an exceedance seen: guard checks from now on
         }
         if (b == a.nb - 1) {
 #pragma unroll
@@ -1890,13 +1964,15 @@ struct DdlmsSolver {
         {
             struct KS { const void* k; size_t smem; };
             const KS ks[] = {
-#define KK_DD_K(P_, S_, T_) {reinterpret_cast<const void*>(ddlms_block_kernel<P_, S_, true, T_>), T_ ? kStageSmem + kTrainSmem : kStageSmem}, \
-                            {reinterpret_cast<const void*>(ddlms_block_kernel<P_, S_, false, T_>), T_ ? kStageSmem + kTrainSmem : kStageSmem}
+#define KK_DD_K1(P_, S_, T_, L_) {reinterpret_cast<const void*>(ddlms_block_kernel<P_, S_, true, T_, L_>), T_ ? kStageSmem + kTrainSmem : kStageSmem}, \
+                            {reinterpret_cast<const void*>(ddlms_block_kernel<P_, S_, false, T_, L_>), T_ ? kStageSmem + kTrainSmem : kStageSmem}
+#define KK_DD_K(P_, S_, T_) KK_DD_K1(P_, S_, T_, false), KK_DD_K1(P_, S_, T_, true)
                 KK_DD_K(true, 0, true), KK_DD_K(true, 2, true), KK_DD_K(true, 4, true), KK_DD_K(true, 8, true),
                 KK_DD_K(false, 0, true), KK_DD_K(false, 2, true), KK_DD_K(false, 4, true), KK_DD_K(false, 8, true),
                 KK_DD_K(true, 0, false), KK_DD_K(true, 2, false), KK_DD_K(true, 4, false), KK_DD_K(true, 8, false),
                 KK_DD_K(false, 0, false), KK_DD_K(false, 2, false), KK_DD_K(false, 4, false), KK_DD_K(false, 8, false)
 #undef KK_DD_K
+#undef KK_DD_K1
             };
             for (const KS& k : ks)
                 if (int rc = ensure_smem_attr(k.k, k.smem, "ddlms_block_kernel smem attribute")) return rc;
@@ -1911,7 +1987,8 @@ struct DdlmsSolver {
                 kern<<<g, kBlockThreads, smem, s>>>(a, sl, lv[0].T, lv[0].P, maxx2, o, to, lo, hi, skip, tol, lst,
                                                     lst_n, write_out, ctl_d);
             };
-#define KK_DD_GO3(P_, S_, T_) (al ? go(ddlms_block_kernel<P_, S_, true, T_>) : go(ddlms_block_kernel<P_, S_, false, T_>))
+#define KK_DD_GO4(P_, S_, T_, L_) (al ? go(ddlms_block_kernel<P_, S_, true, T_, L_>) : go(ddlms_block_kernel<P_, S_, false, T_, L_>))
+#define KK_DD_GO3(P_, S_, T_) (a.lin ? KK_DD_GO4(P_, S_, T_, true) : KK_DD_GO4(P_, S_, T_, false))
 #define KK_DD_GO(P_, S_) (train_blocks ? KK_DD_GO3(P_, S_, true) : KK_DD_GO3(P_, S_, false))
             if (with_p) {
                 if (sq == 2) KK_DD_GO(true, 2);
@@ -1926,6 +2003,7 @@ struct DdlmsSolver {
             }
 #undef KK_DD_GO
 #undef KK_DD_GO3
+#undef KK_DD_GO4
             return check_launch("ddlms_block_kernel");
         };
         if (ext_list) return launch(false, b0, b1, 0, ext_list, ctr + 3);   // device-built list (cascades)
@@ -2013,6 +2091,7 @@ struct DdlmsSolver {
         if (cudaMemsetAsync(over, 0, L.nb * sizeof(int), s) != cudaSuccess ||
             cudaMemsetAsync(hsh, 0, L.nb * 8, s) != cudaSuccess ||
             cudaMemsetAsync(ties, 0, L.nb * sizeof(uint2), s) != cudaSuccess ||
+            cudaMemsetAsync(grun, 0, L.nb * sizeof(int2), s) != cudaSuccess ||
             cudaMemsetAsync(Twritten, 0xFF, L.nb * 16 * sizeof(float), s) != cudaSuccess ||   // NaN: never written
             cudaMemsetAsync(ctr, 0, 4 * sizeof(unsigned long long), s) != cudaSuccess ||
             cudaMemsetAsync(&rb->first_changed, 0xFF, 2 * sizeof(unsigned int), s) != cudaSuccess ||
@@ -2237,7 +2316,7 @@ struct DdlmsSolver {
             static_cast<uint64_t>(a.n_train), f2u(a.mu), f2u(a.scale), static_cast<uint64_t>(a.B),
             static_cast<uint64_t>(a.nb), reinterpret_cast<uint64_t>(ws_base), reinterpret_cast<uint64_t>(to.LT),
             reinterpret_cast<uint64_t>(to.ST), f2u(soft_tol), static_cast<uint64_t>(max_iter),
-            static_cast<uint64_t>(ntb), static_cast<uint64_t>(bt), static_cast<uint64_t>(a.guard_run),
+            static_cast<uint64_t>(ntb), static_cast<uint64_t>(bt), static_cast<uint64_t>(a.guard_run), static_cast<uint64_t>(a.lin),
             static_cast<uint64_t>(sl.kind), static_cast<uint64_t>(sl.npts), static_cast<uint64_t>(sl.m),
             f2u(sl.norm), f2u(sl.thr), static_cast<uint64_t>(sl.sep), f2u(sl.lev_h)};
         for (int i = 0; i < 64; ++i) k.push_back(f2u(sl.pts[i].x) << 32 | f2u(sl.pts[i].y));
@@ -2319,8 +2398,9 @@ struct DdlmsSolver {
     }
 
     int solve_async(float* T_io, int* state_io, int max_iter, int guard_run, float mu_raw, int64_t* stats_out,
-                    uint8_t* labels, float2* soft, bool use_graph) {
+                    uint8_t* labels, float2* soft, bool use_graph, bool widely_linear) {
         a.guard_run = guard_run;
+        a.lin = widely_linear ? 0 : 1;
         ctl_d = rb->ctl;
         if (cudaMemsetAsync(rb, 0, sizeof(ReadBack), s) != cudaSuccess ||
             cudaMemsetAsync(&rb->first_changed, 0xFF, 2 * sizeof(unsigned int), s) != cudaSuccess)
@@ -2411,7 +2491,7 @@ struct DdlmsSolver {
         }
         // mode 1: the exact sequential chain over the frame
         seq_fallback_kernel<<<1, 1, 0, s>>>(a.x, a.nsym, scale, a.train, a.n_train, Tinit_d, T_io, state_io, sl,
-                                            mu_raw, guard_run, to.LT, to.ST, rb);
+                                            mu_raw, guard_run, a.lin ? 0 : 1, to.LT, to.ST, rb);
         if (int rc = check_launch("seq_fallback_kernel")) return rc;
         // mode 4: the freezing block's chain; modes 3 / 4: frozen-tap map
         freeze_chain_kernel<<<1, 1, 0, s>>>(a, sl, lv[0].T, rb, to.LT, to.ST);
@@ -2638,9 +2718,9 @@ extern "C" int kk_ddlms_solve(const void* x, int64_t nsym, float scale, const vo
 extern "C" int kk_ddlms_solve_async(const void* x, int64_t nsym, float scale, const void* train, int64_t n_train,
                                     float* T_io, int* state_io, int order, const float* pts_host,
                                     const uint8_t* grid_host, int grid_m, float norm, float max_radius,
-                                    float guard_factor, int guard_run, float mu, int block, int max_iter,
-                                    float soft_tol, uint8_t* labels, void* soft, void* workspace, size_t ws_bytes,
-                                    int64_t* stats_out, void* stream) {
+                                    float guard_factor, int guard_run, float mu, int widely_linear, int block,
+                                    int max_iter, float soft_tol, uint8_t* labels, void* soft, void* workspace,
+                                    size_t ws_bytes, int64_t* stats_out, void* stream) {
     clear_error();
     if (nsym <= 0) return KK_OK;
     if (!T_io) return set_error(KK_ERR_PARAM, "T_io missing");
@@ -2653,7 +2733,7 @@ extern "C" int kk_ddlms_solve_async(const void* x, int64_t nsym, float scale, co
     sv.bind_outputs(labels, static_cast<float2*>(soft));
     const bool use_graph = max_iter > 0;
     return sv.solve_async(T_io, state_io, max_iter > 0 ? max_iter : -max_iter, guard_run, mu, stats_out, labels,
-                          static_cast<float2*>(soft), use_graph);
+                          static_cast<float2*>(soft), use_graph, widely_linear != 0);
 }
 
 // enqueue the sync kernels; the 4 result doubles land in `res` (device or

@@ -831,7 +831,8 @@ class RxPipeline:
         # div_count} for the block-parallel solver; otherwise the complex
         # taps (w, g) + {frozen, div_count} of the sequential chain.
         st0 = EqualizerState.initial(cfg.ddlms.n_taps)
-        self._solver_form = bool(cfg.ddlms.widely_linear) and cfg.ddlms.n_taps == 4
+        # (the linear equaliser too: T keeps the form T1 = T0 M)
+        self._solver_form = cfg.ddlms.n_taps == 4
         if self._solver_form:
             self._T_dev = _upload(_T_from_wg(st0.w, st0.g), self.dev)
         else:
@@ -1080,7 +1081,7 @@ class RxPipeline:
             _lib.call("kk_ddlms_solve_async", x_ptr, nsym, float(self._eq_scale), train_ptr, n_train,
                       _ptr(self._T_dev), _ptr(self._state_dev), tb.order, tb.pts_ri.ctypes.data,
                       tb.grid.ctypes.data if tb.grid_m else None, tb.grid_m, tb.norm, tb.max_radius,
-                      float(d.divergence_factor), int(d.divergence_run), float(d.mu), B,
+                      float(d.divergence_factor), int(d.divergence_run), float(d.mu), int(bool(d.widely_linear)), B,
                       # worker-thread frames (streaming receive): host-driven loop, no graph
                       # (KK_DDLMS_GRAPH=0 forces it: profilers that replay graph nodes)
                       -int(self.gpu.ddlms_max_iter) if (self._async or not _DDLMS_GRAPH)

@@ -310,6 +310,29 @@ def _burst_stream(factor=100.0, start=150_000, length=600):
     return cap, x
 
 
+@pytest.mark.parametrize("name", ["c1_qpsk_b2b", "c2_16qam_5600km_rel-20", "c3_64qam_1600km_rel-20"])
+def test_pipeline_linear_equalizer_vs_oracle(name):
+    """widely_linear=False (rx:71-78; the linear LMS of rx:491-497) through
+    the block-parallel solver (affine maps I - mu (X X^T + JX JX^T)): same
+    decisions as the oracle's sequential linear recurrence, and as the
+    sequential kernel from the same start."""
+    import dataclasses
+
+    cap = load_capture(name)
+    cfg = cap.pipeline_config(ddlms_frame_symbols=1 << 15, ddlms_block=128)
+    cfg = dataclasses.replace(cfg, ddlms=dataclasses.replace(cfg.ddlms, widely_linear=False))
+    pipe = rxdsp.RxPipeline(cfg, reference_symbols=cap.symbols())
+    pipe.feed(AdcCodes(cap.adc_h, cap.half_lsb))
+    dec, _ = pipe.finish()
+    assert all(s["mode"] == "solve" for s in pipe.ddlms_stats), pipe.ddlms_stats
+    ocfg = ko.OracleConfig(taps=cap.taps, order=cap.order, mu=cap.meta["mu"],
+                           startup_symbols=cap.meta["startup_symbols"], widely_linear=False)
+    _, d_ref, _ = ko.receive(cap.adc_float(), ocfg, cap.symbols(), cap.meta["buffer_len"])
+    assert len(dec) == len(d_ref)
+    agree = float(np.mean(to_idx(dec, cap.order) == to_idx(d_ref, cap.order)))
+    assert agree >= DEC_AGREE, agree
+
+
 def test_pipeline_guard_exceedances_without_freeze_exact():
     """Exceedance runs shorter than guard_run do not freeze the taps: the
     block-parallel fixpoint stays exact (no fallback) -- same decisions as
