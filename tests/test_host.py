@@ -255,3 +255,25 @@ def test_pack12_round_trip_and_layout():
         pack12(np.array([1, 2], np.int16))          # even code: not a mid-rise level
     with pytest.raises(ParameterError):
         AdcPacked12(p[:3], 1.0, 3)                  # odd sample count
+
+
+def test_bench_refuses_more_gpus_than_visible():
+    """bench.py --gpus N without torchrun self-launches N ranks, but refuses
+    (exit 2, message) when fewer than N GPUs are visible; a WORLD_SIZE that
+    differs from --gpus is refused too (no line may claim a GPU count it did
+    not run on)."""
+    import os
+    import subprocess
+    import sys
+
+    repo = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
+    env["CUDA_VISIBLE_DEVICES"] = ""
+    r = subprocess.run([sys.executable, os.path.join(repo, "bench.py"), "--gpus", "2", "--steps", "1"],
+                       capture_output=True, text=True, env=env, timeout=300)
+    assert r.returncode == 2, (r.returncode, r.stderr[-500:])
+    assert "--gpus 2 requested" in r.stderr
+    env["WORLD_SIZE"] = "1"
+    r = subprocess.run([sys.executable, os.path.join(repo, "bench.py"), "--gpus", "2", "--steps", "1"],
+                       capture_output=True, text=True, env=env, timeout=300)
+    assert r.returncode == 2 and "WORLD_SIZE=1" in r.stderr
