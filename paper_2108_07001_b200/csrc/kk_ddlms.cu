@@ -794,14 +794,8 @@ __device__ __forceinline__ int stage_idx(int chunk, int row, int col) {
     return (chunk * kChunkRows + row) * 32 + (col ^ ((row * 4) & 31));
 }
 
-// normalised slicer units (level spacing 1): distance from v to the nearest
-// decision boundary of level f's cell (edge levels are open outwards) ...
-__device__ __forceinline__ float axis_margin(float v, float f, float m1f) {
-    const float up = f < m1f ? 0.5f - (v - f) : 3.0e38f;
-    const float dn = f > 0.f ? 0.5f + (v - f) : 3.0e38f;
-    return fminf(up, dn);
-}
-// ... and how far v lies outside level s's cell (negative inside)
+// normalised slicer units (level spacing 1): how far v lies outside level
+// s's cell (negative inside; edge levels are open outwards)
 __device__ __forceinline__ float cell_excess(float v, float s, float m1f) {
     const float up = s < m1f ? v - s : -3.0e38f;
     const float dn = s > 0.f ? s - v : -3.0e38f;
@@ -990,12 +984,11 @@ ddlms_block_kernel(SolveArgs a, Slicer sl, const float* __restrict__ Tstart, flo
     // 16..23 grid cell (ir * SQ + ii), bits 0..15 symbol within the block
     unsigned tie0 = 0u, tie1 = 0u;
     bool ties_dirty = false;
-    // divergence-guard runs (|y| > thr): leading / current run length and the
-    // first in-block run reaching guard_run; gmt: min | |y|^2 - thr^2 |
-    int g_pre = 0, g_run = 0, g_first = 0xffff;
-    bool g_lead = true;
-    float gmt = 3.0e38f;
-    (void)g_pre;
+    // divergence-guard runs (|y| > thr), tracked only at exceedances (a
+    // warp vote per symbol; the slow path is rare): last exceeding symbol,
+    // current run and its start, the leading run (from symbol 0) and the
+    // first in-block run reaching guard_run
+    int g_prev = -2, g_run = 0, g_start = 0, g_lead = 0, g_first = 0xffff;
     if constexpr (!WITH_P) {
         if (run) {
             const uint2 t = o.ties[b];
@@ -1060,11 +1053,13 @@ ddlms_block_kernel(SolveArgs a, Slicer sl, const float* __restrict__ Tstart, flo
                 constexpr float kMagic = 12582912.0f;
                 const float vr = fmaf(yr, half_norm, off), vi = fmaf(yi, half_norm, off);
                 const float m1f = static_cast<float>(m1);
-                float fr = fminf(fmaxf((vr + kMagic) - kMagic, 0.f), m1f);
-                float fi = fminf(fmaxf((vi + kMagic) - kMagic, 0.f), m1f);
-                // distance to the nearest decision boundary (an edge level has
-                // none on its outer side)
-                float mg_s = fminf(axis_margin(vr, fr, m1f), axis_margin(vi, fi, m1f));
+                // distance to the nearest decision boundary; an edge level has
+                // none on its outer side, so v is clamped to the level range
+                // first (margin 0.5 there: conservative)
+                const float vcr = fminf(fmaxf(vr, 0.f), m1f), vci = fminf(fmaxf(vi, 0.f), m1f);
+                float fr = (vcr + kMagic) - kMagic;
+                float fi = (vci + kMagic) - kMagic;
+                float mg_s = 0.5f - fmaxf(fabsf(vcr - fr), fabsf(vci - fi));
                 if constexpr (!WITH_P) {
                     const bool near = live && !trn && mg_s < kTieEps;
                     if (__any_sync(0xffffffffu, near) && near)
@@ -1090,9 +1085,10 @@ ddlms_block_kernel(SolveArgs a, Slicer sl, const float* __restrict__ Tstart, flo
                 if (sl.kind == 0) {
                     vr = fmaf(yr, half_norm, off);
                     vi = fmaf(yi, half_norm, off);
-                    fr = fminf(fmaxf(rintf(vr), 0.f), m1f);
-                    fi = fminf(fmaxf(rintf(vi), 0.f), m1f);
-                    mg_s = fminf(axis_margin(vr, fr, m1f), axis_margin(vi, fi, m1f));
+                    const float vcr = fminf(fmaxf(vr, 0.f), m1f), vci = fminf(fmaxf(vi, 0.f), m1f);
+                    fr = rintf(vcr);
+                    fi = rintf(vci);
+                    mg_s = 0.5f - fmaxf(fabsf(vcr - fr), fabsf(vci - fi));
                     if constexpr (!WITH_P) {
                         const bool near = live && !trn && mg_s < kTieEps;
                         if (__any_sync(0xffffffffu, near) && near)
@@ -1119,20 +1115,18 @@ ddlms_block_kernel(SolveArgs a, Slicer sl, const float* __restrict__ Tstart, flo
             {
                 const float d2 = fmaf(yr, yr, yi * yi);
                 my2 = live ? fmaxf(my2, d2) : my2;
-                {   // every pass (the P pass too: a block not re-run later keeps these)
-                    gmt = live ? fminf(gmt, fabsf(d2 - thr2)) : gmt;
-                    if (live) {
-                        if (d2 > thr2) {
-                            ++g_run;
-                            if (!g_lead && g_run == a.guard_run && g_first == 0xffff) g_first = i;
-                        } else {
-                            if (g_lead) {
-                                g_pre = g_run;
-                                g_lead = false;
-                            }
-                            g_run = 0;
-                        }
+                // every pass (the P pass too: a block not re-run later keeps these)
+                const bool exc = live && d2 > thr2;
+                if (__any_sync(0xffffffffu, exc) && exc) {
+                    if (g_prev == i - 1) {
+                        ++g_run;
+                    } else {
+                        g_run = 1;
+                        g_start = i;
                     }
+                    g_prev = i;
+                    if (g_start == 0) g_lead = g_run;
+                    else if (g_run == a.guard_run && g_first == 0xffff) g_first = i;
                 }
             }
             const float er = live ? tm * (dr - yr) : 0.f, ei = live ? tm * (di - yi) : 0.f;
@@ -1257,16 +1251,17 @@ ddlms_block_kernel(SolveArgs a, Slicer sl, const float* __restrict__ Tstart, flo
         }
         const bool sq = SQ > 0 || sl.kind == 0;
         const float mg = sq ? fminf(mgl, 0.5f * 3.0e38f) * (2.0f / sl.norm) : mgb;
-        // guard certificate: every symbol's side of the threshold, not only
-        // the block maximum's (| |y| - thr | >= | |y|^2 - thr^2 | / (2 max(|y|, thr)))
-        const float gm = gmt / (2.0f * sqrtf(fmaxf(my2, thr2)));
+        // guard certificate: without exceedances the block maximum is the
+        // closest to the threshold; a block with exceedances gets margin 0
+        // (re-run whenever its start moves: rare, and exact)
+        const float gm = my2 > thr2 ? 0.f : sl.thr - sqrtf(my2);
         o.margin[b] = fminf(mg, gm);
         o.over[b] = my2 > thr2 ? 1 : 0;
         {
             // first in-block run stored +1 (0: none), so a zeroed table means "no runs"
-            const int full = g_lead ? 1 : 0;
-            const int pre = g_lead ? g_run : g_pre;
-            o.grun[b] = make_int2((pre & 0xffff) | ((g_run & 0xffff) << 16),
+            const int full = g_lead >= nk ? 1 : 0;
+            const int suf = g_prev == nk - 1 ? g_run : 0;
+            o.grun[b] = make_int2((g_lead & 0xffff) | ((suf & 0xffff) << 16),
                                   ((g_first == 0xffff ? 0 : g_first + 1) & 0xffff) | (full << 16));
             if (!WITH_P && my2 > thr2) atomicMax(o.counters + 2, 1ull);   // an exceedance seen: guard checks from now on
         }
