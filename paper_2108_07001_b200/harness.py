@@ -199,85 +199,41 @@ def run_single(cfg, output_dir: str | None = None, save_captures: bool = False) 
     return report
 
 
-SWEEP_CSV_FIELDS = ["axis", "value", "distance_km", "status", "ber", "q_db", "evm_pct", "n_bits", "n_errors"]
+def _kkmodem():
+    """The reference package (installed in baseline/_ref by
+    tools/install_reference.py, or importable otherwise)."""
+    import importlib
+    import importlib.util
+    import os
+    import sys
 
-
-def _apply_axis(c: dict, axis: str, value) -> dict:
-    """One sweep point's config (sweep.py:20-38), on the dict layout."""
-    import copy
-
-    out = copy.deepcopy(c)
-    if axis == "cspr_db":
-        out["tx"]["cspr_db"] = float(value)
-    elif axis == "rel_launch_db":
-        out["link"]["rel_launch_db"] = float(value)
-    elif axis == "format":
-        out["tx"]["constellation_order"] = int(value)
-    elif axis == "osnr_db":
-        out["rx"]["osnr_override_db"] = float(value)
-    elif axis == "distance_km":
-        n_spans = int(round(float(value) / out["link"]["span_length_km"]))
-        if n_spans < 1:
-            raise ParameterError("distance shorter than one span")
-        out["link"]["n_spans"] = n_spans
-        out["link"]["monitor_every_n_spans"] = n_spans          # final distance only
-    else:
-        raise ParameterError(f"unknown sweep axis {axis}")
-    return out
-
-
-def sweep_argmax_summary(rows: list) -> list:
-    """Best axis value per distance (highest Q among successful points), sweep.py:86-98."""
-    by_dist: dict = {}
-    for r in rows:
-        if r["status"] == "ok" and r["q_db"] != "":
-            by_dist.setdefault(float(r["distance_km"]), []).append(r)
-    out = []
-    for dist in sorted(by_dist):
-        best = max(by_dist[dist], key=lambda r: float(r["q_db"]))
-        out.append({"distance_km": dist, "best_value": best["value"], "best_q_db": float(best["q_db"])})
-    return out
+    if importlib.util.find_spec("kkmodem") is None:
+        ref = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "baseline", "_ref")
+        if os.path.isdir(os.path.join(ref, "kkmodem")):
+            os.environ.setdefault("NUMBA_CACHE_DIR", "/tmp/kkb200_numba_cache")
+            sys.path.append(ref)
+    try:
+        return importlib.import_module("kkmodem.harness.sweep"), importlib.import_module("kkmodem.harness.config")
+    except ImportError as exc:
+        raise ParameterError("run_sweep drives the reference's own sweep driver: kkmodem must be importable "
+                             "(tools/install_reference.py installs it into baseline/_ref)") from exc
 
 
 def run_sweep(cfg, output_dir: str | None = None) -> dict:
-    """The configured one-axis sweep (sweep.py:41-83): run_single per axis
-    value (each on the GPU), tidy rows, the per-distance argmax summary and
-    the two CSV files; same result keys.  With common_noise_seeds every
-    point reuses the seed, else seed + i.  Failed points are recorded."""
-    import copy
-    import csv
-    import os
-
-    c = copy.deepcopy(cfg.to_dict() if hasattr(cfg, "to_dict") else cfg)
-    sw = c.get("sweep")
-    if not sw:
-        raise ParameterError("config has no sweep section")
-    axis, values = sw["axis"], list(sw["values"])
-    rows, reports = [], []
-    for i, value in enumerate(values):
-        pc = _apply_axis(c, axis, value)
-        pc["sweep"] = None
-        if not c.get("common_noise_seeds", True):
-            pc["seed"] = int(c.get("seed", 0)) + i
-        report = run_single(pc)
-        reports.append(report)
-        for p in report["points"]:
-            rows.append({"axis": axis, "value": value, "distance_km": p["distance_km"], "status": p["status"],
-                         **{k: p.get(k, "") for k in ("ber", "q_db", "evm_pct", "n_bits", "n_errors")}})
-    summary = sweep_argmax_summary(rows)
-    if output_dir:
-        os.makedirs(output_dir, exist_ok=True)
-        with open(os.path.join(output_dir, "sweep.csv"), "w", newline="") as f:
-            w = csv.DictWriter(f, fieldnames=SWEEP_CSV_FIELDS)
-            w.writeheader()
-            for r in rows:
-                w.writerow({k: r.get(k, "") for k in SWEEP_CSV_FIELDS})
-        with open(os.path.join(output_dir, "sweep_optimum.csv"), "w", newline="") as f:
-            w = csv.DictWriter(f, fieldnames=["distance_km", "best_value", "best_q_db"])
-            w.writeheader()
-            for r in summary:
-                w.writerow(r)
-    return {"axis": axis, "values": values, "rows": rows, "summary": summary, "reports": reports}
+    """The reference's own sweep driver (kkmodem.harness.sweep.run_sweep,
+    sweep.py:41-83: axis application, rows, per-distance argmax summary, the
+    two CSV files) with every point's run_single on the GPU (this module's
+    run_single: GPU capture generator + B200 receive + device metrics).
+    `cfg`: the reference's ExperimentConfig or its dict layout."""
+    sweep, config = _kkmodem()
+    ec = cfg if isinstance(cfg, config.ExperimentConfig) else config.ExperimentConfig.from_dict(
+        cfg.to_dict() if hasattr(cfg, "to_dict") else cfg)
+    orig = sweep.run_single
+    sweep.run_single = lambda point_cfg, *a, **k: run_single(point_cfg.to_dict())
+    try:
+        return sweep.run_sweep(ec, output_dir)
+    finally:
+        sweep.run_single = orig
 
 
 def run_sustained(cfg, n_adc_samples: int, osnr_db: float | None = None, chunk_symbols: int = 1 << 16) -> dict:

@@ -141,27 +141,30 @@ def test_bench_throughput_needs_enough_samples():
         bench_throughput(cfg, n_samples=1 << 10)
 
 
-def test_sweep_axis_and_summary():
-    """sweep.py:20-38 axis application and :86-98 argmax summary (host logic
-    of harness.run_sweep); a config without a sweep section raises."""
-    from paper_2108_07001_b200.harness import _apply_axis, run_sweep, sweep_argmax_summary
+def test_run_sweep_drives_the_reference_sweep(tmp_path, monkeypatch):
+    """harness.run_sweep is the reference's own sweep driver (sweep.py:41-83:
+    axis application, rows, argmax summary, CSVs) with run_single swapped for
+    the GPU one -- here a stand-in returning a fixed report per point."""
+    from paper_2108_07001_b200 import harness
 
+    seen = []
+
+    def fake_run_single(c):
+        seen.append(c["tx"]["cspr_db"])
+        q = 10.0 - abs(c["tx"]["cspr_db"] - 10.0)
+        return {"points": [{"distance_km": 1e4, "status": "ok", "ber": 1e-3, "q_db": q, "evm_pct": 5.0,
+                            "n_bits": 100, "n_errors": 1}]}
+
+    monkeypatch.setattr(harness, "run_single", fake_run_single)
     c = load_capture("c4_qpsk_10000km_cspr10").meta["config"]
-    assert _apply_axis(c, "cspr_db", 6)["tx"]["cspr_db"] == 6.0
-    assert _apply_axis(c, "format", 16)["tx"]["constellation_order"] == 16
-    d = _apply_axis(c, "distance_km", 2000)["link"]
-    assert d["n_spans"] == 20 and d["monitor_every_n_spans"] == 20
-    assert c["tx"]["cspr_db"] == 10.0                       # input untouched
-    with pytest.raises(ParameterError):
-        _apply_axis(c, "distance_km", 10)
-    with pytest.raises(ParameterError):
-        _apply_axis(c, "nonsense", 1)
-    rows = [{"status": "ok", "q_db": 9.0, "distance_km": 1e4, "value": 6},
-            {"status": "ok", "q_db": 11.0, "distance_km": 1e4, "value": 10},
-            {"status": "failed", "q_db": "", "distance_km": 1e4, "value": 4}]
-    assert sweep_argmax_summary(rows) == [{"distance_km": 1e4, "best_value": 10, "best_q_db": 11.0}]
-    with pytest.raises(ParameterError):
-        run_sweep(dict(c, sweep=None))
+    c = dict(c, sweep={"axis": "cspr_db", "values": [6.0, 10.0, 14.0]})
+    res = harness.run_sweep(c, output_dir=str(tmp_path))
+    assert seen == [6.0, 10.0, 14.0]
+    assert len(res["rows"]) == 3 and res["summary"][0]["best_value"] == 10.0
+    assert (tmp_path / "sweep.csv").read_text().count("\n") == 4
+    assert (tmp_path / "sweep_optimum.csv").exists()
+    with pytest.raises(ValueError):                    # the reference's ParameterError
+        harness.run_sweep(dict(c, sweep=None))
 
 
 # --- the reference's host-side tap criteria (kkmodem test_rxdsp.py:158-385),
