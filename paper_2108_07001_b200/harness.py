@@ -514,6 +514,11 @@ def pack_labels_host(labels, sym0: int, train_idx, order: int, bits_host) -> int
     return nb
 
 
+# stream priorities of a streaming receive (KK_FRONT_PRIO / KK_DDLMS_PRIO:
+# lower = scheduled first)
+_FRONT_PRIO = int(__import__("os").environ.get("KK_FRONT_PRIO", "0"))
+
+
 def receive_host_stream(cfg, host_codes, half_lsb: float, reference_symbols, chunk_samples: int = 1 << 25,
                         bits_host=None, device=None, staging=None, trace=None, packed12_samples: int | None = None):
     """End-to-end receive of an int16 ADC stream in pinned HOST memory; the
@@ -540,7 +545,7 @@ def receive_host_stream(cfg, host_codes, half_lsb: float, reference_symbols, chu
 
     dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
     caller = torch.cuda.current_stream(dev)
-    comp = side_stream(dev, "front")
+    comp = side_stream(dev, "front", _FRONT_PRIO)
     comp.wait_stream(caller)
     with torch.cuda.stream(comp):
         out = _receive_host_stream(cfg, host_codes, half_lsb, reference_symbols, chunk_samples, bits_host, dev,
@@ -726,7 +731,7 @@ def receive_raw_file(cfg, path: str, reference_symbols, chunk_samples: int = 1 <
     n = int(meta["length"])
     dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
     caller = torch.cuda.current_stream(dev)
-    comp = side_stream(dev, "front")
+    comp = side_stream(dev, "front", _FRONT_PRIO)
     copy = side_stream(dev, "h2d")
     d2h = side_stream(dev, "d2h")
     comp.wait_stream(caller)

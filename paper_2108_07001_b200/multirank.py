@@ -278,6 +278,7 @@ def receive_rank(cfg, adc, reference_prefix, job: SuperframeJob, dist, chunk_sam
     train_total = min(cfg.ddlms.startup_symbols, len(reference_prefix)) if reference_prefix is not None else 0
     n_train = int(max(0, min(nsym, train_total - k0)))
     train_ptr = (pipe._ref_dev.data_ptr() + k0 * 8) if (n_train > 0 and pipe._ref_dev is not None) else 0
+    t_dd0 = pipe._ev()          # the chained DDLMS counts as the "ddlms" stage (rx:652-654)
     solver = GpuFrameSolver(pipe._y2.ptr(drop + 2 * k0), nsym, scale, train_ptr, n_train, cfg, dev)
     st0 = EqualizerState.initial(cfg.ddlms.n_taps)
     T_init = _T_from_wg(st0.w, st0.g)
@@ -306,6 +307,7 @@ def receive_rank(cfg, adc, reference_prefix, job: SuperframeJob, dist, chunk_sam
 
     if guard_chain(comm, guards, T_init, run_sequential):
         mode = "multirank(guard: sequential chain)"
+    pipe._events.append(("ddlms", t_dd0, pipe._ev()))
     pipe.release_buffers()
     stats = [{"k0": k0, "nsym": nsym, "mode": mode, "iterations": iters, "per_iter": per_iter}]
     return SuperframeResult(labels, soft, k0, pipe, stats, offset if job.rank == 0 else None)

@@ -324,6 +324,8 @@ def _as_device_input(x, dev):
 _NVTX = _os.environ.get("KK_NVTX", "0") == "1"
 # the DDLMS fixpoint loop as a CUDA-graph WHILE node (default) or host-driven
 _DDLMS_GRAPH = _os.environ.get("KK_DDLMS_GRAPH", "1") != "0"
+# priority of the asynchronous DDLMS worker stream (lower = scheduled first)
+_DDLMS_PRIO = int(_os.environ.get("KK_DDLMS_PRIO", "-1"))
 
 _SIDE_STREAMS = {}
 import threading as _threading
@@ -1167,7 +1169,7 @@ class RxPipeline:
             self._job_q = queue.Queue()
             # high priority: the frame chain is the critical path at the end
             # of a stream (measured 0.1-0.5 GBaud better end to end)
-            self._worker_stream = side_stream(self.dev, "ddlms", -1)
+            self._worker_stream = side_stream(self.dev, "ddlms", _DDLMS_PRIO)
             self._worker = threading.Thread(target=self._worker_loop, daemon=True)
             self._worker.start()
         # device memory is allocated here, on the host thread's stream (the
