@@ -78,7 +78,7 @@ const float2* twiddle_table_device() {
         return nullptr;
     }
     std::call_once(g_tw_once[dev], [dev]() {
-        std::vector<float2> h(kTwEntries);
+        std::vector<float2> h(kTwEntries + kTwPassEntries);
         const double two_pi = 6.283185307179586476925286766559;
         for (int M = 256; M <= 32768; M *= 2) {
             const int o = tw_offset(M);
@@ -91,9 +91,23 @@ const float2* twiddle_table_device() {
                 h[o + 32 + i] = make_float2(static_cast<float>(std::cos(a)), static_cast<float>(std::sin(a)));
             }
         }
+        // K1's per-pass tables (kk_common.cuh DirectTwiddle), after the two-level ones
+        for (int r = 1; r < 16; ++r)
+            for (int m = 0; m < 16; ++m) {
+                const double a = -two_pi * ((r * m) % 256) / 256.0;
+                h[kTwEntries + kTwPass16 + (r - 1) * 16 + m] =
+                    make_float2(static_cast<float>(std::cos(a)), static_cast<float>(std::sin(a)));
+            }
+        for (int r = 1; r < 4; ++r)
+            for (int m = 0; m < 256; ++m) {
+                const double a = -two_pi * ((r * m) % 1024) / 1024.0;
+                h[kTwEntries + kTwPass4 + (r - 1) * 256 + m] =
+                    make_float2(static_cast<float>(std::cos(a)), static_cast<float>(std::sin(a)));
+            }
         float2* d = nullptr;
-        if (cudaMalloc(&d, kTwEntries * sizeof(float2)) == cudaSuccess &&
-            cudaMemcpy(d, h.data(), kTwEntries * sizeof(float2), cudaMemcpyHostToDevice) == cudaSuccess)
+        const size_t nt = kTwEntries + kTwPassEntries;
+        if (cudaMalloc(&d, nt * sizeof(float2)) == cudaSuccess &&
+            cudaMemcpy(d, h.data(), nt * sizeof(float2), cudaMemcpyHostToDevice) == cudaSuccess)
             g_tw[dev] = d;
     });
     if (!g_tw[dev]) set_error(KK_ERR_CUDA, "twiddle table allocation failed");

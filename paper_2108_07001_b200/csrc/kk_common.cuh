@@ -142,6 +142,30 @@ struct Twiddle {
     }
 };
 
+// Per-pass twiddle tables of K1's 1024-point transforms, appended to the
+// global table after kTwEntries: W_256^{r m} (r = 1..15, m = 0..15) for the
+// radix-16 pass with NS = 16 and W_1024^{r m} (r = 1..3, m = 0..255) for the
+// radix-4 pass with NS = 256 -- one load per twiddle instead of a running
+// product (fewer instructions, correctly rounded twiddles).  Read through the
+// read-only path (L1 resident; K1's shared memory is its occupancy limit).
+constexpr int kTwPass16 = 0;
+constexpr int kTwPass4 = 15 * 16;
+constexpr int kTwPassEntries = kTwPass4 + 3 * 256;
+
+struct DirectTwiddle : Twiddle {
+    const float2* p;     // pass tables (global)
+    static constexpr bool kDirect = true;
+    template <int NS, int R>
+    __device__ __forceinline__ float2 d(int r, int m) const {
+        if constexpr (NS == 16 && R == 16) return __ldg(p + kTwPass16 + (r - 1) * 16 + m);
+        else return __ldg(p + kTwPass4 + (r - 1) * 256 + m);
+    }
+};
+template <class T, class = void>
+struct has_direct { static constexpr bool value = false; };
+template <class T>
+struct has_direct<T, decltype(void(T::kDirect))> { static constexpr bool value = T::kDirect; };
+
 __device__ __forceinline__ void load_twiddles(float2* sm, const float2* __restrict__ g, int tid, int nt) {
     for (int i = tid; i < kTwEntries; i += nt) sm[i] = g[i];
 }
@@ -230,13 +254,14 @@ __device__ __forceinline__ void stockham_load(int tid, const Load& load, float2 
     }
 }
 
-template <int N, int R, int NS, int NT, bool INV, int NBF = PassShape<N, R, NT>::BPT, class Store>
-__device__ __forceinline__ void stockham_compute_store(int tid, const Twiddle& tw, float2 (&v)[NBF][R],
+template <int N, int R, int NS, int NT, bool INV, int NBF = PassShape<N, R, NT>::BPT, class Store, class TW>
+__device__ __forceinline__ void stockham_compute_store(int tid, const TW& tw, float2 (&v)[NBF][R],
                                                        const Store& store) {
     if (PassShape<N, R, NT>::PARTIAL && tid >= PassShape<N, R, NT>::NB) return;
+    constexpr bool kDirect = has_direct<TW>::value && NS > 1 && ((NS == 16 && R == 16) || (NS == 256 && R == 4));
     // when NT is a multiple of NS every butterfly of this thread has the same
     // twiddle index (j % NS == tid % NS): build the chain once, apply to all
-    constexpr bool kShared = (NS > 1) && (NT % NS == 0) && (NBF > 1);
+    constexpr bool kShared = !kDirect && (NS > 1) && (NT % NS == 0) && (NBF > 1);
     if constexpr (kShared) {
         const float2 w1 = tw.template w<NS * R>(tid % NS);
         float2 wr = w1;
@@ -250,7 +275,13 @@ __device__ __forceinline__ void stockham_compute_store(int tid, const Twiddle& t
 #pragma unroll
     for (int q = 0; q < NBF; ++q) {
         const int j = tid + q * NT;
-        if constexpr (NS > 1 && !kShared) {
+        if constexpr (kDirect) {
+#pragma unroll
+            for (int r = 1; r < R; ++r) {
+                const float2 w = tw.template d<NS, R>(r, j % NS);
+                v[q][r] = INV ? cmulc(v[q][r], w) : cmul(v[q][r], w);
+            }
+        } else if constexpr (NS > 1 && !kShared) {
             // w_r = w1^r by a running product (2 live registers; error <= R ulp)
             const float2 w1 = tw.template w<NS * R>(j % NS);
             float2 wr = w1;
@@ -292,8 +323,9 @@ struct GroupBarrier {
     }
 };
 
-template <int N, int R, int NS, int NT, bool INV, bool SYNC_IN, class Load, class Store, class Bar = BlockBarrier>
-__device__ __forceinline__ void stockham_pass(int tid, const Twiddle& tw, const Load& load, const Store& store,
+template <int N, int R, int NS, int NT, bool INV, bool SYNC_IN, class Load, class Store, class Bar = BlockBarrier,
+          class TW = Twiddle>
+__device__ __forceinline__ void stockham_pass(int tid, const TW& tw, const Load& load, const Store& store,
                                               const Bar& bar = Bar{}) {
     if constexpr (SYNC_IN) {
         float2 v[PassShape<N, R, NT>::BPT][R];

@@ -118,8 +118,11 @@ __device__ __forceinline__ void k1_sincos(float x, float* s, float* c) {
     else __sincosf(reduce_2pi(x), s, c);
 }
 
+#ifndef KK_K1_MINB
+#define KK_K1_MINB 4
+#endif
 template <typename TIn, bool PRECISE>
-__global__ void __launch_bounds__(kK1Threads, 4)
+__global__ void __launch_bounds__(kK1Threads, KK_K1_MINB)
 kk_pairs_kernel(const typename InElem<TIn>::T* __restrict__ in, float in_scale, float clamp_rel, int64_t n_hops,
                 const float* __restrict__ st_u, const float* __restrict__ st_a,
                 const uint8_t* __restrict__ st_dead,
@@ -247,7 +250,16 @@ kk_pairs_kernel(const typename InElem<TIn>::T* __restrict__ in, float in_scale, 
     const int64_t pair = int64_t(blockIdx.x) * kPairsPerCta + g;
     const int64_t hop_a = 2 * pair;          // output hop of the real-part block
     const bool active = hop_a < n_hops;
+#ifndef KK_K1_DIRECT_TW
+#define KK_K1_DIRECT_TW 1
+#endif
+#if KK_K1_DIRECT_TW
+    DirectTwiddle tw;
+    tw.t = S.tw;
+    tw.p = tw_g + kTwEntries;
+#else
     const Twiddle tw{S.tw};
+#endif
     SmemPlanes P{S.buf[g]};
     const float* ua = S.u + (2 * g) * kHop;          // block a: stage hops 2g, 2g+1
     const float* ub = S.u + (2 * g + 1) * kHop;      // block b: stage hops 2g+1, 2g+2
