@@ -85,6 +85,35 @@ int kk_reconstruct_pairs(int in_dtype, const void *in, float in_scale, float cla
                          int64_t n0_global, int rot_p, int rot_q, const void *rot_tab,
                          int mirror, void *stream);
 
+/*
+ * Batched K1 (B200 addition): independent streams (sweep
+ * points) in one launch; every job is one kk_reconstruct_pairs call (same
+ * argument meaning), all with the same in_dtype.  The job array is host
+ * memory (copied into the launch).
+ */
+typedef struct {
+    const void *in;
+    float in_scale;
+    float clamp_rel;
+    int64_t n_hops;
+    const float *st_u;
+    const float *st_a;
+    const uint8_t *st_dead;
+    float *new_u;
+    float *new_a;
+    uint8_t *new_dead;
+    void *out;
+    void *hop_sum;
+    uint8_t *hop_dead;
+    unsigned long long *clamped;
+    int64_t n0_global;
+    int rot_p;
+    int rot_q;
+    const void *rot_tab;
+    int mirror;
+} kk_k1_job;
+int kk_reconstruct_pairs_batch(int in_dtype, const kk_k1_job *jobs, int n_jobs, void *stream);
+
 /* packed 12-bit codes (KK_DTYPE_P12 layout, n even) -> int16 odd codes h */
 int kk_unpack12(const uint8_t *in, int64_t n, int16_t *out, void *stream);
 
@@ -108,6 +137,28 @@ int kk_static_blocks(const void *z, int64_t z_index0, int64_t hb0, int64_t n_blo
                      const void *seg_mean, int64_t seg_index0, int seg_len, int carrier, int rot_p,
                      int rot_q, const void *rot_tab, int mirror, const void *h_even, const void *h_odd,
                      void *out, void *stream);
+
+/* Batched K2 (B200 addition): one job per stream, each a
+ * kk_static_blocks call with the same argument meaning; host job array. */
+typedef struct {
+    const void *z;
+    int64_t z_index0;
+    int64_t hb0;
+    int64_t n_blocks;
+    int64_t valid_end;
+    const void *seg_mean;
+    int64_t seg_index0;
+    int seg_len;
+    int carrier;
+    int rot_p;
+    int rot_q;
+    const void *rot_tab;
+    int mirror;
+    const void *h_even;
+    const void *h_odd;
+    void *out;
+} kk_k2_job;
+int kk_static_blocks_batch(const kk_k2_job *jobs, int n_jobs, void *stream);
 
 /*
  * K3 sync -- replaces rxdsp.py:574-601 `symbol_sync` and the eq_scale RMS of

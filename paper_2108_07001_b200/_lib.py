@@ -69,6 +69,24 @@ _SIGS = {
     "kk_pack_bits": ([_P, _I64, _I64, _P, _I64, _I, _P, _I, _P, _P], _I),
 }
 
+class K1Job(ctypes.Structure):
+    """kk_k1_job (include/kkb200.h): one stream's kk_reconstruct_pairs arguments."""
+    _fields_ = [("in_", _P), ("in_scale", _F), ("clamp_rel", _F), ("n_hops", _I64), ("st_u", _P), ("st_a", _P),
+                ("st_dead", _P), ("new_u", _P), ("new_a", _P), ("new_dead", _P), ("out", _P), ("hop_sum", _P),
+                ("hop_dead", _P), ("clamped", _P), ("n0_global", _I64), ("rot_p", _I), ("rot_q", _I),
+                ("rot_tab", _P), ("mirror", _I)]
+
+
+class K2Job(ctypes.Structure):
+    """kk_k2_job (include/kkb200.h): one stream's kk_static_blocks arguments."""
+    _fields_ = [("z", _P), ("z_index0", _I64), ("hb0", _I64), ("n_blocks", _I64), ("valid_end", _I64),
+                ("seg_mean", _P), ("seg_index0", _I64), ("seg_len", _I), ("carrier", _I), ("rot_p", _I),
+                ("rot_q", _I), ("rot_tab", _P), ("mirror", _I), ("h_even", _P), ("h_odd", _P), ("out", _P)]
+
+
+_SIGS["kk_reconstruct_pairs_batch"] = ([_I, ctypes.POINTER(K1Job), _I, _P], _I)
+_SIGS["kk_static_blocks_batch"] = ([ctypes.POINTER(K2Job), _I, _P], _I)
+
 EXPORTED = sorted(_SIGS)
 _lib = None
 

@@ -122,21 +122,21 @@ __device__ __forceinline__ void k1_sincos(float x, float* s, float* c) {
 #define KK_K1_MINB 4
 #endif
 template <typename TIn, bool PRECISE>
-__global__ void __launch_bounds__(kK1Threads, KK_K1_MINB)
-kk_pairs_kernel(const typename InElem<TIn>::T* __restrict__ in, float in_scale, float clamp_rel, int64_t n_hops,
-                const float* __restrict__ st_u, const float* __restrict__ st_a,
-                const uint8_t* __restrict__ st_dead,
-                float* __restrict__ new_u, float* __restrict__ new_a, uint8_t* __restrict__ new_dead,
-                float2* __restrict__ out, float2* __restrict__ hop_sum, uint8_t* __restrict__ hop_dead,
-                unsigned long long* __restrict__ clamped_total,
-                int64_t n0_global, int rot_p, int rot_q, const float2* __restrict__ rot_tab,
-                int mirror, const float2* __restrict__ tw_g)
+__device__ __forceinline__ void
+k1_body(const int bx, const typename InElem<TIn>::T* __restrict__ in, float in_scale, float clamp_rel, int64_t n_hops,
+        const float* __restrict__ st_u, const float* __restrict__ st_a,
+        const uint8_t* __restrict__ st_dead,
+        float* __restrict__ new_u, float* __restrict__ new_a, uint8_t* __restrict__ new_dead,
+        float2* __restrict__ out, float2* __restrict__ hop_sum, uint8_t* __restrict__ hop_dead,
+        unsigned long long* __restrict__ clamped_total,
+        int64_t n0_global, int rot_p, int rot_q, const float2* __restrict__ rot_tab,
+        int mirror, const float2* __restrict__ tw_g)
 {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     K1Smem& S = *reinterpret_cast<K1Smem*>(smem_raw);
     const int tid = threadIdx.x;
     const int warp = tid >> 5, lane = tid & 31;
-    const int64_t hop0 = int64_t(blockIdx.x) * (2 * kPairsPerCta) - 1;   // chunk hop of stage hop 0
+    const int64_t hop0 = int64_t(bx) * (2 * kPairsPerCta) - 1;   // chunk hop of stage hop 0
 
     for (int i = tid; i < kK1TwEntries; i += kK1Threads) S.tw[i] = tw_g[i];
     if (tid == 0) S.clamped = 0;
@@ -247,7 +247,7 @@ kk_pairs_kernel(const typename InElem<TIn>::T* __restrict__ in, float in_scale, 
     // ---- per pair: forward FFT1024 of u_a + j u_b, multiplier, inverse ----
     const int g = tid / kGroupThreads;
     const int gt = tid % kGroupThreads;
-    const int64_t pair = int64_t(blockIdx.x) * kPairsPerCta + g;
+    const int64_t pair = int64_t(bx) * kPairsPerCta + g;
     const int64_t hop_a = 2 * pair;          // output hop of the real-part block
     const bool active = hop_a < n_hops;
 #ifndef KK_K1_DIRECT_TW
@@ -383,6 +383,67 @@ kk_pairs_kernel(const typename InElem<TIn>::T* __restrict__ in, float in_scale, 
 }
 
 template <typename TIn, bool PRECISE>
+__global__ void __launch_bounds__(kK1Threads, KK_K1_MINB)
+kk_pairs_kernel(const typename InElem<TIn>::T* __restrict__ in, float in_scale, float clamp_rel, int64_t n_hops,
+                const float* __restrict__ st_u, const float* __restrict__ st_a,
+                const uint8_t* __restrict__ st_dead,
+                float* __restrict__ new_u, float* __restrict__ new_a, uint8_t* __restrict__ new_dead,
+                float2* __restrict__ out, float2* __restrict__ hop_sum, uint8_t* __restrict__ hop_dead,
+                unsigned long long* __restrict__ clamped_total,
+                int64_t n0_global, int rot_p, int rot_q, const float2* __restrict__ rot_tab,
+                int mirror, const float2* __restrict__ tw_g) {
+    k1_body<TIn, PRECISE>(blockIdx.x, in, in_scale, clamp_rel, n_hops, st_u, st_a, st_dead, new_u, new_a, new_dead, out,
+                          hop_sum, hop_dead, clamped_total, n0_global, rot_p, rot_q, rot_tab, mirror, tw_g);
+}
+
+// Batched K1 (independent streams -- sweep points -- in one launch, SURVEY
+// §8(f)3): blockIdx.y selects the stream's job, CTAs beyond its own grid
+// return at once.
+constexpr int kK1BatchMax = 32;
+struct K1Batch {
+    kk_k1_job job[kK1BatchMax];
+};
+
+template <typename TIn, bool PRECISE>
+__global__ void __launch_bounds__(kK1Threads, KK_K1_MINB)
+kk_pairs_batch_kernel(const __grid_constant__ K1Batch b, const float2* __restrict__ tw_g) {
+    const kk_k1_job& j = b.job[blockIdx.y];
+    const int64_t ctas = ((j.n_hops + 1) / 2 + kPairsPerCta - 1) / kPairsPerCta;
+    if (blockIdx.x >= ctas) return;
+    const int q = j.rot_q;
+    const int64_t n0m = q > 0 ? ((j.n0_global % q) + q) % q : 0;
+    k1_body<TIn, PRECISE>(blockIdx.x, static_cast<const typename InElem<TIn>::T*>(j.in), j.in_scale, j.clamp_rel,
+                          j.n_hops, j.st_u, j.st_a, j.st_dead, j.new_u, j.new_a, j.new_dead,
+                          static_cast<float2*>(j.out), static_cast<float2*>(j.hop_sum), j.hop_dead, j.clamped, n0m,
+                          j.rot_p, q, static_cast<const float2*>(j.rot_tab), j.mirror, tw_g);
+}
+
+template <typename TIn, bool PRECISE>
+static int launch_k1_batch(const kk_k1_job* jobs, int n, cudaStream_t s) {
+    const float2* tw = twiddle_table_device();
+    if (!tw) return KK_ERR_CUDA;
+    const size_t smem = sizeof(K1Smem);
+    if (int rc = ensure_smem_attr(reinterpret_cast<const void*>(kk_pairs_batch_kernel<TIn, PRECISE>), smem,
+                                  "K1 batch smem attr"))
+        return rc;
+    for (int a = 0; a < n; a += kK1BatchMax) {
+        K1Batch b;
+        const int m = std::min(kK1BatchMax, n - a);
+        int64_t gx = 0;
+        for (int i = 0; i < m; ++i) {
+            b.job[i] = jobs[a + i];
+            if (b.job[i].n_hops >= (int64_t(1) << 31)) return set_error(KK_ERR_PARAM, "n_hops must be < 2^31 per job");
+            gx = std::max<int64_t>(gx, ((b.job[i].n_hops + 1) / 2 + kPairsPerCta - 1) / kPairsPerCta);
+        }
+        if (gx == 0) continue;
+        kk_pairs_batch_kernel<TIn, PRECISE><<<dim3(static_cast<unsigned>(gx), static_cast<unsigned>(m)), kK1Threads,
+                                                smem, s>>>(b, tw);
+        if (int rc = check_launch("kk_pairs_batch_kernel")) return rc;
+    }
+    return KK_OK;
+}
+
+template <typename TIn, bool PRECISE>
 static int launch_k1(const void* in, float in_scale, float clamp_rel, int64_t n_hops, const float* st_u, const float* st_a,
                      const uint8_t* st_dead, float* new_u, float* new_a, uint8_t* new_dead, float2* out,
                      float2* hop_sum, uint8_t* hop_dead, unsigned long long* clamped, int64_t n0,
@@ -467,4 +528,30 @@ extern "C" int kk_unpack12(const uint8_t* in, int64_t n, int16_t* out, void* str
     const int64_t blocks = std::min<int64_t>((n + 255) / 256, 148 * 32);
     unpack12_kernel<<<static_cast<unsigned>(blocks), 256, 0, static_cast<cudaStream_t>(stream)>>>(in, n, out);
     return check_launch("unpack12_kernel");
+}
+
+extern "C" int kk_reconstruct_pairs_batch(int in_dtype, const kk_k1_job* jobs, int n_jobs, void* stream) {
+    using namespace kk;
+    clear_error();
+    if (n_jobs <= 0) return KK_OK;
+    if (!jobs) return set_error(KK_ERR_PARAM, "jobs missing");
+    for (int i = 0; i < n_jobs; ++i) {
+        if (jobs[i].n_hops < 0) return set_error(KK_ERR_PARAM, "n_hops must be >= 0");
+        if (jobs[i].rot_q > 0 && !jobs[i].rot_tab) return set_error(KK_ERR_PARAM, "rotation table missing");
+        if ((in_dtype & ~KK_DTYPE_PRECISE) == KK_DTYPE_P12 && (reinterpret_cast<uintptr_t>(jobs[i].in) & 3))
+            return set_error(KK_ERR_PARAM, "packed 12-bit input must be 4-byte aligned");
+    }
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const bool precise = (in_dtype & KK_DTYPE_PRECISE) != 0;
+    switch (in_dtype & ~KK_DTYPE_PRECISE) {
+        case KK_DTYPE_I16: return precise ? launch_k1_batch<int16_t, true>(jobs, n_jobs, s)
+                                          : launch_k1_batch<int16_t, false>(jobs, n_jobs, s);
+        case KK_DTYPE_F32: return precise ? launch_k1_batch<float, true>(jobs, n_jobs, s)
+                                          : launch_k1_batch<float, false>(jobs, n_jobs, s);
+        case KK_DTYPE_F64: return precise ? launch_k1_batch<double, true>(jobs, n_jobs, s)
+                                          : launch_k1_batch<double, false>(jobs, n_jobs, s);
+        case KK_DTYPE_P12: return precise ? launch_k1_batch<P12, true>(jobs, n_jobs, s)
+                                          : launch_k1_batch<P12, false>(jobs, n_jobs, s);
+        default: return set_error(KK_ERR_PARAM, "unsupported input dtype");
+    }
 }

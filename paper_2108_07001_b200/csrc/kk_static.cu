@@ -219,7 +219,8 @@ __device__ __forceinline__ void k2_load_column_ab(const K2Params& p, const Block
 }
 
 template <bool FAST>
-__global__ void __launch_bounds__(kK2Threads, 1) static_blocks_kernel(K2Params p, const float2* __restrict__ tw_g) {
+__device__ __forceinline__ void k2_body(const int bx, const int64_t grid_x, const K2Params& p,
+                                        const float2* __restrict__ tw_g) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     K2Smem& S = *reinterpret_cast<K2Smem*>(smem_raw);
     const int tid = threadIdx.x;
@@ -259,15 +260,15 @@ __global__ void __launch_bounds__(kK2Threads, 1) static_blocks_kernel(K2Params p
 
     const Twiddle tw{S.tw};
     const SmemPlanes P{S.buf};
-    const int64_t hb = p.hb0 + blockIdx.x;
+    const int64_t hb = p.hb0 + bx;
     // L2 prefetch of the input of the block this SM most likely runs next
     // (one CTA per SM, CTAs dispatched in index order -> this block + #SMs):
     // pass 1 of both chains then reads L2 instead of stalling on HBM latency
     // with only 16 warps per SM (measured: 20.8 -> 18.3 ms per 2^30 samples;
     // a persistent-CTA variant with the exact next block was slower)
     if (FAST && tid < 16) {
-        const int64_t nb = static_cast<int64_t>(blockIdx.x) + p.prefetch_ahead;
-        if (nb < gridDim.x) {
+        const int64_t nb = static_cast<int64_t>(bx) + p.prefetch_ahead;
+        if (nb < grid_x) {
             const int64_t g0 = (p.hb0 + nb - 1) * kHopS - p.z_index0;   // first sample of that block
             const char* a0 = reinterpret_cast<const char*>(p.z + g0) + tid * (kNS * 8 / 16);
             const uintptr_t al = reinterpret_cast<uintptr_t>(a0) & ~uintptr_t(15);
@@ -395,7 +396,7 @@ __global__ void __launch_bounds__(kK2Threads, 1) static_blocks_kernel(K2Params p
             };
             warp_fft512<true>(E + warp * kRowI, lane, tw, st_o);
             __syncthreads();
-            float2* out = p.out + int64_t(blockIdx.x) * kNOut;
+            float2* out = p.out + int64_t(bx) * kNOut;
 #pragma unroll 4
             for (int i = tid; i < kNOut; i += kK2Threads) out[i] = S.A[padi(i)];
         }
@@ -406,6 +407,86 @@ __global__ void __launch_bounds__(kK2Threads, 1) static_blocks_kernel(K2Params p
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem_base_sh), "n"(kTmemCols));
 }
 
+template <bool FAST>
+__global__ void __launch_bounds__(kK2Threads, 1) static_blocks_kernel(K2Params p, const float2* __restrict__ tw_g) {
+    k2_body<FAST>(blockIdx.x, gridDim.x, p, tw_g);
+}
+
+// Batched K2 (independent streams in one launch): blockIdx.y
+// selects the job (a contiguous run of blocks of one stream)
+constexpr int kK2BatchMax = 32;
+struct K2Batch {
+    K2Params job[kK2BatchMax];
+    int n_blocks[kK2BatchMax];
+};
+template <bool FAST>
+__global__ void __launch_bounds__(kK2Threads, 1) static_blocks_batch_kernel(const __grid_constant__ K2Batch b,
+                                                                            const float2* __restrict__ tw_g) {
+    const int nb = b.n_blocks[blockIdx.y];
+    if (static_cast<int>(blockIdx.x) >= nb) return;
+    k2_body<FAST>(blockIdx.x, nb, b.job[blockIdx.y], tw_g);
+}
+
+}  // namespace kk
+
+namespace kk {
+// the up-to-three launch ranges of one stream's blocks: the interior ones
+// (inside [0, valid_end), <= 1 carrier boundary) take the FAST
+// specialisation, the stream-edge ones the generic one
+struct K2Range {
+    bool fast;
+    int64_t a, b;
+};
+static int k2_plan(const kk_k2_job& j, K2Params& p, K2Range (&r)[3]) {
+    if (j.carrier && (j.seg_len <= 0 || !j.seg_mean)) return set_error(KK_ERR_PARAM, "carrier means missing");
+    if (j.rot_q > 0 && !j.rot_tab) return set_error(KK_ERR_PARAM, "rotation table missing");
+    if (j.rot_q > kRotMax) return set_error(KK_ERR_PARAM, "rotation denominator must be <= 1024");
+    p.z = static_cast<const float2*>(j.z);
+    p.z_index0 = j.z_index0;
+    p.hb0 = j.hb0;
+    p.valid_end = j.valid_end;
+    p.seg_mean = static_cast<const float2*>(j.seg_mean);
+    p.seg_index0 = j.seg_index0;
+    p.seg_len = j.seg_len;
+    p.carrier = j.carrier;
+    p.rot_p = j.rot_p;
+    p.rot_q = j.rot_q;
+    p.rot_tab = static_cast<const float2*>(j.rot_tab);
+    p.mirror = j.mirror;
+    p.h_even = static_cast<const float2*>(j.h_even);
+    p.h_odd = static_cast<const float2*>(j.h_odd);
+    p.out = static_cast<float2*>(j.out);
+    p.prefetch_ahead = num_sms();
+    const int64_t hb0 = j.hb0, hb1 = j.hb0 + j.n_blocks;
+    int64_t lo = hb0, hi = hb1;
+    if (!j.carrier || (j.seg_len >= kNS && j.seg_len % kHopS == 0)) {
+        lo = std::max<int64_t>(hb0, 1);
+        hi = std::min<int64_t>(hb1, j.valid_end / kHopS);
+        if (hi < lo) { lo = hb0; hi = hb0; }
+    } else {
+        lo = hi = hb0;
+    }
+    r[0] = {false, hb0, lo};
+    r[1] = {true, lo, hi};
+    r[2] = {false, hi, hb1};
+    return KK_OK;
+}
+static K2Params k2_sub(const K2Params& p, int64_t hb0, int64_t a) {
+    K2Params q = p;
+    q.hb0 = a;
+    q.out = p.out + (a - hb0) * kNOut;
+    return q;
+}
+static int k2_attrs() {
+    const size_t smem = sizeof(K2Smem);
+    if (int rc = ensure_smem_attr(reinterpret_cast<const void*>(static_blocks_kernel<true>), smem, "K2 smem attr"))
+        return rc;
+    if (int rc = ensure_smem_attr(reinterpret_cast<const void*>(static_blocks_kernel<false>), smem, "K2 smem attr"))
+        return rc;
+    if (int rc = ensure_smem_attr(reinterpret_cast<const void*>(static_blocks_batch_kernel<true>), smem, "K2 smem attr"))
+        return rc;
+    return ensure_smem_attr(reinterpret_cast<const void*>(static_blocks_batch_kernel<false>), smem, "K2 smem attr");
+}
 }  // namespace kk
 
 extern "C" int kk_static_blocks(const void* z, int64_t z_index0, int64_t hb0, int64_t n_blocks,
@@ -415,59 +496,73 @@ extern "C" int kk_static_blocks(const void* z, int64_t z_index0, int64_t hb0, in
     using namespace kk;
     clear_error();
     if (n_blocks <= 0) return KK_OK;
-    if (carrier && (seg_len <= 0 || !seg_mean)) return set_error(KK_ERR_PARAM, "carrier means missing");
-    if (rot_q > 0 && !rot_tab) return set_error(KK_ERR_PARAM, "rotation table missing");
     const float2* tw = twiddle_table_device();
     if (!tw) return KK_ERR_CUDA;
-    const size_t smem = sizeof(K2Smem);
-    if (int rc = ensure_smem_attr(reinterpret_cast<const void*>(static_blocks_kernel<true>), smem, "K2 smem attr"))
-        return rc;
-    if (int rc = ensure_smem_attr(reinterpret_cast<const void*>(static_blocks_kernel<false>), smem, "K2 smem attr"))
-        return rc;
-    if (rot_q > kRotMax) return set_error(KK_ERR_PARAM, "rotation denominator must be <= 1024");
+    if (int rc = k2_attrs()) return rc;
+    const kk_k2_job j = {z, z_index0, hb0, n_blocks, valid_end, seg_mean, seg_index0, seg_len, carrier, rot_p,
+                         rot_q, rot_tab, mirror, h_even, h_odd, out};
     K2Params p;
-    p.z = static_cast<const float2*>(z);
-    p.z_index0 = z_index0;
-    p.hb0 = hb0;
-    p.valid_end = valid_end;
-    p.seg_mean = static_cast<const float2*>(seg_mean);
-    p.seg_index0 = seg_index0;
-    p.seg_len = seg_len;
-    p.carrier = carrier;
-    p.rot_p = rot_p;
-    p.rot_q = rot_q;
-    p.rot_tab = static_cast<const float2*>(rot_tab);
-    p.mirror = mirror;
-    p.h_even = static_cast<const float2*>(h_even);
-    p.h_odd = static_cast<const float2*>(h_odd);
-    p.out = static_cast<float2*>(out);
-    p.prefetch_ahead = num_sms();
-    // interior blocks (inside [0, valid_end), <= 1 carrier boundary) take the
-    // FAST specialisation; the stream-edge blocks the generic one
+    K2Range r[3];
+    if (int rc = k2_plan(j, p, r)) return rc;
     cudaStream_t s = static_cast<cudaStream_t>(stream);
-    const int64_t hb1 = hb0 + n_blocks;
-    int64_t lo = hb0, hi = hb1;
-    if (!carrier || (seg_len >= kNS && seg_len % kHopS == 0)) {
-        lo = std::max<int64_t>(hb0, 1);
-        hi = std::min<int64_t>(hb1, valid_end / kHopS);
-        if (hi < lo) { lo = hb0; hi = hb0; }
-    } else {
-        lo = hi = hb0;
-    }
-    auto launch = [&](bool fast, int64_t a, int64_t b) -> int {
-        if (b <= a) return KK_OK;
-        K2Params q = p;
-        q.hb0 = a;
-        q.out = p.out + (a - hb0) * kNOut;
-        if (fast)
-            static_blocks_kernel<true><<<static_cast<unsigned>(b - a), kK2Threads, smem, s>>>(q, tw);
+    const size_t smem = sizeof(K2Smem);
+    for (const K2Range& g : r) {
+        if (g.b <= g.a) continue;
+        const K2Params q = k2_sub(p, hb0, g.a);
+        if (g.fast)
+            static_blocks_kernel<true><<<static_cast<unsigned>(g.b - g.a), kK2Threads, smem, s>>>(q, tw);
         else
-            static_blocks_kernel<false><<<static_cast<unsigned>(b - a), kK2Threads, smem, s>>>(q, tw);
-        return check_launch("static_blocks_kernel");
-    };
-    if (int rc = launch(false, hb0, lo)) return rc;
-    if (int rc = launch(true, lo, hi)) return rc;
-    return launch(false, hi, hb1);
+            static_blocks_kernel<false><<<static_cast<unsigned>(g.b - g.a), kK2Threads, smem, s>>>(q, tw);
+        if (int rc = check_launch("static_blocks_kernel")) return rc;
+    }
+    return KK_OK;
+}
+
+extern "C" int kk_static_blocks_batch(const kk_k2_job* jobs, int n_jobs, void* stream) {
+    using namespace kk;
+    clear_error();
+    if (n_jobs <= 0) return KK_OK;
+    if (!jobs) return set_error(KK_ERR_PARAM, "jobs missing");
+    const float2* tw = twiddle_table_device();
+    if (!tw) return KK_ERR_CUDA;
+    if (int rc = k2_attrs()) return rc;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const size_t smem = sizeof(K2Smem);
+    // all jobs' ranges, grouped by specialisation, kK2BatchMax per launch
+    for (int fast = 0; fast < 2; ++fast) {
+        K2Batch b;
+        int m = 0;
+        int64_t gx = 0;
+        auto flush = [&]() -> int {
+            if (m == 0) return KK_OK;
+            if (fast)
+                static_blocks_batch_kernel<true><<<dim3(static_cast<unsigned>(gx), static_cast<unsigned>(m)),
+                                                    kK2Threads, smem, s>>>(b, tw);
+            else
+                static_blocks_batch_kernel<false><<<dim3(static_cast<unsigned>(gx), static_cast<unsigned>(m)),
+                                                     kK2Threads, smem, s>>>(b, tw);
+            m = 0;
+            gx = 0;
+            return check_launch("static_blocks_batch_kernel");
+        };
+        for (int i = 0; i < n_jobs; ++i) {
+            if (jobs[i].n_blocks <= 0) continue;
+            K2Params p;
+            K2Range r[3];
+            if (int rc = k2_plan(jobs[i], p, r)) return rc;
+            for (const K2Range& g : r) {
+                if (g.b <= g.a || g.fast != (fast == 1)) continue;
+                if (g.b - g.a >= (int64_t(1) << 31)) return set_error(KK_ERR_PARAM, "too many blocks per job");
+                b.job[m] = k2_sub(p, jobs[i].hb0, g.a);
+                b.n_blocks[m] = static_cast<int>(g.b - g.a);
+                gx = std::max<int64_t>(gx, g.b - g.a);
+                if (++m == kK2BatchMax)
+                    if (int rc = flush()) return rc;
+            }
+        }
+        if (int rc = flush()) return rc;
+    }
+    return KK_OK;
 }
 
 // ---------------------------------------------------------------------------

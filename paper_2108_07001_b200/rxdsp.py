@@ -63,7 +63,7 @@ from .sigcore import (
 )
 
 __all__ = [
-    "DdlmsConfig", "EqualizerState", "RxPipelineConfig", "GpuOptions", "RxPipeline", "SyncError",
+    "DdlmsConfig", "EqualizerState", "RxPipelineConfig", "GpuOptions", "RxPipeline", "SyncError", "feed_batch",
     "stream_buffers", "kk_reconstruct", "downshift_dc", "compute_static_taps", "static_tap_coverage",
     "design_receive_taps", "refine_static_taps", "static_equalize_and_resample", "ddlms_wl", "demap",
     "symbol_sync",
@@ -324,6 +324,7 @@ def _as_device_input(x, dev):
 _NVTX = _os.environ.get("KK_NVTX", "0") == "1"
 # the DDLMS fixpoint loop as a CUDA-graph WHILE node (default) or host-driven
 _DDLMS_GRAPH = _os.environ.get("KK_DDLMS_GRAPH", "1") != "0"
+_GRAPH_MIN_SYMBOLS = 1 << 22
 # priority of the asynchronous DDLMS worker stream (lower = scheduled first)
 _DDLMS_PRIO = int(_os.environ.get("KK_DDLMS_PRIO", "-1"))
 
@@ -840,6 +841,7 @@ class RxPipeline:
         else:
             self._wg_dev = _upload(np.concatenate([st0.w, st0.g]).astype(np.complex64), self.dev)
         self._state_dev = torch.zeros(2, dtype=torch.int32, device=self.dev)     # {frozen, div_count}
+        self._graph_loop = _DDLMS_GRAPH       # large frames: fixpoint loop as a CUDA graph
         self._ws = None
         self._stats: list[dict] = []
 
@@ -921,22 +923,24 @@ class RxPipeline:
         else:
             self._raw = torch.cat([self._raw, x])
 
-    def _run_kk(self, chunk, n_hops):
-        torch = _torch()
+    def _kk_job(self, chunk, n_hops):
+        """K1 arguments for n_hops hops of `chunk` (outputs reserved); the
+        caller launches (alone or batched) and then calls _kk_commit."""
         hop = self.cfg.kk_plan.hop
         g0 = self._z.end
-        h0 = self._hs.end
         out = self._z.reserve(n_hops * hop)
         hs = self._hs.reserve(n_hops)
         hd = self._hd.reserve(n_hops)
         su, sa, sd = self._kk_state[self._kk_cur]
         nu, na, nd = self._kk_state[1 - self._kk_cur]
-        clamped_before = self._clamped * 1       # (a kernel, not a D2D memcpy)
-        rq = self._rot_q
-        _lib.call("kk_reconstruct_pairs", self._raw_dt, _ptr(chunk), float(self._raw_scale), 1e-12, n_hops,
-                  _ptr(su), _ptr(sa), _ptr(sd), _ptr(nu), _ptr(na), _ptr(nd), _ptr(out), _ptr(hs), _ptr(hd),
-                  _ptr(self._clamped), g0, self._rot_p, rq, _ptr(self._rot_tab), int(bool(self.cfg.mirror)),
-                  _stream(self.dev))
+        self._kk_pending = (self._hs.end, self._clamped * 1)       # (a kernel, not a D2D memcpy)
+        return _lib.K1Job(_ptr(chunk), float(self._raw_scale), 1e-12, n_hops, _ptr(su), _ptr(sa), _ptr(sd),
+                          _ptr(nu), _ptr(na), _ptr(nd), _ptr(out), _ptr(hs), _ptr(hd), _ptr(self._clamped), g0,
+                          self._rot_p, self._rot_q, _ptr(self._rot_tab), int(bool(self.cfg.mirror)))
+
+    def _kk_commit(self, n_hops):
+        hop = self.cfg.kk_plan.hop
+        h0, clamped_before = self._kk_pending
         self._kk_cur = 1 - self._kk_cur
         self._z.commit(n_hops * hop)
         self._hs.commit(n_hops)
@@ -944,6 +948,13 @@ class RxPipeline:
         # diagnostics are materialised lazily (no host sync per feed)
         self._pending_diag.append((self._chunk_index, h0, n_hops, clamped_before, self._clamped * 1,
                                    self._state_dev[0] * 1))
+
+    def _run_kk(self, chunk, n_hops):
+        j = self._kk_job(chunk, n_hops)
+        _lib.call("kk_reconstruct_pairs", self._raw_dt, j.in_, j.in_scale, j.clamp_rel, j.n_hops, j.st_u, j.st_a,
+                  j.st_dead, j.new_u, j.new_a, j.new_dead, j.out, j.hop_sum, j.hop_dead, j.clamped, j.n0_global,
+                  j.rot_p, j.rot_q, j.rot_tab, j.mirror, _stream(self.dev))
+        self._kk_commit(n_hops)
 
     def _run_carrier(self, flush):
         cfg = self.cfg
@@ -967,25 +978,40 @@ class RxPipeline:
             self._hs.keep = n_tot * hps
         self._c_end = z_end if flush else n_full * seg
 
-    def _run_static(self, flush):
+    def _static_job(self, flush):
+        """K2 arguments for the static blocks ready now (outputs reserved), or
+        None; then _static_commit."""
         hop = self.cfg.static_plan.hop
         c_end = self._c_end
         hb_end = -(-c_end // hop) if flush else c_end // hop
         n = hb_end - self._hb_next
         if n <= 0:
-            return
+            return None
         nout = hop // 2
         out = self._y2.reserve(n * nout)
         seg = self.cfg.carrier_segment_len
-        seg0 = self._seg.base
-        _lib.call("kk_static_blocks", _ptr(self._z.buf), self._z.base, self._hb_next, n, c_end,
-                  _ptr(self._seg.buf), seg0, seg, int(bool(self.cfg.carrier_removal)),
-                  self._rot_p, self._rot_q, _ptr(self._rot_tab), int(bool(self.cfg.mirror)),
-                  _ptr(self._h_even), _ptr(self._h_odd), _ptr(out), _stream(self.dev))
-        self._y2.commit(n * nout)
+        self._static_pending = (n, hb_end)
+        return _lib.K2Job(_ptr(self._z.buf), self._z.base, self._hb_next, n, c_end, _ptr(self._seg.buf),
+                          self._seg.base, seg, int(bool(self.cfg.carrier_removal)), self._rot_p, self._rot_q,
+                          _ptr(self._rot_tab), int(bool(self.cfg.mirror)), _ptr(self._h_even), _ptr(self._h_odd),
+                          _ptr(out))
+
+    def _static_commit(self):
+        hop = self.cfg.static_plan.hop
+        n, hb_end = self._static_pending
+        self._y2.commit(n * (hop // 2))
         self._hb_next = hb_end
         self._z.keep = max(0, (self._hb_next - 1) * hop)
-        self._seg.keep = max(0, ((self._hb_next - 1) * hop) // seg)
+        self._seg.keep = max(0, ((self._hb_next - 1) * hop) // self.cfg.carrier_segment_len)
+
+    def _run_static(self, flush):
+        j = self._static_job(flush)
+        if j is None:
+            return
+        _lib.call("kk_static_blocks", j.z, j.z_index0, j.hb0, j.n_blocks, j.valid_end, j.seg_mean, j.seg_index0,
+                  j.seg_len, j.carrier, j.rot_p, j.rot_q, j.rot_tab, j.mirror, j.h_even, j.h_odd, j.out,
+                  _stream(self.dev))
+        self._static_commit()
 
     def _sync_head_len(self) -> int:
         cfg = self.cfg
@@ -1084,10 +1110,14 @@ class RxPipeline:
                       _ptr(self._T_dev), _ptr(self._state_dev), tb.order, tb.pts_ri.ctypes.data,
                       tb.grid.ctypes.data if tb.grid_m else None, tb.grid_m, tb.norm, tb.max_radius,
                       float(d.divergence_factor), int(d.divergence_run), float(d.mu), int(bool(d.widely_linear)), B,
-                      # worker-thread frames (streaming receive): host-driven loop, no graph
+                      # the CUDA-graph loop for large frames only: instantiating one costs
+                      # ~0.6 ms of host time and allocates device memory (which serialises
+                      # concurrent streams); small frames, worker-thread frames (streaming
+                      # receive) and batched sweep points take the host-driven loop
                       # (KK_DDLMS_GRAPH=0 forces it: profilers that replay graph nodes)
-                      -int(self.gpu.ddlms_max_iter) if (self._async or not _DDLMS_GRAPH)
-                      else int(self.gpu.ddlms_max_iter),
+                      int(self.gpu.ddlms_max_iter) if (self._graph_loop and not self._async
+                                                       and nsym >= _GRAPH_MIN_SYMBOLS)
+                      else -int(self.gpu.ddlms_max_iter),
                       float(self.gpu.ddlms_soft_tol), _ptr(labels), _ptr(soft),
                       _ptr(self._ws), wsb, st.data_ptr(), stream.cuda_stream)
             ev = torch.cuda.Event()
@@ -1530,6 +1560,79 @@ class RxPipeline:
         with open(path, "w") as f:
             for rec in self.diagnostics:
                 f.write(json.dumps(rec, sort_keys=True) + "\n")
+
+
+def feed_batch(pipes, chunks, ddlms: bool = True) -> None:
+    """One whole-stream feed (flush) of every pipeline in one set of front-end
+    launches (sweep points): K1 of all streams in one
+    launch, the carrier means per stream, K2 of all streams in one launch
+    per specialisation; then every stream's sync is enqueued before any is
+    resolved, and the DDLMS frames follow (asynchronous).  Same outputs as
+    pipe.feed(chunk, flush=True) on each.  All pipelines on the current
+    stream and device; the chunks share one input format."""
+    torch = _torch()
+    if not pipes:
+        return
+    dev = pipes[0].dev
+    stream = _stream(dev)
+    for p in pipes:
+        if p.dev != dev or p._synced or p._raw is not None and p._raw_len():
+            raise ParameterError("feed_batch: fresh pipelines on one device")
+    inputs = [_as_device_input(c, dev) if _len(c) else (None, None, None) for c in chunks]
+    dts = {dt for _, dt, _ in inputs if dt is not None}
+    if len(dts) > 1:
+        raise ParameterError("feed_batch: all chunks in one input format")
+    hop = pipes[0].cfg.kk_plan.hop
+    jobs, live = [], []
+    for p, c, (x, dt, sc) in zip(pipes, chunks, inputs):
+        p.samples_in += _len(c)
+        if x is not None:
+            p._append_raw(x, dt, sc)
+        n_raw = p._raw_len()
+        if n_raw % hop:
+            p._raw, p._raw_dt = p._unpacked(p._raw, p._raw_dt)
+            p._raw = torch.cat([p._raw, torch.zeros(hop - n_raw % hop, dtype=p._raw.dtype, device=dev)])
+            n_raw = p._raw_len()
+        n_hops = n_raw // hop
+        p._batch_t0 = p._ev()
+        if n_hops:
+            jobs.append(p._kk_job(p._raw_slice(0, n_hops * hop), n_hops))
+            live.append((p, n_hops))
+    dts = {p._raw_dt for p, _ in live}
+    if len(dts) > 1:
+        raise ParameterError("feed_batch: all chunks in one input format")
+    if jobs:
+        arr = (_lib.K1Job * len(jobs))(*jobs)
+        _lib.call("kk_reconstruct_pairs_batch", dts.pop(), arr, len(jobs), stream)
+    for p, n_hops in live:
+        p._kk_commit(n_hops)
+        p._raw = p._raw_slice(n_hops * hop)
+    t1 = pipes[0]._ev()
+    for p in pipes:
+        p._run_carrier(True)
+    t2 = pipes[0]._ev()
+    k2 = []
+    for p in pipes:
+        j = p._static_job(True)
+        if j is not None:
+            k2.append((p, j))
+    if k2:
+        arr = (_lib.K2Job * len(k2))(*[j for _, j in k2])
+        _lib.call("kk_static_blocks_batch", arr, len(k2), stream)
+    for p, _ in k2:
+        p._static_commit()
+    t3 = pipes[0]._ev()
+    for p in pipes:                        # every sync in flight before any is awaited
+        if not p._synced and p._sync_pending is None:
+            p._sync_launch(True)
+    for p in pipes:
+        p._events += [("kk", p._batch_t0, t1), ("carrier", t1, t2), ("static", t2, t3)]
+        p._chunk_index += 1
+        if ddlms:
+            t3p = p._ev()
+            p._run_ddlms(True)
+            p._events.append(("ddlms", t3p, p._ev()))
+            p._flushed = True
 
 
 def _len(x) -> int:

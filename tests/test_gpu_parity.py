@@ -532,13 +532,14 @@ def test_measure_point_device_vs_host_and_reference():
 
 
 def test_receive_batch_equals_single_streams():
-    """a batch of independent sweep points received
-    concurrently gives each stream's single-stream decisions exactly."""
+    """a batch of independent sweep points received through one
+    set of front-end launches (batched K1 / K2) gives each stream's
+    single-stream decisions and soft outputs exactly."""
     from paper_2108_07001_b200.harness import receive_batch
 
-    names = ["c4_qpsk_10000km_cspr4", "c4_qpsk_10000km_cspr8", "c4_qpsk_10000km_cspr12",
-             "c2_16qam_5600km_rel-20"]
-    caps = [load_capture(n) for n in names]
+    from paper_2108_07001_b200.captures import list_captures
+
+    caps = [load_capture(n) for n in list_captures() if not n.endswith("_tile")]   # 11 configs, 3 formats
     res = receive_batch([(c.pipeline_config(), c.adc, c.symbols()) for c in caps])
     for cap, (lab, soft, pipe) in zip(caps, res):
         p1 = rxdsp.RxPipeline(cap.pipeline_config(), reference_symbols=cap.symbols())

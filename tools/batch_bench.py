@@ -13,7 +13,7 @@ from paper_2108_07001_b200 import rxdsp  # noqa: E402
 from paper_2108_07001_b200.captures import list_captures, load_capture  # noqa: E402
 from paper_2108_07001_b200.harness import receive_batch  # noqa: E402
 
-names = [n for n in list_captures() if n.startswith(("c1", "c2", "c3", "c4"))]
+names = [n for n in list_captures() if n.startswith(("c1", "c2", "c3", "c4")) and not n.endswith("_tile")]
 caps = [load_capture(n) for n in names]
 items = [(c.pipeline_config(), c.adc, c.symbols()) for c in caps]
 nsyms = 0
@@ -37,7 +37,7 @@ def bat(conc):
     return sum(x[0].numel() for x in r)
 
 
-for f, lab in ((seq, "sequential"), (lambda: bat(4), "batch x4"), (lambda: bat(12), "batch x12")):
+for f, lab in ((seq, "sequential"), (lambda: bat(None), "batched")):
     f()
     t = time.perf_counter()
     reps = 3
