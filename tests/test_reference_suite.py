@@ -14,10 +14,10 @@ Selected: tests/test_rxdsp.py (every receive-path unit test),
 tests/test_harness.py (contiguity, diagnostics, run_single, sweeps, bench,
 sustained; the CLI tests are excluded: they start `python -m kkmodem...`
 subprocesses without the switch, and the plot test needs matplotlib), the
-acceptance criteria that exercise the receiver (C2
-contiguity, C3 10,000 km CD, C4 KK, C6 widely-linear, C10 sustained 2^26
-samples, C11 bench stability; C5/C7 use demap / run_single too), and this
-repo's switch-behaviour checks (tests/reference_switch/).
+acceptance criteria (C1, C2 contiguity, C3 10,000 km CD, C4
+KK, C5, C6 widely-linear, C7 formats x distances, C9, C10 sustained 2^26
+samples, C11 bench stability; C8 excluded for time), and this repo's
+switch-behaviour checks (tests/reference_switch/).
 """
 
 from __future__ import annotations
@@ -38,8 +38,9 @@ REF_TESTS = os.path.join(REF, "kkmodem_tests")
 CASES = {
     "rxdsp": (["test_rxdsp.py"], None),
     "harness": (["test_harness.py"], "not TestCli"),
-    "acceptance": (["test_acceptance.py"], "criterion_02 or criterion_03 or criterion_04 or criterion_05 "
-                                           "or criterion_06 or criterion_07 or criterion_10 or criterion_11"),
+    # every criterion but C8 (SSFM trade-offs: ~5 min of the reference's CPU channel
+    # model per run; it passes through the switch like C7, whose run_single it shares)
+    "acceptance": (["test_acceptance.py"], "not criterion_08"),
     "switch": ([os.path.join(REPO, "tests", "reference_switch", "test_switch_behaviour.py")], None),
 }
 
