@@ -1224,10 +1224,16 @@ class RxPipeline:
         torch = _torch()
         torch.cuda.set_device(self.dev)
         ws = self._worker_stream
+        failed = None          # a failed frame poisons every later one (their start taps depend on it)
         while True:
             job = self._job_q.get()
             if job is None:
                 return
+            if failed is not None:
+                job["error"] = RuntimeError(f"DDLMS frame at symbol {job['k0']} not solved: an earlier frame "
+                                            f"failed ({failed!r})")
+                job["finished"].set()
+                continue
             try:
                 with torch.cuda.stream(ws):
                     ws.wait_event(job["ready"])
@@ -1242,6 +1248,7 @@ class RxPipeline:
                     job["done"] = e1
             except BaseException as exc:   # re-raised on the host thread by drain_device
                 job["error"] = exc
+                failed = exc
             job["finished"].set()
 
     def _collect_frames(self, block: bool, wait_stream=None, max_frames: int | None = None):

@@ -42,6 +42,9 @@ CASES = {
     # model per run; it passes through the switch like C7, whose run_single it shares)
     "acceptance": (["test_acceptance.py"], "not criterion_08"),
     "switch": ([os.path.join(REPO, "tests", "reference_switch", "test_switch_behaviour.py")], None),
+    # the rest of kkmodem's unit tests, with the switch installed (they exercise
+    # sigcore / txdsp / channel / frontend / metrics: the receiver must not disturb them)
+    "other": (["test_sigcore.py", "test_txdsp.py", "test_channel.py", "test_frontend.py", "test_metrics.py"], None),
 }
 
 
