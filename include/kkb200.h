@@ -286,6 +286,44 @@ int kk_demap(const void *symbols, int64_t n, int order, const float *pts_host, u
 int kk_pack_bits(const uint8_t *labels, int64_t n, int64_t sym0, const uint8_t *train_idx, int64_t n_train,
                  int bits_per_symbol, const uint8_t *point_label_host, int order, uint8_t *out, void *stream);
 
+/*
+ * frame_sync's bipolar cross-correlation (metrics.py frame_sync :69-112)
+ * over all lags, on the device: rx / tx are 0/1 bytes.  Linear (circular=0):
+ * c = conv(2rx-1, reverse(2tx-1)) of length n_rx + n_tx - 1 (scipy
+ * fftconvolve "full" indexing); circular (circular=1, n_rx == n_tx): c[k] =
+ * sum_i (2rx[i+k mod n]-1)(2tx[i]-1).  Evaluated with float64 FFTs rounded
+ * to the exact integers.  out3 (device, int64[3]) = {k = first index of
+ * max |c|, |c[k]|, max |c| outside [k-2, k+2] (linear) / outside k
+ * (circular)}; the caller forms the peak ratio and the alignment as the
+ * reference does.  ws: kk_bit_xcorr_workspace_bytes() bytes of device
+ * memory (32 B per FFT point plus tables; 0 = unsupported size).
+ */
+size_t kk_bit_xcorr_workspace_bytes(int64_t n_rx, int64_t n_tx, int circular);
+int kk_bit_xcorr(const uint8_t *rx, int64_t n_rx, const uint8_t *tx, int64_t n_tx, int circular, void *ws,
+                 size_t ws_bytes, long long *out3, void *stream);
+
+/*
+ * Decided labels -> one byte per bit (rxdsp.py demap :548-567 bit order,
+ * MSB first): out[i*k + b] = (point_label[labels[i]] >> (k-1-b)) & 1.
+ */
+int kk_label_bits(const uint8_t *labels, int64_t n, const uint8_t *point_label_host, int order,
+                  int bits_per_symbol, uint8_t *out, void *stream);
+
+/*
+ * Bit errors of two aligned bit streams (runner.py measure_point :104-137):
+ * total += count(a[i] != b[i]); win_counts[w] += the errors of bits
+ * [w*bpw, (w+1)*bpw) for the n / bpw whole windows (metrics.py windowed_q
+ * :130-150; win_counts may be NULL).  Counters are accumulated, not reset.
+ */
+int kk_bit_error_windows(const uint8_t *a, const uint8_t *b, int64_t n, int64_t bits_per_window,
+                         unsigned long long *total, unsigned long long *win_counts, void *stream);
+
+/*
+ * EVM sums (metrics.py evm :169-179): sums[0] += sum |soft - ref|^2,
+ * sums[1] += sum |ref|^2 in float64; soft complex64, ref complex128.
+ */
+int kk_evm_sums(const void *soft, const void *ref, int64_t n, double *sums, void *stream);
+
 #ifdef __cplusplus
 }
 #endif

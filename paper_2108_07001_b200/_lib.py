@@ -67,6 +67,11 @@ _SIGS = {
     "kk_bit_errors": ([_P, _P, _I64, _P, _I64, _P, _P, _I64, _I64, _I64, _P, _P], _I),
     "kk_demap": ([_P, _I64, _I, _P, _P, _P, _P], _I),
     "kk_pack_bits": ([_P, _I64, _I64, _P, _I64, _I, _P, _I, _P, _P], _I),
+    "kk_bit_xcorr_workspace_bytes": ([_I64, _I64, _I], _SZ),
+    "kk_bit_xcorr": ([_P, _I64, _P, _I64, _I, _P, _SZ, _P, _P], _I),
+    "kk_label_bits": ([_P, _I64, _P, _I, _I, _P, _P], _I),
+    "kk_bit_error_windows": ([_P, _P, _I64, _I64, _P, _P, _P], _I),
+    "kk_evm_sums": ([_P, _P, _I64, _P, _P], _I),
 }
 
 class K1Job(ctypes.Structure):

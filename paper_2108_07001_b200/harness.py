@@ -377,10 +377,11 @@ def receive_batch(items, device=None, max_concurrency: int | None = None):
 
 def frame_sync_device(rx_bits, tx_bits, min_peak_ratio: float = 3.0):
     """GPU frame_sync (metrics.py:69-112 semantics): bipolar cross-correlation
-    of the received and transmitted bit streams (uint8 CUDA tensors) with the
-    FFT on the device (cuFFT, float64), peak-to-sidelobe test excluding +-2
-    lags, linear correlation -- or circular when the lengths are equal.
-    Returns (lag, aligned rx bits, aligned tx bits) as device views."""
+    of the received and transmitted bit streams (uint8 CUDA tensors) over all
+    lags by kk_bit_xcorr (the repo's float64 Stockham FFT, rounded to the
+    exact integer correlation), peak-to-sidelobe test excluding +-2 lags,
+    linear correlation -- or circular when the lengths are equal.  Returns
+    (lag, aligned rx bits, aligned tx bits) as device views."""
     import torch
 
     n_rx, n_tx = int(rx_bits.shape[0]), int(tx_bits.shape[0])
@@ -388,26 +389,24 @@ def frame_sync_device(rx_bits, tx_bits, min_peak_ratio: float = 3.0):
         raise ParameterError("reference must be at least 2^14 bits")
     if n_rx < 64:
         raise SyncFailure("received stream too short")
-    rx = rx_bits.to(torch.float64) * 2 - 1
-    tx = tx_bits.to(torch.float64) * 2 - 1
-    if n_rx == n_tx:
-        c = torch.fft.irfft(torch.fft.rfft(rx) * torch.conj(torch.fft.rfft(tx)), n=n_rx)
-        mag = c.abs()
-        k = int(torch.argmax(mag))
-        m2 = mag.clone()
-        m2[k] = -1.0
-        ratio = float(mag[k] / (m2.max() + 1e-30))
+    dev = rx_bits.device
+    circular = int(n_rx == n_tx)
+    rx_bits = rx_bits.contiguous()
+    tx_bits = tx_bits.contiguous()
+    nws = int(_lib.load().kk_bit_xcorr_workspace_bytes(n_rx, n_tx, circular))
+    if nws == 0:
+        raise ParameterError("bit streams too long for frame sync (correlation length > 2^31)")
+    ws = torch.empty(nws, dtype=torch.uint8, device=dev)
+    out = torch.empty(3, dtype=torch.int64, device=dev)
+    _lib.call("kk_bit_xcorr", rx_bits.data_ptr(), n_rx, tx_bits.data_ptr(), n_tx, circular, ws.data_ptr(), nws,
+              out.data_ptr(), torch.cuda.current_stream(dev).cuda_stream)
+    k, peak, side = (int(v) for v in out.cpu())
+    del ws
+    ratio = peak / (side + 1e-30)
+    if circular:
         if ratio < min_peak_ratio:
             raise SyncFailure(f"no circular correlation peak (ratio {ratio:.2f})")
         return k, torch.roll(rx_bits, -k), tx_bits
-    L = n_rx + n_tx - 1
-    nfft = 1 << (L - 1).bit_length()
-    c = torch.fft.irfft(torch.fft.rfft(rx, n=nfft) * torch.fft.rfft(torch.flip(tx, [0]), n=nfft), n=nfft)[:L]
-    mag = c.abs()
-    k = int(torch.argmax(mag))
-    m2 = mag.clone()
-    m2[max(0, k - 2):min(L, k + 3)] = -1.0
-    ratio = float(mag[k] / (m2.max() + 1e-30))
     if ratio < min_peak_ratio:
         raise SyncFailure(f"no correlation peak (ratio {ratio:.2f})")
     lag = (n_tx - 1) - k
@@ -421,42 +420,49 @@ def frame_sync_device(rx_bits, tx_bits, min_peak_ratio: float = 3.0):
 def measure_point_device(labels, soft, bits, syms, cfg) -> dict:
     """measure_point (hr:104-137) with the decisions left on the GPU: labels
     (uint8 point indices) and soft (complex64) CUDA tensors, bits / syms the
-    transmitted bits and symbols (host).  Demap, frame sync, error count,
-    windowed Q and EVM all run on the device; only scalars come back."""
+    transmitted bits and symbols (host).  Labels -> bits (kk_label_bits),
+    frame sync (kk_bit_xcorr), error and per-window counts
+    (kk_bit_error_windows) and the EVM sums (kk_evm_sums) all run in the
+    repo's kernels; only scalars and the window counts come back."""
     import torch
-
-    from .constellation import slicer_tables
 
     spec = make_constellation(cfg.tx.constellation_order)
     k = spec.bits_per_symbol
     dev = labels.device
+    st = torch.cuda.current_stream(dev).cuda_stream
     head = cfg.rx.startup_symbols + cfg.metrics.head_guard_symbols
     stop = min(int(labels.shape[0]), len(syms)) - cfg.metrics.tail_guard_symbols
     if stop - head < 1000:
         raise SyncFailure("too few symbols beyond the startup region")
-    pl = torch.from_numpy(slicer_tables(spec.order).point_label.astype(np.int64)).to(dev)
-    lab = pl[labels[head:stop].long()]
-    shifts = torch.arange(k - 1, -1, -1, device=dev)
-    rx_bits = ((lab[:, None] >> shifts[None, :]) & 1).to(torch.uint8).reshape(-1)
+    pl = np.ascontiguousarray(slicer_tables(spec.order).point_label, dtype=np.uint8)
+    lab = labels[head:stop].contiguous()
+    rx_bits = torch.empty(int(lab.shape[0]) * k, dtype=torch.uint8, device=dev)
+    _lib.call("kk_label_bits", lab.data_ptr(), int(lab.shape[0]), pl.ctypes.data, spec.order, k,
+              rx_bits.data_ptr(), st)
     tx_bits = torch.from_numpy(np.ascontiguousarray(bits, dtype=np.uint8)).to(dev)
     offset, a_rx, a_tx = frame_sync_device(rx_bits, tx_bits)
-    errors = a_rx != a_tx
-    n_bits = int(errors.shape[0])
-    n_err = int(errors.sum())
-    ber = n_err / n_bits
-    s = soft[head:stop]
-    r = torch.from_numpy(np.ascontiguousarray(syms[head:stop], dtype=np.complex128)).to(dev)
-    evm_pct = float(100.0 * torch.sqrt(torch.mean((s.to(torch.complex128) - r).abs() ** 2) /
-                                       torch.mean(r.abs() ** 2)))
-    point = {"ber": ber, "q_db": q_from_ber(ber), "evm_pct": evm_pct, "n_bits": n_bits, "n_errors": n_err,
-             "sync_offset": int(offset)}
+    a_rx, a_tx = a_rx.contiguous(), a_tx.contiguous()
+    n_bits = int(a_rx.shape[0])
     bit_rate = cfg.tx.baud_hz * k
     win = cfg.metrics.windowed_q_window_s
     bpw = int(round(win * bit_rate))
-    if n_bits >= int(win * bit_rate) and bpw >= 1:
-        nw = n_bits // bpw
-        counts = errors[:nw * bpw].view(nw, bpw).sum(1).cpu().numpy()
-        point["windowed_q"] = [[float(t), float(q)] for t, q in windowed_q_from_counts(counts, bpw, win)]
+    n_win = n_bits // bpw if (n_bits >= int(win * bit_rate) and bpw >= 1) else 0
+    counts = torch.zeros(1 + max(n_win, 1), dtype=torch.int64, device=dev)
+    _lib.call("kk_bit_error_windows", a_rx.data_ptr(), a_tx.data_ptr(), n_bits, bpw if n_win else 0,
+              counts.data_ptr(), counts[1:].data_ptr() if n_win else None, st)
+    s = soft[head:stop].contiguous()
+    r = torch.from_numpy(np.ascontiguousarray(syms[head:stop], dtype=np.complex128)).to(dev)
+    sums = torch.zeros(2, dtype=torch.float64, device=dev)
+    _lib.call("kk_evm_sums", s.data_ptr(), r.data_ptr(), int(s.shape[0]), sums.data_ptr(), st)
+    c = counts.cpu().numpy()
+    se, sr = (float(v) for v in sums.cpu())
+    n_err = int(c[0])
+    ber = n_err / n_bits
+    evm_pct = float(100.0 * np.sqrt((se / s.shape[0]) / (sr / s.shape[0])))
+    point = {"ber": ber, "q_db": q_from_ber(ber), "evm_pct": evm_pct, "n_bits": n_bits, "n_errors": n_err,
+             "sync_offset": int(offset)}
+    if n_win:
+        point["windowed_q"] = [[float(t), float(q)] for t, q in windowed_q_from_counts(c[1:1 + n_win], bpw, win)]
     else:
         point["windowed_q"] = []
     return point
