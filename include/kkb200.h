@@ -321,8 +321,35 @@ int kk_bit_error_windows(const uint8_t *a, const uint8_t *b, int64_t n, int64_t 
 /*
  * EVM sums (metrics.py evm :169-179): sums[0] += sum |soft - ref|^2,
  * sums[1] += sum |ref|^2 in float64; soft complex64, ref complex128.
+ * Deterministic (fixed reduction order); scratch: 1024 doubles of device
+ * memory.
  */
-int kk_evm_sums(const void *soft, const void *ref, int64_t n, double *sums, void *stream);
+int kk_evm_sums(const void *soft, const void *ref, int64_t n, double *sums, double *scratch, void *stream);
+
+/*
+ * Float64 complex FFT of any length (numpy.fft.fft / ifft semantics, the
+ * transforms kkmodem's channel runs: channel.py apply_cd :90-103, ssfm_span
+ * :124-158): `batch` contiguous rows of n complex128 values from in to out
+ * (in == out allowed); inverse != 0 -> ifft with the 1/n normalisation.
+ * Powers of two run as Stockham passes, other lengths as Bluestein's
+ * chirp-z on a power-of-two length >= 2n - 1.  ws: kk_fft_workspace_bytes()
+ * bytes of device memory (0 = unsupported size).
+ */
+size_t kk_fft_workspace_bytes(int64_t n, int64_t batch);
+int kk_fft(const void *in, void *out, int64_t n, int64_t batch, int inverse, void *ws, size_t ws_bytes,
+           void *stream);
+
+/*
+ * One fiber span by the symmetric split-step Fourier method, in place on n
+ * complex128 field samples (replaces channel.py ssfm_span :124-158): n_steps
+ * times { half-step dispersion exp(-1j a_half f^2) (f = fftfreq(n, 1/fs));
+ * x *= exp(1j gamma (|x|^2 1e-3) l_eff); half-step dispersion; x *= loss_amp }.
+ * The caller derives n_steps, a_half, l_eff and loss_amp from the span as
+ * the reference does.  ws: kk_ssfm_workspace_bytes(n) bytes of device memory.
+ */
+size_t kk_ssfm_workspace_bytes(int64_t n);
+int kk_ssfm_span(void *x, int64_t n, double sample_rate_hz, int n_steps, double a_half, double gamma_per_w_km,
+                 double l_eff_km, double loss_amp, void *ws, size_t ws_bytes, void *stream);
 
 #ifdef __cplusplus
 }

@@ -487,3 +487,38 @@ def count_errors_aligned(dec_idx: np.ndarray, sym_idx: np.ndarray, order: int,
 def to_index(values: np.ndarray, order: int) -> np.ndarray:
     pts = constellation(order).points
     return np.argmin(np.abs(np.asarray(values)[:, None] - pts[None, :]), axis=1).astype(np.uint8)
+
+
+# ---------------------------------------------------------------------------
+# fiber span, split-step Fourier (channel.py ssfm_span :124-158, cd
+# coefficient :80-85) -- the step before the receive path;
+# pinned to kkmodem by tests/golden/channel_ssfm.npz (tools/gen_golden_channel.py)
+# ---------------------------------------------------------------------------
+def cd_phase_coefficient(dispersion_ps_nm_km: float, length_km: float, lambda_nm: float) -> float:
+    d_si = dispersion_ps_nm_km * 1e-6
+    lam = lambda_nm * 1e-9
+    return np.pi * d_si * lam ** 2 * (length_km * 1e3) / 299792458.0
+
+
+def ssfm_span(samples: np.ndarray, fs: float, length_km: float, loss_db_per_km: float, dispersion_ps_nm_km: float,
+              gamma_per_w_km: float, step_km: float | None = None, lambda_nm: float = 1550.116) -> np.ndarray:
+    if step_km is None:
+        step_km = 1.0
+    if step_km <= 0:
+        raise ValueError("step_km must be positive")
+    step_km = min(step_km, length_km) if length_km > 0 else step_km
+    n_steps = max(1, int(round(length_km / step_km)))
+    dz = length_km / n_steps
+    alpha = loss_db_per_km * np.log(10.0) / 10.0
+    a_half = cd_phase_coefficient(dispersion_ps_nm_km, dz / 2.0, lambda_nm)
+    f = np.fft.fftfreq(len(samples), 1.0 / fs)
+    lin_half = np.exp(-1j * a_half * f * f)
+    l_eff = (1.0 - np.exp(-alpha * dz)) / alpha if alpha > 0 else dz
+    loss_amp = np.exp(-alpha * dz / 2.0)
+    x = np.asarray(samples, dtype=np.complex128).copy()
+    for _ in range(n_steps):
+        x = np.fft.ifft(np.fft.fft(x) * lin_half)
+        x = x * np.exp(1j * gamma_per_w_km * (np.abs(x) ** 2 * 1e-3) * l_eff)
+        x = np.fft.ifft(np.fft.fft(x) * lin_half)
+        x *= loss_amp
+    return x

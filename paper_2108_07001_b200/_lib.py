@@ -71,7 +71,12 @@ _SIGS = {
     "kk_bit_xcorr": ([_P, _I64, _P, _I64, _I, _P, _SZ, _P, _P], _I),
     "kk_label_bits": ([_P, _I64, _P, _I, _I, _P, _P], _I),
     "kk_bit_error_windows": ([_P, _P, _I64, _I64, _P, _P, _P], _I),
-    "kk_evm_sums": ([_P, _P, _I64, _P, _P], _I),
+    "kk_evm_sums": ([_P, _P, _I64, _P, _P, _P], _I),
+    "kk_fft_workspace_bytes": ([_I64, _I64], _SZ),
+    "kk_fft": ([_P, _P, _I64, _I64, _I, _P, _SZ, _P], _I),
+    "kk_ssfm_workspace_bytes": ([_I64], _SZ),
+    "kk_ssfm_span": ([_P, _I64, ctypes.c_double, _I, ctypes.c_double, ctypes.c_double, ctypes.c_double,
+                      ctypes.c_double, _P, _SZ, _P], _I),
 }
 
 class K1Job(ctypes.Structure):

@@ -19,7 +19,7 @@ REPO = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 OUT_DIR = os.path.join(PKG, "_lib")
 LIB = os.path.join(OUT_DIR, "libkkb200.so")
-SOURCES = ["kk_capi.cu", "kk_kk.cu", "kk_static.cu", "kk_ddlms.cu", "kk_metrics.cu"]
+SOURCES = ["kk_capi.cu", "kk_kk.cu", "kk_static.cu", "kk_ddlms.cu", "kk_metrics.cu", "kk_fft.cu"]
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

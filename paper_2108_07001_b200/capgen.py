@@ -17,8 +17,8 @@ Reference stages it restates (kkmodem):
             low-pass), adc_quantize fe:103-118 (super-Gaussian AA low-pass,
             decimation, mid-rise 12-bit quantizer at 3x RMS full scale)
 
-B200 design: one overlap-save pipeline at the simulation rate on cuFFT
-(torch.fft, library FFTs -- this is not the receive hot path):
+B200 design: one overlap-save pipeline at the simulation rate, its FFTs the
+repo's float64 transforms (channel.fft / ifft -> kk_fft, batched rows):
   A  shaping FIR straight at the simulation rate (sps_sim = fs / baud), the
      carrier tone (exact rational phase) and the Wiener phase (carried);
   B  FFT(field) * CD(total length) + FFT(ASE) -> * OBPF -> IFFT, where the
@@ -49,6 +49,21 @@ from .sigcore import AdcCodes, ParameterError, cd_phase_coefficient, design_rrc
 PRBS_TAPS = {7: (6, 7), 15: (14, 15), 23: (18, 23), 31: (28, 31)}
 
 _C = 299792458.0
+
+
+def _fft(x, n=None):
+    """FFT over the last axis (zero padded to n) on kk_fft."""
+    import torch
+
+    from .channel import fft
+    if n is not None and x.shape[-1] < n:
+        x = torch.cat([x, x.new_zeros(*x.shape[:-1], n - x.shape[-1])], -1)
+    return fft(x.contiguous())
+
+
+def _ifft(x):
+    from .channel import ifft
+    return ifft(x.contiguous())
 _H = 6.62607015e-34
 
 
@@ -233,7 +248,7 @@ class CaptureGenerator:
         x[::sps] = sym_c
         xx = torch.cat([self.fir_tail, x])
         L = 1 << int(np.ceil(np.log2(len(xx) + self.n_fir)))
-        y = torch.fft.ifft(torch.fft.fft(xx, n=L) * torch.fft.fft(self.rrc.to(torch.complex64), n=L))
+        y = _ifft(_fft(xx, L) * _fft(self.rrc.to(torch.complex64), L)).to(torch.complex64)
         y = y[self.n_fir - 1:self.n_fir - 1 + n]              # causal linear convolution, chunk part
         self.fir_tail = xx[-(self.n_fir - 1):]
         if self.scale_sig is None:                             # amplitudes frozen on the first chunk
@@ -293,12 +308,12 @@ class CaptureGenerator:
         need = self.ov + nblk * hop + (self.N - hop - self.ov)
         if xx.shape[-1] < need:
             xx = torch.nn.functional.pad(xx, (0, need - xx.shape[-1]))
-        return torch.fft.fft(xx.unfold(-1, self.N, hop), dim=-1)
+        return _fft(xx.unfold(-1, self.N, hop)).to(torch.complex64)
 
     def _ols_out(self, Y, n):
         import torch
 
-        y = torch.fft.ifft(Y, dim=-1)[..., self.ov:]
+        y = _ifft(Y).to(torch.complex64)[..., self.ov:]
         return y.reshape(*y.shape[:-2], -1)[..., :n]
 
     def next_chunk(self, n_symbols: int):

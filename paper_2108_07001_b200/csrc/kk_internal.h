@@ -26,4 +26,15 @@ int num_sms();
 // set once per (device, kernel) for the whole process (thread-safe)
 int ensure_smem_attr(const void* fn, size_t smem, const char* what);
 
+// float64 power-of-two FFT (kk_fft.cu): twiddle tables for 2^log_n points
+// (table_bytes of device memory, built stream-ordered), and the batched
+// forward transform of `batch` rows ping-ponging between a and b (*result is
+// whichever holds the output).
+namespace fft64 {
+size_t table_bytes(int log_n);
+int build_tables(void* mem, int log_n, cudaStream_t st);
+int forward_pow2(double2* a, double2* b, int log_n, int64_t batch, const void* tables, cudaStream_t st,
+                 double2** result);
+}  // namespace fft64
+
 }  // namespace kk

@@ -142,7 +142,7 @@ def run_single(cfg, output_dir: str | None = None, save_captures: bool = False) 
     c = copy.deepcopy(cfg.to_dict() if hasattr(cfg, "to_dict") else cfg)
     ln = c["link"]
     if ln.get("nonlinearity_enabled"):
-        raise ParameterError("run_single on the GPU models the linear link only")
+        return _run_single_nonlinear(c, output_dir, save_captures)
     order = int(c["tx"]["constellation_order"])
     pts = make_constellation(order).points
     n_symbols = int(c["tx"]["n_symbols"])
@@ -217,6 +217,22 @@ def _kkmodem():
     except ImportError as exc:
         raise ParameterError("run_sweep drives the reference's own sweep driver: kkmodem must be importable "
                              "(tools/install_reference.py installs it into baseline/_ref)") from exc
+
+
+def _run_single_nonlinear(c: dict, output_dir, save_captures) -> dict:
+    """run_single for a nonlinear link: the split-step fiber is a whole-
+    capture recurrence (channel.py ssfm_span :124-158 over the full signal,
+    not chunkable like capgen's linear overlap-save), so the reference's own
+    run_single (runner.py:140-196) runs with the backend switch installed --
+    its ssfm_span spans and its receiver are this package's GPU ones
+    (kkmodem_backend), transmitter / EDFAs / front end stay kkmodem's."""
+    _kkmodem()
+    import kkmodem.harness.config as kcfg
+    import kkmodem.harness.runner as krun
+
+    from . import kkmodem_backend
+    kkmodem_backend.install()
+    return krun.run_single(kcfg.ExperimentConfig.from_dict(c), output_dir, save_captures)
 
 
 def run_sweep(cfg, output_dir: str | None = None) -> dict:
@@ -452,10 +468,10 @@ def measure_point_device(labels, soft, bits, syms, cfg) -> dict:
               counts.data_ptr(), counts[1:].data_ptr() if n_win else None, st)
     s = soft[head:stop].contiguous()
     r = torch.from_numpy(np.ascontiguousarray(syms[head:stop], dtype=np.complex128)).to(dev)
-    sums = torch.zeros(2, dtype=torch.float64, device=dev)
-    _lib.call("kk_evm_sums", s.data_ptr(), r.data_ptr(), int(s.shape[0]), sums.data_ptr(), st)
+    sums = torch.zeros(2 + 1024, dtype=torch.float64, device=dev)
+    _lib.call("kk_evm_sums", s.data_ptr(), r.data_ptr(), int(s.shape[0]), sums.data_ptr(), sums[2:].data_ptr(), st)
     c = counts.cpu().numpy()
-    se, sr = (float(v) for v in sums.cpu())
+    se, sr = (float(v) for v in sums[:2].cpu())
     n_err = int(c[0])
     ber = n_err / n_bits
     evm_pct = float(100.0 * np.sqrt((se / s.shape[0]) / (sr / s.shape[0])))

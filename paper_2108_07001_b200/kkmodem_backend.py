@@ -12,9 +12,12 @@ or, for the reference's own test-suite,
 
 `install()` rebinds the receive-path names of `kkmodem.rxdsp`
 (rxdsp.py:608-824 `RxPipeline` and the functional stages rx:184-601) to this
-package, and the names `kkmodem.harness.runner` imported from it by value
-(runner.py:16-24: `RxPipeline`, `demap`).  Everything else -- transmitter,
-channel, front end, metrics, sweeps, CLI -- stays the reference's own code,
+package, the names `kkmodem.harness.runner` imported from it by value
+(runner.py:16-24: `RxPipeline`, `demap`), and the nonlinear fiber span
+`kkmodem.channel.ssfm_span` (channel.py:124-158, called by name from
+propagate_link :208-209) to the GPU split-step span.
+Everything else -- transmitter, linear channel, front end, metrics, sweeps,
+CLI -- stays the reference's own code,
 so `run_single`, `run_sweep`, `run_sustained` and `bench_throughput` drive
 the GPU receiver unmodified.  The exception types this package raises are
 subclasses of kkmodem's (`sigcore.ParameterError` sigcore.py:37,
@@ -42,6 +45,8 @@ RXDSP_NAMES = (
 )
 # names harness/runner.py:16-24 imported by value from ..rxdsp
 RUNNER_NAMES = ("RxPipeline", "demap")
+# the nonlinear span of kkmodem.channel (propagate_link looks it up by name)
+CHANNEL_NAMES = ("ssfm_span",)
 
 _saved: dict | None = None
 
@@ -55,9 +60,11 @@ def install() -> None:
     global _saved
     if _saved is not None:
         return
+    import kkmodem.channel as kch
     import kkmodem.rxdsp as krx
     import kkmodem.harness.runner as krun
 
+    from . import channel as gch
     from . import rxdsp as gpu
     from ._lib import SyncError
     from .sigcore import ParameterError
@@ -72,10 +79,13 @@ def install() -> None:
     gpu._lib.load()
     saved = {("rx", n): getattr(krx, n) for n in RXDSP_NAMES}
     saved.update({("run", n): getattr(krun, n) for n in RUNNER_NAMES})
+    saved.update({("ch", n): getattr(kch, n) for n in CHANNEL_NAMES})
     for n in RXDSP_NAMES:
         setattr(krx, n, getattr(gpu, n))
     for n in RUNNER_NAMES:
         setattr(krun, n, getattr(gpu, n))
+    for n in CHANNEL_NAMES:
+        setattr(kch, n, getattr(gch, n))
     _saved = saved
 
 
@@ -84,11 +94,13 @@ def uninstall() -> None:
     global _saved
     if _saved is None:
         return
+    import kkmodem.channel as kch
     import kkmodem.rxdsp as krx
     import kkmodem.harness.runner as krun
 
+    mods = {"rx": krx, "run": krun, "ch": kch}
     for (where, n), v in _saved.items():
-        setattr(krx if where == "rx" else krun, n, v)
+        setattr(mods[where], n, v)
     _saved = None
 
 

@@ -17,6 +17,7 @@ import importlib
 import importlib.util
 import json
 import os
+import sys
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -26,12 +27,18 @@ def kkmodem_class(module: str, name: str):
     """kkmodem's own class `module.name` when the reference package is
     importable (so errors raised here are caught by the reference's callers,
     e.g. runner.py:182 `except (SyncError, SyncFailure)`), else None.
-    KKB200_NO_KKMODEM=1 disables the lookup."""
+    The repo-local reference install (baseline/_ref, tools/install_reference.py)
+    is used when kkmodem is not otherwise importable.  KKB200_NO_KKMODEM=1
+    disables the lookup."""
     if os.environ.get("KKB200_NO_KKMODEM") == "1":
         return None
     try:
         if importlib.util.find_spec("kkmodem") is None:
-            return None
+            ref = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "baseline", "_ref")
+            if not os.path.isdir(os.path.join(ref, "kkmodem")):
+                return None
+            os.environ.setdefault("NUMBA_CACHE_DIR", "/tmp/kkb200_numba_cache")
+            sys.path.append(ref)
         return getattr(importlib.import_module(module), name)
     except Exception:   # a broken or partial kkmodem install: stand alone
         return None

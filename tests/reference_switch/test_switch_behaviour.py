@@ -61,3 +61,22 @@ def test_forced_sync_failure_marks_point_failed():
     (point,) = report["points"]
     assert point["status"] == "failed", point
     assert "peak" in point["reason"] or "correlation" in point["reason"], point["reason"]
+
+
+def test_nonlinear_link_runs_gpu_spans():
+    """channel.py:208-209: propagate_link calls ssfm_span by name, so with the
+    switch the nonlinear spans are the GPU split-step (kk_ssfm_span); its
+    output equals the reference's own span to float64 rounding."""
+    import kkmodem.channel as kch
+    from paper_2108_07001_b200 import channel as gch
+
+    assert kch.ssfm_span is gch.ssfm_span
+    orig = kkmodem_backend._saved[("ch", "ssfm_span")]
+    rng = np.random.default_rng(8)
+    x = ksc.ComplexSignal(np.sqrt(5.0) * (rng.standard_normal(6000) + 1j * rng.standard_normal(6000)), 16e9)
+    span = kch.FiberSpan(length_km=100.0)
+    got = kch.ssfm_span(x, span, 10.0)
+    want = orig(x, span, 10.0)
+    assert type(got) is type(want)
+    err = np.linalg.norm(got.samples - want.samples) / np.linalg.norm(want.samples)
+    assert err < 1e-10, err

@@ -167,10 +167,15 @@ def test_label_bits_error_windows_evm():
         assert np.array_equal(c[1:], e[: nw * bpw].reshape(nw, bpw).sum(1))
     s = (rng.standard_normal(50_001) + 1j * rng.standard_normal(50_001)).astype(np.complex64)
     r = rng.standard_normal(50_001) + 1j * rng.standard_normal(50_001)
-    sums = torch.zeros(2, dtype=torch.float64, device=dev)
-    _lib.call("kk_evm_sums", torch.from_numpy(s).to(dev).data_ptr(), torch.from_numpy(r).to(dev).data_ptr(),
-              len(s), sums.data_ptr(), torch.cuda.current_stream().cuda_stream)
-    se, sr = sums.cpu().numpy()
+    sums = torch.zeros(2 + 1024, dtype=torch.float64, device=dev)
+    ds, dr = torch.from_numpy(s).to(dev), torch.from_numpy(r).to(dev)
+    _lib.call("kk_evm_sums", ds.data_ptr(), dr.data_ptr(), len(s), sums.data_ptr(), sums[2:].data_ptr(),
+              torch.cuda.current_stream().cuda_stream)
+    se, sr = sums[:2].cpu().numpy()
+    again = torch.zeros(2 + 1024, dtype=torch.float64, device=dev)
+    _lib.call("kk_evm_sums", ds.data_ptr(), dr.data_ptr(), len(s), again.data_ptr(), again[2:].data_ptr(),
+              torch.cuda.current_stream().cuda_stream)
+    assert torch.equal(again[:2], sums[:2])   # deterministic
     assert abs(se - np.sum(np.abs(s.astype(np.complex128) - r) ** 2)) < 1e-9 * se
     assert abs(sr - np.sum(np.abs(r) ** 2)) < 1e-9 * sr
 

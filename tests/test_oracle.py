@@ -92,3 +92,25 @@ def test_oracle_kk_constant_and_zero_block():
     out, _, dg = ko.kk_reconstruct(x)
     assert dg["zero_blocks"] == [1]
     assert np.all(out[768:1280] == 0)
+
+
+def _ssfm_cases():
+    z = np.load(os.path.join(os.path.dirname(__file__), "golden", "channel_ssfm.npz"))
+    out = []
+    i = 0
+    while f"x{i}" in z:
+        n, fs, L, loss, D, g, step, p = z[f"p{i}"]
+        out.append((z[f"x{i}"], z[f"y{i}"], dict(fs=fs, length_km=L, loss_db_per_km=loss, dispersion_ps_nm_km=D,
+                                                 gamma_per_w_km=g, step_km=None if np.isnan(step) else step)))
+        i += 1
+    return out
+
+
+def test_oracle_ssfm_span_reproduces_reference():
+    """The split-step span restatement (channel.py:124-158) equals kkmodem's
+    own ssfm_span on the golden inputs (same numpy calls and order)."""
+    cases = _ssfm_cases()
+    assert len(cases) == 4
+    for x, y, kw in cases:
+        got = ko.ssfm_span(x, **kw)
+        assert np.array_equal(got, y)
