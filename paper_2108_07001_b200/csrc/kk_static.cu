@@ -154,12 +154,44 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float2 (&v)[8]) {
 __device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory"); }
 __device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory"); }
 
+// Bulk (TMA-engine) copies global -> shared with mbarrier completion: the
+// second column's inputs of chain 0 (x0 and x1 halves, 16 runs of 512
+// samples each = 128 KB) are copied by one thread while the first column is
+// transformed, instead of 16 per-thread cp.async + 16 __ldg per thread.
+#ifndef KK_K2_BULK
+#define KK_K2_BULK 1
+#endif
+#ifndef KK_K2_BULK_X1
+#define KK_K2_BULK_X1 0
+#endif
+__device__ __forceinline__ void mbar_init(uint32_t bar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(bar), "r"(count) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(bar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait_parity(uint32_t bar, unsigned parity) {
+    asm volatile(
+        "{\n.reg .pred p;\nKK_MBAR_WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra KK_MBAR_WAIT_%=;\n}\n" ::"r"(bar),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, unsigned bytes, uint32_t bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(dst),
+                 "l"(src), "r"(bytes), "r"(bar)
+                 : "memory");
+}
+
 // Chain 0 column j: v[r] = a(n), and the odd chain's b(n) W32^r parked in
 // TMEM at taddr (+16 columns for r >= 8).
 template <bool FAST>
 __device__ __forceinline__ void k2_load_column_ab(const K2Params& p, const BlockIn& b, const float2* rot_s, int j,
                                                   float2 mA, float2 mB, int bnd, unsigned s1024, unsigned s16384,
-                                                  float2 (&v)[16], uint32_t taddr, const float2* x0_s = nullptr) {
+                                                  float2 (&v)[16], uint32_t taddr, const float2* x0_s = nullptr,
+                                                  const float2* x1_s = nullptr) {
     float2 w[8];
     if constexpr (FAST) {
         const float2* z0 = p.z + (b.base - p.z_index0) + j;
@@ -188,7 +220,9 @@ __device__ __forceinline__ void k2_load_column_ab(const K2Params& p, const Block
         for (int r = 0; r < 16; ++r) {
             // x0 of the second column arrives early in smem (cp.async at chain start)
             const float2 x0 = x0_s ? x0_s[r * kK2Threads] : __ldg(z0 + 1024 * r);
-            const float2 x1 = __ldg(z0 + kHopS + 1024 * r);
+            // x1 staged by the bulk copies: run r at row r of the FFT buffer,
+            // right half, +1 slot on odd rows (16 B alignment)
+            const float2 x1 = x1_s ? x1_s[r * kRowE + (r & 1)] : __ldg(z0 + kHopS + 1024 * r);
             float2 ua = cadd(x0, x1), ub = csub(x0, x1);
             if (p.carrier) {
                 ua = csub(ua, ca);
@@ -292,6 +326,22 @@ __device__ __forceinline__ void k2_body(const int bx, const int64_t grid_x, cons
 
     const int warp = tid >> 5, lane = tid & 31;
     float2* E = S.buf;
+    __shared__ __align__(8) unsigned long long bulk_bar;
+    const uint32_t bar_a = static_cast<uint32_t>(__cvta_generic_to_shared(&bulk_bar));
+    const float2* zq = p.z + (bi.base - p.z_index0);
+    const bool bulk = KK_K2_BULK && FAST && ((reinterpret_cast<uintptr_t>(zq) & 15) == 0);
+    if (bulk && tid == 0) {
+        mbar_init(bar_a, 1);
+        mbar_expect_tx(bar_a, (KK_K2_BULK_X1 ? 32u : 16u) * kK2Threads * sizeof(float2));
+#pragma unroll 1
+        for (int r = 0; r < 16; ++r) {
+            bulk_g2s(static_cast<uint32_t>(__cvta_generic_to_shared(S.A + r * kK2Threads)), zq + kK2Threads + 1024 * r,
+                     kK2Threads * sizeof(float2), bar_a);
+            if (KK_K2_BULK_X1)
+                bulk_g2s(static_cast<uint32_t>(__cvta_generic_to_shared(E + r * kRowE + kK2Threads + (r & 1))),
+                         zq + kHopS + kK2Threads + 1024 * r, kK2Threads * sizeof(float2), bar_a);
+        }
+    }
     // TMEM scratch (one CTA per SM: the allocation always succeeds)
     __shared__ uint32_t tmem_base_sh;
     if (warp == 0) {
@@ -315,12 +365,21 @@ __device__ __forceinline__ void k2_body(const int bx, const int64_t grid_x, cons
             const uint32_t taddr = tmem_thread + 32 * q;
             if (chain == 0) {
                 const float2* x0s = nullptr;
+                const float2* x1s = nullptr;
                 if (FAST && q == 1) {
-                    asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+                    if (bulk) {
+                        mbar_wait_parity(bar_a, 0);
+                        if (KK_K2_BULK_X1) x1s = E + kK2Threads + tid;
+                    } else {
+                        asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+                    }
                     x0s = S.A + tid;
                 }
-                k2_load_column_ab<FAST>(p, bi, S.rot, j, mA, mB, bnd, s1024, s16384, v, taddr, x0s);
-                if (FAST && q == 0) {
+                k2_load_column_ab<FAST>(p, bi, S.rot, j, mA, mB, bnd, s1024, s16384, v, taddr, x0s, x1s);
+                // the staged x1 of odd rows sits one slot right: the slot this
+                // thread's row outputs overwrite belongs to the neighbour's input
+                if (KK_K2_BULK_X1 && bulk && q == 1) __syncthreads();
+                if (FAST && !bulk && q == 0) {
                     // the second column's x0 half (16 x 8 B per thread) is copied into
                     // the (still unused) A buffer while the first column is transformed
                     // (K2 11.83 -> 11.54 ms per 2^30 samples; issuing it before the first

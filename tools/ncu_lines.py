@@ -13,7 +13,7 @@ def main():
     rep, kern = sys.argv[1], sys.argv[2]
     skip = sys.argv[3] if len(sys.argv) > 3 else "0"
     top = int(sys.argv[4]) if len(sys.argv) > 4 else 40
-    out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "cuda", "--kernel-name",
+    out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "cuda,sass", "--kernel-name",
                           f"regex:{kern}", "--launch-skip", skip, "--launch-count", "1"],
                          capture_output=True, text=True).stdout
     rows = list(csv.reader(out.splitlines()))
@@ -23,14 +23,14 @@ def main():
     for r in rows:
         if not r:
             continue
-        if r[0] == "File Path" or r[0] == "File Name":
+        if r[0] in ("File Path", "File Name"):
             cur_file = r[1].split("/")[-1]
             continue
         if r[0] == "Line No":
             hdr = r
             continue
-        if hdr is None or len(r) != len(hdr):
-            continue
+        if hdr is None or len(r) != len(hdr) or (len(r) > 2 and r[2] != "-"):
+            continue   # source-line rows only (SASS rows carry an address)
         try:
             ie = float(r[hdr.index("Instructions Executed")].replace(",", "") or 0)
             ss = float(r[hdr.index("Warp Stall Sampling (All Samples)")].replace(",", "") or 0)
