@@ -130,6 +130,9 @@ class GpuOptions:
     # cannot hide (measured: 2^22-symbol frame 0.47 ms at B=128, 0.61 at 512)
     ddlms_block_min: int = 128
     ddlms_frame_symbols: int = 1 << 28
+    # drain() closes the open frame at the last produced symbol when at
+    # least this many symbols are undecided (RxPipeline._release_decidable)
+    ddlms_release_min_symbols: int = 1
     ddlms_max_iter: int = 1024
     ddlms_soft_tol: float = 1e-5
     ddlms_tail_min_symbols: int = 1 << 24
@@ -1519,9 +1522,30 @@ class RxPipeline:
         self._out = []
         return labels, soft, meta
 
+    def _release_decidable(self) -> None:
+        """Close the open DDLMS frame at the last symbol the front end has
+        produced (drain() releases everything decidable so far, as the
+        reference's per-feed DDLMS does, rx:803-809).  Frame boundaries then
+        follow the caller's drain() calls: the decisions equal the
+        grid-framed ones (the frames chain exactly) except at fp32 ties, and
+        a stream that is never drained mid-way keeps the chunk-invariant
+        grid."""
+        if self._flushed or not self._synced or getattr(self, "_front_only", False):
+            return
+        n_q = self._y2.end - self._drop
+        nt = self.cfg.ddlms.n_taps
+        total = (n_q - nt) // 2 + 1 if n_q >= nt else 0
+        k0 = self._sym_done
+        if total - k0 >= int(self.gpu.ddlms_release_min_symbols):
+            (self._submit_frame if self._async else self._solve_frame)(k0, total)
+
     def drain(self):
         """Return (decisions, soft) accumulated so far as complex128 and clear
-        them (rx:803-809)."""
+        them (rx:803-809).  Every symbol the front end has produced is
+        decided first (see _release_decidable)."""
+        self._release_decidable()
+        if self._async:
+            self._wait_frames()
         labels, soft, meta = self.drain_device()
         if labels.numel() == 0:
             return np.zeros(0, dtype=np.complex128), np.zeros(0, dtype=np.complex128)
