@@ -33,7 +33,7 @@
 extern "C" {
 #endif
 
-#define KK_ABI_VERSION 1
+#define KK_ABI_VERSION 2
 
 #define KK_OK 0
 #define KK_ERR_PARAM 1
@@ -73,8 +73,12 @@ int kk_upload(void *dst_dev, const void *src_host, int64_t bytes, void *stream);
  * Processes n_hops hops of 512 ADC samples in pairs (hop 2p, 2p+1 of this
  * call).  State in/out = the reference state dict: u_tail[512] (float),
  * a_hist[256] (float), dead_hist[256] (uint8).  Output out[n_hops*512] is
- * the field, rotated by exp(-2 pi i (rot_p*g mod rot_q)/rot_q) at global
- * index g = n0_global + i when rot_q > 0, conjugated when mirror != 0.
+ * the field, rotated by the downshift (sigcore.py frequency_shift :286-299 by
+ * -tone) at global index g = n0_global + i, conjugated when mirror != 0:
+ * rot_q > 0: exp(-2 pi i (rot_p*g mod rot_q)/rot_q) (tone/fs = rot_p/rot_q,
+ * rot_q <= 1024, rot_tab[a] = exp(-2 pi i a/rot_q)); rot_q == 0 and
+ * rot_step != 0: any tone, exp(-2 pi i (g*rot_step mod 2^64)/2^64) with
+ * rot_step = tone/fs as a 64-bit fixed-point fraction; both 0: none.
  * hop_sum[n_hops]: per-hop sum of the (unrotated) field; hop_dead[n_hops];
  * clamped: += clamped-sample count.  clamp_rel: rxdsp.py:188 (1e-12).
  */
@@ -83,7 +87,7 @@ int kk_reconstruct_pairs(int in_dtype, const void *in, float in_scale, float cla
                          float *new_u, float *new_a, uint8_t *new_dead, void *out,
                          void *hop_sum, uint8_t *hop_dead, unsigned long long *clamped,
                          int64_t n0_global, int rot_p, int rot_q, const void *rot_tab,
-                         int mirror, void *stream);
+                         unsigned long long rot_step, int mirror, void *stream);
 
 /*
  * Batched K1 (B200 addition): independent streams (sweep
@@ -110,6 +114,7 @@ typedef struct {
     int rot_p;
     int rot_q;
     const void *rot_tab;
+    unsigned long long rot_step;
     int mirror;
 } kk_k1_job;
 int kk_reconstruct_pairs_batch(int in_dtype, const kk_k1_job *jobs, int n_jobs, void *stream);
@@ -131,12 +136,13 @@ int kk_carrier_means(const void *hop_sum, int64_t n_segs, int hops_per_seg, int6
  * subtraction rxdsp.py:687.  Block hb (global static hop, 16384 samples)
  * reads s[16384(hb-1) .. 16384(hb+1)) where s = z - conj(mean*rot)
  * (mirror) and writes 8192 2-sps outputs.  h_even/h_odd: the response
- * _static_response (rxdsp.py:401-411) at even / odd kept indices.
+ * _static_response (rxdsp.py:401-411) at even / odd kept indices.  The
+ * rotation arguments mean what they mean for kk_reconstruct_pairs.
  */
 int kk_static_blocks(const void *z, int64_t z_index0, int64_t hb0, int64_t n_blocks, int64_t valid_end,
                      const void *seg_mean, int64_t seg_index0, int seg_len, int carrier, int rot_p,
-                     int rot_q, const void *rot_tab, int mirror, const void *h_even, const void *h_odd,
-                     void *out, void *stream);
+                     int rot_q, const void *rot_tab, unsigned long long rot_step, int mirror,
+                     const void *h_even, const void *h_odd, void *out, void *stream);
 
 /* Batched K2 (B200 addition): one job per stream, each a
  * kk_static_blocks call with the same argument meaning; host job array. */
@@ -153,6 +159,7 @@ typedef struct {
     int rot_p;
     int rot_q;
     const void *rot_tab;
+    unsigned long long rot_step;
     int mirror;
     const void *h_even;
     const void *h_odd;

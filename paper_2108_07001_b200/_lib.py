@@ -35,6 +35,7 @@ _I = ctypes.c_int
 _F = ctypes.c_float
 _D = ctypes.c_double
 _SZ = ctypes.c_size_t
+_U64 = ctypes.c_uint64
 
 _SIGS = {
     "kk_last_error": ([], ctypes.c_char_p),
@@ -43,10 +44,11 @@ _SIGS = {
     "kk_launch_count": ([], ctypes.c_ulonglong),
     "kk_fma_peak": ([_P, _P], _I),
     "kk_upload": ([_P, _P, _I64, _P], _I),
-    "kk_reconstruct_pairs": ([_I, _P, _F, _F, _I64, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _I64, _I, _I, _P, _I, _P], _I),
+    "kk_reconstruct_pairs": ([_I, _P, _F, _F, _I64, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _I64, _I, _I, _P, _U64, _I,
+                              _P], _I),
     "kk_unpack12": ([_P, _I64, _P, _P], _I),
     "kk_carrier_means": ([_P, _I64, _I, _I64, _I64, _I, _P, _P], _I),
-    "kk_static_blocks": ([_P, _I64, _I64, _I64, _I64, _P, _I64, _I, _I, _I, _I, _P, _I, _P, _P, _P, _P], _I),
+    "kk_static_blocks": ([_P, _I64, _I64, _I64, _I64, _P, _I64, _I, _I, _I, _I, _P, _U64, _I, _P, _P, _P, _P], _I),
     "kk_symbol_sync_scratch_bytes": ([_I64, _I], _SZ),
     "kk_symbol_sync": ([_P, _I64, _P, _I, _I64, _P, _P, _SZ, _P], _I),
     "kk_symbol_sync_enqueue": ([_P, _I64, _P, _I, _I64, _P, _P, _SZ, _P], _I),
@@ -84,14 +86,15 @@ class K1Job(ctypes.Structure):
     _fields_ = [("in_", _P), ("in_scale", _F), ("clamp_rel", _F), ("n_hops", _I64), ("st_u", _P), ("st_a", _P),
                 ("st_dead", _P), ("new_u", _P), ("new_a", _P), ("new_dead", _P), ("out", _P), ("hop_sum", _P),
                 ("hop_dead", _P), ("clamped", _P), ("n0_global", _I64), ("rot_p", _I), ("rot_q", _I),
-                ("rot_tab", _P), ("mirror", _I)]
+                ("rot_tab", _P), ("rot_step", _U64), ("mirror", _I)]
 
 
 class K2Job(ctypes.Structure):
     """kk_k2_job (include/kkb200.h): one stream's kk_static_blocks arguments."""
     _fields_ = [("z", _P), ("z_index0", _I64), ("hb0", _I64), ("n_blocks", _I64), ("valid_end", _I64),
                 ("seg_mean", _P), ("seg_index0", _I64), ("seg_len", _I), ("carrier", _I), ("rot_p", _I),
-                ("rot_q", _I), ("rot_tab", _P), ("mirror", _I), ("h_even", _P), ("h_odd", _P), ("out", _P)]
+                ("rot_q", _I), ("rot_tab", _P), ("rot_step", _U64), ("mirror", _I), ("h_even", _P), ("h_odd", _P),
+                ("out", _P)]
 
 
 _SIGS["kk_reconstruct_pairs_batch"] = ([_I, ctypes.POINTER(K1Job), _I, _P], _I)

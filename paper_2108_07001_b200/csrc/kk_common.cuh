@@ -42,6 +42,24 @@ __device__ __forceinline__ unsigned fmod_u(unsigned x, unsigned d, float inv_d, 
     return static_cast<unsigned>(r);
 }
 
+// Downshift rotation of a general tone (rot_q == 0, rot_step != 0 in the C
+// ABI): exp(-2 pi i ph / 2^64), ph = g * rot_step (mod 2^64) the phase of
+// global sample g as a 64-bit fixed-point fraction of a cycle (exact at any
+// stream index; sigcore.py frequency_shift :286-299 computes the same phase
+// in float64).  Fast: the top 32 bits through the SFU (~1e-6 absolute);
+// precise: float64 sincospi of the whole phase.
+__device__ __forceinline__ float2 rot_phase_fast(unsigned long long ph) {
+    const float x = static_cast<float>(static_cast<int>(static_cast<unsigned>(ph >> 32))) * 2.3283064365386963e-10f;
+    float s, c;
+    __sincosf(-6.283185307179586f * x, &s, &c);     // x in [-0.5, 0.5): no range reduction needed
+    return make_float2(c, s);
+}
+__device__ __forceinline__ float2 rot_phase_precise(unsigned long long ph) {
+    double s, c;
+    sincospi(-2.0 * static_cast<double>(static_cast<long long>(ph)) * 5.421010862427522170e-20, &s, &c);
+    return make_float2(static_cast<float>(c), static_cast<float>(s));
+}
+
 // cos/sin(2*pi*t/16) for t in [0,8)
 __host__ __device__ constexpr float c16(int t) {
     return t == 0 ? 1.0f : t == 1 ? 0.92387953251128674f : t == 2 ? 0.70710678118654752f

@@ -130,7 +130,7 @@ k1_body(const int bx, const typename InElem<TIn>::T* __restrict__ in, float in_s
         float2* __restrict__ out, float2* __restrict__ hop_sum, uint8_t* __restrict__ hop_dead,
         unsigned long long* __restrict__ clamped_total,
         int64_t n0_global, int rot_p, int rot_q, const float2* __restrict__ rot_tab,
-        int mirror, const float2* __restrict__ tw_g)
+        unsigned long long rot_step, int mirror, const float2* __restrict__ tw_g)
 {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     K1Smem& S = *reinterpret_cast<K1Smem*>(smem_raw);
@@ -301,10 +301,14 @@ k1_body(const int bx, const typename InElem<TIn>::T* __restrict__ in, float in_s
         rot_base = (static_cast<unsigned>(n0_global) + (static_cast<unsigned>(hop_a) % Q) * (512u % Q)) % Q;
     }
     float2 rot_cache = make_float2(1.f, 0.f), r256 = rot_cache, r512 = rot_cache;
+    const bool rotate = rot_q > 0 || rot_step != 0ull;
     if (rot_q > 0) {
         const unsigned Q = static_cast<unsigned>(rot_q), Pp = static_cast<unsigned>(rot_p);
         r256 = __ldg(rot_tab + (256u * Pp) % Q);     // exp(-2 pi i (256 p mod q) / q)
         r512 = __ldg(rot_tab + (512u * Pp) % Q);
+    } else if (rot_step) {
+        r256 = PRECISE ? rot_phase_precise(256ull * rot_step) : rot_phase_fast(256ull * rot_step);
+        r512 = PRECISE ? rot_phase_precise(512ull * rot_step) : rot_phase_fast(512ull * rot_step);
     }
     auto st_out = [&](int n, float2 v) {
         if (n < kHop) return;
@@ -327,17 +331,22 @@ k1_body(const int bx, const typename InElem<TIn>::T* __restrict__ in, float in_s
         const int64_t pa = hop_a * kHop + i;           // chunk positions
         const int64_t pb = pa + kHop;
         float2 za = fa, zb = fb;
-        if (rot_q > 0) {
-            // field * exp(-2 pi i a/q).  A butterfly's outputs i = j and
-            // j + 256 of hops a and b are 256 / 512 samples apart: one sincos
-            // for the first, exact constant rotations (table entries) for the
-            // others
+        if (rotate) {
+            // field * exp(-2 pi i a/q) (or the general tone's phase).  A
+            // butterfly's outputs i = j and j + 256 of hops a and b are 256 /
+            // 512 samples apart: one sincos for the first, exact constant
+            // rotations (table entries) for the others
             if (i < kHop / 2) {
-                const unsigned Q = static_cast<unsigned>(rot_q), P = static_cast<unsigned>(rot_p);
-                const int ia = static_cast<int>(fmod_u((rot_base + i) * P, Q, inv_q));
-                float sr, cr;
-                k1_sincos<PRECISE>(-two_pi_over_q * static_cast<float>(ia), &sr, &cr);
-                rot_cache = make_float2(cr, sr);
+                if (rot_q > 0) {
+                    const unsigned Q = static_cast<unsigned>(rot_q), P = static_cast<unsigned>(rot_p);
+                    const int ia = static_cast<int>(fmod_u((rot_base + i) * P, Q, inv_q));
+                    float sr, cr;
+                    k1_sincos<PRECISE>(-two_pi_over_q * static_cast<float>(ia), &sr, &cr);
+                    rot_cache = make_float2(cr, sr);
+                } else {
+                    const unsigned long long ph = static_cast<unsigned long long>(n0_global + pa) * rot_step;
+                    rot_cache = PRECISE ? rot_phase_precise(ph) : rot_phase_fast(ph);
+                }
             } else {
                 rot_cache = cmul(rot_cache, r256);
             }
@@ -391,9 +400,9 @@ kk_pairs_kernel(const typename InElem<TIn>::T* __restrict__ in, float in_scale, 
                 float2* __restrict__ out, float2* __restrict__ hop_sum, uint8_t* __restrict__ hop_dead,
                 unsigned long long* __restrict__ clamped_total,
                 int64_t n0_global, int rot_p, int rot_q, const float2* __restrict__ rot_tab,
-                int mirror, const float2* __restrict__ tw_g) {
+                unsigned long long rot_step, int mirror, const float2* __restrict__ tw_g) {
     k1_body<TIn, PRECISE>(blockIdx.x, in, in_scale, clamp_rel, n_hops, st_u, st_a, st_dead, new_u, new_a, new_dead, out,
-                          hop_sum, hop_dead, clamped_total, n0_global, rot_p, rot_q, rot_tab, mirror, tw_g);
+                          hop_sum, hop_dead, clamped_total, n0_global, rot_p, rot_q, rot_tab, rot_step, mirror, tw_g);
 }
 
 // Batched K1 (independent streams -- sweep points -- in one launch, SURVEY
@@ -411,11 +420,12 @@ kk_pairs_batch_kernel(const __grid_constant__ K1Batch b, const float2* __restric
     const int64_t ctas = ((j.n_hops + 1) / 2 + kPairsPerCta - 1) / kPairsPerCta;
     if (blockIdx.x >= ctas) return;
     const int q = j.rot_q;
-    const int64_t n0m = q > 0 ? ((j.n0_global % q) + q) % q : 0;
+    // rational tones need the stream index modulo q only; general tones the index itself
+    const int64_t n0m = q > 0 ? ((j.n0_global % q) + q) % q : j.n0_global;
     k1_body<TIn, PRECISE>(blockIdx.x, static_cast<const typename InElem<TIn>::T*>(j.in), j.in_scale, j.clamp_rel,
                           j.n_hops, j.st_u, j.st_a, j.st_dead, j.new_u, j.new_a, j.new_dead,
                           static_cast<float2*>(j.out), static_cast<float2*>(j.hop_sum), j.hop_dead, j.clamped, n0m,
-                          j.rot_p, q, static_cast<const float2*>(j.rot_tab), j.mirror, tw_g);
+                          j.rot_p, q, static_cast<const float2*>(j.rot_tab), j.rot_step, j.mirror, tw_g);
 }
 
 template <typename TIn, bool PRECISE>
@@ -447,7 +457,8 @@ template <typename TIn, bool PRECISE>
 static int launch_k1(const void* in, float in_scale, float clamp_rel, int64_t n_hops, const float* st_u, const float* st_a,
                      const uint8_t* st_dead, float* new_u, float* new_a, uint8_t* new_dead, float2* out,
                      float2* hop_sum, uint8_t* hop_dead, unsigned long long* clamped, int64_t n0,
-                     int rot_p, int rot_q, const float2* rot_tab, int mirror, cudaStream_t s) {
+                     int rot_p, int rot_q, const float2* rot_tab, unsigned long long rot_step, int mirror,
+                     cudaStream_t s) {
     const float2* tw = twiddle_table_device();
     if (!tw) return KK_ERR_CUDA;
     const size_t smem = sizeof(K1Smem);
@@ -456,12 +467,12 @@ static int launch_k1(const void* in, float in_scale, float clamp_rel, int64_t n_
     if (n_hops >= (int64_t(1) << 31)) return set_error(KK_ERR_PARAM, "n_hops must be < 2^31 per call");
     const int64_t pairs = (n_hops + 1) / 2;
     const int64_t grid = (pairs + kPairsPerCta - 1) / kPairsPerCta;
-    // the kernel only needs the stream index modulo the rotation period
-    const int64_t n0m = rot_q > 0 ? ((n0 % rot_q) + rot_q) % rot_q : 0;
+    // a rational tone needs the stream index modulo its period only
+    const int64_t n0m = rot_q > 0 ? ((n0 % rot_q) + rot_q) % rot_q : n0;
     kk_pairs_kernel<TIn, PRECISE><<<static_cast<unsigned>(grid), kK1Threads, smem, s>>>(
         static_cast<const typename InElem<TIn>::T*>(in), in_scale, clamp_rel, n_hops, st_u, st_a, st_dead, new_u, new_a,
         new_dead, out,
-        hop_sum, hop_dead, clamped, n0m, rot_p, rot_q, rot_tab, mirror, tw);
+        hop_sum, hop_dead, clamped, n0m, rot_p, rot_q, rot_tab, rot_step, mirror, tw);
     return check_launch("kk_pairs_kernel");
 }
 
@@ -472,7 +483,7 @@ extern "C" int kk_reconstruct_pairs(int in_dtype, const void* in, float in_scale
                                     float* new_u, float* new_a, uint8_t* new_dead, void* out,
                                     void* hop_sum, uint8_t* hop_dead, unsigned long long* clamped,
                                     int64_t n0_global, int rot_p, int rot_q, const void* rot_tab,
-                                    int mirror, void* stream) {
+                                    unsigned long long rot_step, int mirror, void* stream) {
     using namespace kk;
     clear_error();
     if (n_hops <= 0) return set_error(KK_ERR_PARAM, "n_hops must be positive");
@@ -484,7 +495,7 @@ extern "C" int kk_reconstruct_pairs(int in_dtype, const void* in, float in_scale
     const bool precise = (in_dtype & KK_DTYPE_PRECISE) != 0;
 #define KK_LAUNCH_K1(T, PR)                                                                                    \
     return launch_k1<T, PR>(in, in_scale, clamp_rel, n_hops, st_u, st_a, st_dead, new_u, new_a, new_dead, o, hs, \
-                            hop_dead, clamped, n0_global, rot_p, rot_q, rt, mirror, s)
+                            hop_dead, clamped, n0_global, rot_p, rot_q, rt, rot_step, mirror, s)
     switch (in_dtype & ~KK_DTYPE_PRECISE) {
         case KK_DTYPE_I16:
             if (precise) KK_LAUNCH_K1(int16_t, true);

@@ -60,8 +60,9 @@ struct K2Params {
     int64_t seg_index0;
     int seg_len;
     int carrier;            // subtract the carrier mean
-    int rot_p, rot_q;       // rotation exp(-2 pi i (p g mod q)/q); q == 0 -> none
+    int rot_p, rot_q;       // rotation exp(-2 pi i (p g mod q)/q); q == 0 -> rot_step
     const float2* rot_tab;
+    unsigned long long rot_step;   // general tone: exp(-2 pi i (g rot_step mod 2^64)/2^64); 0 -> none
     int mirror;
     const float2* h_even;   // H at kept index 2m'  (8192)
     const float2* h_odd;    // H at kept index 2m'+1 (8192)
@@ -117,6 +118,8 @@ __device__ __forceinline__ float2 static_input(const K2Params& p, const BlockIn&
                                       static_cast<unsigned>(p.rot_q), b.inv_q);
             const float2 r = (p.rot_q <= kRotMax) ? rot_s[a] : __ldg(p.rot_tab + a);
             mr = cmul(mr, r);
+        } else if (p.rot_step) {
+            mr = cmul(mr, rot_phase_fast(static_cast<unsigned long long>(g) * p.rot_step));
         }
         if (p.mirror) mr = cconj(mr);
         v = csub(v, mr);
@@ -207,6 +210,11 @@ __device__ __forceinline__ void k2_load_column_ab(const K2Params& p, const Block
                 c0 = cmul(c0, rot_s[a0]);
                 c1 = cmul(c1, rot_s[a1]);
                 st = rot_s[s1024];
+            } else if (p.rot_step) {
+                const unsigned long long ph0 = static_cast<unsigned long long>(b.base + j) * p.rot_step;
+                c0 = cmul(c0, rot_phase_fast(ph0));
+                c1 = cmul(c1, rot_phase_fast(ph0 + 16384ull * p.rot_step));
+                st = rot_phase_fast(1024ull * p.rot_step);
             }
             ca = cadd(c0, c1);
             cb = csub(c0, c1);
@@ -511,6 +519,7 @@ static int k2_plan(const kk_k2_job& j, K2Params& p, K2Range (&r)[3]) {
     p.rot_p = j.rot_p;
     p.rot_q = j.rot_q;
     p.rot_tab = static_cast<const float2*>(j.rot_tab);
+    p.rot_step = j.rot_q > 0 ? 0ull : j.rot_step;
     p.mirror = j.mirror;
     p.h_even = static_cast<const float2*>(j.h_even);
     p.h_odd = static_cast<const float2*>(j.h_odd);
@@ -550,8 +559,9 @@ static int k2_attrs() {
 
 extern "C" int kk_static_blocks(const void* z, int64_t z_index0, int64_t hb0, int64_t n_blocks,
                                 int64_t valid_end, const void* seg_mean, int64_t seg_index0, int seg_len,
-                                int carrier, int rot_p, int rot_q, const void* rot_tab, int mirror,
-                                const void* h_even, const void* h_odd, void* out, void* stream) {
+                                int carrier, int rot_p, int rot_q, const void* rot_tab,
+                                unsigned long long rot_step, int mirror, const void* h_even, const void* h_odd,
+                                void* out, void* stream) {
     using namespace kk;
     clear_error();
     if (n_blocks <= 0) return KK_OK;
@@ -559,7 +569,7 @@ extern "C" int kk_static_blocks(const void* z, int64_t z_index0, int64_t hb0, in
     if (!tw) return KK_ERR_CUDA;
     if (int rc = k2_attrs()) return rc;
     const kk_k2_job j = {z, z_index0, hb0, n_blocks, valid_end, seg_mean, seg_index0, seg_len, carrier, rot_p,
-                         rot_q, rot_tab, mirror, h_even, h_odd, out};
+                         rot_q, rot_tab, rot_step, mirror, h_even, h_odd, out};
     K2Params p;
     K2Range r[3];
     if (int rc = k2_plan(j, p, r)) return rc;

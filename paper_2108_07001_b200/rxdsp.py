@@ -237,19 +237,24 @@ def _device_const(kind: str, a: np.ndarray, dev):
 
 
 def _tone_rotation(tone_hz: float, fs: float):
-    """Exact rational form p/q of tone/fs for the phase-continuous downshift
-    exp(-2 pi i (p g mod q)/q) (sigcore.py:297-298 computes the same phase
-    in float64; the integer form stays exact at any stream index)."""
+    """Phase-continuous downshift exp(-2 pi i tone g / fs) at global sample g
+    (sigcore.py frequency_shift :286-299 computes the phase in float64):
+    (p, q, table, 0) for tone/fs = p/q exactly with q <= 1024 (integer
+    phase p g mod q, exact table entries), else (0, 0, None, step) with
+    step = tone/fs (mod 1) as a 64-bit fixed-point fraction (phase g*step
+    mod 2^64: exact at any stream index, any tone)."""
     if tone_hz == 0.0:
-        return 0, 0, None
-    fr = Fraction(tone_hz / fs).limit_denominator(1024)
-    if abs(float(fr) - tone_hz / fs) > 1e-12:
-        raise ParameterError("tone_freq_hz / adc_rate_hz must be a rational p/q with q <= 1024")
-    q = fr.denominator
-    p = fr.numerator % q
-    a = np.arange(q)
-    tab = np.exp(-2j * np.pi * a / q).astype(np.complex64)
-    return p, q, tab
+        return 0, 0, None, 0
+    r = tone_hz / fs
+    fr = Fraction(r).limit_denominator(1024)
+    if abs(float(fr) - r) <= 1e-15 * max(1.0, abs(r)):
+        q = fr.denominator
+        p = fr.numerator % q
+        a = np.arange(q)
+        tab = np.exp(-2j * np.pi * a / q).astype(np.complex64)
+        return p, q, tab, 0
+    step = int(round((Fraction(r) % 1) * (1 << 64))) % (1 << 64)
+    return 0, 0, None, step
 
 
 _RESP_CACHE: dict = {}
@@ -465,7 +470,7 @@ def kk_reconstruct(current, plan: BlockPlan, state: dict | None = None, clamp_re
     # log/exp/sincos; the pipeline uses the SFU approximations)
     _lib.call("kk_reconstruct_pairs", dt | _lib.KK_DTYPE_PRECISE, _ptr(x), sc, float(clamp_rel), n_hops,
               _ptr(su), _ptr(sa), _ptr(sd),
-              _ptr(nu), _ptr(na), _ptr(nd), _ptr(out), _ptr(hs), _ptr(hd), _ptr(cl), 0, 0, 0, None, 0,
+              _ptr(nu), _ptr(na), _ptr(nd), _ptr(out), _ptr(hs), _ptr(hd), _ptr(cl), 0, 0, 0, None, 0, 0,
               _stream(dev))
     new_state = {"u_tail": nu.cpu().numpy().astype(np.float64), "a_hist": na.cpu().numpy().astype(np.float64),
                  "dead_hist": nd.cpu().numpy().astype(bool)}
@@ -621,7 +626,7 @@ def static_equalize_and_resample(field: ComplexSignal, static_taps: FirFilter, p
     nb = nx // hop
     out = torch.empty(nb * (hop // 2), dtype=torch.complex64, device=dev)
     # global indexing: tail = [0, hop), x = [hop, hop + nx); blocks hb = 1..nb
-    _lib.call("kk_static_blocks", _ptr(z), 0, 1, nb, hop + nx, None, 0, 0, 0, 0, 0, None, 0,
+    _lib.call("kk_static_blocks", _ptr(z), 0, 1, nb, hop + nx, None, 0, 0, 0, 0, 0, None, 0, 0,
               _ptr(he), _ptr(ho), _ptr(out), _stream(dev))
     new_tail = xx[-hop:]
     if device_output:
@@ -777,8 +782,8 @@ class RxPipeline:
         self._aa_delay = cfg.static_plan.fft_size // 4
         self._kept, self._resp = _static_response(taps, cfg.static_plan, cfg.adc_rate_hz, cfg.aa_edge, self._aa_delay)
         self._h_even, self._h_odd = _h_split(self._resp, self.dev, cached=True)
-        p, q, tab = _tone_rotation(cfg.tone_freq_hz, cfg.adc_rate_hz)
-        self._rot_p, self._rot_q = p, q
+        p, q, tab, step = _tone_rotation(cfg.tone_freq_hz, cfg.adc_rate_hz)
+        self._rot_p, self._rot_q, self._rot_step = p, q, step
         self._rot_tab = _device_const("rot", tab, self.dev) if tab is not None else None
         self._spec = make_constellation(cfg.constellation_order)
         self._tables = slicer_tables(cfg.constellation_order)
@@ -939,7 +944,7 @@ class RxPipeline:
         self._kk_pending = (self._hs.end, self._clamped * 1)       # (a kernel, not a D2D memcpy)
         return _lib.K1Job(_ptr(chunk), float(self._raw_scale), 1e-12, n_hops, _ptr(su), _ptr(sa), _ptr(sd),
                           _ptr(nu), _ptr(na), _ptr(nd), _ptr(out), _ptr(hs), _ptr(hd), _ptr(self._clamped), g0,
-                          self._rot_p, self._rot_q, _ptr(self._rot_tab), int(bool(self.cfg.mirror)))
+                          self._rot_p, self._rot_q, _ptr(self._rot_tab), self._rot_step, int(bool(self.cfg.mirror)))
 
     def _kk_commit(self, n_hops):
         hop = self.cfg.kk_plan.hop
@@ -956,7 +961,7 @@ class RxPipeline:
         j = self._kk_job(chunk, n_hops)
         _lib.call("kk_reconstruct_pairs", self._raw_dt, j.in_, j.in_scale, j.clamp_rel, j.n_hops, j.st_u, j.st_a,
                   j.st_dead, j.new_u, j.new_a, j.new_dead, j.out, j.hop_sum, j.hop_dead, j.clamped, j.n0_global,
-                  j.rot_p, j.rot_q, j.rot_tab, j.mirror, _stream(self.dev))
+                  j.rot_p, j.rot_q, j.rot_tab, j.rot_step, j.mirror, _stream(self.dev))
         self._kk_commit(n_hops)
 
     def _run_carrier(self, flush):
@@ -996,7 +1001,8 @@ class RxPipeline:
         self._static_pending = (n, hb_end)
         return _lib.K2Job(_ptr(self._z.buf), self._z.base, self._hb_next, n, c_end, _ptr(self._seg.buf),
                           self._seg.base, seg, int(bool(self.cfg.carrier_removal)), self._rot_p, self._rot_q,
-                          _ptr(self._rot_tab), int(bool(self.cfg.mirror)), _ptr(self._h_even), _ptr(self._h_odd),
+                          _ptr(self._rot_tab), self._rot_step, int(bool(self.cfg.mirror)), _ptr(self._h_even),
+                          _ptr(self._h_odd),
                           _ptr(out))
 
     def _static_commit(self):
@@ -1012,7 +1018,7 @@ class RxPipeline:
         if j is None:
             return
         _lib.call("kk_static_blocks", j.z, j.z_index0, j.hb0, j.n_blocks, j.valid_end, j.seg_mean, j.seg_index0,
-                  j.seg_len, j.carrier, j.rot_p, j.rot_q, j.rot_tab, j.mirror, j.h_even, j.h_odd, j.out,
+                  j.seg_len, j.carrier, j.rot_p, j.rot_q, j.rot_tab, j.rot_step, j.mirror, j.h_even, j.h_odd, j.out,
                   _stream(self.dev))
         self._static_commit()
 

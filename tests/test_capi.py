@@ -20,7 +20,7 @@ def test_library_builds_and_loads():
 
     build.build()
     lib = _lib.load()
-    assert lib.kk_version() == 1
+    assert lib.kk_version() == 2
 
 
 def test_exports_match_header():
@@ -43,7 +43,7 @@ def test_last_error_and_status_mapping():
     # parameter validation happens before any device work
     with pytest.raises(ParameterError):
         _lib.call("kk_reconstruct_pairs", 0, None, 1.0, 1e-12, 0, None, None, None, None, None, None, None,
-                  None, None, None, 0, 0, 0, None, 0, None)
+                  None, None, None, 0, 0, 0, None, 0, 0, None)
     assert b"n_hops" in lib.kk_last_error()
 
 

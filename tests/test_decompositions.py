@@ -125,11 +125,29 @@ def test_twiddle_tables_and_chains():
 
 
 def test_tone_rotation_is_exact_rational():
-    p, q, tab = _tone_rotation(0.516e9, 4e9)
-    assert (p, q) == (129, 1000)
+    p, q, tab, step = _tone_rotation(0.516e9, 4e9)
+    assert (p, q, step) == (129, 1000, 0)
     n = np.array([0, 1, 999, 1000, 2 ** 30 + 12345, 2 ** 40 + 7])
     exact = np.exp(-2j * np.pi * ((p * (n % q)) % q) / q)
     assert np.max(np.abs(tab[(p * (n % q)) % q] - exact)) < 1e-7
+
+
+@pytest.mark.parametrize("tone", [0.5123456789e9, 0.516e9 + 1.0, -0.3e9 + 0.123, 1.2345e9])
+def test_tone_rotation_general_fixed_point(tone):
+    """Tones that are not p/q with q <= 1024: a 64-bit fixed-point phase step
+    (K1/K2 compute exp(-2 pi i (g step mod 2^64) / 2^64)); the phase equals
+    the float64 phase of sigcore.py frequency_shift :297-298 to ~1e-7 rad at
+    g ~ 2^30 (the float64 reference's own rounding)."""
+    from fractions import Fraction
+
+    p, q, tab, step = _tone_rotation(tone, 4e9)
+    assert q == 0 and tab is None and 0 < step < 2 ** 64
+    for g in (0, 1, 12345, 2 ** 30 + 777, 2 ** 36 + 5):
+        ph = (g * step) % 2 ** 64
+        cyc = ph / 2 ** 64
+        exact = (Fraction(tone) / Fraction(4e9) * g) % 1
+        d = abs(cyc - float(exact))
+        assert min(d, 1 - d) * 2 * np.pi < 1e-9 * max(1, g / 2 ** 20)
 
 
 def test_wl_taps_real_form_roundtrip():

@@ -897,3 +897,49 @@ def test_run_sweep_cspr_vs_reference(tmp_path):
         print(r["value"], r["ber"], ref["ber"])
         assert max(ref["ber"], 1e-4) / 3 < max(r["ber"], 1e-4) < 3 * max(ref["ber"], 1e-4)
     assert len(res["summary"]) == 1
+
+
+def test_general_tone_fixed_point_rotation():
+    """Tones that are not p/q with q <= 1024 (the downshift of any tone,
+    sigcore.py frequency_shift :286-299): K1 / K2 rotate by the 64-bit
+    fixed-point phase g*step.  (1) The shipped tone forced through that path
+    gives the rational path's outputs to fp32 rounding; (2) a tone 2.5 Hz off
+    any small-denominator rational matches the oracle run with the same tone
+    (sync offset, decisions, soft outputs)."""
+    import dataclasses
+    from fractions import Fraction
+
+    cap = load_capture("c4_qpsk_10000km_cspr10")
+    syms = cap.symbols()
+    cfg = cap.pipeline_config()
+
+    def run(cfg, force_step=None):
+        orig = rxdsp._tone_rotation
+        if force_step is not None:
+            rxdsp._tone_rotation = lambda t, fs: (0, 0, None, force_step)
+        try:
+            pipe = rxdsp.RxPipeline(cfg, reference_symbols=syms)
+            pipe.feed(AdcCodes(cap.adc_h, cap.half_lsb))
+            dec, soft = pipe.finish()
+        finally:
+            rxdsp._tone_rotation = orig
+        return pipe, dec, soft
+
+    p0, d0, s0 = run(cfg)
+    step = int(round(Fraction(129, 1000) * (1 << 64)))
+    p1, d1, s1 = run(cfg, force_step=step)
+    assert p1.sync_offset == p0.sync_offset
+    assert np.mean(to_idx(d1, 4) == to_idx(d0, 4)) >= DEC_AGREE
+    assert rel_l2(s1, s0) < 1e-4
+
+    tone = 0.516e9 + 2.5
+    assert rxdsp._tone_rotation(tone, 4e9)[1] == 0           # general path
+    cfg2 = dataclasses.replace(cfg, tone_freq_hz=tone)
+    p2, d2, s2 = run(cfg2)
+    ocfg = ko.OracleConfig(taps=cap.taps, tone_freq_hz=tone, mu=cap.meta["mu"],
+                           startup_symbols=cap.meta["startup_symbols"])
+    ref, d_ref, s_ref = ko.receive(cap.adc_float(), ocfg, syms, cap.meta["buffer_len"])
+    assert p2.sync_offset == ref.sync_offset
+    assert len(d2) == len(d_ref)
+    assert np.mean(to_idx(d2, 4) == to_idx(d_ref, 4)) >= DEC_AGREE
+    assert rel_l2(s2, s_ref) < 1e-3

@@ -37,7 +37,7 @@ def main():
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
         _lib.call("kk_reconstruct_pairs", 0, p(x), cap.half_lsb, 1e-12, nh, p(su), p(sa), p(sd), p(nu), p(na), p(nd),
-                  p(out), p(hs), p(hd), p(cl), 0, 129, 1000, p(tab), 1, s)
+                  p(out), p(hs), p(hd), p(cl), 0, 129, 1000, p(tab), 0, 1, s)
         e1.record()
         torch.cuda.synchronize()
         if i:
