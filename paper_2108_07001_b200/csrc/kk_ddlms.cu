@@ -1510,6 +1510,68 @@ __global__ void xcorr_kernel(const float2* __restrict__ head, int64_t n_head, co
     mag[t] = sqrt(R * R + I * I);
 }
 
+// Tiled form: a CTA owns kXcTile consecutive lags of one parity (thread t:
+// lags t + 256 m, m < 4) and one kXcChunk-symbol segment of the reference
+// (blockIdx.z), both staged in shared memory, so each head sample is read
+// from L2 once per tile instead of once per lag (the per-lag kernel above
+// re-read the window for every lag, ~2 GB of L1/L2 loads per stream head),
+// and a 2^16-lag head gives 512 CTAs.  fp32 sums within a segment; the
+// segments' float64 partials are combined in a fixed order (deterministic).
+constexpr int kXcThreads = 256, kXcPer = 4, kXcTile = kXcThreads * kXcPer, kXcChunk = 512;
+__global__ void __launch_bounds__(kXcThreads) xcorr_tiled_kernel(const float2* __restrict__ head, int64_t n_head,
+                                                                 const float2* __restrict__ ref, int n_ref,
+                                                                 int64_t n_lag0, int64_t n_lag1,
+                                                                 double2* __restrict__ part) {
+    __shared__ float2 sref[kXcChunk];
+    __shared__ float2 sz[kXcTile + kXcChunk];
+    const int parity = blockIdx.y;
+    const int64_t nl = parity ? n_lag1 : n_lag0;
+    const int64_t k0 = int64_t(blockIdx.x) * kXcTile;
+    if (k0 >= nl) return;
+    const int t = threadIdx.x;
+    const int i0 = blockIdx.z * kXcChunk;
+    const int nc = min(kXcChunk, n_ref - i0);
+    for (int c = t; c < kXcChunk; c += kXcThreads) sref[c] = c < nc ? ref[i0 + c] : make_float2(0.f, 0.f);
+    for (int j = t; j < kXcTile + kXcChunk; j += kXcThreads) {
+        const int64_t si = parity + 2 * (k0 + i0 + j);
+        sz[j] = si < n_head ? __ldg(head + si) : make_float2(0.f, 0.f);
+    }
+    __syncthreads();
+    float re[kXcPer], im[kXcPer];
+#pragma unroll
+    for (int m = 0; m < kXcPer; ++m) re[m] = im[m] = 0.f;
+#pragma unroll 8
+    for (int c = 0; c < kXcChunk; ++c) {
+        const float2 r = sref[c];
+#pragma unroll
+        for (int m = 0; m < kXcPer; ++m) {
+            const float2 z = sz[t + kXcThreads * m + c];
+            re[m] = fmaf(z.x, r.x, fmaf(z.y, r.y, re[m]));      // z * conj(r)
+            im[m] = fmaf(z.y, r.x, fmaf(-z.x, r.y, im[m]));
+        }
+    }
+    // part[segment][lag], lags of both parities concatenated (parity 1 at n_lag0)
+    double2* out = part + int64_t(blockIdx.z) * (n_lag0 + n_lag1) + (parity ? n_lag0 : 0);
+#pragma unroll
+    for (int m = 0; m < kXcPer; ++m) {
+        const int64_t k = k0 + t + kXcThreads * m;
+        if (k < nl) out[k] = make_double2(re[m], im[m]);
+    }
+}
+
+__global__ void xcorr_combine_kernel(const double2* __restrict__ part, int n_seg, int64_t n_lags,
+                                     double* __restrict__ mag) {
+    for (int64_t k = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; k < n_lags; k += int64_t(gridDim.x) * blockDim.x) {
+        double R = 0.0, I = 0.0;
+        for (int sgm = 0; sgm < n_seg; ++sgm) {
+            const double2 v = part[int64_t(sgm) * n_lags + k];
+            R += v.x;
+            I += v.y;
+        }
+        mag[k] = sqrt(R * R + I * I);
+    }
+}
+
 __global__ void sync_reduce_kernel(const double* __restrict__ mag, int64_t n_lag0, int64_t n_lag1,
                                    const float2* __restrict__ head, int64_t n_head, int64_t skip,
                                    double* __restrict__ res) {
@@ -2733,24 +2795,49 @@ extern "C" int kk_ddlms_solve_async(const void* x, int64_t nsym, float scale, co
 
 // enqueue the sync kernels; the 4 result doubles land in `res` (device or
 // UVA-mapped pinned host memory)
+// sync scratch (doubles): [mag: n_lags rounded to 32 | result: 32 | the
+// tiled correlation's per-segment partials: n_seg * n_lags double2]
+static inline int64_t sync_part_offset(int64_t n_lags) { return ((n_lags + 31) / 32) * 32 + 32; }
+static inline size_t sync_scratch_bytes(int64_t n_lags, int n_ref) {
+    const int64_t n_seg = n_ref > 0 ? (n_ref + kXcChunk - 1) / kXcChunk : 0;
+    return static_cast<size_t>(sync_part_offset(n_lags) + 2 * n_seg * n_lags) * sizeof(double) + 256;
+}
+
 static int symbol_sync_launch(const void* head, int64_t n_head, const void* ref, int n_ref, int64_t skip,
                               double* res_out, void* scratch, size_t scratch_bytes, cudaStream_t s) {
     const int64_t l0 = (n_head + 1) / 2, l1 = n_head / 2;
     const int64_t nl0 = (ref && n_ref > 0 && l0 >= n_ref) ? l0 - n_ref + 1 : 0;
     const int64_t nl1 = (ref && n_ref > 0 && l1 >= n_ref) ? l1 - n_ref + 1 : 0;
-    const size_t need = (nl0 + nl1 + 4) * sizeof(double) + 256;
+    const size_t need = sync_scratch_bytes(nl0 + nl1, n_ref);
     if (scratch_bytes < need) return set_error(KK_ERR_PARAM, "sync scratch too small");
     double* mag = static_cast<double*>(scratch);
     if (nl0 + nl1 > 0) {
-        const int th = 256;
-        const size_t sm = static_cast<size_t>(n_ref) * sizeof(float2);
-        if (sm > 48 * 1024 &&
-            cudaFuncSetAttribute(xcorr_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm)) !=
-                cudaSuccess)
-            return set_cuda_error("xcorr smem");
-        xcorr_kernel<<<static_cast<unsigned>((nl0 + nl1 + th - 1) / th), th, sm, s>>>(
-            static_cast<const float2*>(head), n_head, static_cast<const float2*>(ref), n_ref, nl0, nl1, mag);
-        if (int rc = check_launch("xcorr_kernel")) return rc;
+#ifndef KK_XCORR_TILED
+#define KK_XCORR_TILED 1
+#endif
+        if (KK_XCORR_TILED) {
+            const int n_seg = (n_ref + kXcChunk - 1) / kXcChunk;
+            double2* part = reinterpret_cast<double2*>(mag + sync_part_offset(nl0 + nl1));
+            const dim3 grid(static_cast<unsigned>((std::max(nl0, nl1) + kXcTile - 1) / kXcTile), 2,
+                            static_cast<unsigned>(n_seg));
+            xcorr_tiled_kernel<<<grid, kXcThreads, 0, s>>>(static_cast<const float2*>(head), n_head,
+                                                           static_cast<const float2*>(ref), n_ref, nl0, nl1, part);
+            if (int rc = check_launch("xcorr_tiled_kernel")) return rc;
+            const int64_t nl = nl0 + nl1;
+            xcorr_combine_kernel<<<static_cast<unsigned>(std::min<int64_t>((nl + 255) / 256, 1184)), 256, 0, s>>>(
+                part, n_seg, nl, mag);
+            if (int rc = check_launch("xcorr_combine_kernel")) return rc;
+        } else {
+            const int th = 256;
+            const size_t sm = static_cast<size_t>(n_ref) * sizeof(float2);
+            if (sm > 48 * 1024 &&
+                cudaFuncSetAttribute(xcorr_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     static_cast<int>(sm)) != cudaSuccess)
+                return set_cuda_error("xcorr smem");
+            xcorr_kernel<<<static_cast<unsigned>((nl0 + nl1 + th - 1) / th), th, sm, s>>>(
+                static_cast<const float2*>(head), n_head, static_cast<const float2*>(ref), n_ref, nl0, nl1, mag);
+            if (int rc = check_launch("xcorr_kernel")) return rc;
+        }
     }
     sync_reduce_kernel<<<1, 1024, 0, s>>>(mag, nl0, nl1, static_cast<const float2*>(head), n_head, skip, res_out);
     return check_launch("sync_reduce_kernel");
@@ -2780,7 +2867,7 @@ extern "C" size_t kk_symbol_sync_scratch_bytes(int64_t n_head, int n_ref) {
     const int64_t l0 = (n_head + 1) / 2, l1 = n_head / 2;
     const int64_t nl0 = (n_ref > 0 && l0 >= n_ref) ? l0 - n_ref + 1 : 0;
     const int64_t nl1 = (n_ref > 0 && l1 >= n_ref) ? l1 - n_ref + 1 : 0;
-    return static_cast<size_t>(((nl0 + nl1 + 31) / 32) * 32 + 4) * sizeof(double) + 256;
+    return sync_scratch_bytes(nl0 + nl1, n_ref);
 }
 
 extern "C" int kk_bit_errors(const uint8_t* labels, const uint8_t* ref_idx, int64_t n, const uint8_t* point_label,
