@@ -119,6 +119,15 @@ typedef struct {
 } kk_k1_job;
 int kk_reconstruct_pairs_batch(int in_dtype, const kk_k1_job *jobs, int n_jobs, void *stream);
 
+/*
+ * Standalone downshift (downshift_dc rx:247-257 = frequency_shift
+ * sigcore.py:286-299 by -tone), complex128 in/out (x == y allowed):
+ * y[i] = x[i] exp(j ((two_pi_df (start_index + i)) / fs)), two_pi_df =
+ * 2 pi delta_f as the caller forms it.
+ */
+int kk_frequency_shift(const void *x, void *y, int64_t n, double two_pi_df, double fs, int64_t start_index,
+                       void *stream);
+
 /* packed 12-bit codes (KK_DTYPE_P12 layout, n even) -> int16 odd codes h */
 int kk_unpack12(const uint8_t *in, int64_t n, int16_t *out, void *stream);
 

@@ -47,6 +47,7 @@ _SIGS = {
     "kk_reconstruct_pairs": ([_I, _P, _F, _F, _I64, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _I64, _I, _I, _P, _U64, _I,
                               _P], _I),
     "kk_unpack12": ([_P, _I64, _P, _P], _I),
+    "kk_frequency_shift": ([_P, _P, _I64, _D, _D, _I64, _P], _I),
     "kk_carrier_means": ([_P, _I64, _I, _I64, _I64, _I, _P, _P], _I),
     "kk_static_blocks": ([_P, _I64, _I64, _I64, _I64, _P, _I64, _I, _I, _I, _I, _P, _U64, _I, _P, _P, _P, _P], _I),
     "kk_symbol_sync_scratch_bytes": ([_I64, _I], _SZ),

@@ -531,6 +531,41 @@ __global__ void unpack12_kernel(const uint8_t* __restrict__ in, int64_t n, int16
 }
 }  // namespace kk
 
+// ---------------------------------------------------------------------------
+// Standalone downshift (the functional downshift_dc, rx:247-257 ->
+// sigcore.py frequency_shift :286-299), complex128: y[i] = x[i] *
+// exp(j theta), theta = ((2 pi df) * n) * (1 / fs) with n = start + i in
+// float64 -- numpy evaluates the reference's `2j*pi*df*n / fs` as a complex
+// quotient, i.e. times the reciprocal of fs -- and the complex product without
+// FMA contraction, as numpy forms it.  (The pipeline's downshift is fused in
+// K1.)
+// ---------------------------------------------------------------------------
+namespace kk {
+__global__ void frequency_shift_kernel(const double2* __restrict__ x, double2* __restrict__ y, int64_t n,
+                                       double two_pi_df, double inv_fs, int64_t start) {
+    for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
+        const double th = __dmul_rn(__dmul_rn(two_pi_df, static_cast<double>(start + i)), inv_fs);
+        double s, c;
+        sincos(th, &s, &c);
+        const double2 v = x[i];
+        y[i] = make_double2(__dsub_rn(__dmul_rn(v.x, c), __dmul_rn(v.y, s)),
+                            __dadd_rn(__dmul_rn(v.x, s), __dmul_rn(v.y, c)));
+    }
+}
+}  // namespace kk
+
+extern "C" int kk_frequency_shift(const void* x, void* y, int64_t n, double two_pi_df, double fs, int64_t start_index,
+                                  void* stream) {
+    using namespace kk;
+    clear_error();
+    if (n < 0 || !(fs > 0) || (n > 0 && (!x || !y))) return set_error(KK_ERR_PARAM, "kk_frequency_shift: bad arguments");
+    if (n == 0) return KK_OK;
+    const int64_t blocks = std::min<int64_t>((n + 255) / 256, 148 * 16);
+    frequency_shift_kernel<<<static_cast<unsigned>(blocks), 256, 0, static_cast<cudaStream_t>(stream)>>>(
+        static_cast<const double2*>(x), static_cast<double2*>(y), n, two_pi_df, 1.0 / fs, start_index);
+    return check_launch("frequency_shift_kernel");
+}
+
 extern "C" int kk_unpack12(const uint8_t* in, int64_t n, int16_t* out, void* stream) {
     using namespace kk;
     clear_error();

@@ -482,7 +482,8 @@ def kk_reconstruct(current, plan: BlockPlan, state: dict | None = None, clamp_re
 def downshift_dc(field: ComplexSignal, tone_freq_hz: float, start_index: int = 0) -> ComplexSignal:
     """Shift the payload band to DC (rx:247-257 -> sigcore.py:286-299),
     phase-continuous via start_index.  In the pipeline this is fused into K1;
-    the standalone form evaluates the reference's float64 phase on the device."""
+    the standalone form is kk_frequency_shift: the reference's float64 phase
+    and complex product on the device."""
     torch = _torch()
     fs = field.sample_rate_hz
     if tone_freq_hz == 0 and start_index == 0:
@@ -494,9 +495,11 @@ def downshift_dc(field: ComplexSignal, tone_freq_hz: float, start_index: int = 0
     s = field.samples
     was_np = not isinstance(s, torch.Tensor)
     x = torch.as_tensor(np.asarray(s, np.complex128)) if was_np else s
-    x = x.to(dev, torch.complex128)
-    n = torch.arange(start_index, start_index + x.shape[0], dtype=torch.float64, device=dev)
-    y = x * torch.exp(2j * np.pi * (-tone_freq_hz) * n / fs)
+    x = x.to(dev, torch.complex128).contiguous()
+    y = torch.empty_like(x)
+    # frequency_shift by -tone: theta = ((2 pi (-tone)) n) / fs (sigcore.py:297)
+    _lib.call("kk_frequency_shift", _ptr(x), _ptr(y), int(x.shape[0]), float(2 * np.pi * (-tone_freq_hz)), float(fs),
+              int(start_index), _stream(dev))
     return ComplexSignal(y.cpu().numpy() if was_np else y, fs)
 
 

@@ -943,3 +943,16 @@ def test_general_tone_fixed_point_rotation():
     assert len(d2) == len(d_ref)
     assert np.mean(to_idx(d2, 4) == to_idx(d_ref, 4)) >= DEC_AGREE
     assert rel_l2(s2, s_ref) < 1e-3
+
+
+@pytest.mark.parametrize("tone,start", [(0.516e9, 0), (0.516e9, 2 ** 33 + 17), (0.5123456789e9, 12345), (-1.1e9, 7)])
+def test_downshift_dc_kernel_vs_oracle(tone, start):
+    """The standalone downshift (rx:247-257 -> sigcore.py frequency_shift
+    :286-299) on kk_frequency_shift: the reference's float64 phase and
+    product, equal to the oracle's numpy evaluation to float64 rounding of
+    sin/cos (1 ulp)."""
+    rng = np.random.default_rng(4)
+    x = rng.standard_normal(100_003) + 1j * rng.standard_normal(100_003)
+    got = rxdsp.downshift_dc(ComplexSignal(x, 4e9), tone, start_index=start).samples
+    want = ko.freq_shift(x, -tone, 4e9, start)
+    assert np.max(np.abs(got - want)) <= 1e-15 * np.max(np.abs(x))
