@@ -817,7 +817,9 @@ class RxPipeline:
         self._hd = _DevStream(torch.uint8, self.dev, start=stream_offset // hop)        # per-hop dead flags
         self._seg = _DevStream(torch.complex64, self.dev, start=stream_offset // seg)   # carrier means, global segment
         self._y2 = _DevStream(torch.complex64, self.dev, start=hb0 * (cfg.static_plan.hop // 2))  # static out, 2-sps
-        self._clamped = torch.zeros(1, dtype=torch.int64, device=self.dev)
+        # clamped-sample count per fed chunk: K1 adds into the chunk's own
+        # slot, so the per-chunk diagnostics need no device snapshots
+        self._clamped_log = torch.zeros(256, dtype=torch.int64, device=self.dev)
         self._c_end = stream_offset
         self._hb_next = hb0
         self._flushed = False
@@ -858,6 +860,7 @@ class RxPipeline:
 
         self._out: list[tuple] = []
         self._pending_diag: list[tuple] = []
+        self._diag_frames: dict = {}      # chunk -> DDLMS frames submitted by the end of its feed
         self._diagnostics: list[dict] = []
         self._events: list[tuple] = []
         self._stage_acc = {"kk": 0.0, "carrier": 0.0, "downshift": 0.0, "static": 0.0, "ddlms": 0.0}
@@ -883,12 +886,30 @@ class RxPipeline:
 
     @property
     def diagnostics(self) -> list:
+        """One record per fed chunk (rx:663-668): clamped samples (K1's per-
+        chunk counter slot), zero (dead) KK blocks, and whether the divergence
+        guard had frozen the taps by the end of the DDLMS frames that chunk
+        completed (frames are the DDLMS granularity here)."""
         torch = _torch()
-        for chunk, h0, n, cl0, cl1, frozen in self._pending_diag:
+        if not self._pending_diag:
+            return self._diagnostics
+        frames = self.ddlms_stats
+        frozen_after = []   # sticky: frozen after frame f
+        fz = False
+        for st in frames:
+            fz = fz or bool(st.get("frozen_end", False))
+            frozen_after.append(fz)
+        counts = self._clamped_log[: self._chunk_index + 1].cpu().tolist()
+        by_chunk: dict = {}      # chunk -> (first hop of the chunk, dead hops relative to it)
+        for chunk, h0, n in self._pending_diag:
             dead = self._hd.view(h0, h0 + n)
-            zb = torch.nonzero(dead).flatten().cpu().tolist()
-            self._diagnostics.append({"chunk": chunk, "clamped": int(cl1.item() - cl0.item()),
-                                      "zero_blocks": zb, "diverged": bool(frozen.item())})
+            first, lst = by_chunk.setdefault(chunk, (h0, []))
+            lst.extend((h0 - first + torch.nonzero(dead).flatten()).cpu().tolist())
+        for chunk in sorted(by_chunk):
+            nf = self._diag_frames.get(chunk, len(frames))
+            self._diagnostics.append({"chunk": chunk, "clamped": int(counts[chunk]) if chunk < len(counts) else 0,
+                                      "zero_blocks": sorted(set(by_chunk[chunk][1])),
+                                      "diverged": bool(frozen_after[nf - 1]) if nf > 0 else False})
         self._pending_diag = []
         return self._diagnostics
 
@@ -944,21 +965,25 @@ class RxPipeline:
         hd = self._hd.reserve(n_hops)
         su, sa, sd = self._kk_state[self._kk_cur]
         nu, na, nd = self._kk_state[1 - self._kk_cur]
-        self._kk_pending = (self._hs.end, self._clamped * 1)       # (a kernel, not a D2D memcpy)
+        self._kk_pending = self._hs.end
+        if self._chunk_index >= self._clamped_log.shape[0]:
+            grown = torch.zeros(2 * self._clamped_log.shape[0], dtype=torch.int64, device=self.dev)
+            grown[: self._clamped_log.shape[0]] = self._clamped_log
+            self._clamped_log = grown
+        clamped = self._clamped_log[self._chunk_index:]
         return _lib.K1Job(_ptr(chunk), float(self._raw_scale), 1e-12, n_hops, _ptr(su), _ptr(sa), _ptr(sd),
-                          _ptr(nu), _ptr(na), _ptr(nd), _ptr(out), _ptr(hs), _ptr(hd), _ptr(self._clamped), g0,
+                          _ptr(nu), _ptr(na), _ptr(nd), _ptr(out), _ptr(hs), _ptr(hd), _ptr(clamped), g0,
                           self._rot_p, self._rot_q, _ptr(self._rot_tab), self._rot_step, int(bool(self.cfg.mirror)))
 
     def _kk_commit(self, n_hops):
         hop = self.cfg.kk_plan.hop
-        h0, clamped_before = self._kk_pending
+        h0 = self._kk_pending
         self._kk_cur = 1 - self._kk_cur
         self._z.commit(n_hops * hop)
         self._hs.commit(n_hops)
         self._hd.commit(n_hops)
         # diagnostics are materialised lazily (no host sync per feed)
-        self._pending_diag.append((self._chunk_index, h0, n_hops, clamped_before, self._clamped * 1,
-                                   self._state_dev[0] * 1))
+        self._pending_diag.append((self._chunk_index, h0, n_hops))
 
     def _run_kk(self, chunk, n_hops):
         j = self._kk_job(chunk, n_hops)
@@ -1141,11 +1166,15 @@ class RxPipeline:
             tv = self._ref_dev[k0:k0 + n_train] if n_train > 0 else None
             _seq_ddlms(xv, nsym, self._eq_scale, d, tb.order, self._wg_dev, self._state_dev, tv, n_train, labels,
                        soft, None, self.dev)
+            stats["_frozen"] = self._state_dev[:1].clone()     # one small copy per frame (diagnostics)
         return labels, soft, n_train, stats
 
     @staticmethod
     def _materialise(stats: dict) -> dict:
         """Fill a frame's statistics from its device-written record."""
+        fz = stats.pop("_frozen", None)
+        if fz is not None:
+            stats["frozen_end"] = bool(fz.item())
         pend = stats.pop("_pending", None)
         if pend is None:
             return stats
@@ -1158,6 +1187,7 @@ class RxPipeline:
                      T_start=[float(v) for v in T_start.cpu().numpy()])
         stats["mode"] = {1: "sequential(guard)", 2: "solve+chain(not converged)", 3: "frozen(map)",
                          4: "solve+freeze(map)"}.get(stats["fallback"], stats["mode"])
+        stats["frozen_end"] = stats["fallback"] in (1, 3, 4)   # the guard froze the taps in / before this frame
         return stats
 
     @property
@@ -1446,6 +1476,7 @@ class RxPipeline:
             nv and torch.cuda.nvtx.range_pop()
         t4 = self._ev()
         self._events.append(("ddlms", t3, t4))
+        self._diag_frames[self._chunk_index] = len(self._stats) + len(self._jobs)
         self._chunk_index += 1
         if flush:
             self._flushed = True

@@ -33,14 +33,22 @@ st = torch.empty(3 << 29, dtype=torch.uint8, device="cuda")
 lib = _lib.load()
 marks = {}
 t_call = [0.0]
+spent = {}
+lastm = {}
 
 
 def wrap(name):
     f = getattr(lib, name)
 
     def g(*a):
-        marks.setdefault(name, time.perf_counter() - t_call[0])
-        return f(*a)
+        t0 = time.perf_counter()
+        marks.setdefault(name, t0 - t_call[0])
+        r = f(*a)
+        c, tt, mx = spent.get(name, (0, 0.0, 0.0))
+        d = time.perf_counter() - t0
+        spent[name] = (c + 1, tt + d, max(mx, d))
+        lastm[name] = t0 - t_call[0]
+        return r
     g.argtypes, g.restype = f.argtypes, f.restype
     setattr(lib, name, g)
 
@@ -56,6 +64,7 @@ def step():
 
 for i in range(4):
     marks.clear()
+    spent.clear()
     torch.cuda.synchronize()
     t_call[0] = time.perf_counter()
     pipe, bh, n = step()
@@ -63,6 +72,9 @@ for i in range(4):
     dt = time.perf_counter() - t_call[0]
     print(f"step {i}: {dt * 1e3:.1f} ms; first enqueue (ms after call): "
           + ", ".join(f"{k} {v * 1e3:.2f}" for k, v in sorted(marks.items(), key=lambda kv: kv[1])), flush=True)
+    print("   last enqueue (ms):", {k: round(v * 1e3, 2) for k, v in lastm.items()})
+    print("   host time in library calls:", {k: (c, round(tt * 1e3, 2), round(mx * 1e3, 2)) for k, (c, tt, mx) in
+                                         spent.items()}, flush=True)
     pipe.release_buffers()
 
 pr = cProfile.Profile()
@@ -73,3 +85,4 @@ torch.cuda.synchronize()
 pr.disable()
 pipe.release_buffers()
 pstats.Stats(pr).sort_stats("cumulative").print_stats(35)
+pstats.Stats(pr).sort_stats("tottime").print_stats(30)
