@@ -442,8 +442,6 @@ def kk_reconstruct(current, plan: BlockPlan, state: dict | None = None, clamp_re
     tensor; with device_output=True the field stays a complex64 CUDA tensor.
     """
     torch = _torch()
-    if plan.fft_size != KK_FFT:
-        raise ParameterError("the B200 KK kernel is built for kk_plan.fft_size == 1024")
     fs = getattr(current, "sample_rate_hz", 4e9)
     n = len(current) if isinstance(current, (AdcCodes, AdcPacked12)) else len(
         current.samples if is_signal(current) else current)
@@ -456,6 +454,8 @@ def kk_reconstruct(current, plan: BlockPlan, state: dict | None = None, clamp_re
     if state is None:
         state = {"u_tail": np.zeros(hop), "a_hist": np.zeros(hop // 2),
                  "dead_hist": np.zeros(hop // 2, dtype=bool)}
+    if plan.fft_size != KK_FFT:
+        return _kk_reconstruct_generic(x, dt, sc, n, plan.fft_size, state, clamp_rel, fs, dev, device_output)
     su = torch.as_tensor(np.asarray(state["u_tail"], np.float32), device=dev)
     sa = torch.as_tensor(np.asarray(state["a_hist"], np.float32), device=dev)
     sd = torch.as_tensor(np.asarray(state["dead_hist"], np.uint8), device=dev)
@@ -477,6 +477,84 @@ def kk_reconstruct(current, plan: BlockPlan, state: dict | None = None, clamp_re
     diag = {"clamped": int(cl.item()), "zero_blocks": torch.nonzero(hd).flatten().cpu().tolist()}
     field = out if device_output else out.cpu().numpy().astype(np.complex128)
     return ComplexSignal(field, fs), new_state, diag
+
+
+def _hilbert_full(nfft: int, dev):
+    """rx:170-181's rfft multiplier (-j, delayed by nfft/4, 0 at DC and
+    Nyquist) extended Hermitian to the full nfft-bin spectrum (complex128)."""
+    def make():
+        k = np.arange(nfft // 2 + 1)
+        m = np.full(nfft // 2 + 1, -1j, dtype=np.complex128)
+        m[0] = 0.0
+        m[-1] = 0.0
+        m = m * np.exp(-2j * np.pi * k * (nfft // 4) / nfft)
+        full = np.zeros(nfft, np.complex128)
+        full[: nfft // 2 + 1] = m
+        full[nfft // 2 + 1:] = np.conj(m[1: nfft // 2][::-1])
+        return full
+    return _device_const(f"hilbert_full_{nfft}", make(), dev)
+
+
+def _kk_reconstruct_generic(x, dt, sc, n: int, nfft: int, state: dict, clamp_rel: float, fs: float, dev,
+                            device_output: bool):
+    """kk_reconstruct for block sizes other than K1's 1024 (any power of two,
+    BlockPlan sc:121-147): the reference algorithm (rx:184-244) in float64 on
+    the device, the block transforms on the repo FFT (kk_fft, batched rows).
+    Not the streaming hot path."""
+    torch = _torch()
+    from .channel import fft as gfft, ifft as gifft
+
+    if nfft < 4 or nfft & (nfft - 1):
+        raise ParameterError("kk_plan.fft_size must be a power of two >= 4")
+    hop, half = nfft // 2, nfft // 4
+    if dt == _lib.KK_DTYPE_P12:
+        x, dt = _unpack12_dev(x, n, dev), _lib.KK_DTYPE_I16
+    xf = x.to(torch.float64) * (float(sc) if dt == _lib.KK_DTYPE_I16 else 1.0)
+    hops = xf[:n].reshape(-1, hop)
+    mean = hops.mean(dim=1)
+    dead = mean <= 0.0
+    thr = torch.where(dead, torch.ones_like(mean), clamp_rel * mean.abs())
+    clamped = int(((hops < thr[:, None]) & ~dead[:, None]).sum())
+    safe = torch.maximum(hops, thr[:, None])
+    safe[dead] = 1.0
+    flat = safe.reshape(-1)
+    amp = flat.sqrt()
+    u = 0.5 * flat.log()
+    dmask = dead.repeat_interleave(hop)
+    u_all = torch.cat([torch.as_tensor(np.asarray(state["u_tail"], np.float64), device=dev), u])
+    blocks = u_all.unfold(0, nfft, hop).to(torch.complex128).contiguous()
+    spec = gfft(blocks) * _hilbert_full(nfft, dev)
+    phi = gifft(spec).real[:, hop:].reshape(-1)
+    a_d = torch.cat([torch.as_tensor(np.asarray(state["a_hist"], np.float64), device=dev), amp])[:n]
+    d_d = torch.cat([torch.as_tensor(np.asarray(state["dead_hist"], bool), device=dev), dmask])[:n]
+    out = a_d * torch.exp(1j * phi)
+    out[d_d] = 0.0
+    new_state = {"u_tail": u[-hop:].cpu().numpy().copy(), "a_hist": amp[-half:].cpu().numpy().copy(),
+                 "dead_hist": dmask[-half:].cpu().numpy().copy()}
+    diag = {"clamped": clamped, "zero_blocks": torch.nonzero(dead).flatten().cpu().tolist()}
+    field = out.to(torch.complex64) if device_output else out.cpu().numpy()
+    return ComplexSignal(field, fs), new_state, diag
+
+
+def _unpack12_dev(x, n: int, dev):
+    torch = _torch()
+    out = torch.empty(n, dtype=torch.int16, device=dev)
+    _lib.call("kk_unpack12", _ptr(x), n, _ptr(out), _stream(dev))
+    return out
+
+
+def _static_generic(z, nb: int, n: int, hop: int, kept, h, dev):
+    """static_equalize_and_resample for block sizes other than K2's 32768
+    (rx:414-453 in float64 on the device, transforms on kk_fft): blocks of n
+    at hop n/2, kept bins x H, inverse of n/2 points, the second half kept."""
+    torch = _torch()
+    from .channel import fft as gfft, ifft as gifft
+
+    m = n // 2
+    blocks = z.unfold(0, n, hop)[:nb].contiguous()
+    kept_d = _device_const(f"kept_{n}", np.asarray(kept, np.int64), dev)
+    y = gifft((gfft(blocks)[:, kept_d] * h).contiguous()) * (m / n)
+    return y[:, m // 2:].reshape(-1)
 
 
 def downshift_dc(field: ComplexSignal, tone_freq_hz: float, start_index: int = 0) -> ComplexSignal:
@@ -606,8 +684,8 @@ def static_equalize_and_resample(field: ComplexSignal, static_taps: FirFilter, p
     if abs(static_taps.nominal_rate_hz - fs_in / 2.0) > 1e-3:
         raise ParameterError("static taps must be defined at half the input rate")
     n, hop = plan.fft_size, plan.hop
-    if n != STATIC_FFT:
-        raise ParameterError("the B200 static kernel is built for static_plan.fft_size == 32768")
+    if n < 8 or n & (n - 1):
+        raise ParameterError("static_plan.fft_size must be a power of two >= 8")
     if aa_delay is None:
         aa_delay = n // 4
     if aa_delay % 2 != 0:
@@ -621,7 +699,19 @@ def static_equalize_and_resample(field: ComplexSignal, static_taps: FirFilter, p
     if len(tail) != hop:
         raise ParameterError("tail length must equal plan.hop")
     dev = _device()
-    _, h = _static_response(static_taps, plan, fs_in, edge, aa_delay)
+    kept, h = _static_response(static_taps, plan, fs_in, edge, aa_delay)
+    if n != STATIC_FFT:   # other block sizes: float64 on the repo FFT (not the streaming hot path)
+        tx = tail if isinstance(tail, torch.Tensor) else torch.from_numpy(np.asarray(tail, np.complex128))
+        xx = x if isinstance(x, torch.Tensor) else torch.from_numpy(np.asarray(x, np.complex128))
+        z = torch.cat([tx.to(dev, torch.complex128), xx.to(dev, torch.complex128)])
+        hd = torch.as_tensor(np.asarray(h, np.complex128), device=dev)
+        out = _static_generic(z, nx // hop, n, hop, kept, hd, dev)
+        new_tail = xx[-hop:]
+        if device_output:
+            return ComplexSignal(out.to(torch.complex64), fs_in / 2.0), new_tail.to(dev)
+        return (ComplexSignal(out.cpu().numpy(), fs_in / 2.0),
+                np.asarray(new_tail.cpu().numpy() if isinstance(new_tail, torch.Tensor) else new_tail,
+                           dtype=np.complex128).copy())
     he, ho = _h_split(h, dev)
     tx = tail if isinstance(tail, torch.Tensor) else torch.from_numpy(np.asarray(tail, np.complex128))
     xx = x if isinstance(x, torch.Tensor) else torch.from_numpy(np.asarray(x, np.complex128))

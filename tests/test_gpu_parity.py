@@ -956,3 +956,46 @@ def test_downshift_dc_kernel_vs_oracle(tone, start):
     got = rxdsp.downshift_dc(ComplexSignal(x, 4e9), tone, start_index=start).samples
     want = ko.freq_shift(x, -tone, 4e9, start)
     assert np.max(np.abs(got - want)) <= 1e-15 * np.max(np.abs(x))
+
+
+@pytest.mark.parametrize("nfft", [256, 512, 2048, 4096])
+def test_kk_reconstruct_other_block_sizes_vs_oracle(nfft):
+    """Any power-of-two KK plan (sc:121-147): block sizes other than K1's
+    1024 run the reference algorithm in float64 on the device (kk_fft
+    transforms): the oracle's field, state and diagnostics; state carries
+    across calls."""
+    cap = load_capture("c1_qpsk_b2b")
+    x = cap.adc_float()[: 1 << 16]
+    x = x.copy()
+    x[5 * nfft: 5 * nfft + nfft // 2] = -1.0      # one dead hop
+    ref, st_ref, dg_ref = ko.kk_reconstruct(x, nfft)
+    plan = BlockPlan(nfft, buffer_len=len(x))
+    out, st, dg = rxdsp.kk_reconstruct(RealSignal(x, 4e9), plan)
+    assert rel_l2(out.samples, ref) < 1e-12
+    assert dg == dg_ref
+    assert np.allclose(st["u_tail"], st_ref["u_tail"], rtol=1e-13) and np.array_equal(st["dead_hist"],
+                                                                                       st_ref["dead_hist"])
+    h = len(x) // 2
+    o1, s1, _ = rxdsp.kk_reconstruct(RealSignal(x[:h], 4e9), plan)
+    o2, _, _ = rxdsp.kk_reconstruct(RealSignal(x[h:], 4e9), plan, state=s1)
+    assert rel_l2(np.concatenate([o1.samples, o2.samples]), ref) < 1e-12
+
+
+@pytest.mark.parametrize("n", [8192, 16384, 65536])
+def test_static_other_block_sizes_vs_oracle(n):
+    rng = np.random.default_rng(n)
+    nx = 4 * n
+    x = rng.standard_normal(nx) + 1j * rng.standard_normal(nx)
+    taps = (rng.standard_normal(203) + 1j * rng.standard_normal(203)) * np.exp(-0.03 * np.abs(np.arange(203) - 101))
+    taps /= np.linalg.norm(taps)
+    plan = BlockPlan(n, buffer_len=nx)
+    kept, h = ko.static_response(taps, 2e9, n, 4e9, 0.01, n // 4)
+    from numpy.lib.stride_tricks import sliding_window_view
+    blocks = sliding_window_view(np.concatenate([np.zeros(n // 2, complex), x]), n)[:: n // 2]
+    ref = (np.fft.ifft(np.fft.fft(blocks, axis=1)[:, kept] * h, axis=1) * 0.5)[:, n // 4:].reshape(-1)
+    out, tail = rxdsp.static_equalize_and_resample(ComplexSignal(x, 4e9), FirFilter(taps, 2e9), plan)
+    assert len(out) == nx // 2
+    assert rel_l2(out.samples, ref) < 1e-12
+    o1, t1 = rxdsp.static_equalize_and_resample(ComplexSignal(x[: nx // 2], 4e9), FirFilter(taps, 2e9), plan)
+    o2, _ = rxdsp.static_equalize_and_resample(ComplexSignal(x[nx // 2:], 4e9), FirFilter(taps, 2e9), plan, tail=t1)
+    assert rel_l2(np.concatenate([o1.samples, o2.samples]), ref) < 1e-12
