@@ -507,33 +507,56 @@ def _kk_reconstruct_generic(x, dt, sc, n: int, nfft: int, state: dict, clamp_rel
     if nfft < 4 or nfft & (nfft - 1):
         raise ParameterError("kk_plan.fft_size must be a power of two >= 4")
     hop, half = nfft // 2, nfft // 4
+    xf = _raw_f64(x, dt, sc, n, dev)
+    st = (torch.as_tensor(np.asarray(state["u_tail"], np.float64), device=dev),
+          torch.as_tensor(np.asarray(state["a_hist"], np.float64), device=dev),
+          torch.as_tensor(np.asarray(state["dead_hist"], bool), device=dev))
+    out, (u_t, a_h, d_h), clamped, dead = _kk_generic_core(xf, nfft, st, clamp_rel, dev)
+    new_state = {"u_tail": u_t.cpu().numpy().copy(), "a_hist": a_h.cpu().numpy().copy(),
+                 "dead_hist": d_h.cpu().numpy().copy()}
+    diag = {"clamped": int(clamped), "zero_blocks": torch.nonzero(dead).flatten().cpu().tolist()}
+    field = out.to(torch.complex64) if device_output else out.cpu().numpy()
+    return ComplexSignal(field, fs), new_state, diag
+
+
+def _raw_f64(x, dt, sc, n: int, dev):
+    """Raw input (int16 codes, packed 12-bit, f32, f64) -> float64 samples."""
+    torch = _torch()
     if dt == _lib.KK_DTYPE_P12:
         x, dt = _unpack12_dev(x, n, dev), _lib.KK_DTYPE_I16
-    xf = x.to(torch.float64) * (float(sc) if dt == _lib.KK_DTYPE_I16 else 1.0)
-    hops = xf[:n].reshape(-1, hop)
+    return x[:n].to(torch.float64) * (float(sc) if dt == _lib.KK_DTYPE_I16 else 1.0)
+
+
+def _kk_generic_core(xf, nfft: int, state, clamp_rel: float, dev):
+    """rx:184-244 on device tensors (float64): field (complex128, delayed by
+    hop/2 like the reference), the new (u_tail, a_hist, dead_hist) state,
+    the clamped count (device) and the per-hop dead flags."""
+    torch = _torch()
+    from .channel import fft as gfft, ifft as gifft
+
+    hop, half = nfft // 2, nfft // 4
+    n = int(xf.shape[0])
+    u_tail, a_hist, dead_hist = state
+    hops = xf.reshape(-1, hop)
     mean = hops.mean(dim=1)
     dead = mean <= 0.0
     thr = torch.where(dead, torch.ones_like(mean), clamp_rel * mean.abs())
-    clamped = int(((hops < thr[:, None]) & ~dead[:, None]).sum())
+    clamped = ((hops < thr[:, None]) & ~dead[:, None]).sum()
     safe = torch.maximum(hops, thr[:, None])
     safe[dead] = 1.0
     flat = safe.reshape(-1)
     amp = flat.sqrt()
     u = 0.5 * flat.log()
     dmask = dead.repeat_interleave(hop)
-    u_all = torch.cat([torch.as_tensor(np.asarray(state["u_tail"], np.float64), device=dev), u])
+    u_all = torch.cat([u_tail, u])
     blocks = u_all.unfold(0, nfft, hop).to(torch.complex128).contiguous()
     spec = gfft(blocks) * _hilbert_full(nfft, dev)
     phi = gifft(spec).real[:, hop:].reshape(-1)
-    a_d = torch.cat([torch.as_tensor(np.asarray(state["a_hist"], np.float64), device=dev), amp])[:n]
-    d_d = torch.cat([torch.as_tensor(np.asarray(state["dead_hist"], bool), device=dev), dmask])[:n]
+    a_d = torch.cat([a_hist, amp])[:n]
+    d_d = torch.cat([dead_hist, dmask])[:n]
     out = a_d * torch.exp(1j * phi)
     out[d_d] = 0.0
-    new_state = {"u_tail": u[-hop:].cpu().numpy().copy(), "a_hist": amp[-half:].cpu().numpy().copy(),
-                 "dead_hist": dmask[-half:].cpu().numpy().copy()}
-    diag = {"clamped": clamped, "zero_blocks": torch.nonzero(dead).flatten().cpu().tolist()}
-    field = out.to(torch.complex64) if device_output else out.cpu().numpy()
-    return ComplexSignal(field, fs), new_state, diag
+    return out, (u[-hop:].clone(), amp[-half:].clone(), dmask[-half:].clone()), clamped, dead
 
 
 def _unpack12_dev(x, n: int, dev):
@@ -541,6 +564,19 @@ def _unpack12_dev(x, n: int, dev):
     out = torch.empty(n, dtype=torch.int16, device=dev)
     _lib.call("kk_unpack12", _ptr(x), n, _ptr(out), _stream(dev))
     return out
+
+
+def _rotate(x, tone_hz: float, fs: float, g0: int, dev):
+    """x[i] * exp(-2 pi i tone (g0 + i) / fs) (the downshift, sc:286-299 by
+    -tone; kk_frequency_shift), complex128."""
+    torch = _torch()
+    if tone_hz == 0.0:
+        return x
+    x = x.to(torch.complex128).contiguous()
+    y = torch.empty_like(x)
+    _lib.call("kk_frequency_shift", _ptr(x), _ptr(y), int(x.shape[0]), float(2 * np.pi * (-tone_hz)), float(fs),
+              int(g0), _stream(dev))
+    return y
 
 
 def _static_generic(z, nb: int, n: int, hop: int, kept, h, dev):
@@ -856,10 +892,12 @@ class RxPipeline:
         self.cfg = cfg
         self.gpu = getattr(cfg, "gpu", None) or GpuOptions()
         self.dev = torch.device(device) if device is not None else _device()
-        if cfg.kk_plan.fft_size != KK_FFT or cfg.static_plan.fft_size != STATIC_FFT:
-            raise ParameterError("the B200 kernels are built for kk_plan 1024 / static_plan 32768")
+        # K1 / K2 are built for the reference's default plans (kk 1024, static
+        # 32768, every shipped config); other power-of-two plans run the
+        # front end in float64 on the repo FFT (_run_kk_generic, _run_static_generic)
+        self._generic_front = cfg.kk_plan.fft_size != KK_FFT or cfg.static_plan.fft_size != STATIC_FFT
         if cfg.carrier_segment_len % (2 * cfg.kk_plan.hop) or cfg.carrier_segment_len <= 0:
-            raise ParameterError("carrier_segment_len must be a positive multiple of 1024")
+            raise ParameterError("carrier_segment_len must be a positive multiple of kk_plan.fft_size")
         # only the sync + training prefix of the reference is ever read
         # (rx:740, rx:745, rx:755); keep just that on host and device
         self._ref_len = 0
@@ -949,6 +987,7 @@ class RxPipeline:
         self._stats: list[dict] = []
 
         self._out: list[tuple] = []
+        self._kk_gstate = None             # float64 KK state of the generic front end (other plans)
         self._pending_diag: list[tuple] = []
         self._diag_frames: dict = {}      # chunk -> DDLMS frames submitted by the end of its feed
         self._diagnostics: list[dict] = []
@@ -1075,7 +1114,69 @@ class RxPipeline:
         # diagnostics are materialised lazily (no host sync per feed)
         self._pending_diag.append((self._chunk_index, h0, n_hops))
 
+    def _run_kk_generic(self, chunk, n_hops):
+        """K1's contract for other KK block sizes: the field (float64, repo
+        FFT), conj(field * rot) into the z FIFO, the unrotated hop sums, dead
+        flags and the chunk's clamped count."""
+        torch = _torch()
+        cfg = self.cfg
+        hop = cfg.kk_plan.hop
+        n = n_hops * hop
+        g0 = self._z.end
+        self._kk_pending = self._hs.end
+        out = self._z.reserve(n)
+        hs = self._hs.reserve(n_hops)
+        hd = self._hd.reserve(n_hops)
+        if self._kk_gstate is None:
+            self._kk_gstate = (torch.zeros(hop, dtype=torch.float64, device=self.dev),
+                               torch.zeros(hop // 2, dtype=torch.float64, device=self.dev),
+                               torch.zeros(hop // 2, dtype=torch.bool, device=self.dev))
+        xf = _raw_f64(chunk, self._raw_dt, self._raw_scale, n, self.dev)
+        field, self._kk_gstate, clamped, dead = _kk_generic_core(xf, cfg.kk_plan.fft_size, self._kk_gstate, 1e-12,
+                                                                 self.dev)
+        hs.copy_(field.reshape(-1, hop).sum(dim=1).to(torch.complex64))
+        hd.copy_(dead.to(torch.uint8))
+        z = _rotate(field, cfg.tone_freq_hz, cfg.adc_rate_hz, g0, self.dev)
+        out.copy_((z.conj() if cfg.mirror else z).to(torch.complex64))
+        if self._chunk_index >= self._clamped_log.shape[0]:
+            grown = torch.zeros(2 * self._clamped_log.shape[0], dtype=torch.int64, device=self.dev)
+            grown[: self._clamped_log.shape[0]] = self._clamped_log
+            self._clamped_log = grown
+        self._clamped_log[self._chunk_index] += clamped
+        self._kk_commit(n_hops)
+
+    def _run_static_generic(self, flush):
+        """K2's contract for other static block sizes: s = z - conj(mean *
+        rot) (mirror) over the blocks ready now, the reference's overlap-save
+        (rx:698-720) in float64 on the repo FFT, 2-sps outputs into y2."""
+        torch = _torch()
+        cfg = self.cfg
+        j = self._static_job(flush)
+        if j is None:
+            return
+        hop = cfg.static_plan.hop
+        n = cfg.static_plan.fft_size
+        nb, hb0 = j.n_blocks, j.hb0
+        g_lo, g_hi = (hb0 - 1) * hop, (hb0 + nb) * hop
+        s = torch.zeros(g_hi - g_lo, dtype=torch.complex128, device=self.dev)
+        a, b = max(g_lo, 0, self._z.base), min(g_hi, j.valid_end)
+        if b > a:
+            v = self._z.view(a, b).to(torch.complex128)
+            if cfg.carrier_removal:
+                seg = cfg.carrier_segment_len
+                si = torch.arange(a, b, device=self.dev) // seg - self._seg.base
+                m = self._seg.buf[si].to(torch.complex128)
+                mr = _rotate(m, cfg.tone_freq_hz, cfg.adc_rate_hz, a, self.dev)
+                v = v - (mr.conj() if cfg.mirror else mr)
+            s[a - g_lo:b - g_lo] = v
+        kept_h = torch.as_tensor(np.asarray(self._resp, np.complex128), device=self.dev)
+        y = _static_generic(s, nb, n, hop, self._kept, kept_h, self.dev)
+        self._y2.view(self._y2.end, self._y2.end + nb * (hop // 2)).copy_(y.to(torch.complex64))
+        self._static_commit()
+
     def _run_kk(self, chunk, n_hops):
+        if self._generic_front:
+            return self._run_kk_generic(chunk, n_hops)
         j = self._kk_job(chunk, n_hops)
         _lib.call("kk_reconstruct_pairs", self._raw_dt, j.in_, j.in_scale, j.clamp_rel, j.n_hops, j.st_u, j.st_a,
                   j.st_dead, j.new_u, j.new_a, j.new_dead, j.out, j.hop_sum, j.hop_dead, j.clamped, j.n0_global,
@@ -1132,6 +1233,8 @@ class RxPipeline:
         self._seg.keep = max(0, ((self._hb_next - 1) * hop) // self.cfg.carrier_segment_len)
 
     def _run_static(self, flush):
+        if self._generic_front:
+            return self._run_static_generic(flush)
         j = self._static_job(flush)
         if j is None:
             return
@@ -1739,6 +1842,14 @@ def feed_batch(pipes, chunks, ddlms: bool = True) -> None:
     for p in pipes:
         if p.dev != dev or p._synced or p._raw is not None and p._raw_len():
             raise ParameterError("feed_batch: fresh pipelines on one device")
+    if any(p._generic_front for p in pipes):
+        # non-default plans (float64 generic front end): stream by stream
+        for p, c in zip(pipes, chunks):
+            if ddlms:
+                p.feed(c, flush=True)
+            else:
+                p.front_end(c, flush=True)
+        return
     inputs = [_as_device_input(c, dev) if _len(c) else (None, None, None) for c in chunks]
     dts = {dt for _, dt, _ in inputs if dt is not None}
     if len(dts) > 1:

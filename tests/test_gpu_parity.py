@@ -999,3 +999,28 @@ def test_static_other_block_sizes_vs_oracle(n):
     o1, t1 = rxdsp.static_equalize_and_resample(ComplexSignal(x[: nx // 2], 4e9), FirFilter(taps, 2e9), plan)
     o2, _ = rxdsp.static_equalize_and_resample(ComplexSignal(x[nx // 2:], 4e9), FirFilter(taps, 2e9), plan, tail=t1)
     assert rel_l2(np.concatenate([o1.samples, o2.samples]), ref) < 1e-12
+
+
+@pytest.mark.parametrize("kk_n,st_n", [(2048, 32768), (1024, 16384), (512, 65536)])
+def test_pipeline_other_plans_vs_oracle(kk_n, st_n):
+    """RxPipeline with KK / static plans other than K1 / K2's 1024 / 32768
+    (any power-of-two BlockPlan, sc:121-147): the float64 generic front end
+    and the same DDLMS give the oracle's sync offset and decisions."""
+    import dataclasses
+
+    cap = load_capture("c4_qpsk_10000km_cspr10")
+    syms = cap.symbols()
+    cfg = cap.pipeline_config()
+    cfg = dataclasses.replace(cfg, kk_plan=BlockPlan(kk_n, buffer_len=cfg.kk_plan.buffer_len),
+                              static_plan=BlockPlan(st_n, buffer_len=cfg.static_plan.buffer_len))
+    pipe = rxdsp.RxPipeline(cfg, reference_symbols=syms)
+    pipe.feed(AdcCodes(cap.adc_h, cap.half_lsb))
+    dec, soft = pipe.finish()
+    ocfg = ko.OracleConfig(taps=cap.taps, kk_fft=kk_n, static_fft=st_n, mu=cap.meta["mu"],
+                           startup_symbols=cap.meta["startup_symbols"])
+    ref, d_ref, s_ref = ko.receive(cap.adc_float(), ocfg, syms, cap.meta["buffer_len"])
+    assert pipe.sync_offset == ref.sync_offset
+    assert len(dec) == len(d_ref)
+    assert np.mean(to_idx(dec, 4) == to_idx(d_ref, 4)) >= DEC_AGREE
+    assert rel_l2(soft, s_ref) < 1e-3
+    assert [d["chunk"] for d in pipe.diagnostics] == [0]
