@@ -135,7 +135,7 @@ class GpuOptions:
     ddlms_release_min_symbols: int = 1
     ddlms_max_iter: int = 1024
     ddlms_soft_tol: float = 1e-5
-    ddlms_tail_min_symbols: int = 1 << 24
+    ddlms_tail_min_symbols: int = 1 << 25
     # run the DDLMS frames on a worker thread / CUDA stream so the front end
     # of later chunks overlaps them (streaming receive, harness.receive_host_stream)
     ddlms_async: bool = False

@@ -737,7 +737,7 @@ def test_parallel_solver_fallback_equals_sequential(max_iter):
     assert np.median(np.abs(soft - s_seq)) < 1e-5
 
 
-@pytest.mark.parametrize("tail_min", [1 << 24, 64])
+@pytest.mark.parametrize("tail_min", [1 << 25, 64])
 def test_host_stream_ragged_length_and_chunks(tail_min):
     """Streaming receive of a ragged stream (length not a multiple of the
     chunk, the KK hop or the static hop; ragged chunk size): the same bits as

@@ -7,7 +7,7 @@ from paper_2108_07001_b200.sigcore import pack12
 import dataclasses
 cap = load_capture("c5_qpsk_10000km_tile")
 cfg = cap.pipeline_config()
-cfg = dataclasses.replace(cfg, gpu=dataclasses.replace(cfg.gpu, ddlms_frame_symbols=1 << int(os.environ.get("KK_E2E_FRAME_LOG2", "26"))))
+cfg = dataclasses.replace(cfg, gpu=dataclasses.replace(cfg.gpu, ddlms_frame_symbols=1 << int(os.environ.get("KK_E2E_FRAME_LOG2", "26")), ddlms_tail_min_symbols=1 << int(os.environ.get("KK_E2E_TAIL_LOG2", "25"))))
 codes, _ = tile(cap, 1 << 30)
 host = torch.from_numpy(pack12(codes)).pin_memory()
 pts = cap.symbols()[:10000]
