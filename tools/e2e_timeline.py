@@ -31,7 +31,7 @@ def main():
 
     cap = load_capture(args.format)
     cfg = cap.pipeline_config()
-    cfg = dataclasses.replace(cfg, gpu=dataclasses.replace(cfg.gpu, ddlms_frame_symbols=1 << 26))
+    cfg = dataclasses.replace(cfg, gpu=dataclasses.replace(cfg.gpu, ddlms_frame_symbols=1 << 25))   # as bench.py e2e
     n = 1 << 30
     codes, _ = tile(cap, n)
     from paper_2108_07001_b200.sigcore import pack12
@@ -43,7 +43,7 @@ def main():
           else torch.empty(n, dtype=torch.int16, device="cuda"))
 
     def step():
-        pipe, _, _ = receive_host_stream(cfg, host, cap.half_lsb, pts, chunk_samples=1 << 25, bits_host=bits,
+        pipe, _, _ = receive_host_stream(cfg, host, cap.half_lsb, pts, chunk_samples=1 << 26, bits_host=bits,
                                          staging=st, packed12_samples=n if args.packed12 else None)
         pipe.release_buffers()
 
