@@ -334,7 +334,7 @@ _NVTX = _os.environ.get("KK_NVTX", "0") == "1"
 _DDLMS_GRAPH = _os.environ.get("KK_DDLMS_GRAPH", "1") != "0"
 _GRAPH_MIN_SYMBOLS = 1 << 22
 # priority of the asynchronous DDLMS worker stream (lower = scheduled first)
-_DDLMS_PRIO = int(_os.environ.get("KK_DDLMS_PRIO", "-1"))
+_DDLMS_PRIO = int(_os.environ.get("KK_DDLMS_PRIO", "-2"))
 
 _SIDE_STREAMS = {}
 import threading as _threading
