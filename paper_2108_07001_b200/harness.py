@@ -565,7 +565,8 @@ def receive_host_stream(cfg, host_codes, half_lsb: float, reference_symbols, chu
     return out
 
 
-def _stream_receiver(cfg, reference_symbols, n: int, chunk_samples: int, dev, chunk_ends=None):
+def _stream_receiver(cfg, reference_symbols, n: int, chunk_samples: int, dev, chunk_ends=None,
+                     stage_timing: bool = False):
     """Pipeline + output packing state of a streaming receive (shared by the
     pinned-host and raw-file ingest paths)."""
     import dataclasses
@@ -576,7 +577,9 @@ def _stream_receiver(cfg, reference_symbols, n: int, chunk_samples: int, dev, ch
 
     # DDLMS frames run asynchronously (worker thread + stream) so the front
     # end of later chunks overlaps them.
-    gpu = dataclasses.replace(cfg.gpu, ddlms_async=True)
+    # No stage-timing events: each one drains the front-end stream before its
+    # timestamp (~1 ms per 2^30-sample stream); stage_seconds reports zeros.
+    gpu = dataclasses.replace(cfg.gpu, ddlms_async=True, stage_timing=stage_timing)
     cfg = dataclasses.replace(cfg, gpu=gpu)
     pipe = RxPipeline(cfg, reference_symbols=reference_symbols, device=dev)
     pipe.expect(n, chunk_samples, chunk_ends=chunk_ends)

@@ -133,6 +133,10 @@ class GpuOptions:
     # drain() closes the open frame at the last produced symbol when at
     # least this many symbols are undecided (RxPipeline._release_decidable)
     ddlms_release_min_symbols: int = 1
+    # CUDA timing events at the stage boundaries (stage_seconds); each one
+    # drains the stream before its timestamp, so streaming receives
+    # (harness.receive_host_stream) turn them off
+    stage_timing: bool = True
     ddlms_max_iter: int = 1024
     ddlms_soft_tol: float = 1e-5
     ddlms_tail_min_symbols: int = 1 << 25
@@ -988,6 +992,7 @@ class RxPipeline:
 
         self._out: list[tuple] = []
         self._kk_gstate = None             # float64 KK state of the generic front end (other plans)
+        self._stage_timing = bool(getattr(self.gpu, "stage_timing", True))
         self._pending_diag: list[tuple] = []
         self._diag_frames: dict = {}      # chunk -> DDLMS frames submitted by the end of its feed
         self._diagnostics: list[dict] = []
@@ -999,17 +1004,23 @@ class RxPipeline:
     # -- timing ---------------------------------------------------------------
 
     def _ev(self):
+        """Stage boundary marker.  With GpuOptions.stage_timing a timing
+        event (CUDA-event stage_seconds); a timing event drains the stream
+        before its timestamp (~28 us per boundary on B200, ~1 ms per 2^30-
+        sample streaming receive), so streaming receives turn it off and
+        record plain markers (stage_seconds then reports zeros)."""
         torch = _torch()
-        e = torch.cuda.Event(enable_timing=True)
+        e = torch.cuda.Event(enable_timing=self._stage_timing)
         e.record(torch.cuda.current_stream(self.dev))
         return e
 
     @property
     def stage_seconds(self) -> dict:
         if self._events:
-            _torch().cuda.current_stream(self.dev).synchronize()
-            for name, a, b in self._events:
-                self._stage_acc[name] += a.elapsed_time(b) / 1e3
+            if self._stage_timing:
+                _torch().cuda.current_stream(self.dev).synchronize()
+                for name, a, b in self._events:
+                    self._stage_acc[name] += a.elapsed_time(b) / 1e3
             self._events = []
         return dict(self._stage_acc)
 
