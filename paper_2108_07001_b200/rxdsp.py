@@ -1483,10 +1483,10 @@ class RxPipeline:
             try:
                 with torch.cuda.stream(ws):
                     ws.wait_event(job["ready"])
-                    e0 = torch.cuda.Event(enable_timing=True)
+                    e0 = torch.cuda.Event(enable_timing=self._stage_timing)
                     e0.record(ws)
                     job["out"] = self._solve_frame_impl(job["k0"], job["k1"], job["labels"], job["soft"])
-                    e1 = torch.cuda.Event(enable_timing=True)
+                    e1 = torch.cuda.Event(enable_timing=self._stage_timing)
                     e1.record(ws)
                     for t in (job["labels"], job["soft"], self._ws):
                         t.record_stream(ws)
