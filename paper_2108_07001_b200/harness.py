@@ -530,7 +530,7 @@ def pack_labels_host(labels, sym0: int, train_idx, order: int, bits_host) -> int
 _FRONT_PRIO = int(__import__("os").environ.get("KK_FRONT_PRIO", "0"))
 
 
-def receive_host_stream(cfg, host_codes, half_lsb: float, reference_symbols, chunk_samples: int = 1 << 26,
+def receive_host_stream(cfg, host_codes, half_lsb: float, reference_symbols, chunk_samples: int = 1 << 25,
                         bits_host=None, device=None, staging=None, trace=None, packed12_samples: int | None = None):
     """End-to-end receive of an int16 ADC stream in pinned HOST memory; the
     receiver's output -- the demapped bit stream, packed (np.packbits

@@ -43,7 +43,7 @@ def main():
           else torch.empty(n, dtype=torch.int16, device="cuda"))
 
     def step():
-        pipe, _, _ = receive_host_stream(cfg, host, cap.half_lsb, pts, chunk_samples=1 << 26, bits_host=bits,
+        pipe, _, _ = receive_host_stream(cfg, host, cap.half_lsb, pts, chunk_samples=1 << 25, bits_host=bits,
                                          staging=st, packed12_samples=n if args.packed12 else None)
         pipe.release_buffers()
 

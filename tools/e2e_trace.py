@@ -16,7 +16,7 @@ st = torch.empty(3 << 29, dtype=torch.uint8, device="cuda")
 for i in range(5):
     torch.cuda.synchronize()
     t = time.perf_counter()
-    pipe, bh, n = receive_host_stream(cfg, host, cap.half_lsb, pts, chunk_samples=1 << int(os.environ.get("KK_E2E_CHUNK_LOG2", "26")), bits_host=bits, staging=st, packed12_samples=1 << 30)
+    pipe, bh, n = receive_host_stream(cfg, host, cap.half_lsb, pts, chunk_samples=1 << int(os.environ.get("KK_E2E_CHUNK_LOG2", "25")), bits_host=bits, staging=st, packed12_samples=1 << 30)
     torch.cuda.synchronize()
     dt = time.perf_counter() - t
     print(f"e2e step {i}: {dt*1e3:.1f} ms  {n/dt/1e9:.3f} GBaud", [(s['nsym'], s.get('iterations'), s.get('mode')) for s in pipe.ddlms_stats], flush=True)
