@@ -384,6 +384,31 @@ struct ReadBack {
 
 __device__ __forceinline__ bool ctl_done(const int* ctl) { return ctl && *ctl == kModeDone; }
 
+// Counter / control resets of the readback record in one launch (replaces
+// 2-3 small memsets per frame step; each costs a launch slot on the stream).
+enum : int {
+    kRbCtr01 = 1, kRbCtr2 = 2, kRbCtr3 = 4, kRbFirst0 = 8, kRbFirst1 = 16, kRbCtl = 32, kRbAll = 64,
+};
+__global__ void rb_reset_kernel(ReadBack* __restrict__ rb, int what) {
+    if (threadIdx.x != 0) return;
+    if (what & kRbAll) {
+        unsigned long long* w = reinterpret_cast<unsigned long long*>(rb);
+        for (size_t i = 0; i < sizeof(ReadBack) / 8; ++i) w[i] = 0ull;
+        rb->first_changed = ~0u;
+        rb->last_first = ~0u;
+        return;
+    }
+    if (what & kRbCtr01) rb->ctr[0] = rb->ctr[1] = 0ull;
+    if (what & kRbCtr2) rb->ctr[2] = 0ull;
+    if (what & kRbCtr3) rb->ctr[3] = 0ull;
+    if (what & kRbFirst0) rb->first_changed = ~0u;
+    if (what & kRbFirst1) rb->last_first = ~0u;
+    if (what & kRbCtl) rb->ctl[0] = rb->ctl[1] = rb->ctl[2] = rb->ctl[3] = 0;
+}
+static_assert(sizeof(ReadBack) % 8 == 0, "ReadBack layout");
+
+
+
 __device__ bool fallback_gate(const ReadBack* rb, int64_t& b_lo) {
     if (rb->ctl[3] != 2) return false;
     b_lo = rb->last_first;
@@ -2145,16 +2170,13 @@ struct DdlmsSolver {
         o.first_changed = &rb->first_changed;
         bt = std::min<int64_t>(n_train / block, L.nb);
         ntb = std::min<int64_t>((n_train + block - 1) / block, L.nb);
-        if (cudaMemsetAsync(over, 0, L.nb * sizeof(int), s) != cudaSuccess ||
-            cudaMemsetAsync(hsh, 0, L.nb * 8, s) != cudaSuccess ||
-            cudaMemsetAsync(ties, 0, L.nb * sizeof(uint2), s) != cudaSuccess ||
-            cudaMemsetAsync(grun, 0, L.nb * sizeof(int2), s) != cudaSuccess ||
-            cudaMemsetAsync(Twritten, 0xFF, L.nb * 16 * sizeof(float), s) != cudaSuccess ||   // NaN: never written
-            cudaMemsetAsync(ctr, 0, 4 * sizeof(unsigned long long), s) != cudaSuccess ||
-            cudaMemsetAsync(&rb->first_changed, 0xFF, 2 * sizeof(unsigned int), s) != cudaSuccess ||
-            cudaMemsetAsync(rb->ctl, 0, sizeof(rb->ctl), s) != cudaSuccess)
+        // over, hsh, ties and grun are contiguous in the workspace: one memset
+        const size_t zero_bytes = reinterpret_cast<char*>(grun + L.nb) - reinterpret_cast<char*>(over);
+        if (cudaMemsetAsync(over, 0, zero_bytes, s) != cudaSuccess ||
+            cudaMemsetAsync(Twritten, 0xFF, L.nb * 16 * sizeof(float), s) != cudaSuccess)   // NaN: never written
             return set_cuda_error("solver init");
-        return KK_OK;
+        rb_reset_kernel<<<1, 32, 0, s>>>(rb, kRbCtr01 | kRbCtr2 | kRbCtr3 | kRbFirst0 | kRbFirst1 | kRbCtl);
+        return check_launch("rb_reset_kernel");
     }
 
     // the final pass writes straight into the caller's arrays when bound
@@ -2213,10 +2235,8 @@ struct DdlmsSolver {
         if (!speculated) return set_error(KK_ERR_PARAM, "speculate() must precede iterate()");
         if (int rc = set_start(T_start)) return rc;
         if (int rc = scan_down()) return rc;
-        if (cudaMemsetAsync(ctr, 0, 2 * sizeof(unsigned long long), s) != cudaSuccess ||
-            cudaMemsetAsync(ctr + 3, 0, sizeof(unsigned long long), s) != cudaSuccess ||
-            cudaMemsetAsync(&rb->first_changed, 0xFF, sizeof(unsigned int), s) != cudaSuccess)
-            return set_cuda_error("ctr");
+        rb_reset_kernel<<<1, 32, 0, s>>>(rb, kRbCtr01 | kRbCtr3 | kRbFirst0);
+        if (int rc = check_launch("rb_reset_kernel")) return rc;
         // decision pass: compacted re-run of the blocks whose certified margin
         // the start move could cross, no outputs; output pass: also the blocks
         // whose outputs are missing or were written from a start more than
@@ -2253,10 +2273,10 @@ struct DdlmsSolver {
         if (!speculated) return set_error(KK_ERR_PARAM, "speculate() must precede solve_loop()");
         if (T_start)
             if (int rc = set_start(T_start)) return rc;
-        if (reset && (cudaMemsetAsync(ctr, 0, 4 * sizeof(unsigned long long), s) != cudaSuccess ||
-                      cudaMemsetAsync(rb->ctl, 0, sizeof(rb->ctl), s) != cudaSuccess ||
-                      cudaMemsetAsync(&rb->first_changed, 0xFF, 2 * sizeof(unsigned int), s) != cudaSuccess))
-            return set_cuda_error("solve_loop init");
+        if (reset) {
+            rb_reset_kernel<<<1, 32, 0, s>>>(rb, kRbCtr01 | kRbCtr2 | kRbCtr3 | kRbCtl | kRbFirst0 | kRbFirst1);
+            if (int rc = check_launch("rb_reset_kernel")) return rc;
+        }
         *converged = false;
         ReadBack h;
         int queued = 0;
@@ -2459,9 +2479,8 @@ struct DdlmsSolver {
         a.guard_run = guard_run;
         a.lin = widely_linear ? 0 : 1;
         ctl_d = rb->ctl;
-        if (cudaMemsetAsync(rb, 0, sizeof(ReadBack), s) != cudaSuccess ||
-            cudaMemsetAsync(&rb->first_changed, 0xFF, 2 * sizeof(unsigned int), s) != cudaSuccess)
-            return set_cuda_error("solve_async init");
+        rb_reset_kernel<<<1, 32, 0, s>>>(rb, kRbAll);
+        if (int rc = check_launch("rb_reset_kernel")) return rc;
         frame_begin_kernel<<<1, 32, 0, s>>>(T_io, scale, Tinit_d, state_io, rb);
         if (int rc = check_launch("frame_begin_kernel")) return rc;
         // pure training blocks (exact from the frame start), then the first
@@ -2484,9 +2503,8 @@ struct DdlmsSolver {
         if (int rc = scan_up(true)) return rc;
         speculated = true;
         speculated_async = true;
-        if (cudaMemsetAsync(ctr, 0, 4 * sizeof(unsigned long long), s) != cudaSuccess ||
-            cudaMemsetAsync(&rb->first_changed, 0xFF, sizeof(unsigned int), s) != cudaSuccess)
-            return set_cuda_error("solve_async counters");
+        rb_reset_kernel<<<1, 32, 0, s>>>(rb, kRbCtr01 | kRbCtr2 | kRbCtr3 | kRbFirst0);
+        if (int rc = check_launch("rb_reset_kernel")) return rc;
         if (!use_graph) {
             // host-driven batches with readbacks (blocks the calling thread):
             // for frames solved by a worker thread while other streams work --
