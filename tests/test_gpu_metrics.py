@@ -212,3 +212,28 @@ def test_measure_point_device_windowed_q():
     for key in ("n_bits", "n_errors", "sync_offset", "windowed_q"):
         assert got[key] == want[key], key
     assert abs(got["evm_pct"] - want["evm_pct"]) < 1e-9 * want["evm_pct"]
+
+
+def test_bit_xcorr_minimum_sizes_and_errors():
+    """Edge sizes of frame_sync (me:69-112): the shortest reference (2^14
+    bits) against the shortest received stream (64 bits), and the errors the
+    reference raises."""
+    from paper_2108_07001_b200.sigcore import ParameterError
+
+    rng = np.random.default_rng(17)
+    tx = rng.integers(0, 2, 1 << 14, dtype=np.uint8)
+    rx = tx[5000:5064].copy()
+    assert _xcorr(rx, tx, False) == _expected(rx, tx, False)
+    dev = torch.device("cuda:0")
+    with pytest.raises(SyncFailure):
+        frame_sync_device(torch.from_numpy(rx[:63]).to(dev), torch.from_numpy(tx).to(dev))
+    with pytest.raises(ParameterError):
+        frame_sync_device(torch.from_numpy(rx).to(dev), torch.from_numpy(tx[:(1 << 14) - 1]).to(dev))
+
+
+def test_bit_xcorr_all_equal_streams():
+    """Degenerate input: constant streams (every lag correlates) -- the peak
+    is the full-overlap lag, the sidelobes are exact."""
+    tx = np.ones(1 << 14, dtype=np.uint8)
+    rx = np.ones(3000, dtype=np.uint8)
+    assert _xcorr(rx, tx, False) == _expected(rx, tx, False)

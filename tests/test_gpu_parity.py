@@ -1024,3 +1024,23 @@ def test_pipeline_other_plans_vs_oracle(kk_n, st_n):
     assert np.mean(to_idx(dec, 4) == to_idx(d_ref, 4)) >= DEC_AGREE
     assert rel_l2(soft, s_ref) < 1e-3
     assert [d["chunk"] for d in pipe.diagnostics] == [0]
+
+
+def test_drain_without_release_keeps_grid_framing():
+    """drain() with ddlms_release_min_symbols above the stream length closes
+    no frame early: the outputs are bit-identical to a single feed."""
+    cap = load_capture("c4_qpsk_10000km_cspr10")
+    cfg = cap.pipeline_config(ddlms_release_min_symbols=1 << 40)
+    p1 = rxdsp.RxPipeline(cfg, reference_symbols=cap.symbols())
+    p1.feed(AdcCodes(cap.adc_h, cap.half_lsb))
+    d1, s1 = p1.finish()
+    p2 = rxdsp.RxPipeline(cfg, reference_symbols=cap.symbols())
+    decs, softs = [], []
+    for a in range(0, len(cap.adc_h), 1 << 17):
+        p2.feed(AdcCodes(cap.adc_h[a:a + (1 << 17)], cap.half_lsb))
+        d, s = p2.drain()
+        decs.append(d)
+        softs.append(s)
+        assert len(d) == 0
+    d, s = p2.finish()
+    assert np.array_equal(np.concatenate(decs + [d]), d1) and np.array_equal(np.concatenate(softs + [s]), s1)
