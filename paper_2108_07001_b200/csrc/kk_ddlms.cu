@@ -1940,6 +1940,25 @@ extern "C" size_t kk_ddlms_workspace_bytes(int64_t nsym, int block) {
 // A frame map (P, Q) means T_end = T_start P + Q (host float[64 + 16]).
 // ---------------------------------------------------------------------------
 namespace {
+#ifndef KK_DD_TRAIN_FORK
+#define KK_DD_TRAIN_FORK 1
+#endif
+// per-device non-blocking side stream for the training blocks' speculative
+// pass (created once, never destroyed: process lifetime)
+inline cudaStream_t train_side_stream() {
+    static std::mutex mu;
+    static cudaStream_t side[64] = {};
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return nullptr;
+    std::lock_guard<std::mutex> lock(mu);
+    if (!side[dev]) {
+        int lo = 0, hi = 0;
+        cudaDeviceGetStreamPriorityRange(&lo, &hi);
+        if (cudaStreamCreateWithPriority(&side[dev], cudaStreamNonBlocking, hi) != cudaSuccess) side[dev] = nullptr;
+    }
+    return side[dev];
+}
+
 struct DdlmsSolver {
     cudaStream_t s;
     Layout L;
@@ -2090,9 +2109,38 @@ struct DdlmsSolver {
         };
         if (ext_list) return launch(false, b0, b1, 0, ext_list, ctr + 3);   // device-built list (cascades)
         const int64_t t1 = std::min(b1, ntb);
+        const int64_t d0 = std::max(b0, ntb);
+        // the speculative P pass's blocks holding training symbols (one CTA,
+        // a sequential chain of ~170 us) run on a side stream next to the
+        // main launch instead of before it (not while a graph is captured)
+        cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+        const bool fork = KK_DD_TRAIN_FORK && with_p && b0 < t1 && d0 < b1 &&
+                          cudaStreamIsCapturing(s, &cap) == cudaSuccess && cap == cudaStreamCaptureStatusNone;
+        if (fork) {
+            cudaStream_t side = train_side_stream();
+            cudaEvent_t e0 = nullptr, e1 = nullptr;
+            if (!side || cudaEventCreateWithFlags(&e0, cudaEventDisableTiming) != cudaSuccess ||
+                cudaEventCreateWithFlags(&e1, cudaEventDisableTiming) != cudaSuccess)
+                return set_cuda_error("train fork events");
+            const cudaStream_t main_s = s;
+            int rc = KK_OK;
+            if (cudaEventRecord(e0, main_s) != cudaSuccess || cudaStreamWaitEvent(side, e0, 0) != cudaSuccess)
+                rc = set_cuda_error("train fork");
+            if (rc == KK_OK) {
+                s = side;
+                rc = launch(true, b0, t1, 0, nullptr, nullptr);
+                s = main_s;
+            }
+            if (rc == KK_OK) rc = launch(false, d0, b1, 0, nullptr, nullptr);
+            if (rc == KK_OK && (cudaEventRecord(e1, side) != cudaSuccess ||
+                                cudaStreamWaitEvent(main_s, e1, 0) != cudaSuccess))
+                rc = set_cuda_error("train join");
+            cudaEventDestroy(e0);
+            cudaEventDestroy(e1);
+            return rc;
+        }
         if (b0 < t1)
             if (int rc = launch(true, b0, t1, (use_skip && !with_p) ? 1 : 0, nullptr, nullptr)) return rc;
-        const int64_t d0 = std::max(b0, ntb);
         if (d0 >= b1) return KK_OK;
         if (use_skip && !with_p) {
             // compact the blocks to re-run so that warps only carry live chains
