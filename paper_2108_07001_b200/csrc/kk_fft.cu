@@ -401,8 +401,11 @@ __global__ void spec_mul_conj_kernel(double2* __restrict__ a, const double2* __r
 }
 
 // Transform `batch` rows of n points from x into y (x == y allowed).
+// prepared: the twiddle tables (and, for Bluestein lengths, the chirp and its
+// spectrum) are already in ws from an earlier call with the same n (the
+// split-step loop runs four transforms of one length per step).
 int transform(const double2* x, double2* y, int64_t n, int64_t batch, bool inverse, void* ws, size_t ws_bytes,
-              cudaStream_t st) {
+              cudaStream_t st, bool prepared = false) {
     const AnyPlan p = plan_any(n, batch);
     if (p.log_m > 31) return set_error(KK_ERR_PARAM, "fft: length too large");
     if (!ws || ws_bytes < p.total) return set_error(KK_ERR_PARAM, "fft: workspace too small");
@@ -410,7 +413,7 @@ int transform(const double2* x, double2* y, int64_t n, int64_t batch, bool inver
     double2* a = reinterpret_cast<double2*>(base + p.off_a);
     double2* b = reinterpret_cast<double2*>(base + p.off_b);
     void* tab = base + p.off_tab;
-    int rc = build_tables(tab, p.log_m, st);
+    int rc = prepared ? KK_OK : build_tables(tab, p.log_m, st);
     if (rc != KK_OK) return rc;
     const unsigned g = grid_for(p.batch * p.m, 256);
     double2* res = nullptr;
@@ -424,14 +427,16 @@ int transform(const double2* x, double2* y, int64_t n, int64_t batch, bool inver
     }
     double2* w = reinterpret_cast<double2*>(base + p.off_chirp);
     double2* bs = reinterpret_cast<double2*>(base + p.off_bspec);
-    chirp_kernel<<<grid_for(n, 256), 256, 0, st>>>(w, n);
-    if ((rc = check_launch("fft chirp_kernel")) != KK_OK) return rc;
-    // chirp spectrum: one row in a, transformed into bs
-    bluestein_b_kernel<<<grid_for(p.m, 256), 256, 0, st>>>(w, a, n, p.m);
-    if ((rc = check_launch("fft bluestein_b_kernel")) != KK_OK) return rc;
-    if ((rc = forward_pow2(a, b, p.log_m, 1, tab, st, &res)) != KK_OK) return rc;
-    if (cudaMemcpyAsync(bs, res, size_t(p.m) * sizeof(double2), cudaMemcpyDeviceToDevice, st) != cudaSuccess)
-        return set_cuda_error("fft bluestein copy");
+    if (!prepared) {
+        chirp_kernel<<<grid_for(n, 256), 256, 0, st>>>(w, n);
+        if ((rc = check_launch("fft chirp_kernel")) != KK_OK) return rc;
+        // chirp spectrum: one row in a, transformed into bs
+        bluestein_b_kernel<<<grid_for(p.m, 256), 256, 0, st>>>(w, a, n, p.m);
+        if ((rc = check_launch("fft bluestein_b_kernel")) != KK_OK) return rc;
+        if ((rc = forward_pow2(a, b, p.log_m, 1, tab, st, &res)) != KK_OK) return rc;
+        if (cudaMemcpyAsync(bs, res, size_t(p.m) * sizeof(double2), cudaMemcpyDeviceToDevice, st) != cudaSuccess)
+            return set_cuda_error("fft bluestein copy");
+    }
     load_rows_kernel<<<g, 256, 0, st>>>(x, a, n, p.m, batch, inverse ? 1 : 0, w);
     if ((rc = check_launch("fft load_rows_kernel")) != KK_OK) return rc;
     if ((rc = forward_pow2(a, b, p.log_m, batch, tab, st, &res)) != KK_OK) return rc;
@@ -532,16 +537,17 @@ extern "C" int kk_ssfm_span(void* x, int64_t n, double sample_rate_hz, int n_ste
     ssfm_lin_kernel<<<g, 256, 0, st>>>(lin, n, val, a_half);
     int rc = check_launch("ssfm_lin_kernel");
     for (int s = 0; s < n_steps && rc == KK_OK; ++s) {
-        if ((rc = transform(v, v, n, 1, false, fws, fbytes, st)) != KK_OK) break;
+        // the first transform prepares the tables / chirp in the workspace
+        if ((rc = transform(v, v, n, 1, false, fws, fbytes, st, s > 0)) != KK_OK) break;
         cmul_inplace_kernel<<<g, 256, 0, st>>>(v, lin, n);
         if ((rc = check_launch("ssfm cmul_inplace_kernel")) != KK_OK) break;
-        if ((rc = transform(v, v, n, 1, true, fws, fbytes, st)) != KK_OK) break;
+        if ((rc = transform(v, v, n, 1, true, fws, fbytes, st, true)) != KK_OK) break;
         ssfm_nl_kernel<<<g, 256, 0, st>>>(v, n, gamma_per_w_km, l_eff_km);
         if ((rc = check_launch("ssfm_nl_kernel")) != KK_OK) break;
-        if ((rc = transform(v, v, n, 1, false, fws, fbytes, st)) != KK_OK) break;
+        if ((rc = transform(v, v, n, 1, false, fws, fbytes, st, true)) != KK_OK) break;
         cmul_inplace_kernel<<<g, 256, 0, st>>>(v, lin, n);
         if ((rc = check_launch("ssfm cmul_inplace_kernel")) != KK_OK) break;
-        if ((rc = transform(v, v, n, 1, true, fws, fbytes, st)) != KK_OK) break;
+        if ((rc = transform(v, v, n, 1, true, fws, fbytes, st, true)) != KK_OK) break;
         scale_kernel<<<g, 256, 0, st>>>(v, n, loss_amp);
         rc = check_launch("ssfm scale_kernel");
     }
