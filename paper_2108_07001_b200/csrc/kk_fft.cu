@@ -200,8 +200,15 @@ __device__ __forceinline__ void inner_stage(double2* s, int ls, const double2* _
 }
 
 // One Stockham pass over `cols` = batch * N/R columns.
+#ifndef KK_FFT_MINB
+#define KK_FFT_MINB 2   // 2 CTAs/SM (<= 128 registers): measured 1.45x over 1 CTA at 140
+#endif
+#ifndef KK_FFT_UNROLL
+#define KK_FFT_UNROLL 4
+#endif
+constexpr int kFftUnroll = KK_FFT_UNROLL;
 template <int LOGR>
-__global__ void __launch_bounds__(kThreads) fft_pass_kernel(const double2* __restrict__ in, double2* __restrict__ out,
+__global__ void __launch_bounds__(kThreads, KK_FFT_MINB) fft_pass_kernel(const double2* __restrict__ in, double2* __restrict__ out,
                                                             int log_n, int64_t ns, int64_t cols, const Tables tb) {
     constexpr int R = 1 << LOGR;
     constexpr int TILE = kTilePoints / R;
@@ -211,20 +218,42 @@ __global__ void __launch_bounds__(kThreads) fft_pass_kernel(const double2* __res
     const int64_t nr = int64_t(1) << lnr;
     const int64_t c0 = int64_t(blockIdx.x) * TILE;
     const int64_t tw_step = n / (ns * R);     // w_{Ns R} = w_N^(N / (Ns R))
-    // load + pass twiddle, t fastest (coalesced along q)
-#pragma unroll 4
-    for (int i = 0; i < kTilePoints / kThreads; ++i) {
-        const int e = threadIdx.x + kThreads * i;
-        const int t = e % TILE, m = e / TILE;
+    // load + pass twiddle, t fastest (coalesced along q).  For TILE <= the
+    // thread count a thread keeps one column t for all its elements: the
+    // column's address, twiddle exponent step and bounds test are hoisted.
+    if constexpr (TILE <= kThreads) {
+        constexpr int MS = kThreads / TILE;           // m step per element
+        const int t = threadIdx.x % TILE, m0 = threadIdx.x / TILE;
         const int64_t c = c0 + t;
-        double2 x = make_double2(0.0, 0.0);
-        if (c < cols) {
-            const int64_t row = c >> lnr, q = c & (nr - 1);
-            x = in[(row << log_n) + q + int64_t(m) * nr];
-            const int64_t k = q & (ns - 1);
-            if (k != 0 && m != 0) x = cmul(x, tw_n(tb, ((k * m) * tw_step) & (n - 1)));
+        const bool ok = c < cols;
+        const int64_t q = c & (nr - 1);
+        const double2* src = in + ((c >> lnr) << log_n) + q;
+        const int64_t kstep = (q & (ns - 1)) * tw_step;   // exponent per unit of m
+#pragma unroll kFftUnroll
+        for (int i = 0; i < kTilePoints / kThreads; ++i) {
+            const int m = m0 + MS * i;
+            double2 x = make_double2(0.0, 0.0);
+            if (ok) {
+                x = src[int64_t(m) * nr];
+                if (kstep != 0 && m != 0) x = cmul(x, tw_n(tb, (kstep * m) & (n - 1)));
+            }
+            sm[t * (R + 1) + m] = x;
         }
-        sm[t * (R + 1) + m] = x;
+    } else {
+#pragma unroll 4
+        for (int i = 0; i < kTilePoints / kThreads; ++i) {
+            const int e = threadIdx.x + kThreads * i;
+            const int t = e % TILE, m = e / TILE;
+            const int64_t c = c0 + t;
+            double2 x = make_double2(0.0, 0.0);
+            if (c < cols) {
+                const int64_t row = c >> lnr, q = c & (nr - 1);
+                x = in[(row << log_n) + q + int64_t(m) * nr];
+                const int64_t k = q & (ns - 1);
+                if (k != 0 && m != 0) x = cmul(x, tw_n(tb, ((k * m) * tw_step) & (n - 1)));
+            }
+            sm[t * (R + 1) + m] = x;
+        }
     }
     __syncthreads();
     // R-point DFTs of every column: radix-16 stages, then the remainder
@@ -248,6 +277,19 @@ __global__ void __launch_bounds__(kThreads) fft_pass_kernel(const double2* __res
             const int e = threadIdx.x + kThreads * i;
             const int t = e / R, m = e % R;
             if (c0 + t < cols) out[(c0 + t) * R + m] = sm[t * (R + 1) + m];
+        }
+    } else if constexpr (TILE <= kThreads) {
+        constexpr int MS = kThreads / TILE;
+        const int t = threadIdx.x % TILE, m0 = threadIdx.x / TILE;
+        const int64_t c = c0 + t;
+        if (c < cols) {
+            const int64_t q = c & (nr - 1);
+            double2* dst = out + ((c >> lnr) << log_n) + (q / ns) * ns * R + (q & (ns - 1));
+#pragma unroll kFftUnroll
+            for (int i = 0; i < kTilePoints / kThreads; ++i) {
+                const int m = m0 + MS * i;
+                dst[int64_t(m) * ns] = sm[t * (R + 1) + m];
+            }
         }
     } else {
 #pragma unroll 4
