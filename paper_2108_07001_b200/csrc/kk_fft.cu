@@ -207,7 +207,7 @@ __device__ __forceinline__ void inner_stage(double2* s, int ls, const double2* _
 #define KK_FFT_UNROLL 4
 #endif
 constexpr int kFftUnroll = KK_FFT_UNROLL;
-template <int LOGR>
+template <int LOGR, bool FULL>   // FULL: cols is a multiple of TILE (no bounds tests)
 __global__ void __launch_bounds__(kThreads, KK_FFT_MINB) fft_pass_kernel(const double2* __restrict__ in, double2* __restrict__ out,
                                                             int log_n, int64_t ns, int64_t cols, const Tables tb) {
     constexpr int R = 1 << LOGR;
@@ -225,7 +225,7 @@ __global__ void __launch_bounds__(kThreads, KK_FFT_MINB) fft_pass_kernel(const d
         constexpr int MS = kThreads / TILE;           // m step per element
         const int t = threadIdx.x % TILE, m0 = threadIdx.x / TILE;
         const int64_t c = c0 + t;
-        const bool ok = c < cols;
+        const bool ok = FULL || c < cols;
         const int64_t q = c & (nr - 1);
         const double2* src = in + ((c >> lnr) << log_n) + q;
         const int64_t kstep = (q & (ns - 1)) * tw_step;   // exponent per unit of m
@@ -276,13 +276,13 @@ __global__ void __launch_bounds__(kThreads, KK_FFT_MINB) fft_pass_kernel(const d
         for (int i = 0; i < kTilePoints / kThreads; ++i) {
             const int e = threadIdx.x + kThreads * i;
             const int t = e / R, m = e % R;
-            if (c0 + t < cols) out[(c0 + t) * R + m] = sm[t * (R + 1) + m];
+            if (FULL || c0 + t < cols) out[(c0 + t) * R + m] = sm[t * (R + 1) + m];
         }
     } else if constexpr (TILE <= kThreads) {
         constexpr int MS = kThreads / TILE;
         const int t = threadIdx.x % TILE, m0 = threadIdx.x / TILE;
         const int64_t c = c0 + t;
-        if (c < cols) {
+        if (FULL || c < cols) {
             const int64_t q = c & (nr - 1);
             double2* dst = out + ((c >> lnr) << log_n) + (q / ns) * ns * R + (q & (ns - 1));
 #pragma unroll kFftUnroll
@@ -310,12 +310,21 @@ int launch_pass(const double2* in, double2* out, int log_n, int64_t batch, int64
     constexpr int R = 1 << LOGR;
     constexpr int TILE = kTilePoints / R;
     const size_t smem = size_t(TILE) * (R + 1) * sizeof(double2);
-    if (ensure_smem_attr(reinterpret_cast<const void*>(&fft_pass_kernel<LOGR>), smem, "fft_pass_kernel") != KK_OK)
-        return KK_ERR_CUDA;
     const int64_t cols = batch << (log_n - LOGR);
     const int64_t blocks = (cols + TILE - 1) / TILE;
     if (blocks > 0x7FFFFFFFLL) return set_error(KK_ERR_PARAM, "fft: transform too large");
-    fft_pass_kernel<LOGR><<<static_cast<unsigned>(blocks), kThreads, smem, st>>>(in, out, log_n, ns, cols, tb);
+    if (cols % TILE == 0) {
+        if (ensure_smem_attr(reinterpret_cast<const void*>(&fft_pass_kernel<LOGR, true>), smem, "fft_pass_kernel") !=
+            KK_OK)
+            return KK_ERR_CUDA;
+        fft_pass_kernel<LOGR, true><<<static_cast<unsigned>(blocks), kThreads, smem, st>>>(in, out, log_n, ns, cols, tb);
+    } else {
+        if (ensure_smem_attr(reinterpret_cast<const void*>(&fft_pass_kernel<LOGR, false>), smem, "fft_pass_kernel") !=
+            KK_OK)
+            return KK_ERR_CUDA;
+        fft_pass_kernel<LOGR, false><<<static_cast<unsigned>(blocks), kThreads, smem, st>>>(in, out, log_n, ns, cols,
+                                                                                           tb);
+    }
     return check_launch("fft_pass_kernel");
 }
 
