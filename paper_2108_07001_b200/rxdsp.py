@@ -973,7 +973,13 @@ class RxPipeline:
         self._async = bool(getattr(self.gpu, "ddlms_async", False))
         self._jobs = collections.deque()  # submitted asynchronous frames, in order
         self._worker = None
-        self._y2.before_realloc = self._wait_frames
+        # a weak reference: a bound method would make pipe -> _y2 -> pipe a
+        # reference cycle, and the pipeline's device buffers would then wait
+        # for Python's cyclic GC (measured: sweeps grew by ~30 MiB per batch
+        # and paid fresh cudaMallocs until a GC pass)
+        import weakref
+        wself = weakref.ref(self)
+        self._y2.before_realloc = lambda: (lambda p: p._wait_frames() if p is not None else None)(wself())
         # Equalizer state lives on the device (no host round trip between
         # frames): 4-tap widely-linear -> real 2x8 taps T + {frozen,
         # div_count} for the block-parallel solver; otherwise the complex

@@ -1044,3 +1044,23 @@ def test_drain_without_release_keeps_grid_framing():
         assert len(d) == 0
     d, s = p2.finish()
     assert np.array_equal(np.concatenate(decs + [d]), d1) and np.array_equal(np.concatenate(softs + [s]), s1)
+
+
+def test_pipeline_freed_without_cyclic_gc():
+    """A dropped RxPipeline releases its device buffers at once (no reference
+    cycle waiting for Python's cyclic GC: sweeps creating a pipeline per
+    point otherwise grew by tens of MiB per batch and paid fresh cudaMallocs)."""
+    import gc
+    import weakref
+
+    cap = load_capture("c1_qpsk_b2b")
+    gc.disable()
+    try:
+        pipe = rxdsp.RxPipeline(cap.pipeline_config(), reference_symbols=cap.symbols())
+        pipe.feed(AdcCodes(cap.adc_h, cap.half_lsb), flush=True)
+        lab, _, _ = pipe.drain_device()
+        ref = weakref.ref(pipe)
+        del pipe
+        assert ref() is None
+    finally:
+        gc.enable()
