@@ -1064,3 +1064,28 @@ def test_pipeline_freed_without_cyclic_gc():
         assert ref() is None
     finally:
         gc.enable()
+
+
+def test_pipeline_other_plans_chunked_and_packed12():
+    """The generic (non-default plan) front end: chunked feeds of the packed
+    12-bit wire format give the single int16 feed's outputs."""
+    import dataclasses
+
+    from paper_2108_07001_b200.sigcore import AdcPacked12, pack12
+
+    cap = load_capture("c1_qpsk_b2b")
+    cfg = cap.pipeline_config()
+    cfg = dataclasses.replace(cfg, kk_plan=BlockPlan(2048, buffer_len=cfg.kk_plan.buffer_len),
+                              static_plan=BlockPlan(16384, buffer_len=cfg.static_plan.buffer_len))
+    p1 = rxdsp.RxPipeline(cfg, reference_symbols=cap.symbols())
+    p1.feed(AdcCodes(cap.adc_h, cap.half_lsb))
+    d1, s1 = p1.finish()
+    p2 = rxdsp.RxPipeline(cfg, reference_symbols=cap.symbols())
+    packed = pack12(cap.adc_h)
+    n = len(cap.adc_h)
+    cuts = [0, 40000, 90002, 150000, n]
+    for a, b in zip(cuts, cuts[1:]):
+        p2.feed(AdcPacked12(packed[3 * a // 2: 3 * b // 2], cap.half_lsb, b - a))
+    d2, s2 = p2.finish()
+    assert np.array_equal(d1, d2)
+    assert np.max(np.abs(s1 - s2)) < 1e-5
