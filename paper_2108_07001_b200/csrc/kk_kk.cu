@@ -296,24 +296,27 @@ k1_body(const int bx, const typename InElem<TIn>::T* __restrict__ in, float in_s
     const float inv_q = rot_q > 0 ? 1.0f / static_cast<float>(rot_q) : 0.f;
     const float two_pi_over_q = rot_q > 0 ? 6.283185307179586f / static_cast<float>(rot_q) : 0.f;
     // (32-bit arithmetic: n0_global arrives reduced mod q, hop_a < 2^31)
+    // (one integer modulo for the unbounded hop index; the small arguments,
+    // all < 2^25, reduce through the float reciprocal)
     if (rot_q > 0 && active) {
         const unsigned Q = static_cast<unsigned>(rot_q);
-        rot_base = (static_cast<unsigned>(n0_global) + (static_cast<unsigned>(hop_a) % Q) * (512u % Q)) % Q;
+        const unsigned h = static_cast<unsigned>(hop_a) % Q;
+        rot_base = fmod_u(static_cast<unsigned>(n0_global) + h * fmod_u(512u, Q, inv_q), Q, inv_q);
     }
     float2 rot_cache = make_float2(1.f, 0.f), r256 = rot_cache, r512 = rot_cache;
     const bool rotate = rot_q > 0 || rot_step != 0ull;
     if (rot_q > 0) {
         const unsigned Q = static_cast<unsigned>(rot_q), Pp = static_cast<unsigned>(rot_p);
-        r256 = __ldg(rot_tab + (256u * Pp) % Q);     // exp(-2 pi i (256 p mod q) / q)
-        r512 = __ldg(rot_tab + (512u * Pp) % Q);
+        r256 = __ldg(rot_tab + fmod_u(256u * Pp, Q, inv_q));     // exp(-2 pi i (256 p mod q) / q)
+        r512 = __ldg(rot_tab + fmod_u(512u * Pp, Q, inv_q));
     } else if (rot_step) {
         r256 = PRECISE ? rot_phase_precise(256ull * rot_step) : rot_phase_fast(256ull * rot_step);
         r512 = PRECISE ? rot_phase_precise(512ull * rot_step) : rot_phase_fast(512ull * rot_step);
     }
+    const bool has_b = (hop_a + 1) < n_hops;
     auto st_out = [&](int n, float2 v) {
         if (n < kHop) return;
         const int i = n - kHop;
-        const bool has_b = (hop_a + 1) < n_hops;
         // delayed dead flags: position i-256 of the new hop lies in the
         // previous hop when i < 256
         bool da = (i < kHop / 2) ? (hist ? (S.dead_hist[i] != 0) : (dead_a0 != 0)) : (dead_a1 != 0);
