@@ -19,14 +19,53 @@
 namespace kk {
 
 
+// KK_PACKED_ADD / KK_PACKED_MUL: complex adds and multiplies on sm_100's
+// packed FP32 instructions (FADD2 / FMUL2 / FFMA2: one instruction per re/im
+// pair).  Same roundings as the scalar form (every lane is one add.rn /
+// mul.rn / fma.rn of the same operands), so results are bit-identical; what
+// changes is the issue count of the instruction-bound FFT kernels
+// (tools/f32x2_bench.cu: packed and scalar ops have the same lane
+// throughput, the packed ones take half the issue slots).  Per translation
+// unit (set before this header is included): K1 (kk_kk.cu) uses both, 7.13 ->
+// 6.63 ms per 2^30 samples; K2 (kk_static.cu) measured slower with both.
+#ifndef KK_PACKED_ADD
+#define KK_PACKED_ADD 0
+#endif
+#ifndef KK_PACKED_MUL
+#define KK_PACKED_MUL 0
+#endif
+#if KK_PACKED_ADD
+__device__ __forceinline__ float2 cadd(float2 a, float2 b) { return __fadd2_rn(a, b); }
+__device__ __forceinline__ float2 csub(float2 a, float2 b) { return __fadd2_rn(a, make_float2(-b.x, -b.y)); }
+#else
 __device__ __forceinline__ float2 cadd(float2 a, float2 b) { return make_float2(a.x + b.x, a.y + b.y); }
 __device__ __forceinline__ float2 csub(float2 a, float2 b) { return make_float2(a.x - b.x, a.y - b.y); }
+#endif
+#if KK_PACKED_MUL
+// a * (c + i s) with c, s compile-time constants: (a.x c - a.y s, a.x s + a.y c)
+__device__ __forceinline__ float2 cmul_const(float2 a, float c, float s) {
+    const float2 t = __fmul2_rn(make_float2(a.y, a.y), make_float2(-s, c));
+    return __ffma2_rn(make_float2(a.x, a.x), make_float2(c, s), t);
+}
+__device__ __forceinline__ float2 cmul(float2 a, float2 b) {
+    const float2 t = __fmul2_rn(make_float2(a.y, a.y), make_float2(-b.y, b.x));
+    return __ffma2_rn(make_float2(a.x, a.x), b, t);
+}
+__device__ __forceinline__ float2 cmulc(float2 a, float2 b) {  // a * conj(b)
+    const float2 t = __fmul2_rn(make_float2(a.y, a.x), make_float2(b.y, -b.y));
+    return __ffma2_rn(a, make_float2(b.x, b.x), t);
+}
+#else
+__device__ __forceinline__ float2 cmul_const(float2 a, float c, float s) {
+    return make_float2(fmaf(a.x, c, -a.y * s), fmaf(a.x, s, a.y * c));
+}
 __device__ __forceinline__ float2 cmul(float2 a, float2 b) {
     return make_float2(fmaf(a.x, b.x, -a.y * b.y), fmaf(a.x, b.y, a.y * b.x));
 }
 __device__ __forceinline__ float2 cmulc(float2 a, float2 b) {  // a * conj(b)
     return make_float2(fmaf(a.x, b.x, a.y * b.y), fmaf(a.y, b.x, -a.x * b.y));
 }
+#endif
 __device__ __forceinline__ float2 cconj(float2 a) { return make_float2(a.x, -a.y); }
 __device__ __forceinline__ float2 cscale(float2 a, float s) { return make_float2(a.x * s, a.y * s); }
 __device__ __forceinline__ float2 mul_mj(float2 a) { return make_float2(a.y, -a.x); }   // * (-j)
@@ -82,7 +121,7 @@ __device__ __forceinline__ float2 tw16(float2 a) {
     } else {
         constexpr float c = c16(T);
         constexpr float s = INV ? s16(T) : -s16(T);
-        return make_float2(fmaf(a.x, c, -a.y * s), fmaf(a.x, s, a.y * c));
+        return cmul_const(a, c, s);
     }
 }
 

@@ -21,6 +21,15 @@
 #include <algorithm>
 #include <type_traits>
 
+// packed FP32 complex arithmetic (kk_common.cuh; measured 7.13 -> 6.63 ms)
+#ifndef KK_K1_PACKED_ADD
+#define KK_K1_PACKED_ADD 1
+#endif
+#ifndef KK_K1_PACKED_MUL
+#define KK_K1_PACKED_MUL 1
+#endif
+#define KK_PACKED_ADD KK_K1_PACKED_ADD
+#define KK_PACKED_MUL KK_K1_PACKED_MUL
 #include "kk_common.cuh"
 #include "kk_internal.h"
 
@@ -107,10 +116,27 @@ __device__ __forceinline__ float2 apply_mult(int k, float2 z) {
 // approximations (the functional kk_reconstruct API, whose reference tests
 // demand e.g. a constant current reconstructed to 1e-8 absolute,
 // test_rxdsp.py:83-89); the streaming pipeline uses the fast variant.
+// The fast forms are __logf / __expf without their subnormal fix-ups (the
+// .ftz MUFU forms; 3 instructions less each, same results for normal
+// operands and results): log's argument is >= the clamp threshold or 1, and
+// an amplitude below 2^-126 flushes to 0 (an absolute difference < 1.2e-38).
+__device__ __forceinline__ float log_ftz(float x) {
+    float r;
+    asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r * 0.693147180559945309f;
+}
+__device__ __forceinline__ float exp_ftz(float x) {
+    float r;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x * 1.442695040888963407f));
+    return r;
+}
+#ifndef KK_K1_FTZ
+#define KK_K1_FTZ 1
+#endif
 template <bool PRECISE>
-__device__ __forceinline__ float k1_log(float x) { return PRECISE ? logf(x) : __logf(x); }
+__device__ __forceinline__ float k1_log(float x) { return PRECISE ? logf(x) : (KK_K1_FTZ ? log_ftz(x) : __logf(x)); }
 template <bool PRECISE>
-__device__ __forceinline__ float k1_exp(float x) { return PRECISE ? expf(x) : __expf(x); }
+__device__ __forceinline__ float k1_exp(float x) { return PRECISE ? expf(x) : (KK_K1_FTZ ? exp_ftz(x) : __expf(x)); }
 // sin/cos of a phase; the fast form first reduces to [-pi, pi]
 template <bool PRECISE>
 __device__ __forceinline__ void k1_sincos(float x, float* s, float* c) {

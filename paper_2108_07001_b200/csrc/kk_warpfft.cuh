@@ -37,7 +37,7 @@ __device__ __forceinline__ float2 tw32(float2 a, int t) {
     if (t == 0) return a;
     if (t == 8) return INV ? mul_pj(a) : mul_mj(a);
     const float c = c32(t), s = INV ? s32(t) : -s32(t);
-    return make_float2(fmaf(a.x, c, -a.y * s), fmaf(a.x, s, a.y * c));
+    return cmul_const(a, c, s);
 }
 
 template <bool INV, int K = 0>
