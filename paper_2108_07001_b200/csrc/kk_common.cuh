@@ -26,8 +26,10 @@ namespace kk {
 // changes is the issue count of the instruction-bound FFT kernels
 // (tools/f32x2_bench.cu: packed and scalar ops have the same lane
 // throughput, the packed ones take half the issue slots).  Per translation
-// unit (set before this header is included): K1 (kk_kk.cu) uses both, 7.13 ->
-// 6.63 ms per 2^30 samples; K2 (kk_static.cu) measured slower with both.
+// unit (set before this header is included), A/B'd per kernel: K1 (kk_kk.cu)
+// packs all three, 7.13 -> 6.63 ms per 2^30 samples; K2 (kk_static.cu) the
+// adds and constant-twiddle multiplies, 11.80 -> 11.51 ms.  KK_PACKED_CONST
+// (constant multiplies) follows KK_PACKED_MUL unless set.
 #ifndef KK_PACKED_ADD
 #define KK_PACKED_ADD 0
 #endif
@@ -41,12 +43,21 @@ __device__ __forceinline__ float2 csub(float2 a, float2 b) { return __fadd2_rn(a
 __device__ __forceinline__ float2 cadd(float2 a, float2 b) { return make_float2(a.x + b.x, a.y + b.y); }
 __device__ __forceinline__ float2 csub(float2 a, float2 b) { return make_float2(a.x - b.x, a.y - b.y); }
 #endif
-#if KK_PACKED_MUL
+#ifndef KK_PACKED_CONST
+#define KK_PACKED_CONST KK_PACKED_MUL
+#endif
+#if KK_PACKED_CONST
 // a * (c + i s) with c, s compile-time constants: (a.x c - a.y s, a.x s + a.y c)
 __device__ __forceinline__ float2 cmul_const(float2 a, float c, float s) {
     const float2 t = __fmul2_rn(make_float2(a.y, a.y), make_float2(-s, c));
     return __ffma2_rn(make_float2(a.x, a.x), make_float2(c, s), t);
 }
+#else
+__device__ __forceinline__ float2 cmul_const(float2 a, float c, float s) {
+    return make_float2(fmaf(a.x, c, -a.y * s), fmaf(a.x, s, a.y * c));
+}
+#endif
+#if KK_PACKED_MUL
 __device__ __forceinline__ float2 cmul(float2 a, float2 b) {
     const float2 t = __fmul2_rn(make_float2(a.y, a.y), make_float2(-b.y, b.x));
     return __ffma2_rn(make_float2(a.x, a.x), b, t);
@@ -56,9 +67,6 @@ __device__ __forceinline__ float2 cmulc(float2 a, float2 b) {  // a * conj(b)
     return __ffma2_rn(a, make_float2(b.x, b.x), t);
 }
 #else
-__device__ __forceinline__ float2 cmul_const(float2 a, float c, float s) {
-    return make_float2(fmaf(a.x, c, -a.y * s), fmaf(a.x, s, a.y * c));
-}
 __device__ __forceinline__ float2 cmul(float2 a, float2 b) {
     return make_float2(fmaf(a.x, b.x, -a.y * b.y), fmaf(a.x, b.y, a.y * b.x));
 }

@@ -30,6 +30,9 @@
 #endif
 #define KK_PACKED_ADD KK_K1_PACKED_ADD
 #define KK_PACKED_MUL KK_K1_PACKED_MUL
+#ifdef KK_K1_PACKED_CONST
+#define KK_PACKED_CONST KK_K1_PACKED_CONST
+#endif
 #include "kk_common.cuh"
 #include "kk_internal.h"
 

@@ -29,17 +29,22 @@
 // to HBM coalesced.
 #include <algorithm>
 
-// packed FP32 complex arithmetic (kk_common.cuh): adds / multiplies A/B'd
-// separately: both packed 11.80 -> 12.03 ms (the multiplies cost it), adds
-// only 11.82 -> 11.79 ms
+// packed FP32 complex arithmetic (kk_common.cuh), A/B'd per operation:
+// adds 11.82 -> 11.79 ms, constant-twiddle multiplies -> 11.51 ms; the
+// general multiplies (running twiddle products) measured slower packed
+// (both packed: 12.03 ms), so they stay scalar
 #ifndef KK_K2_PACKED_ADD
 #define KK_K2_PACKED_ADD 1
 #endif
 #ifndef KK_K2_PACKED_MUL
 #define KK_K2_PACKED_MUL 0
 #endif
+#ifndef KK_K2_PACKED_CONST
+#define KK_K2_PACKED_CONST 1
+#endif
 #define KK_PACKED_ADD KK_K2_PACKED_ADD
 #define KK_PACKED_MUL KK_K2_PACKED_MUL
+#define KK_PACKED_CONST KK_K2_PACKED_CONST
 #include "kk_common.cuh"
 #include "kk_internal.h"
 #include "kk_warpfft.cuh"
