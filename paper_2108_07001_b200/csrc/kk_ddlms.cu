@@ -759,6 +759,11 @@ __global__ void fill_T_kernel(float* __restrict__ T, int64_t b0, int64_t b1, con
 #ifndef KK_DD_MINB_P
 #define KK_DD_MINB_P 4    // resident CTAs / SM of the P pass (4: 128 registers, 16 B spill, measured 8.33 -> 8.29 ms)
 #endif
+// per-symbol tap products / updates and the P_b rank-1 updates on the packed
+// FP32 pipe (FFMA2: two lanes per instruction, same roundings as scalar)
+#ifndef KK_DD_PACKED
+#define KK_DD_PACKED 1
+#endif
 constexpr int kBlockThreads = 128;
 
 __device__ __forceinline__ void cp_async16(void* smem, const void* g, int src_bytes) {
@@ -1058,6 +1063,18 @@ ddlms_block_kernel(SolveArgs a, Slicer sl, const float* __restrict__ Tstart, flo
             X[0] = X[4]; X[1] = X[5]; X[2] = X[6]; X[3] = X[7];
             const float4 rw = WITH_P ? stage[stage_idx(c % kChunks, j, lane)] : rows[WITH_P ? 0 : j];
             X[4] = rw.x; X[5] = rw.y; X[6] = rw.z; X[7] = rw.w;
+#if KK_DD_PACKED
+            // (re, im) pairs (T[jj], T[8 + jj]) on the packed FP32 pipe: the
+            // same fma sequence per lane as the scalar form
+            float2 yza = make_float2(0.f, 0.f), yzb = make_float2(0.f, 0.f);
+#pragma unroll
+            for (int jj = 0; jj < 8; jj += 2) {
+                yza = __ffma2_rn(make_float2(T[jj], T[8 + jj]), make_float2(X[jj], X[jj]), yza);
+                yzb = __ffma2_rn(make_float2(T[jj + 1], T[9 + jj]), make_float2(X[jj + 1], X[jj + 1]), yzb);
+            }
+            const float2 yri = __fadd2_rn(yza, yzb);
+            const float yr = yri.x, yi = yri.y;
+#else
             float ya = 0.f, yb = 0.f, za = 0.f, zb = 0.f;
 #pragma unroll
             for (int jj = 0; jj < 8; jj += 2) {
@@ -1067,6 +1084,7 @@ ddlms_block_kernel(SolveArgs a, Slicer sl, const float* __restrict__ Tstart, flo
                 zb = fmaf(T[9 + jj], X[jj + 1], zb);
             }
             const float yr = ya + yb, yi = za + zb;
+#endif
             float dr, di;
             int lab;
             float2 tcur = make_float2(0.f, 0.f);
@@ -1186,6 +1204,28 @@ ddlms_block_kernel(SolveArgs a, Slicer sl, const float* __restrict__ Tstart, flo
                         for (int jj = 0; jj < 8; ++jj)
                             P[r * 8 + jj] = fmaf(-w[r], JX[jj], fmaf(-v[r], X[jj], P[r * 8 + jj]));
                 } else {
+#if KK_DD_PACKED
+                    // rows (2q, 2q + 1) as pairs: the scalar form's fma order per row
+                    float2 nv[4];
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        float2 sacc = make_float2(0.f, 0.f);
+#pragma unroll
+                        for (int jj = 0; jj < 8; ++jj)
+                            sacc = __ffma2_rn(make_float2(P[2 * q * 8 + jj], P[(2 * q + 1) * 8 + jj]),
+                                              make_float2(X[jj], X[jj]), sacc);
+                        nv[q] = live ? __fmul2_rn(sacc, make_float2(-tm, -tm)) : make_float2(0.f, 0.f);
+                    }
+#pragma unroll
+                    for (int q = 0; q < 4; ++q)
+#pragma unroll
+                        for (int jj = 0; jj < 8; ++jj) {
+                            const float2 np = __ffma2_rn(nv[q], make_float2(X[jj], X[jj]),
+                                                         make_float2(P[2 * q * 8 + jj], P[(2 * q + 1) * 8 + jj]));
+                            P[2 * q * 8 + jj] = np.x;
+                            P[(2 * q + 1) * 8 + jj] = np.y;
+                        }
+#else
                     float v[8];
 #pragma unroll
                     for (int r = 0; r < 8; ++r) {
@@ -1198,6 +1238,7 @@ ddlms_block_kernel(SolveArgs a, Slicer sl, const float* __restrict__ Tstart, flo
                     for (int r = 0; r < 8; ++r)
 #pragma unroll
                         for (int jj = 0; jj < 8; ++jj) P[r * 8 + jj] = fmaf(-v[r], X[jj], P[r * 8 + jj]);
+#endif
                 }
             }
             if constexpr (LIN) {
@@ -1214,11 +1255,21 @@ ddlms_block_kernel(SolveArgs a, Slicer sl, const float* __restrict__ Tstart, flo
                     T[9 + 2 * u] += d0;
                 }
             } else {
+#if KK_DD_PACKED
+                const float2 e2 = make_float2(er, ei);
+#pragma unroll
+                for (int jj = 0; jj < 8; ++jj) {
+                    const float2 nt = __ffma2_rn(e2, make_float2(X[jj], X[jj]), make_float2(T[jj], T[8 + jj]));
+                    T[jj] = nt.x;
+                    T[8 + jj] = nt.y;
+                }
+#else
 #pragma unroll
                 for (int jj = 0; jj < 8; ++jj) {
                     T[jj] = fmaf(er, X[jj], T[jj]);
                     T[8 + jj] = fmaf(ei, X[jj], T[8 + jj]);
                 }
+#endif
             }
             hsh = live ? (hsh ^ static_cast<unsigned long long>(lab & 0xff)) * 1099511628211ull : hsh;
             soft8[j] = make_float2(yr, yi);
