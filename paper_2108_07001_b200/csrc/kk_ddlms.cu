@@ -764,6 +764,9 @@ __global__ void fill_T_kernel(float* __restrict__ T, int64_t b0, int64_t b1, con
 #ifndef KK_DD_PACKED
 #define KK_DD_PACKED 1
 #endif
+#ifndef KK_DD_SLICER_PACKED       // the square-grid slicer's pair arithmetic too
+#define KK_DD_SLICER_PACKED KK_DD_PACKED
+#endif
 constexpr int kBlockThreads = 128;
 
 __device__ __forceinline__ void cp_async16(void* smem, const void* g, int src_bytes) {
@@ -1094,8 +1097,18 @@ ddlms_block_kernel(SolveArgs a, Slicer sl, const float* __restrict__ Tstart, flo
                 // branch-free: no F2I (MIO) and no control flow on the chain.
                 // (v + 1.5*2^23) - 1.5*2^23 == rint(v) for |v| < 2^22.
                 constexpr float kMagic = 12582912.0f;
-                const float vr = fmaf(yr, half_norm, off), vi = fmaf(yi, half_norm, off);
                 const float m1f = static_cast<float>(m1);
+#if KK_DD_SLICER_PACKED
+                const float2 v2 = __ffma2_rn(yri, make_float2(half_norm, half_norm), make_float2(off, off));
+                const float vr = v2.x, vi = v2.y;
+                const float2 vc2 = make_float2(fminf(fmaxf(vr, 0.f), m1f), fminf(fmaxf(vi, 0.f), m1f));
+                const float2 f2 = __fadd2_rn(__fadd2_rn(vc2, make_float2(kMagic, kMagic)),
+                                             make_float2(-kMagic, -kMagic));
+                const float2 dv = __fadd2_rn(vc2, make_float2(-f2.x, -f2.y));
+                float fr = f2.x, fi = f2.y;
+                float mg_s = 0.5f - fmaxf(fabsf(dv.x), fabsf(dv.y));
+#else
+                const float vr = fmaf(yr, half_norm, off), vi = fmaf(yi, half_norm, off);
                 // distance to the nearest decision boundary; an edge level has
                 // none on its outer side, so v is clamped to the level range
                 // first (margin 0.5 there: conservative)
@@ -1103,6 +1116,7 @@ ddlms_block_kernel(SolveArgs a, Slicer sl, const float* __restrict__ Tstart, flo
                 float fr = (vcr + kMagic) - kMagic;
                 float fi = (vci + kMagic) - kMagic;
                 float mg_s = 0.5f - fmaxf(fabsf(vcr - fr), fabsf(vci - fi));
+#endif
                 if constexpr (!WITH_P) {
                     const bool near = live && !trn && mg_s < kTieEps;
                     if (__any_sync(0xffffffffu, near) && near)
@@ -1113,8 +1127,16 @@ ddlms_block_kernel(SolveArgs a, Slicer sl, const float* __restrict__ Tstart, flo
                 const int ii = __float_as_int(fi + kMagic) - __float_as_int(kMagic);
                 // level value (2 i - (m-1)) * h: exact for the constellation
                 // (checked on the host, Slicer::sep)
+#if KK_DD_SLICER_PACKED
+                const float2 lev = __fmul2_rn(__ffma2_rn(make_float2(2.0f, 2.0f), make_float2(fr, fi),
+                                                         make_float2(-m1f, -m1f)),
+                                              make_float2(lev_h, lev_h));
+                dr = trn ? tcur.x : lev.x;
+                di = trn ? tcur.y : lev.y;
+#else
                 dr = trn ? tcur.x : fmaf(2.0f, fr, -static_cast<float>(m1)) * lev_h;
                 di = trn ? tcur.y : fmaf(2.0f, fi, -static_cast<float>(m1)) * lev_h;
+#endif
                 int sl_lab;
                 if constexpr (SQ == 2) sl_lab = (glab >> (8 * (ir * 2 + ii))) & 0xff;
                 else sl_lab = grid[ir * SQ + ii];
@@ -1172,7 +1194,12 @@ ddlms_block_kernel(SolveArgs a, Slicer sl, const float* __restrict__ Tstart, flo
                     else if (g_run == a.guard_run && g_first == 0xffff) g_first = i;
                 }
             }
+#if KK_DD_PACKED
+            const float2 e2p = __fmul2_rn(make_float2(tm, tm), __fadd2_rn(make_float2(dr, di), make_float2(-yr, -yi)));
+            const float er = live ? e2p.x : 0.f, ei = live ? e2p.y : 0.f;
+#else
             const float er = live ? tm * (dr - yr) : 0.f, ei = live ? tm * (di - yi) : 0.f;
+#endif
             if constexpr (WITH_P) {
                 float n2 = 0.f;
 #pragma unroll
