@@ -136,6 +136,9 @@ __device__ __forceinline__ float exp_ftz(float x) {
 #ifndef KK_K1_FTZ
 #define KK_K1_FTZ 1
 #endif
+#ifndef KK_K1_EPI_PACKED      // epilogue phase scaling / amplitude products as packed pairs
+#define KK_K1_EPI_PACKED 1
+#endif
 template <bool PRECISE>
 __device__ __forceinline__ float k1_log(float x) { return PRECISE ? logf(x) : (KK_K1_FTZ ? log_ftz(x) : __logf(x)); }
 template <bool PRECISE>
@@ -354,10 +357,18 @@ k1_body(const int bx, const typename InElem<TIn>::T* __restrict__ in, float in_s
         const float amp_a = (hist && i < kHop / 2) ? S.ahist[i] : k1_exp<PRECISE>(ua_d[i]);
         const float amp_b = k1_exp<PRECISE>(ub_d[i]);
         float sa, ca, sb, cb;
+#if KK_K1_EPI_PACKED
+        const float2 ph = __fmul2_rn(v, make_float2(1.0f / 1024.0f, 1.0f / 1024.0f));
+        k1_sincos<PRECISE>(ph.x, &sa, &ca);
+        k1_sincos<PRECISE>(ph.y, &sb, &cb);
+        float2 fa = da ? make_float2(0.f, 0.f) : __fmul2_rn(make_float2(amp_a, amp_a), make_float2(ca, sa));
+        float2 fb = db ? make_float2(0.f, 0.f) : __fmul2_rn(make_float2(amp_b, amp_b), make_float2(cb, sb));
+#else
         k1_sincos<PRECISE>(v.x * (1.0f / 1024.0f), &sa, &ca);
         k1_sincos<PRECISE>(v.y * (1.0f / 1024.0f), &sb, &cb);
         float2 fa = da ? make_float2(0.f, 0.f) : make_float2(amp_a * ca, amp_a * sa);
         float2 fb = db ? make_float2(0.f, 0.f) : make_float2(amp_b * cb, amp_b * sb);
+#endif
         if (!active) return;
         acc_a = cadd(acc_a, fa);
         const int64_t pa = hop_a * kHop + i;           // chunk positions
