@@ -46,18 +46,38 @@ __device__ __forceinline__ float2 csub(float2 a, float2 b) { return make_float2(
 #ifndef KK_PACKED_CONST
 #define KK_PACKED_CONST KK_PACKED_MUL
 #endif
+// KK_PACKED_NP: the forms below let ptxas fold the one-lane negation into the
+// FFMA2 addend (the ".NP" operand modifier) and the re/im swap into an operand
+// selector, so a complex multiply is FMUL2 + FFMA2 with no pair-forming moves
+#ifndef KK_PACKED_NP
+#define KK_PACKED_NP 1
+#endif
 #if KK_PACKED_CONST
 // a * (c + i s) with c, s compile-time constants: (a.x c - a.y s, a.x s + a.y c)
 __device__ __forceinline__ float2 cmul_const(float2 a, float c, float s) {
+#if KK_PACKED_NP
+    const float2 t = __fmul2_rn(make_float2(a.y, a.y), make_float2(s, c));
+    return __ffma2_rn(make_float2(a.x, a.x), make_float2(c, s), make_float2(-t.x, t.y));
+#else
     const float2 t = __fmul2_rn(make_float2(a.y, a.y), make_float2(-s, c));
     return __ffma2_rn(make_float2(a.x, a.x), make_float2(c, s), t);
+#endif
 }
 #else
 __device__ __forceinline__ float2 cmul_const(float2 a, float c, float s) {
     return make_float2(fmaf(a.x, c, -a.y * s), fmaf(a.x, s, a.y * c));
 }
 #endif
-#if KK_PACKED_MUL
+#if KK_PACKED_MUL && KK_PACKED_NP
+__device__ __forceinline__ float2 cmul(float2 a, float2 b) {
+    const float2 t = __fmul2_rn(make_float2(a.y, a.y), make_float2(b.y, b.x));
+    return __ffma2_rn(make_float2(a.x, a.x), b, make_float2(-t.x, t.y));
+}
+__device__ __forceinline__ float2 cmulc(float2 a, float2 b) {  // a * conj(b)
+    const float2 t = __fmul2_rn(make_float2(a.y, a.x), make_float2(b.y, b.y));
+    return __ffma2_rn(a, make_float2(b.x, b.x), make_float2(t.x, -t.y));
+}
+#elif KK_PACKED_MUL
 __device__ __forceinline__ float2 cmul(float2 a, float2 b) {
     const float2 t = __fmul2_rn(make_float2(a.y, a.y), make_float2(-b.y, b.x));
     return __ffma2_rn(make_float2(a.x, a.x), b, t);
