@@ -10,7 +10,7 @@ timeout 300 python tools/e2e_timeline.py --packed12 --out gpurun_out/e2e_timelin
 timeout 600 python tools/ddlms_modes_bench.py > gpurun_out/modes.log 2>&1
 export KK_DDLMS_GRAPH=0
 python tools/prof_run.py 26 2 > gpurun_out/plain.log 2>&1 && \
-ncu --set full --clock-control none --import-source on -k regex:"kk_pairs_kernel|static_blocks_kernel|ddlms_block_kernel" -c 12 -o gpurun_out/prof_r2k python tools/prof_run.py 26 2 > gpurun_out/ncu_full.log 2>&1
+ncu --set full --clock-control none --import-source on -k regex:"kk_pairs_kernel|static_blocks_kernel|ddlms_block_kernel" -c 12 -o gpurun_out/prof_r2l python tools/prof_run.py 26 2 > gpurun_out/ncu_full.log 2>&1
 python bench.py --steps 2 --warmup 1 --no-checks --no-64qam --no-cpu-baseline > gpurun_out/plain_bench.log 2>&1 && \
-ncu --metrics gpu__time_duration.sum --clock-control none -c 2000 --csv --log-file gpurun_out/launches_r2k.csv python bench.py --steps 2 --warmup 1 --no-checks --no-64qam --no-cpu-baseline > gpurun_out/ncu_launch.log 2>&1
+ncu --metrics gpu__time_duration.sum --clock-control none -c 2000 --csv --log-file gpurun_out/launches_r2l.csv python bench.py --steps 2 --warmup 1 --no-checks --no-64qam --no-cpu-baseline > gpurun_out/ncu_launch.log 2>&1
 ls -la gpurun_out
